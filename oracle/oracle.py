@@ -1,0 +1,219 @@
+"""CPU oracle for the RNG index-construction hot path -- TEST INFRASTRUCTURE.
+
+Only tests/, ``__graft_entry__.smoke()`` and ``bench.py`` (cpu_baseline leg and
+``--impl reference``) may import this module, and only as the checker / the
+timed CPU baseline.  The product package never imports it.
+
+Two layers:
+
+* ``pgk_oracle.c`` (built to ``oracle/liboracle.so``): plain-C restatement of
+  the reference's numba kernels (_kernels.py:17-42, 298-324, 364-427, 530-588)
+  and a float64 direct-difference exact-kNN pool.  OpenMP over points.
+* numpy orchestration restating prune.py:109-151 (phase A / phase B) and
+  oracle.py:31-65 (``ground_truth_table``, float64 BLAS norm expansion plus a
+  stable argsort, exactly as the reference computes it).
+
+Pinned against tests/golden/*.npz, which hold outputs of the reference itself
+(tests/golden/make_golden.py); see tests/test_oracle_golden.py.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+SRC = HERE / "pgk_oracle.c"
+LIB = HERE / "liboracle.so"
+
+EMPTY = -1
+_STRATEGIES = ("rng", "alpha")
+
+
+def build(force: bool = False) -> Path:
+    """Compile the C restatement (gcc, OpenMP, no FMA contraction)."""
+    if force or not LIB.exists() or LIB.stat().st_mtime < SRC.stat().st_mtime:
+        tmp = LIB.with_suffix(".so.tmp")
+        subprocess.check_call([
+            "gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+            "-fPIC", "-shared", "-std=c99", str(SRC), "-o", str(tmp), "-lm"])
+        os.replace(tmp, LIB)
+    return LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(str(LIB))
+        P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        L.orc_squared_l2.restype = ctypes.c_float
+        L.orc_squared_l2.argtypes = [P, P, I64]
+        L.orc_cos_angle_from_sq.restype = D
+        L.orc_cos_angle_from_sq.argtypes = [ctypes.c_float] * 3
+        L.orc_prune_batch.restype = None
+        L.orc_prune_batch.argtypes = [P, I64, I64, P, P, P, P, I32, D, I64, I64,
+                                      P, P, P, P, P]
+        L.orc_sort_pairs.argtypes = [P, P, I64]
+        L.orc_scatter_reverse.argtypes = [P, P, P, I64, I64, P, P, P]
+        L.orc_merge_with_reverse.argtypes = [P, P, P, I64, I64, P, P, P, P, P, P, P]
+        L.orc_knn_pool.argtypes = [P, I64, I64, I64, I32, P, I64, P, P]
+        L.orc_list_dists_sorted.argtypes = [P, I64, P, I64, I64, P, P]
+        L.orc_num_threads.restype = I32
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def num_threads() -> int:
+    return int(lib().orc_num_threads())
+
+
+def cos_alpha(alpha_deg: float) -> float:
+    """PruneParams.cos_alpha (prune.py:54-56)."""
+    return math.cos(math.radians(alpha_deg))
+
+
+def squared_l2(a, b) -> float:
+    a, b = _f32(a), _f32(b)
+    return float(lib().orc_squared_l2(_p(a), _p(b), a.shape[0]))
+
+
+def prune_all(data, cand_off, cand_counts, cand_ids, cand_dists, M: int,
+              strategy: str = "rng", alpha: float = 60.0, cap=None):
+    """prune.py:109-126 -> (ids (n, width), dists, counts, dist_evals, angle_evals)."""
+    data = _f32(data)
+    n, d = data.shape
+    width = M if cap is None else cap
+    cand_off = np.ascontiguousarray(cand_off, np.int64)
+    cand_counts = np.ascontiguousarray(cand_counts, np.int32)
+    cand_ids = np.ascontiguousarray(cand_ids, np.int32)
+    cand_dists = np.ascontiguousarray(cand_dists, np.float32)
+    out_ids = np.full((n, width), EMPTY, np.int32)
+    out_dists = np.full((n, width), np.inf, np.float32)
+    out_counts = np.zeros(n, np.int32)
+    de = np.zeros(n, np.int64)
+    ae = np.zeros(n, np.int64)
+    lib().orc_prune_batch(_p(data), n, d, _p(cand_off), _p(cand_counts), _p(cand_ids),
+                          _p(cand_dists), _STRATEGIES.index(strategy), cos_alpha(alpha),
+                          M, width, _p(out_ids), _p(out_dists), _p(out_counts),
+                          _p(de), _p(ae))
+    return out_ids, out_dists, out_counts, int(de.sum()), int(ae.sum())
+
+
+def add_reverse_and_prune(data, ids, dists, counts, M: int, strategy: str = "rng",
+                          alpha: float = 60.0):
+    """prune.py:129-151 (phase B)."""
+    data = _f32(data)
+    n = data.shape[0]
+    ids = np.ascontiguousarray(ids, np.int32)
+    dists = np.ascontiguousarray(dists, np.float32)
+    counts = np.ascontiguousarray(counts, np.int32)
+    width = ids.shape[1]
+    live = np.arange(width)[None, :] < counts[:, None]
+    flat = ids[live]  # row-major == np.concatenate of live prefixes
+    rev_counts = np.bincount(flat, minlength=n).astype(np.int64)
+    rev_off = np.zeros(n + 1, np.int64)
+    np.cumsum(rev_counts, out=rev_off[1:])
+    rev_ids = np.empty(int(rev_off[-1]), np.int32)
+    rev_dists = np.empty(int(rev_off[-1]), np.float32)
+    lib().orc_scatter_reverse(_p(ids), _p(dists), _p(counts), n, width, _p(rev_off),
+                              _p(rev_ids), _p(rev_dists))
+    mrg_cap = counts.astype(np.int64) + rev_counts
+    mrg_off = np.zeros(n + 1, np.int64)
+    np.cumsum(mrg_cap, out=mrg_off[1:])
+    mrg_ids = np.empty(int(mrg_off[-1]), np.int32)
+    mrg_dists = np.empty(int(mrg_off[-1]), np.float32)
+    mrg_counts = np.zeros(n, np.int32)
+    lib().orc_merge_with_reverse(_p(ids), _p(dists), _p(counts), n, width, _p(rev_off),
+                                 _p(rev_ids), _p(rev_dists), _p(mrg_off), _p(mrg_ids),
+                                 _p(mrg_dists), _p(mrg_counts))
+    return prune_all(data, mrg_off, mrg_counts, mrg_ids, mrg_dists, M, strategy, alpha)
+
+
+def knn_pool_ids(data, k: int, exclude_self: bool = True, rows=None):
+    """Exact k-NN ids in (float64 dist, id) order (oracle.py:31-65 semantics,
+    direct-difference float64).  ``rows`` restricts the query rows."""
+    data = _f32(data)
+    n, d = data.shape
+    if rows is None:
+        nr, rp = n, None
+    else:
+        rows = np.ascontiguousarray(rows, np.int64)
+        nr, rp = rows.shape[0], _p(rows)
+    out = np.empty((nr, k), np.int32)
+    d64 = np.empty((nr, k), np.float64)
+    lib().orc_knn_pool(_p(data), n, d, k, int(exclude_self), rp, nr, _p(out), _p(d64))
+    return out, d64
+
+
+def list_dists_sorted(data, ids, rows=None):
+    """fp32 ``squared_l2(data[v], data[u])`` for an id table, rows re-sorted by
+    (fp32 dist, id) (test_nsg.py:16-24 + sort_pairs)."""
+    data = _f32(data)
+    ids = np.array(ids, dtype=np.int32, copy=True, order="C")
+    nr, k = ids.shape
+    if rows is None:
+        rp = None
+    else:
+        rows = np.ascontiguousarray(rows, np.int64)
+        rp = _p(rows)
+    dists = np.empty((nr, k), np.float32)
+    lib().orc_list_dists_sorted(_p(data), data.shape[1], rp, nr, k, _p(ids), _p(dists))
+    return ids, dists
+
+
+def knn_pools(data, k: int, rows=None):
+    """The hot path's candidate pools: exact k-NN (self excluded), fp32 list
+    distances, rows ascending by (fp32 dist, id)."""
+    ids, _ = knn_pool_ids(data, k, True, rows)
+    return list_dists_sorted(data, ids, rows)
+
+
+def ground_truth_table(data, k: int = 10, exclude_self: bool = False,
+                       chunk: int = 256) -> np.ndarray:
+    """oracle.py:31-65 restated with numpy (queries=None): float64 norm
+    expansion through BLAS, clamp at 0, diagonal +inf, stable argsort."""
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    base = np.asarray(data, dtype=np.float64)
+    n = base.shape[0]
+    base_sq = np.einsum("ij,ij->i", base, base)
+    out = np.empty((n, k), np.int32)
+    for lo in range(0, n, chunk):
+        hi = min(lo + chunk, n)
+        block = base[lo:hi]
+        d2 = base_sq[None, :] - 2.0 * (block @ base.T)
+        d2 += np.einsum("ij,ij->i", block, block)[:, None]
+        np.maximum(d2, 0.0, out=d2)
+        if exclude_self:
+            d2[np.arange(hi - lo), np.arange(lo, hi)] = np.inf
+        order = np.argsort(d2, axis=1, kind="stable")
+        out[lo:hi] = order[:, :k]
+    return out
+
+
+def refine_ab(data, pool_ids, pool_dists, M: int, strategy: str = "rng",
+              alpha: float = 60.0):
+    """Phases A and B on (n, K) pools (prune.py:232-249 with connect=False)."""
+    n, K = pool_ids.shape
+    off = np.arange(n + 1, dtype=np.int64) * K
+    cnt = np.full(n, K, np.int32)
+    a = prune_all(data, off, cnt, pool_ids.ravel(), pool_dists.ravel(), M, strategy, alpha)
+    b = add_reverse_and_prune(data, a[0], a[1], a[2], M, strategy, alpha)
+    return a, b

@@ -1,0 +1,210 @@
+"""Generate the golden fixtures under tests/golden/ by running the REFERENCE.
+
+Run in the build container only (the reference is not present on the GPU box):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONPATH=/root/reference/pkg/src:. \
+        python tests/golden/make_golden.py
+
+It imports the read-only reference package ``pgann`` and records, for a set of
+seeded inputs, the outputs of the hot-path composition the reference's own
+tests use:
+
+  * ``oracle.ground_truth_table(ds, None, k=K, exclude_self=True)`` (oracle.py:31-65)
+  * fp32 list distances ``_kernels.squared_l2`` (_kernels.py:17-24) re-sorted by
+    (fp32 dist, id) with ``_kernels.sort_pairs`` (_kernels.py:298-324)
+  * ``prune.prune_all`` (prune.py:109-126) = phase A, and
+    ``prune.add_reverse_and_prune`` (prune.py:129-151) = phase B,
+    for strategy "rng" and "alpha" (66 degrees).
+
+Large arrays are stored as sha256 digests plus a seeded row sample, small ones
+in full.  The fixtures are what pins ``oracle/`` (tests/test_oracle_golden.py).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent.parent))
+
+from numba import njit, prange  # noqa: E402
+
+from pgann import _kernels  # noqa: E402  (reference)
+from pgann.core import Dataset  # noqa: E402
+from pgann.oracle import ground_truth_table  # noqa: E402
+from pgann.prune import PruneParams, add_reverse_and_prune, prune_all  # noqa: E402
+
+from paper_2410_01231_b200 import synth  # noqa: E402
+
+
+def digest(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@njit(parallel=True, cache=True)
+def _list_dists(data, ids):
+    n, k = ids.shape
+    out = np.empty((n, k), np.float32)
+    for u in prange(n):
+        for j in range(k):
+            out[u, j] = _kernels.squared_l2(data[ids[u, j]], data[u])
+    return out
+
+
+@njit(cache=True)
+def _resort(ids, dists):
+    for u in range(ids.shape[0]):
+        _kernels.sort_pairs(ids[u], dists[u], ids.shape[1])
+
+
+def reference_composition(data: np.ndarray, K: int, R: int):
+    """Reference hot path: exact pool -> fp32 list dists -> phases A, B."""
+    ds = Dataset.from_array(data)
+    n = ds.n
+    truth = ground_truth_table(ds, None, k=K, exclude_self=True)
+    ids = truth.astype(np.int32).copy()
+    dists = _list_dists(ds.data, ids)
+    _resort(ids, dists)
+    off = (np.arange(n + 1, dtype=np.int64) * K)
+    cnt = np.full(n, K, np.int32)
+    out = dict(truth=truth, pool_ids=ids, pool_dists=dists)
+    for tag, params in (("rng", PruneParams(M=R, strategy="rng")),
+                        ("a66", PruneParams(M=R, alpha=66.0, strategy="alpha"))):
+        a_ids, a_d, a_c, a_de, a_ae = prune_all(ds, off, cnt, ids.ravel(),
+                                                dists.ravel(), params)
+        b_ids, b_d, b_c, b_de, b_ae = add_reverse_and_prune(ds, a_ids, a_d, a_c, params)
+        out.update({f"{tag}_a_ids": a_ids, f"{tag}_a_dists": a_d, f"{tag}_a_counts": a_c,
+                    f"{tag}_a_de": np.int64(a_de), f"{tag}_a_ae": np.int64(a_ae),
+                    f"{tag}_b_ids": b_ids, f"{tag}_b_dists": b_d, f"{tag}_b_counts": b_c,
+                    f"{tag}_b_de": np.int64(b_de), f"{tag}_b_ae": np.int64(b_ae)})
+    return out
+
+
+def save_config(name: str, data: np.ndarray, K: int, R: int, meta: dict,
+                full: bool) -> None:
+    res = reference_composition(data, K, R)
+    rec = {"meta_" + k: np.asarray(v) for k, v in meta.items()}
+    rec["data_digest"] = np.asarray(digest(data))
+    rng = np.random.default_rng(1234)
+    sample = np.sort(rng.choice(data.shape[0], size=min(256, data.shape[0]), replace=False))
+    rec["sample_rows"] = sample.astype(np.int64)
+    for k, v in res.items():
+        v = np.asarray(v)
+        if v.ndim == 0:
+            rec[k] = v
+            continue
+        rec[k + "__sha256"] = np.asarray(digest(v))
+        rec[k + "__sample"] = v[sample]
+        if full:
+            rec[k] = v
+    np.savez_compressed(HERE / f"{name}.npz", **rec)
+    print(name, {k: int(res[k]) for k in res if np.asarray(res[k]).ndim == 0})
+
+
+# ---------------------------------------------------------------------------
+# Edge cases taken from the reference's own prune tests (test_prune.py,
+# test_acceptance.py c01): CSR candidate lists that are NOT exact-kNN pools,
+# variable lengths, empty rows, self entries, duplicates and exact ties.
+# ---------------------------------------------------------------------------
+
+def _candidate_list(data, u, size, rng, allow_self=False):
+    n = data.shape[0]
+    others = np.array([v for v in range(n) if allow_self or v != u])
+    size = min(size, len(others))
+    pick = rng.choice(others, size=size, replace=False) if size else np.empty(0, int)
+    dists = np.array([_kernels.squared_l2(data[v], data[u]) for v in pick], np.float32)
+    order = np.lexsort((pick, dists))
+    return pick[order].astype(np.int32), dists[order]
+
+
+def csr_case(data, rng, max_len, allow_self, empty_frac=0.1):
+    n = data.shape[0]
+    lists = []
+    for u in range(n):
+        L = 0 if rng.random() < empty_frac else int(rng.integers(1, max_len + 1))
+        lists.append(_candidate_list(data, u, L, rng, allow_self))
+    counts = np.array([len(i) for i, _ in lists], np.int32)
+    # leave slack between slices: offsets need not be dense (prune_batch reads
+    # cand_counts[u] entries from cand_off[u])
+    slack = rng.integers(0, 3, size=n)
+    off = np.zeros(n + 1, np.int64)
+    np.cumsum(counts + slack, out=off[1:])
+    ids = np.full(int(off[-1]), -7, np.int32)
+    dists = np.full(int(off[-1]), np.nan, np.float32)
+    for u, (i, d) in enumerate(lists):
+        ids[off[u]:off[u] + len(i)] = i
+        dists[off[u]:off[u] + len(i)] = d
+    return off, counts, ids, dists
+
+
+def save_cases() -> None:
+    rec = {}
+    rng = np.random.default_rng(2024)
+    specs = [
+        # (name, data, max_len, allow_self, M, alpha)
+        ("unif", rng.random((200, 6)).astype(np.float32), 40, False, 12, 66.0),
+        ("unif_self", rng.random((150, 4)).astype(np.float32), 30, True, 7, 90.0),
+        ("lattice", np.stack(np.meshgrid(np.arange(12), np.arange(12)), -1)
+         .reshape(-1, 2).astype(np.float32), 30, False, 6, 120.0),
+        ("dups", np.repeat(rng.integers(0, 5, size=(40, 3)).astype(np.float32), 3, axis=0),
+         25, False, 5, 150.0),
+        ("gauss_d33", rng.standard_normal((120, 33)).astype(np.float32), 64, False, 24, 66.0),
+        ("m1", rng.random((80, 5)).astype(np.float32), 20, False, 1, 70.0),
+    ]
+    names = []
+    for name, data, max_len, allow_self, M, alpha in specs:
+        ds = Dataset.from_array(data)
+        off, counts, ids, dists = csr_case(data, rng, max_len, allow_self)
+        rec[f"{name}_data"] = data
+        rec[f"{name}_off"] = off
+        rec[f"{name}_counts"] = counts
+        rec[f"{name}_ids"] = ids
+        rec[f"{name}_dists"] = dists
+        rec[f"{name}_M"] = np.int64(M)
+        rec[f"{name}_alpha"] = np.float64(alpha)
+        for tag, params in (("rng", PruneParams(M=M, strategy="rng")),
+                            ("alpha", PruneParams(M=M, alpha=alpha, strategy="alpha"))):
+            a = prune_all(ds, off, counts, ids, dists, params)
+            b = add_reverse_and_prune(ds, a[0], a[1], a[2], params)
+            for ph, res in (("a", a), ("b", b)):
+                rec[f"{name}_{tag}_{ph}_ids"] = res[0]
+                rec[f"{name}_{tag}_{ph}_dists"] = res[1]
+                rec[f"{name}_{tag}_{ph}_counts"] = res[2]
+                rec[f"{name}_{tag}_{ph}_de"] = np.int64(res[3])
+                rec[f"{name}_{tag}_{ph}_ae"] = np.int64(res[4])
+        # exact pool on the same data (ties, duplicates)
+        k = min(10, data.shape[0] - 1)
+        rec[f"{name}_truth"] = ground_truth_table(ds, None, k=k, exclude_self=True)
+        names.append(name)
+    # hand triangle of test_prune.py:80-96 (angle at a ~ 147.27 degrees)
+    pts = np.array([[0, 0], [1, 0], [2.4, 0.9]], np.float32)
+    rec["tri_data"] = pts
+    rec["tri_d01"] = np.float32(_kernels.squared_l2(pts[1], pts[0]))
+    rec["tri_d02"] = np.float32(_kernels.squared_l2(pts[2], pts[0]))
+    rec["names"] = np.array(names)
+    np.savez_compressed(HERE / "cases.npz", **rec)
+    print("cases", names)
+
+
+def main() -> None:
+    os.makedirs(HERE, exist_ok=True)
+    save_cases()
+    save_config("cfg1_full", synth.cfg1(10_000), 64, 24,
+                dict(config=1, n=10_000, K=64, R=24), full=False)
+    save_config("cfg1_2k", synth.cfg1(2_000), 64, 24,
+                dict(config=1, n=2_000, K=64, R=24), full=True)
+    save_config("cfg2_4k", synth.cfg2(4_000), 128, 32,
+                dict(config=2, n=4_000, K=128, R=32), full=False)
+    save_config("cfg3_2k", synth.cfg3(2_000), 128, 32,
+                dict(config=3, n=2_000, K=128, R=32), full=False)
+    save_config("cfg4_2k", synth.cfg4(2_000), 256, 64,
+                dict(config=4, n=2_000, K=256, R=64), full=False)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,93 @@
+"""Pin the CPU oracle against the reference's own outputs (tests/golden/).
+
+The fixtures were produced by running the reference package itself
+(tests/golden/make_golden.py).  Everything here is CPU-only.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import oracle
+from paper_2410_01231_b200 import synth
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+CASES = ["unif", "unif_self", "lattice", "dups", "gauss_d33", "m1"]
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("strategy", ["rng", "alpha"])
+def test_oracle_prune_matches_reference_cases(golden_cases, name, strategy):
+    g = golden_cases
+    data = g[f"{name}_data"]
+    M = int(g[f"{name}_M"])
+    alpha = float(g[f"{name}_alpha"]) if strategy == "alpha" else 60.0
+    a = oracle.prune_all(data, g[f"{name}_off"], g[f"{name}_counts"], g[f"{name}_ids"],
+                         g[f"{name}_dists"], M, strategy, alpha)
+    b = oracle.add_reverse_and_prune(data, a[0], a[1], a[2], M, strategy, alpha)
+    for ph, res in (("a", a), ("b", b)):
+        p = f"{name}_{strategy}_{ph}_"
+        np.testing.assert_array_equal(res[0], g[p + "ids"])
+        np.testing.assert_array_equal(res[1], g[p + "dists"])
+        np.testing.assert_array_equal(res[2], g[p + "counts"])
+        assert res[3] == int(g[p + "de"]) and res[4] == int(g[p + "ae"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_pool_matches_reference_cases(golden_cases, name):
+    g = golden_cases
+    data = g[f"{name}_data"]
+    truth = g[f"{name}_truth"]
+    ids, _ = oracle.knn_pool_ids(data, truth.shape[1], True)
+    np.testing.assert_array_equal(ids, truth)
+    np.testing.assert_array_equal(oracle.ground_truth_table(data, truth.shape[1], True), truth)
+
+
+def test_oracle_triangle(golden_cases):
+    g = golden_cases
+    pts = g["tri_data"]
+    assert oracle.squared_l2(pts[1], pts[0]) == float(g["tri_d01"])
+    assert oracle.squared_l2(pts[2], pts[0]) == float(g["tri_d02"])
+    ids = np.array([1, 2], np.int32)
+    d = np.array([g["tri_d01"], g["tri_d02"]], np.float32)
+    off = np.array([0, 2, 2, 2], np.int64)
+    cnt = np.array([2, 0, 0], np.int32)
+    for strategy, alpha, want in (("alpha", 120.0, [1]), ("alpha", 150.0, [1, 2]),
+                                  ("rng", 60.0, [1])):
+        r = oracle.prune_all(pts, off, cnt, ids, d, 2, strategy, alpha)
+        assert r[0][0, :r[2][0]].tolist() == want
+
+
+CONFIGS = {
+    "cfg1_2k": lambda: synth.cfg1(2_000),
+    "cfg1_full": lambda: synth.cfg1(10_000),
+    "cfg2_4k": lambda: synth.cfg2(4_000),
+    "cfg3_2k": lambda: synth.cfg3(2_000),
+    "cfg4_2k": lambda: synth.cfg4(2_000),
+}
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_oracle_composition_matches_reference(name):
+    g = load_golden(name)
+    data = CONFIGS[name]()
+    assert sha(data) == str(g["data_digest"]), "synthetic recipe drifted"
+    K, R = int(g["meta_K"]), int(g["meta_R"])
+    truth, _ = oracle.knn_pool_ids(data, K, True)
+    assert sha(truth) == str(g["truth__sha256"])
+    ids, dists = oracle.list_dists_sorted(data, truth)
+    assert sha(ids) == str(g["pool_ids__sha256"])
+    assert sha(dists) == str(g["pool_dists__sha256"])
+    for tag, strategy, alpha in (("rng", "rng", 60.0), ("a66", "alpha", 66.0)):
+        a, b = oracle.refine_ab(data, ids, dists, R, strategy, alpha)
+        for ph, res in (("a", a), ("b", b)):
+            p = f"{tag}_{ph}_"
+            assert sha(res[0]) == str(g[p + "ids__sha256"]), p
+            assert sha(res[1]) == str(g[p + "dists__sha256"]), p
+            assert sha(res[2]) == str(g[p + "counts__sha256"]), p
+            assert res[3] == int(g[p + "de"]) and res[4] == int(g[p + "ae"]), p
