@@ -1,0 +1,131 @@
+/*
+ * pgk.h -- C ABI of the B200 (sm_100a) RNG index-construction hot path.
+ *
+ * The reference (pgann, Python + numba) has no FFI of its own: its hot loops are
+ * numba kernels called from prune.py / oracle.py with plain numpy arrays and
+ * caller-allocated out-params.  Each entry point below replaces one of those
+ * call sites (cited per function) and keeps its array conventions:
+ *   data      float32 (n, d) row-major, row i == id i        (core.py:18-47)
+ *   offsets   int64, counts int32, ids int32 (-1 = EMPTY), dists float32
+ *   strategy  0 = "rng", 1 = "alpha"; cos_alpha float64      (prune.py:24-56)
+ *
+ * Conventions of this ABI:
+ *   - every pointer argument is a DEVICE pointer unless the name says _host;
+ *   - `stream` is a cudaStream_t passed as void*; work is enqueued
+ *     asynchronously on it (no host synchronisation unless stated);
+ *   - no hidden allocations: scratch comes from the caller as (ws, ws_bytes),
+ *     sized by the matching *_workspace() query;
+ *   - no global mutable state; return PGK_OK (0) or an error code, with a
+ *     message from pgk_last_error() (thread-local).  Nothing throws across
+ *     the ABI.
+ *   - outputs are written in full, padding included (-1 ids / +inf dists), so
+ *     the caller need not pre-fill them the way prune.py:117-120 does.
+ */
+#ifndef PGK_H_
+#define PGK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PGK_OK 0
+#define PGK_ERR_INVALID 1     /* bad argument (shim raises ValueError)      */
+#define PGK_ERR_CUDA 2        /* CUDA launch / runtime error (RuntimeError) */
+#define PGK_ERR_NOMEM 3       /* workspace too small (MemoryError)          */
+#define PGK_ERR_UNSUPPORTED 4 /* shape outside the supported range          */
+
+/* Distance mode of the exact-kNN pool kernel. */
+#define PGK_POOL_AUTO 0 /* detect (one small device->host read)              */
+#define PGK_POOL_U8 1   /* every value an integer in [0,255], d <= 258: exact */
+#define PGK_POOL_F32 2  /* general fp32 data: approximate pass + fp64 rerank  */
+
+const char *pgk_version(void);
+const char *pgk_last_error(void);
+
+/* Number of SMs / device sanity check; returns PGK_OK when an sm_100 device is
+ * current. */
+int pgk_device_check(int *sm_count_host);
+
+/* ---------------------------------------------------------------------------
+ * Phase A edge selection.  Replaces _kernels.prune_batch (_kernels.py:412-427,
+ * called at prune.py:123-125) / _prune_row (_kernels.py:364-409).
+ * For every u: greedy occlusion / alpha-angle scan of the ascending (dist, id)
+ * slice cand_ids[cand_off[u] .. cand_off[u]+cand_counts[u]), kept <= M.
+ * out rows have stride `width` (>= M); dist_evals / angle_evals are per-node
+ * counters, identical to the reference's.  Bit-exact with the reference
+ * (fp32 sequential squared L2, fp64 law-of-cosines angle).
+ * ------------------------------------------------------------------------- */
+int pgk_prune_batch(const float *data, int64_t n, int64_t d,
+                    const int64_t *cand_off, const int32_t *cand_counts,
+                    const int32_t *cand_ids, const float *cand_dists,
+                    int strategy, double cos_alpha, int64_t M, int64_t width,
+                    int32_t *out_ids, float *out_dists, int32_t *out_counts,
+                    int64_t *dist_evals, int64_t *angle_evals, void *stream);
+
+/* Same scan for an arbitrary set of rows: row r holds the candidates of node
+ * row_node[r] (self-skip uses that id).  prune_row_single (_kernels.py:948-958)
+ * is the one-row case; pgk_prune_batch is row_node == NULL (row r == node r). */
+int pgk_prune_rows(const float *data, int64_t n, int64_t d, int64_t n_rows,
+                   const int32_t *row_node, const int64_t *cand_off,
+                   const int32_t *cand_counts, const int32_t *cand_ids,
+                   const float *cand_dists, int strategy, double cos_alpha,
+                   int64_t M, int64_t width, int32_t *out_ids, float *out_dists,
+                   int32_t *out_counts, int64_t *dist_evals, int64_t *angle_evals,
+                   void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Phase B: reverse-edge insertion + re-prune.  Replaces
+ * prune.add_reverse_and_prune (prune.py:129-151) = np.bincount/cumsum +
+ * _kernels.scatter_reverse (_kernels.py:530-541) + merge_with_reverse
+ * (_kernels.py:544-588) + prune_all.  a_* is the phase-A adjacency
+ * (n, a_width); outputs as pgk_prune_batch with stride out_width (>= M).
+ * ------------------------------------------------------------------------- */
+int pgk_reverse_workspace(int64_t n, int64_t a_width, size_t *ws_bytes_host);
+int pgk_add_reverse_and_prune(const float *data, int64_t n, int64_t d,
+                              const int32_t *a_ids, const float *a_dists,
+                              const int32_t *a_counts, int64_t a_width,
+                              int strategy, double cos_alpha, int64_t M,
+                              int64_t out_width, int32_t *out_ids,
+                              float *out_dists, int32_t *out_counts,
+                              int64_t *dist_evals, int64_t *angle_evals,
+                              void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Exact k-NN candidate pools.  Replaces oracle.ground_truth_table
+ * (oracle.py:31-65; queries = data rows, exclude_self) composed with the fp32
+ * list distances _kernels.squared_l2 (_kernels.py:17-24) and the (dist, id)
+ * re-sort sort_pairs (_kernels.py:298-324) that the reference's tests use to
+ * feed prune_all (test_nsg.py:16-24, test_prune.py:35-41).
+ *   queries == NULL  -> queries are the data rows (nq == n);
+ *   gt_ids (optional, may be NULL): (nq, k) ids in (float64 dist, id) order,
+ *                     i.e. ground_truth_table's output;
+ *   pool_ids / pool_dists: (nq, k) ids + fp32 squared_l2 dists, rows ascending
+ *                     by (fp32 dist, id).
+ * mode: PGK_POOL_*; AUTO performs a single blocking 4-byte read.
+ * ------------------------------------------------------------------------- */
+int pgk_detect_u8(const float *data, int64_t n, int64_t d, int *is_u8_host,
+                  void *ws, size_t ws_bytes, void *stream);
+int pgk_knn_workspace(int64_t n, int64_t nq, int64_t d, int64_t k, int mode,
+                      size_t *ws_bytes_host);
+int pgk_knn_pools(const float *data, int64_t n, int64_t d,
+                  const float *queries, int64_t nq, int64_t k, int exclude_self,
+                  int mode, int32_t *gt_ids, int32_t *pool_ids,
+                  float *pool_dists, void *ws, size_t ws_bytes, void *stream);
+
+/* Number of query rows that needed the exact float64 fallback scan in the most
+ * recent pgk_knn_pools call on this workspace (device int32 inside ws; this
+ * helper performs a blocking read). */
+int pgk_knn_fallback_rows(const void *ws, int *rows_host, void *stream);
+
+/* Cumulative number of kernel launches this library has issued since it was
+ * loaded (process-wide; the bench reports the difference around its timed
+ * region as gpu_launches). */
+int64_t pgk_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PGK_H_ */

@@ -1,0 +1,105 @@
+"""ctypes binding of libpgk.so (include/pgk.h).
+
+There is deliberately no CPU fallback: if the library is missing or no CUDA
+device is present, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import torch
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libpgk.so"
+
+OK, ERR_INVALID, ERR_CUDA, ERR_NOMEM, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
+POOL_AUTO, POOL_U8, POOL_F32 = 0, 1, 2
+
+_lib = None
+
+
+def lib():
+    """Load libpgk.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(python -m paper_2410_01231_b200.build_ext)")
+        L = ctypes.CDLL(str(LIB_PATH))
+        P, I64, I, D, SZ = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                            ctypes.c_double, ctypes.c_size_t)
+        L.pgk_version.restype = ctypes.c_char_p
+        L.pgk_last_error.restype = ctypes.c_char_p
+        L.pgk_launch_count.restype = I64
+        L.pgk_device_check.argtypes = [P]
+        L.pgk_prune_batch.argtypes = [P, I64, I64, P, P, P, P, I, D, I64, I64,
+                                      P, P, P, P, P, P]
+        L.pgk_prune_rows.argtypes = [P, I64, I64, I64, P, P, P, P, P, I, D, I64, I64,
+                                     P, P, P, P, P, P]
+        L.pgk_reverse_workspace.argtypes = [I64, I64, P]
+        L.pgk_add_reverse_and_prune.argtypes = [P, I64, I64, P, P, P, I64, I, D, I64, I64,
+                                                P, P, P, P, P, P, SZ, P]
+        L.pgk_detect_u8.argtypes = [P, I64, I64, P, P, SZ, P]
+        L.pgk_knn_workspace.argtypes = [I64, I64, I64, I64, I, P]
+        L.pgk_knn_pools.argtypes = [P, I64, I64, P, I64, I64, I, I, P, P, P, P, SZ, P]
+        L.pgk_knn_fallback_rows.argtypes = [P, P, P]
+        for f in ("pgk_device_check", "pgk_prune_batch", "pgk_prune_rows", "pgk_reverse_workspace",
+                  "pgk_add_reverse_and_prune", "pgk_detect_u8", "pgk_knn_workspace",
+                  "pgk_knn_pools", "pgk_knn_fallback_rows"):
+            getattr(L, f).restype = I
+        _lib = L
+    return _lib
+
+
+EXPORTS = ("pgk_version", "pgk_last_error", "pgk_device_check", "pgk_prune_batch",
+           "pgk_prune_rows",
+           "pgk_reverse_workspace", "pgk_add_reverse_and_prune", "pgk_detect_u8",
+           "pgk_knn_workspace", "pgk_knn_pools", "pgk_knn_fallback_rows",
+           "pgk_launch_count")
+
+
+def check(rc: int) -> None:
+    if rc == OK:
+        return
+    msg = lib().pgk_last_error().decode(errors="replace")
+    if rc == ERR_INVALID:
+        raise ValueError(msg)
+    if rc == ERR_NOMEM:
+        raise MemoryError(msg)
+    if rc == ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise RuntimeError(f"CUDA error: {msg}")
+
+
+_device_ok = False
+
+
+def device() -> torch.device:
+    """The CUDA device the kernels run on (raises without a B200)."""
+    global _device_ok
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2410_01231_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    if not _device_ok:
+        sms = ctypes.c_int(0)
+        check(lib().pgk_device_check(ctypes.byref(sms)))
+        _device_ok = True
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def stream_handle():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def launch_count() -> int:
+    return int(lib().pgk_launch_count())
+
+
+def workspace(nbytes: int) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device())

@@ -1,0 +1,150 @@
+// api.cu -- the extern "C" boundary (include/pgk.h).  Validates arguments,
+// maps errors to codes + a thread-local message, forwards to the kernels.
+#include <cstdarg>
+
+#include "common.cuh"
+
+namespace pgk {
+
+static thread_local char g_err[512] = "";
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int num_sms() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached = v > 0 ? v : 148;
+  }
+  return cached;
+}
+
+int launch_prune(const float *, int64_t, int64_t, const int32_t *, const int64_t *, const int32_t *,
+                 const int32_t *, const float *, int, double, int64_t, int64_t,
+                 int32_t *, float *, int32_t *, int64_t *, int64_t *, cudaStream_t);
+int reverse_workspace(int64_t n, int64_t width, size_t *bytes);
+int add_reverse_and_prune(const float *, int64_t, int64_t, const int32_t *, const float *,
+                          const int32_t *, int64_t, int, double, int64_t, int64_t,
+                          int32_t *, float *, int32_t *, int64_t *, int64_t *, void *,
+                          size_t, cudaStream_t);
+int knn_workspace(int64_t, int64_t, int64_t, int64_t, int, size_t *);
+int knn_pools(const float *, int64_t, int64_t, const float *, int64_t, int64_t, int, int,
+              int32_t *, int32_t *, float *, void *, size_t, cudaStream_t);
+int detect_u8(const float *, int64_t, int64_t, int *, void *, size_t, cudaStream_t);
+int fallback_rows(const void *, int *, cudaStream_t);
+
+}  // namespace pgk
+
+using namespace pgk;
+
+static int check_prune_args(const float *data, int64_t n, int64_t d, int strategy,
+                            int64_t M, int64_t width) {
+  PGK_REQUIRE(n >= 0 && d >= 1, "bad shape n=%lld d=%lld", (long long)n, (long long)d);
+  PGK_REQUIRE(n == 0 || data, "data is NULL");
+  PGK_REQUIRE(strategy == 0 || strategy == 1, "strategy must be 0 (rng) or 1 (alpha)");
+  PGK_REQUIRE(M >= 1, "M must be >= 1");
+  PGK_REQUIRE(width >= M, "row width %lld < M %lld", (long long)width, (long long)M);
+  PGK_REQUIRE(n < 0x7fffffffLL && width < 0x7fffffffLL, "n / width exceed int32 ids");
+  return PGK_OK;
+}
+
+extern "C" {
+
+const char *pgk_version(void) { return "pgk 0.1 (sm_100a)"; }
+const char *pgk_last_error(void) { return g_err; }
+int64_t pgk_launch_count(void) { return g_launches.load(); }
+
+int pgk_device_check(int *sm_count_host) {
+  int dev = 0;
+  PGK_CUDA(cudaGetDevice(&dev));
+  cudaDeviceProp p;
+  PGK_CUDA(cudaGetDeviceProperties(&p, dev));
+  if (sm_count_host) *sm_count_host = p.multiProcessorCount;
+  if (p.major != 10) {
+    set_error("device %s is sm_%d%d; this library is built for sm_100a", p.name, p.major,
+              p.minor);
+    return PGK_ERR_UNSUPPORTED;
+  }
+  return PGK_OK;
+}
+
+int pgk_prune_batch(const float *data, int64_t n, int64_t d, const int64_t *cand_off,
+                    const int32_t *cand_counts, const int32_t *cand_ids,
+                    const float *cand_dists, int strategy, double cos_alpha, int64_t M,
+                    int64_t width, int32_t *out_ids, float *out_dists, int32_t *out_counts,
+                    int64_t *dist_evals, int64_t *angle_evals, void *stream) {
+  int rc = check_prune_args(data, n, d, strategy, M, width);
+  if (rc) return rc;
+  return launch_prune(data, n, d, nullptr, cand_off, cand_counts, cand_ids, cand_dists, strategy,
+                      cos_alpha, M, width, out_ids, out_dists, out_counts, dist_evals,
+                      angle_evals, (cudaStream_t)stream);
+}
+
+int pgk_prune_rows(const float *data, int64_t n, int64_t d, int64_t n_rows,
+                   const int32_t *row_node, const int64_t *cand_off,
+                   const int32_t *cand_counts, const int32_t *cand_ids,
+                   const float *cand_dists, int strategy, double cos_alpha, int64_t M,
+                   int64_t width, int32_t *out_ids, float *out_dists, int32_t *out_counts,
+                   int64_t *dist_evals, int64_t *angle_evals, void *stream) {
+  int rc = check_prune_args(data, n, d, strategy, M, width);
+  if (rc) return rc;
+  PGK_REQUIRE(n_rows >= 0, "n_rows must be >= 0");
+  return launch_prune(data, n_rows, d, row_node, cand_off, cand_counts, cand_ids, cand_dists,
+                      strategy, cos_alpha, M, width, out_ids, out_dists, out_counts,
+                      dist_evals, angle_evals, (cudaStream_t)stream);
+}
+
+int pgk_reverse_workspace(int64_t n, int64_t a_width, size_t *ws_bytes_host) {
+  PGK_REQUIRE(ws_bytes_host, "ws_bytes_host is NULL");
+  return reverse_workspace(n, a_width, ws_bytes_host);
+}
+
+int pgk_add_reverse_and_prune(const float *data, int64_t n, int64_t d, const int32_t *a_ids,
+                              const float *a_dists, const int32_t *a_counts,
+                              int64_t a_width, int strategy, double cos_alpha, int64_t M,
+                              int64_t out_width, int32_t *out_ids, float *out_dists,
+                              int32_t *out_counts, int64_t *dist_evals,
+                              int64_t *angle_evals, void *ws, size_t ws_bytes,
+                              void *stream) {
+  int rc = check_prune_args(data, n, d, strategy, M, out_width);
+  if (rc) return rc;
+  PGK_REQUIRE(a_width >= 1, "phase-A width must be >= 1");
+  return add_reverse_and_prune(data, n, d, a_ids, a_dists, a_counts, a_width, strategy,
+                               cos_alpha, M, out_width, out_ids, out_dists, out_counts,
+                               dist_evals, angle_evals, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int pgk_detect_u8(const float *data, int64_t n, int64_t d, int *is_u8_host, void *ws,
+                  size_t ws_bytes, void *stream) {
+  PGK_REQUIRE(data && is_u8_host, "NULL argument");
+  return detect_u8(data, n, d, is_u8_host, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int pgk_knn_workspace(int64_t n, int64_t nq, int64_t d, int64_t k, int mode,
+                      size_t *ws_bytes_host) {
+  PGK_REQUIRE(ws_bytes_host, "ws_bytes_host is NULL");
+  return knn_workspace(n, nq <= 0 ? n : nq, d, k, mode, ws_bytes_host);
+}
+
+int pgk_knn_pools(const float *data, int64_t n, int64_t d, const float *queries, int64_t nq,
+                  int64_t k, int exclude_self, int mode, int32_t *gt_ids, int32_t *pool_ids,
+                  float *pool_dists, void *ws, size_t ws_bytes, void *stream) {
+  PGK_REQUIRE(data && pool_ids && pool_dists && ws, "NULL argument");
+  return knn_pools(data, n, d, queries, nq, k, exclude_self, mode, gt_ids, pool_ids,
+                   pool_dists, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int pgk_knn_fallback_rows(const void *ws, int *rows_host, void *stream) {
+  PGK_REQUIRE(ws && rows_host, "NULL argument");
+  return fallback_rows(ws, rows_host, (cudaStream_t)stream);
+}
+
+}  // extern "C"

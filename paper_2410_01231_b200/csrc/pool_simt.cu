@@ -1,0 +1,612 @@
+// pool_simt.cu -- exact k-NN candidate pools on CUDA cores (the general path)
+// plus the finalisation / fp64 rerank / exact fallback kernels shared with the
+// tensor-core path (pool_tc.cu).
+//
+// Reference: oracle.ground_truth_table (oracle.py:31-65) ranks every row of the
+// N x N float64 distance matrix with a stable argsort ((dist, id) order); the
+// tests then recompute fp32 squared_l2 list distances and re-sort by
+// (fp32 dist, id) (test_nsg.py:16-24, sort_pairs _kernels.py:298-324).
+//
+// Two exact modes:
+//  * U8  -- every value an integer in [0,255] and d <= 258 (config 2).  Then
+//           x.y, |x|^2 and the distance are integers below 2^24, so one FFMA
+//           dot product per pair plus the integer norm expansion is EXACT and
+//           equals both the reference's float64 ranking distance and its fp32
+//           sequential list distance.  Top-K by packed (dist, id) key is final.
+//  * F32 -- general data.  Pass 1 keeps the S = K + m best keys of an fp32
+//           direct-difference distance (FMA-accumulated; relative error
+//           <= (d+2)*2^-24, no cancellation).  Pass 2 reranks the S survivors
+//           with the oracle's float64 sequential distance and proves the K
+//           chosen are the exact top-K: every non-survivor j has
+//           d_j >= approx_S / (1 + gamma) > d64_K.  Rows where the proof fails
+//           (near-ties at the boundary, many exact duplicates) are rerun by an
+//           exact float64 full scan.
+//
+// Tile kernel: CTA = 32 query rows x stream of 128-column tiles, 256 threads,
+// each thread a 4 x 4 micro-tile; warp w owns rows 4w..4w+3 outright, so each
+// row's candidate buffer (CAP packed keys in shared memory) and threshold
+// (the S-th best key seen so far, warp-uniform in registers) need no atomics:
+// a ballot per (row, 32 columns) appends survivors, and a full buffer is
+// compacted by the owning warp alone (bitonic sort, keep S, raise threshold).
+#include "common.cuh"
+
+namespace pgk {
+
+constexpr int MODE_U8 = 1, MODE_F32 = 2;
+constexpr int TBM = 32, TBN = 128, TBK = 32;
+
+__global__ void detect_u8_kernel(const float *__restrict__ X, int64_t total,
+                                 int *__restrict__ flag) {
+  bool ok = true;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float v = X[e];
+    ok &= (v >= 0.0f) && (v <= 255.0f) && (v == rintf(v));
+  }
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicExch(flag, 0);
+}
+
+// Integer squared norms (exact: d * 255^2 < 2^31).
+__global__ void norms_u8_kernel(const float *__restrict__ X, int64_t n, int d,
+                                int32_t *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int acc = 0;
+    for (int i = lane; i < d; i += 32) {
+      int v = (int)X[r * d + i];
+      acc += v * v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[r] = acc;
+  }
+}
+
+// Sort one row's buffer (warp), keep the best S, raise the threshold.
+template <int CAP>
+__device__ __forceinline__ void compact_row(uint64_t *b, int &cnt, uint64_t &tau,
+                                            int S, int lane) {
+  for (int i = cnt + lane; i < CAP; i += 32) b[i] = KEY_MAX;
+  __syncwarp();
+  warp_bitonic_sort(b, CAP, lane);
+  if (cnt >= S) {
+    cnt = S;
+    tau = b[S - 1];
+  }
+  __syncwarp();
+}
+
+template <int MODE, int CAP>
+__global__ void __launch_bounds__(256, 1)
+    knn_tile_kernel(const float *__restrict__ X, int64_t n, int d,
+                    const float *__restrict__ Q, int64_t nq, int exclude_self,
+                    const int32_t *__restrict__ xnorm,
+                    const int32_t *__restrict__ qnorm, int S, int vec4,
+                    uint64_t *__restrict__ out_keys) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  float(*sA)[TBM + 1] = reinterpret_cast<float(*)[TBM + 1]>(smem);
+  float(*sB)[TBN + 1] =
+      reinterpret_cast<float(*)[TBN + 1]>(smem + TBK * (TBM + 1) * sizeof(float));
+  size_t off = (TBK * (TBM + 1) + TBK * (TBN + 1)) * sizeof(float);
+  off = (off + 15) & ~size_t(15);
+  uint64_t *sbuf = reinterpret_cast<uint64_t *>(smem + off);
+  int32_t *sxn = reinterpret_cast<int32_t *>(sbuf + TBM * CAP);
+
+  const int tid = threadIdx.x, ty = tid >> 5, tx = tid & 31;
+  const int64_t row0 = (int64_t)blockIdx.x * TBM;
+
+  int cnt[4];
+  uint64_t tau[4];
+  int32_t qn[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    cnt[i] = 0;
+    tau[i] = KEY_MAX;
+    int64_t g = row0 + ty * 4 + i;
+    qn[i] = (MODE == MODE_U8 && g < nq) ? qnorm[g] : 0;
+  }
+
+  // global -> register staging of one (column tile, k chunk)
+  const int lr = tid >> 3, lk = (tid & 7) * 4;  // A: row lr, dims lk..lk+3
+  float4 ra, rb[4];
+  auto load_regs = [&](int64_t c0, int k0) {
+    const int kk = k0 + lk;
+    {
+      int64_t g = row0 + lr;
+      ra = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (g < nq) {
+        const float *p = Q + g * d + kk;
+        if (vec4 && kk + 3 < d) ra = __ldg(reinterpret_cast<const float4 *>(p));
+        else {
+          if (kk < d) ra.x = __ldg(p);
+          if (kk + 1 < d) ra.y = __ldg(p + 1);
+          if (kk + 2 < d) ra.z = __ldg(p + 2);
+          if (kk + 3 < d) ra.w = __ldg(p + 3);
+        }
+      }
+    }
+#pragma unroll
+    for (int p4 = 0; p4 < 4; ++p4) {
+      int64_t c = c0 + lr + 32 * p4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c < n) {
+        const float *p = X + c * d + kk;
+        if (vec4 && kk + 3 < d) v = __ldg(reinterpret_cast<const float4 *>(p));
+        else {
+          if (kk < d) v.x = __ldg(p);
+          if (kk + 1 < d) v.y = __ldg(p + 1);
+          if (kk + 2 < d) v.z = __ldg(p + 2);
+          if (kk + 3 < d) v.w = __ldg(p + 3);
+        }
+      }
+      rb[p4] = v;
+    }
+  };
+
+  const int nk = (d + TBK - 1) / TBK;
+  const int64_t ntiles = (n + TBN - 1) / TBN;
+  const int64_t steps = ntiles * nk;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
+
+  load_regs(0, 0);
+  for (int64_t st = 0; st < steps; ++st) {
+    const int64_t ct = st / nk;
+    const int kc = (int)(st - ct * nk);
+    const int64_t c0 = ct * TBN;
+    // registers -> shared (transposed: [k][row] / [k][col])
+    sA[lk + 0][lr] = ra.x;
+    sA[lk + 1][lr] = ra.y;
+    sA[lk + 2][lr] = ra.z;
+    sA[lk + 3][lr] = ra.w;
+#pragma unroll
+    for (int p4 = 0; p4 < 4; ++p4) {
+      sB[lk + 0][lr + 32 * p4] = rb[p4].x;
+      sB[lk + 1][lr + 32 * p4] = rb[p4].y;
+      sB[lk + 2][lr + 32 * p4] = rb[p4].z;
+      sB[lk + 3][lr + 32 * p4] = rb[p4].w;
+    }
+    if (MODE == MODE_U8 && kc == 0 && tid < TBN) {
+      int64_t c = c0 + tid;
+      sxn[tid] = c < n ? xnorm[c] : 0;
+    }
+    __syncthreads();
+    if (st + 1 < steps) {
+      const int64_t ct1 = (st + 1) / nk;
+      load_regs(ct1 * TBN, (int)((st + 1) - ct1 * nk) * TBK);
+    }
+#pragma unroll 8
+    for (int k = 0; k < TBK; ++k) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = sA[k][ty * 4 + i];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) b[q] = sB[k][tx + 32 * q];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (MODE == MODE_U8) {
+            acc[i][q] = fmaf(a[i], b[q], acc[i][q]);
+          } else {
+            float t = a[i] - b[q];
+            acc[i][q] = fmaf(t, t, acc[i][q]);
+          }
+        }
+    }
+    if (kc == nk - 1) {
+      // epilogue: filter against the row thresholds, append survivors
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = ty * 4 + i;
+        const int64_t g = row0 + r;
+        uint64_t *b = sbuf + (size_t)r * CAP;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t c = c0 + tx + 32 * q;
+          bool valid = g < nq && c < n && !(exclude_self && c == g);
+          float dist;
+          if (MODE == MODE_U8) {
+            int di = qn[i] + sxn[tx + 32 * q] - 2 * __float2int_rn(acc[i][q]);
+            dist = (float)di;
+          } else {
+            dist = acc[i][q];
+          }
+          uint64_t key = pack_key(dist, (int32_t)c);
+          bool pass = valid && key < tau[i];
+          unsigned bal = __ballot_sync(0xffffffffu, pass);
+          if (bal) {
+            int np = __popc(bal);
+            if (cnt[i] + np > CAP) {
+              compact_row<CAP>(b, cnt[i], tau[i], S, tx);
+              pass = pass && key < tau[i];
+              bal = __ballot_sync(0xffffffffu, pass);
+              np = __popc(bal);
+            }
+            if (pass) b[cnt[i] + __popc(bal & lanemask_lt())] = key;
+            cnt[i] += np;
+          }
+          acc[i][q] = 0.f;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // final: sort each row, write the best S keys
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = ty * 4 + i;
+    const int64_t g = row0 + r;
+    uint64_t *b = sbuf + (size_t)r * CAP;
+    __syncwarp();
+    compact_row<CAP>(b, cnt[i], tau[i], S, tx);
+    if (g < nq)
+      for (int j = tx; j < S; j += 32) out_keys[g * S + j] = j < cnt[i] ? b[j] : KEY_MAX;
+  }
+}
+
+// U8 mode: keys are exact (dist, id); both output orders coincide.
+__global__ void finalize_exact_kernel(const uint64_t *__restrict__ keys, int64_t nq,
+                                      int S, int K, int32_t *__restrict__ gt_ids,
+                                      int32_t *__restrict__ pool_ids,
+                                      float *__restrict__ pool_dists) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nq * K;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / K;
+    int j = (int)(e - r * K);
+    uint64_t k = keys[r * S + j];
+    int32_t id = k == KEY_MAX ? -1 : key_id(k);
+    float dist = k == KEY_MAX ? __int_as_float(0x7f800000) : key_dist(k);
+    if (gt_ids) gt_ids[e] = id;
+    pool_ids[e] = id;
+    pool_dists[e] = dist;
+  }
+}
+
+// Given the exact top-K ids of one row in (d64, id) order in s_id[0..K), write
+// gt ids, then fp32 sequential list distances re-sorted by (fp32 dist, id).
+__device__ void write_pool_row(const float *__restrict__ X, const float *__restrict__ q,
+                               int d, bool vec4, int K, const int32_t *s_id,
+                               uint64_t *s_key, int K2, int64_t row,
+                               int32_t *__restrict__ gt_ids,
+                               int32_t *__restrict__ pool_ids,
+                               float *__restrict__ pool_dists, int lane) {
+  for (int j = lane; j < K2; j += 32) {
+    if (j < K) {
+      int32_t v = s_id[j];
+      if (gt_ids) gt_ids[row * K + j] = v;
+      float dist = v < 0 ? __int_as_float(0x7f800000)
+                         : (vec4 ? sql2_seq<true>(X + (int64_t)v * d, q, d)
+                                 : sql2_seq<false>(X + (int64_t)v * d, q, d));
+      s_key[j] = v < 0 ? KEY_MAX : pack_key(dist, v);
+    } else {
+      s_key[j] = KEY_MAX;
+    }
+  }
+  __syncwarp();
+  warp_bitonic_sort(s_key, K2, lane);
+  for (int j = lane; j < K; j += 32) {
+    uint64_t k = s_key[j];
+    pool_ids[row * K + j] = k == KEY_MAX ? -1 : key_id(k);
+    pool_dists[row * K + j] = k == KEY_MAX ? __int_as_float(0x7f800000) : key_dist(k);
+  }
+  __syncwarp();
+}
+
+constexpr int RR_WARPS = 4;
+constexpr int RR_MAXS = 512;
+
+// F32 mode pass 2: float64 rerank of the S survivors + boundary proof.
+__global__ void __launch_bounds__(RR_WARPS * 32)
+    rerank_kernel(const float *__restrict__ X, int d, const float *__restrict__ Q,
+                  int64_t nq, const uint64_t *__restrict__ keys, int S, int K,
+                  double gamma, int vec4, int32_t *__restrict__ gt_ids,
+                  int32_t *__restrict__ pool_ids, float *__restrict__ pool_dists,
+                  int32_t *__restrict__ fb_list, int32_t *__restrict__ fb_count) {
+  __shared__ double s_d[RR_WARPS][RR_MAXS];
+  __shared__ int32_t s_id[RR_WARPS][RR_MAXS];
+  __shared__ uint64_t s_key[RR_WARPS][RR_MAXS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S2 = next_pow2(S), K2 = next_pow2(K);
+  for (int64_t r = (int64_t)blockIdx.x * RR_WARPS + warp; r < nq;
+       r += (int64_t)gridDim.x * RR_WARPS) {
+    const float *q = Q + r * d;
+    __syncwarp();
+    for (int j = lane; j < S2; j += 32) {
+      uint64_t k = j < S ? keys[r * S + j] : KEY_MAX;
+      if (k != KEY_MAX) {
+        int32_t v = key_id(k);
+        s_id[warp][j] = v;
+        s_d[warp][j] = sql2_f64(X + (int64_t)v * d, q, d, vec4);
+      } else {
+        s_id[warp][j] = 0x7fffffff;
+        s_d[warp][j] = __longlong_as_double(0x7ff0000000000000ll);
+      }
+    }
+    __syncwarp();
+    warp_bitonic_sort_pairs(s_d[warp], s_id[warp], S2, lane);
+    const uint64_t klast = keys[r * S + S - 1];
+    bool safe = true;
+    if (klast != KEY_MAX) {
+      // every non-survivor has approx >= approx_S, hence true distance
+      // >= approx_S / (1 + gamma); its float64 value is within 1e-12 of that
+      const double lb = (double)key_dist(klast) / (1.0 + gamma) * (1.0 - 1e-12);
+      safe = s_d[warp][K - 1] < lb;
+    }
+    if (!safe) {
+      if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = (int32_t)r;
+      continue;
+    }
+    for (int j = lane; j < K; j += 32)
+      if (s_id[warp][j] == 0x7fffffff) s_id[warp][j] = -1;
+    __syncwarp();
+    write_pool_row(X, q, d, vec4, K, s_id[warp], s_key[warp], K2, r, gt_ids, pool_ids,
+                   pool_dists, lane);
+  }
+}
+
+// Exact float64 full scan for rows whose boundary proof failed.  One CTA per
+// listed row: 256 columns per round, survivors of the (d64, id) threshold are
+// appended to a shared buffer that is block-sorted when it could overflow.
+constexpr int FB_THREADS = 256;
+constexpr int FB_CAP = 1024;
+
+__global__ void __launch_bounds__(FB_THREADS)
+    fallback_kernel(const float *__restrict__ X, int64_t n, int d,
+                    const float *__restrict__ Q, int exclude_self, int K, int vec4,
+                    const int32_t *__restrict__ fb_list,
+                    const int32_t *__restrict__ fb_count,
+                    int32_t *__restrict__ gt_ids, int32_t *__restrict__ pool_ids,
+                    float *__restrict__ pool_dists) {
+  __shared__ double s_d[FB_CAP];
+  __shared__ int32_t s_id[FB_CAP];
+  __shared__ uint64_t s_key[FB_CAP];
+  __shared__ int s_cnt;
+  __shared__ double s_td;
+  __shared__ int32_t s_tid;
+  const int nl = *fb_count;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int li = blockIdx.x; li < nl; li += gridDim.x) {
+    const int64_t r = fb_list[li];
+    const float *q = Q + r * d;
+    if (tid == 0) {
+      s_cnt = 0;
+      s_td = __longlong_as_double(0x7ff0000000000000ll);
+      s_tid = 0x7fffffff;
+    }
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < n; c0 += FB_THREADS) {
+      const int64_t c = c0 + tid;
+      bool pass = false;
+      double dd = 0.0;
+      if (c < n && !(exclude_self && c == r)) {
+        dd = sql2_f64(X + c * d, q, d, vec4);
+        pass = dd < s_td || (dd == s_td && (int32_t)c < s_tid);
+      }
+      if (pass) {
+        int p = atomicAdd(&s_cnt, 1);
+        s_d[p] = dd;
+        s_id[p] = (int32_t)c;
+      }
+      __syncthreads();
+      if (s_cnt > FB_CAP - FB_THREADS || c0 + FB_THREADS >= n) {
+        // block bitonic sort of (d, id) pairs, keep K
+        const int cnt = s_cnt;
+        for (int i = cnt + tid; i < FB_CAP; i += FB_THREADS) {
+          s_d[i] = __longlong_as_double(0x7ff0000000000000ll);
+          s_id[i] = 0x7fffffff;
+        }
+        __syncthreads();
+        for (int k = 2; k <= FB_CAP; k <<= 1)
+          for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = tid; i < FB_CAP; i += FB_THREADS) {
+              int ixj = i ^ j;
+              if (ixj > i) {
+                double da = s_d[i], db = s_d[ixj];
+                int32_t ia = s_id[i], ib = s_id[ixj];
+                bool up = (i & k) == 0;
+                if (pair_gt(da, ia, db, ib) == up) {
+                  s_d[i] = db; s_d[ixj] = da; s_id[i] = ib; s_id[ixj] = ia;
+                }
+              }
+            }
+            __syncthreads();
+          }
+        if (tid == 0 && cnt >= K) {
+          s_cnt = K;
+          s_td = s_d[K - 1];
+          s_tid = s_id[K - 1];
+        }
+        __syncthreads();
+      }
+    }
+    if (tid < 32) {
+      for (int j = lane; j < K; j += 32)
+        if (j >= s_cnt || s_id[j] == 0x7fffffff) s_id[j] = -1;
+      __syncwarp();
+      write_pool_row(X, q, d, vec4, K, s_id, s_key, next_pow2(K), r, gt_ids, pool_ids,
+                     pool_dists, lane);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+struct KnnLayout {
+  int *flag;
+  int32_t *xnorm, *qnorm, *fb_list, *fb_count;
+  uint64_t *keys;
+  size_t total;
+};
+
+int pool_S(int64_t k, int mode) {
+  if (mode == PGK_POOL_U8) return (int)k;
+  int64_t m = k / 4 < 8 ? 8 : k / 4;
+  return (int)(k + m);
+}
+
+static KnnLayout knn_layout(void *ws, size_t bytes, int64_t n, int64_t nq, int64_t k,
+                            int mode) {
+  KnnLayout L{};
+  Carve c(ws, bytes);
+  const int S = pool_S(k, mode == PGK_POOL_AUTO ? PGK_POOL_F32 : mode);
+  L.flag = c.take<int>(4);
+  L.fb_count = c.take<int32_t>(4);
+  L.xnorm = c.take<int32_t>(n);
+  L.qnorm = c.take<int32_t>(nq);
+  L.fb_list = c.take<int32_t>(nq);
+  L.keys = c.take<uint64_t>((size_t)nq * S);
+  L.total = c.off;
+  return L;
+}
+
+int knn_workspace(int64_t n, int64_t nq, int64_t d, int64_t k, int mode, size_t *bytes) {
+  (void)d;
+  *bytes = knn_layout(nullptr, 0, n, nq, k, mode).total;
+  return PGK_OK;
+}
+
+int fallback_rows(const void *ws, int *rows_host, cudaStream_t stream) {
+  // fb_count sits right after the 4-int flag block (see knn_layout)
+  Carve c(const_cast<void *>(ws), ~size_t(0));
+  c.take<int>(4);
+  int32_t *fb = c.take<int32_t>(4);
+  PGK_CUDA(cudaMemcpyAsync(rows_host, fb, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  PGK_CUDA(cudaStreamSynchronize(stream));
+  return PGK_OK;
+}
+
+int detect_u8(const float *X, int64_t n, int64_t d, int *is_u8, void *ws, size_t bytes,
+              cudaStream_t stream) {
+  PGK_REQUIRE(ws && bytes >= sizeof(int) * 4, "detect_u8: workspace too small");
+  int *flag = reinterpret_cast<int *>(ws);
+  const int one = 1;
+  PGK_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, stream));
+  const int64_t total = n * d;
+  unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+  if (blocks == 0) blocks = 1;
+  detect_u8_kernel<<<blocks, 256, 0, stream>>>(X, total, flag);
+  PGK_CHECK_LAUNCH("detect_u8_kernel");
+  int h = 0;
+  PGK_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  PGK_CUDA(cudaStreamSynchronize(stream));
+  *is_u8 = (h != 0) && d <= 258;
+  return PGK_OK;
+}
+
+template <int MODE, int CAP>
+static int launch_tile(const float *X, int64_t n, int d, const float *Q, int64_t nq,
+                       int exclude_self, const int32_t *xn, const int32_t *qn, int S,
+                       int vec4, uint64_t *keys, cudaStream_t stream) {
+  size_t smem = (TBK * (TBM + 1) + TBK * (TBN + 1)) * sizeof(float);
+  smem = (smem + 15) & ~size_t(15);
+  smem += (size_t)TBM * CAP * sizeof(uint64_t) + TBN * sizeof(int32_t);
+  static bool attr = false;
+  if (!attr) {
+    PGK_CUDA(cudaFuncSetAttribute(knn_tile_kernel<MODE, CAP>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const unsigned grid = (unsigned)((nq + TBM - 1) / TBM);
+  knn_tile_kernel<MODE, CAP><<<grid, 256, smem, stream>>>(X, n, d, Q, nq, exclude_self, xn,
+                                                          qn, S, vec4, keys);
+  PGK_CHECK_LAUNCH("knn_tile_kernel");
+  return PGK_OK;
+}
+
+int launch_pool_tc_u8(const float *X, int64_t n, int d, const float *Q, int64_t nq,
+                      int exclude_self, const int32_t *xnorm, const int32_t *qnorm,
+                      int K, uint64_t *keys, cudaStream_t stream, bool *handled);
+
+int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, int64_t k,
+              int exclude_self, int mode, int32_t *gt_ids, int32_t *pool_ids,
+              float *pool_dists, void *ws, size_t bytes, cudaStream_t stream) {
+  PGK_REQUIRE(k >= 1, "k must be >= 1");
+  PGK_REQUIRE(n >= 1 && d >= 1, "dataset must be non-empty");
+  const bool self = (Q == nullptr);
+  if (self) { Q = X; nq = n; }
+  PGK_REQUIRE(!exclude_self || self, "exclude_self requires queries=None");
+  PGK_REQUIRE(k <= (exclude_self ? n - 1 : n), "k=%lld exceeds the number of candidates",
+              (long long)k);
+  if (mode == PGK_POOL_AUTO) {
+    int a = 0, b = 1;
+    int rc = detect_u8(X, n, d, &a, ws, bytes, stream);
+    if (rc) return rc;
+    if (!self) {
+      rc = detect_u8(Q, nq, d, &b, ws, bytes, stream);
+      if (rc) return rc;
+    }
+    mode = (a && b) ? PGK_POOL_U8 : PGK_POOL_F32;
+  }
+  PGK_REQUIRE(mode == PGK_POOL_U8 || mode == PGK_POOL_F32, "bad pool mode %d", mode);
+  if (mode == PGK_POOL_U8 && d > 258) {
+    set_error("U8 pool mode needs d <= 258");
+    return PGK_ERR_UNSUPPORTED;
+  }
+  KnnLayout L = knn_layout(ws, bytes, n, nq, k, mode);
+  if (L.total > bytes) {
+    set_error("knn workspace too small: need %zu, got %zu", L.total, bytes);
+    return PGK_ERR_NOMEM;
+  }
+  const int S = pool_S(k, mode);
+  if (S > 480 || k > 480) {
+    set_error("pool width k=%lld unsupported (max 480 in U8 mode, 384 in F32 mode)",
+              (long long)k);
+    return PGK_ERR_UNSUPPORTED;
+  }
+  const int vec4 = (d % 4 == 0) && ((uintptr_t)X % 16 == 0) && ((uintptr_t)Q % 16 == 0);
+  const int sms = num_sms();
+  PGK_CUDA(cudaMemsetAsync(L.fb_count, 0, sizeof(int32_t), stream));
+  int rc;
+  if (mode == PGK_POOL_U8) {
+    norms_u8_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(X, n, (int)d, L.xnorm);
+    PGK_CHECK_LAUNCH("norms_u8_kernel");
+    const int32_t *qn = L.xnorm;
+    if (!self) {
+      norms_u8_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(Q, nq, (int)d, L.qnorm);
+      PGK_CHECK_LAUNCH("norms_u8_kernel");
+      qn = L.qnorm;
+    }
+    bool handled = false;
+    rc = launch_pool_tc_u8(X, n, (int)d, Q, nq, exclude_self, L.xnorm, qn, (int)k, L.keys,
+                           stream, &handled);
+    if (rc) return rc;
+    if (!handled) {
+      rc = S <= 224 ? launch_tile<MODE_U8, 256>(X, n, (int)d, Q, nq, exclude_self, L.xnorm,
+                                                qn, S, vec4, L.keys, stream)
+                    : launch_tile<MODE_U8, 512>(X, n, (int)d, Q, nq, exclude_self, L.xnorm,
+                                                qn, S, vec4, L.keys, stream);
+      if (rc) return rc;
+    }
+    finalize_exact_kernel<<<(unsigned)sms * 8, 256, 0, stream>>>(L.keys, nq, S, (int)k,
+                                                                 gt_ids, pool_ids, pool_dists);
+    PGK_CHECK_LAUNCH("finalize_exact_kernel");
+    return PGK_OK;
+  }
+  rc = S <= 224 ? launch_tile<MODE_F32, 256>(X, n, (int)d, Q, nq, exclude_self, nullptr,
+                                             nullptr, S, vec4, L.keys, stream)
+                : launch_tile<MODE_F32, 512>(X, n, (int)d, Q, nq, exclude_self, nullptr,
+                                             nullptr, S, vec4, L.keys, stream);
+  if (rc) return rc;
+  // (1+u)^(d+2) <= 1 + gamma for u = 2^-24
+  const double gamma = (double)(d + 2) * 5.9604644775390625e-08 * 1.001 + 1e-12;
+  const unsigned rgrid =
+      (unsigned)std::min<int64_t>((nq + RR_WARPS - 1) / RR_WARPS, (int64_t)sms * 16);
+  rerank_kernel<<<rgrid, RR_WARPS * 32, 0, stream>>>(X, (int)d, Q, nq, L.keys, S, (int)k,
+                                                     gamma, vec4, gt_ids, pool_ids,
+                                                     pool_dists, L.fb_list, L.fb_count);
+  PGK_CHECK_LAUNCH("rerank_kernel");
+  fallback_kernel<<<(unsigned)sms * 2, FB_THREADS, 0, stream>>>(
+      X, n, (int)d, Q, exclude_self, (int)k, vec4, L.fb_list, L.fb_count, gt_ids, pool_ids,
+      pool_dists);
+  PGK_CHECK_LAUNCH("fallback_kernel");
+  return PGK_OK;
+}
+
+}  // namespace pgk

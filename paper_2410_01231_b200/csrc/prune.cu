@@ -1,0 +1,227 @@
+// prune.cu -- phase-A edge selection (the reference's _prune_row /
+// prune_batch, _kernels.py:364-427) as a warp-per-point sm_100a kernel.
+//
+// Layout: one warp owns one point u.  The candidate slice is processed in
+// windows of W entries held in shared memory (id, dist, per-entry counters)
+// plus an order-preserving "alive" index list.  The greedy scan is run as
+// rounds over the kept set: whenever a candidate w is kept, every still-alive
+// later candidate is tested against w in parallel (one candidate per lane,
+// each lane computing the full fp32 sequential distance).  A candidate leaves
+// the alive list the moment some kept w dominates it.
+//
+// That evaluates exactly the reference's lazy pair set -- for each examined v,
+// the kept w's in kept order up to and including the first dominator -- so the
+// per-node dist_evals / angle_evals counters come out identical, and because
+// every pair distance uses the reference's arithmetic the verdicts (and thus
+// the adjacency) are bit-identical.  Entries after the point where the M-th
+// neighbour is kept are never examined by the reference; their counters are
+// discarded (their distances may have been computed speculatively).
+#include "common.cuh"
+
+namespace pgk {
+
+constexpr int PRUNE_WARPS = 8;
+constexpr int PRUNE_W = 256;  // window entries per warp
+
+struct PruneSmem {
+  int32_t id[PRUNE_WARPS][PRUNE_W];
+  float dist[PRUNE_WARPS][PRUNE_W];
+  int32_t de[PRUNE_WARPS][PRUNE_W];
+  int32_t ae[PRUNE_WARPS][PRUNE_W];
+  int16_t alive[PRUNE_WARPS][PRUNE_W];
+};
+
+// Test alive entries alive[a0 .. n_alive) against kept neighbour w; returns
+// the new alive count (survivors compacted to alive[0..), order kept).
+template <bool VEC4>
+__device__ __forceinline__ int test_round(
+    const float *__restrict__ X, int d, int32_t w, float duw, int strategy,
+    double cos_alpha, int a0, int n_alive, int32_t *s_id, float *s_dist,
+    int32_t *s_de, int32_t *s_ae, int16_t *s_alive, int lane) {
+  if (duw == 0.0f) return 0;  // _kernels.py:387-389: dominated, no evaluation
+  const float *xw = X + (int64_t)w * d;
+  int new_n = 0;
+  for (int base = a0; base < n_alive; base += 32) {
+    int a = base + lane;
+    bool act = a < n_alive;
+    bool survive = false;
+    int j = 0;
+    if (act) {
+      j = s_alive[a];
+      int32_t v = s_id[j];
+      float dv = s_dist[j];
+      // _kernels.py:390: dwv = squared_l2(data[w], data[v])
+      float dwv = sql2_seq<VEC4>(xw, X + (int64_t)v * d, d);
+      s_de[j] += 1;
+      bool dom;
+      if (dwv == 0.0f) {
+        dom = true;
+      } else if (dwv < dv) {
+        if (strategy == 0) {
+          dom = true;
+        } else {
+          double c = cos_angle_from_sq(duw, dwv, dv);
+          s_ae[j] += 1;
+          dom = c < cos_alpha;
+        }
+      } else {
+        dom = false;
+      }
+      survive = !dom;
+    }
+    unsigned b = __ballot_sync(0xffffffffu, survive);
+    if (survive) s_alive[new_n + __popc(b & lanemask_lt())] = (int16_t)j;
+    new_n += __popc(b);
+  }
+  __syncwarp();
+  return new_n;
+}
+
+template <bool VEC4>
+__global__ void __launch_bounds__(PRUNE_WARPS * 32)
+    prune_kernel(const float *__restrict__ X, int64_t n, int d,
+                 const int32_t *__restrict__ row_node,
+                 const int64_t *__restrict__ cand_off,
+                 const int32_t *__restrict__ cand_counts,
+                 const int32_t *__restrict__ cand_ids,
+                 const float *__restrict__ cand_dists, int strategy,
+                 double cos_alpha, int M, int width, int32_t *__restrict__ out_ids,
+                 float *__restrict__ out_dists, int32_t *__restrict__ out_counts,
+                 int64_t *__restrict__ dist_evals,
+                 int64_t *__restrict__ angle_evals) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PruneSmem &sm = *reinterpret_cast<PruneSmem *>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t *s_id = sm.id[warp];
+  float *s_dist = sm.dist[warp];
+  int32_t *s_de = sm.de[warp];
+  int32_t *s_ae = sm.ae[warp];
+  int16_t *s_alive = sm.alive[warp];
+
+  for (int64_t u = (int64_t)blockIdx.x * PRUNE_WARPS + warp; u < n;
+       u += (int64_t)gridDim.x * PRUNE_WARPS) {
+    const int64_t base = cand_off[u];
+    const int cnt = cand_counts[u];
+    const int32_t self = row_node ? row_node[u] : (int32_t)u;
+    int32_t *orow = out_ids + u * width;
+    float *odrow = out_dists + u * width;
+    int kept = 0;
+    bool stop = false;
+    long long de_tot = 0, ae_tot = 0;
+
+    for (int s = 0; s < cnt && !stop; s += PRUNE_W) {
+      const int wn = min(PRUNE_W, cnt - s);
+      __syncwarp();
+      for (int j = lane; j < wn; j += 32) {
+        s_id[j] = cand_ids[base + s + j];
+        s_dist[j] = cand_dists[base + s + j];
+        s_de[j] = 0;
+        s_ae[j] = 0;
+      }
+      __syncwarp();
+      // alive = examined candidates other than u itself (_kernels.py:380-382)
+      int n_alive = 0;
+      for (int j0 = 0; j0 < wn; j0 += 32) {
+        int j = j0 + lane;
+        bool al = j < wn && s_id[j] != self;
+        unsigned b = __ballot_sync(0xffffffffu, al);
+        if (al) s_alive[n_alive + __popc(b & lanemask_lt())] = (int16_t)j;
+        n_alive += __popc(b);
+      }
+      __syncwarp();
+      // rounds against neighbours kept in earlier windows
+      for (int kj = 0; kj < kept && n_alive > 0; ++kj) {
+        int32_t w = orow[kj];
+        float duw = odrow[kj];
+        n_alive = test_round<VEC4>(X, d, w, duw, strategy, cos_alpha, 0, n_alive,
+                                   s_id, s_dist, s_de, s_ae, s_alive, lane);
+      }
+      // in-window greedy: the first alive entry is the next kept neighbour
+      int stop_j = wn - 1;
+      while (n_alive > 0) {
+        const int e = s_alive[0];
+        const int32_t w = s_id[e];
+        const float duw = s_dist[e];
+        if (lane == 0) {
+          orow[kept] = w;
+          odrow[kept] = duw;
+        }
+        ++kept;
+        if (kept == M) {  // _kernels.py:378: later candidates never examined
+          stop = true;
+          stop_j = e;
+          break;
+        }
+        n_alive = test_round<VEC4>(X, d, w, duw, strategy, cos_alpha, 1, n_alive,
+                                   s_id, s_dist, s_de, s_ae, s_alive, lane);
+      }
+      __syncwarp();
+      long long de = 0, ae = 0;
+      for (int j = lane; j <= stop_j; j += 32) {
+        de += s_de[j];
+        ae += s_ae[j];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        de += __shfl_xor_sync(0xffffffffu, de, o);
+        ae += __shfl_xor_sync(0xffffffffu, ae, o);
+      }
+      de_tot += de;
+      ae_tot += ae;
+    }
+    __syncwarp();
+    for (int j = kept + lane; j < width; j += 32) {
+      orow[j] = -1;
+      odrow[j] = __int_as_float(0x7f800000);
+    }
+    if (lane == 0) {
+      out_counts[u] = kept;
+      dist_evals[u] = de_tot;
+      angle_evals[u] = ae_tot;
+    }
+  }
+}
+
+int launch_prune(const float *X, int64_t n, int64_t d, const int32_t *row_node,
+                 const int64_t *cand_off,
+                 const int32_t *cand_counts, const int32_t *cand_ids,
+                 const float *cand_dists, int strategy, double cos_alpha,
+                 int64_t M, int64_t width, int32_t *out_ids, float *out_dists,
+                 int32_t *out_counts, int64_t *dist_evals, int64_t *angle_evals,
+                 cudaStream_t stream) {
+  if (n == 0) return PGK_OK;
+  const size_t smem = sizeof(PruneSmem);
+  const bool vec4 = (d % 4 == 0) && ((uintptr_t)X % 16 == 0);
+  int64_t blocks = (n + PRUNE_WARPS - 1) / PRUNE_WARPS;
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (vec4) {
+    static bool attr = false;
+    if (!attr) {
+      PGK_CUDA(cudaFuncSetAttribute(prune_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      attr = true;
+    }
+    prune_kernel<true><<<(unsigned)blocks, PRUNE_WARPS * 32, smem, stream>>>(
+        X, n, (int)d, row_node, cand_off, cand_counts, cand_ids, cand_dists, strategy,
+        cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts,
+        dist_evals, angle_evals);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      PGK_CUDA(cudaFuncSetAttribute(prune_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      attr = true;
+    }
+    prune_kernel<false><<<(unsigned)blocks, PRUNE_WARPS * 32, smem, stream>>>(
+        X, n, (int)d, row_node, cand_off, cand_counts, cand_ids, cand_dists, strategy,
+        cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts,
+        dist_evals, angle_evals);
+  }
+  PGK_CHECK_LAUNCH("prune_kernel");
+  return PGK_OK;
+}
+
+}  // namespace pgk

@@ -1,0 +1,337 @@
+// reverse.cu -- phase B: reverse-edge insertion + re-prune
+// (prune.add_reverse_and_prune, prune.py:129-151).
+//
+// Reference: bincount of all live phase-A targets + cumsum (prune.py:134-138),
+// a serial owner-ascending scatter of (owner, owner's stored dist)
+// (_kernels.scatter_reverse :530-541), a per-node sort_pairs of the reverse
+// slice, a merge with the node's own row (own first on equal (dist, id)) that
+// drops consecutive duplicate ids (_kernels.merge_with_reverse :544-588), and
+// prune_all of every merged row with the same params.
+//
+// GPU pipeline (all on one stream, no host sync):
+//   1. count    : atomic in-degree histogram                      (rev_cnt)
+//   2. scan     : mrg_off = exclusive_scan(counts + rev_cnt)  (block scan,
+//                 recursive over block totals)
+//   3. scatter  : own entries to the front of each merged slice, reverse
+//                 entries after them at mrg_off[v] + counts[v] + atomic slot,
+//                 as packed (dist, id) keys
+//   4. sort     : per node, ascending sort of the whole slice (warp bitonic in
+//                 shared memory; long slices: block bitonic in global scratch)
+//                 then drop consecutive duplicate ids.  Sorting the union by
+//                 (dist, id) yields the same sequence as the reference's merge
+//                 (entries with equal (dist, id) are identical), so the atomic
+//                 arrival order never shows: the output is deterministic.
+//   5. re-prune : prune_kernel on the merged CSR.
+#include "common.cuh"
+
+namespace pgk {
+
+int launch_prune(const float *X, int64_t n, int64_t d, const int32_t *row_node,
+                 const int64_t *cand_off,
+                 const int32_t *cand_counts, const int32_t *cand_ids,
+                 const float *cand_dists, int strategy, double cos_alpha,
+                 int64_t M, int64_t width, int32_t *out_ids, float *out_dists,
+                 int32_t *out_counts, int64_t *dist_evals, int64_t *angle_evals,
+                 cudaStream_t stream);
+
+constexpr int SORT_WARPS = 8;
+constexpr int SORT_SMEM_KEYS = 512;  // per-warp in-shared-memory sort capacity
+
+__global__ void rev_count_kernel(const int32_t *__restrict__ ids,
+                                 const int32_t *__restrict__ counts, int64_t n,
+                                 int width, int32_t *__restrict__ rev_cnt) {
+  const int64_t total = n * width;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t u = e / width;
+    int j = (int)(e - u * width);
+    if (j < counts[u]) atomicAdd(rev_cnt + ids[e], 1);
+  }
+}
+
+// merged-slice capacity of node u: own entries + reverse entries (index n
+// holds 0 so an (n+1)-item exclusive scan also yields the total).
+__global__ void cap_kernel(const int32_t *__restrict__ counts,
+                           const int32_t *__restrict__ rev, int64_t n,
+                           int64_t *__restrict__ cap) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u <= n;
+       u += (int64_t)gridDim.x * blockDim.x)
+    cap[u] = u < n ? (int64_t)counts[u] + rev[u] : 0;
+}
+
+// Exclusive scan of int64: 1024 threads x 4 items per block, block totals
+// scanned recursively, then added back.
+constexpr int SCAN_T = 1024, SCAN_ITEMS = 4, SCAN_TILE = SCAN_T * SCAN_ITEMS;
+
+__global__ void __launch_bounds__(SCAN_T)
+    scan_block_kernel(const int64_t *__restrict__ in, int64_t *__restrict__ out,
+                      int64_t m, int64_t *__restrict__ bsum) {
+  __shared__ int64_t warp_tot[SCAN_T / 32];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  int64_t v[SCAN_ITEMS], run = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; ++i) {
+    v[i] = base + i < m ? in[base + i] : 0;
+    run += v[i];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = warp_tot[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t t = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += t;
+    }
+    warp_tot[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  int64_t pre = incl - run + (warp > 0 ? warp_tot[warp - 1] : 0);
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; ++i) {
+    if (base + i < m) out[base + i] = pre;
+    pre += v[i];
+  }
+  if (threadIdx.x == SCAN_T - 1) bsum[blockIdx.x] = pre;
+}
+
+__global__ void scan_add_kernel(int64_t *__restrict__ out, int64_t m,
+                                const int64_t *__restrict__ boff) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x)
+    out[e] += boff[e / SCAN_TILE];
+}
+
+static size_t scan_scratch(int64_t m) {
+  size_t tot = 0;
+  while (m > 1) {
+    int64_t nb = (m + SCAN_TILE - 1) / SCAN_TILE;
+    tot += 2 * (size_t)nb;
+    m = nb;
+  }
+  return tot + 2;
+}
+
+static int exclusive_scan(const int64_t *in, int64_t *out, int64_t m, int64_t *scratch,
+                          cudaStream_t stream) {
+  const int64_t nb = (m + SCAN_TILE - 1) / SCAN_TILE;
+  int64_t *bsum = scratch, *boff = scratch + nb;
+  scan_block_kernel<<<(unsigned)nb, SCAN_T, 0, stream>>>(in, out, m, bsum);
+  PGK_CHECK_LAUNCH("scan_block_kernel");
+  if (nb > 1) {
+    int rc = exclusive_scan(bsum, boff, nb, scratch + 2 * nb, stream);
+    if (rc) return rc;
+    unsigned g = (unsigned)std::min<int64_t>((m + 255) / 256, (int64_t)num_sms() * 16);
+    scan_add_kernel<<<g, 256, 0, stream>>>(out, m, boff);
+    PGK_CHECK_LAUNCH("scan_add_kernel");
+  }
+  return PGK_OK;
+}
+
+__global__ void scatter_kernel(const int32_t *__restrict__ ids,
+                               const float *__restrict__ dists,
+                               const int32_t *__restrict__ counts, int64_t n,
+                               int width, const int64_t *__restrict__ mrg_off,
+                               int32_t *__restrict__ rev_left,
+                               uint64_t *__restrict__ keys) {
+  const int64_t total = n * width;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t u = e / width;
+    int j = (int)(e - u * width);
+    if (j >= counts[u]) continue;
+    int32_t v = ids[e];
+    float dd = dists[e];
+    keys[mrg_off[u] + j] = pack_key(dd, v);  // own entry
+    int slot = atomicSub(rev_left + v, 1) - 1;
+    keys[mrg_off[v] + counts[v] + slot] = pack_key(dd, (int32_t)u);  // reverse
+  }
+}
+
+// Drop consecutive duplicate ids from a sorted key run, writing ids/dists at
+// out; returns the kept count.  Warp-cooperative.
+__device__ __forceinline__ int warp_dedupe(const uint64_t *s, int len,
+                                           int32_t *out_ids, float *out_d,
+                                           int lane) {
+  int m = 0;
+  for (int b = 0; b < len; b += 32) {
+    int i = b + lane;
+    bool keep = false;
+    uint64_t k = 0;
+    if (i < len) {
+      k = s[i];
+      keep = (i == 0) || key_id(s[i - 1]) != key_id(k);
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      int p = m + __popc(bal & lanemask_lt());
+      out_ids[p] = key_id(k);
+      out_d[p] = key_dist(k);
+    }
+    m += __popc(bal);
+  }
+  return m;
+}
+
+__global__ void __launch_bounds__(SORT_WARPS * 32)
+    merge_sort_kernel(const int64_t *__restrict__ mrg_off, int64_t n,
+                      const uint64_t *__restrict__ keys,
+                      int32_t *__restrict__ mrg_ids, float *__restrict__ mrg_d,
+                      int32_t *__restrict__ mrg_counts,
+                      int32_t *__restrict__ long_list,
+                      int32_t *__restrict__ long_count) {
+  __shared__ uint64_t s[SORT_WARPS][SORT_SMEM_KEYS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t *sk = s[warp];
+  for (int64_t u = (int64_t)blockIdx.x * SORT_WARPS + warp; u < n;
+       u += (int64_t)gridDim.x * SORT_WARPS) {
+    const int64_t lo = mrg_off[u];
+    const int len = (int)(mrg_off[u + 1] - lo);
+    if (len > SORT_SMEM_KEYS) {
+      if (lane == 0) long_list[atomicAdd(long_count, 1)] = (int32_t)u;
+      continue;
+    }
+    const int size = next_pow2(len < 2 ? 2 : len);
+    __syncwarp();
+    for (int i = lane; i < size; i += 32) sk[i] = i < len ? keys[lo + i] : KEY_MAX;
+    __syncwarp();
+    warp_bitonic_sort(sk, size, lane);
+    int m = warp_dedupe(sk, len, mrg_ids + lo, mrg_d + lo, lane);
+    if (lane == 0) mrg_counts[u] = m;
+  }
+}
+
+// Long slices (in-degree beyond the shared-memory capacity; hubs): one block
+// per node, bitonic sort in a pow2-padded global scratch, warp 0 dedupes.
+__global__ void long_sort_kernel(const int64_t *__restrict__ mrg_off,
+                                 const uint64_t *__restrict__ keys,
+                                 uint64_t *__restrict__ scratch,
+                                 const int32_t *__restrict__ long_list,
+                                 const int32_t *__restrict__ long_count,
+                                 int32_t *__restrict__ mrg_ids,
+                                 float *__restrict__ mrg_d,
+                                 int32_t *__restrict__ mrg_counts) {
+  const int nl = *long_count;
+  for (int li = blockIdx.x; li < nl; li += gridDim.x) {
+    const int64_t u = long_list[li];
+    const int64_t lo = mrg_off[u];
+    const int len = (int)(mrg_off[u + 1] - lo);
+    const int size = next_pow2(len);
+    // scratch region for this node: keys slice of 2*len >= size entries is
+    // reserved at 2*lo (the workspace holds 2x the key capacity)
+    uint64_t *g = scratch + 2 * lo;
+    for (int i = threadIdx.x; i < size; i += blockDim.x) g[i] = i < len ? keys[lo + i] : KEY_MAX;
+    __syncthreads();
+    for (int k = 2; k <= size; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < size; i += blockDim.x) {
+          int ixj = i ^ j;
+          if (ixj > i) {
+            uint64_t a = g[i], b = g[ixj];
+            bool up = (i & k) == 0;
+            if ((a > b) == up) { g[i] = b; g[ixj] = a; }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (threadIdx.x < 32) {
+      int m = warp_dedupe(g, len, mrg_ids + lo, mrg_d + lo, threadIdx.x);
+      if (threadIdx.x == 0) mrg_counts[u] = m;
+    }
+    __syncthreads();
+  }
+}
+
+struct RevLayout {
+  int32_t *rev_cnt, *rev_left, *long_list, *long_count;
+  int64_t *mrg_off;
+  uint64_t *keys, *scratch;
+  int32_t *mrg_ids, *mrg_counts;
+  float *mrg_d;
+  int64_t *cap, *scan_tmp;
+  size_t total;
+};
+
+static RevLayout rev_layout(void *ws, size_t ws_bytes, int64_t n, int64_t width) {
+  RevLayout L{};
+  Carve c(ws, ws_bytes);
+  const int64_t cap = 2 * n * width;  // own + reverse entries <= 2 * sum(counts)
+  L.rev_cnt = c.take<int32_t>(n);
+  L.rev_left = c.take<int32_t>(n);
+  L.long_list = c.take<int32_t>(n);
+  L.long_count = c.take<int32_t>(1);
+  L.mrg_off = c.take<int64_t>(n + 1);
+  L.mrg_counts = c.take<int32_t>(n);
+  L.keys = c.take<uint64_t>(cap);
+  L.scratch = c.take<uint64_t>(2 * cap + 2);
+  L.mrg_ids = c.take<int32_t>(cap);
+  L.mrg_d = c.take<float>(cap);
+  L.cap = c.take<int64_t>(n + 1);
+  L.scan_tmp = c.take<int64_t>(scan_scratch(n + 1));
+  L.total = c.off;
+  return L;
+}
+
+int reverse_workspace(int64_t n, int64_t width, size_t *bytes) {
+  *bytes = rev_layout(nullptr, 0, n, width).total;
+  return PGK_OK;
+}
+
+int add_reverse_and_prune(const float *X, int64_t n, int64_t d,
+                          const int32_t *a_ids, const float *a_dists,
+                          const int32_t *a_counts, int64_t a_width, int strategy,
+                          double cos_alpha, int64_t M, int64_t out_width,
+                          int32_t *out_ids, float *out_dists, int32_t *out_counts,
+                          int64_t *dist_evals, int64_t *angle_evals, void *ws,
+                          size_t ws_bytes, cudaStream_t stream) {
+  if (n == 0) return PGK_OK;
+  RevLayout L = rev_layout(ws, ws_bytes, n, a_width);
+  if (L.total > ws_bytes) {
+    set_error("reverse workspace too small: need %zu bytes, got %zu", L.total, ws_bytes);
+    return PGK_ERR_NOMEM;
+  }
+  const int sms = num_sms();
+  const int64_t edges = n * a_width;
+  const unsigned eblocks = (unsigned)std::min<int64_t>((edges + 255) / 256, (int64_t)sms * 16);
+
+  PGK_CUDA(cudaMemsetAsync(L.rev_cnt, 0, sizeof(int32_t) * n, stream));
+  PGK_CUDA(cudaMemsetAsync(L.long_count, 0, sizeof(int32_t), stream));
+  rev_count_kernel<<<eblocks, 256, 0, stream>>>(a_ids, a_counts, n, (int)a_width, L.rev_cnt);
+  PGK_CHECK_LAUNCH("rev_count_kernel");
+
+  // mrg_off[u] = sum_{t<u} (counts[t] + rev_cnt[t]); mrg_off[n] = total
+  cap_kernel<<<eblocks, 256, 0, stream>>>(a_counts, L.rev_cnt, n, L.cap);
+  PGK_CHECK_LAUNCH("cap_kernel");
+  int rc = exclusive_scan(L.cap, L.mrg_off, n + 1, L.scan_tmp, stream);
+  if (rc) return rc;
+  PGK_CUDA(cudaMemcpyAsync(L.rev_left, L.rev_cnt, sizeof(int32_t) * n,
+                           cudaMemcpyDeviceToDevice, stream));
+
+  scatter_kernel<<<eblocks, 256, 0, stream>>>(a_ids, a_dists, a_counts, n, (int)a_width,
+                                              L.mrg_off, L.rev_left, L.keys);
+  PGK_CHECK_LAUNCH("scatter_kernel");
+
+  const unsigned sblocks =
+      (unsigned)std::min<int64_t>((n + SORT_WARPS - 1) / SORT_WARPS, (int64_t)sms * 8);
+  merge_sort_kernel<<<sblocks, SORT_WARPS * 32, 0, stream>>>(
+      L.mrg_off, n, L.keys, L.mrg_ids, L.mrg_d, L.mrg_counts, L.long_list, L.long_count);
+  PGK_CHECK_LAUNCH("merge_sort_kernel");
+  long_sort_kernel<<<(unsigned)sms, 512, 0, stream>>>(L.mrg_off, L.keys, L.scratch,
+                                                      L.long_list, L.long_count,
+                                                      L.mrg_ids, L.mrg_d, L.mrg_counts);
+  PGK_CHECK_LAUNCH("long_sort_kernel");
+
+  return launch_prune(X, n, d, nullptr, L.mrg_off, L.mrg_counts, L.mrg_ids, L.mrg_d, strategy,
+                      cos_alpha, M, out_width, out_ids, out_dists, out_counts,
+                      dist_evals, angle_evals, stream);
+}
+
+}  // namespace pgk

@@ -1,0 +1,85 @@
+"""The whole hot path as one call: exact k-NN pools -> phase-A selection ->
+reverse-edge insertion + re-prune (the composition of
+oracle.ground_truth_table, fp32 list distances, prune.prune_all and
+prune.add_reverse_and_prune that the reference's tests use).
+
+``RngBuilder`` owns every device buffer for a fixed (n, d, K, R) so repeated
+builds (the bench) allocate nothing; ``build_rng_index`` is the host-buffer
+convenience call (numpy in, ProximityGraph out).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, kernels
+from .graph import ProximityGraph
+from .prune import PruneParams
+
+
+@dataclass
+class BuildOutput:
+    ids: torch.Tensor        # (n, R) int32 final adjacency, -1 padded
+    dists: torch.Tensor      # (n, R) float32
+    counts: torch.Tensor     # (n,) int32
+    a_counts: torch.Tensor   # phase-A degrees
+    dist_evals: torch.Tensor  # (2,) int64: phase A, phase B (device)
+    angle_evals: torch.Tensor
+
+
+class RngBuilder:
+    """Preallocated device pipeline for one problem shape."""
+
+    def __init__(self, n: int, d: int, K: int, params: PruneParams, mode: int):
+        dev = _lib.device()
+        self.n, self.d, self.K, self.params, self.mode = n, d, K, params, mode
+        M = params.M
+        I32, F32, I64 = torch.int32, torch.float32, torch.int64
+        self.pool_ws = _lib.workspace(kernels.knn_workspace_bytes(n, n, d, K, mode))
+        self.pool_out = (torch.empty((n, K), dtype=I32, device=dev),
+                         torch.empty((n, K), dtype=F32, device=dev), None)
+        self.cand_off = torch.arange(0, (n + 1) * K, K, dtype=I64, device=dev)
+        self.cand_counts = torch.full((n,), K, dtype=I32, device=dev)
+        self.a_out = (torch.empty((n, M), dtype=I32, device=dev),
+                      torch.empty((n, M), dtype=F32, device=dev),
+                      torch.empty(n, dtype=I32, device=dev),
+                      torch.empty(n, dtype=I64, device=dev),
+                      torch.empty(n, dtype=I64, device=dev))
+        self.rev_ws = _lib.workspace(kernels.reverse_workspace_bytes(n, M))
+        self.b_out = tuple(torch.empty_like(t) for t in self.a_out)
+
+    def pools(self, X: torch.Tensor):
+        r = kernels.knn_pools(X, self.K, None, True, self.mode, False, self.pool_ws,
+                              self.pool_out)
+        return r.pool_ids, r.pool_dists
+
+    def build(self, X: torch.Tensor) -> BuildOutput:
+        """Enqueue the whole path on the current stream (no host sync)."""
+        p = self.params
+        ids, dists = self.pools(X)
+        a = kernels.prune_batch(X, self.cand_off, self.cand_counts, ids, dists,
+                                p.strategy_code, p.cos_alpha, p.M, p.M, out=self.a_out)
+        b = kernels.add_reverse_and_prune(X, a[0], a[1], a[2], p.strategy_code, p.cos_alpha,
+                                          p.M, p.M, ws=self.rev_ws, out=self.b_out)
+        de = torch.stack([a[3].sum(), b[3].sum()])
+        ae = torch.stack([a[4].sum(), b[4].sum()])
+        return BuildOutput(b[0], b[1], b[2], a[2], de, ae)
+
+
+def pool_mode(X: torch.Tensor) -> int:
+    return _lib.POOL_U8 if kernels.detect_u8(X) else _lib.POOL_F32
+
+
+def build_rng_index(data, K: int, R: int, strategy: str = "rng", alpha: float = 60.0,
+                    ep: int = 0) -> ProximityGraph:
+    """Host-buffer entry point: numpy (n, d) float32 in, ProximityGraph out
+    (phases A+B, connect=False, as prune.refine(..., connect=False, ep=ep))."""
+    data = np.ascontiguousarray(data, dtype=np.float32)
+    X = torch.from_numpy(data).to(_lib.device())
+    params = PruneParams(M=R, alpha=alpha, strategy=strategy)
+    b = RngBuilder(data.shape[0], data.shape[1], K, params, pool_mode(X)).build(X)
+    return ProximityGraph(adj=b.ids.cpu().numpy(), counts=b.counts.cpu().numpy(), M=R,
+                          ep=ep)

@@ -1,0 +1,154 @@
+"""Device-level wrappers over the C ABI: torch CUDA tensors in, torch CUDA
+tensors out, everything enqueued on the current stream with no host sync.
+
+These are the building blocks of the reference-signature API (prune.py,
+pool.py) and of the bench's device-resident timed region.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import check, ptr
+
+_F32, _I32, _I64 = torch.float32, torch.int32, torch.int64
+
+
+def _dev(t, dtype) -> torch.Tensor:
+    dev = _lib.device()
+    if isinstance(t, torch.Tensor):
+        t = t.to(device=dev, dtype=dtype)
+    else:
+        t = torch.as_tensor(t, dtype=dtype).to(dev)
+    return t.contiguous()
+
+
+def prune_batch(X: torch.Tensor, cand_off, cand_counts, cand_ids, cand_dists,
+                strategy: int, cos_alpha: float, M: int, width: int | None = None,
+                row_node=None, out=None):
+    """Phase-A scan (pgk_prune_batch / pgk_prune_rows).  Returns device tensors
+    (ids (rows, width), dists, counts, dist_evals (rows,), angle_evals (rows,))."""
+    X = _dev(X, _F32)
+    n, d = X.shape
+    cand_off = _dev(cand_off, _I64)
+    cand_counts = _dev(cand_counts, _I32)
+    cand_ids = _dev(cand_ids, _I32)
+    cand_dists = _dev(cand_dists, _F32)
+    rows = cand_counts.shape[0]
+    width = M if width is None else width
+    dev = X.device
+    if out is None:
+        out = (torch.empty((rows, width), dtype=_I32, device=dev),
+               torch.empty((rows, width), dtype=_F32, device=dev),
+               torch.empty(rows, dtype=_I32, device=dev),
+               torch.empty(rows, dtype=_I64, device=dev),
+               torch.empty(rows, dtype=_I64, device=dev))
+    ids, dists, counts, de, ae = out
+    if row_node is None and rows == n:
+        rc = _lib.lib().pgk_prune_batch(
+            ptr(X), n, d, ptr(cand_off), ptr(cand_counts), ptr(cand_ids), ptr(cand_dists),
+            int(strategy), float(cos_alpha), int(M), int(width), ptr(ids), ptr(dists),
+            ptr(counts), ptr(de), ptr(ae), _lib.stream_handle())
+    else:
+        rn = None if row_node is None else _dev(row_node, _I32)
+        rc = _lib.lib().pgk_prune_rows(
+            ptr(X), n, d, rows, ptr(rn), ptr(cand_off), ptr(cand_counts), ptr(cand_ids),
+            ptr(cand_dists), int(strategy), float(cos_alpha), int(M), int(width), ptr(ids),
+            ptr(dists), ptr(counts), ptr(de), ptr(ae), _lib.stream_handle())
+    check(rc)
+    return ids, dists, counts, de, ae
+
+
+def reverse_workspace_bytes(n: int, a_width: int) -> int:
+    b = ctypes.c_size_t(0)
+    check(_lib.lib().pgk_reverse_workspace(int(n), int(a_width), ctypes.byref(b)))
+    return int(b.value)
+
+
+def add_reverse_and_prune(X: torch.Tensor, a_ids, a_dists, a_counts, strategy: int,
+                          cos_alpha: float, M: int, width: int | None = None, ws=None,
+                          out=None):
+    """Phase B (pgk_add_reverse_and_prune); device tensors in and out."""
+    X = _dev(X, _F32)
+    n, d = X.shape
+    a_ids = _dev(a_ids, _I32)
+    a_dists = _dev(a_dists, _F32)
+    a_counts = _dev(a_counts, _I32)
+    a_width = a_ids.shape[1]
+    width = M if width is None else width
+    dev = X.device
+    if ws is None:
+        ws = _lib.workspace(reverse_workspace_bytes(n, a_width))
+    if out is None:
+        out = (torch.empty((n, width), dtype=_I32, device=dev),
+               torch.empty((n, width), dtype=_F32, device=dev),
+               torch.empty(n, dtype=_I32, device=dev),
+               torch.empty(n, dtype=_I64, device=dev),
+               torch.empty(n, dtype=_I64, device=dev))
+    ids, dists, counts, de, ae = out
+    check(_lib.lib().pgk_add_reverse_and_prune(
+        ptr(X), n, d, ptr(a_ids), ptr(a_dists), ptr(a_counts), a_width, int(strategy),
+        float(cos_alpha), int(M), int(width), ptr(ids), ptr(dists), ptr(counts), ptr(de),
+        ptr(ae), ptr(ws), ws.numel(), _lib.stream_handle()))
+    return ids, dists, counts, de, ae
+
+
+def knn_workspace_bytes(n: int, nq: int, d: int, k: int, mode: int) -> int:
+    b = ctypes.c_size_t(0)
+    check(_lib.lib().pgk_knn_workspace(int(n), int(nq), int(d), int(k), int(mode),
+                                       ctypes.byref(b)))
+    return int(b.value)
+
+
+def detect_u8(X: torch.Tensor) -> bool:
+    """True when every value is an integer in [0, 255] (and d <= 258): the
+    exact integer pool path applies.  One blocking 4-byte read."""
+    X = _dev(X, _F32)
+    ws = _lib.workspace(256)
+    flag = ctypes.c_int(0)
+    check(_lib.lib().pgk_detect_u8(ptr(X), X.shape[0], X.shape[1], ctypes.byref(flag),
+                                   ptr(ws), ws.numel(), _lib.stream_handle()))
+    return bool(flag.value)
+
+
+@dataclass
+class PoolResult:
+    pool_ids: torch.Tensor    # (nq, k) int32, rows ascending by (fp32 dist, id)
+    pool_dists: torch.Tensor  # (nq, k) float32 squared_l2 list distances
+    gt_ids: torch.Tensor | None  # (nq, k) int32 in (float64 dist, id) order
+    ws: torch.Tensor
+
+
+def knn_pools(X: torch.Tensor, k: int, queries=None, exclude_self: bool = True,
+              mode: int = _lib.POOL_AUTO, want_gt: bool = True, ws=None,
+              out=None) -> PoolResult:
+    """Exact k-NN pools (pgk_knn_pools); device tensors, no sync (unless
+    mode == AUTO, which reads one flag)."""
+    X = _dev(X, _F32)
+    n, d = X.shape
+    Q = None if queries is None else _dev(queries, _F32)
+    nq = n if Q is None else Q.shape[0]
+    dev = X.device
+    if ws is None:
+        ws = _lib.workspace(knn_workspace_bytes(n, nq, d, k, mode))
+    if out is None:
+        out = (torch.empty((nq, k), dtype=_I32, device=dev),
+               torch.empty((nq, k), dtype=_F32, device=dev),
+               torch.empty((nq, k), dtype=_I32, device=dev) if want_gt else None)
+    pool_ids, pool_dists, gt = out
+    check(_lib.lib().pgk_knn_pools(
+        ptr(X), n, d, ptr(Q), nq, int(k), int(bool(exclude_self)), int(mode), ptr(gt),
+        ptr(pool_ids), ptr(pool_dists), ptr(ws), ws.numel(), _lib.stream_handle()))
+    return PoolResult(pool_ids, pool_dists, gt, ws)
+
+
+def fallback_rows(ws: torch.Tensor) -> int:
+    """Rows of the last knn_pools call on ``ws`` that needed the exact
+    float64 rescan (blocking)."""
+    v = ctypes.c_int(0)
+    check(_lib.lib().pgk_knn_fallback_rows(ptr(ws), ctypes.byref(v), _lib.stream_handle()))
+    return int(v.value)

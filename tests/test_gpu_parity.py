@@ -1,0 +1,247 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+outputs and the pinned CPU oracle.  Integer / index work must be bit-exact;
+list distances must equal the reference's fp32 squared_l2 bit-for-bit (the
+north star's 1e-5 relative tolerance is checked too, as the weaker bound)."""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+from oracle import oracle
+from paper_2410_01231_b200 import (Dataset, PruneParams, add_reverse_and_prune, alpha_prune,
+                                   ground_truth_table, knn_pools, prune_all, refine,
+                                   rng_prune, synth)
+from paper_2410_01231_b200 import kernels
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-5  # north_star: pairwise distances within 1e-5 relative
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+CASES = ["unif", "unif_self", "lattice", "dups", "gauss_d33", "m1"]
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("strategy", ["rng", "alpha"])
+def test_prune_phases_match_reference_cases(golden_cases, name, strategy):
+    g = golden_cases
+    ds = Dataset.from_array(g[f"{name}_data"])
+    M = int(g[f"{name}_M"])
+    alpha = float(g[f"{name}_alpha"]) if strategy == "alpha" else 60.0
+    params = PruneParams(M=M, alpha=alpha, strategy=strategy)
+    a = prune_all(ds, g[f"{name}_off"], g[f"{name}_counts"], g[f"{name}_ids"],
+                  g[f"{name}_dists"], params)
+    b = add_reverse_and_prune(ds, a[0], a[1], a[2], params)
+    for ph, res in (("a", a), ("b", b)):
+        p = f"{name}_{strategy}_{ph}_"
+        np.testing.assert_array_equal(res[0], g[p + "ids"])
+        np.testing.assert_array_equal(res[1], g[p + "dists"])
+        np.testing.assert_array_equal(res[2], g[p + "counts"])
+        assert res[3] == int(g[p + "de"]) and res[4] == int(g[p + "ae"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_ground_truth_table_matches_reference_cases(golden_cases, name):
+    g = golden_cases
+    ds = Dataset.from_array(g[f"{name}_data"])
+    truth = g[f"{name}_truth"]
+    np.testing.assert_array_equal(ground_truth_table(ds, None, k=truth.shape[1],
+                                                     exclude_self=True), truth)
+
+
+def test_hand_triangle_and_single_row_api(golden_cases):
+    g = golden_cases
+    pts = g["tri_data"]
+    ds = Dataset.from_array(pts)
+    ids = np.array([1, 2], np.int32)
+    d = np.array([g["tri_d01"], g["tri_d02"]], np.float32)
+    assert alpha_prune(ds, 0, ids, d, 2, 120.0)[0].tolist() == [1]
+    assert alpha_prune(ds, 0, ids, d, 2, 150.0)[0].tolist() == [1, 2]
+    assert rng_prune(ds, 0, ids, d, 2)[0].tolist() == [1]
+    with pytest.raises(ValueError, match="ascending"):
+        rng_prune(ds, 0, ids[::-1].copy(), d[::-1].copy(), 2)
+    # coincident points (test_prune.py:123-146)
+    pts = np.array([[0, 0], [0, 0], [1, 0], [0, 1]], np.float32)
+    ds = Dataset.from_array(pts)
+    assert rng_prune(ds, 0, np.array([1, 2, 3], np.int32),
+                     np.array([0, 1, 1], np.float32), 3)[0].tolist() == [1]
+    pts = np.array([[0, 0], [1, 0], [1, 0]], np.float32)
+    ds = Dataset.from_array(pts)
+    assert alpha_prune(ds, 0, np.array([1, 2], np.int32), np.array([1, 1], np.float32),
+                       2, 179.0)[0].tolist() == [1]
+
+
+def test_reverse_phase_adds_missing_backlink():
+    pts = np.array([[0.0], [1.0], [2.1]], np.float32)
+    ds = Dataset.from_array(pts)
+    ids = np.full((3, 2), -1, np.int32)
+    dists = np.full((3, 2), np.inf, np.float32)
+    counts = np.zeros(3, np.int32)
+    ids[1, 0], dists[1, 0], counts[1] = 0, 1.0, 1
+    ids[2, 0], dists[2, 0], counts[2] = 1, oracle.squared_l2(pts[2], pts[1]), 1
+    b_ids, _, b_counts, _, _ = add_reverse_and_prune(ds, ids, dists, counts,
+                                                     PruneParams(M=2, strategy="rng"))
+    assert 1 in b_ids[0, : b_counts[0]]
+    assert 2 in b_ids[1, : b_counts[1]]
+
+
+CONFIGS = {
+    "cfg1_2k": lambda: synth.cfg1(2_000),
+    "cfg1_full": lambda: synth.cfg1(10_000),
+    "cfg2_4k": lambda: synth.cfg2(4_000),
+    "cfg3_2k": lambda: synth.cfg3(2_000),
+    "cfg4_2k": lambda: synth.cfg4(2_000),
+}
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_hot_path_matches_reference_configs(name):
+    """pool -> phase A -> phase B against the reference's own outputs, exact."""
+    g = load_golden(name)
+    data = CONFIGS[name]()
+    assert sha(data) == str(g["data_digest"])
+    K, R = int(g["meta_K"]), int(g["meta_R"])
+    ds = Dataset.from_array(data)
+    ids, dists, gt = knn_pools(ds, K, want_gt=True)
+    assert sha(gt) == str(g["truth__sha256"])
+    assert sha(ids) == str(g["pool_ids__sha256"])
+    assert sha(dists) == str(g["pool_dists__sha256"])
+    n = ds.n
+    off = np.arange(n + 1, dtype=np.int64) * K
+    cnt = np.full(n, K, np.int32)
+    for tag, params in (("rng", PruneParams(M=R)),
+                        ("a66", PruneParams(M=R, alpha=66.0, strategy="alpha"))):
+        a = prune_all(ds, off, cnt, ids.ravel(), dists.ravel(), params)
+        b = add_reverse_and_prune(ds, a[0], a[1], a[2], params)
+        for ph, res in (("a", a), ("b", b)):
+            p = f"{tag}_{ph}_"
+            assert sha(res[0]) == str(g[p + "ids__sha256"]), p
+            assert sha(res[1]) == str(g[p + "dists__sha256"]), p
+            assert sha(res[2]) == str(g[p + "counts__sha256"]), p
+            assert res[3] == int(g[p + "de"]) and res[4] == int(g[p + "ae"]), p
+        graph = refine(ds, off, cnt, ids.ravel(), dists.ravel(), params, connect=False, ep=0)
+        graph.validate()
+        assert sha(graph.adj) == str(g[f"{tag}_b_ids__sha256"])
+
+
+def _edge_agreement(a_ids, a_cnt, b_ids, b_cnt):
+    n = a_ids.shape[0]
+    ea = {(u, int(v)) for u in range(n) for v in a_ids[u, :a_cnt[u]]}
+    eb = {(u, int(v)) for u in range(n) for v in b_ids[u, :b_cnt[u]]}
+    return len(ea & eb) / max(1, len(ea | eb))
+
+
+@pytest.mark.parametrize("gen,n,K,R", [(synth.cfg2, 20_000, 128, 32),
+                                       (synth.cfg1, 10_000, 64, 24),
+                                       (synth.cfg3, 6_000, 128, 32)])
+def test_larger_prefixes_against_oracle(gen, n, K, R):
+    """Bigger seeded prefixes: the CUDA path vs the oracle, exact."""
+    data = gen(n)
+    ds = Dataset.from_array(data)
+    ids, dists = knn_pools(ds, K)
+    rng = np.random.default_rng(5)
+    rows = np.sort(rng.choice(n, 300, replace=False))
+    o_ids, o_d = oracle.knn_pools(data, K, rows)
+    np.testing.assert_array_equal(ids[rows], o_ids)
+    np.testing.assert_array_equal(dists[rows], o_d)
+    for strategy, alpha in (("rng", 60.0), ("alpha", 66.0)):
+        params = PruneParams(M=R, alpha=alpha, strategy=strategy)
+        off = np.arange(n + 1, dtype=np.int64) * K
+        cnt = np.full(n, K, np.int32)
+        a = prune_all(ds, off, cnt, ids.ravel(), dists.ravel(), params)
+        b = add_reverse_and_prune(ds, a[0], a[1], a[2], params)
+        oa, ob = oracle.refine_ab(data, ids, dists, R, strategy, alpha)
+        for res, ores in ((a, oa), (b, ob)):
+            np.testing.assert_array_equal(res[0], ores[0])
+            np.testing.assert_array_equal(res[1], ores[1])
+            np.testing.assert_array_equal(res[2], ores[2])
+            assert res[3] == ores[3] and res[4] == ores[4]
+
+
+def test_float_fallback_rows_with_duplicates():
+    """Many exact duplicates at the pool boundary defeat the fp32 margin proof:
+    those rows go through the exact float64 rescan and must still match."""
+    rng = np.random.default_rng(3)
+    base = rng.standard_normal((20, 16)).astype(np.float32)
+    data = np.repeat(base, 100, axis=0)  # 2000 points, 100 exact copies each
+    data[::7] += 1e-3 * rng.standard_normal((len(data[::7]), 16)).astype(np.float32)
+    ds = Dataset.from_array(data)
+    K = 48
+    r = kernels.knn_pools(ds.device_data(), K, None, True, 2, True)
+    fb = kernels.fallback_rows(r.ws)
+    assert fb > 0
+    o_ids, o_d = oracle.knn_pools(data, K)
+    np.testing.assert_array_equal(r.pool_ids.cpu().numpy(), o_ids)
+    np.testing.assert_array_equal(r.pool_dists.cpu().numpy(), o_d)
+    gt, _ = oracle.knn_pool_ids(data, K)
+    np.testing.assert_array_equal(r.gt_ids.cpu().numpy(), gt)
+
+
+def test_hub_node_long_reverse_list():
+    """A hub chosen by every point: its merged list is far longer than the
+    per-warp shared-memory sort, exercising the long-slice path."""
+    rng = np.random.default_rng(8)
+    pts = rng.standard_normal((3000, 64))
+    pts /= np.linalg.norm(pts, axis=1, keepdims=True)
+    data = np.vstack([np.zeros((1, 64)), pts]).astype(np.float32)
+    ds = Dataset.from_array(data)
+    K, R = 16, 8
+    ids, dists = knn_pools(ds, K)
+    assert (ids[1:, 0] == 0).mean() > 0.99
+    params = PruneParams(M=R)
+    off = np.arange(ds.n + 1, dtype=np.int64) * K
+    cnt = np.full(ds.n, K, np.int32)
+    a = prune_all(ds, off, cnt, ids.ravel(), dists.ravel(), params)
+    b = add_reverse_and_prune(ds, a[0], a[1], a[2], params)
+    oa, ob = oracle.refine_ab(data, ids, dists, R)
+    for res, ores in ((a, oa), (b, ob)):
+        for i in range(3):
+            np.testing.assert_array_equal(res[i], ores[i])
+        assert res[3] == ores[3] and res[4] == ores[4]
+
+
+def test_queries_table_and_errors():
+    data = synth.cfg1(3000)
+    ds = Dataset.from_array(data)
+    q = synth.gen_synthetic(50, 32, "gaussian", seed=77)
+    table = ground_truth_table(ds, q, k=7)
+    assert table.shape == (50, 7)
+    for i in range(50):
+        d64 = ((data.astype(np.float64) - q[i].astype(np.float64)) ** 2).sum(1)
+        order = np.lexsort((np.arange(len(d64)), d64))[:7]
+        assert table[i].tolist() == order.tolist()
+    with pytest.raises(ValueError):
+        ground_truth_table(ds, q[:, :5], k=3)
+    with pytest.raises(ValueError):
+        ground_truth_table(ds, q, k=3, exclude_self=True)
+
+
+def test_distance_tolerance_statement():
+    """The north-star tolerance (1e-5 relative) holds trivially: list
+    distances are bit-identical to the reference's fp32 squared_l2."""
+    data = synth.cfg3(1500)
+    ds = Dataset.from_array(data)
+    ids, dists = knn_pools(ds, 64)
+    for u in range(0, 1500, 97):
+        for j in range(0, 64, 9):
+            ref = oracle.squared_l2(data[ids[u, j]], data[u])
+            assert dists[u, j] == ref
+            assert abs(dists[u, j] - ref) <= REL_TOL * ref
+
+
+def test_device_resident_api_keeps_tensors_on_gpu():
+    data = torch.from_numpy(synth.cfg2(3000)).cuda()
+    ds = Dataset(data)
+    assert ds.is_u8()
+    ids, dists = knn_pools(ds, 32)
+    assert ids.is_cuda and dists.is_cuda
+    off = torch.arange(0, 3001 * 32, 32, dtype=torch.int64, device="cuda")
+    cnt = torch.full((3000,), 32, dtype=torch.int32, device="cuda")
+    a = prune_all(ds, off, cnt, ids.reshape(-1), dists.reshape(-1), PruneParams(M=16))
+    assert a[0].is_cuda and int(a[3]) > 0
