@@ -442,8 +442,13 @@ struct KnnLayout {
   int *flag;
   int32_t *xnorm, *qnorm, *fb_list, *fb_count;
   uint64_t *keys;
+  void *tc_ws;
+  size_t tc_bytes;
   size_t total;
 };
+
+size_t tc_pool_workspace(int64_t n, int64_t nq, bool self);
+bool tc_pool_supported(int64_t d, int64_t k);
 
 int pool_S(int64_t k, int mode) {
   if (mode == PGK_POOL_U8) return (int)k;
@@ -451,8 +456,8 @@ int pool_S(int64_t k, int mode) {
   return (int)(k + m);
 }
 
-static KnnLayout knn_layout(void *ws, size_t bytes, int64_t n, int64_t nq, int64_t k,
-                            int mode) {
+static KnnLayout knn_layout(void *ws, size_t bytes, int64_t n, int64_t nq, int64_t d,
+                            int64_t k, int mode) {
   KnnLayout L{};
   Carve c(ws, bytes);
   const int S = pool_S(k, mode == PGK_POOL_AUTO ? PGK_POOL_F32 : mode);
@@ -462,13 +467,18 @@ static KnnLayout knn_layout(void *ws, size_t bytes, int64_t n, int64_t nq, int64
   L.qnorm = c.take<int32_t>(nq);
   L.fb_list = c.take<int32_t>(nq);
   L.keys = c.take<uint64_t>((size_t)nq * S);
+  L.tc_bytes = 0;
+  L.tc_ws = nullptr;
+  if (mode != PGK_POOL_F32 && tc_pool_supported(d, k)) {
+    L.tc_bytes = tc_pool_workspace(n, nq, false);
+    L.tc_ws = c.take<char>(L.tc_bytes);
+  }
   L.total = c.off;
   return L;
 }
 
 int knn_workspace(int64_t n, int64_t nq, int64_t d, int64_t k, int mode, size_t *bytes) {
-  (void)d;
-  *bytes = knn_layout(nullptr, 0, n, nq, k, mode).total;
+  *bytes = knn_layout(nullptr, 0, n, nq, d, k, mode).total;
   return PGK_OK;
 }
 
@@ -521,8 +531,9 @@ static int launch_tile(const float *X, int64_t n, int d, const float *Q, int64_t
 }
 
 int launch_pool_tc_u8(const float *X, int64_t n, int d, const float *Q, int64_t nq,
-                      int exclude_self, const int32_t *xnorm, const int32_t *qnorm,
-                      int K, uint64_t *keys, cudaStream_t stream, bool *handled);
+                      int exclude_self, const int32_t *xnorm, const int32_t *qnorm, int K,
+                      uint64_t *keys, void *tc_ws, size_t tc_bytes, cudaStream_t stream,
+                      bool *handled);
 
 int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, int64_t k,
               int exclude_self, int mode, int32_t *gt_ids, int32_t *pool_ids,
@@ -549,7 +560,7 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
     set_error("U8 pool mode needs d <= 258");
     return PGK_ERR_UNSUPPORTED;
   }
-  KnnLayout L = knn_layout(ws, bytes, n, nq, k, mode);
+  KnnLayout L = knn_layout(ws, bytes, n, nq, d, k, mode);
   if (L.total > bytes) {
     set_error("knn workspace too small: need %zu, got %zu", L.total, bytes);
     return PGK_ERR_NOMEM;
@@ -574,9 +585,11 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
       qn = L.qnorm;
     }
     bool handled = false;
-    rc = launch_pool_tc_u8(X, n, (int)d, Q, nq, exclude_self, L.xnorm, qn, (int)k, L.keys,
-                           stream, &handled);
-    if (rc) return rc;
+    if (L.tc_ws) {
+      rc = launch_pool_tc_u8(X, n, (int)d, Q, nq, exclude_self, L.xnorm, qn, (int)k, L.keys,
+                             L.tc_ws, L.tc_bytes, stream, &handled);
+      if (rc) return rc;
+    }
     if (!handled) {
       rc = S <= 224 ? launch_tile<MODE_U8, 256>(X, n, (int)d, Q, nq, exclude_self, L.xnorm,
                                                 qn, S, vec4, L.keys, stream)

@@ -1,16 +1,447 @@
-// pool_tc.cu -- tensor-core (tcgen05, kind::i8) exact k-NN pool for
-// integer-valued data.  (placeholder: returns handled=false until the kernel
-// lands; the SIMT U8 tile kernel is used meanwhile.)
+// pool_tc.cu -- exact k-NN pools on the 5th-gen tensor cores (tcgen05,
+// kind::i8) for integer-valued data in [0, 255] with d <= 128 (config 2).
+//
+// Why it is exact: with u8 operands and s32 accumulation every dot product is
+// an exact integer, so dist = |q|^2 + |x|^2 - 2 q.x is the exact squared
+// distance -- equal to the reference's float64 ranking value
+// (oracle.py:52-58) and to its fp32 sequential squared_l2 (_kernels.py:17-24;
+// all partial sums are integers < 2^24).  Top-K by packed (dist, id) key is
+// therefore the reference's (dist, id) order, no rerank needed.
+//
+// Kernel shape (persistent, 2 CTAs / SM, 256 threads):
+//   warp 0      TMA producer: the block's 128 query rows (A, once per block)
+//               and a ring of 128-point data tiles (B), 128 B/row, SW128
+//   warp 1      MMA issuer: D[128 x 128] (s32, TMEM) = A . B^T, 4 x K=32
+//               tcgen05.mma per tile, double-buffered accumulator
+//   warp 2      TMEM allocator (256 columns)
+//   warps 4..7  epilogue: warp q reads TMEM lanes 32q..32q+31, i.e. thread =
+//               query row; per 32 columns one IMAD + one compare per value
+//               against the row's running K-th best (fast reject), rare
+//               survivors appended to a per-row candidate buffer in global
+//               memory (L2); a full buffer is compacted by the whole warp
+//               (bitonic sort in shared memory, keep K, raise the threshold).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 
 namespace pgk {
+namespace tc {
+
+constexpr int BM = 128;   // query rows per block == TMEM lanes
+constexpr int BN = 128;   // data points per tile == MMA N
+constexpr int KB = 128;   // bytes per (padded) row
+constexpr int STAGES = 4;
+constexpr int TILE_BYTES = BN * KB;
+constexpr int CAP = 512;  // per-row candidate buffer (keys)
+constexpr int THREADS = 256;
+constexpr int TMEM_COLS = 256;
+
+struct __align__(1024) Smem {
+  uint8_t a[BM * KB];
+  uint8_t b[STAGES][TILE_BYTES];
+  uint64_t scratch[4][CAP];
+  uint64_t full[STAGES], empty[STAGES];
+  uint64_t tfull[2], tempty[2];
+  uint64_t a_full, a_empty;
+  uint32_t tmem_base;
+};
+
+// ---- PTX wrappers ----------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, uint64_t *bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// SW128 K-major smem matrix descriptor (8-row x 128-byte atoms, SBO = 1024 B)
+__device__ __forceinline__ uint64_t sw128_desc(const void *p) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO
+  d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// kind::i8 instruction descriptor: D s32, A/B u8, K-major, M=128, N=BN
+constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+// Warp-cooperative: sort row `src`'s buffer, keep the best K, return the new
+// count and threshold to every lane.  Optionally emit the best K to `out`.
+__device__ __forceinline__ void compact_row(uint64_t *buf, int cnt, int K, uint64_t *scratch,
+                                            int lane, uint64_t *out, int &new_cnt,
+                                            uint64_t &new_tau) {
+  __syncwarp();
+  for (int i = lane; i < CAP; i += 32) scratch[i] = i < cnt ? buf[i] : KEY_MAX;
+  __syncwarp();
+  warp_bitonic_sort(scratch, CAP, lane);
+  const int keep = cnt < K ? cnt : K;
+  for (int i = lane; i < keep; i += 32) buf[i] = scratch[i];
+  if (out)
+    for (int i = lane; i < K; i += 32) out[i] = scratch[i];
+  new_cnt = keep;
+  new_tau = cnt >= K ? scratch[K - 1] : KEY_MAX;
+  __syncwarp();
+}
+
+__device__ __forceinline__ int tau_prefilter(uint64_t tau, int nx) {
+  if (tau == KEY_MAX) return 0x7fffffff;
+  return (int)key_dist(tau) - nx;  // exact: distances are integers < 2^24
+}
+
+__global__ void __launch_bounds__(THREADS, 2)
+    tc_pool_u8_kernel(const __grid_constant__ CUtensorMap tmX,
+                      const __grid_constant__ CUtensorMap tmQ, int64_t n, int64_t nq,
+                      int exclude_self, const int32_t *__restrict__ xnorm,
+                      const int32_t *__restrict__ qnorm, int K, uint64_t *__restrict__ bufs,
+                      uint64_t *__restrict__ out_keys) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem &s = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                      ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nblocks = (int)((nq + BM - 1) / BM);
+  const int ntiles = (int)((n + BN - 1) / BN);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&s.full[i], 1);
+      mbar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s.tfull[i], 1);
+      mbar_init(&s.tempty[i], 4);
+    }
+    mbar_init(&s.a_full, 1);
+    mbar_init(&s.a_empty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&s.tmem_base)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmX) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmQ) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
+        mbar_wait(&s.a_empty, (it & 1) ^ 1);
+        mbar_expect_tx(&s.a_full, BM * KB);
+        tma_load_2d(s.a, &tmQ, &s.a_full, 0, b * BM);
+        for (int t = 0; t < ntiles; ++t) {
+          mbar_wait(&s.empty[stage], phase ^ 1);
+          mbar_expect_tx(&s.full[stage], TILE_BYTES);
+          tma_load_2d(s.b[stage], &tmX, &s.full[stage], 0, t * BN);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      int it = 0;
+      for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
+        mbar_wait(&s.a_full, it & 1);
+        tc_fence_after();
+        const uint64_t adesc = sw128_desc(s.a);
+        for (int t = 0; t < ntiles; ++t) {
+          mbar_wait(&s.tempty[acc], acc_phase ^ 1);
+          mbar_wait(&s.full[stage], phase);
+          tc_fence_after();
+          const uint64_t bdesc = sw128_desc(s.b[stage]);
+#pragma unroll
+          for (int kk = 0; kk < KB / 32; ++kk)  // K = 32 bytes per MMA; +32 B = +2 (16 B units)
+            mma_i8(tmem + acc * BN, adesc + 2 * kk, bdesc + 2 * kk, IDESC, kk > 0);
+          tc_commit(&s.empty[stage]);
+          tc_commit(&s.tfull[acc]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+        tc_commit(&s.a_empty);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const int q = warp - 4;  // TMEM lane quarter (warp % 4)
+    uint64_t *scratch = s.scratch[q];
+    uint64_t *wbuf = bufs + ((size_t)blockIdx.x * BM + q * 32) * CAP;  // this warp's rows
+    uint64_t *mybuf = wbuf + (size_t)lane * CAP;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int b = blockIdx.x; b < nblocks; b += gridDim.x) {
+      const int64_t row = (int64_t)b * BM + q * 32 + lane;
+      const bool row_ok = row < nq;
+      const int nx = row_ok ? qnorm[row] : 0;
+      int cnt = 0;
+      uint64_t tau = KEY_MAX;
+      int tp = row_ok ? 0x7fffffff : -0x7fffffff;  // invalid rows never pass
+      for (int t = 0; t < ntiles; ++t) {
+        mbar_wait(&s.tfull[acc], acc_phase);
+        tc_fence_after();
+        const int64_t col0 = (int64_t)t * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+          tmem_wait_ld();
+          if (c == BN / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.tempty[acc]);
+          }
+          const int64_t cb = col0 + c * 32;
+          int ny[32];
+          if (cb + 32 <= n) {
+            const int4 *p = reinterpret_cast<const int4 *>(xnorm + cb);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              int4 w = __ldg(p + v);
+              ny[4 * v] = w.x; ny[4 * v + 1] = w.y; ny[4 * v + 2] = w.z; ny[4 * v + 3] = w.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) ny[j] = cb + j < n ? __ldg(xnorm + cb + j) : 0x3fffffff;
+          }
+          bool any = false;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            int sj = ny[j] - 2 * (int)r[j];
+            any |= sj <= tp;
+          }
+          if (__any_sync(0xffffffffu, any)) {
+            // room for up to 32 appends in every row of the warp
+            unsigned need = __ballot_sync(0xffffffffu, cnt > CAP - 32);
+            while (need) {
+              const int src = __ffs(need) - 1;
+              need &= need - 1;
+              const int c_src = __shfl_sync(0xffffffffu, cnt, src);
+              int nc;
+              uint64_t nt;
+              compact_row(wbuf + (size_t)src * CAP, c_src, K, scratch, lane, nullptr, nc, nt);
+              if (lane == src) {
+                cnt = nc;
+                tau = nt;
+                tp = tau_prefilter(tau, nx);
+              }
+            }
+            if (any) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int sj = ny[j] - 2 * (int)r[j];
+                if (sj <= tp) {
+                  const int64_t col = cb + j;
+                  if (col < n && !(exclude_self && col == row)) {
+                    const uint64_t key = pack_key((float)(sj + nx), (int32_t)col);
+                    if (key < tau) mybuf[cnt++] = key;
+                  }
+                }
+              }
+            }
+            __syncwarp();
+          }
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+      // block done: emit every row's best K (sorted), reset for the next block
+      for (int src = 0; src < 32; ++src) {
+        const int64_t r_src = (int64_t)b * BM + q * 32 + src;
+        if (r_src >= nq) break;
+        const int c_src = __shfl_sync(0xffffffffu, cnt, src);
+        int nc;
+        uint64_t nt;
+        compact_row(wbuf + (size_t)src * CAP, c_src, K, scratch, lane, out_keys + r_src * K,
+                    nc, nt);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(TMEM_COLS));
+  }
+}
+
+// float (integer-valued, d <= 128) -> u8 rows padded to 128 bytes
+__global__ void to_u8_kernel(const float *__restrict__ X, int64_t n, int d,
+                             uint8_t *__restrict__ out) {
+  const int64_t total = n * KB;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / KB;
+    int c = (int)(e - r * KB);
+    out[e] = c < d ? (uint8_t)__float2int_rn(X[r * d + c]) : (uint8_t)0;
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static bool make_map(CUtensorMap *tm, const uint8_t *base, int64_t rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)KB, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)KB};
+  cuuint32_t box[2] = {(cuuint32_t)KB, (cuuint32_t)BN};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void *)base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace tc
+
+size_t tc_pool_workspace(int64_t n, int64_t nq, bool self) {
+  const int sms = num_sms();
+  size_t b = (size_t)n * tc::KB + 1024;
+  if (!self) b += (size_t)nq * tc::KB + 1024;
+  b += (size_t)2 * sms * tc::BM * tc::CAP * sizeof(uint64_t) + 1024;
+  return b;
+}
+
+bool tc_pool_supported(int64_t d, int64_t k) {
+  static int env = -1;
+  if (env < 0) {
+    const char *e = getenv("PGK_DISABLE_TC");
+    env = (e && e[0] == '1') ? 1 : 0;
+  }
+  return !env && d <= tc::KB && k >= 1 && k <= 256;
+}
 
 int launch_pool_tc_u8(const float *X, int64_t n, int d, const float *Q, int64_t nq,
                       int exclude_self, const int32_t *xnorm, const int32_t *qnorm, int K,
-                      uint64_t *keys, cudaStream_t stream, bool *handled) {
-  (void)X; (void)n; (void)d; (void)Q; (void)nq; (void)exclude_self; (void)xnorm;
-  (void)qnorm; (void)K; (void)keys; (void)stream;
+                      uint64_t *keys, void *tc_ws, size_t tc_bytes, cudaStream_t stream,
+                      bool *handled) {
   *handled = false;
+  if (!tc_pool_supported(d, K)) return PGK_OK;
+  const bool self = (Q == X);
+  if (tc_bytes < tc_pool_workspace(n, nq, self)) {
+    set_error("tc pool workspace too small");
+    return PGK_ERR_NOMEM;
+  }
+  Carve c(tc_ws, tc_bytes);
+  uint8_t *xu8 = c.take<uint8_t>((size_t)n * tc::KB);
+  uint8_t *qu8 = self ? xu8 : c.take<uint8_t>((size_t)nq * tc::KB);
+  const int sms = num_sms();
+  uint64_t *bufs = c.take<uint64_t>((size_t)2 * sms * tc::BM * tc::CAP);
+  const unsigned cg = (unsigned)std::min<int64_t>((n * tc::KB + 255) / 256, (int64_t)sms * 16);
+  tc::to_u8_kernel<<<cg, 256, 0, stream>>>(X, n, d, xu8);
+  PGK_CHECK_LAUNCH("to_u8_kernel");
+  if (!self) {
+    tc::to_u8_kernel<<<cg, 256, 0, stream>>>(Q, nq, d, qu8);
+    PGK_CHECK_LAUNCH("to_u8_kernel");
+  }
+  CUtensorMap tmX, tmQ;
+  if (!tc::make_map(&tmX, xu8, n) || !tc::make_map(&tmQ, qu8, nq)) {
+    set_error("cuTensorMapEncodeTiled failed");
+    return PGK_ERR_CUDA;
+  }
+  const size_t smem = sizeof(tc::Smem) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    PGK_CUDA(cudaFuncSetAttribute(tc::tc_pool_u8_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int nblocks = (int)((nq + tc::BM - 1) / tc::BM);
+  const unsigned grid = (unsigned)std::min<int64_t>(nblocks, (int64_t)2 * sms);
+  tc::tc_pool_u8_kernel<<<grid, tc::THREADS, smem, stream>>>(tmX, tmQ, n, nq, exclude_self,
+                                                             xnorm, qnorm, K, bufs, keys);
+  PGK_CHECK_LAUNCH("tc_pool_u8_kernel");
+  *handled = true;
   return PGK_OK;
 }
 

@@ -1,0 +1,67 @@
+"""GPU: the tcgen05 (kind::i8) exact pool kernel against the SIMT kernel and
+the oracle (integer-valued data in [0,255], d <= 128)."""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_2410_01231_b200 import Dataset, knn_pools, synth, kernels
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.mark.parametrize("n,K", [(200, 10), (1000, 64), (5000, 128), (20000, 128), (3001, 256)])
+def test_tc_pool_matches_oracle(n, K):
+    data = synth.cfg2(n)
+    ds = Dataset.from_array(data)
+    assert ds.is_u8()
+    ids, dists, gt = knn_pools(ds, K, want_gt=True)
+    rows = np.unique(np.concatenate([np.arange(min(n, 64)), np.arange(n - 64, n),
+                                     np.random.default_rng(n).choice(n, 200)]))
+    o_ids, o_d = oracle.knn_pools(data, K, rows)
+    np.testing.assert_array_equal(ids[rows], o_ids)
+    np.testing.assert_array_equal(dists[rows], o_d)
+    np.testing.assert_array_equal(gt[rows], o_ids)  # exact integers: both orders coincide
+
+
+def test_tc_pool_small_d_and_ties():
+    """d = 3 integer lattice with massive exact ties (id tie-break)."""
+    g = np.stack(np.meshgrid(np.arange(20), np.arange(20), np.arange(3)), -1)
+    data = g.reshape(-1, 3).astype(np.float32)
+    ds = Dataset.from_array(data)
+    ids, dists = knn_pools(ds, 30)
+    o_ids, o_d = oracle.knn_pools(data, 30)
+    np.testing.assert_array_equal(ids, o_ids)
+    np.testing.assert_array_equal(dists, o_d)
+
+
+def test_tc_matches_simt_path():
+    """Same pools from the SIMT U8 kernel (PGK_DISABLE_TC=1, fresh process)."""
+    n, K = 12000, 128
+    data = synth.cfg2(n)
+    ids, dists = knn_pools(Dataset.from_array(data), K)
+    code = ("import sys, numpy as np; sys.path.insert(0, %r);"
+            "from paper_2410_01231_b200 import Dataset, knn_pools, synth;"
+            "i, d = knn_pools(Dataset.from_array(synth.cfg2(%d)), %d);"
+            "np.save('/tmp/pgk_simt_ids.npy', i); np.save('/tmp/pgk_simt_d.npy', d)"
+            % (str(ROOT), n, K))
+    env = dict(os.environ, PGK_DISABLE_TC="1")
+    subprocess.check_call([sys.executable, "-c", code], env=env, timeout=600)
+    np.testing.assert_array_equal(ids, np.load("/tmp/pgk_simt_ids.npy"))
+    np.testing.assert_array_equal(dists, np.load("/tmp/pgk_simt_d.npy"))
+
+
+def test_tc_queries_table():
+    data = synth.cfg2(4000)
+    q = synth.cfg2(4100)[4000:]
+    from paper_2410_01231_b200 import ground_truth_table
+    table = ground_truth_table(Dataset.from_array(data), q, k=16)
+    for i in range(0, 100, 7):
+        d64 = ((data.astype(np.float64) - q[i].astype(np.float64)) ** 2).sum(1)
+        assert table[i].tolist() == np.lexsort((np.arange(4000), d64))[:16].tolist()
