@@ -463,7 +463,7 @@ static KnnLayout knn_layout(void *ws, size_t bytes, int64_t n, int64_t nq, int64
   const int S = pool_S(k, mode == PGK_POOL_AUTO ? PGK_POOL_F32 : mode);
   L.flag = c.take<int>(4);
   L.fb_count = c.take<int32_t>(4);
-  L.xnorm = c.take<int32_t>(n);
+  L.xnorm = c.take<int32_t>(n + 128);  // + padding to a whole tile (pool_tc.cu)
   L.qnorm = c.take<int32_t>(nq);
   L.fb_list = c.take<int32_t>(nq);
   L.keys = c.take<uint64_t>((size_t)nq * S);

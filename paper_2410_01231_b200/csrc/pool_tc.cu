@@ -40,7 +40,8 @@ constexpr int TMEM_COLS = 256;
 struct __align__(1024) Smem {
   uint8_t a[BM * KB];
   uint8_t b[STAGES][TILE_BYTES];
-  uint64_t scratch[4][CAP];
+  int32_t sv[4][32 * 36];  // per epilogue warp: one chunk of s values per lane
+  alignas(16) int32_t ny[2][BN];  // |x|^2 of the tile in each accumulator stage
   uint64_t full[STAGES], empty[STAGES];
   uint64_t tfull[2], tempty[2];
   uint64_t a_full, a_empty;
@@ -58,6 +59,19 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes,
+                                          uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -135,35 +149,164 @@ __device__ __forceinline__ void tmem_wait_ld() {
 // kind::i8 instruction descriptor: D s32, A/B u8, K-major, M=128, N=BN
 constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
-// Warp-cooperative: sort row `src`'s buffer, keep the best K, return the new
-// count and threshold to every lane.  Optionally emit the best K to `out`.
-__device__ __forceinline__ void compact_row(uint64_t *buf, int cnt, int K, uint64_t *scratch,
-                                            int lane, uint64_t *out, int &new_cnt,
-                                            uint64_t &new_tau) {
+// Internal keys of this kernel: ((uint64)dist << 32) | id with dist the exact
+// integer distance (< 2^25), so key order == (dist, id) order.
+__device__ __forceinline__ uint32_t khi(uint64_t k) { return (uint32_t)(k >> 32); }
+
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Warp-cooperative selection on one row's candidate buffer (cnt > K keys in
+// global memory): keep exactly the K smallest keys (unordered) at buf[0..K)
+// and return the K-th smallest key.  Two binary searches over the register-
+// resident keys (distance bits, then id bits among distance ties); no sort.
+constexpr int KPL = CAP / 32;  // keys per lane
+__device__ __noinline__ uint64_t select_k(uint64_t *buf, int cnt, int K, uint32_t hi_bound,
+                                          int lane) {
+  uint64_t kk[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int idx = i * 32 + lane;
+    kk[i] = idx < cnt ? buf[idx] : KEY_MAX;
+  }
+  // smallest td with #{dist <= td} >= K
+  uint32_t lo = 0, hi = hi_bound;
+  while (lo < hi) {
+    const uint32_t mid = lo + ((hi - lo) >> 1);
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) c += khi(kk[i]) <= mid;
+    if (warp_sum(c) >= K) hi = mid;
+    else lo = mid + 1;
+  }
+  const uint32_t td = lo;
+  int c_lt = 0, c_eq = 0;
+  uint32_t id_max = 0;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    c_lt += khi(kk[i]) < td;
+    if (khi(kk[i]) == td) {
+      ++c_eq;
+      id_max = max(id_max, (uint32_t)kk[i]);
+    }
+  }
+  c_lt = warp_sum(c_lt);
+  c_eq = warp_sum(c_eq);
+  const int need = K - c_lt;
+  uint32_t tid;
+  if (c_eq == need) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) id_max = max(id_max, __shfl_xor_sync(0xffffffffu, id_max, o));
+    tid = id_max;
+  } else {  // distance ties straddle the boundary: smallest ids win
+    uint32_t a = 0, b = 0x7fffffffu;
+    while (a < b) {
+      const uint32_t mid = a + ((b - a) >> 1);
+      int c = 0;
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) c += khi(kk[i]) == td && (uint32_t)kk[i] <= mid;
+      if (warp_sum(c) >= need) b = mid;
+      else a = mid + 1;
+    }
+    tid = a;
+  }
+  const uint64_t tau = ((uint64_t)td << 32) | tid;
   __syncwarp();
-  for (int i = lane; i < CAP; i += 32) scratch[i] = i < cnt ? buf[i] : KEY_MAX;
+  int p = 0;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const bool keep = kk[i] <= tau;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) buf[p + __popc(bal & lanemask_lt())] = kk[i];
+    p += __popc(bal);
+  }
   __syncwarp();
-  warp_bitonic_sort(scratch, CAP, lane);
-  const int keep = cnt < K ? cnt : K;
-  for (int i = lane; i < keep; i += 32) buf[i] = scratch[i];
-  if (out)
-    for (int i = lane; i < K; i += 32) out[i] = scratch[i];
-  new_cnt = keep;
-  new_tau = cnt >= K ? scratch[K - 1] : KEY_MAX;
-  __syncwarp();
+  return tau;
+}
+
+// Register bitonic sort of 32*NPL keys (element i = slot*32 + lane).
+template <int NPL>
+__device__ __forceinline__ void reg_bitonic(uint64_t (&e)[NPL], int lane) {
+  constexpr int SIZE = 32 * NPL;
+#pragma unroll
+  for (int k = 2; k <= SIZE; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int js = j >> 5;
+#pragma unroll
+        for (int s0 = 0; s0 < NPL; ++s0) {
+          if (s0 & js) continue;
+          const int s1 = s0 ^ js;
+          const bool up = (((s0 << 5) | lane) & k) == 0;
+          const uint64_t a = e[s0], b = e[s1];
+          const bool sw = (a > b) == up;
+          e[s0] = sw ? b : a;
+          e[s1] = sw ? a : b;
+        }
+      } else {
+        const bool lower = (lane & j) == 0;
+#pragma unroll
+        for (int s0 = 0; s0 < NPL; ++s0) {
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, e[s0], j);
+          const bool up = (((s0 << 5) | lane) & k) == 0;
+          const uint64_t mn = e[s0] < o ? e[s0] : o, mx = e[s0] < o ? o : e[s0];
+          e[s0] = (lower == up) ? mn : mx;
+        }
+      }
+    }
+  }
+}
+
+// Final per-row output: best K keys, ascending, in the library's packed
+// (float dist, id) key format.
+template <int NPL>
+__device__ __forceinline__ void emit_sorted(const uint64_t *buf, int cnt, int K,
+                                            uint64_t *out, int lane) {
+  uint64_t e[NPL];
+#pragma unroll
+  for (int s0 = 0; s0 < NPL; ++s0) {
+    const int idx = s0 * 32 + lane;
+    e[s0] = idx < cnt && idx < K ? buf[idx] : KEY_MAX;
+  }
+  reg_bitonic<NPL>(e, lane);
+#pragma unroll
+  for (int s0 = 0; s0 < NPL; ++s0) {
+    const int idx = s0 * 32 + lane;
+    if (idx < K)
+      out[idx] = e[s0] == KEY_MAX ? KEY_MAX : pack_key((float)khi(e[s0]), (int32_t)(uint32_t)e[s0]);
+  }
 }
 
 __device__ __forceinline__ int tau_prefilter(uint64_t tau, int nx) {
   if (tau == KEY_MAX) return 0x7fffffff;
-  return (int)key_dist(tau) - nx;  // exact: distances are integers < 2^24
+  return (int)khi(tau) - nx;
 }
 
+// Optional epilogue instrumentation (PGK_TC_STATS=1): cycles / event counts.
+enum { ST_WAIT, ST_MAIN, ST_SLOW, ST_COMPACT, ST_FINAL, ST_NSLOW, ST_NCOMPACT, ST_NAPPEND,
+       ST_COUNT };
+
+template <bool STATS>
 __global__ void __launch_bounds__(THREADS, 2)
     tc_pool_u8_kernel(const __grid_constant__ CUtensorMap tmX,
                       const __grid_constant__ CUtensorMap tmQ, int64_t n, int64_t nq,
                       int exclude_self, const int32_t *__restrict__ xnorm,
                       const int32_t *__restrict__ qnorm, int K, uint64_t *__restrict__ bufs,
-                      uint64_t *__restrict__ out_keys) {
+                      uint64_t *__restrict__ out_keys, unsigned long long *stats) {
+  unsigned long long st[ST_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_prev = STATS ? clock64() : 0;
+#define PGK_TICK(slot)                          \
+  do {                                          \
+    if (STATS) {                                \
+      long long t_ = clock64();                 \
+      st[slot] += (unsigned long long)(t_ - t_prev); \
+      t_prev = t_;                              \
+    }                                           \
+  } while (0)
   extern __shared__ uint8_t smem_raw[];
   Smem &s = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                       ~uintptr_t(1023));
@@ -227,6 +370,10 @@ __global__ void __launch_bounds__(THREADS, 2)
         const uint64_t adesc = sw128_desc(s.a);
         for (int t = 0; t < ntiles; ++t) {
           mbar_wait(&s.tempty[acc], acc_phase ^ 1);
+          // the tile's |x|^2 (xnorm is padded to a multiple of BN) lands with the
+          // accumulator: tfull completes on the commit AND these bytes
+          mbar_expect_tx_only(&s.tfull[acc], BN * 4);
+          bulk_load(s.ny[acc], xnorm + (int64_t)t * BN, BN * 4, &s.tfull[acc]);
           mbar_wait(&s.full[stage], phase);
           tc_fence_after();
           const uint64_t bdesc = sw128_desc(s.b[stage]);
@@ -244,7 +391,7 @@ __global__ void __launch_bounds__(THREADS, 2)
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
     const int q = warp - 4;  // TMEM lane quarter (warp % 4)
-    uint64_t *scratch = s.scratch[q];
+    int32_t *sv = s.sv[q] + lane * 36;
     uint64_t *wbuf = bufs + ((size_t)blockIdx.x * BM + q * 32) * CAP;  // this warp's rows
     uint64_t *mybuf = wbuf + (size_t)lane * CAP;
     int acc = 0;
@@ -257,84 +404,120 @@ __global__ void __launch_bounds__(THREADS, 2)
       uint64_t tau = KEY_MAX;
       int tp = row_ok ? 0x7fffffff : -0x7fffffff;  // invalid rows never pass
       for (int t = 0; t < ntiles; ++t) {
+        PGK_TICK(ST_MAIN);
         mbar_wait(&s.tfull[acc], acc_phase);
         tc_fence_after();
+        PGK_TICK(ST_WAIT);
         const int64_t col0 = (int64_t)t * BN;
-#pragma unroll 1
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+        uint32_t rbuf[2][32];
+        tmem_ld32(tbase, rbuf[0]);
+#pragma unroll
         for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+          uint32_t(&r)[32] = rbuf[c & 1];
           tmem_wait_ld();
-          if (c == BN / 32 - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s.tempty[acc]);
-          }
+          if (c + 1 < BN / 32)
+            tmem_ld32(tbase + (c + 1) * 32, rbuf[(c + 1) & 1]);  // overlaps this chunk
           const int64_t cb = col0 + c * 32;
-          int ny[32];
-          if (cb + 32 <= n) {
-            const int4 *p = reinterpret_cast<const int4 *>(xnorm + cb);
+          const int4 *nyp = reinterpret_cast<const int4 *>(s.ny[acc] + c * 32);
+          // s_j = |x_j|^2 - 2 q.x_j ; pass iff s_j <= tau_dist - |q|^2
+          uint32_t mask = 0;
 #pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              int4 w = __ldg(p + v);
-              ny[4 * v] = w.x; ny[4 * v + 1] = w.y; ny[4 * v + 2] = w.z; ny[4 * v + 3] = w.w;
+          for (int v = 0; v < 8; ++v) {
+            const int4 w = nyp[v];
+            mask |= ((w.x - 2 * (int)r[4 * v]) <= tp) ? (1u << (4 * v)) : 0u;
+            mask |= ((w.y - 2 * (int)r[4 * v + 1]) <= tp) ? (1u << (4 * v + 1)) : 0u;
+            mask |= ((w.z - 2 * (int)r[4 * v + 2]) <= tp) ? (1u << (4 * v + 2)) : 0u;
+            mask |= ((w.w - 2 * (int)r[4 * v + 3]) <= tp) ? (1u << (4 * v + 3)) : 0u;
+          }
+          if (__any_sync(0xffffffffu, mask != 0)) {
+            PGK_TICK(ST_MAIN);
+            if (STATS) st[ST_NSLOW]++;
+            if (mask) {
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                const int4 w = nyp[v];
+                int4 o;
+                o.x = w.x - 2 * (int)r[4 * v];
+                o.y = w.y - 2 * (int)r[4 * v + 1];
+                o.z = w.z - 2 * (int)r[4 * v + 2];
+                o.w = w.w - 2 * (int)r[4 * v + 3];
+                reinterpret_cast<int4 *>(sv)[v] = o;
+              }
             }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) ny[j] = cb + j < n ? __ldg(xnorm + cb + j) : 0x3fffffff;
-          }
-          bool any = false;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            int sj = ny[j] - 2 * (int)r[j];
-            any |= sj <= tp;
-          }
-          if (__any_sync(0xffffffffu, any)) {
-            // room for up to 32 appends in every row of the warp
-            unsigned need = __ballot_sync(0xffffffffu, cnt > CAP - 32);
+            // room for this chunk's survivors in every row of the warp
+            unsigned need = __ballot_sync(0xffffffffu, cnt + __popc(mask) > CAP);
+            if (STATS) st[ST_NCOMPACT] += __popc(need);
             while (need) {
               const int src = __ffs(need) - 1;
               need &= need - 1;
               const int c_src = __shfl_sync(0xffffffffu, cnt, src);
-              int nc;
-              uint64_t nt;
-              compact_row(wbuf + (size_t)src * CAP, c_src, K, scratch, lane, nullptr, nc, nt);
+              const uint64_t t_src = __shfl_sync(0xffffffffu, tau, src);
+              const uint64_t nt = select_k(wbuf + (size_t)src * CAP, c_src, K,
+                                           t_src == KEY_MAX ? (1u << 25) : khi(t_src), lane);
               if (lane == src) {
-                cnt = nc;
+                cnt = K;
                 tau = nt;
                 tp = tau_prefilter(tau, nx);
               }
             }
-            if (any) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const int sj = ny[j] - 2 * (int)r[j];
-                if (sj <= tp) {
-                  const int64_t col = cb + j;
-                  if (col < n && !(exclude_self && col == row)) {
-                    const uint64_t key = pack_key((float)(sj + nx), (int32_t)col);
-                    if (key < tau) mybuf[cnt++] = key;
-                  }
-                }
+            PGK_TICK(ST_COMPACT);
+            const int cnt_before = cnt;
+            while (mask) {  // only lanes with survivors iterate
+              const int j = __ffs(mask) - 1;
+              mask &= mask - 1;
+              const int sj = sv[j];
+              const int64_t col = cb + j;
+              if (sj <= tp && col < n && !(exclude_self && col == row)) {
+                const uint64_t key = ((uint64_t)(uint32_t)(sj + nx) << 32) | (uint32_t)col;
+                if (key < tau) mybuf[cnt++] = key;
               }
             }
+            if (STATS) st[ST_NAPPEND] += cnt - cnt_before;
             __syncwarp();
+            PGK_TICK(ST_SLOW);
           }
         }
+        // accumulator and its norms fully consumed: hand the stage back
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s.tempty[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
       // block done: emit every row's best K (sorted), reset for the next block
+      PGK_TICK(ST_MAIN);
+      __syncwarp();
       for (int src = 0; src < 32; ++src) {
         const int64_t r_src = (int64_t)b * BM + q * 32 + src;
         if (r_src >= nq) break;
-        const int c_src = __shfl_sync(0xffffffffu, cnt, src);
-        int nc;
-        uint64_t nt;
-        compact_row(wbuf + (size_t)src * CAP, c_src, K, scratch, lane, out_keys + r_src * K,
-                    nc, nt);
+        int c_src = __shfl_sync(0xffffffffu, cnt, src);
+        const uint64_t t_src = __shfl_sync(0xffffffffu, tau, src);
+        uint64_t *bsrc = wbuf + (size_t)src * CAP;
+        if (c_src > K) {
+          select_k(bsrc, c_src, K, t_src == KEY_MAX ? (1u << 25) : khi(t_src), lane);
+          c_src = K;
+        }
+        uint64_t *o = out_keys + r_src * K;
+        if (K <= 32) emit_sorted<1>(bsrc, c_src, K, o, lane);
+        else if (K <= 64) emit_sorted<2>(bsrc, c_src, K, o, lane);
+        else if (K <= 128) emit_sorted<4>(bsrc, c_src, K, o, lane);
+        else emit_sorted<8>(bsrc, c_src, K, o, lane);
+        __syncwarp();
+      }
+      PGK_TICK(ST_FINAL);
+    }
+    if (STATS) {
+      for (int i = 0; i < ST_COUNT; ++i) {
+        unsigned long long v = st[i];
+        if (i == ST_NAPPEND) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        }
+        if (lane == 0) atomicAdd(stats + i, v);
       }
     }
   }
+#undef PGK_TICK
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -393,6 +576,7 @@ size_t tc_pool_workspace(int64_t n, int64_t nq, bool self) {
 }
 
 bool tc_pool_supported(int64_t d, int64_t k) {
+  static_assert(tc::CAP >= 256 + 32, "CAP must leave room for K <= 256 plus one chunk");
   static int env = -1;
   if (env < 0) {
     const char *e = getenv("PGK_DISABLE_TC");
@@ -424,6 +608,11 @@ int launch_pool_tc_u8(const float *X, int64_t n, int d, const float *Q, int64_t 
     tc::to_u8_kernel<<<cg, 256, 0, stream>>>(Q, nq, d, qu8);
     PGK_CHECK_LAUNCH("to_u8_kernel");
   }
+  // pad |x|^2 to a multiple of BN with a huge value (0x3f3f3f3f > any distance):
+  // the kernel bulk-copies whole 128-entry tiles of it
+  const int64_t n_pad = (n + tc::BN - 1) / tc::BN * tc::BN;
+  if (n_pad > n)
+    PGK_CUDA(cudaMemsetAsync(const_cast<int32_t *>(xnorm) + n, 0x3f, (n_pad - n) * 4, stream));
   CUtensorMap tmX, tmQ;
   if (!tc::make_map(&tmX, xu8, n) || !tc::make_map(&tmQ, qu8, nq)) {
     set_error("cuTensorMapEncodeTiled failed");
@@ -432,15 +621,37 @@ int launch_pool_tc_u8(const float *X, int64_t n, int d, const float *Q, int64_t 
   const size_t smem = sizeof(tc::Smem) + 1024;
   static bool attr = false;
   if (!attr) {
-    PGK_CUDA(cudaFuncSetAttribute(tc::tc_pool_u8_kernel,
+    PGK_CUDA(cudaFuncSetAttribute(tc::tc_pool_u8_kernel<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PGK_CUDA(cudaFuncSetAttribute(tc::tc_pool_u8_kernel<true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   const int nblocks = (int)((nq + tc::BM - 1) / tc::BM);
   const unsigned grid = (unsigned)std::min<int64_t>(nblocks, (int64_t)2 * sms);
-  tc::tc_pool_u8_kernel<<<grid, tc::THREADS, smem, stream>>>(tmX, tmQ, n, nq, exclude_self,
-                                                             xnorm, qnorm, K, bufs, keys);
-  PGK_CHECK_LAUNCH("tc_pool_u8_kernel");
+  const char *se = getenv("PGK_TC_STATS");
+  if (se && se[0] == '1') {
+    unsigned long long *dstats = nullptr;
+    PGK_CUDA(cudaMalloc(&dstats, sizeof(unsigned long long) * tc::ST_COUNT));
+    PGK_CUDA(cudaMemsetAsync(dstats, 0, sizeof(unsigned long long) * tc::ST_COUNT, stream));
+    tc::tc_pool_u8_kernel<true><<<grid, tc::THREADS, smem, stream>>>(
+        tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, dstats);
+    PGK_CHECK_LAUNCH("tc_pool_u8_kernel<stats>");
+    unsigned long long h[tc::ST_COUNT];
+    PGK_CUDA(cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    PGK_CUDA(cudaStreamSynchronize(stream));
+    cudaFree(dstats);
+    const double warps = 4.0 * grid;
+    fprintf(stderr,
+            "[tc stats] per epilogue warp: wait %.3g main %.3g slow %.3g compact %.3g final %.3g "
+            "cycles; slow-chunks %.3g compactions %.3g; appends/row-block %.1f\n",
+            h[0] / warps, h[1] / warps, h[2] / warps, h[3] / warps, h[4] / warps, h[5] / warps,
+            h[6] / warps, (double)h[7] / (double)nq);
+  } else {
+    tc::tc_pool_u8_kernel<false><<<grid, tc::THREADS, smem, stream>>>(
+        tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr);
+    PGK_CHECK_LAUNCH("tc_pool_u8_kernel");
+  }
   *handled = true;
   return PGK_OK;
 }

@@ -22,6 +22,8 @@ namespace pgk {
 
 constexpr int PRUNE_WARPS = 8;
 constexpr int PRUNE_W = 256;  // window entries per warp
+constexpr int DC = 64;        // dimensions per staged chunk
+constexpr int SROW = DC + 4;  // staged row stride (floats): == 4 mod 32 -> LDS.128 conflict-free
 
 struct PruneSmem {
   int32_t id[PRUNE_WARPS][PRUNE_W];
@@ -29,29 +31,65 @@ struct PruneSmem {
   int32_t de[PRUNE_WARPS][PRUNE_W];
   int32_t ae[PRUNE_WARPS][PRUNE_W];
   int16_t alive[PRUNE_WARPS][PRUNE_W];
+  alignas(16) float stage[PRUNE_WARPS][32 * SROW];  // 32 candidate rows, one chunk
 };
 
 // Test alive entries alive[a0 .. n_alive) against kept neighbour w; returns
 // the new alive count (survivors compacted to alive[0..), order kept).
+//
+// One lane per candidate; each lane accumulates its full squared distance in
+// the reference's sequential fp32 order.  VEC4 (d % 4 == 0, aligned rows):
+// the batch's 32 candidate rows are staged through shared memory 64 dims at a
+// time with coalesced float4 loads (two rows per warp instruction) and read
+// back conflict-free, instead of 32 scattered per-lane row walks.
 template <bool VEC4>
 __device__ __forceinline__ int test_round(
     const float *__restrict__ X, int d, int32_t w, float duw, int strategy,
     double cos_alpha, int a0, int n_alive, int32_t *s_id, float *s_dist,
-    int32_t *s_de, int32_t *s_ae, int16_t *s_alive, int lane) {
+    int32_t *s_de, int32_t *s_ae, int16_t *s_alive, float *stage, int lane) {
   if (duw == 0.0f) return 0;  // _kernels.py:387-389: dominated, no evaluation
   const float *xw = X + (int64_t)w * d;
   int new_n = 0;
   for (int base = a0; base < n_alive; base += 32) {
-    int a = base + lane;
-    bool act = a < n_alive;
+    const int a = base + lane;
+    const bool act = a < n_alive;
+    const int nb = min(32, n_alive - base);
+    const int j = act ? s_alive[a] : s_alive[base];
+    const int32_t v = s_id[j];
+    float dwv = 0.0f;  // _kernels.py:390: squared_l2(data[w], data[v])
+    if (VEC4) {
+      const int half = lane >> 4, l16 = lane & 15;
+      for (int c0 = 0; c0 < d; c0 += DC) {
+        const int dc = min(DC, d - c0);
+        __syncwarp();
+        for (int e0 = 0; e0 < nb; e0 += 2) {
+          const int e = e0 + half;
+          const int32_t ve = __shfl_sync(0xffffffffu, v, e & 31);
+          if (e < nb && 4 * l16 < dc)
+            *reinterpret_cast<float4 *>(stage + e * SROW + 4 * l16) =
+                __ldg(reinterpret_cast<const float4 *>(X + (int64_t)ve * d + c0) + l16);
+        }
+        __syncwarp();
+        if (act) {
+          const float *srow = stage + lane * SROW;
+          const float4 *w4 = reinterpret_cast<const float4 *>(xw + c0);
+#pragma unroll 4
+          for (int k = 0; k < dc; k += 4) {
+            const float4 x = __ldg(w4 + (k >> 2));
+            const float4 y = *reinterpret_cast<const float4 *>(srow + k);
+            dwv = sq_step(dwv, x.x, y.x);
+            dwv = sq_step(dwv, x.y, y.y);
+            dwv = sq_step(dwv, x.z, y.z);
+            dwv = sq_step(dwv, x.w, y.w);
+          }
+        }
+      }
+    } else if (act) {
+      dwv = sql2_seq<false>(xw, X + (int64_t)v * d, d);
+    }
     bool survive = false;
-    int j = 0;
     if (act) {
-      j = s_alive[a];
-      int32_t v = s_id[j];
-      float dv = s_dist[j];
-      // _kernels.py:390: dwv = squared_l2(data[w], data[v])
-      float dwv = sql2_seq<VEC4>(xw, X + (int64_t)v * d, d);
+      const float dv = s_dist[j];
       s_de[j] += 1;
       bool dom;
       if (dwv == 0.0f) {
@@ -97,6 +135,7 @@ __global__ void __launch_bounds__(PRUNE_WARPS * 32)
   int32_t *s_de = sm.de[warp];
   int32_t *s_ae = sm.ae[warp];
   int16_t *s_alive = sm.alive[warp];
+  float *stage = sm.stage[warp];
 
   for (int64_t u = (int64_t)blockIdx.x * PRUNE_WARPS + warp; u < n;
        u += (int64_t)gridDim.x * PRUNE_WARPS) {
@@ -134,7 +173,7 @@ __global__ void __launch_bounds__(PRUNE_WARPS * 32)
         int32_t w = orow[kj];
         float duw = odrow[kj];
         n_alive = test_round<VEC4>(X, d, w, duw, strategy, cos_alpha, 0, n_alive,
-                                   s_id, s_dist, s_de, s_ae, s_alive, lane);
+                                   s_id, s_dist, s_de, s_ae, s_alive, stage, lane);
       }
       // in-window greedy: the first alive entry is the next kept neighbour
       int stop_j = wn - 1;
@@ -153,7 +192,7 @@ __global__ void __launch_bounds__(PRUNE_WARPS * 32)
           break;
         }
         n_alive = test_round<VEC4>(X, d, w, duw, strategy, cos_alpha, 1, n_alive,
-                                   s_id, s_dist, s_de, s_ae, s_alive, lane);
+                                   s_id, s_dist, s_de, s_ae, s_alive, stage, lane);
       }
       __syncwarp();
       long long de = 0, ae = 0;
@@ -193,7 +232,7 @@ int launch_prune(const float *X, int64_t n, int64_t d, const int32_t *row_node,
   const size_t smem = sizeof(PruneSmem);
   const bool vec4 = (d % 4 == 0) && ((uintptr_t)X % 16 == 0);
   int64_t blocks = (n + PRUNE_WARPS - 1) / PRUNE_WARPS;
-  int64_t cap = (int64_t)num_sms() * 8;
+  int64_t cap = (int64_t)num_sms() * 2;  // 2 resident blocks per SM (~106 KB smem each)
   if (blocks > cap) blocks = cap;
   if (vec4) {
     static bool attr = false;
