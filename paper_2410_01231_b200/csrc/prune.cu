@@ -22,7 +22,7 @@ namespace pgk {
 
 constexpr int PRUNE_WARPS = 8;
 constexpr int PRUNE_W = 256;  // window entries per warp
-constexpr int DC = 64;        // dimensions per staged chunk
+constexpr int DC = 32;        // dimensions per staged chunk
 constexpr int SROW = DC + 4;  // staged row stride (floats): == 4 mod 32 -> LDS.128 conflict-free
 
 struct PruneSmem {
@@ -31,7 +31,7 @@ struct PruneSmem {
   int32_t de[PRUNE_WARPS][PRUNE_W];
   int32_t ae[PRUNE_WARPS][PRUNE_W];
   int16_t alive[PRUNE_WARPS][PRUNE_W];
-  alignas(16) float stage[PRUNE_WARPS][32 * SROW];  // 32 candidate rows, one chunk
+  alignas(16) float stage[PRUNE_WARPS][2][32 * SROW];  // 32 candidate rows x 2 chunks
 };
 
 // Test alive entries alive[a0 .. n_alive) against kept neighbour w; returns
@@ -42,6 +42,20 @@ struct PruneSmem {
 // the batch's 32 candidate rows are staged through shared memory 64 dims at a
 // time with coalesced float4 loads (two rows per warp instruction) and read
 // back conflict-free, instead of 32 scattered per-lane row walks.
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <bool VEC4>
 __device__ __forceinline__ int test_round(
     const float *__restrict__ X, int d, int32_t w, float duw, int strategy,
@@ -58,20 +72,35 @@ __device__ __forceinline__ int test_round(
     const int32_t v = s_id[j];
     float dwv = 0.0f;  // _kernels.py:390: squared_l2(data[w], data[v])
     if (VEC4) {
-      const int half = lane >> 4, l16 = lane & 15;
-      for (int c0 = 0; c0 < d; c0 += DC) {
+      // stage chunk c0 of the batch's rows: 8 lanes per row, 4 rows per
+      // instruction, all 8 cp.async instructions in flight together
+      const int l8 = lane & 7, rsub = lane >> 3;
+      auto issue = [&](int c0, float *buf) {
         const int dc = min(DC, d - c0);
-        __syncwarp();
-        for (int e0 = 0; e0 < nb; e0 += 2) {
-          const int e = e0 + half;
-          const int32_t ve = __shfl_sync(0xffffffffu, v, e & 31);
-          if (e < nb && 4 * l16 < dc)
-            *reinterpret_cast<float4 *>(stage + e * SROW + 4 * l16) =
-                __ldg(reinterpret_cast<const float4 *>(X + (int64_t)ve * d + c0) + l16);
+#pragma unroll
+        for (int e0 = 0; e0 < 32; e0 += 4) {
+          const int e = e0 + rsub;
+          const int32_t ve = __shfl_sync(0xffffffffu, v, e);
+          if (e < nb && 4 * l8 < dc)
+            cp_async16(buf + e * SROW + 4 * l8, X + (int64_t)ve * d + c0 + 4 * l8);
+        }
+        cp_async_commit();
+      };
+      __syncwarp();
+      issue(0, stage);
+      int cur = 0;
+      for (int c0 = 0; c0 < d; c0 += DC) {
+        const bool more = c0 + DC < d;
+        if (more) {
+          issue(c0 + DC, stage + (cur ^ 1) * 32 * SROW);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
         }
         __syncwarp();
         if (act) {
-          const float *srow = stage + lane * SROW;
+          const int dc = min(DC, d - c0);
+          const float *srow = stage + cur * 32 * SROW + lane * SROW;
           const float4 *w4 = reinterpret_cast<const float4 *>(xw + c0);
 #pragma unroll 4
           for (int k = 0; k < dc; k += 4) {
@@ -83,6 +112,8 @@ __device__ __forceinline__ int test_round(
             dwv = sq_step(dwv, x.w, y.w);
           }
         }
+        __syncwarp();
+        cur ^= 1;
       }
     } else if (act) {
       dwv = sql2_seq<false>(xw, X + (int64_t)v * d, d);
@@ -116,7 +147,7 @@ __device__ __forceinline__ int test_round(
 }
 
 template <bool VEC4>
-__global__ void __launch_bounds__(PRUNE_WARPS * 32)
+__global__ void __launch_bounds__(PRUNE_WARPS * 32, 2)
     prune_kernel(const float *__restrict__ X, int64_t n, int d,
                  const int32_t *__restrict__ row_node,
                  const int64_t *__restrict__ cand_off,
@@ -135,7 +166,7 @@ __global__ void __launch_bounds__(PRUNE_WARPS * 32)
   int32_t *s_de = sm.de[warp];
   int32_t *s_ae = sm.ae[warp];
   int16_t *s_alive = sm.alive[warp];
-  float *stage = sm.stage[warp];
+  float *stage = sm.stage[warp][0];
 
   for (int64_t u = (int64_t)blockIdx.x * PRUNE_WARPS + warp; u < n;
        u += (int64_t)gridDim.x * PRUNE_WARPS) {
