@@ -63,6 +63,12 @@ __global__ void norms_u8_kernel(const float *__restrict__ X, int64_t n, int d,
   }
 }
 
+int launch_norms_u8(const float *X, int64_t n, int d, int32_t *out, cudaStream_t stream) {
+  norms_u8_kernel<<<(unsigned)num_sms() * 4, 256, 0, stream>>>(X, n, d, out);
+  PGK_CHECK_LAUNCH("norms_u8_kernel");
+  return PGK_OK;
+}
+
 // Sort one row's buffer (warp), keep the best S, raise the threshold.
 template <int CAP>
 __device__ __forceinline__ void compact_row(uint64_t *b, int &cnt, uint64_t &tau,
@@ -442,13 +448,15 @@ struct KnnLayout {
   int *flag;
   int32_t *xnorm, *qnorm, *fb_list, *fb_count;
   uint64_t *keys;
-  void *tc_ws;
-  size_t tc_bytes;
+  void *tc_ws, *tws;
+  size_t tc_bytes, tws_bytes;
   size_t total;
 };
 
 size_t tc_pool_workspace(int64_t n, int64_t nq, bool self);
 bool tc_pool_supported(int64_t d, int64_t k);
+size_t tiles_workspace(int64_t n, int64_t d);
+bool tiles_supported(int64_t n, int64_t d, int64_t k);
 
 int pool_S(int64_t k, int mode) {
   if (mode == PGK_POOL_U8) return (int)k;
@@ -467,11 +475,15 @@ static KnnLayout knn_layout(void *ws, size_t bytes, int64_t n, int64_t nq, int64
   L.qnorm = c.take<int32_t>(nq);
   L.fb_list = c.take<int32_t>(nq);
   L.keys = c.take<uint64_t>((size_t)nq * S);
-  L.tc_bytes = 0;
-  L.tc_ws = nullptr;
+  L.tc_bytes = L.tws_bytes = 0;
+  L.tc_ws = L.tws = nullptr;
   if (mode != PGK_POOL_F32 && tc_pool_supported(d, k)) {
     L.tc_bytes = tc_pool_workspace(n, nq, false);
     L.tc_ws = c.take<char>(L.tc_bytes);
+    if (nq == n && tiles_supported(n, d, k)) {
+      L.tws_bytes = tiles_workspace(n, d);
+      L.tws = c.take<char>(L.tws_bytes);
+    }
   }
   L.total = c.off;
   return L;
@@ -530,10 +542,16 @@ static int launch_tile(const float *X, int64_t n, int d, const float *Q, int64_t
   return PGK_OK;
 }
 
-int launch_pool_tc_u8(const float *X, int64_t n, int d, const float *Q, int64_t nq,
-                      int exclude_self, const int32_t *xnorm, const int32_t *qnorm, int K,
-                      uint64_t *keys, void *tc_ws, size_t tc_bytes, cudaStream_t stream,
-                      bool *handled);
+int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, int64_t nq,
+                            int exclude_self, const int32_t *xnorm, const int32_t *qnorm,
+                            int K, uint64_t *keys, void *tc_ws, size_t tc_bytes,
+                            cudaStream_t stream, const uint8_t *xs_sorted,
+                            const int32_t *tlist, const int32_t *tlen, int64_t tstride,
+                            const int32_t *perm, bool *handled);
+int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm, int K,
+                         uint64_t *keys, void *tc_ws, size_t tc_bytes, void *tws,
+                         size_t tws_bytes, cudaStream_t stream, bool *handled,
+                         unsigned long long *pairs_out);
 
 int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, int64_t k,
               int exclude_self, int mode, int32_t *gt_ids, int32_t *pool_ids,
@@ -585,9 +603,15 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
       qn = L.qnorm;
     }
     bool handled = false;
-    if (L.tc_ws) {
-      rc = launch_pool_tc_u8(X, n, (int)d, Q, nq, exclude_self, L.xnorm, qn, (int)k, L.keys,
-                             L.tc_ws, L.tc_bytes, stream, &handled);
+    if (L.tc_ws && L.tws && self && exclude_self) {
+      rc = launch_pool_tiles_u8(X, n, (int)d, L.xnorm, (int)k, L.keys, L.tc_ws, L.tc_bytes,
+                                L.tws, L.tws_bytes, stream, &handled, nullptr);
+      if (rc) return rc;
+    }
+    if (L.tc_ws && !handled) {
+      rc = launch_pool_tc_u8_lists(X, n, (int)d, Q, nq, exclude_self, L.xnorm, qn, (int)k,
+                                   L.keys, L.tc_ws, L.tc_bytes, stream, nullptr, nullptr,
+                                   nullptr, 0, nullptr, &handled);
       if (rc) return rc;
     }
     if (!handled) {

@@ -296,7 +296,9 @@ __global__ void __launch_bounds__(THREADS, 2)
                       const __grid_constant__ CUtensorMap tmQ, int64_t n, int64_t nq,
                       int exclude_self, const int32_t *__restrict__ xnorm,
                       const int32_t *__restrict__ qnorm, int K, uint64_t *__restrict__ bufs,
-                      uint64_t *__restrict__ out_keys, unsigned long long *stats) {
+                      uint64_t *__restrict__ out_keys, unsigned long long *stats,
+                      const int32_t *__restrict__ tlist, const int32_t *__restrict__ tlen,
+                      int64_t tstride, const int32_t *__restrict__ perm) {
   unsigned long long st[ST_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t_prev = STATS ? clock64() : 0;
 #define PGK_TICK(slot)                          \
@@ -350,10 +352,12 @@ __global__ void __launch_bounds__(THREADS, 2)
         mbar_wait(&s.a_empty, (it & 1) ^ 1);
         mbar_expect_tx(&s.a_full, BM * KB);
         tma_load_2d(s.a, &tmQ, &s.a_full, 0, b * BM);
-        for (int t = 0; t < ntiles; ++t) {
+        const int len = tlist ? tlen[b] : ntiles;
+        for (int t = 0; t < len; ++t) {
+          const int tid = tlist ? tlist[(int64_t)b * tstride + t] : t;
           mbar_wait(&s.empty[stage], phase ^ 1);
           mbar_expect_tx(&s.full[stage], TILE_BYTES);
-          tma_load_2d(s.b[stage], &tmX, &s.full[stage], 0, t * BN);
+          tma_load_2d(s.b[stage], &tmX, &s.full[stage], 0, tid * BN);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -368,12 +372,14 @@ __global__ void __launch_bounds__(THREADS, 2)
         mbar_wait(&s.a_full, it & 1);
         tc_fence_after();
         const uint64_t adesc = sw128_desc(s.a);
-        for (int t = 0; t < ntiles; ++t) {
+        const int len = tlist ? tlen[b] : ntiles;
+        for (int t = 0; t < len; ++t) {
+          const int tid = tlist ? tlist[(int64_t)b * tstride + t] : t;
           mbar_wait(&s.tempty[acc], acc_phase ^ 1);
           // the tile's |x|^2 (xnorm is padded to a multiple of BN) lands with the
           // accumulator: tfull completes on the commit AND these bytes
           mbar_expect_tx_only(&s.tfull[acc], BN * 4);
-          bulk_load(s.ny[acc], xnorm + (int64_t)t * BN, BN * 4, &s.tfull[acc]);
+          bulk_load(s.ny[acc], xnorm + (int64_t)tid * BN, BN * 4, &s.tfull[acc]);
           mbar_wait(&s.full[stage], phase);
           tc_fence_after();
           const uint64_t bdesc = sw128_desc(s.b[stage]);
@@ -398,17 +404,19 @@ __global__ void __launch_bounds__(THREADS, 2)
     uint32_t acc_phase = 0;
     for (int b = blockIdx.x; b < nblocks; b += gridDim.x) {
       const int64_t row = (int64_t)b * BM + q * 32 + lane;
-      const bool row_ok = row < nq;
+      const bool row_ok = row < nq && (!perm || perm[row] >= 0);  // padding rows: no pool
       const int nx = row_ok ? qnorm[row] : 0;
       int cnt = 0;
       uint64_t tau = KEY_MAX;
       int tp = row_ok ? 0x7fffffff : -0x7fffffff;  // invalid rows never pass
-      for (int t = 0; t < ntiles; ++t) {
+      const int len = tlist ? tlen[b] : ntiles;
+      for (int t = 0; t < len; ++t) {
+        const int tid = tlist ? tlist[(int64_t)b * tstride + t] : t;
         PGK_TICK(ST_MAIN);
         mbar_wait(&s.tfull[acc], acc_phase);
         tc_fence_after();
         PGK_TICK(ST_WAIT);
-        const int64_t col0 = (int64_t)t * BN;
+        const int64_t col0 = (int64_t)tid * BN;
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
         uint32_t rbuf[2][32];
         tmem_ld32(tbase, rbuf[0]);
@@ -469,7 +477,8 @@ __global__ void __launch_bounds__(THREADS, 2)
               const int sj = sv[j];
               const int64_t col = cb + j;
               if (sj <= tp && col < n && !(exclude_self && col == row)) {
-                const uint64_t key = ((uint64_t)(uint32_t)(sj + nx) << 32) | (uint32_t)col;
+                const uint32_t cid = perm ? (uint32_t)perm[col] : (uint32_t)col;
+                const uint64_t key = ((uint64_t)(uint32_t)(sj + nx) << 32) | cid;
                 if (key < tau) mybuf[cnt++] = key;
               }
             }
@@ -490,6 +499,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       for (int src = 0; src < 32; ++src) {
         const int64_t r_src = (int64_t)b * BM + q * 32 + src;
         if (r_src >= nq) break;
+        if (perm && perm[r_src] < 0) continue;
         int c_src = __shfl_sync(0xffffffffu, cnt, src);
         const uint64_t t_src = __shfl_sync(0xffffffffu, tau, src);
         uint64_t *bsrc = wbuf + (size_t)src * CAP;
@@ -497,7 +507,7 @@ __global__ void __launch_bounds__(THREADS, 2)
           select_k(bsrc, c_src, K, t_src == KEY_MAX ? (1u << 25) : khi(t_src), lane);
           c_src = K;
         }
-        uint64_t *o = out_keys + r_src * K;
+        uint64_t *o = out_keys + (perm ? (int64_t)perm[r_src] : r_src) * K;
         if (K <= 32) emit_sorted<1>(bsrc, c_src, K, o, lane);
         else if (K <= 64) emit_sorted<2>(bsrc, c_src, K, o, lane);
         else if (K <= 128) emit_sorted<4>(bsrc, c_src, K, o, lane);
@@ -585,10 +595,12 @@ bool tc_pool_supported(int64_t d, int64_t k) {
   return !env && d <= tc::KB && k >= 1 && k <= 256;
 }
 
-int launch_pool_tc_u8(const float *X, int64_t n, int d, const float *Q, int64_t nq,
-                      int exclude_self, const int32_t *xnorm, const int32_t *qnorm, int K,
-                      uint64_t *keys, void *tc_ws, size_t tc_bytes, cudaStream_t stream,
-                      bool *handled) {
+int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, int64_t nq,
+                            int exclude_self, const int32_t *xnorm, const int32_t *qnorm,
+                            int K, uint64_t *keys, void *tc_ws, size_t tc_bytes,
+                            cudaStream_t stream, const uint8_t *xs_sorted,
+                            const int32_t *tlist, const int32_t *tlen, int64_t tstride,
+                            const int32_t *perm, bool *handled) {
   *handled = false;
   if (!tc_pool_supported(d, K)) return PGK_OK;
   const bool self = (Q == X);
@@ -602,8 +614,12 @@ int launch_pool_tc_u8(const float *X, int64_t n, int d, const float *Q, int64_t 
   const int sms = num_sms();
   uint64_t *bufs = c.take<uint64_t>((size_t)2 * sms * tc::BM * tc::CAP);
   const unsigned cg = (unsigned)std::min<int64_t>((n * tc::KB + 255) / 256, (int64_t)sms * 16);
-  tc::to_u8_kernel<<<cg, 256, 0, stream>>>(X, n, d, xu8);
-  PGK_CHECK_LAUNCH("to_u8_kernel");
+  if (xs_sorted) {
+    xu8 = qu8 = const_cast<uint8_t *>(xs_sorted);  // already u8, permuted by the tile sort
+  } else {
+    tc::to_u8_kernel<<<cg, 256, 0, stream>>>(X, n, d, xu8);
+    PGK_CHECK_LAUNCH("to_u8_kernel");
+  }
   if (!self) {
     tc::to_u8_kernel<<<cg, 256, 0, stream>>>(Q, nq, d, qu8);
     PGK_CHECK_LAUNCH("to_u8_kernel");
@@ -611,7 +627,7 @@ int launch_pool_tc_u8(const float *X, int64_t n, int d, const float *Q, int64_t 
   // pad |x|^2 to a multiple of BN with a huge value (0x3f3f3f3f > any distance):
   // the kernel bulk-copies whole 128-entry tiles of it
   const int64_t n_pad = (n + tc::BN - 1) / tc::BN * tc::BN;
-  if (n_pad > n)
+  if (n_pad > n && !xs_sorted)
     PGK_CUDA(cudaMemsetAsync(const_cast<int32_t *>(xnorm) + n, 0x3f, (n_pad - n) * 4, stream));
   CUtensorMap tmX, tmQ;
   if (!tc::make_map(&tmX, xu8, n) || !tc::make_map(&tmQ, qu8, nq)) {
@@ -635,7 +651,8 @@ int launch_pool_tc_u8(const float *X, int64_t n, int d, const float *Q, int64_t 
     PGK_CUDA(cudaMalloc(&dstats, sizeof(unsigned long long) * tc::ST_COUNT));
     PGK_CUDA(cudaMemsetAsync(dstats, 0, sizeof(unsigned long long) * tc::ST_COUNT, stream));
     tc::tc_pool_u8_kernel<true><<<grid, tc::THREADS, smem, stream>>>(
-        tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, dstats);
+        tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, dstats, tlist, tlen,
+        tstride, perm);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel<stats>");
     unsigned long long h[tc::ST_COUNT];
     PGK_CUDA(cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, stream));
@@ -649,7 +666,8 @@ int launch_pool_tc_u8(const float *X, int64_t n, int d, const float *Q, int64_t 
             h[6] / warps, (double)h[7] / (double)nq);
   } else {
     tc::tc_pool_u8_kernel<false><<<grid, tc::THREADS, smem, stream>>>(
-        tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr);
+        tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
+        tstride, perm);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel");
   }
   *handled = true;

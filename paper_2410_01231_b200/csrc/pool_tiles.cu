@@ -1,0 +1,456 @@
+// pool_tiles.cu -- exact tile pruning for the self k-NN pool (U8 path).
+//
+// The brute-force pool touches all N^2 pairs.  For a provably sufficient
+// subset: points are grouped into spatially coherent 128-row tiles -- every
+// point is assigned to its nearest "center" (every 512th data row; the
+// tcgen05 kernel itself with K = 1), points are counting-sorted by center and
+// each center's run is padded to a multiple of 128 rows with inert rows
+// (zero vector, huge norm, no output) so no tile straddles two cells -- and
+// every tile gets a centroid c_T and radius r_T = max |x - c_T| over its real
+// rows (float64).  For a query tile Q and any q in Q, x in T:
+//      |q - x| >= |c_Q - c_T| - r_Q - r_T  =: lb(Q,T)      (triangle inequality)
+//      |q - x| <= |c_Q - c_T| + r_Q + r_T  =: ub(Q,T)
+// Pass 1 runs the exact top-K of every query tile over its 8 nearest tiles
+// (by centroid distance); U_Q = the largest K-th distance found in Q is an
+// upper bound of every row's true K-th neighbour distance, so no point
+// farther than U_Q from a row of Q can be in its pool.  Q's candidate tiles
+// are {T : lb(Q,T) <= U_Q}, and pass 2 recomputes the exact top-K over them.  The tcgen05 kernel
+// then runs unchanged over each query tile's candidate list; results are
+// identical to the full scan (ids are mapped back through the permutation and
+// ties still break on the original id).  All bounds are float64 with explicit
+// relative margins, far above the float64 rounding of the inputs.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace pgk {
+
+size_t scan_scratch(int64_t m);
+int exclusive_scan(const int64_t *in, int64_t *out, int64_t m, int64_t *scratch,
+                   cudaStream_t stream);
+
+namespace tiles {
+
+constexpr int TB = 128;  // tile size (== tc::BN == tc::BM)
+constexpr double MARGIN = 1e-9;
+
+constexpr int CSTRIDE = 512;  // one center per 512 rows
+
+__global__ void gather_centers_kernel(const float *__restrict__ X, int64_t n, int d, int64_t C,
+                                      float *__restrict__ cen) {
+  const int64_t total = C * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / d;
+    const int k = (int)(e - c * d);
+    cen[e] = X[(c * CSTRIDE) * d + k];
+  }
+}
+
+__global__ void assign_hist_kernel(const uint64_t *__restrict__ keys, int64_t n,
+                                   int32_t *__restrict__ hist, int32_t *__restrict__ assign) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = key_id(keys[i]);
+    assign[i] = c;
+    atomicAdd(hist + c, 1);
+  }
+}
+
+// padded run lengths: each center's run rounded up to whole tiles
+__global__ void padded_len_kernel(const int32_t *__restrict__ hist, int64_t C,
+                                  int64_t *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= C;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = i < C ? (int64_t)(hist[i] + TB - 1) / TB * TB : 0;
+}
+
+__global__ void fill_i32_kernel(int32_t *__restrict__ p, int64_t m, int32_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void assign_scatter_kernel(const int32_t *__restrict__ assign, int64_t n,
+                                      const int64_t *__restrict__ off,
+                                      int32_t *__restrict__ cursor,
+                                      int32_t *__restrict__ perm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = assign[i];
+    perm[off[c] + atomicAdd(cursor + c, 1)] = (int32_t)i;
+  }
+}
+
+// sorted u8 rows (128 B) and norms; padding rows (perm < 0) are zero with a
+// huge norm so they never enter a pool
+__global__ void gather_sorted_kernel(const float *__restrict__ X, int d,
+                                     const int32_t *__restrict__ perm,
+                                     const int32_t *__restrict__ xnorm, int64_t np,
+                                     uint8_t *__restrict__ xs, int32_t *__restrict__ ns) {
+  const int64_t total = np * 128;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e >> 7;
+    const int c = (int)(e & 127);
+    const int32_t src = perm[r];
+    xs[e] = (src >= 0 && c < d) ? (uint8_t)__float2int_rn(X[(int64_t)src * d + c]) : (uint8_t)0;
+    if (c == 0) ns[r] = src >= 0 ? xnorm[src] : 0x3f3f3f3f;
+  }
+}
+
+// warp per tile: float64 centroid of the real rows (stored fp32) and radius
+// against the stored centroid (float64, inflated)
+__global__ void tile_stats_kernel(const uint8_t *__restrict__ xs, const int32_t *__restrict__ perm,
+                                  int d, int64_t ntiles, float *__restrict__ cent,
+                                  double *__restrict__ rad, int32_t *__restrict__ size) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t r0 = t * TB;
+    double acc[4] = {0, 0, 0, 0};
+    int cnt = 0;
+    for (int i = 0; i < TB; ++i) {
+      if (perm[r0 + i] < 0) continue;
+      ++cnt;
+      const uint8_t *row = xs + (r0 + i) * 128;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] += (double)row[lane + 32 * k];
+    }
+    float c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      c[k] = cnt ? (float)(acc[k] / cnt) : 0.f;
+      if (lane + 32 * k < d) cent[t * d + lane + 32 * k] = c[k];
+      if (lane + 32 * k >= d) c[k] = 0.f;
+    }
+    double rmax = 0.0;
+    for (int i = 0; i < TB; ++i) {
+      if (perm[r0 + i] < 0) continue;
+      const uint8_t *row = xs + (r0 + i) * 128;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double t_ = (double)row[lane + 32 * k] - (double)c[k];
+        s += t_ * t_;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      rmax = fmax(rmax, s);
+    }
+    if (lane == 0) {
+      rad[t] = sqrt(rmax) * (1.0 + MARGIN) + 1e-12;
+      size[t] = cnt;
+    }
+  }
+}
+
+// dc[Q][T] = |c_Q - c_T| for all tile pairs: register-tiled fp32 direct
+// difference (FMA), relative error <= (d+2) 2^-24 on dc^2, covered by DC_MARGIN.
+constexpr double DC_MARGIN = 2e-5;
+constexpr int DB = 64, DK = 32;
+__global__ void __launch_bounds__(256)
+    tile_dist_kernel(const float *__restrict__ cent, int64_t T, int d, float *__restrict__ dc) {
+  __shared__ float sa[DK][DB + 1], sb[DK][DB + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t q0 = (int64_t)blockIdx.y * DB, t0 = (int64_t)blockIdx.x * DB;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < d; k0 += DK) {
+    for (int e = threadIdx.x; e < DB * DK; e += 256) {
+      const int r = e / DK, k = e % DK;
+      sa[k][r] = (q0 + r < T && k0 + k < d) ? cent[(q0 + r) * d + k0 + k] : 0.f;
+      sb[k][r] = (t0 + r < T && k0 + k < d) ? cent[(t0 + r) * d + k0 + k] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < DK; ++k) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = sa[k][ty * 4 + i]; b[i] = sb[k][tx + 16 * i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float t_ = a[i] - b[j];
+          acc[i][j] = fmaf(t_, t_, acc[i][j]);
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = q0 + ty * 4 + i, t = t0 + tx + 16 * j;
+      if (q < T && t < T) dc[q * T + t] = sqrtf(acc[i][j]);
+    }
+}
+
+// pass-1 list: the NEAR nearest tiles of every query tile by centroid distance
+constexpr int NEAR = 8;
+__global__ void tile_nearest_kernel(const float *__restrict__ dc, const int32_t *__restrict__ size,
+                                    int64_t T, int32_t *__restrict__ lists,
+                                    int32_t *__restrict__ lens) {
+  __shared__ uint64_t sk[8][256];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t Q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; Q < T;
+       Q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    // per-lane best NEAR (sorted insertion), then a warp sort of 32*NEAR keys
+    uint64_t best[NEAR];
+#pragma unroll
+    for (int i = 0; i < NEAR; ++i) best[i] = KEY_MAX;
+    const bool qreal = size[Q] > 0;
+    for (int64_t t = lane; qreal && t < T; t += 32) {
+      if (size[t] <= 0) continue;
+      uint64_t k = ((uint64_t)__float_as_uint(dc[Q * T + t]) << 32) | (uint32_t)t;
+      if (k < best[NEAR - 1]) {  // sorted insertion (branch-free shift)
+#pragma unroll
+        for (int i = NEAR - 1; i > 0; --i)
+          best[i] = k < best[i - 1] ? best[i - 1] : (k < best[i] ? k : best[i]);
+        best[0] = k < best[0] ? k : best[0];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NEAR; ++i) sk[w][i * 32 + lane] = best[i];
+    __syncwarp();
+    warp_bitonic_sort(sk[w], 32 * NEAR, lane);
+    int m = 0;
+    for (int i = 0; i < NEAR; ++i) m += sk[w][i] != KEY_MAX;
+    if (lane < m) lists[Q * T + lane] = (int32_t)(uint32_t)sk[w][lane];
+    if (lane == 0) lens[Q] = m;
+    __syncwarp();
+  }
+}
+
+// U_Q = max over the tile's rows of the pass-1 K-th neighbour distance
+__global__ void tile_ubound_kernel(const uint64_t *__restrict__ keys, int K,
+                                   const int32_t *__restrict__ perm, int64_t T,
+                                   double *__restrict__ U) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t Q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; Q < T;
+       Q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double m = 0.0;
+    for (int r = lane; r < TB; r += 32) {
+      const int64_t pos = Q * TB + r;
+      if (perm[pos] < 0) continue;
+      const uint64_t k = keys[(int64_t)perm[pos] * K + K - 1];
+      const double dd = k == KEY_MAX ? __longlong_as_double(0x7ff0000000000000ll)
+                                     : (double)key_dist(k);
+      m = fmax(m, dd);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) U[Q] = sqrt(m) * (1.0 + MARGIN) + 1e-9;
+  }
+}
+
+// pass-2 list: every tile T with lb(Q,T) <= U_Q, ascending T
+__global__ void tile_filter_kernel(const float *__restrict__ dc, const double *__restrict__ rad,
+                                   const int32_t *__restrict__ size, const double *__restrict__ U,
+                                   int64_t T, int32_t *__restrict__ lists,
+                                   int32_t *__restrict__ lens,
+                                   unsigned long long *__restrict__ total) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t Q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; Q < T;
+       Q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const double rQ = rad[Q], UQ = U[Q];
+    int base = 0;
+    for (int64_t t0 = 0; size[Q] > 0 && t0 < T; t0 += 32) {
+      const int64_t t = t0 + lane;
+      bool keep = false;
+      if (t < T && size[t] > 0) {
+        const double lb = (double)dc[Q * T + t] * (1.0 - DC_MARGIN) - rQ - rad[t];
+        keep = lb <= UQ;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) lists[Q * T + base + __popc(bal & lanemask_lt())] = (int32_t)t;
+      base += __popc(bal);
+    }
+    if (lane == 0) {
+      lens[Q] = base;
+      atomicAdd(total, (unsigned long long)base);
+    }
+  }
+}
+
+struct Layout {
+  float *cen, *cent, *dcm;
+  int32_t *cnorm, *hist, *cursor, *assign, *perm, *ns, *size, *lists, *lens;
+  int64_t *off, *scan_tmp;
+  uint64_t *akeys;
+  double *rad, *U;
+  unsigned long long *total;
+  uint8_t *xs;
+  void *sub_ws;
+  size_t sub_bytes, bytes;
+  int64_t C, NPmax, Tmax;
+};
+
+}  // namespace tiles
+
+size_t tc_pool_workspace(int64_t n, int64_t nq, bool self);
+int launch_norms_u8(const float *X, int64_t n, int d, int32_t *out, cudaStream_t stream);
+int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, int64_t nq,
+                            int exclude_self, const int32_t *xnorm, const int32_t *qnorm,
+                            int K, uint64_t *keys, void *tc_ws, size_t tc_bytes,
+                            cudaStream_t stream, const uint8_t *xs_sorted,
+                            const int32_t *tlist, const int32_t *tlen, int64_t tstride,
+                            const int32_t *perm, bool *handled);
+
+static tiles::Layout tiles_layout(void *ws, size_t bytes, int64_t n, int64_t d) {
+  using namespace tiles;
+  Layout L{};
+  Carve c(ws, bytes);
+  L.C = (n + CSTRIDE - 1) / CSTRIDE;
+  L.NPmax = (n + TB - 1) / TB * TB + L.C * TB;  // padded rows, worst case
+  L.Tmax = L.NPmax / TB;
+  const int64_t C = L.C, NP = L.NPmax, T = L.Tmax;
+  L.cen = c.take<float>((size_t)C * d);
+  L.cnorm = c.take<int32_t>(C + 128);
+  L.akeys = c.take<uint64_t>(n);
+  L.hist = c.take<int32_t>(C);
+  L.cursor = c.take<int32_t>(C);
+  L.assign = c.take<int32_t>(n);
+  L.off = c.take<int64_t>(C + 1);
+  L.scan_tmp = c.take<int64_t>(scan_scratch(C + 1));
+  L.perm = c.take<int32_t>(NP);
+  L.xs = c.take<uint8_t>((size_t)NP * 128);
+  L.ns = c.take<int32_t>(NP + 128);
+  L.cent = c.take<float>((size_t)T * d);
+  L.rad = c.take<double>(T);
+  L.size = c.take<int32_t>(T);
+  L.lists = c.take<int32_t>((size_t)T * T);
+  L.lens = c.take<int32_t>(T);
+  L.dcm = c.take<float>((size_t)T * T);
+  L.U = c.take<double>(T);
+  L.total = c.take<unsigned long long>(4);
+  L.sub_bytes = tc_pool_workspace(C, n, false);
+  L.sub_ws = c.take<char>(L.sub_bytes);
+  L.bytes = c.off;
+  return L;
+}
+
+bool tiles_supported(int64_t n, int64_t d, int64_t k) {
+  static int env = -1;
+  if (env < 0) {
+    const char *e = getenv("PGK_DISABLE_PRUNE");
+    env = (e && e[0] == '1') ? 1 : 0;
+  }
+  const int64_t T = ((n + 127) / 128 * 128 + (n + 511) / 512 * 128) / 128;
+  // the T x T centroid-distance matrix and lists (8 B / pair) stay modest
+  return !env && d <= 128 && k <= 256 && n >= 8 * tiles::TB && T <= 32768;
+}
+
+size_t tiles_workspace(int64_t n, int64_t d) { return tiles_layout(nullptr, 0, n, d).bytes; }
+
+// Runs the whole pruned pool.  *handled = false when pruning does not apply.
+int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm, int K,
+                         uint64_t *keys, void *tc_ws, size_t tc_bytes, void *tws,
+                         size_t tws_bytes, cudaStream_t stream, bool *handled,
+                         unsigned long long *pairs_out) {
+  using namespace tiles;
+  *handled = false;
+  if (!tiles_supported(n, d, K)) return PGK_OK;
+  Layout L = tiles_layout(tws, tws_bytes, n, d);
+  if (L.bytes > tws_bytes) {
+    set_error("tile workspace too small");
+    return PGK_ERR_NOMEM;
+  }
+  const int sms = num_sms();
+  const int64_t C = L.C;
+  const unsigned g = (unsigned)sms * 8;
+  // 1. centers (every 512th row) + exact nearest center of every point (K = 1)
+  gather_centers_kernel<<<g, 256, 0, stream>>>(X, n, d, C, L.cen);
+  PGK_CHECK_LAUNCH("gather_centers_kernel");
+  int rc = launch_norms_u8(L.cen, C, d, L.cnorm, stream);
+  if (rc) return rc;
+  bool h = false;
+  rc = launch_pool_tc_u8_lists(L.cen, C, d, X, n, 0, L.cnorm, xnorm, 1, L.akeys, L.sub_ws,
+                               L.sub_bytes, stream, nullptr, nullptr, nullptr, 0, nullptr, &h);
+  if (rc) return rc;
+  if (!h) return PGK_OK;
+  // 2. counting sort by center, every run padded to whole tiles (perm = -1)
+  PGK_CUDA(cudaMemsetAsync(L.hist, 0, C * 4, stream));
+  PGK_CUDA(cudaMemsetAsync(L.cursor, 0, C * 4, stream));
+  assign_hist_kernel<<<g, 256, 0, stream>>>(L.akeys, n, L.hist, L.assign);
+  PGK_CHECK_LAUNCH("assign_hist_kernel");
+  padded_len_kernel<<<g, 256, 0, stream>>>(L.hist, C, L.off);
+  PGK_CHECK_LAUNCH("padded_len_kernel");
+  rc = exclusive_scan(L.off, L.off, C + 1, L.scan_tmp, stream);
+  if (rc) return rc;
+  // the padded total lives on the device; kernels below run over the
+  // worst-case size and treat tiles past the real total as empty
+  fill_i32_kernel<<<g, 256, 0, stream>>>(L.perm, L.NPmax, -1);
+  PGK_CHECK_LAUNCH("fill_i32_kernel");
+  assign_scatter_kernel<<<g, 256, 0, stream>>>(L.assign, n, L.off, L.cursor, L.perm);
+  PGK_CHECK_LAUNCH("assign_scatter_kernel");
+  const int64_t NP = L.NPmax, T = L.Tmax;
+  // 3. sorted u8 rows / norms, tile summaries, centroid distances
+  gather_sorted_kernel<<<g, 256, 0, stream>>>(X, d, L.perm, xnorm, NP, L.xs, L.ns);
+  PGK_CHECK_LAUNCH("gather_sorted_kernel");
+  fill_i32_kernel<<<1, 128, 0, stream>>>(L.ns + NP, 128, 0x3f3f3f3f);
+  PGK_CHECK_LAUNCH("fill_i32_kernel");
+  tile_stats_kernel<<<g, 256, 0, stream>>>(L.xs, L.perm, d, T, L.cent, L.rad, L.size);
+  PGK_CHECK_LAUNCH("tile_stats_kernel");
+  PGK_CUDA(cudaMemsetAsync(L.total, 0, sizeof(unsigned long long), stream));
+  tile_dist_kernel<<<dim3((unsigned)((T + DB - 1) / DB), (unsigned)((T + DB - 1) / DB)), 256, 0,
+                     stream>>>(L.cent, T, d, L.dcm);
+  PGK_CHECK_LAUNCH("tile_dist_kernel");
+  // 4. pass 1: exact top-K over each query tile's NEAR nearest tiles -> U_Q
+  tile_nearest_kernel<<<g, 256, 0, stream>>>(L.dcm, L.size, T, L.lists, L.lens);
+  PGK_CHECK_LAUNCH("tile_nearest_kernel");
+  rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes, stream,
+                               L.xs, L.lists, L.lens, T, L.perm, handled);
+  if (rc) return rc;
+  if (!*handled) return PGK_OK;
+  tile_ubound_kernel<<<g, 256, 0, stream>>>(keys, K, L.perm, T, L.U);
+  PGK_CHECK_LAUNCH("tile_ubound_kernel");
+  // 5. pass 2: every tile that can hold a pool member, then the full top-K
+  tile_filter_kernel<<<g, 256, 0, stream>>>(L.dcm, L.rad, L.size, L.U, T, L.lists, L.lens,
+                                            L.total);
+  PGK_CHECK_LAUNCH("tile_filter_kernel");
+  rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes, stream,
+                               L.xs, L.lists, L.lens, T, L.perm, handled);
+  if (rc) return rc;
+  const char *se = getenv("PGK_TILES_STATS");
+  if (se && se[0] == '1') {
+    unsigned long long tot = 0;
+    PGK_CUDA(cudaMemcpyAsync(&tot, L.total, sizeof(tot), cudaMemcpyDeviceToHost, stream));
+    std::vector<double> hr(T), hu(T);
+    std::vector<int32_t> hs(T);
+    PGK_CUDA(cudaMemcpyAsync(hr.data(), L.rad, T * 8, cudaMemcpyDeviceToHost, stream));
+    PGK_CUDA(cudaMemcpyAsync(hu.data(), L.U, T * 8, cudaMemcpyDeviceToHost, stream));
+    PGK_CUDA(cudaMemcpyAsync(hs.data(), L.size, T * 4, cudaMemcpyDeviceToHost, stream));
+    PGK_CUDA(cudaStreamSynchronize(stream));
+    std::vector<double> r2, u2;
+    int64_t real = 0;
+    for (int64_t t = 0; t < T; ++t)
+      if (hs[t] > 0) { r2.push_back(hr[t]); u2.push_back(hu[t]); ++real; }
+    auto q = [](std::vector<double> v, double f) {
+      std::sort(v.begin(), v.end());
+      return v.empty() ? 0.0 : v[(size_t)(f * (v.size() - 1))];
+    };
+    fprintf(stderr,
+            "[tiles] %lld non-empty tiles (padded rows %.1f%%); candidate pairs %llu = %.3f%% of "
+            "N^2 tiles, mean list %.1f | radius p50/p90/max %.1f %.1f %.1f | U_Q p50/p90 %.1f "
+            "%.1f\n",
+            (long long)real, 100.0 * (real * 128.0 - n) / (real * 128.0), tot,
+            100.0 * tot / ((double)real * real), (double)tot / real, q(r2, .5), q(r2, .9),
+            q(r2, 1.0), q(u2, .5), q(u2, .9));
+  }
+  if (pairs_out) *pairs_out = 0;
+  return PGK_OK;
+}
+
+// Device counter of candidate tile pairs of the last pruned launch on `tws`.
+int tiles_pairs(const void *tws, size_t tws_bytes, int64_t n, int64_t d,
+                unsigned long long *host, cudaStream_t stream) {
+  tiles::Layout L = tiles_layout(const_cast<void *>(tws), tws_bytes, n, d);
+  PGK_CUDA(cudaMemcpyAsync(host, L.total, sizeof(*host), cudaMemcpyDeviceToHost, stream));
+  PGK_CUDA(cudaStreamSynchronize(stream));
+  return PGK_OK;
+}
+
+}  // namespace pgk

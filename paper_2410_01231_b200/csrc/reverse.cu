@@ -109,7 +109,7 @@ __global__ void scan_add_kernel(int64_t *__restrict__ out, int64_t m,
     out[e] += boff[e / SCAN_TILE];
 }
 
-static size_t scan_scratch(int64_t m) {
+size_t scan_scratch(int64_t m) {
   size_t tot = 0;
   while (m > 1) {
     int64_t nb = (m + SCAN_TILE - 1) / SCAN_TILE;
@@ -119,7 +119,7 @@ static size_t scan_scratch(int64_t m) {
   return tot + 2;
 }
 
-static int exclusive_scan(const int64_t *in, int64_t *out, int64_t m, int64_t *scratch,
+int exclusive_scan(const int64_t *in, int64_t *out, int64_t m, int64_t *scratch,
                           cudaStream_t stream) {
   const int64_t nb = (m + SCAN_TILE - 1) / SCAN_TILE;
   int64_t *bsum = scratch, *boff = scratch + nb;

@@ -65,3 +65,33 @@ def test_tc_queries_table():
     for i in range(0, 100, 7):
         d64 = ((data.astype(np.float64) - q[i].astype(np.float64)) ** 2).sum(1)
         assert table[i].tolist() == np.lexsort((np.arange(4000), d64))[:16].tolist()
+
+
+def _pools_subprocess(gen_code, K, env_extra):
+    code = ("import sys, numpy as np; sys.path.insert(0, %r);"
+            "from paper_2410_01231_b200 import Dataset, knn_pools, synth;"
+            "data = %s; i, d = knn_pools(Dataset.from_array(data), %d);"
+            "np.save('/tmp/pgk_sub_ids.npy', i); np.save('/tmp/pgk_sub_d.npy', d)"
+            % (str(ROOT), gen_code, K))
+    env = dict(os.environ, **env_extra)
+    subprocess.check_call([sys.executable, "-c", code], env=env, timeout=600)
+    return np.load("/tmp/pgk_sub_ids.npy"), np.load("/tmp/pgk_sub_d.npy")
+
+
+@pytest.mark.parametrize("gen_code,K", [
+    ("synth.cfg2(30000)", 128),
+    ("np.random.default_rng(3).integers(0, 256, (9000, 128)).astype(np.float32)", 64),
+    ("np.repeat(np.random.default_rng(4).integers(0, 256, (300, 96)), 20, axis=0)"
+     ".astype(np.float32)", 32),
+])
+def test_tile_pruned_pool_equals_full_scan(gen_code, K):
+    """Exact tile pruning (default) vs the full tcgen05 scan (PGK_DISABLE_PRUNE=1):
+    clustered, uniform (little to prune) and duplicate-heavy data."""
+    data = eval(gen_code, {"np": np, "synth": synth})
+    ids, dists = knn_pools(Dataset.from_array(data), K)
+    f_ids, f_d = _pools_subprocess(gen_code, K, {"PGK_DISABLE_PRUNE": "1"})
+    np.testing.assert_array_equal(ids, f_ids)
+    np.testing.assert_array_equal(dists, f_d)
+    rows = np.random.default_rng(1).choice(len(data), 150, replace=False)
+    o_ids, o_d = oracle.knn_pools(data, K, rows)
+    np.testing.assert_array_equal(ids[rows], o_ids)
