@@ -154,26 +154,31 @@ constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)
 __device__ __forceinline__ uint32_t khi(uint64_t k) { return (uint32_t)(k >> 32); }
 
 __device__ __forceinline__ int warp_sum(int v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+  return (int)__reduce_add_sync(0xffffffffu, (unsigned)v);
 }
 
 // Warp-cooperative selection on one row's candidate buffer (cnt > K keys in
 // global memory): keep exactly the K smallest keys (unordered) at buf[0..K)
-// and return the K-th smallest key.  Two binary searches over the register-
-// resident keys (distance bits, then id bits among distance ties); no sort.
+// and return the K-th smallest key.  Binary searches over the register-
+// resident keys (distance within [min, max], then id among distance ties;
+// REDUX warp sums); no sort.
 constexpr int KPL = CAP / 32;  // keys per lane
 __device__ __noinline__ uint64_t select_k(uint64_t *buf, int cnt, int K, uint32_t hi_bound,
                                           int lane) {
   uint64_t kk[KPL];
+  uint32_t dmin = 0xffffffffu, dmax = 0;
 #pragma unroll
   for (int i = 0; i < KPL; ++i) {
     const int idx = i * 32 + lane;
     kk[i] = idx < cnt ? buf[idx] : KEY_MAX;
+    if (idx < cnt) {
+      dmin = min(dmin, khi(kk[i]));
+      dmax = max(dmax, khi(kk[i]));
+    }
   }
-  // smallest td with #{dist <= td} >= K
-  uint32_t lo = 0, hi = hi_bound;
+  // smallest td with #{dist <= td} >= K, searched in [min, max]
+  uint32_t lo = __reduce_min_sync(0xffffffffu, dmin);
+  uint32_t hi = min(__reduce_max_sync(0xffffffffu, dmax), hi_bound);
   while (lo < hi) {
     const uint32_t mid = lo + ((hi - lo) >> 1);
     int c = 0;
@@ -198,9 +203,7 @@ __device__ __noinline__ uint64_t select_k(uint64_t *buf, int cnt, int K, uint32_
   const int need = K - c_lt;
   uint32_t tid;
   if (c_eq == need) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) id_max = max(id_max, __shfl_xor_sync(0xffffffffu, id_max, o));
-    tid = id_max;
+    tid = __reduce_max_sync(0xffffffffu, id_max);
   } else {  // distance ties straddle the boundary: smallest ids win
     uint32_t a = 0, b = 0x7fffffffu;
     while (a < b) {
@@ -298,7 +301,8 @@ __global__ void __launch_bounds__(THREADS, 2)
                       const int32_t *__restrict__ qnorm, int K, uint64_t *__restrict__ bufs,
                       uint64_t *__restrict__ out_keys, unsigned long long *stats,
                       const int32_t *__restrict__ tlist, const int32_t *__restrict__ tlen,
-                      int64_t tstride, const int32_t *__restrict__ perm) {
+                      int64_t tstride, const int32_t *__restrict__ perm,
+                      const uint64_t *__restrict__ init_keys) {
   unsigned long long st[ST_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t_prev = STATS ? clock64() : 0;
 #define PGK_TICK(slot)                          \
@@ -408,7 +412,14 @@ __global__ void __launch_bounds__(THREADS, 2)
       const int nx = row_ok ? qnorm[row] : 0;
       int cnt = 0;
       uint64_t tau = KEY_MAX;
-      int tp = row_ok ? 0x7fffffff : -0x7fffffff;  // invalid rows never pass
+      if (row_ok && init_keys) {
+        // a previous pass's K-th key of this row (library key format) bounds
+        // its true K-th key from above: keep only keys <= it
+        const uint64_t k0 = init_keys[(perm ? (int64_t)perm[row] : row) * K + K - 1];
+        if (k0 != KEY_MAX)
+          tau = (((uint64_t)(uint32_t)key_dist(k0) << 32) | (uint32_t)key_id(k0)) + 1;
+      }
+      int tp = row_ok ? tau_prefilter(tau, nx) : -0x7fffffff;  // invalid rows never pass
       const int len = tlist ? tlen[b] : ntiles;
       for (int t = 0; t < len; ++t) {
         const int tid = tlist ? tlist[(int64_t)b * tstride + t] : t;
@@ -453,6 +464,24 @@ __global__ void __launch_bounds__(THREADS, 2)
                 reinterpret_cast<int4 *>(sv)[v] = o;
               }
             }
+            if (K == 1) {  // nearest neighbour only: the threshold IS the answer
+              while (mask) {
+                const int j = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const int sj = sv[j];
+                const int64_t col = cb + j;
+                if (sj <= tp && col < n && !(exclude_self && col == row)) {
+                  const uint32_t cid = perm ? (uint32_t)perm[col] : (uint32_t)col;
+                  const uint64_t key = ((uint64_t)(uint32_t)(sj + nx) << 32) | cid;
+                  if (key < tau) {
+                    tau = key;
+                    tp = tau_prefilter(tau, nx);
+                  }
+                }
+              }
+              __syncwarp();
+              continue;
+            }
             // room for this chunk's survivors in every row of the warp
             unsigned need = __ballot_sync(0xffffffffu, cnt + __popc(mask) > CAP);
             if (STATS) st[ST_NCOMPACT] += __popc(need);
@@ -496,7 +525,12 @@ __global__ void __launch_bounds__(THREADS, 2)
       // block done: emit every row's best K (sorted), reset for the next block
       PGK_TICK(ST_MAIN);
       __syncwarp();
-      for (int src = 0; src < 32; ++src) {
+      if (K == 1) {
+        if (row_ok)
+          out_keys[perm ? (int64_t)perm[row] : row] =
+              tau == KEY_MAX ? KEY_MAX : pack_key((float)khi(tau), (int32_t)(uint32_t)tau);
+      }
+      for (int src = 0; K > 1 && src < 32; ++src) {
         const int64_t r_src = (int64_t)b * BM + q * 32 + src;
         if (r_src >= nq) break;
         if (perm && perm[r_src] < 0) continue;
@@ -600,7 +634,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             int K, uint64_t *keys, void *tc_ws, size_t tc_bytes,
                             cudaStream_t stream, const uint8_t *xs_sorted,
                             const int32_t *tlist, const int32_t *tlen, int64_t tstride,
-                            const int32_t *perm, bool *handled) {
+                            const int32_t *perm, bool *handled, const uint64_t *init_keys) {
   *handled = false;
   if (!tc_pool_supported(d, K)) return PGK_OK;
   const bool self = (Q == X);
@@ -652,7 +686,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
     PGK_CUDA(cudaMemsetAsync(dstats, 0, sizeof(unsigned long long) * tc::ST_COUNT, stream));
     tc::tc_pool_u8_kernel<true><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, dstats, tlist, tlen,
-        tstride, perm);
+        tstride, perm, init_keys);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel<stats>");
     unsigned long long h[tc::ST_COUNT];
     PGK_CUDA(cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, stream));
@@ -667,7 +701,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   } else {
     tc::tc_pool_u8_kernel<false><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
-        tstride, perm);
+        tstride, perm, init_keys);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel");
   }
   *handled = true;

@@ -297,7 +297,8 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             int K, uint64_t *keys, void *tc_ws, size_t tc_bytes,
                             cudaStream_t stream, const uint8_t *xs_sorted,
                             const int32_t *tlist, const int32_t *tlen, int64_t tstride,
-                            const int32_t *perm, bool *handled);
+                            const int32_t *perm, bool *handled,
+                            const uint64_t *init_keys = nullptr);
 
 static tiles::Layout tiles_layout(void *ws, size_t bytes, int64_t n, int64_t d) {
   using namespace tiles;
@@ -412,7 +413,7 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
                                             L.total);
   PGK_CHECK_LAUNCH("tile_filter_kernel");
   rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes, stream,
-                               L.xs, L.lists, L.lens, T, L.perm, handled);
+                               L.xs, L.lists, L.lens, T, L.perm, handled, keys);
   if (rc) return rc;
   const char *se = getenv("PGK_TILES_STATS");
   if (se && se[0] == '1') {
