@@ -229,11 +229,13 @@ def run_ours(args):
             e[0].record(stream)
             pids, pd = builder.pools(X)
             e[1].record(stream)
+            u8 = builder.u8_rows(X)
             a = kernels.prune_batch(X, builder.cand_off, builder.cand_counts, pids, pd,
-                                    p.strategy_code, p.cos_alpha, p.M, p.M, out=builder.a_out)
+                                    p.strategy_code, p.cos_alpha, p.M, p.M, out=builder.a_out,
+                                    u8=u8)
             e[2].record(stream)
             kernels.add_reverse_and_prune(X, a[0], a[1], a[2], p.strategy_code, p.cos_alpha,
-                                          p.M, p.M, ws=builder.rev_ws, out=builder.b_out)
+                                          p.M, p.M, ws=builder.rev_ws, out=builder.b_out, u8=u8)
             e[3].record(stream)
         barrier()
     launches = _lib.launch_count() - launches0

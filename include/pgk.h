@@ -76,6 +76,24 @@ int pgk_prune_rows(const float *data, int64_t n, int64_t d, int64_t n_rows,
                    int32_t *out_counts, int64_t *dist_evals, int64_t *angle_evals,
                    void *stream);
 
+/* Exact-integer variants.  When every value of `data` is an integer in
+ * [0,255] and d <= 128 (pgk_detect_u8), the reference's sequential fp32
+ * squared_l2 never leaves the exact-integer range (all partial sums < 2^24),
+ * so the kernels may compute it as |w|^2 + |v|^2 - 2 w.v on a u8 copy of the
+ * rows: bit-identical results, 4x fewer bytes.  pgk_make_u8 builds that copy
+ * (rows of 128 bytes, zero padded; int32 squared norms).  data_u8 == NULL
+ * selects the fp32 path (then these equal pgk_prune_rows). */
+int pgk_make_u8(const float *data, int64_t n, int64_t d, uint8_t *out_u8,
+                int32_t *out_norms, void *stream);
+int pgk_prune_rows_ex(const float *data, const uint8_t *data_u8,
+                      const int32_t *norms_u8, int64_t n, int64_t d, int64_t n_rows,
+                      const int32_t *row_node, const int64_t *cand_off,
+                      const int32_t *cand_counts, const int32_t *cand_ids,
+                      const float *cand_dists, int strategy, double cos_alpha,
+                      int64_t M, int64_t width, int32_t *out_ids, float *out_dists,
+                      int32_t *out_counts, int64_t *dist_evals,
+                      int64_t *angle_evals, void *stream);
+
 /* ---------------------------------------------------------------------------
  * Phase B: reverse-edge insertion + re-prune.  Replaces
  * prune.add_reverse_and_prune (prune.py:129-151) = np.bincount/cumsum +
@@ -92,6 +110,16 @@ int pgk_add_reverse_and_prune(const float *data, int64_t n, int64_t d,
                               float *out_dists, int32_t *out_counts,
                               int64_t *dist_evals, int64_t *angle_evals,
                               void *ws, size_t ws_bytes, void *stream);
+/* exact-integer variant (see pgk_prune_rows_ex) */
+int pgk_add_reverse_and_prune_ex(const float *data, const uint8_t *data_u8,
+                                 const int32_t *norms_u8, int64_t n, int64_t d,
+                                 const int32_t *a_ids, const float *a_dists,
+                                 const int32_t *a_counts, int64_t a_width,
+                                 int strategy, double cos_alpha, int64_t M,
+                                 int64_t out_width, int32_t *out_ids,
+                                 float *out_dists, int32_t *out_counts,
+                                 int64_t *dist_evals, int64_t *angle_evals,
+                                 void *ws, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Exact k-NN candidate pools.  Replaces oracle.ground_truth_table

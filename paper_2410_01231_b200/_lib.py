@@ -38,6 +38,11 @@ def lib():
                                       P, P, P, P, P, P]
         L.pgk_prune_rows.argtypes = [P, I64, I64, I64, P, P, P, P, P, I, D, I64, I64,
                                      P, P, P, P, P, P]
+        L.pgk_prune_rows_ex.argtypes = [P, P, P, I64, I64, I64, P, P, P, P, P, I, D, I64, I64,
+                                        P, P, P, P, P, P]
+        L.pgk_make_u8.argtypes = [P, I64, I64, P, P, P]
+        L.pgk_add_reverse_and_prune_ex.argtypes = [P, P, P, I64, I64, P, P, P, I64, I, D, I64,
+                                                   I64, P, P, P, P, P, P, SZ, P]
         L.pgk_reverse_workspace.argtypes = [I64, I64, P]
         L.pgk_add_reverse_and_prune.argtypes = [P, I64, I64, P, P, P, I64, I, D, I64, I64,
                                                 P, P, P, P, P, P, SZ, P]
@@ -45,7 +50,8 @@ def lib():
         L.pgk_knn_workspace.argtypes = [I64, I64, I64, I64, I, P]
         L.pgk_knn_pools.argtypes = [P, I64, I64, P, I64, I64, I, I, P, P, P, P, SZ, P]
         L.pgk_knn_fallback_rows.argtypes = [P, P, P]
-        for f in ("pgk_device_check", "pgk_prune_batch", "pgk_prune_rows", "pgk_reverse_workspace",
+        for f in ("pgk_device_check", "pgk_prune_batch", "pgk_prune_rows", "pgk_prune_rows_ex",
+                  "pgk_make_u8", "pgk_add_reverse_and_prune_ex", "pgk_reverse_workspace",
                   "pgk_add_reverse_and_prune", "pgk_detect_u8", "pgk_knn_workspace",
                   "pgk_knn_pools", "pgk_knn_fallback_rows"):
             getattr(L, f).restype = I
@@ -54,7 +60,7 @@ def lib():
 
 
 EXPORTS = ("pgk_version", "pgk_last_error", "pgk_device_check", "pgk_prune_batch",
-           "pgk_prune_rows",
+           "pgk_prune_rows", "pgk_prune_rows_ex", "pgk_make_u8", "pgk_add_reverse_and_prune_ex",
            "pgk_reverse_workspace", "pgk_add_reverse_and_prune", "pgk_detect_u8",
            "pgk_knn_workspace", "pgk_knn_pools", "pgk_knn_fallback_rows",
            "pgk_launch_count")

@@ -31,6 +31,7 @@ class Dataset:
         self.data = data
         self._dev = data if isinstance(data, torch.Tensor) and data.is_cuda else None
         self._u8 = None
+        self._u8_rows = None
 
     @classmethod
     def from_array(cls, arr) -> "Dataset":
@@ -72,6 +73,15 @@ class Dataset:
         if self._u8 is None:
             self._u8 = kernels.detect_u8(self.device_data())
         return self._u8
+
+    def device_u8(self):
+        """(u8 rows (n, 128), int32 norms) for the exact-integer selection path,
+        or None when the data are not [0,255] integers with d <= 128."""
+        if self.d > 128 or not self.is_u8():
+            return None
+        if self._u8_rows is None:
+            self._u8_rows = kernels.make_u8(self.device_data())
+        return self._u8_rows
 
 
 def centroid(ds: Dataset) -> np.ndarray:

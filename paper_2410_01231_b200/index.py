@@ -50,20 +50,32 @@ class RngBuilder:
                       torch.empty(n, dtype=I64, device=dev))
         self.rev_ws = _lib.workspace(kernels.reverse_workspace_bytes(n, M))
         self.b_out = tuple(torch.empty_like(t) for t in self.a_out)
+        self.u8_out = (torch.empty((n, 128), dtype=torch.uint8, device=dev),
+                       torch.empty(n, dtype=I32, device=dev))
 
     def pools(self, X: torch.Tensor):
         r = kernels.knn_pools(X, self.K, None, True, self.mode, False, self.pool_ws,
                               self.pool_out)
         return r.pool_ids, r.pool_dists
 
+    def u8_rows(self, X: torch.Tensor):
+        """Exact-integer rows for the selection passes (U8 mode, d <= 128)."""
+        if self.mode != _lib.POOL_U8 or self.d > 128:
+            return None
+        xu8, norms = self.u8_out
+        _lib.check(_lib.lib().pgk_make_u8(_lib.ptr(X), self.n, self.d, _lib.ptr(xu8),
+                                          _lib.ptr(norms), _lib.stream_handle()))
+        return self.u8_out
+
     def build(self, X: torch.Tensor) -> BuildOutput:
         """Enqueue the whole path on the current stream (no host sync)."""
         p = self.params
         ids, dists = self.pools(X)
+        u8 = self.u8_rows(X)
         a = kernels.prune_batch(X, self.cand_off, self.cand_counts, ids, dists,
-                                p.strategy_code, p.cos_alpha, p.M, p.M, out=self.a_out)
+                                p.strategy_code, p.cos_alpha, p.M, p.M, out=self.a_out, u8=u8)
         b = kernels.add_reverse_and_prune(X, a[0], a[1], a[2], p.strategy_code, p.cos_alpha,
-                                          p.M, p.M, ws=self.rev_ws, out=self.b_out)
+                                          p.M, p.M, ws=self.rev_ws, out=self.b_out, u8=u8)
         de = torch.stack([a[3].sum(), b[3].sum()])
         ae = torch.stack([a[4].sum(), b[4].sum()])
         return BuildOutput(b[0], b[1], b[2], a[2], de, ae)

@@ -27,11 +27,23 @@ def _dev(t, dtype) -> torch.Tensor:
     return t.contiguous()
 
 
+def make_u8(X: torch.Tensor):
+    """Exact-integer copy of an integer-valued [0,255] dataset (d <= 128):
+    (rows of 128 bytes, int32 squared norms) -- pgk_make_u8."""
+    X = _dev(X, _F32)
+    n, d = X.shape
+    xu8 = torch.empty((n, 128), dtype=torch.uint8, device=X.device)
+    norms = torch.empty(n, dtype=_I32, device=X.device)
+    check(_lib.lib().pgk_make_u8(ptr(X), n, d, ptr(xu8), ptr(norms), _lib.stream_handle()))
+    return xu8, norms
+
+
 def prune_batch(X: torch.Tensor, cand_off, cand_counts, cand_ids, cand_dists,
                 strategy: int, cos_alpha: float, M: int, width: int | None = None,
-                row_node=None, out=None):
-    """Phase-A scan (pgk_prune_batch / pgk_prune_rows).  Returns device tensors
-    (ids (rows, width), dists, counts, dist_evals (rows,), angle_evals (rows,))."""
+                row_node=None, out=None, u8=None):
+    """Phase-A scan (pgk_prune_rows_ex).  ``u8`` = make_u8(X) selects the
+    exact-integer distance path.  Returns device tensors (ids (rows, width),
+    dists, counts, dist_evals (rows,), angle_evals (rows,))."""
     X = _dev(X, _F32)
     n, d = X.shape
     cand_off = _dev(cand_off, _I64)
@@ -48,18 +60,12 @@ def prune_batch(X: torch.Tensor, cand_off, cand_counts, cand_ids, cand_dists,
                torch.empty(rows, dtype=_I64, device=dev),
                torch.empty(rows, dtype=_I64, device=dev))
     ids, dists, counts, de, ae = out
-    if row_node is None and rows == n:
-        rc = _lib.lib().pgk_prune_batch(
-            ptr(X), n, d, ptr(cand_off), ptr(cand_counts), ptr(cand_ids), ptr(cand_dists),
-            int(strategy), float(cos_alpha), int(M), int(width), ptr(ids), ptr(dists),
-            ptr(counts), ptr(de), ptr(ae), _lib.stream_handle())
-    else:
-        rn = None if row_node is None else _dev(row_node, _I32)
-        rc = _lib.lib().pgk_prune_rows(
-            ptr(X), n, d, rows, ptr(rn), ptr(cand_off), ptr(cand_counts), ptr(cand_ids),
-            ptr(cand_dists), int(strategy), float(cos_alpha), int(M), int(width), ptr(ids),
-            ptr(dists), ptr(counts), ptr(de), ptr(ae), _lib.stream_handle())
-    check(rc)
+    rn = None if row_node is None else _dev(row_node, _I32)
+    xu8, norms = (None, None) if u8 is None else u8
+    check(_lib.lib().pgk_prune_rows_ex(
+        ptr(X), ptr(xu8), ptr(norms), n, d, rows, ptr(rn), ptr(cand_off), ptr(cand_counts),
+        ptr(cand_ids), ptr(cand_dists), int(strategy), float(cos_alpha), int(M), int(width),
+        ptr(ids), ptr(dists), ptr(counts), ptr(de), ptr(ae), _lib.stream_handle()))
     return ids, dists, counts, de, ae
 
 
@@ -71,7 +77,7 @@ def reverse_workspace_bytes(n: int, a_width: int) -> int:
 
 def add_reverse_and_prune(X: torch.Tensor, a_ids, a_dists, a_counts, strategy: int,
                           cos_alpha: float, M: int, width: int | None = None, ws=None,
-                          out=None):
+                          out=None, u8=None):
     """Phase B (pgk_add_reverse_and_prune); device tensors in and out."""
     X = _dev(X, _F32)
     n, d = X.shape
@@ -90,8 +96,10 @@ def add_reverse_and_prune(X: torch.Tensor, a_ids, a_dists, a_counts, strategy: i
                torch.empty(n, dtype=_I64, device=dev),
                torch.empty(n, dtype=_I64, device=dev))
     ids, dists, counts, de, ae = out
-    check(_lib.lib().pgk_add_reverse_and_prune(
-        ptr(X), n, d, ptr(a_ids), ptr(a_dists), ptr(a_counts), a_width, int(strategy),
+    xu8, norms = (None, None) if u8 is None else u8
+    check(_lib.lib().pgk_add_reverse_and_prune_ex(
+        ptr(X), ptr(xu8), ptr(norms), n, d, ptr(a_ids), ptr(a_dists), ptr(a_counts), a_width,
+        int(strategy),
         float(cos_alpha), int(M), int(width), ptr(ids), ptr(dists), ptr(counts), ptr(de),
         ptr(ae), ptr(ws), ws.numel(), _lib.stream_handle()))
     return ids, dists, counts, de, ae

@@ -245,3 +245,29 @@ def test_device_resident_api_keeps_tensors_on_gpu():
     cnt = torch.full((3000,), 32, dtype=torch.int32, device="cuda")
     a = prune_all(ds, off, cnt, ids.reshape(-1), dists.reshape(-1), PruneParams(M=16))
     assert a[0].is_cuda and int(a[3]) > 0
+
+
+@pytest.mark.parametrize("strategy,alpha", [("rng", 60.0), ("alpha", 66.0)])
+def test_exact_integer_selection_equals_fp32_path(strategy, alpha):
+    """Integer-valued [0,255] data: the u8 dp4a selection path (pgk_prune_rows_ex
+    with data_u8) gives the same rows and counters as the fp32 sequential path."""
+    data = synth.cfg2(8000)
+    ds = Dataset.from_array(data)
+    K, R = 64, 24
+    ids, dists = knn_pools(ds, K)
+    X = ds.device_data()
+    u8 = kernels.make_u8(X)
+    params = PruneParams(M=R, alpha=alpha, strategy=strategy)
+    off = np.arange(ds.n + 1, dtype=np.int64) * K
+    cnt = np.full(ds.n, K, np.int32)
+    args = (X, off, cnt, ids.ravel(), dists.ravel(), params.strategy_code, params.cos_alpha, R)
+    a32 = kernels.prune_batch(*args)
+    a8 = kernels.prune_batch(*args, u8=u8)
+    for x, y in zip(a32, a8):
+        assert torch.equal(x, y)
+    b32 = kernels.add_reverse_and_prune(X, a32[0], a32[1], a32[2], params.strategy_code,
+                                        params.cos_alpha, R)
+    b8 = kernels.add_reverse_and_prune(X, a8[0], a8[1], a8[2], params.strategy_code,
+                                       params.cos_alpha, R, u8=u8)
+    for x, y in zip(b32, b8):
+        assert torch.equal(x, y)
