@@ -148,6 +148,14 @@ int pgk_knn_pools(const float *data, int64_t n, int64_t d,
  * helper performs a blocking read). */
 int pgk_knn_fallback_rows(const void *ws, int *rows_host, void *stream);
 
+/* Work record of the most recent pgk_knn_pools call on this workspace
+ * (blocking read; same n, nq, d, k, mode as the workspace query):
+ * work_host[0] = pass-2 128x128 tile pairs, [1] = pass-1 pairs,
+ * [2] = center-assignment pairs, [3] = 1 when the exact tile-pruned tcgen05
+ * path ran (all zero otherwise: the brute-force kernels ran). */
+int pgk_knn_work(const void *ws, int64_t n, int64_t nq, int64_t d, int64_t k,
+                 int mode, uint64_t *work_host, void *stream);
+
 /* Cumulative number of kernel launches this library has issued since it was
  * loaded (process-wide; the bench reports the difference around its timed
  * region as gpu_launches). */

@@ -50,10 +50,11 @@ def lib():
         L.pgk_knn_workspace.argtypes = [I64, I64, I64, I64, I, P]
         L.pgk_knn_pools.argtypes = [P, I64, I64, P, I64, I64, I, I, P, P, P, P, SZ, P]
         L.pgk_knn_fallback_rows.argtypes = [P, P, P]
+        L.pgk_knn_work.argtypes = [P, I64, I64, I64, I64, I, P, P]
         for f in ("pgk_device_check", "pgk_prune_batch", "pgk_prune_rows", "pgk_prune_rows_ex",
                   "pgk_make_u8", "pgk_add_reverse_and_prune_ex", "pgk_reverse_workspace",
                   "pgk_add_reverse_and_prune", "pgk_detect_u8", "pgk_knn_workspace",
-                  "pgk_knn_pools", "pgk_knn_fallback_rows"):
+                  "pgk_knn_pools", "pgk_knn_fallback_rows", "pgk_knn_work"):
             getattr(L, f).restype = I
         _lib = L
     return _lib
@@ -62,7 +63,7 @@ def lib():
 EXPORTS = ("pgk_version", "pgk_last_error", "pgk_device_check", "pgk_prune_batch",
            "pgk_prune_rows", "pgk_prune_rows_ex", "pgk_make_u8", "pgk_add_reverse_and_prune_ex",
            "pgk_reverse_workspace", "pgk_add_reverse_and_prune", "pgk_detect_u8",
-           "pgk_knn_workspace", "pgk_knn_pools", "pgk_knn_fallback_rows",
+           "pgk_knn_workspace", "pgk_knn_pools", "pgk_knn_fallback_rows", "pgk_knn_work",
            "pgk_launch_count")
 
 

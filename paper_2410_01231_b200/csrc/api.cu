@@ -43,6 +43,8 @@ int knn_pools(const float *, int64_t, int64_t, const float *, int64_t, int64_t, 
               int32_t *, int32_t *, float *, void *, size_t, cudaStream_t);
 int detect_u8(const float *, int64_t, int64_t, int *, void *, size_t, cudaStream_t);
 int fallback_rows(const void *, int *, cudaStream_t);
+int knn_work(const void *, int64_t, int64_t, int64_t, int64_t, int, unsigned long long *,
+             cudaStream_t);
 
 }  // namespace pgk
 
@@ -178,6 +180,13 @@ int pgk_knn_pools(const float *data, int64_t n, int64_t d, const float *queries,
   PGK_REQUIRE(data && pool_ids && pool_dists && ws, "NULL argument");
   return knn_pools(data, n, d, queries, nq, k, exclude_self, mode, gt_ids, pool_ids,
                    pool_dists, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int pgk_knn_work(const void *ws, int64_t n, int64_t nq, int64_t d, int64_t k, int mode,
+                 uint64_t *work_host, void *stream) {
+  PGK_REQUIRE(ws && work_host, "NULL argument");
+  return knn_work(ws, n, nq <= 0 ? n : nq, d, k, mode,
+                  reinterpret_cast<unsigned long long *>(work_host), (cudaStream_t)stream);
 }
 
 int pgk_knn_fallback_rows(const void *ws, int *rows_host, void *stream) {

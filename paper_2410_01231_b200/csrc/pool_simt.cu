@@ -494,6 +494,20 @@ int knn_workspace(int64_t n, int64_t nq, int64_t d, int64_t k, int mode, size_t 
   return PGK_OK;
 }
 
+int tiles_work(const void *tws, int64_t n, int64_t d, unsigned long long out[4],
+               cudaStream_t stream);
+
+// Executed 128x128 tensor-core tile pairs of the last pool call on `ws`
+// (0 when the SIMT path ran): brute force = ceil(nq/128) * ceil(n/128);
+// pruned = pass 1 + pass 2 + center assignment.
+int knn_work(const void *ws, int64_t n, int64_t nq, int64_t d, int64_t k, int mode,
+             unsigned long long out[4], cudaStream_t stream) {
+  KnnLayout L = knn_layout(const_cast<void *>(ws), ~size_t(0), n, nq, d, k, mode);
+  out[0] = out[1] = out[2] = out[3] = 0;
+  if (L.tws) return tiles_work(L.tws, n, d, out, stream);
+  return PGK_OK;
+}
+
 int fallback_rows(const void *ws, int *rows_host, cudaStream_t stream) {
   // fb_count sits right after the 4-int flag block (see knn_layout)
   Carve c(const_cast<void *>(ws), ~size_t(0));

@@ -191,7 +191,8 @@ __global__ void __launch_bounds__(256)
 constexpr int NEAR = 8;
 __global__ void tile_nearest_kernel(const float *__restrict__ dc, const int32_t *__restrict__ size,
                                     int64_t T, int32_t *__restrict__ lists,
-                                    int32_t *__restrict__ lens) {
+                                    int32_t *__restrict__ lens,
+                                    unsigned long long *__restrict__ total) {
   __shared__ uint64_t sk[8][256];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t Q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; Q < T;
@@ -219,7 +220,10 @@ __global__ void tile_nearest_kernel(const float *__restrict__ dc, const int32_t 
     int m = 0;
     for (int i = 0; i < NEAR; ++i) m += sk[w][i] != KEY_MAX;
     if (lane < m) lists[Q * T + lane] = (int32_t)(uint32_t)sk[w][lane];
-    if (lane == 0) lens[Q] = m;
+    if (lane == 0) {
+      lens[Q] = m;
+      atomicAdd(total, (unsigned long long)m);
+    }
     __syncwarp();
   }
 }
@@ -395,12 +399,12 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   PGK_CHECK_LAUNCH("fill_i32_kernel");
   tile_stats_kernel<<<g, 256, 0, stream>>>(L.xs, L.perm, d, T, L.cent, L.rad, L.size);
   PGK_CHECK_LAUNCH("tile_stats_kernel");
-  PGK_CUDA(cudaMemsetAsync(L.total, 0, sizeof(unsigned long long), stream));
+  PGK_CUDA(cudaMemsetAsync(L.total, 0, 4 * sizeof(unsigned long long), stream));
   tile_dist_kernel<<<dim3((unsigned)((T + DB - 1) / DB), (unsigned)((T + DB - 1) / DB)), 256, 0,
                      stream>>>(L.cent, T, d, L.dcm);
   PGK_CHECK_LAUNCH("tile_dist_kernel");
   // 4. pass 1: exact top-K over each query tile's NEAR nearest tiles -> U_Q
-  tile_nearest_kernel<<<g, 256, 0, stream>>>(L.dcm, L.size, T, L.lists, L.lens);
+  tile_nearest_kernel<<<g, 256, 0, stream>>>(L.dcm, L.size, T, L.lists, L.lens, L.total + 1);
   PGK_CHECK_LAUNCH("tile_nearest_kernel");
   rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes, stream,
                                L.xs, L.lists, L.lens, T, L.perm, handled);
@@ -415,6 +419,11 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes, stream,
                                L.xs, L.lists, L.lens, T, L.perm, handled, keys);
   if (rc) return rc;
+  {  // work record: [0] pass-2 tile pairs, [1] pass-1 pairs, [2] assignment pairs, [3] done
+    const unsigned long long rec[2] = {
+        (unsigned long long)((n + TB - 1) / TB) * (unsigned long long)((C + TB - 1) / TB), 1ull};
+    PGK_CUDA(cudaMemcpyAsync(L.total + 2, rec, sizeof(rec), cudaMemcpyHostToDevice, stream));
+  }
   const char *se = getenv("PGK_TILES_STATS");
   if (se && se[0] == '1') {
     unsigned long long tot = 0;
@@ -445,11 +454,14 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   return PGK_OK;
 }
 
-// Device counter of candidate tile pairs of the last pruned launch on `tws`.
-int tiles_pairs(const void *tws, size_t tws_bytes, int64_t n, int64_t d,
-                unsigned long long *host, cudaStream_t stream) {
-  tiles::Layout L = tiles_layout(const_cast<void *>(tws), tws_bytes, n, d);
-  PGK_CUDA(cudaMemcpyAsync(host, L.total, sizeof(*host), cudaMemcpyDeviceToHost, stream));
+// Work record of the last pruned launch on `tws` (blocking read):
+// out[0] pass-2 tile pairs, out[1] pass-1, out[2] assignment, out[3] = 1 if
+// the pruned path ran.
+int tiles_work(const void *tws, int64_t n, int64_t d, unsigned long long out[4],
+               cudaStream_t stream) {
+  tiles::Layout L = tiles_layout(const_cast<void *>(tws), ~size_t(0), n, d);
+  PGK_CUDA(cudaMemcpyAsync(out, L.total, 4 * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, stream));
   PGK_CUDA(cudaStreamSynchronize(stream));
   return PGK_OK;
 }

@@ -154,6 +154,15 @@ def knn_pools(X: torch.Tensor, k: int, queries=None, exclude_self: bool = True,
     return PoolResult(pool_ids, pool_dists, gt, ws)
 
 
+def knn_work(ws: torch.Tensor, n: int, nq: int, d: int, k: int, mode: int):
+    """(pass-2, pass-1, assignment) 128x128 tile pairs executed by the last
+    pruned pool call on ``ws`` and whether the pruned path ran (blocking)."""
+    out = (ctypes.c_uint64 * 4)()
+    check(_lib.lib().pgk_knn_work(ptr(ws), int(n), int(nq), int(d), int(k), int(mode), out,
+                                  _lib.stream_handle()))
+    return int(out[0]), int(out[1]), int(out[2]), bool(out[3])
+
+
 def fallback_rows(ws: torch.Tensor) -> int:
     """Rows of the last knn_pools call on ``ws`` that needed the exact
     float64 rescan (blocking)."""
