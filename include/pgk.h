@@ -82,12 +82,15 @@ int pgk_prune_rows(const float *data, int64_t n, int64_t d, int64_t n_rows,
  * so the kernels may compute it as |w|^2 + |v|^2 - 2 w.v on a u8 copy of the
  * rows: bit-identical results, 4x fewer bytes.  pgk_make_u8 builds that copy
  * (rows of 128 bytes, zero padded; int32 squared norms).  data_u8 == NULL
- * selects the fp32 path (then these equal pgk_prune_rows). */
+ * selects the fp32 path (then these equal pgk_prune_rows).  row_order
+ * (optional, a permutation of 0..n_rows-1) is only the processing order --
+ * e.g. pgk_knn_order's locality order; results do not depend on it. */
 int pgk_make_u8(const float *data, int64_t n, int64_t d, uint8_t *out_u8,
                 int32_t *out_norms, void *stream);
 int pgk_prune_rows_ex(const float *data, const uint8_t *data_u8,
                       const int32_t *norms_u8, int64_t n, int64_t d, int64_t n_rows,
-                      const int32_t *row_node, const int64_t *cand_off,
+                      const int32_t *row_node, const int32_t *row_order,
+                      const int64_t *cand_off,
                       const int32_t *cand_counts, const int32_t *cand_ids,
                       const float *cand_dists, int strategy, double cos_alpha,
                       int64_t M, int64_t width, int32_t *out_ids, float *out_dists,
@@ -112,7 +115,8 @@ int pgk_add_reverse_and_prune(const float *data, int64_t n, int64_t d,
                               void *ws, size_t ws_bytes, void *stream);
 /* exact-integer variant (see pgk_prune_rows_ex) */
 int pgk_add_reverse_and_prune_ex(const float *data, const uint8_t *data_u8,
-                                 const int32_t *norms_u8, int64_t n, int64_t d,
+                                 const int32_t *norms_u8, const int32_t *row_order,
+                                 int64_t n, int64_t d,
                                  const int32_t *a_ids, const float *a_dists,
                                  const int32_t *a_counts, int64_t a_width,
                                  int strategy, double cos_alpha, int64_t M,
@@ -155,6 +159,13 @@ int pgk_knn_fallback_rows(const void *ws, int *rows_host, void *stream);
  * path ran (all zero otherwise: the brute-force kernels ran). */
 int pgk_knn_work(const void *ws, int64_t n, int64_t nq, int64_t d, int64_t k,
                  int mode, uint64_t *work_host, void *stream);
+
+/* A locality-friendly processing order (permutation of 0..n-1, written to
+ * `order`, device int32[n]) for the selection passes: the exact-pruned pool's
+ * spatial tile order, identity when the pruned path did not run.  Enqueued
+ * on the stream, no host sync. */
+int pgk_knn_order(const void *ws, int64_t n, int64_t d, int64_t k, int mode,
+                  int32_t *order, void *stream);
 
 /* Cumulative number of kernel launches this library has issued since it was
  * loaded (process-wide; the bench reports the difference around its timed

@@ -28,12 +28,14 @@ int num_sms() {
 }
 
 int launch_prune(const float *, const uint8_t *, const int32_t *, int64_t, int64_t,
-                 const int32_t *, const int64_t *, const int32_t *, const int32_t *,
+                 const int32_t *, const int32_t *, const int64_t *, const int32_t *,
+                 const int32_t *,
                  const float *, int, double, int64_t, int64_t, int32_t *, float *, int32_t *,
                  int64_t *, int64_t *, cudaStream_t);
 int make_u8(const float *, int64_t, int64_t, uint8_t *, int32_t *, cudaStream_t);
 int reverse_workspace(int64_t n, int64_t width, size_t *bytes);
-int add_reverse_and_prune(const float *, const uint8_t *, const int32_t *, int64_t, int64_t,
+int add_reverse_and_prune(const float *, const uint8_t *, const int32_t *, const int32_t *,
+                          int64_t, int64_t,
                           const int32_t *, const float *,
                           const int32_t *, int64_t, int, double, int64_t, int64_t,
                           int32_t *, float *, int32_t *, int64_t *, int64_t *, void *,
@@ -45,6 +47,7 @@ int detect_u8(const float *, int64_t, int64_t, int *, void *, size_t, cudaStream
 int fallback_rows(const void *, int *, cudaStream_t);
 int knn_work(const void *, int64_t, int64_t, int64_t, int64_t, int, unsigned long long *,
              cudaStream_t);
+int knn_order(const void *, int64_t, int64_t, int64_t, int64_t, int, int32_t *, cudaStream_t);
 
 }  // namespace pgk
 
@@ -88,8 +91,8 @@ int pgk_prune_batch(const float *data, int64_t n, int64_t d, const int64_t *cand
                     int64_t *dist_evals, int64_t *angle_evals, void *stream) {
   int rc = check_prune_args(data, n, d, strategy, M, width);
   if (rc) return rc;
-  return launch_prune(data, nullptr, nullptr, n, d, nullptr, cand_off, cand_counts, cand_ids,
-                      cand_dists, strategy,
+  return launch_prune(data, nullptr, nullptr, n, d, nullptr, nullptr, cand_off, cand_counts,
+                      cand_ids, cand_dists, strategy,
                       cos_alpha, M, width, out_ids, out_dists, out_counts, dist_evals,
                       angle_evals, (cudaStream_t)stream);
 }
@@ -100,13 +103,14 @@ int pgk_prune_rows(const float *data, int64_t n, int64_t d, int64_t n_rows,
                    const float *cand_dists, int strategy, double cos_alpha, int64_t M,
                    int64_t width, int32_t *out_ids, float *out_dists, int32_t *out_counts,
                    int64_t *dist_evals, int64_t *angle_evals, void *stream) {
-  return pgk_prune_rows_ex(data, nullptr, nullptr, n, d, n_rows, row_node, cand_off,
+  return pgk_prune_rows_ex(data, nullptr, nullptr, n, d, n_rows, row_node, nullptr, cand_off,
                            cand_counts, cand_ids, cand_dists, strategy, cos_alpha, M, width,
                            out_ids, out_dists, out_counts, dist_evals, angle_evals, stream);
 }
 
 int pgk_prune_rows_ex(const float *data, const uint8_t *data_u8, const int32_t *norms_u8,
                       int64_t n, int64_t d, int64_t n_rows, const int32_t *row_node,
+                      const int32_t *row_order,
                       const int64_t *cand_off, const int32_t *cand_counts,
                       const int32_t *cand_ids, const float *cand_dists, int strategy,
                       double cos_alpha, int64_t M, int64_t width, int32_t *out_ids,
@@ -116,9 +120,9 @@ int pgk_prune_rows_ex(const float *data, const uint8_t *data_u8, const int32_t *
   if (rc) return rc;
   PGK_REQUIRE(n_rows >= 0, "n_rows must be >= 0");
   PGK_REQUIRE(!data_u8 || (norms_u8 && d <= 128), "u8 rows need norms and d <= 128");
-  return launch_prune(data, data_u8, norms_u8, n_rows, d, row_node, cand_off, cand_counts,
-                      cand_ids, cand_dists, strategy, cos_alpha, M, width, out_ids, out_dists,
-                      out_counts, dist_evals, angle_evals, (cudaStream_t)stream);
+  return launch_prune(data, data_u8, norms_u8, n_rows, d, row_node, row_order, cand_off,
+                      cand_counts, cand_ids, cand_dists, strategy, cos_alpha, M, width, out_ids,
+                      out_dists, out_counts, dist_evals, angle_evals, (cudaStream_t)stream);
 }
 
 int pgk_make_u8(const float *data, int64_t n, int64_t d, uint8_t *out_u8, int32_t *out_norms,
@@ -139,14 +143,16 @@ int pgk_add_reverse_and_prune(const float *data, int64_t n, int64_t d, const int
                               int32_t *out_counts, int64_t *dist_evals,
                               int64_t *angle_evals, void *ws, size_t ws_bytes,
                               void *stream) {
-  return pgk_add_reverse_and_prune_ex(data, nullptr, nullptr, n, d, a_ids, a_dists, a_counts,
+  return pgk_add_reverse_and_prune_ex(data, nullptr, nullptr, nullptr, n, d, a_ids, a_dists,
+                                      a_counts,
                                       a_width, strategy, cos_alpha, M, out_width, out_ids,
                                       out_dists, out_counts, dist_evals, angle_evals, ws,
                                       ws_bytes, stream);
 }
 
 int pgk_add_reverse_and_prune_ex(const float *data, const uint8_t *data_u8,
-                                 const int32_t *norms_u8, int64_t n, int64_t d,
+                                 const int32_t *norms_u8, const int32_t *row_order,
+                                 int64_t n, int64_t d,
                                  const int32_t *a_ids, const float *a_dists,
                                  const int32_t *a_counts, int64_t a_width, int strategy,
                                  double cos_alpha, int64_t M, int64_t out_width,
@@ -157,7 +163,8 @@ int pgk_add_reverse_and_prune_ex(const float *data, const uint8_t *data_u8,
   if (rc) return rc;
   PGK_REQUIRE(a_width >= 1, "phase-A width must be >= 1");
   PGK_REQUIRE(!data_u8 || (norms_u8 && d <= 128), "u8 rows need norms and d <= 128");
-  return add_reverse_and_prune(data, data_u8, norms_u8, n, d, a_ids, a_dists, a_counts, a_width,
+  return add_reverse_and_prune(data, data_u8, norms_u8, row_order, n, d, a_ids, a_dists,
+                               a_counts, a_width,
                                strategy, cos_alpha, M, out_width, out_ids, out_dists, out_counts,
                                dist_evals, angle_evals, ws, ws_bytes, (cudaStream_t)stream);
 }
@@ -187,6 +194,12 @@ int pgk_knn_work(const void *ws, int64_t n, int64_t nq, int64_t d, int64_t k, in
   PGK_REQUIRE(ws && work_host, "NULL argument");
   return knn_work(ws, n, nq <= 0 ? n : nq, d, k, mode,
                   reinterpret_cast<unsigned long long *>(work_host), (cudaStream_t)stream);
+}
+
+int pgk_knn_order(const void *ws, int64_t n, int64_t d, int64_t k, int mode, int32_t *order,
+                  void *stream) {
+  PGK_REQUIRE(ws && order, "NULL argument");
+  return knn_order(ws, n, n, d, k, mode, order, (cudaStream_t)stream);
 }
 
 int pgk_knn_fallback_rows(const void *ws, int *rows_host, void *stream) {

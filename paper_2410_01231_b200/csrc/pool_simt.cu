@@ -456,6 +456,7 @@ struct KnnLayout {
 size_t tc_pool_workspace(int64_t n, int64_t nq, bool self);
 bool tc_pool_supported(int64_t d, int64_t k);
 size_t tiles_workspace(int64_t n, int64_t d);
+int64_t tiles_rows(int64_t n);
 bool tiles_supported(int64_t n, int64_t d, int64_t k);
 
 int pool_S(int64_t k, int mode) {
@@ -478,9 +479,11 @@ static KnnLayout knn_layout(void *ws, size_t bytes, int64_t n, int64_t nq, int64
   L.tc_bytes = L.tws_bytes = 0;
   L.tc_ws = L.tws = nullptr;
   if (mode != PGK_POOL_F32 && tc_pool_supported(d, k)) {
-    L.tc_bytes = tc_pool_workspace(n, nq, false);
+    const bool tiles = nq == n && tiles_supported(n, d, k);
+    const int64_t rows = tiles ? std::max(nq, tiles_rows(n)) : nq;
+    L.tc_bytes = tc_pool_workspace(tiles ? rows : n, rows, false);
     L.tc_ws = c.take<char>(L.tc_bytes);
-    if (nq == n && tiles_supported(n, d, k)) {
+    if (tiles) {
       L.tws_bytes = tiles_workspace(n, d);
       L.tws = c.take<char>(L.tws_bytes);
     }
@@ -505,6 +508,25 @@ int knn_work(const void *ws, int64_t n, int64_t nq, int64_t d, int64_t k, int mo
   KnnLayout L = knn_layout(const_cast<void *>(ws), ~size_t(0), n, nq, d, k, mode);
   out[0] = out[1] = out[2] = out[3] = 0;
   if (L.tws) return tiles_work(L.tws, n, d, out, stream);
+  return PGK_OK;
+}
+
+int tiles_order(void *tws, int64_t n, int64_t d, int32_t *out, cudaStream_t stream);
+
+__global__ void iota_kernel(int32_t *__restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)i;
+}
+
+// A locality-friendly processing order of the data rows (a permutation of
+// 0..n-1): the pruned pool's tile order, identity otherwise.  No host sync.
+int knn_order(const void *ws, int64_t n, int64_t nq, int64_t d, int64_t k, int mode,
+              int32_t *out, cudaStream_t stream) {
+  KnnLayout L = knn_layout(const_cast<void *>(ws), ~size_t(0), n, nq, d, k, mode);
+  if (L.tws) return tiles_order(L.tws, n, d, out, stream);
+  iota_kernel<<<(unsigned)num_sms() * 4, 256, 0, stream>>>(out, n);
+  PGK_CHECK_LAUNCH("iota_kernel");
   return PGK_OK;
 }
 
@@ -562,7 +584,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             cudaStream_t stream, const uint8_t *xs_sorted,
                             const int32_t *tlist, const int32_t *tlen, int64_t tstride,
                             const int32_t *perm, bool *handled,
-                            const uint64_t *init_keys = nullptr);
+                            const uint64_t *init_keys = nullptr, int kth_only = 0);
 int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm, int K,
                          uint64_t *keys, void *tc_ws, size_t tc_bytes, void *tws,
                          size_t tws_bytes, cudaStream_t stream, bool *handled,

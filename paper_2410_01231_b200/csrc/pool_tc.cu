@@ -33,7 +33,7 @@ constexpr int BN = 128;   // data points per tile == MMA N
 constexpr int KB = 128;   // bytes per (padded) row
 constexpr int STAGES = 4;
 constexpr int TILE_BYTES = BN * KB;
-constexpr int CAP = 512;  // per-row candidate buffer (keys)
+constexpr int CAP = 1024;  // per-row candidate buffer (keys, global memory)
 constexpr int THREADS = 256;
 constexpr int TMEM_COLS = 256;
 
@@ -42,6 +42,7 @@ struct __align__(1024) Smem {
   uint8_t b[STAGES][TILE_BYTES];
   int32_t sv[4][32 * 36];  // per epilogue warp: one chunk of s values per lane
   alignas(16) int32_t ny[2][BN];  // |x|^2 of the tile in each accumulator stage
+  alignas(16) int32_t pid[2][BN];  // original ids of the tile's columns (pruned path)
   uint64_t full[STAGES], empty[STAGES];
   uint64_t tfull[2], tempty[2];
   uint64_t a_full, a_empty;
@@ -162,9 +163,10 @@ __device__ __forceinline__ int warp_sum(int v) {
 // and return the K-th smallest key.  Binary searches over the register-
 // resident keys (distance within [min, max], then id among distance ties;
 // REDUX warp sums); no sort.
-constexpr int KPL = CAP / 32;  // keys per lane
-__device__ __noinline__ uint64_t select_k(uint64_t *buf, int cnt, int K, uint32_t hi_bound,
-                                          int lane) {
+template <int KPL>
+__device__ __noinline__ uint64_t select_kt(uint64_t *buf, int cnt, int K, uint32_t hi_bound,
+                                           int lane) {
+  static_assert(KPL <= 32, "selection holds the whole buffer in registers");
   uint64_t kk[KPL];
   uint32_t dmin = 0xffffffffu, dmax = 0;
 #pragma unroll
@@ -228,6 +230,14 @@ __device__ __noinline__ uint64_t select_k(uint64_t *buf, int cnt, int K, uint32_
   }
   __syncwarp();
   return tau;
+}
+
+// cnt <= 32*KPL keys per call
+__device__ __forceinline__ uint64_t select_k(uint64_t *buf, int cnt, int K, uint32_t hi_bound,
+                                             int lane) {
+  if (cnt <= 256) return select_kt<8>(buf, cnt, K, hi_bound, lane);
+  if (cnt <= 512) return select_kt<16>(buf, cnt, K, hi_bound, lane);
+  return select_kt<CAP / 32>(buf, cnt, K, hi_bound, lane);
 }
 
 // Register bitonic sort of 32*NPL keys (element i = slot*32 + lane).
@@ -302,7 +312,8 @@ __global__ void __launch_bounds__(THREADS, 2)
                       uint64_t *__restrict__ out_keys, unsigned long long *stats,
                       const int32_t *__restrict__ tlist, const int32_t *__restrict__ tlen,
                       int64_t tstride, const int32_t *__restrict__ perm,
-                      const uint64_t *__restrict__ init_keys) {
+                      const uint64_t *__restrict__ init_keys, int32_t *__restrict__ row_cnt,
+                      uint64_t *__restrict__ row_tau) {
   unsigned long long st[ST_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t_prev = STATS ? clock64() : 0;
 #define PGK_TICK(slot)                          \
@@ -382,8 +393,9 @@ __global__ void __launch_bounds__(THREADS, 2)
           mbar_wait(&s.tempty[acc], acc_phase ^ 1);
           // the tile's |x|^2 (xnorm is padded to a multiple of BN) lands with the
           // accumulator: tfull completes on the commit AND these bytes
-          mbar_expect_tx_only(&s.tfull[acc], BN * 4);
+          mbar_expect_tx_only(&s.tfull[acc], perm ? BN * 8 : BN * 4);
           bulk_load(s.ny[acc], xnorm + (int64_t)tid * BN, BN * 4, &s.tfull[acc]);
+          if (perm) bulk_load(s.pid[acc], perm + (int64_t)tid * BN, BN * 4, &s.tfull[acc]);
           mbar_wait(&s.full[stage], phase);
           tc_fence_after();
           const uint64_t bdesc = sw128_desc(s.b[stage]);
@@ -402,13 +414,14 @@ __global__ void __launch_bounds__(THREADS, 2)
     // ---------------- epilogue ----------------
     const int q = warp - 4;  // TMEM lane quarter (warp % 4)
     int32_t *sv = s.sv[q] + lane * 36;
-    uint64_t *wbuf = bufs + ((size_t)blockIdx.x * BM + q * 32) * CAP;  // this warp's rows
-    uint64_t *mybuf = wbuf + (size_t)lane * CAP;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int b = blockIdx.x; b < nblocks; b += gridDim.x) {
       const int64_t row = (int64_t)b * BM + q * 32 + lane;
       const bool row_ok = row < nq && (!perm || perm[row] >= 0);  // padding rows: no pool
+      // per-row candidate buffers (global memory, CAP keys per row)
+      uint64_t *wbuf = bufs + ((int64_t)b * BM + q * 32) * CAP;  // this warp's rows
+      uint64_t *mybuf = wbuf + (size_t)lane * CAP;
       const int nx = row_ok ? qnorm[row] : 0;
       int cnt = 0;
       uint64_t tau = KEY_MAX;
@@ -471,7 +484,7 @@ __global__ void __launch_bounds__(THREADS, 2)
                 const int sj = sv[j];
                 const int64_t col = cb + j;
                 if (sj <= tp && col < n && !(exclude_self && col == row)) {
-                  const uint32_t cid = perm ? (uint32_t)perm[col] : (uint32_t)col;
+                  const uint32_t cid = perm ? (uint32_t)s.pid[acc][c * 32 + j] : (uint32_t)col;
                   const uint64_t key = ((uint64_t)(uint32_t)(sj + nx) << 32) | cid;
                   if (key < tau) {
                     tau = key;
@@ -506,7 +519,7 @@ __global__ void __launch_bounds__(THREADS, 2)
               const int sj = sv[j];
               const int64_t col = cb + j;
               if (sj <= tp && col < n && !(exclude_self && col == row)) {
-                const uint32_t cid = perm ? (uint32_t)perm[col] : (uint32_t)col;
+                const uint32_t cid = perm ? (uint32_t)s.pid[acc][c * 32 + j] : (uint32_t)col;
                 const uint64_t key = ((uint64_t)(uint32_t)(sj + nx) << 32) | cid;
                 if (key < tau) mybuf[cnt++] = key;
               }
@@ -522,31 +535,12 @@ __global__ void __launch_bounds__(THREADS, 2)
         if (lane == 0) mbar_arrive(&s.tempty[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
-      // block done: emit every row's best K (sorted), reset for the next block
+      // block done: record each row's buffer fill and threshold; selection
+      // and sorting run in the massively parallel finalize kernel
       PGK_TICK(ST_MAIN);
-      __syncwarp();
-      if (K == 1) {
-        if (row_ok)
-          out_keys[perm ? (int64_t)perm[row] : row] =
-              tau == KEY_MAX ? KEY_MAX : pack_key((float)khi(tau), (int32_t)(uint32_t)tau);
-      }
-      for (int src = 0; K > 1 && src < 32; ++src) {
-        const int64_t r_src = (int64_t)b * BM + q * 32 + src;
-        if (r_src >= nq) break;
-        if (perm && perm[r_src] < 0) continue;
-        int c_src = __shfl_sync(0xffffffffu, cnt, src);
-        const uint64_t t_src = __shfl_sync(0xffffffffu, tau, src);
-        uint64_t *bsrc = wbuf + (size_t)src * CAP;
-        if (c_src > K) {
-          select_k(bsrc, c_src, K, t_src == KEY_MAX ? (1u << 25) : khi(t_src), lane);
-          c_src = K;
-        }
-        uint64_t *o = out_keys + (perm ? (int64_t)perm[r_src] : r_src) * K;
-        if (K <= 32) emit_sorted<1>(bsrc, c_src, K, o, lane);
-        else if (K <= 64) emit_sorted<2>(bsrc, c_src, K, o, lane);
-        else if (K <= 128) emit_sorted<4>(bsrc, c_src, K, o, lane);
-        else emit_sorted<8>(bsrc, c_src, K, o, lane);
-        __syncwarp();
+      if (row < nq) {
+        row_cnt[row] = row_ok ? cnt : -1;
+        row_tau[row] = tau;
       }
       PGK_TICK(ST_FINAL);
     }
@@ -568,6 +562,60 @@ __global__ void __launch_bounds__(THREADS, 2)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "n"(TMEM_COLS));
+  }
+}
+
+// Warp per (sorted) row: cut the row's buffer to its K best keys (selection
+// only when it holds more), then either the sorted K (FULL) or only the K-th
+// key (KTH, the pass-1 bound) in the library key format at the original row.
+template <int NPL>
+__device__ __forceinline__ void finalize_row(uint64_t *buf, int cnt, uint64_t tau, int K,
+                                             bool kth_only, uint64_t *out, int lane) {
+  if (K == 1) {
+    if (lane == 0)
+      out[0] = tau == KEY_MAX ? KEY_MAX : pack_key((float)khi(tau), (int32_t)(uint32_t)tau);
+    return;
+  }
+  uint64_t kth = KEY_MAX;
+  if (cnt > K) {
+    kth = select_k(buf, cnt, K, tau == KEY_MAX ? (1u << 25) : khi(tau), lane);
+    cnt = K;
+  }
+  if (kth_only && cnt == K && kth != KEY_MAX) {
+    if (lane == 0) out[K - 1] = pack_key((float)khi(kth), (int32_t)(uint32_t)kth);
+    return;
+  }
+  uint64_t e[NPL];
+#pragma unroll
+  for (int s0 = 0; s0 < NPL; ++s0) {
+    const int idx = s0 * 32 + lane;
+    e[s0] = idx < cnt ? buf[idx] : KEY_MAX;
+  }
+  reg_bitonic<NPL>(e, lane);
+#pragma unroll
+  for (int s0 = 0; s0 < NPL; ++s0) {
+    const int idx = s0 * 32 + lane;
+    if (idx < K && (!kth_only || idx == K - 1))
+      out[idx] = e[s0] == KEY_MAX ? KEY_MAX : pack_key((float)khi(e[s0]), (int32_t)(uint32_t)e[s0]);
+  }
+}
+
+__global__ void tc_finalize_kernel(uint64_t *__restrict__ bufs, const int32_t *__restrict__ row_cnt,
+                                   const uint64_t *__restrict__ row_tau, int64_t nrows, int K,
+                                   const int32_t *__restrict__ perm, int kth_only,
+                                   uint64_t *__restrict__ out_keys) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < nrows;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int cnt = row_cnt[r];
+    if (cnt < 0) continue;  // padding row
+    uint64_t *o = out_keys + (perm ? (int64_t)perm[r] : r) * K;
+    uint64_t *b = bufs + r * CAP;
+    const uint64_t tau = row_tau[r];
+    if (K <= 32) finalize_row<1>(b, cnt, tau, K, kth_only, o, lane);
+    else if (K <= 64) finalize_row<2>(b, cnt, tau, K, kth_only, o, lane);
+    else if (K <= 128) finalize_row<4>(b, cnt, tau, K, kth_only, o, lane);
+    else finalize_row<8>(b, cnt, tau, K, kth_only, o, lane);
   }
 }
 
@@ -615,12 +663,15 @@ size_t tc_pool_workspace(int64_t n, int64_t nq, bool self) {
   const int sms = num_sms();
   size_t b = (size_t)n * tc::KB + 1024;
   if (!self) b += (size_t)nq * tc::KB + 1024;
-  b += (size_t)2 * sms * tc::BM * tc::CAP * sizeof(uint64_t) + 1024;
+  const int64_t rows = (nq + tc::BM - 1) / tc::BM * tc::BM;
+  b += (size_t)rows * tc::CAP * sizeof(uint64_t) + 1024;  // per-row candidate buffers
+  b += (size_t)rows * (sizeof(int32_t) + sizeof(uint64_t)) + 2048;
   return b;
 }
 
 bool tc_pool_supported(int64_t d, int64_t k) {
   static_assert(tc::CAP >= 256 + 32, "CAP must leave room for K <= 256 plus one chunk");
+  static_assert(tc::CAP <= 1024, "select_k holds CAP keys in registers");
   static int env = -1;
   if (env < 0) {
     const char *e = getenv("PGK_DISABLE_TC");
@@ -634,7 +685,8 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             int K, uint64_t *keys, void *tc_ws, size_t tc_bytes,
                             cudaStream_t stream, const uint8_t *xs_sorted,
                             const int32_t *tlist, const int32_t *tlen, int64_t tstride,
-                            const int32_t *perm, bool *handled, const uint64_t *init_keys) {
+                            const int32_t *perm, bool *handled, const uint64_t *init_keys,
+                            int kth_only) {
   *handled = false;
   if (!tc_pool_supported(d, K)) return PGK_OK;
   const bool self = (Q == X);
@@ -646,7 +698,10 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   uint8_t *xu8 = c.take<uint8_t>((size_t)n * tc::KB);
   uint8_t *qu8 = self ? xu8 : c.take<uint8_t>((size_t)nq * tc::KB);
   const int sms = num_sms();
-  uint64_t *bufs = c.take<uint64_t>((size_t)2 * sms * tc::BM * tc::CAP);
+  const int64_t rows = (nq + tc::BM - 1) / tc::BM * tc::BM;
+  uint64_t *bufs = c.take<uint64_t>((size_t)rows * tc::CAP);
+  int32_t *row_cnt = c.take<int32_t>(rows);
+  uint64_t *row_tau = c.take<uint64_t>(rows);
   const unsigned cg = (unsigned)std::min<int64_t>((n * tc::KB + 255) / 256, (int64_t)sms * 16);
   if (xs_sorted) {
     xu8 = qu8 = const_cast<uint8_t *>(xs_sorted);  // already u8, permuted by the tile sort
@@ -686,7 +741,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
     PGK_CUDA(cudaMemsetAsync(dstats, 0, sizeof(unsigned long long) * tc::ST_COUNT, stream));
     tc::tc_pool_u8_kernel<true><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, dstats, tlist, tlen,
-        tstride, perm, init_keys);
+        tstride, perm, init_keys, row_cnt, row_tau);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel<stats>");
     unsigned long long h[tc::ST_COUNT];
     PGK_CUDA(cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, stream));
@@ -701,9 +756,12 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   } else {
     tc::tc_pool_u8_kernel<false><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
-        tstride, perm, init_keys);
+        tstride, perm, init_keys, row_cnt, row_tau);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel");
   }
+  tc::tc_finalize_kernel<<<(unsigned)sms * 16, 256, 0, stream>>>(bufs, row_cnt, row_tau, nq, K,
+                                                                  perm, kth_only, keys);
+  PGK_CHECK_LAUNCH("tc_finalize_kernel");
   *handled = true;
   return PGK_OK;
 }

@@ -187,13 +187,15 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// pass-1 list: the NEAR nearest tiles of every query tile by centroid distance
-constexpr int NEAR = 8;
+// pass-1 list: the nearest tiles of every query tile by centroid distance,
+// as many as needed to hold >= P1_MULT * K points (at most NEAR tiles)
+constexpr int NEAR = 16;
+constexpr int P1_MULT = 4;
 __global__ void tile_nearest_kernel(const float *__restrict__ dc, const int32_t *__restrict__ size,
-                                    int64_t T, int32_t *__restrict__ lists,
+                                    int64_t T, int K, int32_t *__restrict__ lists,
                                     int32_t *__restrict__ lens,
                                     unsigned long long *__restrict__ total) {
-  __shared__ uint64_t sk[8][256];
+  __shared__ uint64_t sk[8][32 * NEAR];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t Q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; Q < T;
        Q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -217,8 +219,13 @@ __global__ void tile_nearest_kernel(const float *__restrict__ dc, const int32_t 
     for (int i = 0; i < NEAR; ++i) sk[w][i * 32 + lane] = best[i];
     __syncwarp();
     warp_bitonic_sort(sk[w], 32 * NEAR, lane);
-    int m = 0;
-    for (int i = 0; i < NEAR; ++i) m += sk[w][i] != KEY_MAX;
+    // prefix of tiles until they hold P1_MULT * K points
+    int m = 0, pts = 0;
+    for (int i = 0; i < NEAR && sk[w][i] != KEY_MAX; ++i) {
+      pts += size[(uint32_t)sk[w][i]];
+      m = i + 1;
+      if (pts >= P1_MULT * K) break;
+    }
     if (lane < m) lists[Q * T + lane] = (int32_t)(uint32_t)sk[w][lane];
     if (lane == 0) {
       lens[Q] = m;
@@ -302,7 +309,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             cudaStream_t stream, const uint8_t *xs_sorted,
                             const int32_t *tlist, const int32_t *tlen, int64_t tstride,
                             const int32_t *perm, bool *handled,
-                            const uint64_t *init_keys = nullptr);
+                            const uint64_t *init_keys = nullptr, int kth_only = 0);
 
 static tiles::Layout tiles_layout(void *ws, size_t bytes, int64_t n, int64_t d) {
   using namespace tiles;
@@ -349,6 +356,9 @@ bool tiles_supported(int64_t n, int64_t d, int64_t k) {
 }
 
 size_t tiles_workspace(int64_t n, int64_t d) { return tiles_layout(nullptr, 0, n, d).bytes; }
+
+// rows of the padded, tile-sorted problem (the tc workspace must cover them)
+int64_t tiles_rows(int64_t n) { return tiles_layout(nullptr, 0, n, 1).NPmax; }
 
 // Runs the whole pruned pool.  *handled = false when pruning does not apply.
 int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm, int K,
@@ -404,10 +414,10 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
                      stream>>>(L.cent, T, d, L.dcm);
   PGK_CHECK_LAUNCH("tile_dist_kernel");
   // 4. pass 1: exact top-K over each query tile's NEAR nearest tiles -> U_Q
-  tile_nearest_kernel<<<g, 256, 0, stream>>>(L.dcm, L.size, T, L.lists, L.lens, L.total + 1);
+  tile_nearest_kernel<<<g, 256, 0, stream>>>(L.dcm, L.size, T, K, L.lists, L.lens, L.total + 1);
   PGK_CHECK_LAUNCH("tile_nearest_kernel");
   rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes, stream,
-                               L.xs, L.lists, L.lens, T, L.perm, handled);
+                               L.xs, L.lists, L.lens, T, L.perm, handled, nullptr, 1);
   if (rc) return rc;
   if (!*handled) return PGK_OK;
   tile_ubound_kernel<<<g, 256, 0, stream>>>(keys, K, L.perm, T, L.U);
@@ -451,6 +461,67 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
             q(r2, 1.0), q(u2, .5), q(u2, .9));
   }
   if (pairs_out) *pairs_out = 0;
+  return PGK_OK;
+}
+
+// Locality order of the last pruned launch: the real rows of the tile
+// permutation, tile by tile (identity when the pruned path did not run).
+__global__ void order_scan_kernel(const int32_t *__restrict__ size, int64_t T,
+                                  int64_t *__restrict__ toff) {
+  // single block: per-thread serial chunk + block scan of chunk sums
+  __shared__ int64_t part[1024];
+  const int64_t per = (T + 1023) / 1024;
+  const int64_t lo = threadIdx.x * per, hi = min(T, lo + per);
+  int64_t sum = 0;
+  for (int64_t t = lo; t < hi; ++t) sum += size[t];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int64_t v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int64_t run = part[threadIdx.x] - sum;
+  for (int64_t t = lo; t < hi; ++t) {
+    toff[t] = run;
+    run += size[t];
+  }
+}
+
+__global__ void order_emit_kernel(const int32_t *__restrict__ perm, const int64_t *__restrict__ toff,
+                                  int64_t T, int64_t n,
+                                  const unsigned long long *__restrict__ work,
+                                  int32_t *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const bool pruned = work[3] != 0;
+  if (!pruned) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+      out[i] = (int32_t)i;
+    return;
+  }
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < T;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int64_t o = toff[t];
+    for (int r0 = 0; r0 < tiles::TB; r0 += 32) {
+      const int32_t v = perm[t * tiles::TB + r0 + lane];
+      const unsigned b = __ballot_sync(0xffffffffu, v >= 0);
+      if (v >= 0) out[o + __popc(b & lanemask_lt())] = v;
+      o += __popc(b);
+    }
+  }
+}
+
+int tiles_order(void *tws, int64_t n, int64_t d, int32_t *out, cudaStream_t stream) {
+  tiles::Layout L = tiles_layout(tws, ~size_t(0), n, d);
+  // toff reuses the assignment-key scratch (n >= T entries, free after the sort)
+  int64_t *toff = reinterpret_cast<int64_t *>(L.akeys);
+  order_scan_kernel<<<1, 1024, 0, stream>>>(L.size, L.Tmax, toff);
+  PGK_CHECK_LAUNCH("order_scan_kernel");
+  order_emit_kernel<<<(unsigned)num_sms() * 4, 256, 0, stream>>>(L.perm, toff, L.Tmax, n, L.total,
+                                                                out);
+  PGK_CHECK_LAUNCH("order_emit_kernel");
   return PGK_OK;
 }
 

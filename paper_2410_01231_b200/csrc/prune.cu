@@ -191,7 +191,7 @@ template <int MODE>
 __global__ void __launch_bounds__(PRUNE_WARPS * 32, 2)
     prune_kernel(const float *__restrict__ X, const uint8_t *__restrict__ xu8,
                  const int32_t *__restrict__ norms, int64_t n, int d,
-                 const int32_t *__restrict__ row_node,
+                 const int32_t *__restrict__ row_node, const int32_t *__restrict__ row_order,
                  const int64_t *__restrict__ cand_off,
                  const int32_t *__restrict__ cand_counts,
                  const int32_t *__restrict__ cand_ids,
@@ -210,8 +210,9 @@ __global__ void __launch_bounds__(PRUNE_WARPS * 32, 2)
   int16_t *s_alive = sm.alive[warp];
   float *stage = sm.stage[warp][0];
 
-  for (int64_t u = (int64_t)blockIdx.x * PRUNE_WARPS + warp; u < n;
-       u += (int64_t)gridDim.x * PRUNE_WARPS) {
+  for (int64_t i = (int64_t)blockIdx.x * PRUNE_WARPS + warp; i < n;
+       i += (int64_t)gridDim.x * PRUNE_WARPS) {
+    const int64_t u = row_order ? row_order[i] : i;
     const int64_t base = cand_off[u];
     const int cnt = cand_counts[u];
     const int32_t self = row_node ? row_node[u] : (int32_t)u;
@@ -294,9 +295,234 @@ __global__ void __launch_bounds__(PRUNE_WARPS * 32, 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Exact-integer selection with window-resident rows.  Same scan, rounds and
+// counters as prune_kernel, but a window of up to 128 candidates keeps its
+// u8 rows (128 B each) in shared memory for all rounds: one cp.async burst per
+// window instead of a global round trip per round.
+// ---------------------------------------------------------------------------
+constexpr int U8_WARPS = 10;
+constexpr int U8_W = 128;
+constexpr int U8_ROW = 144;  // padded row stride (36 words == 4 mod 32)
+
+struct PruneU8Smem {
+  int32_t id[U8_WARPS][U8_W];
+  float dist[U8_WARPS][U8_W];
+  int32_t de[U8_WARPS][U8_W];
+  int32_t ae[U8_WARPS][U8_W];
+  int32_t nrm[U8_WARPS][U8_W];
+  int16_t alive[U8_WARPS][U8_W];
+  alignas(16) uint8_t rows[U8_WARPS][U8_W * U8_ROW];
+};
+
+// test alive[a0..n_alive) against kept w (row wr in registers, norm nw)
+__device__ __forceinline__ int test_round_u8(const uint4 (&wr)[8], int nw, float duw,
+                                             int strategy, double cos_alpha, int a0,
+                                             int n_alive, const float *s_dist, int32_t *s_de,
+                                             int32_t *s_ae, int16_t *s_alive,
+                                             const int32_t *s_nrm, const uint8_t *rows,
+                                             int lane) {
+  if (duw == 0.0f) return 0;  // _kernels.py:387-389
+  int new_n = 0;
+  for (int base = a0; base < n_alive; base += 32) {
+    const int a = base + lane;
+    const bool act = a < n_alive;
+    bool survive = false;
+    int j = 0;
+    if (act) {
+      j = s_alive[a];
+      const uint4 *sr = reinterpret_cast<const uint4 *>(rows + j * U8_ROW);
+      unsigned d0 = 0, d1 = 0, d2 = 0, d3 = 0;  // 4 independent chains
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 b = sr[i];
+        d0 = __dp4a(wr[i].x, b.x, d0);
+        d1 = __dp4a(wr[i].y, b.y, d1);
+        d2 = __dp4a(wr[i].z, b.z, d2);
+        d3 = __dp4a(wr[i].w, b.w, d3);
+      }
+      const unsigned dot = (d0 + d1) + (d2 + d3);
+      // == squared_l2(data[w], data[v]) exactly (integers < 2^24)
+      const float dwv = (float)(nw + s_nrm[j] - 2 * (int)dot);
+      const float dv = s_dist[j];
+      s_de[j] += 1;
+      bool dom;
+      if (dwv == 0.0f) {
+        dom = true;
+      } else if (dwv < dv) {
+        if (strategy == 0) {
+          dom = true;
+        } else {
+          const double c = cos_angle_from_sq(duw, dwv, dv);
+          s_ae[j] += 1;
+          dom = c < cos_alpha;
+        }
+      } else {
+        dom = false;
+      }
+      survive = !dom;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, survive);
+    if (survive) s_alive[new_n + __popc(b & lanemask_lt())] = (int16_t)j;
+    new_n += __popc(b);
+  }
+  __syncwarp();
+  return new_n;
+}
+
+__global__ void __launch_bounds__(U8_WARPS * 32, 1)
+    prune_u8_kernel(const uint8_t *__restrict__ xu8, const int32_t *__restrict__ norms,
+                    int64_t n, const int32_t *__restrict__ row_node,
+                    const int32_t *__restrict__ row_order,
+                    const int64_t *__restrict__ cand_off,
+                    const int32_t *__restrict__ cand_counts,
+                    const int32_t *__restrict__ cand_ids, const float *__restrict__ cand_dists,
+                    int strategy, double cos_alpha, int M, int width,
+                    int32_t *__restrict__ out_ids, float *__restrict__ out_dists,
+                    int32_t *__restrict__ out_counts, int64_t *__restrict__ dist_evals,
+                    int64_t *__restrict__ angle_evals) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PruneU8Smem &sm = *reinterpret_cast<PruneU8Smem *>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t *s_id = sm.id[warp];
+  float *s_dist = sm.dist[warp];
+  int32_t *s_de = sm.de[warp];
+  int32_t *s_ae = sm.ae[warp];
+  int32_t *s_nrm = sm.nrm[warp];
+  int16_t *s_alive = sm.alive[warp];
+  uint8_t *rows = sm.rows[warp];
+
+  for (int64_t i = (int64_t)blockIdx.x * U8_WARPS + warp; i < n;
+       i += (int64_t)gridDim.x * U8_WARPS) {
+    const int64_t u = row_order ? row_order[i] : i;
+    const int64_t base = cand_off[u];
+    const int cnt = cand_counts[u];
+    const int32_t self = row_node ? row_node[u] : (int32_t)u;
+    int32_t *orow = out_ids + u * width;
+    float *odrow = out_dists + u * width;
+    int kept = 0;
+    bool stop = false;
+    long long de_tot = 0, ae_tot = 0;
+
+    for (int s = 0; s < cnt && !stop; s += U8_W) {
+      const int wn = min(U8_W, cnt - s);
+      __syncwarp();
+      // window: ids first (coalesced), then every candidate row in one
+      // cp.async burst, then norms / dists while the rows land
+      for (int j = lane; j < wn; j += 32) s_id[j] = cand_ids[base + s + j];
+      __syncwarp();
+#pragma unroll 4
+      for (int j0 = 0; j0 < wn; j0 += 4) {
+        const int j = j0 + (lane >> 3);
+        if (j < wn)
+          cp_async16(rows + j * U8_ROW + 16 * (lane & 7),
+                     xu8 + (int64_t)s_id[j] * 128 + 16 * (lane & 7));
+      }
+      cp_async_commit();
+      for (int j = lane; j < wn; j += 32) {
+        s_dist[j] = cand_dists[base + s + j];
+        s_nrm[j] = __ldg(norms + s_id[j]);
+        s_de[j] = 0;
+        s_ae[j] = 0;
+      }
+      __syncwarp();
+      int n_alive = 0;
+      for (int j0 = 0; j0 < wn; j0 += 32) {
+        const int j = j0 + lane;
+        const bool al = j < wn && s_id[j] != self;  // _kernels.py:380-382
+        const unsigned b = __ballot_sync(0xffffffffu, al);
+        if (al) s_alive[n_alive + __popc(b & lanemask_lt())] = (int16_t)j;
+        n_alive += __popc(b);
+      }
+      cp_async_wait<0>();
+      __syncwarp();
+      // rounds against neighbours kept in earlier windows (rows from global)
+      for (int kj = 0; kj < kept && n_alive > 0; ++kj) {
+        const int32_t w = orow[kj];
+        uint4 wr[8];
+        const uint4 *gp = reinterpret_cast<const uint4 *>(xu8 + (int64_t)w * 128);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) wr[i] = __ldg(gp + i);
+        n_alive = test_round_u8(wr, __ldg(norms + w), odrow[kj], strategy, cos_alpha, 0, n_alive,
+                                s_dist, s_de, s_ae, s_alive, s_nrm, rows, lane);
+      }
+      // in-window greedy: the first alive entry is the next kept neighbour
+      int stop_j = wn - 1;
+      while (n_alive > 0) {
+        const int e = s_alive[0];
+        const float duw = s_dist[e];
+        if (lane == 0) {
+          orow[kept] = s_id[e];
+          odrow[kept] = duw;
+        }
+        ++kept;
+        if (kept == M) {  // _kernels.py:378
+          stop = true;
+          stop_j = e;
+          break;
+        }
+        uint4 wr[8];
+        const uint4 *sp = reinterpret_cast<const uint4 *>(rows + e * U8_ROW);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) wr[i] = sp[i];
+        n_alive = test_round_u8(wr, s_nrm[e], duw, strategy, cos_alpha, 1, n_alive, s_dist, s_de,
+                                s_ae, s_alive, s_nrm, rows, lane);
+      }
+      __syncwarp();
+      long long de = 0, ae = 0;
+      for (int j = lane; j <= stop_j; j += 32) {
+        de += s_de[j];
+        ae += s_ae[j];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        de += __shfl_xor_sync(0xffffffffu, de, o);
+        ae += __shfl_xor_sync(0xffffffffu, ae, o);
+      }
+      de_tot += de;
+      ae_tot += ae;
+    }
+    __syncwarp();
+    for (int j = kept + lane; j < width; j += 32) {
+      orow[j] = -1;
+      odrow[j] = __int_as_float(0x7f800000);
+    }
+    if (lane == 0) {
+      out_counts[u] = kept;
+      dist_evals[u] = de_tot;
+      angle_evals[u] = ae_tot;
+    }
+  }
+}
+
+static int launch_u8(const uint8_t *xu8, const int32_t *norms, int64_t n,
+                     const int32_t *row_node, const int32_t *row_order, const int64_t *cand_off,
+                     const int32_t *cand_counts, const int32_t *cand_ids,
+                     const float *cand_dists, int strategy, double cos_alpha, int64_t M,
+                     int64_t width, int32_t *out_ids, float *out_dists, int32_t *out_counts,
+                     int64_t *dist_evals, int64_t *angle_evals, cudaStream_t stream) {
+  const size_t smem = sizeof(PruneU8Smem);
+  static bool attr = false;
+  if (!attr) {
+    PGK_CUDA(cudaFuncSetAttribute(prune_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    attr = true;
+  }
+  int64_t blocks = (n + U8_WARPS - 1) / U8_WARPS;
+  const int64_t cap = (int64_t)num_sms();  // one ~210 KB block per SM
+  if (blocks > cap) blocks = cap;
+  prune_u8_kernel<<<(unsigned)blocks, U8_WARPS * 32, smem, stream>>>(
+      xu8, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
+      cos_alpha,
+      (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals);
+  PGK_CHECK_LAUNCH("prune_u8_kernel");
+  return PGK_OK;
+}
+
 template <int MODE>
 static int launch_mode(const float *X, const uint8_t *xu8, const int32_t *norms, int64_t n,
-                       int64_t d, const int32_t *row_node, const int64_t *cand_off,
+                       int64_t d, const int32_t *row_node, const int32_t *row_order,
+                       const int64_t *cand_off,
                        const int32_t *cand_counts, const int32_t *cand_ids,
                        const float *cand_dists, int strategy, double cos_alpha, int64_t M,
                        int64_t width, int32_t *out_ids, float *out_dists, int32_t *out_counts,
@@ -312,7 +538,8 @@ static int launch_mode(const float *X, const uint8_t *xu8, const int32_t *norms,
     attr = true;
   }
   prune_kernel<MODE><<<(unsigned)blocks, PRUNE_WARPS * 32, smem, stream>>>(
-      X, xu8, norms, n, (int)d, row_node, cand_off, cand_counts, cand_ids, cand_dists, strategy,
+      X, xu8, norms, n, (int)d, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists,
+      strategy,
       cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals);
   PGK_CHECK_LAUNCH("prune_kernel");
   return PGK_OK;
@@ -322,21 +549,25 @@ static int launch_mode(const float *X, const uint8_t *xu8, const int32_t *norms,
 // zero padded) and its integer squared norms -- valid only when every value
 // of X is an integer in [0,255] and d <= 128 (pgk_detect_u8).
 int launch_prune(const float *X, const uint8_t *xu8, const int32_t *norms, int64_t n,
-                 int64_t d, const int32_t *row_node, const int64_t *cand_off,
+                 int64_t d, const int32_t *row_node, const int32_t *row_order,
+                 const int64_t *cand_off,
                  const int32_t *cand_counts, const int32_t *cand_ids, const float *cand_dists,
                  int strategy, double cos_alpha, int64_t M, int64_t width, int32_t *out_ids,
                  float *out_dists, int32_t *out_counts, int64_t *dist_evals,
                  int64_t *angle_evals, cudaStream_t stream) {
   if (n == 0) return PGK_OK;
   if (xu8 && norms && d <= 128)
-    return launch_mode<2>(X, xu8, norms, n, d, row_node, cand_off, cand_counts, cand_ids,
-                          cand_dists, strategy, cos_alpha, M, width, out_ids, out_dists,
-                          out_counts, dist_evals, angle_evals, stream);
+    return launch_u8(xu8, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids,
+                     cand_dists,
+                     strategy, cos_alpha, M, width, out_ids, out_dists, out_counts, dist_evals,
+                     angle_evals, stream);
   if ((d % 4 == 0) && ((uintptr_t)X % 16 == 0))
-    return launch_mode<1>(X, nullptr, nullptr, n, d, row_node, cand_off, cand_counts, cand_ids,
+    return launch_mode<1>(X, nullptr, nullptr, n, d, row_node, row_order, cand_off, cand_counts,
+                          cand_ids,
                           cand_dists, strategy, cos_alpha, M, width, out_ids, out_dists,
                           out_counts, dist_evals, angle_evals, stream);
-  return launch_mode<0>(X, nullptr, nullptr, n, d, row_node, cand_off, cand_counts, cand_ids,
+  return launch_mode<0>(X, nullptr, nullptr, n, d, row_node, row_order, cand_off, cand_counts,
+                        cand_ids,
                         cand_dists, strategy, cos_alpha, M, width, out_ids, out_dists,
                         out_counts, dist_evals, angle_evals, stream);
 }

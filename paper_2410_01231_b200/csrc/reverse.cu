@@ -27,7 +27,8 @@
 namespace pgk {
 
 int launch_prune(const float *X, const uint8_t *xu8, const int32_t *norms, int64_t n,
-                 int64_t d, const int32_t *row_node, const int64_t *cand_off,
+                 int64_t d, const int32_t *row_node, const int32_t *row_order,
+                 const int64_t *cand_off,
                  const int32_t *cand_counts, const int32_t *cand_ids,
                  const float *cand_dists, int strategy, double cos_alpha,
                  int64_t M, int64_t width, int32_t *out_ids, float *out_dists,
@@ -286,7 +287,7 @@ int reverse_workspace(int64_t n, int64_t width, size_t *bytes) {
 }
 
 int add_reverse_and_prune(const float *X, const uint8_t *xu8, const int32_t *norms,
-                          int64_t n, int64_t d,
+                          const int32_t *row_order, int64_t n, int64_t d,
                           const int32_t *a_ids, const float *a_dists,
                           const int32_t *a_counts, int64_t a_width, int strategy,
                           double cos_alpha, int64_t M, int64_t out_width,
@@ -330,7 +331,7 @@ int add_reverse_and_prune(const float *X, const uint8_t *xu8, const int32_t *nor
                                                       L.mrg_ids, L.mrg_d, L.mrg_counts);
   PGK_CHECK_LAUNCH("long_sort_kernel");
 
-  return launch_prune(X, xu8, norms, n, d, nullptr, L.mrg_off, L.mrg_counts, L.mrg_ids, L.mrg_d, strategy,
+  return launch_prune(X, xu8, norms, n, d, nullptr, row_order, L.mrg_off, L.mrg_counts, L.mrg_ids, L.mrg_d, strategy,
                       cos_alpha, M, out_width, out_ids, out_dists, out_counts,
                       dist_evals, angle_evals, stream);
 }

@@ -52,6 +52,12 @@ class RngBuilder:
         self.b_out = tuple(torch.empty_like(t) for t in self.a_out)
         self.u8_out = (torch.empty((n, 128), dtype=torch.uint8, device=dev),
                        torch.empty(n, dtype=I32, device=dev))
+        self.order_out = torch.empty(n, dtype=I32, device=dev)
+
+    def order(self):
+        """Locality order of the last pools() call (selection passes only)."""
+        return kernels.knn_order(self.pool_ws, self.n, self.d, self.K, self.mode,
+                                 self.order_out)
 
     def pools(self, X: torch.Tensor):
         r = kernels.knn_pools(X, self.K, None, True, self.mode, False, self.pool_ws,
@@ -72,10 +78,13 @@ class RngBuilder:
         p = self.params
         ids, dists = self.pools(X)
         u8 = self.u8_rows(X)
+        order = self.order()
         a = kernels.prune_batch(X, self.cand_off, self.cand_counts, ids, dists,
-                                p.strategy_code, p.cos_alpha, p.M, p.M, out=self.a_out, u8=u8)
+                                p.strategy_code, p.cos_alpha, p.M, p.M, out=self.a_out, u8=u8,
+                                order=order)
         b = kernels.add_reverse_and_prune(X, a[0], a[1], a[2], p.strategy_code, p.cos_alpha,
-                                          p.M, p.M, ws=self.rev_ws, out=self.b_out, u8=u8)
+                                          p.M, p.M, ws=self.rev_ws, out=self.b_out, u8=u8,
+                                          order=order)
         de = torch.stack([a[3].sum(), b[3].sum()])
         ae = torch.stack([a[4].sum(), b[4].sum()])
         return BuildOutput(b[0], b[1], b[2], a[2], de, ae)

@@ -40,7 +40,7 @@ def make_u8(X: torch.Tensor):
 
 def prune_batch(X: torch.Tensor, cand_off, cand_counts, cand_ids, cand_dists,
                 strategy: int, cos_alpha: float, M: int, width: int | None = None,
-                row_node=None, out=None, u8=None):
+                row_node=None, out=None, u8=None, order=None):
     """Phase-A scan (pgk_prune_rows_ex).  ``u8`` = make_u8(X) selects the
     exact-integer distance path.  Returns device tensors (ids (rows, width),
     dists, counts, dist_evals (rows,), angle_evals (rows,))."""
@@ -63,7 +63,8 @@ def prune_batch(X: torch.Tensor, cand_off, cand_counts, cand_ids, cand_dists,
     rn = None if row_node is None else _dev(row_node, _I32)
     xu8, norms = (None, None) if u8 is None else u8
     check(_lib.lib().pgk_prune_rows_ex(
-        ptr(X), ptr(xu8), ptr(norms), n, d, rows, ptr(rn), ptr(cand_off), ptr(cand_counts),
+        ptr(X), ptr(xu8), ptr(norms), n, d, rows, ptr(rn), ptr(order), ptr(cand_off),
+        ptr(cand_counts),
         ptr(cand_ids), ptr(cand_dists), int(strategy), float(cos_alpha), int(M), int(width),
         ptr(ids), ptr(dists), ptr(counts), ptr(de), ptr(ae), _lib.stream_handle()))
     return ids, dists, counts, de, ae
@@ -77,8 +78,8 @@ def reverse_workspace_bytes(n: int, a_width: int) -> int:
 
 def add_reverse_and_prune(X: torch.Tensor, a_ids, a_dists, a_counts, strategy: int,
                           cos_alpha: float, M: int, width: int | None = None, ws=None,
-                          out=None, u8=None):
-    """Phase B (pgk_add_reverse_and_prune); device tensors in and out."""
+                          out=None, u8=None, order=None):
+    """Phase B (pgk_add_reverse_and_prune_ex); device tensors in and out."""
     X = _dev(X, _F32)
     n, d = X.shape
     a_ids = _dev(a_ids, _I32)
@@ -98,7 +99,7 @@ def add_reverse_and_prune(X: torch.Tensor, a_ids, a_dists, a_counts, strategy: i
     ids, dists, counts, de, ae = out
     xu8, norms = (None, None) if u8 is None else u8
     check(_lib.lib().pgk_add_reverse_and_prune_ex(
-        ptr(X), ptr(xu8), ptr(norms), n, d, ptr(a_ids), ptr(a_dists), ptr(a_counts), a_width,
+        ptr(X), ptr(xu8), ptr(norms), ptr(order), n, d, ptr(a_ids), ptr(a_dists), ptr(a_counts), a_width,
         int(strategy),
         float(cos_alpha), int(M), int(width), ptr(ids), ptr(dists), ptr(counts), ptr(de),
         ptr(ae), ptr(ws), ws.numel(), _lib.stream_handle()))
@@ -161,6 +162,15 @@ def knn_work(ws: torch.Tensor, n: int, nq: int, d: int, k: int, mode: int):
     check(_lib.lib().pgk_knn_work(ptr(ws), int(n), int(nq), int(d), int(k), int(mode), out,
                                   _lib.stream_handle()))
     return int(out[0]), int(out[1]), int(out[2]), bool(out[3])
+
+
+def knn_order(ws: torch.Tensor, n: int, d: int, k: int, mode: int, out=None):
+    """Locality processing order for the selection passes (pgk_knn_order)."""
+    if out is None:
+        out = torch.empty(n, dtype=_I32, device=ws.device)
+    check(_lib.lib().pgk_knn_order(ptr(ws), int(n), int(d), int(k), int(mode), ptr(out),
+                                   _lib.stream_handle()))
+    return out
 
 
 def fallback_rows(ws: torch.Tensor) -> int:

@@ -271,3 +271,29 @@ def test_exact_integer_selection_equals_fp32_path(strategy, alpha):
                                        params.cos_alpha, R, u8=u8)
     for x, y in zip(b32, b8):
         assert torch.equal(x, y)
+
+
+def test_row_order_does_not_change_results():
+    """The selection kernels' optional processing order (pgk_knn_order) is a
+    performance hint only."""
+    data = synth.cfg2(6000)
+    ds = Dataset.from_array(data)
+    K, R = 48, 16
+    r = kernels.knn_pools(ds.device_data(), K, None, True, 1, False)
+    order = kernels.knn_order(r.ws, ds.n, ds.d, K, 1)
+    assert sorted(order.cpu().tolist()) == list(range(ds.n))
+    X = ds.device_data()
+    u8 = kernels.make_u8(X)
+    params = PruneParams(M=R, alpha=66.0, strategy="alpha")
+    off = np.arange(ds.n + 1, dtype=np.int64) * K
+    cnt = np.full(ds.n, K, np.int32)
+    args = (X, off, cnt, r.pool_ids.reshape(-1), r.pool_dists.reshape(-1), 1, params.cos_alpha, R)
+    a0 = kernels.prune_batch(*args, u8=u8)
+    a1 = kernels.prune_batch(*args, u8=u8, order=order)
+    for x, y in zip(a0, a1):
+        assert torch.equal(x, y)
+    b0 = kernels.add_reverse_and_prune(X, a0[0], a0[1], a0[2], 1, params.cos_alpha, R, u8=u8)
+    b1 = kernels.add_reverse_and_prune(X, a0[0], a0[1], a0[2], 1, params.cos_alpha, R, u8=u8,
+                                       order=order)
+    for x, y in zip(b0, b1):
+        assert torch.equal(x, y)

@@ -35,13 +35,14 @@ def main():
         if a.stage in ("pool", "all"):
             ids, d = b.pools(X)
         u8 = b.u8_rows(X)
+        order = b.order()
         if a.stage in ("prune", "all"):
             r = kernels.prune_batch(X, b.cand_off, b.cand_counts, ids, d, p.strategy_code,
-                                    p.cos_alpha, p.M, p.M, out=b.a_out, u8=u8)
+                                    p.cos_alpha, p.M, p.M, out=b.a_out, u8=u8, order=order)
         if a.stage in ("reverse", "all"):
             kernels.add_reverse_and_prune(X, b.a_out[0], b.a_out[1], b.a_out[2],
                                           p.strategy_code, p.cos_alpha, p.M, p.M, ws=b.rev_ws,
-                                          out=b.b_out, u8=u8)
+                                          out=b.b_out, u8=u8, order=order)
         torch.cuda.synchronize()
         print(f"{a.stage} n={a.n}: {1e3 * (time.perf_counter() - t0):.2f} ms")
 
