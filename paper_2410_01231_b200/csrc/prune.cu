@@ -301,8 +301,8 @@ __global__ void __launch_bounds__(PRUNE_WARPS * 32, 2)
 // u8 rows (128 B each) in shared memory for all rounds: one cp.async burst per
 // window instead of a global round trip per round.
 // ---------------------------------------------------------------------------
-constexpr int U8_WARPS = 10;
-constexpr int U8_W = 128;
+constexpr int U8_WARPS = 16;
+constexpr int U8_W = 64;
 constexpr int U8_ROW = 144;  // padded row stride (36 words == 4 mod 32)
 
 struct PruneU8Smem {
