@@ -31,20 +31,22 @@ namespace tc {
 constexpr int BM = 128;   // query rows per block == TMEM lanes
 constexpr int BN = 128;   // data points per tile == MMA N
 constexpr int KB = 128;   // bytes per (padded) row
-constexpr int STAGES = 4;
+constexpr int STAGES = 2;       // B-tile ring depth
+constexpr int ACC = 1;          // TMEM accumulator stages (128 columns each)
+constexpr int CTAS_PER_SM = 3;  // co-resident CTAs share the tensor core
 constexpr int TILE_BYTES = BN * KB;
 constexpr int CAP = 1024;  // per-row candidate buffer (keys, global memory)
-constexpr int THREADS = 256;
-constexpr int TMEM_COLS = 256;
+constexpr int THREADS = 192;  // warp 0 TMA, warp 1 TMEM alloc + MMA, warps 2-5 epilogue
+constexpr int TMEM_COLS = ACC * BN;
 
 struct __align__(1024) Smem {
   uint8_t a[BM * KB];
   uint8_t b[STAGES][TILE_BYTES];
   int32_t sv[4][32 * 36];  // per epilogue warp: one chunk of s values per lane
-  alignas(16) int32_t ny[2][BN];  // |x|^2 of the tile in each accumulator stage
-  alignas(16) int32_t pid[2][BN];  // original ids of the tile's columns (pruned path)
+  alignas(16) int32_t ny[ACC][BN];   // |x|^2 of the tile in each accumulator stage
+  alignas(16) int32_t pid[ACC][BN];  // original ids of the tile's columns (pruned path)
   uint64_t full[STAGES], empty[STAGES];
-  uint64_t tfull[2], tempty[2];
+  uint64_t tfull[ACC], tempty[ACC];
   uint64_t a_full, a_empty;
   uint32_t tmem_base;
 };
@@ -304,7 +306,7 @@ enum { ST_WAIT, ST_MAIN, ST_SLOW, ST_COMPACT, ST_FINAL, ST_NSLOW, ST_NCOMPACT, S
        ST_COUNT };
 
 template <bool STATS>
-__global__ void __launch_bounds__(THREADS, 2)
+__global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     tc_pool_u8_kernel(const __grid_constant__ CUtensorMap tmX,
                       const __grid_constant__ CUtensorMap tmQ, int64_t n, int64_t nq,
                       int exclude_self, const int32_t *__restrict__ xnorm,
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       mbar_init(&s.full[i], 1);
       mbar_init(&s.empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < ACC; ++i) {
       mbar_init(&s.tfull[i], 1);
       mbar_init(&s.tempty[i], 4);
     }
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     mbar_init(&s.a_empty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 2) {
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&s.tmem_base)),
                  "n"(TMEM_COLS));
@@ -405,15 +407,15 @@ __global__ void __launch_bounds__(THREADS, 2)
           tc_commit(&s.empty[stage]);
           tc_commit(&s.tfull[acc]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
-          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
         }
         tc_commit(&s.a_empty);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 2) {
     // ---------------- epilogue ----------------
-    const int q = warp - 4;  // TMEM lane quarter (warp % 4)
-    int32_t *sv = s.sv[q] + lane * 36;
+    const int q = warp & 3;  // TMEM lane quarter this warp may access (warp % 4)
+    int32_t *sv = s.sv[warp - 2] + lane * 36;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int b = blockIdx.x; b < nblocks; b += gridDim.x) {
@@ -442,14 +444,12 @@ __global__ void __launch_bounds__(THREADS, 2)
         PGK_TICK(ST_WAIT);
         const int64_t col0 = (int64_t)tid * BN;
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
-        uint32_t rbuf[2][32];
-        tmem_ld32(tbase, rbuf[0]);
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
-          uint32_t(&r)[32] = rbuf[c & 1];
+          // (co-resident CTAs hide the TMEM-load latency; one chunk in flight)
+          uint32_t r[32];
+          tmem_ld32(tbase + c * 32, r);
           tmem_wait_ld();
-          if (c + 1 < BN / 32)
-            tmem_ld32(tbase + (c + 1) * 32, rbuf[(c + 1) & 1]);  // overlaps this chunk
           const int64_t cb = col0 + c * 32;
           const int4 *nyp = reinterpret_cast<const int4 *>(s.ny[acc] + c * 32);
           // s_j = |x_j|^2 - 2 q.x_j ; pass iff s_j <= tau_dist - |q|^2
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s.tempty[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
       }
       // block done: record each row's buffer fill and threshold; selection
       // and sorting run in the massively parallel finalize kernel
@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 #undef PGK_TICK
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "n"(TMEM_COLS));
@@ -733,7 +733,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
     attr = true;
   }
   const int nblocks = (int)((nq + tc::BM - 1) / tc::BM);
-  const unsigned grid = (unsigned)std::min<int64_t>(nblocks, (int64_t)2 * sms);
+  const unsigned grid = (unsigned)std::min<int64_t>(nblocks, (int64_t)tc::CTAS_PER_SM * sms);
   const char *se = getenv("PGK_TC_STATS");
   if (se && se[0] == '1') {
     unsigned long long *dstats = nullptr;
