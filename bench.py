@@ -233,7 +233,7 @@ def run_ours(args):
             order = builder.order()
             a = kernels.prune_batch(X, builder.cand_off, builder.cand_counts, pids, pd,
                                     p.strategy_code, p.cos_alpha, p.M, p.M, out=builder.a_out,
-                                    u8=u8, order=order)
+                                    u8=u8, order=order, ws=builder.prune_ws)
             e[2].record(stream)
             kernels.add_reverse_and_prune(X, a[0], a[1], a[2], p.strategy_code, p.cos_alpha,
                                           p.M, p.M, ws=builder.rev_ws, out=builder.b_out, u8=u8,

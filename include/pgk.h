@@ -95,7 +95,11 @@ int pgk_prune_rows_ex(const float *data, const uint8_t *data_u8,
                       const float *cand_dists, int strategy, double cos_alpha,
                       int64_t M, int64_t width, int32_t *out_ids, float *out_dists,
                       int32_t *out_counts, int64_t *dist_evals,
-                      int64_t *angle_evals, void *stream);
+                      int64_t *angle_evals, void *ws, size_t ws_bytes, void *stream);
+/* Workspace of pgk_prune_rows_ex's exact-integer path: with it (and data_u8),
+ * rows of <= 128 candidates run through the tensor-core C x C Gram kernel
+ * (one tcgen05 kind::i8 MMA per point); without it, the per-warp kernel. */
+int pgk_prune_workspace(int64_t n_rows, size_t *ws_bytes_host);
 
 /* ---------------------------------------------------------------------------
  * Phase B: reverse-edge insertion + re-prune.  Replaces

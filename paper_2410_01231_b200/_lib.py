@@ -39,7 +39,8 @@ def lib():
         L.pgk_prune_rows.argtypes = [P, I64, I64, I64, P, P, P, P, P, I, D, I64, I64,
                                      P, P, P, P, P, P]
         L.pgk_prune_rows_ex.argtypes = [P, P, P, I64, I64, I64, P, P, P, P, P, P, I, D, I64,
-                                        I64, P, P, P, P, P, P]
+                                        I64, P, P, P, P, P, P, SZ, P]
+        L.pgk_prune_workspace.argtypes = [I64, P]
         L.pgk_make_u8.argtypes = [P, I64, I64, P, P, P]
         L.pgk_add_reverse_and_prune_ex.argtypes = [P, P, P, P, I64, I64, P, P, P, I64, I, D,
                                                    I64, I64, P, P, P, P, P, P, SZ, P]
@@ -53,6 +54,7 @@ def lib():
         L.pgk_knn_fallback_rows.argtypes = [P, P, P]
         L.pgk_knn_work.argtypes = [P, I64, I64, I64, I64, I, P, P]
         for f in ("pgk_device_check", "pgk_prune_batch", "pgk_prune_rows", "pgk_prune_rows_ex",
+                  "pgk_prune_workspace",
                   "pgk_make_u8", "pgk_add_reverse_and_prune_ex", "pgk_reverse_workspace",
                   "pgk_add_reverse_and_prune", "pgk_detect_u8", "pgk_knn_workspace",
                   "pgk_knn_pools", "pgk_knn_fallback_rows", "pgk_knn_work", "pgk_knn_order"):
@@ -62,7 +64,7 @@ def lib():
 
 
 EXPORTS = ("pgk_version", "pgk_last_error", "pgk_device_check", "pgk_prune_batch",
-           "pgk_prune_rows", "pgk_prune_rows_ex", "pgk_make_u8", "pgk_add_reverse_and_prune_ex",
+           "pgk_prune_rows", "pgk_prune_rows_ex", "pgk_prune_workspace", "pgk_make_u8", "pgk_add_reverse_and_prune_ex",
            "pgk_reverse_workspace", "pgk_add_reverse_and_prune", "pgk_detect_u8",
            "pgk_knn_workspace", "pgk_knn_pools", "pgk_knn_fallback_rows", "pgk_knn_work",
            "pgk_knn_order",

@@ -27,9 +27,10 @@ int num_sms() {
   return cached;
 }
 
+size_t prune_workspace(int64_t n_rows);
 int launch_prune(const float *, const uint8_t *, const int32_t *, int64_t, int64_t,
-                 const int32_t *, const int32_t *, const int64_t *, const int32_t *,
-                 const int32_t *,
+                 const int32_t *, const int32_t *, void *, size_t, const int64_t *,
+                 const int32_t *, const int32_t *,
                  const float *, int, double, int64_t, int64_t, int32_t *, float *, int32_t *,
                  int64_t *, int64_t *, cudaStream_t);
 int make_u8(const float *, int64_t, int64_t, uint8_t *, int32_t *, cudaStream_t);
@@ -91,8 +92,8 @@ int pgk_prune_batch(const float *data, int64_t n, int64_t d, const int64_t *cand
                     int64_t *dist_evals, int64_t *angle_evals, void *stream) {
   int rc = check_prune_args(data, n, d, strategy, M, width);
   if (rc) return rc;
-  return launch_prune(data, nullptr, nullptr, n, d, nullptr, nullptr, cand_off, cand_counts,
-                      cand_ids, cand_dists, strategy,
+  return launch_prune(data, nullptr, nullptr, n, d, nullptr, nullptr, nullptr, 0, cand_off,
+                      cand_counts, cand_ids, cand_dists, strategy,
                       cos_alpha, M, width, out_ids, out_dists, out_counts, dist_evals,
                       angle_evals, (cudaStream_t)stream);
 }
@@ -105,7 +106,8 @@ int pgk_prune_rows(const float *data, int64_t n, int64_t d, int64_t n_rows,
                    int64_t *dist_evals, int64_t *angle_evals, void *stream) {
   return pgk_prune_rows_ex(data, nullptr, nullptr, n, d, n_rows, row_node, nullptr, cand_off,
                            cand_counts, cand_ids, cand_dists, strategy, cos_alpha, M, width,
-                           out_ids, out_dists, out_counts, dist_evals, angle_evals, stream);
+                           out_ids, out_dists, out_counts, dist_evals, angle_evals, nullptr, 0,
+                           stream);
 }
 
 int pgk_prune_rows_ex(const float *data, const uint8_t *data_u8, const int32_t *norms_u8,
@@ -115,14 +117,21 @@ int pgk_prune_rows_ex(const float *data, const uint8_t *data_u8, const int32_t *
                       const int32_t *cand_ids, const float *cand_dists, int strategy,
                       double cos_alpha, int64_t M, int64_t width, int32_t *out_ids,
                       float *out_dists, int32_t *out_counts, int64_t *dist_evals,
-                      int64_t *angle_evals, void *stream) {
+                      int64_t *angle_evals, void *ws, size_t ws_bytes, void *stream) {
   int rc = check_prune_args(data, n, d, strategy, M, width);
   if (rc) return rc;
   PGK_REQUIRE(n_rows >= 0, "n_rows must be >= 0");
   PGK_REQUIRE(!data_u8 || (norms_u8 && d <= 128), "u8 rows need norms and d <= 128");
-  return launch_prune(data, data_u8, norms_u8, n_rows, d, row_node, row_order, cand_off,
+  return launch_prune(data, data_u8, norms_u8, n_rows, d, row_node, row_order, ws, ws_bytes,
+                      cand_off,
                       cand_counts, cand_ids, cand_dists, strategy, cos_alpha, M, width, out_ids,
                       out_dists, out_counts, dist_evals, angle_evals, (cudaStream_t)stream);
+}
+
+int pgk_prune_workspace(int64_t n_rows, size_t *ws_bytes_host) {
+  PGK_REQUIRE(ws_bytes_host, "ws_bytes_host is NULL");
+  *ws_bytes_host = prune_workspace(n_rows);
+  return PGK_OK;
 }
 
 int pgk_make_u8(const float *data, int64_t n, int64_t d, uint8_t *out_u8, int32_t *out_norms,

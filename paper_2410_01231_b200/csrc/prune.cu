@@ -372,7 +372,8 @@ __device__ __forceinline__ int test_round_u8(const uint4 (&wr)[8], int nw, float
 
 __global__ void __launch_bounds__(U8_WARPS * 32, 1)
     prune_u8_kernel(const uint8_t *__restrict__ xu8, const int32_t *__restrict__ norms,
-                    int64_t n, const int32_t *__restrict__ row_node,
+                    int64_t n, const int32_t *__restrict__ n_dev,
+                    const int32_t *__restrict__ row_node,
                     const int32_t *__restrict__ row_order,
                     const int64_t *__restrict__ cand_off,
                     const int32_t *__restrict__ cand_counts,
@@ -391,6 +392,7 @@ __global__ void __launch_bounds__(U8_WARPS * 32, 1)
   int32_t *s_nrm = sm.nrm[warp];
   int16_t *s_alive = sm.alive[warp];
   uint8_t *rows = sm.rows[warp];
+  if (n_dev) n = *n_dev;  // row count produced on the device (hub list)
 
   for (int64_t i = (int64_t)blockIdx.x * U8_WARPS + warp; i < n;
        i += (int64_t)gridDim.x * U8_WARPS) {
@@ -495,8 +497,9 @@ __global__ void __launch_bounds__(U8_WARPS * 32, 1)
   }
 }
 
-static int launch_u8(const uint8_t *xu8, const int32_t *norms, int64_t n,
-                     const int32_t *row_node, const int32_t *row_order, const int64_t *cand_off,
+int launch_prune_u8_rows(const uint8_t *xu8, const int32_t *norms, int64_t n,
+                         const int32_t *n_dev, const int32_t *row_node,
+                         const int32_t *row_order, const int64_t *cand_off,
                      const int32_t *cand_counts, const int32_t *cand_ids,
                      const float *cand_dists, int strategy, double cos_alpha, int64_t M,
                      int64_t width, int32_t *out_ids, float *out_dists, int32_t *out_counts,
@@ -512,8 +515,8 @@ static int launch_u8(const uint8_t *xu8, const int32_t *norms, int64_t n,
   const int64_t cap = (int64_t)num_sms();  // one ~210 KB block per SM
   if (blocks > cap) blocks = cap;
   prune_u8_kernel<<<(unsigned)blocks, U8_WARPS * 32, smem, stream>>>(
-      xu8, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
-      cos_alpha,
+      xu8, norms, n, n_dev, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists,
+      strategy, cos_alpha,
       (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals);
   PGK_CHECK_LAUNCH("prune_u8_kernel");
   return PGK_OK;
@@ -548,17 +551,33 @@ static int launch_mode(const float *X, const uint8_t *xu8, const int32_t *norms,
 // xu8 / norms (optional): the exact-integer copy of X (rows of 128 bytes,
 // zero padded) and its integer squared norms -- valid only when every value
 // of X is an integer in [0,255] and d <= 128 (pgk_detect_u8).
+bool gram_enabled();
+size_t gram_workspace(int64_t n);
+int launch_prune_gram(const uint8_t *xu8, const int32_t *norms, int64_t n,
+                      const int32_t *row_node, const int32_t *row_order,
+                      const int64_t *cand_off, const int32_t *cand_counts,
+                      const int32_t *cand_ids, const float *cand_dists, int strategy,
+                      double cos_alpha, int64_t M, int64_t width, int32_t *out_ids,
+                      float *out_dists, int32_t *out_counts, int64_t *dist_evals,
+                      int64_t *angle_evals, void *ws, cudaStream_t stream);
+
+size_t prune_workspace(int64_t n_rows) { return gram_workspace(n_rows); }
+
 int launch_prune(const float *X, const uint8_t *xu8, const int32_t *norms, int64_t n,
-                 int64_t d, const int32_t *row_node, const int32_t *row_order,
-                 const int64_t *cand_off,
+                 int64_t d, const int32_t *row_node, const int32_t *row_order, void *ws,
+                 size_t ws_bytes, const int64_t *cand_off,
                  const int32_t *cand_counts, const int32_t *cand_ids, const float *cand_dists,
                  int strategy, double cos_alpha, int64_t M, int64_t width, int32_t *out_ids,
                  float *out_dists, int32_t *out_counts, int64_t *dist_evals,
                  int64_t *angle_evals, cudaStream_t stream) {
   if (n == 0) return PGK_OK;
+  if (xu8 && norms && d <= 128 && ws && ws_bytes >= gram_workspace(n) && gram_enabled())
+    return launch_prune_gram(xu8, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids,
+                             cand_dists, strategy, cos_alpha, M, width, out_ids, out_dists,
+                             out_counts, dist_evals, angle_evals, ws, stream);
   if (xu8 && norms && d <= 128)
-    return launch_u8(xu8, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids,
-                     cand_dists,
+    return launch_prune_u8_rows(xu8, norms, n, nullptr, row_node, row_order, cand_off,
+                     cand_counts, cand_ids, cand_dists,
                      strategy, cos_alpha, M, width, out_ids, out_dists, out_counts, dist_evals,
                      angle_evals, stream);
   if ((d % 4 == 0) && ((uintptr_t)X % 16 == 0))

@@ -26,9 +26,10 @@
 
 namespace pgk {
 
+size_t prune_workspace(int64_t n_rows);
 int launch_prune(const float *X, const uint8_t *xu8, const int32_t *norms, int64_t n,
-                 int64_t d, const int32_t *row_node, const int32_t *row_order,
-                 const int64_t *cand_off,
+                 int64_t d, const int32_t *row_node, const int32_t *row_order, void *ws,
+                 size_t ws_bytes, const int64_t *cand_off,
                  const int32_t *cand_counts, const int32_t *cand_ids,
                  const float *cand_dists, int strategy, double cos_alpha,
                  int64_t M, int64_t width, int32_t *out_ids, float *out_dists,
@@ -258,6 +259,8 @@ struct RevLayout {
   int32_t *mrg_ids, *mrg_counts;
   float *mrg_d;
   int64_t *cap, *scan_tmp;
+  void *prune_ws;
+  size_t prune_bytes;
   size_t total;
 };
 
@@ -277,6 +280,8 @@ static RevLayout rev_layout(void *ws, size_t ws_bytes, int64_t n, int64_t width)
   L.mrg_d = c.take<float>(cap);
   L.cap = c.take<int64_t>(n + 1);
   L.scan_tmp = c.take<int64_t>(scan_scratch(n + 1));
+  L.prune_bytes = prune_workspace(n);
+  L.prune_ws = c.take<char>(L.prune_bytes);
   L.total = c.off;
   return L;
 }
@@ -331,7 +336,8 @@ int add_reverse_and_prune(const float *X, const uint8_t *xu8, const int32_t *nor
                                                       L.mrg_ids, L.mrg_d, L.mrg_counts);
   PGK_CHECK_LAUNCH("long_sort_kernel");
 
-  return launch_prune(X, xu8, norms, n, d, nullptr, row_order, L.mrg_off, L.mrg_counts, L.mrg_ids, L.mrg_d, strategy,
+  return launch_prune(X, xu8, norms, n, d, nullptr, row_order, L.prune_ws, L.prune_bytes,
+                      L.mrg_off, L.mrg_counts, L.mrg_ids, L.mrg_d, strategy,
                       cos_alpha, M, out_width, out_ids, out_dists, out_counts,
                       dist_evals, angle_evals, stream);
 }

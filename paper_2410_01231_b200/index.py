@@ -53,6 +53,7 @@ class RngBuilder:
         self.u8_out = (torch.empty((n, 128), dtype=torch.uint8, device=dev),
                        torch.empty(n, dtype=I32, device=dev))
         self.order_out = torch.empty(n, dtype=I32, device=dev)
+        self.prune_ws = _lib.workspace(kernels.prune_workspace_bytes(n))
 
     def order(self):
         """Locality order of the last pools() call (selection passes only)."""
@@ -81,7 +82,7 @@ class RngBuilder:
         order = self.order()
         a = kernels.prune_batch(X, self.cand_off, self.cand_counts, ids, dists,
                                 p.strategy_code, p.cos_alpha, p.M, p.M, out=self.a_out, u8=u8,
-                                order=order)
+                                order=order, ws=self.prune_ws)
         b = kernels.add_reverse_and_prune(X, a[0], a[1], a[2], p.strategy_code, p.cos_alpha,
                                           p.M, p.M, ws=self.rev_ws, out=self.b_out, u8=u8,
                                           order=order)

@@ -40,7 +40,7 @@ def make_u8(X: torch.Tensor):
 
 def prune_batch(X: torch.Tensor, cand_off, cand_counts, cand_ids, cand_dists,
                 strategy: int, cos_alpha: float, M: int, width: int | None = None,
-                row_node=None, out=None, u8=None, order=None):
+                row_node=None, out=None, u8=None, order=None, ws=None):
     """Phase-A scan (pgk_prune_rows_ex).  ``u8`` = make_u8(X) selects the
     exact-integer distance path.  Returns device tensors (ids (rows, width),
     dists, counts, dist_evals (rows,), angle_evals (rows,))."""
@@ -62,12 +62,21 @@ def prune_batch(X: torch.Tensor, cand_off, cand_counts, cand_ids, cand_dists,
     ids, dists, counts, de, ae = out
     rn = None if row_node is None else _dev(row_node, _I32)
     xu8, norms = (None, None) if u8 is None else u8
+    if ws is None and u8 is not None:
+        ws = _lib.workspace(prune_workspace_bytes(rows))
     check(_lib.lib().pgk_prune_rows_ex(
         ptr(X), ptr(xu8), ptr(norms), n, d, rows, ptr(rn), ptr(order), ptr(cand_off),
         ptr(cand_counts),
         ptr(cand_ids), ptr(cand_dists), int(strategy), float(cos_alpha), int(M), int(width),
-        ptr(ids), ptr(dists), ptr(counts), ptr(de), ptr(ae), _lib.stream_handle()))
+        ptr(ids), ptr(dists), ptr(counts), ptr(de), ptr(ae), ptr(ws),
+        0 if ws is None else ws.numel(), _lib.stream_handle()))
     return ids, dists, counts, de, ae
+
+
+def prune_workspace_bytes(n_rows: int) -> int:
+    b = ctypes.c_size_t(0)
+    check(_lib.lib().pgk_prune_workspace(int(n_rows), ctypes.byref(b)))
+    return int(b.value)
 
 
 def reverse_workspace_bytes(n: int, a_width: int) -> int:

@@ -297,3 +297,73 @@ def test_row_order_does_not_change_results():
                                        order=order)
     for x, y in zip(b0, b1):
         assert torch.equal(x, y)
+
+
+def test_gram_selection_hub_rows_and_fallback():
+    """Exact-integer data with a hub: rows of <= 128 candidates go through the
+    tensor-core Gram kernel, the hub's long merged list through the per-warp
+    kernel; both must match the oracle (and the fp32 path)."""
+    rng = np.random.default_rng(21)
+    center = np.full((1, 64), 128.0)
+    pts = center + 30.0 * rng.choice([-1.0, 1.0], size=(2500, 64))
+    data = np.vstack([center, pts]).astype(np.float32)
+    ds = Dataset.from_array(data)
+    assert ds.is_u8()
+    K, R = 24, 12
+    ids, dists = knn_pools(ds, K)
+    for strategy, alpha in (("rng", 60.0), ("alpha", 70.0)):
+        params = PruneParams(M=R, alpha=alpha, strategy=strategy)
+        off = np.arange(ds.n + 1, dtype=np.int64) * K
+        cnt = np.full(ds.n, K, np.int32)
+        a = prune_all(ds, off, cnt, ids.ravel(), dists.ravel(), params)
+        b = add_reverse_and_prune(ds, a[0], a[1], a[2], params)
+        oa, ob = oracle.refine_ab(data, ids, dists, R, strategy, alpha)
+        for res, ores in ((a, oa), (b, ob)):
+            for i in range(3):
+                np.testing.assert_array_equal(res[i], ores[i])
+            assert res[3] == ores[3] and res[4] == ores[4]
+    # the hub's reverse list is long (in-degree > 128)
+    assert (a[0][1:, 0] == 0).mean() > 0.9
+
+
+def test_tensor_core_cxc_gram_selection_path():
+    """The batched per-point C x C Gram kernel (tcgen05 kind::i8 + bitmask scan,
+    opt-in via PGK_GRAM=1) gives the same phase A / B rows and counters as the
+    default path, in a fresh process."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, %r)
+from paper_2410_01231_b200 import Dataset, PruneParams, knn_pools, prune_all, add_reverse_and_prune, synth
+rng = np.random.default_rng(21)
+center = np.full((1, 64), 128.0)
+hub = np.vstack([center, center + 30.0 * rng.choice([-1.0, 1.0], size=(1500, 64))])
+out = {}
+for name, data in (("cfg2", synth.cfg2(6000)), ("hub", hub.astype(np.float32))):
+    ds = Dataset.from_array(data)
+    K = 64 if name == "cfg2" else 24
+    ids, dists = knn_pools(ds, K)
+    off = np.arange(ds.n + 1, dtype=np.int64) * K
+    cnt = np.full(ds.n, K, np.int32)
+    for st, al in (("rng", 60.0), ("alpha", 66.0)):
+        p = PruneParams(M=20, alpha=al, strategy=st)
+        a = prune_all(ds, off, cnt, ids.ravel(), dists.ravel(), p)
+        b = add_reverse_and_prune(ds, a[0], a[1], a[2], p)
+        for ph, r in (("a", a), ("b", b)):
+            out[f"{name}_{st}_{ph}_ids"] = r[0]; out[f"{name}_{st}_{ph}_cnt"] = r[2]
+            out[f"{name}_{st}_{ph}_ev"] = np.array([r[3], r[4]])
+np.savez(sys.argv[1], **out)
+''' % str(root)
+    res = {}
+    for tag, env in (("gram", {"PGK_GRAM": "1"}), ("warp", {})):
+        path = f"/tmp/pgk_gram_{tag}.npz"
+        subprocess.check_call([sys.executable, "-c", code, path],
+                              env=dict(os.environ, **env), timeout=600)
+        res[tag] = dict(np.load(path))
+    assert res["gram"].keys() == res["warp"].keys()
+    for k in res["gram"]:
+        np.testing.assert_array_equal(res["gram"][k], res["warp"][k], err_msg=k)

@@ -38,7 +38,8 @@ def main():
         order = b.order()
         if a.stage in ("prune", "all"):
             r = kernels.prune_batch(X, b.cand_off, b.cand_counts, ids, d, p.strategy_code,
-                                    p.cos_alpha, p.M, p.M, out=b.a_out, u8=u8, order=order)
+                                    p.cos_alpha, p.M, p.M, out=b.a_out, u8=u8, order=order,
+                                    ws=b.prune_ws)
         if a.stage in ("reverse", "all"):
             kernels.add_reverse_and_prune(X, b.a_out[0], b.a_out[1], b.a_out[2],
                                           p.strategy_code, p.cos_alpha, p.M, p.M, ws=b.rev_ws,
