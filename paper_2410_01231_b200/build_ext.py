@@ -5,6 +5,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -30,17 +31,20 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
-    objs = []
-    logs = []
-    for s in SOURCES:
+    def compile_one(s):
         obj = CSRC / (s[:-3] + ".o")
         cmd = [NVCC, *FLAGS, "-c", str(CSRC / s), "-o", str(obj)]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return s, str(obj), subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    objs, logs = [], []
+    for s, obj, r in results:
         logs.append(r.stderr)
         if r.returncode != 0:
             sys.stderr.write(r.stderr)
             raise RuntimeError(f"nvcc failed on {s}")
-        objs.append(str(obj))
+        objs.append(obj)
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs,
            "-o", str(tmp)]

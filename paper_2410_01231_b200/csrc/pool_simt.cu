@@ -584,7 +584,8 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             cudaStream_t stream, const uint8_t *xs_sorted,
                             const int32_t *tlist, const int32_t *tlen, int64_t tstride,
                             const int32_t *perm, bool *handled,
-                            const uint64_t *init_keys = nullptr, int kth_only = 0);
+                            const uint64_t *init_keys = nullptr, int kth_only = 0,
+                            float shrink = 1.0f, int32_t *fail_blocks = nullptr);
 int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm, int K,
                          uint64_t *keys, void *tc_ws, size_t tc_bytes, void *tws,
                          size_t tws_bytes, cudaStream_t stream, bool *handled,

@@ -39,6 +39,7 @@ constexpr int TILE_BYTES = BN * KB;
 constexpr int CAP = 1024;  // per-row candidate buffer (keys, global memory)
 constexpr int THREADS = 192;  // warp 0 TMA, warp 1 TMEM alloc + MMA, warps 2-5 epilogue
 constexpr int TMEM_COLS = ACC * BN;
+constexpr int GUESSED = 1 << 30;  // row_cnt flag: the row ran under a guessed threshold
 
 struct __align__(1024) Smem {
   uint8_t a[BM * KB];
@@ -50,6 +51,7 @@ struct __align__(1024) Smem {
   uint64_t tfull[ACC], tempty[ACC];
   uint64_t a_full, a_empty;
   uint32_t tmem_base;
+  int32_t blk[2];  // dynamic schedule: block index per A-tile phase (-1 = done)
 };
 
 // kind::i8 instruction descriptor: D s32, A/B u8, K-major, M=128, N=BN
@@ -204,12 +206,20 @@ __device__ __forceinline__ int tau_prefilter(uint64_t tau, int nx) {
   return (int)khi(tau) - nx;
 }
 
+// s-value prefilter bound of a row: K == 1 keeps dist <= khi(tau) (then the
+// exact key compare), K > 1 keeps dist < khi(tau) (tau = T << 32, exact).
+__device__ __forceinline__ int row_tp(uint64_t tau, int nx, int K) {
+  if (tau == KEY_MAX) return 0x7fffffff;
+  return (int)khi(tau) - nx - (K > 1 ? 1 : 0);
+}
+
 // Optional epilogue instrumentation (PGK_TC_STATS=1): cycles / event counts.
 enum { ST_WAIT, ST_MAIN, ST_SLOW, ST_COMPACT, ST_FINAL, ST_NSLOW, ST_NCOMPACT, ST_NAPPEND,
        ST_COUNT };
 
 template <bool STATS>
-__global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
+// 112 registers keeps CTAS_PER_SM = 3 resident (3 x 6 warps x 112 x 32 <= 64K)
+__global__ void __maxnreg__(112)
     tc_pool_u8_kernel(const __grid_constant__ CUtensorMap tmX,
                       const __grid_constant__ CUtensorMap tmQ, int64_t n, int64_t nq,
                       int exclude_self, const int32_t *__restrict__ xnorm,
@@ -217,8 +227,9 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
                       uint64_t *__restrict__ out_keys, unsigned long long *stats,
                       const int32_t *__restrict__ tlist, const int32_t *__restrict__ tlen,
                       int64_t tstride, const int32_t *__restrict__ perm,
-                      const uint64_t *__restrict__ init_keys, int32_t *__restrict__ row_cnt,
-                      uint64_t *__restrict__ row_tau) {
+                      const uint64_t *__restrict__ init_keys, float shrink,
+                      int32_t *__restrict__ row_cnt, uint64_t *__restrict__ row_tau,
+                      int32_t *__restrict__ sched) {
   unsigned long long st[ST_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t_prev = STATS ? clock64() : 0;
 #define PGK_TICK(slot)                          \
@@ -267,12 +278,23 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmQ) : "memory");
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
+      // dynamic block schedule: claim the next block with work, publish its
+      // index in the 2-slot ring s.blk (read by MMA + epilogue after a_full);
+      // -1 ends the CTA
+      for (int it = 0;; ++it) {
+        int b, len = 0;
+        do {
+          b = atomicAdd(sched, 1);
+          if (b < nblocks) len = tlist ? tlen[b] : ntiles;
+        } while (b < nblocks && len == 0);
         mbar_wait(&s.a_empty, (it & 1) ^ 1);
+        s.blk[it & 1] = b < nblocks ? b : -1;
+        if (b >= nblocks) {
+          mbar_arrive(&s.a_full);
+          break;
+        }
         mbar_expect_tx(&s.a_full, BM * KB);
         tma_load_2d(s.a, &tmQ, &s.a_full, 0, b * BM);
-        const int len = tlist ? tlen[b] : ntiles;
         for (int t = 0; t < len; ++t) {
           const int tid = tlist ? tlist[(int64_t)b * tstride + t] : t;
           mbar_wait(&s.empty[stage], phase ^ 1);
@@ -287,12 +309,13 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       // ---------------- MMA issuer ----------------
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      int it = 0;
-      for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
+      for (int it = 0;; ++it) {
         mbar_wait(&s.a_full, it & 1);
+        const int b = s.blk[it & 1];
+        if (b < 0) break;
+        const int len = tlist ? tlen[b] : ntiles;
         tc_fence_after();
         const uint64_t adesc = sw128_desc(s.a);
-        const int len = tlist ? tlen[b] : ntiles;
         for (int t = 0; t < len; ++t) {
           const int tid = tlist ? tlist[(int64_t)b * tstride + t] : t;
           mbar_wait(&s.tempty[acc], acc_phase ^ 1);
@@ -318,29 +341,55 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   } else if (warp >= 2) {
     // ---------------- epilogue ----------------
     const int q = warp & 3;  // TMEM lane quarter this warp may access (warp % 4)
-    int32_t *sv = s.sv[warp - 2] + lane * 36;
+    int32_t *const svw = s.sv[warp - 2];  // this warp's staging: lane l at svw[l * 36]
+    int32_t *sv = svw + lane * 36;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int b = blockIdx.x; b < nblocks; b += gridDim.x) {
+    for (int it = 0;; ++it) {
+      mbar_wait(&s.a_full, it & 1);
+      const int b = s.blk[it & 1];
+      if (b < 0) break;
       const int64_t row = (int64_t)b * BM + q * 32 + lane;
       const bool row_ok = row < nq && (!perm || perm[row] >= 0);  // padding rows: no pool
       // per-row candidate buffers (global memory, CAP keys per row)
       uint64_t *wbuf = bufs + ((int64_t)b * BM + q * 32) * CAP;  // this warp's rows
-      uint64_t *mybuf = wbuf + (size_t)lane * CAP;
+      const int len = tlist ? tlen[b] : ntiles;
+      int tid_next = tlist ? tlist[(int64_t)b * tstride] : 0;  // prefetched one tile ahead
       const int nx = row_ok ? qnorm[row] : 0;
       int cnt = 0;
+      bool guessed = false;
+      // Row threshold.  K == 1: tau is the exact best key (keep key < tau).
+      // K > 1: tau = T << 32 with T an exclusive DISTANCE bound (keep dist < T),
+      // so the per-value prefilter below is the whole test.
       uint64_t tau = KEY_MAX;
       if (row_ok && init_keys) {
         // a previous pass's K-th key of this row (library key format) bounds
-        // its true K-th key from above: keep only keys <= it
+        // its true K-th key from above
         const uint64_t k0 = init_keys[(perm ? (int64_t)perm[row] : row) * K + K - 1];
-        if (k0 != KEY_MAX)
-          tau = (((uint64_t)(uint32_t)key_dist(k0) << 32) | (uint32_t)key_id(k0)) + 1;
+        if (k0 != KEY_MAX) {
+          const uint32_t d0 = (uint32_t)key_dist(k0);
+          if (K == 1) {
+            tau = (((uint64_t)d0 << 32) | (uint32_t)key_id(k0)) + 1;
+          } else {
+            // optionally a GUESS below the bound (shrink < 1): exact iff the
+            // pass still finds >= K keys under it, which finalize verifies
+            uint32_t t = d0 + 1;
+            if (shrink < 1.0f) {
+              const uint32_t g = (uint32_t)((double)d0 * (double)shrink);
+              if (g < t) {
+                t = g;
+                guessed = true;
+              }
+            }
+            tau = (uint64_t)t << 32;
+          }
+        }
       }
-      int tp = row_ok ? tau_prefilter(tau, nx) : -0x7fffffff;  // invalid rows never pass
-      const int len = tlist ? tlen[b] : ntiles;
+      int tp = row_ok ? row_tp(tau, nx, K) : -0x7fffffff;  // invalid rows never pass
+      int smax = -0x7fffffff;  // largest buffered s value while no threshold is set
       for (int t = 0; t < len; ++t) {
-        const int tid = tlist ? tlist[(int64_t)b * tstride + t] : t;
+        const int tid = tlist ? tid_next : t;
+        if (tlist && t + 1 < len) tid_next = tlist[(int64_t)b * tstride + t + 1];
         PGK_TICK(ST_MAIN);
         mbar_wait(&s.tfull[acc], acc_phase);
         tc_fence_after();
@@ -355,7 +404,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
           tmem_wait_ld();
           const int64_t cb = col0 + c * 32;
           const int4 *nyp = reinterpret_cast<const int4 *>(s.ny[acc] + c * 32);
-          // s_j = |x_j|^2 - 2 q.x_j ; pass iff s_j <= tau_dist - |q|^2
+          // s_j = |x_j|^2 - 2 q.x_j ; pass iff s_j <= tp
           uint32_t mask = 0;
 #pragma unroll
           for (int v = 0; v < 8; ++v) {
@@ -368,6 +417,14 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
           if (__any_sync(0xffffffffu, mask != 0)) {
             PGK_TICK(ST_MAIN);
             if (STATS) st[ST_NSLOW]++;
+            // exact survivor masks: lane j vouches for column cb + j (inside
+            // the data, not a padding slot of the tile sort), and a row never
+            // keeps itself
+            const int64_t colj = cb + lane;
+            const int32_t cidj = perm ? s.pid[acc][c * 32 + lane] : (int32_t)colj;
+            mask &= __ballot_sync(0xffffffffu, colj < n && cidj >= 0);
+            if (exclude_self && row >= cb && row < cb + 32) mask &= ~(1u << (int)(row - cb));
+            const bool track = K > 1 && tau == KEY_MAX && mask;
             if (mask) {
 #pragma unroll
               for (int v = 0; v < 8; ++v) {
@@ -380,19 +437,19 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
                 reinterpret_cast<int4 *>(sv)[v] = o;
               }
             }
+            __syncwarp();
+            if (track) {  // rare: rows still without a threshold
+              for (unsigned mm = mask; mm; mm &= mm - 1) smax = max(smax, sv[__ffs(mm) - 1]);
+            }
             if (K == 1) {  // nearest neighbour only: the threshold IS the answer
               while (mask) {
                 const int j = __ffs(mask) - 1;
                 mask &= mask - 1;
-                const int sj = sv[j];
-                const int64_t col = cb + j;
-                if (sj <= tp && col < n && !(exclude_self && col == row)) {
-                  const uint32_t cid = perm ? (uint32_t)s.pid[acc][c * 32 + j] : (uint32_t)col;
-                  const uint64_t key = ((uint64_t)(uint32_t)(sj + nx) << 32) | cid;
-                  if (key < tau) {
-                    tau = key;
-                    tp = tau_prefilter(tau, nx);
-                  }
+                const uint64_t key = ((uint64_t)(uint32_t)(sv[j] + nx) << 32) |
+                                     (uint32_t)(perm ? s.pid[acc][c * 32 + j] : (int32_t)(cb + j));
+                if (key < tau) {
+                  tau = key;
+                  tp = tau_prefilter(tau, nx);
                 }
               }
               __syncwarp();
@@ -407,27 +464,48 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
               const int c_src = __shfl_sync(0xffffffffu, cnt, src);
               const uint64_t t_src = __shfl_sync(0xffffffffu, tau, src);
               const uint64_t nt = select_k(wbuf + (size_t)src * CAP, c_src, K,
-                                           t_src == KEY_MAX ? (1u << 25) : khi(t_src), lane);
+                                           t_src == KEY_MAX ? 0xffffffffu : khi(t_src), lane);
               if (lane == src) {
                 cnt = K;
-                tau = nt;
-                tp = tau_prefilter(tau, nx);
+                tau = (uint64_t)(khi(nt) + 1) << 32;
+                tp = row_tp(tau, nx, K);
               }
             }
             PGK_TICK(ST_COMPACT);
-            const int cnt_before = cnt;
-            while (mask) {  // only lanes with survivors iterate
-              const int j = __ffs(mask) - 1;
-              mask &= mask - 1;
-              const int sj = sv[j];
-              const int64_t col = cb + j;
-              if (sj <= tp && col < n && !(exclude_self && col == row)) {
-                const uint32_t cid = perm ? (uint32_t)s.pid[acc][c * 32 + j] : (uint32_t)col;
-                const uint64_t key = ((uint64_t)(uint32_t)(sj + nx) << 32) | cid;
-                if (key < tau) mybuf[cnt++] = key;
+            unsigned has = __ballot_sync(0xffffffffu, mask != 0);
+            const int maxc = (int)__reduce_max_sync(0xffffffffu, (unsigned)__popc(mask));
+            if (maxc >= 8 || 2 * maxc >= __popc(has)) {
+              // dense: one coalesced store per row with survivors, the warp
+              // writes that row's keys (lane j: column j) at its buffer end
+              while (has) {
+                const int src = __ffs(has) - 1;
+                has &= has - 1;
+                const unsigned m = __shfl_sync(0xffffffffu, mask, src);
+                const int c0 = __shfl_sync(0xffffffffu, cnt, src);
+                const int nxs = __shfl_sync(0xffffffffu, nx, src);
+                if ((m >> lane) & 1u)
+                  wbuf[(size_t)src * CAP + c0 + __popc(m & lanemask_lt())] =
+                      ((uint64_t)(uint32_t)(svw[src * 36 + lane] + nxs) << 32) | (uint32_t)cidj;
+              }
+            } else {
+              // sparse: every lane appends its own few survivors
+              uint64_t *mybuf = wbuf + (size_t)lane * CAP + cnt;
+              unsigned mm = mask;
+              while (mm) {
+                const int j = __ffs(mm) - 1;
+                mm &= mm - 1;
+                const int32_t cid = perm ? s.pid[acc][c * 32 + j] : (int32_t)(cb + j);
+                *mybuf++ = ((uint64_t)(uint32_t)(sv[j] + nx) << 32) | (uint32_t)cid;
               }
             }
-            if (STATS) st[ST_NAPPEND] += cnt - cnt_before;
+            cnt += __popc(mask);
+            if (STATS) st[ST_NAPPEND] += __popc(mask);
+            // no threshold yet but K keys buffered: their largest distance + 1
+            // bounds the K-th distance from above (exclusive)
+            if (track && cnt >= K) {
+              tau = (uint64_t)((uint32_t)(smax + nx) + 1) << 32;
+              tp = row_tp(tau, nx, K);
+            }
             __syncwarp();
             PGK_TICK(ST_SLOW);
           }
@@ -442,7 +520,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       // and sorting run in the massively parallel finalize kernel
       PGK_TICK(ST_MAIN);
       if (row < nq) {
-        row_cnt[row] = row_ok ? cnt : -1;
+        row_cnt[row] = row_ok ? (cnt | (guessed ? GUESSED : 0)) : -1;
         row_tau[row] = tau;
       }
       PGK_TICK(ST_FINAL);
@@ -506,12 +584,22 @@ __device__ __forceinline__ void finalize_row(uint64_t *buf, int cnt, uint64_t ta
 __global__ void tc_finalize_kernel(uint64_t *__restrict__ bufs, const int32_t *__restrict__ row_cnt,
                                    const uint64_t *__restrict__ row_tau, int64_t nrows, int K,
                                    const int32_t *__restrict__ perm, int kth_only,
-                                   uint64_t *__restrict__ out_keys) {
+                                   uint64_t *__restrict__ out_keys,
+                                   int32_t *__restrict__ fail_blocks,
+                                   const int32_t *__restrict__ tlen) {
   const int lane = threadIdx.x & 31;
   for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < nrows;
        r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int cnt = row_cnt[r];
-    if (cnt < 0) continue;  // padding row
+    if (tlen && tlen[r / BM] == 0) continue;  // block not scheduled in this launch
+    const int raw = row_cnt[r];
+    if (raw < 0) continue;  // padding row
+    const int cnt = raw & ~GUESSED;
+    if ((raw & GUESSED) && cnt < K) {
+      // the guessed threshold was too tight: leave the row's seed in place
+      // and have its block re-run with the true bound
+      if (lane == 0) fail_blocks[r / BM] = 1;
+      continue;
+    }
     uint64_t *o = out_keys + (perm ? (int64_t)perm[r] : r) * K;
     uint64_t *b = bufs + r * CAP;
     const uint64_t tau = row_tau[r];
@@ -569,6 +657,7 @@ size_t tc_pool_workspace(int64_t n, int64_t nq, bool self) {
   const int64_t rows = (nq + tc::BM - 1) / tc::BM * tc::BM;
   b += (size_t)rows * tc::CAP * sizeof(uint64_t) + 1024;  // per-row candidate buffers
   b += (size_t)rows * (sizeof(int32_t) + sizeof(uint64_t)) + 2048;
+  b += 256;  // dynamic block-schedule counter
   return b;
 }
 
@@ -589,8 +678,12 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             cudaStream_t stream, const uint8_t *xs_sorted,
                             const int32_t *tlist, const int32_t *tlen, int64_t tstride,
                             const int32_t *perm, bool *handled, const uint64_t *init_keys,
-                            int kth_only) {
+                            int kth_only, float shrink, int32_t *fail_blocks) {
   *handled = false;
+  if (shrink < 1.0f && !fail_blocks) {
+    set_error("guessed thresholds need a fail-block array");
+    return PGK_ERR_INVALID;
+  }
   if (!tc_pool_supported(d, K)) return PGK_OK;
   const bool self = (Q == X);
   if (tc_bytes < tc_pool_workspace(n, nq, self)) {
@@ -605,6 +698,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   uint64_t *bufs = c.take<uint64_t>((size_t)rows * tc::CAP);
   int32_t *row_cnt = c.take<int32_t>(rows);
   uint64_t *row_tau = c.take<uint64_t>(rows);
+  int32_t *sched = c.take<int32_t>(1);
   const unsigned cg = (unsigned)std::min<int64_t>((n * tc::KB + 255) / 256, (int64_t)sms * 16);
   if (xs_sorted) {
     xu8 = qu8 = const_cast<uint8_t *>(xs_sorted);  // already u8, permuted by the tile sort
@@ -637,6 +731,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   }
   const int nblocks = (int)((nq + tc::BM - 1) / tc::BM);
   const unsigned grid = (unsigned)std::min<int64_t>(nblocks, (int64_t)tc::CTAS_PER_SM * sms);
+  PGK_CUDA(cudaMemsetAsync(sched, 0, sizeof(int32_t), stream));
   const char *se = getenv("PGK_TC_STATS");
   if (se && se[0] == '1') {
     unsigned long long *dstats = nullptr;
@@ -644,7 +739,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
     PGK_CUDA(cudaMemsetAsync(dstats, 0, sizeof(unsigned long long) * tc::ST_COUNT, stream));
     tc::tc_pool_u8_kernel<true><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, dstats, tlist, tlen,
-        tstride, perm, init_keys, row_cnt, row_tau);
+        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel<stats>");
     unsigned long long h[tc::ST_COUNT];
     PGK_CUDA(cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, stream));
@@ -659,11 +754,12 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   } else {
     tc::tc_pool_u8_kernel<false><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
-        tstride, perm, init_keys, row_cnt, row_tau);
+        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel");
   }
   tc::tc_finalize_kernel<<<(unsigned)sms * 16, 256, 0, stream>>>(bufs, row_cnt, row_tau, nq, K,
-                                                                  perm, kth_only, keys);
+                                                                  perm, kth_only, keys,
+                                                                  fail_blocks, tlist ? tlen : nullptr);
   PGK_CHECK_LAUNCH("tc_finalize_kernel");
   *handled = true;
   return PGK_OK;

@@ -20,6 +20,7 @@
 // ties still break on the original id).  All bounds are float64 with explicit
 // relative margins, far above the float64 rounding of the inputs.
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -286,9 +287,33 @@ __global__ void tile_filter_kernel(const float *__restrict__ dc, const double *_
   }
 }
 
+// Blocks whose guessed pass-2 threshold failed somewhere keep their list for
+// the re-run; every other block gets an empty list (skipped).
+__global__ void rerun_lens_kernel(const int32_t *__restrict__ fail,
+                                  const int32_t *__restrict__ lens, int64_t T,
+                                  int32_t *__restrict__ lens2) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T;
+       t += (int64_t)gridDim.x * blockDim.x)
+    lens2[t] = fail[t] ? lens[t] : 0;
+}
+
+// Pass-2 threshold guess: seed * SHRINK (exclusive squared-distance bound).
+// In high dimension the final K-th distance is a near-constant fraction of
+// the pass-1 seed (config 2: 0.86-0.92), so the guess cuts the buffered
+// survivors ~2.5x; rows where it proves too tight re-run with the seed.
+static float seed_shrink() {
+  static float v = -1.0f;
+  if (v < 0.0f) {
+    const char *e = getenv("PGK_SEED_SHRINK");
+    v = e ? (float)atof(e) : 0.93f;
+    if (!(v > 0.0f && v <= 1.0f)) v = 1.0f;
+  }
+  return v;
+}
+
 struct Layout {
   float *cen, *cent, *dcm;
-  int32_t *cnorm, *hist, *cursor, *assign, *perm, *ns, *size, *lists, *lens;
+  int32_t *cnorm, *hist, *cursor, *assign, *perm, *ns, *size, *lists, *lens, *fail, *lens2;
   int64_t *off, *scan_tmp;
   uint64_t *akeys;
   double *rad, *U;
@@ -309,7 +334,8 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             cudaStream_t stream, const uint8_t *xs_sorted,
                             const int32_t *tlist, const int32_t *tlen, int64_t tstride,
                             const int32_t *perm, bool *handled,
-                            const uint64_t *init_keys = nullptr, int kth_only = 0);
+                            const uint64_t *init_keys = nullptr, int kth_only = 0,
+                            float shrink = 1.0f, int32_t *fail_blocks = nullptr);
 
 static tiles::Layout tiles_layout(void *ws, size_t bytes, int64_t n, int64_t d) {
   using namespace tiles;
@@ -335,6 +361,8 @@ static tiles::Layout tiles_layout(void *ws, size_t bytes, int64_t n, int64_t d) 
   L.size = c.take<int32_t>(T);
   L.lists = c.take<int32_t>((size_t)T * T);
   L.lens = c.take<int32_t>(T);
+  L.fail = c.take<int32_t>(T);
+  L.lens2 = c.take<int32_t>(T);
   L.dcm = c.take<float>((size_t)T * T);
   L.U = c.take<double>(T);
   L.total = c.take<unsigned long long>(4);
@@ -426,16 +454,67 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   tile_filter_kernel<<<g, 256, 0, stream>>>(L.dcm, L.rad, L.size, L.U, T, L.lists, L.lens,
                                             L.total);
   PGK_CHECK_LAUNCH("tile_filter_kernel");
+  const char *se = getenv("PGK_TILES_STATS");
+  const bool stats = se && se[0] == '1';
+  std::vector<uint64_t> seed_k, final_k;
+  if (stats) {  // each row's pass-1 K-th key (the pass-2 seed)
+    seed_k.resize(n);
+    PGK_CUDA(cudaMemcpy2DAsync(seed_k.data(), 8, keys + K - 1, (size_t)K * 8, 8, n,
+                               cudaMemcpyDeviceToHost, stream));
+  }
+  const float shrink = seed_shrink();
+  PGK_CUDA(cudaMemsetAsync(L.fail, 0, T * 4, stream));
   rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes, stream,
-                               L.xs, L.lists, L.lens, T, L.perm, handled, keys);
+                               L.xs, L.lists, L.lens, T, L.perm, handled, keys, 0, shrink,
+                               L.fail);
   if (rc) return rc;
+  if (shrink < 1.0f) {
+    // 6. re-run the blocks holding a row whose guess was too tight, seeded by
+    // its untouched pass-1 key (finished rows re-derive the same result)
+    rerun_lens_kernel<<<g, 256, 0, stream>>>(L.fail, L.lens, T, L.lens2);
+    PGK_CHECK_LAUNCH("rerun_lens_kernel");
+    if (stats) {
+      std::vector<int32_t> hf(T);
+      PGK_CUDA(cudaMemcpyAsync(hf.data(), L.fail, T * 4, cudaMemcpyDeviceToHost, stream));
+      PGK_CUDA(cudaStreamSynchronize(stream));
+      int64_t nf = 0;
+      for (auto f : hf) nf += f != 0;
+      fprintf(stderr, "[tiles] guess %.3f: %lld of %lld blocks re-run\n", shrink, (long long)nf,
+              (long long)T);
+    }
+    rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes,
+                                 stream, L.xs, L.lists, L.lens2, T, L.perm, handled, keys);
+    if (rc) return rc;
+  }
+  if (stats) {
+    final_k.resize(n);
+    PGK_CUDA(cudaMemcpy2DAsync(final_k.data(), 8, keys + K - 1, (size_t)K * 8, 8, n,
+                               cudaMemcpyDeviceToHost, stream));
+    PGK_CUDA(cudaStreamSynchronize(stream));
+    std::vector<double> ratio;
+    for (int64_t i = 0; i < n; ++i) {
+      const uint32_t a = (uint32_t)(seed_k[i] >> 32) & 0x7fffffffu,
+                     b = (uint32_t)(final_k[i] >> 32) & 0x7fffffffu;
+      float fa, fb;
+      memcpy(&fa, &a, 4);
+      memcpy(&fb, &b, 4);
+      if (fa > 0) ratio.push_back(fb / fa);
+    }
+    std::sort(ratio.begin(), ratio.end());
+    auto qq = [&](double f) { return ratio.empty() ? 0.0 : ratio[(size_t)(f * (ratio.size() - 1))]; };
+    fprintf(stderr, "[tiles] final/seed K-th dist ratio p1/p10/p50/p90/p99 %.3f %.3f %.3f %.3f %.3f max %.3f\n",
+            qq(.01), qq(.1), qq(.5), qq(.9), qq(.99), qq(1.0));
+    for (double f : {0.90, 0.92, 0.93, 0.94, 0.95, 0.96}) {
+      const size_t above = ratio.end() - std::lower_bound(ratio.begin(), ratio.end(), f);
+      fprintf(stderr, "[tiles]   rows with ratio >= %.2f: %zu\n", f, above);
+    }
+  }
   {  // work record: [0] pass-2 tile pairs, [1] pass-1 pairs, [2] assignment pairs, [3] done
     const unsigned long long rec[2] = {
         (unsigned long long)((n + TB - 1) / TB) * (unsigned long long)((C + TB - 1) / TB), 1ull};
     PGK_CUDA(cudaMemcpyAsync(L.total + 2, rec, sizeof(rec), cudaMemcpyHostToDevice, stream));
   }
-  const char *se = getenv("PGK_TILES_STATS");
-  if (se && se[0] == '1') {
+  if (stats) {
     unsigned long long tot = 0;
     PGK_CUDA(cudaMemcpyAsync(&tot, L.total, sizeof(tot), cudaMemcpyDeviceToHost, stream));
     std::vector<double> hr(T), hu(T);

@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--n", type=int, default=131072)
     ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--kernels", action="store_true",
+                    help="per-kernel device time of the last rep (CUPTI trace)")
     a = ap.parse_args()
     c = synth.CONFIGS[a.config]
     data = c["gen"](a.n) if a.config == 1 else c["gen"](a.n, c["n"])
@@ -30,7 +32,11 @@ def main():
     ids, d = b.pools(X)
     torch.cuda.synchronize()
     p = b.params
-    for _ in range(a.reps):
+    prof = None
+    for rep in range(a.reps):
+        if a.kernels and rep == a.reps - 1:
+            prof = torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA])
+            prof.__enter__()
         t0 = time.perf_counter()
         if a.stage in ("pool", "all"):
             ids, d = b.pools(X)
@@ -46,6 +52,12 @@ def main():
                                           out=b.b_out, u8=u8, order=order)
         torch.cuda.synchronize()
         print(f"{a.stage} n={a.n}: {1e3 * (time.perf_counter() - t0):.2f} ms")
+    if prof is not None:
+        prof.__exit__(None, None, None)
+        seq = [(e.name, e.device_time) for e in prof.events()
+               if e.device_type == torch.autograd.DeviceType.CUDA]
+        for name, us in seq:
+            print(f"  {us / 1e3:8.3f} ms  {name[:90]}")
 
 
 if __name__ == "__main__":
