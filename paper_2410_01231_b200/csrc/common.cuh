@@ -158,6 +158,13 @@ __device__ __forceinline__ float key_dist(uint64_t k) {
 }
 constexpr uint64_t KEY_MAX = ~0ull;
 
+// Pool output arrays a kernel may write directly (row-major nq x K).
+struct PoolOut {
+  int32_t *gt_ids;  // optional
+  int32_t *ids;
+  float *dists;
+};
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

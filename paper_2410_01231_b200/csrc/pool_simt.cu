@@ -585,11 +585,13 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             const int32_t *tlist, const int32_t *tlen, int64_t tstride,
                             const int32_t *perm, bool *handled,
                             const uint64_t *init_keys = nullptr, int kth_only = 0,
-                            float shrink = 1.0f, int32_t *fail_blocks = nullptr);
+                            float shrink = 1.0f, int32_t *fail_blocks = nullptr,
+                            const PoolOut *out = nullptr, uint8_t *fail_rows = nullptr,
+                            const uint8_t *row_mask = nullptr);
 int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm, int K,
                          uint64_t *keys, void *tc_ws, size_t tc_bytes, void *tws,
                          size_t tws_bytes, cudaStream_t stream, bool *handled,
-                         unsigned long long *pairs_out);
+                         unsigned long long *pairs_out, const PoolOut *out);
 
 int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, int64_t k,
               int exclude_self, int mode, int32_t *gt_ids, int32_t *pool_ids,
@@ -641,18 +643,22 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
       qn = L.qnorm;
     }
     bool handled = false;
+    // the tensor-core paths write the pool arrays directly from their finalize
+    const PoolOut po{gt_ids, pool_ids, pool_dists};
     if (L.tc_ws && L.tws && self && exclude_self) {
       rc = launch_pool_tiles_u8(X, n, (int)d, L.xnorm, (int)k, L.keys, L.tc_ws, L.tc_bytes,
-                                L.tws, L.tws_bytes, stream, &handled, nullptr);
+                                L.tws, L.tws_bytes, stream, &handled, nullptr, &po);
       if (rc) return rc;
     }
     if (L.tc_ws && !handled) {
       rc = launch_pool_tc_u8_lists(X, n, (int)d, Q, nq, exclude_self, L.xnorm, qn, (int)k,
                                    L.keys, L.tc_ws, L.tc_bytes, stream, nullptr, nullptr,
-                                   nullptr, 0, nullptr, &handled);
+                                   nullptr, 0, nullptr, &handled, nullptr, 0, 1.0f, nullptr,
+                                   &po);
       if (rc) return rc;
     }
-    if (!handled) {
+    if (handled) return PGK_OK;
+    {
       rc = S <= 224 ? launch_tile<MODE_U8, 256>(X, n, (int)d, Q, nq, exclude_self, L.xnorm,
                                                 qn, S, vec4, L.keys, stream)
                     : launch_tile<MODE_U8, 512>(X, n, (int)d, Q, nq, exclude_self, L.xnorm,

@@ -229,7 +229,7 @@ __global__ void __maxnreg__(112)
                       int64_t tstride, const int32_t *__restrict__ perm,
                       const uint64_t *__restrict__ init_keys, float shrink,
                       int32_t *__restrict__ row_cnt, uint64_t *__restrict__ row_tau,
-                      int32_t *__restrict__ sched) {
+                      int32_t *__restrict__ sched, const uint8_t *__restrict__ row_mask) {
   unsigned long long st[ST_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t_prev = STATS ? clock64() : 0;
 #define PGK_TICK(slot)                          \
@@ -350,7 +350,9 @@ __global__ void __maxnreg__(112)
       const int b = s.blk[it & 1];
       if (b < 0) break;
       const int64_t row = (int64_t)b * BM + q * 32 + lane;
-      const bool row_ok = row < nq && (!perm || perm[row] >= 0);  // padding rows: no pool
+      // padding rows (and, in a re-run, rows already finished): no pool
+      const bool row_ok =
+          row < nq && (!perm || perm[row] >= 0) && (!row_mask || row_mask[row]);
       // per-row candidate buffers (global memory, CAP keys per row)
       uint64_t *wbuf = bufs + ((int64_t)b * BM + q * 32) * CAP;  // this warp's rows
       const int len = tlist ? tlen[b] : ntiles;
@@ -546,50 +548,283 @@ __global__ void __maxnreg__(112)
   }
 }
 
-// Warp per (sorted) row: cut the row's buffer to its K best keys (selection
-// only when it holds more), then either the sorted K (FULL) or only the K-th
-// key (KTH, the pass-1 bound) in the library key format at the original row.
-template <int NPL>
-__device__ __forceinline__ void finalize_row(uint64_t *buf, int cnt, uint64_t tau, int K,
-                                             bool kth_only, uint64_t *out, int lane) {
-  if (K == 1) {
-    if (lane == 0)
-      out[0] = tau == KEY_MAX ? KEY_MAX : pack_key((float)khi(tau), (int32_t)(uint32_t)tau);
-    return;
+// ---------------------------------------------------------------------------
+// Finalize: warp per (sorted) row.  Radix selection on the register-resident
+// buffer (8-bit digits of the row's value range, one 256-bin shared-memory
+// histogram per warp), then the K survivors sorted by a lane-contiguous
+// bitonic network.
+// ---------------------------------------------------------------------------
+constexpr int FIN_WARPS = 8;
+constexpr int FIN_STAGE = 256;  // max K
+
+struct FinOut {          // optional direct pool output (pool_simt's arrays)
+  int32_t *gt_ids;       // may be null
+  int32_t *ids;
+  float *dists;
+};
+
+// The need-th smallest participating value (ON_ID: ids of the keys whose
+// distance is tie_d; else distances), need 1-based and updated to the rank
+// left inside the returned value.  With max_passes too small to resolve every
+// digit (exact = false) the result is the upper edge of the selected bucket:
+// an upper bound on the need-th value.
+template <int KPL, bool ON_ID>
+__device__ __forceinline__ uint32_t radix_pick(const uint64_t (&kk)[KPL], int cnt, uint32_t tie_d,
+                                               int &need, uint32_t *hist, int lane,
+                                               int max_passes, bool &exact) {
+  uint32_t vmin = 0xffffffffu, vmax = 0;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const bool p = i * 32 + lane < cnt && (!ON_ID || khi(kk[i]) == tie_d);
+    const uint32_t v = ON_ID ? (uint32_t)kk[i] : khi(kk[i]);
+    if (p) {
+      vmin = min(vmin, v);
+      vmax = max(vmax, v);
+    }
   }
-  uint64_t kth = KEY_MAX;
-  if (cnt > K) {
-    kth = select_k(buf, cnt, K, tau == KEY_MAX ? (1u << 25) : khi(tau), lane);
-    cnt = K;
+  vmin = __reduce_min_sync(0xffffffffu, vmin);
+  vmax = __reduce_max_sync(0xffffffffu, vmax);
+  const uint32_t range = vmax - vmin;
+  int shift = range ? 32 - __clz(range) : 0;
+  uint32_t prefix = 0;
+  for (int pass = 0; shift > 0 && pass < max_passes; ++pass) {
+    const int dig = min(8, shift);
+    shift -= dig;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) hist[t * 32 + lane] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const bool p = i * 32 + lane < cnt && (!ON_ID || khi(kk[i]) == tie_d);
+      const uint32_t v = ((ON_ID ? (uint32_t)kk[i] : khi(kk[i])) - vmin) >> shift;
+      if (p && (v >> dig) == prefix) atomicAdd(&hist[v & ((1u << dig) - 1)], 1u);
+    }
+    __syncwarp();
+    uint32_t c[8], sum = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      c[t] = hist[lane * 8 + t];
+      sum += c[t];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - sum, nd = (uint32_t)need;
+    const int src = __ffs(__ballot_sync(0xffffffffu, excl < nd && nd <= incl)) - 1;
+    int found = 0;
+    uint32_t acc = excl, below = 0;
+    bool done = false;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      if (!done && acc + c[t] >= nd) {
+        found = t;
+        below = acc;
+        done = true;
+      }
+      acc += c[t];
+    }
+    const int bsel = __shfl_sync(0xffffffffu, lane * 8 + found, src);
+    need -= (int)__shfl_sync(0xffffffffu, below, src);
+    prefix = (prefix << dig) | (uint32_t)bsel;
+    __syncwarp();
   }
-  if (kth_only && cnt == K && kth != KEY_MAX) {
-    if (lane == 0) out[K - 1] = pack_key((float)khi(kth), (int32_t)(uint32_t)kth);
-    return;
+  exact = shift == 0;
+  return exact ? vmin + prefix : vmin + (((prefix + 1) << shift) - 1);
+}
+
+// exact K-th smallest (dist, id) key of cnt > K register-resident keys
+template <int KPL>
+__device__ __forceinline__ uint64_t radix_kth(const uint64_t (&kk)[KPL], int cnt, int K,
+                                              uint32_t *hist, int lane) {
+  int need = K;
+  bool exact;
+  const uint32_t td = radix_pick<KPL, false>(kk, cnt, 0, need, hist, lane, 4, exact);
+  int ties = 0;
+  uint32_t idmax = 0;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i)
+    if (i * 32 + lane < cnt && khi(kk[i]) == td) {
+      ++ties;
+      idmax = max(idmax, (uint32_t)kk[i]);
+    }
+  ties = (int)__reduce_add_sync(0xffffffffu, (unsigned)ties);
+  uint32_t tid;
+  if (ties == need) {  // every key at the K-th distance is in: the largest id
+    tid = __reduce_max_sync(0xffffffffu, idmax);
+  } else {             // ties straddle the cut: smallest ids win
+    tid = radix_pick<KPL, true>(kk, cnt, td, need, hist, lane, 4, exact);
   }
-  uint64_t e[NPL];
+  return ((uint64_t)td << 32) | tid;
+}
+
+// bitonic sort of 32*NPL u32 keys, lane-contiguous (element lane*NPL + s):
+// the (k, j) stage loops stay rolled (one copy of each stage body, I-cache)
+template <int NPL, int J>
+__device__ __forceinline__ void bitonic_reg_stage(uint32_t (&e)[NPL], int k, int lane) {
 #pragma unroll
   for (int s0 = 0; s0 < NPL; ++s0) {
-    const int idx = s0 * 32 + lane;
-    e[s0] = idx < cnt ? buf[idx] : KEY_MAX;
-  }
-  reg_bitonic<NPL>(e, lane);
-#pragma unroll
-  for (int s0 = 0; s0 < NPL; ++s0) {
-    const int idx = s0 * 32 + lane;
-    if (idx < K && (!kth_only || idx == K - 1))
-      out[idx] = e[s0] == KEY_MAX ? KEY_MAX : pack_key((float)khi(e[s0]), (int32_t)(uint32_t)e[s0]);
+    if (s0 & J) continue;
+    const int s1 = s0 | J;
+    const bool up = ((lane * NPL + s0) & k) == 0;
+    const uint32_t a = e[s0], b = e[s1];
+    const bool sw = (a > b) == up;
+    e[s0] = sw ? b : a;
+    e[s1] = sw ? a : b;
   }
 }
 
-__global__ void tc_finalize_kernel(uint64_t *__restrict__ bufs, const int32_t *__restrict__ row_cnt,
-                                   const uint64_t *__restrict__ row_tau, int64_t nrows, int K,
-                                   const int32_t *__restrict__ perm, int kth_only,
-                                   uint64_t *__restrict__ out_keys,
-                                   int32_t *__restrict__ fail_blocks,
-                                   const int32_t *__restrict__ tlen) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < nrows;
-       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+template <int NPL>
+__device__ __forceinline__ void bitonic_contig(uint32_t (&e)[NPL], int lane) {
+#pragma unroll 1
+  for (int k = 2; k <= 32 * NPL; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= NPL) {
+        const int lj = j / NPL;
+        const bool lower = (lane & lj) == 0;
+#pragma unroll
+        for (int s0 = 0; s0 < NPL; ++s0) {
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, e[s0], lj);
+          const bool up = ((lane * NPL + s0) & k) == 0;
+          e[s0] = (lower == up) ? min(e[s0], o) : max(e[s0], o);
+        }
+      } else if (NPL > 4 && j == 4) {
+        bitonic_reg_stage<NPL, (NPL > 4 ? 4 : 1)>(e, k, lane);
+      } else if (NPL > 2 && j == 2) {
+        bitonic_reg_stage<NPL, (NPL > 2 ? 2 : 1)>(e, k, lane);
+      } else {
+        bitonic_reg_stage<NPL, 1>(e, k, lane);
+      }
+    }
+  }
+}
+
+// Sort the staged keys (KEY_MAX padded to 32*NPL) and write the row.  The
+// network sorts u32 (dist << 8 | slot) -- exact u8 distances are < 2^23 and
+// K <= 256 -- then odd-even transposition passes on the gathered 64-bit keys
+// put equal distances into id order (runs of ties are short: ~2 passes).
+template <int NPL>
+__device__ __noinline__ void sort_emit(const uint64_t *stage, int K, int64_t orow,
+                                       uint64_t *out_keys, FinOut fo, int lane) {
+  uint32_t e[NPL];
+#pragma unroll
+  for (int s0 = 0; s0 < NPL; ++s0) {
+    const int idx = lane * NPL + s0;
+    const uint64_t k = stage[idx];
+    e[s0] = k == KEY_MAX ? 0xffffffffu : (khi(k) << 8) | (uint32_t)idx;
+  }
+  bitonic_contig<NPL>(e, lane);
+  uint64_t k[NPL];
+#pragma unroll
+  for (int s0 = 0; s0 < NPL; ++s0) k[s0] = e[s0] == 0xffffffffu ? KEY_MAX : stage[e[s0] & 0xffu];
+  int quiet = 0;
+#pragma unroll 1
+  for (int par = 0; quiet < 2; par ^= 1) {
+    bool sw = false;
+#pragma unroll
+    for (int s0 = 0; s0 + 1 < NPL; ++s0)
+      if (((lane * NPL + s0) & 1) == par && k[s0] > k[s0 + 1]) {
+        const uint64_t t = k[s0];
+        k[s0] = k[s0 + 1];
+        k[s0 + 1] = t;
+        sw = true;
+      }
+    const uint64_t nxt = __shfl_down_sync(0xffffffffu, k[0], 1);
+    const uint64_t prv = __shfl_up_sync(0xffffffffu, k[NPL - 1], 1);
+    if (lane < 31 && ((lane * NPL + NPL - 1) & 1) == par && k[NPL - 1] > nxt) {
+      k[NPL - 1] = nxt;
+      sw = true;
+    }
+    if (lane > 0 && (((lane - 1) * NPL + NPL - 1) & 1) == par && prv > k[0]) k[0] = prv;
+    quiet = __any_sync(0xffffffffu, sw) ? 0 : quiet + 1;
+  }
+#pragma unroll
+  for (int s0 = 0; s0 < NPL; ++s0) {
+    const int idx = lane * NPL + s0;
+    if (idx >= K) continue;
+    const uint64_t kk = k[s0];
+    if (fo.ids) {
+      const int32_t id = kk == KEY_MAX ? -1 : (int32_t)(uint32_t)kk;
+      fo.ids[orow * K + idx] = id;
+      fo.dists[orow * K + idx] = kk == KEY_MAX ? __int_as_float(0x7f800000) : (float)khi(kk);
+      if (fo.gt_ids) fo.gt_ids[orow * K + idx] = id;
+    } else {
+      out_keys[orow * K + idx] =
+          kk == KEY_MAX ? KEY_MAX : pack_key((float)khi(kk), (int32_t)(uint32_t)kk);
+    }
+  }
+}
+
+// select (cnt > K) and stage the row's best min(cnt, K) keys, or (kth_only)
+// write the pass-1 bound; returns true when the staged keys need sort_emit
+template <int KPL>
+__device__ __noinline__ bool select_stage(const uint64_t *__restrict__ buf, int cnt, int K,
+                                          bool kth_only, int64_t orow, uint64_t *out_keys,
+                                          uint32_t *hist, uint64_t *stage, int npl32,
+                                          int lane) {
+  uint64_t kk[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) kk[i] = i * 32 + lane < cnt ? buf[i * 32 + lane] : KEY_MAX;
+  if (kth_only) {
+    // pass-1 bound: any key >= the true K-th serves; one histogram pass
+    // gives the K-th distance to within 1/256 of the row's range
+    uint64_t kth = KEY_MAX;
+    if (cnt >= K) {
+      int need = K;
+      bool exact;
+      const uint32_t d = radix_pick<KPL, false>(kk, cnt, 0, need, hist, lane, 1, exact);
+      kth = pack_key((float)d, 0x7fffffff);
+    }
+    if (lane == 0) out_keys[orow * K + K - 1] = kth;
+    return false;
+  }
+  const uint64_t tau = cnt > K ? radix_kth<KPL>(kk, cnt, K, hist, lane) : KEY_MAX;
+  int base = 0;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const bool keep = i * 32 + lane < cnt && kk[i] <= tau;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) stage[base + __popc(bal & lanemask_lt())] = kk[i];
+    base += __popc(bal);
+  }
+  for (int j = base + lane; j < npl32; j += 32) stage[j] = KEY_MAX;
+  __syncwarp();
+  return true;
+}
+
+template <int NPL>
+__device__ __forceinline__ void finalize_row(const uint64_t *buf, int cnt, int K, bool kth_only,
+                                             int64_t orow, uint64_t *out_keys, FinOut fo,
+                                             uint32_t *hist, uint64_t *stage, int lane) {
+  bool sort;
+  if (cnt <= 128)
+    sort = select_stage<4>(buf, cnt, K, kth_only, orow, out_keys, hist, stage, 32 * NPL, lane);
+  else if (cnt <= 256)
+    sort = select_stage<8>(buf, cnt, K, kth_only, orow, out_keys, hist, stage, 32 * NPL, lane);
+  else if (cnt <= 512)
+    sort = select_stage<16>(buf, cnt, K, kth_only, orow, out_keys, hist, stage, 32 * NPL, lane);
+  else
+    sort = select_stage<CAP / 32>(buf, cnt, K, kth_only, orow, out_keys, hist, stage, 32 * NPL,
+                                  lane);
+  if (sort) sort_emit<NPL>(stage, K, orow, out_keys, fo, lane);
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(FIN_WARPS * 32, 4)
+    tc_finalize_kernel(const uint64_t *__restrict__ bufs, const int32_t *__restrict__ row_cnt,
+                       const uint64_t *__restrict__ row_tau, int64_t nrows, int K,
+                       const int32_t *__restrict__ perm, int kth_only,
+                       uint64_t *__restrict__ out_keys, int32_t *__restrict__ fail_blocks,
+                       uint8_t *__restrict__ fail_rows, const int32_t *__restrict__ tlen,
+                       FinOut fo) {
+  __shared__ uint32_t s_hist[FIN_WARPS][256];
+  __shared__ uint64_t s_stage[FIN_WARPS][FIN_STAGE];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t r = (int64_t)blockIdx.x * FIN_WARPS + warp; r < nrows;
+       r += (int64_t)gridDim.x * FIN_WARPS) {
     if (tlen && tlen[r / BM] == 0) continue;  // block not scheduled in this launch
     const int raw = row_cnt[r];
     if (raw < 0) continue;  // padding row
@@ -597,16 +832,34 @@ __global__ void tc_finalize_kernel(uint64_t *__restrict__ bufs, const int32_t *_
     if ((raw & GUESSED) && cnt < K) {
       // the guessed threshold was too tight: leave the row's seed in place
       // and have its block re-run with the true bound
-      if (lane == 0) fail_blocks[r / BM] = 1;
+      if (lane == 0) {
+        fail_blocks[r / BM] = 1;
+        fail_rows[r] = 1;
+      }
       continue;
     }
-    uint64_t *o = out_keys + (perm ? (int64_t)perm[r] : r) * K;
-    uint64_t *b = bufs + r * CAP;
-    const uint64_t tau = row_tau[r];
-    if (K <= 32) finalize_row<1>(b, cnt, tau, K, kth_only, o, lane);
-    else if (K <= 64) finalize_row<2>(b, cnt, tau, K, kth_only, o, lane);
-    else if (K <= 128) finalize_row<4>(b, cnt, tau, K, kth_only, o, lane);
-    else finalize_row<8>(b, cnt, tau, K, kth_only, o, lane);
+    const int64_t orow = perm ? (int64_t)perm[r] : r;
+    if (K == 1) {  // the kernel's threshold is the answer
+      const uint64_t tau = row_tau[r];
+      if (lane == 0) {
+        if (fo.ids && !kth_only) {
+          fo.ids[orow] = tau == KEY_MAX ? -1 : (int32_t)(uint32_t)tau;
+          fo.dists[orow] = tau == KEY_MAX ? __int_as_float(0x7f800000) : (float)khi(tau);
+          if (fo.gt_ids) fo.gt_ids[orow] = fo.ids[orow];
+        } else {
+          out_keys[orow] =
+              tau == KEY_MAX ? KEY_MAX : pack_key((float)khi(tau), (int32_t)(uint32_t)tau);
+        }
+      }
+      continue;
+    }
+    const uint64_t *b = bufs + r * CAP;
+    uint32_t *hist = s_hist[warp];
+    uint64_t *stage = s_stage[warp];
+    if (K <= 32) finalize_row<1>(b, cnt, K, kth_only, orow, out_keys, fo, hist, stage, lane);
+    else if (K <= 64) finalize_row<2>(b, cnt, K, kth_only, orow, out_keys, fo, hist, stage, lane);
+    else if (K <= 128) finalize_row<4>(b, cnt, K, kth_only, orow, out_keys, fo, hist, stage, lane);
+    else finalize_row<8>(b, cnt, K, kth_only, orow, out_keys, fo, hist, stage, lane);
   }
 }
 
@@ -664,6 +917,7 @@ size_t tc_pool_workspace(int64_t n, int64_t nq, bool self) {
 bool tc_pool_supported(int64_t d, int64_t k) {
   static_assert(tc::CAP >= 256 + 32, "CAP must leave room for K <= 256 plus one chunk");
   static_assert(tc::CAP <= 1024, "select_k holds CAP keys in registers");
+  static_assert(tc::FIN_STAGE >= 256, "finalize stages up to K = 256 keys");
   static int env = -1;
   if (env < 0) {
     const char *e = getenv("PGK_DISABLE_TC");
@@ -678,9 +932,10 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             cudaStream_t stream, const uint8_t *xs_sorted,
                             const int32_t *tlist, const int32_t *tlen, int64_t tstride,
                             const int32_t *perm, bool *handled, const uint64_t *init_keys,
-                            int kth_only, float shrink, int32_t *fail_blocks) {
+                            int kth_only, float shrink, int32_t *fail_blocks,
+                            const PoolOut *out, uint8_t *fail_rows, const uint8_t *row_mask) {
   *handled = false;
-  if (shrink < 1.0f && !fail_blocks) {
+  if (shrink < 1.0f && (!fail_blocks || !fail_rows)) {
     set_error("guessed thresholds need a fail-block array");
     return PGK_ERR_INVALID;
   }
@@ -739,7 +994,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
     PGK_CUDA(cudaMemsetAsync(dstats, 0, sizeof(unsigned long long) * tc::ST_COUNT, stream));
     tc::tc_pool_u8_kernel<true><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, dstats, tlist, tlen,
-        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched);
+        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel<stats>");
     unsigned long long h[tc::ST_COUNT];
     PGK_CUDA(cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, stream));
@@ -754,12 +1009,16 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   } else {
     tc::tc_pool_u8_kernel<false><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
-        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched);
+        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel");
   }
-  tc::tc_finalize_kernel<<<(unsigned)sms * 16, 256, 0, stream>>>(bufs, row_cnt, row_tau, nq, K,
-                                                                  perm, kth_only, keys,
-                                                                  fail_blocks, tlist ? tlen : nullptr);
+  tc::FinOut fo{nullptr, nullptr, nullptr};
+  if (out && !kth_only) fo = tc::FinOut{out->gt_ids, out->ids, out->dists};
+  const unsigned fgrid =
+      (unsigned)std::min<int64_t>((nq + tc::FIN_WARPS - 1) / tc::FIN_WARPS, (int64_t)sms * 8);
+  tc::tc_finalize_kernel<<<fgrid, tc::FIN_WARPS * 32, 0, stream>>>(
+      bufs, row_cnt, row_tau, nq, K, perm, kth_only, keys, fail_blocks, fail_rows,
+      tlist ? tlen : nullptr, fo);
   PGK_CHECK_LAUNCH("tc_finalize_kernel");
   *handled = true;
   return PGK_OK;

@@ -314,6 +314,7 @@ static float seed_shrink() {
 struct Layout {
   float *cen, *cent, *dcm;
   int32_t *cnorm, *hist, *cursor, *assign, *perm, *ns, *size, *lists, *lens, *fail, *lens2;
+  uint8_t *fail_rows;
   int64_t *off, *scan_tmp;
   uint64_t *akeys;
   double *rad, *U;
@@ -335,7 +336,9 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             const int32_t *tlist, const int32_t *tlen, int64_t tstride,
                             const int32_t *perm, bool *handled,
                             const uint64_t *init_keys = nullptr, int kth_only = 0,
-                            float shrink = 1.0f, int32_t *fail_blocks = nullptr);
+                            float shrink = 1.0f, int32_t *fail_blocks = nullptr,
+                            const PoolOut *out = nullptr, uint8_t *fail_rows = nullptr,
+                            const uint8_t *row_mask = nullptr);
 
 static tiles::Layout tiles_layout(void *ws, size_t bytes, int64_t n, int64_t d) {
   using namespace tiles;
@@ -363,6 +366,7 @@ static tiles::Layout tiles_layout(void *ws, size_t bytes, int64_t n, int64_t d) 
   L.lens = c.take<int32_t>(T);
   L.fail = c.take<int32_t>(T);
   L.lens2 = c.take<int32_t>(T);
+  L.fail_rows = c.take<uint8_t>(NP);
   L.dcm = c.take<float>((size_t)T * T);
   L.U = c.take<double>(T);
   L.total = c.take<unsigned long long>(4);
@@ -392,7 +396,7 @@ int64_t tiles_rows(int64_t n) { return tiles_layout(nullptr, 0, n, 1).NPmax; }
 int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm, int K,
                          uint64_t *keys, void *tc_ws, size_t tc_bytes, void *tws,
                          size_t tws_bytes, cudaStream_t stream, bool *handled,
-                         unsigned long long *pairs_out) {
+                         unsigned long long *pairs_out, const PoolOut *out) {
   using namespace tiles;
   *handled = false;
   if (!tiles_supported(n, d, K)) return PGK_OK;
@@ -456,7 +460,7 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   PGK_CHECK_LAUNCH("tile_filter_kernel");
   const char *se = getenv("PGK_TILES_STATS");
   const bool stats = se && se[0] == '1';
-  std::vector<uint64_t> seed_k, final_k;
+  std::vector<uint64_t> seed_k;
   if (stats) {  // each row's pass-1 K-th key (the pass-2 seed)
     seed_k.resize(n);
     PGK_CUDA(cudaMemcpy2DAsync(seed_k.data(), 8, keys + K - 1, (size_t)K * 8, 8, n,
@@ -464,9 +468,10 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   }
   const float shrink = seed_shrink();
   PGK_CUDA(cudaMemsetAsync(L.fail, 0, T * 4, stream));
+  PGK_CUDA(cudaMemsetAsync(L.fail_rows, 0, NP, stream));
   rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes, stream,
                                L.xs, L.lists, L.lens, T, L.perm, handled, keys, 0, shrink,
-                               L.fail);
+                               L.fail, out, L.fail_rows);
   if (rc) return rc;
   if (shrink < 1.0f) {
     // 6. re-run the blocks holding a row whose guess was too tight, seeded by
@@ -483,22 +488,21 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
               (long long)T);
     }
     rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes,
-                                 stream, L.xs, L.lists, L.lens2, T, L.perm, handled, keys);
+                                 stream, L.xs, L.lists, L.lens2, T, L.perm, handled, keys, 0,
+                                 1.0f, nullptr, out, nullptr, L.fail_rows);
     if (rc) return rc;
   }
-  if (stats) {
-    final_k.resize(n);
-    PGK_CUDA(cudaMemcpy2DAsync(final_k.data(), 8, keys + K - 1, (size_t)K * 8, 8, n,
+  if (stats && out) {  // final K-th distance (pool output) over the pass-2 seed
+    std::vector<float> final_d(n);
+    PGK_CUDA(cudaMemcpy2DAsync(final_d.data(), 4, out->dists + K - 1, (size_t)K * 4, 4, n,
                                cudaMemcpyDeviceToHost, stream));
     PGK_CUDA(cudaStreamSynchronize(stream));
     std::vector<double> ratio;
     for (int64_t i = 0; i < n; ++i) {
-      const uint32_t a = (uint32_t)(seed_k[i] >> 32) & 0x7fffffffu,
-                     b = (uint32_t)(final_k[i] >> 32) & 0x7fffffffu;
-      float fa, fb;
+      const uint32_t a = (uint32_t)(seed_k[i] >> 32) & 0x7fffffffu;
+      float fa;
       memcpy(&fa, &a, 4);
-      memcpy(&fb, &b, 4);
-      if (fa > 0) ratio.push_back(fb / fa);
+      if (fa > 0) ratio.push_back(final_d[i] / fa);
     }
     std::sort(ratio.begin(), ratio.end());
     auto qq = [&](double f) { return ratio.empty() ? 0.0 : ratio[(size_t)(f * (ratio.size() - 1))]; };
