@@ -7,12 +7,15 @@ device is present, every entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import torch
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libpgk.so"
+# PGK_LIB_PATH: an alternative in-tree build of the same library (kernel
+# variants compared by tools/build_variant.py); default the package's own
+LIB_PATH = Path(os.environ.get("PGK_LIB_PATH", PKG / "libpgk.so"))
 
 OK, ERR_INVALID, ERR_CUDA, ERR_NOMEM, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 POOL_AUTO, POOL_U8, POOL_F32 = 0, 1, 2

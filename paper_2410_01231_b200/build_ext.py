@@ -28,12 +28,19 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps if p.exists())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None,
+          defines: tuple[str, ...] = ()) -> Path:
+    """Compile every source for sm_100a and link libpgk.so (or `out`, with
+    extra -D `defines`: kernel-variant builds for A/B timing)."""
+    lib = Path(out) if out else LIB
+    if not force and not defines and out is None and not _stale():
         return LIB
+    tag = lib.stem if (defines or out) else ""
+    dflags = [f"-D{d}" for d in defines]
+
     def compile_one(s):
-        obj = CSRC / (s[:-3] + ".o")
-        cmd = [NVCC, *FLAGS, "-c", str(CSRC / s), "-o", str(obj)]
+        obj = CSRC / (s[:-3] + (f".{tag}.o" if tag else ".o"))
+        cmd = [NVCC, *FLAGS, *dflags, "-c", str(CSRC / s), "-o", str(obj)]
         return s, str(obj), subprocess.run(cmd, capture_output=True, text=True)
 
     with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
@@ -45,18 +52,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             sys.stderr.write(r.stderr)
             raise RuntimeError(f"nvcc failed on {s}")
         objs.append(obj)
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs,
            "-o", str(tmp)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, LIB)
-    (CSRC / "ptxas.log").write_text("".join(logs))
+    os.replace(tmp, lib)
+    (CSRC / (f"ptxas.{tag}.log" if tag else "ptxas.log")).write_text("".join(logs))
     if verbose:
         print("".join(logs))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

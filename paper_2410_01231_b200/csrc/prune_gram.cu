@@ -20,8 +20,10 @@
 // phase B) are listed and left to prune_u8_kernel.
 //
 // CTA: warp 0 gathers (cp.async, zero-filled tails), warp 1 allocates TMEM and
-// issues the MMA, warps 2-5 scan.  4 CTAs per SM share the tensor core
-// (128 TMEM columns each).
+// issues the MMA, warps 2-5 build the predicate masks (each its lower-
+// triangle chunks of the Gram rows), warp 6 runs the greedy scan and the
+// counters on double-buffered masks, overlapped with the next point's masks.
+// 4 CTAs per SM share the tensor core (128 TMEM columns each).
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -31,24 +33,41 @@ namespace gram {
 using namespace tc;
 
 constexpr int C = 128;          // candidates per point (TMEM lanes)
-constexpr int STAGES = 2;       // gathered points in flight
-constexpr int THREADS = 192;
-constexpr int CTAS_PER_SM = 4;
-constexpr int TMEM_COLS = 128;
+#ifndef GRAM_STAGES
+#define GRAM_STAGES 2
+#endif
+#ifndef GRAM_GROUPS
+#define GRAM_GROUPS 1
+#endif
+#ifndef GRAM_CTAS
+#define GRAM_CTAS 4
+#endif
+constexpr int STAGES = GRAM_STAGES;  // gathered points in flight
+constexpr int GROUPS = GRAM_GROUPS;  // mask warpgroups = TMEM accumulators (point parity)
+constexpr int THREADS = 32 * (3 + 4 * GROUPS);
+constexpr int GREEDY_WARP = 2 + 4 * GROUPS;
+constexpr int CTAS_PER_SM = GRAM_CTAS;
+constexpr int TMEM_COLS = C * GROUPS;
 constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(C >> 3) << 17) | ((uint32_t)(C >> 4) << 24);
 
 struct __align__(1024) Smem {
   uint8_t tile[STAGES][C * 128];  // SW128 K-major: 8-row x 128-byte atoms
   int32_t id[STAGES][C];
   float dist[STAGES][C];
-  int32_t nrm[STAGES][C];
+  alignas(16) int32_t nrm[STAGES][C];
+  int32_t cnt[STAGES];   // -1: end of this CTA's stream
+  int32_t self[STAGES];
   int64_t u[STAGES];
-  int32_t cnt[STAGES];
-  alignas(16) uint32_t pm[C][4];  // pm[j]: candidates i < j that dominate c_j if kept
-  alignas(16) uint32_t am[C][4];  // am[j]: candidates i whose test of c_j evaluates the angle
-  uint32_t ex[4];        // examinable candidates (in range, not u itself)
+  alignas(16) uint32_t pm[GROUPS][C][4];  // pm[j]: candidates i < j that dominate c_j if kept
+  alignas(16) uint32_t am[GROUPS][C][4];  // am[j]: candidates i whose test of c_j evaluates the angle
+  uint32_t ex[GROUPS][4];     // examinable candidates (in range, not u itself)
+  int32_t gid[GROUPS][C];     // the greedy warp's copy of the point (the gather
+  float gdist[GROUPS][C];     // stage is released as soon as the masks are built)
+  int64_t gu[GROUPS];
+  int32_t gcnt[GROUPS];       // -1: end of stream
   uint64_t full[STAGES], empty[STAGES];
-  uint64_t tfull, tempty;
+  uint64_t tfull[GROUPS], tempty[GROUPS];
+  uint64_t mfull[GROUPS], mempty[GROUPS];
   uint32_t tmem_base;
 };
 
@@ -72,10 +91,16 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&s.full[i], 32);   // every gather lane arrives (cp.async.mbarrier)
-      mbar_init(&s.empty[i], 4);   // every scan warp releases the stage
+      mbar_init(&s.empty[i], 4);   // released by the 4 mask warps
     }
-    mbar_init(&s.tfull, 1);
-    mbar_init(&s.tempty, 4);
+    for (int i = 0; i < GROUPS; ++i) {
+      mbar_init(&s.tfull[i], 1);
+      mbar_init(&s.tempty[i], 4);
+    }
+    for (int i = 0; i < GROUPS; ++i) {
+      mbar_init(&s.mfull[i], 4);
+      mbar_init(&s.mempty[i], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -91,36 +116,97 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
 
   if (warp == 0) {
     // ---------------- gather: rows, ids, dists, norms of one point --------
+    // This CTA's points are i = blockIdx.x + k * gridDim.x; their (u, cnt,
+    // off) are loaded 32 at a time (lane j: point k0 + j) and the next
+    // point's candidate ids are prefetched while the current one lands, so
+    // the warp waits on one L2 round trip per batch, not per point.  The
+    // other roles follow the stream published in s.u / s.cnt / s.self.
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t i = blockIdx.x; i < n_rows; i += gridDim.x) {
-      const int64_t u = row_order ? row_order[i] : i;
-      const int cnt = cand_counts[u];
+    const int64_t nb = blockIdx.x < n_rows ? (n_rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    int64_t bu = 0, boff = 0;
+    int bcnt = 0;
+    auto load_batch = [&](int64_t k0) {
+      const int64_t k = k0 + lane;
+      bu = 0;
+      bcnt = 0;
+      boff = 0;
+      if (k < nb) {
+        const int64_t i = blockIdx.x + k * gridDim.x;
+        bu = row_order ? row_order[i] : i;
+        bcnt = cand_counts[bu];
+        boff = cand_off[bu];
+      }
+    };
+    int32_t pv[C / 32];
+    auto load_ids = [&](int64_t base, int cnt) {
+#pragma unroll
+      for (int kk = 0; kk < C / 32; ++kk) {
+        const int r = lane + 32 * kk;
+        pv[kk] = r < cnt ? cand_ids[base + r] : 0;
+      }
+    };
+    if (nb > 0) load_batch(0);
+    int64_t cu = __shfl_sync(0xffffffffu, bu, 0), coff = __shfl_sync(0xffffffffu, boff, 0);
+    int ccnt = __shfl_sync(0xffffffffu, bcnt, 0);
+    if (nb > 0 && ccnt <= C) load_ids(coff, ccnt);
+    for (int64_t k = 0; k < nb; ++k) {
+      const int64_t u = cu, base = coff;
+      const int cnt = ccnt;
+      int32_t v[C / 32];
+#pragma unroll
+      for (int kk = 0; kk < C / 32; ++kk) v[kk] = pv[kk];
+      const int64_t k1 = k + 1;
+      if (k1 < nb) {
+        if ((k1 & 31) == 0) load_batch(k1);
+        cu = __shfl_sync(0xffffffffu, bu, (int)(k1 & 31));
+        coff = __shfl_sync(0xffffffffu, boff, (int)(k1 & 31));
+        ccnt = __shfl_sync(0xffffffffu, bcnt, (int)(k1 & 31));
+      }
       if (cnt > C) {  // hub row: left to the per-warp kernel
         if (lane == 0) long_rows[atomicAdd(long_count, 1)] = (int32_t)u;
+        if (k1 < nb && ccnt <= C) load_ids(coff, ccnt);
         continue;
       }
       mbar_wait(&s.empty[stage], phase ^ 1);
-      const int64_t base = cand_off[u];
       uint8_t *tile = s.tile[stage];
 #pragma unroll
-      for (int k = 0; k < C / 32; ++k) {
-        const int r = lane + 32 * k;
-        const bool ok = r < cnt;
-        const int32_t v = ok ? cand_ids[base + r] : 0;
-        s.id[stage][r] = ok ? v : -1;
-        s.dist[stage][r] = ok ? cand_dists[base + r] : 0.f;
-        s.nrm[stage][r] = ok ? __ldg(norms + v) : 0;
-        const uint8_t *src = xu8 + (int64_t)v * 128;
-        uint8_t *dst = tile + (r >> 3) * 1024 + (r & 7) * 128;
+      for (int kk = 0; kk < C / 32; ++kk) {
+        const int r = lane + 32 * kk;
+        if (r < cnt) {
+          s.id[stage][r] = v[kk];
+          cp_async4(&s.dist[stage][r], cand_dists + base + r);
+          cp_async4(&s.nrm[stage][r], norms + v[kk]);
+        } else {
+          s.id[stage][r] = -1;
+          s.dist[stage][r] = 0.f;
+          s.nrm[stage][r] = 0;
+        }
+        // rows past cnt keep stale bytes: their Gram entries feed no mask bit
+        // that is ever read (t >= cnt is not examinable, i >= cnt > t unused)
+        if (32 * kk < cnt) {
+          const bool ok = r < cnt;
+          const uint8_t *src = xu8 + (int64_t)(ok ? v[kk] : 0) * 128;
+          uint8_t *dst = tile + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch)  // 128B swizzle: chunk ^ (row % 8)
-          cp_async16_zfill(dst + ((ch ^ (r & 7)) << 4), src + ch * 16, ok ? 16u : 0u);
+          for (int ch = 0; ch < 8; ++ch)  // 128B swizzle: chunk ^ (row % 8)
+            cp_async16_zfill(dst + ((ch ^ (r & 7)) << 4), src + ch * 16, ok ? 16u : 0u);
+        }
       }
       if (lane == 0) {
         s.u[stage] = u;
         s.cnt[stage] = cnt;
+        s.self[stage] = row_node ? row_node[u] : (int32_t)u;
       }
+      if (k1 < nb && ccnt <= C) load_ids(coff, ccnt);  // next point, in flight meanwhile
+      __syncwarp();
+      cp_async_mbar_arrive(&s.full[stage]);
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    }
+    // end of stream: one sentinel per mask group (each reads every other point)
+    for (int g = 0; g < GROUPS; ++g) {
+      mbar_wait(&s.empty[stage], phase ^ 1);
+      if (lane == 0) s.cnt[stage] = -1;
       __syncwarp();
       cp_async_mbar_arrive(&s.full[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -128,169 +214,230 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA: G = C C^T per gathered point ----------------
-      int stage = 0;
+      int stage = 0, acc = 0;
       uint32_t phase = 0, tphase = 0;
-      for (int64_t i = blockIdx.x; i < n_rows; i += gridDim.x) {
-        const int64_t u = row_order ? row_order[i] : i;
-        if (cand_counts[u] > C) continue;
+      for (;;) {
         mbar_wait(&s.full[stage], phase);
+        if (s.cnt[stage] < 0) break;
         fence_proxy_async_smem();  // cp.async (generic proxy) -> tensor-core reads
-        mbar_wait(&s.tempty, tphase ^ 1);
+        mbar_wait(&s.tempty[acc], tphase ^ 1);
         tc_fence_after();
         const uint64_t desc = sw128_desc(s.tile[stage]);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_i8(tmem, desc + 2 * kk, desc + 2 * kk, IDESC, kk > 0);
-        tc_commit(&s.tfull);
-        tphase ^= 1;
+          mma_i8(tmem + acc * C, desc + 2 * kk, desc + 2 * kk, IDESC, kk > 0);
+        tc_commit(&s.tfull[acc]);
+        if (++acc == GROUPS) { acc = 0; tphase ^= 1; }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-  } else {
-    // ---------------- scan group: thread t = candidate t = TMEM lane t ----
-    // 1. every candidate t reads its own Gram row G[t][*] from TMEM and
-    //    builds two 128-bit masks over the candidates i < t:
-    //      pm: c_i dominates c_t if c_i is kept (_kernels.py:385-397)
-    //      am: the reference's test of c_t against kept c_i evaluates the angle
-    // 2. one warp runs the greedy scan on the masks (kept = first candidate
-    //    not dominated by an earlier kept one, stop at M) and derives every
-    //    examined candidate's lazy dist / angle evaluation counts.
+  } else if (warp < GREEDY_WARP) {
+    // ---------------- masks: thread t = candidate t = TMEM lane t ----------
+    // Candidate t reads its Gram row G[t][i] (i < t: the lower triangle, so
+    // warp quarter q reads chunks 0..q only) and builds two 128-bit masks:
+    //   pm: c_i dominates c_t if c_i is kept (_kernels.py:385-397)
+    //   am: the reference's test of c_t against kept c_i evaluates the angle
     const int q = warp & 3;               // TMEM lane quarter of this warp
+    const int grp = (warp - 2) >> 2;      // mask group: points k = grp (mod GROUPS)
     const int t = q * 32 + lane;          // candidate index
-    const int sw = warp - 2;              // scan-warp slot 0..3
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    int stage = 0;
-    uint32_t phase = 0, tphase = 0;
-    for (int64_t i = blockIdx.x; i < n_rows; i += gridDim.x) {
-      const int64_t u = row_order ? row_order[i] : i;
-      const int cnt = cand_counts[u];
-      if (cnt > C) continue;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + grp * C;
+    const int mb = grp;  // greedy buffer of this group's points
+    uint32_t tphase = 0, mphase = 0;
+    for (int64_t k = grp;; k += GROUPS) {
+      const int stage = (int)(k % STAGES);
+      const uint32_t phase = (uint32_t)((k / STAGES) & 1);
       mbar_wait(&s.full[stage], phase);
-      mbar_wait(&s.tfull, tphase);
-      tc_fence_after();
-      const int32_t self = row_node ? row_node[u] : (int32_t)u;
+      const int cnt = s.cnt[stage];
+      if (cnt < 0) {  // end of stream: pass it on to the greedy warp
+        mbar_wait(&s.mempty[mb], mphase ^ 1);
+        if (t == 0) s.gcnt[mb] = -1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s.mfull[mb]);
+        break;
+      }
+      const int32_t self = s.self[stage];
       const int32_t *sid = s.id[stage];
       const float *sdist = s.dist[stage];
       const int32_t *snrm = s.nrm[stage];
       const float dv = sdist[t];
       const int nv = snrm[t];
+      // c_i dominates c_t (rng) iff duw == 0 or dwv == 0 or dwv < dv, with
+      // dwv = |c_i|^2 + |c_t|^2 - 2 G[t][i] an exact integer >= 0:
+      //   dwv < dv  <=>  dwv <= ceil(dv) - 1;  dwv == 0  <=>  dwv <= 0
+      // so with x = |c_i|^2 - 2 G[t][i]:  x <= max(ceil(dv) - 1, 0) - |c_t|^2
+      const int dle = dv >= 2.0e9f ? 0x7fffffff : max((int)ceilf(dv) - 1, 0);
+      const int thr = dle == 0x7fffffff ? 0x7fffffff : dle - nv;
       uint32_t pm[4] = {0, 0, 0, 0}, am[4] = {0, 0, 0, 0};
+      mbar_wait(&s.tfull[grp], tphase);
+      tc_fence_after();
+      const int clast = min(q, (cnt - 1) >> 5);  // lower-triangle chunks holding candidates
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c <= clast; ++c) {
         uint32_t g[32];
         tmem_ld32(tl + (uint32_t)(c * 32), g);
+        const uint32_t zu = __ballot_sync(0xffffffffu, sdist[c * 32 + lane] == 0.0f);
+        const uint32_t valid = c < q ? 0xffffffffu : ((1u << lane) - 1u);
         tmem_wait_ld();
-        // branch-free simple verdicts; the fp64 angle tests only for alpha
         uint32_t dm = 0, need = 0;
+        if (STRATEGY == 0) {
+          const int4 *np = reinterpret_cast<const int4 *>(snrm + c * 32);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const int ci = c * 32 + k;
-          const float duw = sdist[ci];
-          const float dwv = (float)(snrm[ci] + nv - 2 * (int)g[k]);  // == squared_l2
-          const bool valid = ci < t;
-          const bool z = (duw == 0.0f) | (dwv == 0.0f);
-          const bool lt = dwv < dv;
-          if (STRATEGY == 0) {
-            dm |= (valid & (z | lt)) ? (1u << k) : 0u;
-          } else {
-            dm |= (valid & z) ? (1u << k) : 0u;
-            const bool ang = valid & !z & lt;
+          for (int v = 0; v < 8; ++v) {
+            const int4 w = np[v];
+            dm |= (w.x - 2 * (int)g[4 * v] <= thr) ? (1u << (4 * v)) : 0u;
+            dm |= (w.y - 2 * (int)g[4 * v + 1] <= thr) ? (1u << (4 * v + 1)) : 0u;
+            dm |= (w.z - 2 * (int)g[4 * v + 2] <= thr) ? (1u << (4 * v + 2)) : 0u;
+            dm |= (w.w - 2 * (int)g[4 * v + 3] <= thr) ? (1u << (4 * v + 3)) : 0u;
+          }
+          dm = (dm | zu) & valid;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const int ci = c * 32 + k;
+            const float duw = sdist[ci];
+            const float dwv = (float)(snrm[ci] + nv - 2 * (int)g[k]);  // == squared_l2
+            const bool z = (duw == 0.0f) | (dwv == 0.0f);
+            const bool lt = dwv < dv;
+            dm |= z ? (1u << k) : 0u;
+            const bool ang = ((valid >> k) & 1u) & !z & lt;
             need |= ang ? (1u << k) : 0u;
             if (ang && cos_angle_from_sq(duw, dwv, dv) < cos_alpha) dm |= 1u << k;
           }
+          dm &= valid;
         }
         am[c] = need;
         pm[c] = dm;
       }
       // TMEM is free for the next point's MMA
       tc_fence_before();
-      named_bar_sync(1, 128);  // previous point's greedy warp is done with pm/am
-      if (lane == 0) mbar_arrive(&s.tempty);
-      *reinterpret_cast<uint4 *>(s.pm[t]) = make_uint4(pm[0], pm[1], pm[2], pm[3]);
-      *reinterpret_cast<uint4 *>(s.am[t]) = make_uint4(am[0], am[1], am[2], am[3]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s.tempty[grp]);
+      mbar_wait(&s.mempty[mb], mphase ^ 1);  // the greedy warp is done with buffer mb
+      *reinterpret_cast<uint4 *>(s.pm[mb][t]) = make_uint4(pm[0], pm[1], pm[2], pm[3]);
+      *reinterpret_cast<uint4 *>(s.am[mb][t]) = make_uint4(am[0], am[1], am[2], am[3]);
       const unsigned exm = __ballot_sync(0xffffffffu, t < cnt && sid[t] != self);
-      if (lane == 0) s.ex[q] = exm;
-      named_bar_sync(1, 128);
-      if (sw == 0) {
-        // ---- greedy scan on the masks (warp 2) ----
-        uint32_t kept_m[4] = {0, 0, 0, 0};
-        int kept = 0, stop_j = C;
-        for (int c = 0; c < 4 && stop_j == C; ++c) {
-          const int j = c * 32 + lane;
-          const uint4 pj = *reinterpret_cast<const uint4 *>(s.pm[j]);
-          const bool blocked = (pj.x & kept_m[0]) | (pj.y & kept_m[1]) | (pj.z & kept_m[2]) |
-                               (pj.w & kept_m[3]);
-          const uint32_t pjc = c == 0 ? pj.x : c == 1 ? pj.y : c == 2 ? pj.z : pj.w;
-          unsigned m = s.ex[c] & __ballot_sync(0xffffffffu, !blocked);
-          while (m) {
-            const int li = __ffs(m) - 1;  // next kept candidate, index c*32+li
-            kept_m[c] |= 1u << li;
-            if (lane == 0) {
-              out_ids[u * width + kept] = sid[c * 32 + li];
-              out_dists[u * width + kept] = sdist[c * 32 + li];
-            }
-            ++kept;
-            if (kept == M) {  // _kernels.py:378: nothing after it is examined
-              stop_j = c * 32 + li;
-              break;
-            }
-            // later lanes of this chunk dominated by c_li
-            const unsigned dom = __ballot_sync(0xffffffffu, (pjc >> li) & 1u);
-            m &= ~(dom | ((2u << li) - 1u));
+      if (lane == 0) s.ex[mb][q] = exm;
+      s.gid[mb][t] = sid[t];
+      s.gdist[mb][t] = dv;
+      if (t == 0) {
+        s.gu[mb] = s.u[stage];
+        s.gcnt[mb] = cnt;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&s.mfull[mb]);
+        mbar_arrive(&s.empty[stage]);
+      }
+      tphase ^= 1;
+      mphase ^= 1;
+    }
+  } else {
+    // ---------------- greedy scan + exact lazy counters (last warp) -------
+    int mb = 0;
+    uint32_t mphase = 0;
+    for (;;) {
+      mbar_wait(&s.mfull[mb], mphase);
+      if (s.gcnt[mb] < 0) break;
+      const int64_t u = s.gu[mb];
+      const int32_t *sid = s.gid[mb];
+      const float *sdist = s.gdist[mb];
+      const uint32_t(*spm)[4] = s.pm[mb];
+      const uint32_t(*sam)[4] = s.am[mb];
+      const uint32_t *sex = s.ex[mb];
+      uint32_t kept_m[4] = {0, 0, 0, 0};  // warp-uniform
+      int kept = 0, stop_j = C;
+      for (int c = 0; c < 4 && stop_j == C; ++c) {
+        const int j = c * 32 + lane;
+        const uint4 pj = *reinterpret_cast<const uint4 *>(spm[j]);
+        const bool blocked = (pj.x & kept_m[0]) | (pj.y & kept_m[1]) | (pj.z & kept_m[2]) |
+                             (pj.w & kept_m[3]);
+        const uint32_t pjc = c == 0 ? pj.x : c == 1 ? pj.y : c == 2 ? pj.z : pj.w;
+        unsigned m = sex[c] & __ballot_sync(0xffffffffu, !blocked);
+        uint32_t km = 0;
+        while (m) {
+          const int li = __ffs(m) - 1;  // next kept candidate, index c*32+li
+          km |= 1u << li;
+          if (++kept == M) {  // _kernels.py:378: nothing after it is examined
+            stop_j = c * 32 + li;
+            break;
           }
+          // later lanes of this chunk dominated by c_li
+          const unsigned dom = __ballot_sync(0xffffffffu, (pjc >> li) & 1u);
+          m &= ~(dom | ((2u << li) - 1u));
         }
-        // ---- exact lazy counters of every examined candidate ----
-        long long dsum = 0, asum = 0;
+        kept_m[c] = km;
+      }
+      // the kept candidates in scan order, written once, coalesced
+      {
+        int base = 0;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const int j = c * 32 + lane;
-          if (j > stop_j || !((s.ex[c] >> lane) & 1u)) continue;
-          const uint4 pj = *reinterpret_cast<const uint4 *>(s.pm[j]);
-          const uint4 aj = *reinterpret_cast<const uint4 *>(s.am[j]);
-          const uint32_t pw[4] = {pj.x, pj.y, pj.z, pj.w}, aw[4] = {aj.x, aj.y, aj.z, aj.w};
-          // kept candidates before j, in order, up to the first dominator
-          int f = -1;
+          if ((kept_m[c] >> lane) & 1u) {
+            const int pos = base + __popc(kept_m[c] & lanemask_lt());
+            out_ids[u * width + pos] = sid[c * 32 + lane];
+            out_dists[u * width + pos] = sdist[c * 32 + lane];
+          }
+          base += __popc(kept_m[c]);
+        }
+      }
+      // ---- exact lazy counters of every examined candidate ----
+      const int kp1 = __popc(kept_m[0]), kp2 = kp1 + __popc(kept_m[1]),
+                kp3 = kp2 + __popc(kept_m[2]);
+      long long dsum = 0, asum = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = c * 32 + lane;
+        if (j > stop_j || !((sex[c] >> lane) & 1u)) continue;
+        const uint4 pj = *reinterpret_cast<const uint4 *>(spm[j]);
+        const uint32_t pw[4] = {pj.x, pj.y, pj.z, pj.w};
+        // the first kept candidate before j that dominates it
+        int f = -1;
+#pragma unroll
+        for (int w = 0; w <= c; ++w) {
+          const uint32_t d = pw[w] & kept_m[w] & (w < c ? 0xffffffffu : lanemask_lt());
+          if (f < 0 && d) f = w * 32 + __ffs(d) - 1;
+        }
+        // kept candidates c_j was tested against: every kept one before the
+        // first dominator (or before j), plus the dominator itself unless its
+        // duw == 0 short-cut needed no distance
+        const int end = f >= 0 ? f : j;
+        const int ew = end >> 5;
+        const uint32_t kw = ew == 0 ? kept_m[0] : ew == 1 ? kept_m[1] : ew == 2 ? kept_m[2] : kept_m[3];
+        int ev = (ew == 0 ? 0 : ew == 1 ? kp1 : ew == 2 ? kp2 : kp3) +
+                 __popc(kw & ((1u << (end & 31)) - 1u));
+        if (f >= 0 && sdist[f] != 0.0f) ev += 1;
+        dsum += ev;
+        if (STRATEGY == 1) {
+          const uint4 aj = *reinterpret_cast<const uint4 *>(sam[j]);
+          const uint32_t aw[4] = {aj.x, aj.y, aj.z, aj.w};
+          int an = 0;
 #pragma unroll
           for (int w = 0; w < 4; ++w) {
-            const uint32_t below = w < c ? 0xffffffffu : (w == c ? ((1u << lane) - 1u) : 0u);
-            const uint32_t d = pw[w] & kept_m[w] & below;
-            if (f < 0 && d) f = w * 32 + __ffs(d) - 1;
+            uint32_t lim = end >= (w + 1) * 32 ? 0xffffffffu
+                                               : (end <= w * 32 ? 0u : ((1u << (end - w * 32)) - 1u));
+            if (f >= 0 && (f >> 5) == w) lim |= 1u << (f & 31);
+            an += __popc(aw[w] & kept_m[w] & lim);
           }
-          int ev = 0, an = 0;
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            uint32_t lim;  // kept candidates examined by c_j: before f (or before j)
-            const int end = f >= 0 ? f : j;
-            lim = end >= (w + 1) * 32 ? 0xffffffffu : (end <= w * 32 ? 0u : ((1u << (end - w * 32)) - 1u));
-            ev += __popc(kept_m[w] & lim);
-            const uint32_t lim_incl = f >= 0 && (f >> 5) == w ? (lim | (1u << (f & 31))) : lim;
-            an += __popc(aw[w] & kept_m[w] & lim_incl);
-          }
-          if (f >= 0 && sdist[f] != 0.0f) ev += 1;  // the dominator's own test (not duw == 0)
-          dsum += ev;
           asum += an;
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
-          asum += __shfl_xor_sync(0xffffffffu, asum, o);
-        }
-        for (int j = kept + lane; j < width; j += 32) {
-          out_ids[u * width + j] = -1;
-          out_dists[u * width + j] = __int_as_float(0x7f800000);
-        }
-        if (lane == 0) {
-          dist_evals[u] = dsum;
-          angle_evals[u] = asum;
-          out_counts[u] = kept;
-        }
-        __syncwarp();
       }
-      // stage (ids / dists / norms) released once the greedy warp is done
-      if (sw == 0 && lane == 0) mbar_arrive(&s.empty[stage]);
-      if (sw != 0 && lane == 0) mbar_arrive(&s.empty[stage]);
-      if (++stage == STAGES) { stage = 0; phase ^= 1; }
-      tphase ^= 1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+        if (STRATEGY == 1) asum += __shfl_xor_sync(0xffffffffu, asum, o);
+      }
+      for (int j = kept + lane; j < width; j += 32) {
+        out_ids[u * width + j] = -1;
+        out_dists[u * width + j] = __int_as_float(0x7f800000);
+      }
+      if (lane == 0) {
+        dist_evals[u] = dsum;
+        angle_evals[u] = asum;
+        out_counts[u] = kept;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s.mempty[mb]);
+      if (++mb == GROUPS) { mb = 0; mphase ^= 1; }
     }
   }
   tc_fence_before();

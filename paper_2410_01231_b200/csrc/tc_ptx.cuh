@@ -34,8 +34,25 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Waiters park in try_wait until the phase completes (suspend-time hint in
+// ns, PGK_MBAR_HINT; 0 = the system default): a spinning consumer otherwise
+// steals issue slots from the warps doing the work.
+#ifndef PGK_MBAR_HINT
+#define PGK_MBAR_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   uint32_t a = smem_u32(bar);
+#if PGK_MBAR_HINT > 0
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity), "n"(PGK_MBAR_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -45,6 +62,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "}\n" ::"r"(a),
       "r"(parity)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, uint64_t *bar,
                                             int c0, int c1) {
@@ -114,6 +132,12 @@ __device__ __forceinline__ void cp_async16_zfill(void *dst, const void *src, uin
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
                    (uint32_t)__cvta_generic_to_shared(dst)),
                "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
                : "memory");
 }
 // arrive on `bar` once all of this thread's prior cp.async have completed
