@@ -42,10 +42,19 @@ constexpr int C = 128;          // candidates per point (TMEM lanes)
 #ifndef GRAM_CTAS
 #define GRAM_CTAS 4
 #endif
+#ifndef GRAM_GREEDY
+#define GRAM_GREEDY 2
+#endif
+#ifndef GRAM_NBUF
+#define GRAM_NBUF 3
+#endif
 constexpr int STAGES = GRAM_STAGES;  // gathered points in flight
 constexpr int GROUPS = GRAM_GROUPS;  // mask warpgroups = TMEM accumulators (point parity)
-constexpr int THREADS = 32 * (3 + 4 * GROUPS);
-constexpr int GREEDY_WARP = 2 + 4 * GROUPS;
+constexpr int NG = GRAM_GREEDY;      // greedy warps: point k goes to warp k % NG
+constexpr int NBUF = GRAM_NBUF;      // mask buffers: point k uses k % NBUF
+static_assert(NBUF >= NG, "every greedy warp needs a buffer");
+constexpr int THREADS = 32 * (2 + 4 * GROUPS + NG);
+constexpr int GREEDY_WARP = 2 + 4 * GROUPS;  // first greedy warp
 constexpr int CTAS_PER_SM = GRAM_CTAS;
 constexpr int TMEM_COLS = C * GROUPS;
 constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(C >> 3) << 17) | ((uint32_t)(C >> 4) << 24);
@@ -58,18 +67,36 @@ struct __align__(1024) Smem {
   int32_t cnt[STAGES];   // -1: end of this CTA's stream
   int32_t self[STAGES];
   int64_t u[STAGES];
-  alignas(16) uint32_t pm[GROUPS][C][4];  // pm[j]: candidates i < j that dominate c_j if kept
-  alignas(16) uint32_t am[GROUPS][C][4];  // am[j]: candidates i whose test of c_j evaluates the angle
-  uint32_t ex[GROUPS][4];     // examinable candidates (in range, not u itself)
-  int32_t gid[GROUPS][C];     // the greedy warp's copy of the point (the gather
-  float gdist[GROUPS][C];     // stage is released as soon as the masks are built)
-  int64_t gu[GROUPS];
-  int32_t gcnt[GROUPS];       // -1: end of stream
+  alignas(16) uint32_t pm[NBUF][C][4];  // pm[j]: candidates i < j that dominate c_j if kept
+  alignas(16) uint32_t am[NBUF][C][4];  // am[j]: candidates i whose test of c_j evaluates the angle
+  uint32_t ex[NBUF][4];     // examinable candidates (in range, not u itself)
+  int32_t gid[NBUF][C];     // the greedy warp's copy of the point (the gather
+  float gdist[NBUF][C];     // stage is released as soon as the masks are built)
+  int64_t gu[NBUF];
+  int32_t gcnt[NBUF];       // -1: end of stream
   uint64_t full[STAGES], empty[STAGES];
   uint64_t tfull[GROUPS], tempty[GROUPS];
-  uint64_t mfull[GROUPS], mempty[GROUPS];
+  uint64_t mfull[NBUF], mempty[NBUF];
   uint32_t tmem_base;
 };
+
+#ifndef GRAM_STATS
+#define GRAM_STATS 0
+#endif
+// GRAM_STATS=1 builds: per-role cycles spent in each mbarrier wait
+// (slots: 0 gather-empty, 1 mma-full, 2 mma-tempty, 3 mask-full, 4 mask-tfull,
+// 5 mask-mempty, 6 greedy-mfull, 7-10 total cycles of gather/mma/mask/greedy)
+__device__ unsigned long long g_gram_stats[16];
+#if GRAM_STATS
+#define GWAIT(slot, expr)                                   \
+  do {                                                      \
+    const long long t0_ = clock64();                        \
+    expr;                                                   \
+    if (lane == 0) atomicAdd(&g_gram_stats[slot], (unsigned long long)(clock64() - t0_)); \
+  } while (0)
+#else
+#define GWAIT(slot, expr) expr
+#endif
 
 template <int STRATEGY>  // 0 = rng, 1 = alpha (compile-time: no angle code for rng)
 __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
@@ -97,7 +124,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       mbar_init(&s.tfull[i], 1);
       mbar_init(&s.tempty[i], 4);
     }
-    for (int i = 0; i < GROUPS; ++i) {
+    for (int i = 0; i < NBUF; ++i) {
       mbar_init(&s.mfull[i], 4);
       mbar_init(&s.mempty[i], 1);
     }
@@ -113,6 +140,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s.tmem_base;
+  const long long t_start = clock64();
 
   if (warp == 0) {
     // ---------------- gather: rows, ids, dists, norms of one point --------
@@ -168,7 +196,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         if (k1 < nb && ccnt <= C) load_ids(coff, ccnt);
         continue;
       }
-      mbar_wait(&s.empty[stage], phase ^ 1);
+      GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
       uint8_t *tile = s.tile[stage];
 #pragma unroll
       for (int kk = 0; kk < C / 32; ++kk) {
@@ -205,8 +233,8 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     }
     // end of stream: one sentinel per mask group (each reads every other point)
     for (int g = 0; g < GROUPS; ++g) {
-      mbar_wait(&s.empty[stage], phase ^ 1);
-      if (lane == 0) s.cnt[stage] = -1;
+      GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
+      if (lane == 0) s.cnt[stage] = g == 0 ? -1 : -2;
       __syncwarp();
       cp_async_mbar_arrive(&s.full[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -217,10 +245,10 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       int stage = 0, acc = 0;
       uint32_t phase = 0, tphase = 0;
       for (;;) {
-        mbar_wait(&s.full[stage], phase);
+        GWAIT(1, mbar_wait(&s.full[stage], phase));
         if (s.cnt[stage] < 0) break;
         fence_proxy_async_smem();  // cp.async (generic proxy) -> tensor-core reads
-        mbar_wait(&s.tempty[acc], tphase ^ 1);
+        GWAIT(2, mbar_wait(&s.tempty[acc], tphase ^ 1));
         tc_fence_after();
         const uint64_t desc = sw128_desc(s.tile[stage]);
 #pragma unroll
@@ -241,18 +269,22 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     const int grp = (warp - 2) >> 2;      // mask group: points k = grp (mod GROUPS)
     const int t = q * 32 + lane;          // candidate index
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + grp * C;
-    const int mb = grp;  // greedy buffer of this group's points
-    uint32_t tphase = 0, mphase = 0;
+    uint32_t tphase = 0;
     for (int64_t k = grp;; k += GROUPS) {
       const int stage = (int)(k % STAGES);
       const uint32_t phase = (uint32_t)((k / STAGES) & 1);
-      mbar_wait(&s.full[stage], phase);
+      const int mb = (int)(k % NBUF);  // greedy buffer of point k
+      const uint32_t mphase = (uint32_t)((k / NBUF) & 1);
+      GWAIT(3, mbar_wait(&s.full[stage], phase));
       const int cnt = s.cnt[stage];
-      if (cnt < 0) {  // end of stream: pass it on to the greedy warp
-        mbar_wait(&s.mempty[mb], mphase ^ 1);
-        if (t == 0) s.gcnt[mb] = -1;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s.mfull[mb]);
+      if (cnt < 0) {  // end of stream: the first group to see it tells every greedy warp
+        for (int64_t kk = k; cnt == -1 && kk < k + NG; ++kk) {
+          const int b = (int)(kk % NBUF);
+          GWAIT(5, mbar_wait(&s.mempty[b], ((uint32_t)((kk / NBUF) & 1)) ^ 1));
+          if (t == 0) s.gcnt[b] = -1;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s.mfull[b]);
+        }
         break;
       }
       const int32_t self = s.self[stage];
@@ -268,7 +300,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       const int dle = dv >= 2.0e9f ? 0x7fffffff : max((int)ceilf(dv) - 1, 0);
       const int thr = dle == 0x7fffffff ? 0x7fffffff : dle - nv;
       uint32_t pm[4] = {0, 0, 0, 0}, am[4] = {0, 0, 0, 0};
-      mbar_wait(&s.tfull[grp], tphase);
+      GWAIT(4, mbar_wait(&s.tfull[grp], tphase));
       tc_fence_after();
       const int clast = min(q, (cnt - 1) >> 5);  // lower-triangle chunks holding candidates
 #pragma unroll 1
@@ -312,7 +344,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s.tempty[grp]);
-      mbar_wait(&s.mempty[mb], mphase ^ 1);  // the greedy warp is done with buffer mb
+      GWAIT(5, mbar_wait(&s.mempty[mb], mphase ^ 1));  // the greedy warp is done with buffer mb
       *reinterpret_cast<uint4 *>(s.pm[mb][t]) = make_uint4(pm[0], pm[1], pm[2], pm[3]);
       *reinterpret_cast<uint4 *>(s.am[mb][t]) = make_uint4(am[0], am[1], am[2], am[3]);
       const unsigned exm = __ballot_sync(0xffffffffu, t < cnt && sid[t] != self);
@@ -329,14 +361,13 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         mbar_arrive(&s.empty[stage]);
       }
       tphase ^= 1;
-      mphase ^= 1;
     }
   } else {
-    // ---------------- greedy scan + exact lazy counters (last warp) -------
-    int mb = 0;
-    uint32_t mphase = 0;
-    for (;;) {
-      mbar_wait(&s.mfull[mb], mphase);
+    // ---------------- greedy scan + exact lazy counters (NG warps) ---------
+    const int gw = warp - GREEDY_WARP;
+    for (int64_t k = gw;; k += NG) {
+      const int mb = (int)(k % NBUF);
+      GWAIT(6, mbar_wait(&s.mfull[mb], (uint32_t)((k / NBUF) & 1)));
       if (s.gcnt[mb] < 0) break;
       const int64_t u = s.gu[mb];
       const int32_t *sid = s.gid[mb];
@@ -344,15 +375,31 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       const uint32_t(*spm)[4] = s.pm[mb];
       const uint32_t(*sam)[4] = s.am[mb];
       const uint32_t *sex = s.ex[mb];
+      // everything this lane needs, loaded at once (one shared-memory latency)
+      uint4 pjv[4];
+      uint32_t exv[4];
+      int32_t idv[4];
+      float dsv[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        pjv[c] = *reinterpret_cast<const uint4 *>(spm[c * 32 + lane]);
+        exv[c] = sex[c];
+        idv[c] = sid[c * 32 + lane];
+        dsv[c] = sdist[c * 32 + lane];
+      }
+      uint32_t zu[4];  // candidates with duw == 0 (no distance computed against them)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) zu[c] = __ballot_sync(0xffffffffu, dsv[c] == 0.0f);
       uint32_t kept_m[4] = {0, 0, 0, 0};  // warp-uniform
       int kept = 0, stop_j = C;
-      for (int c = 0; c < 4 && stop_j == C; ++c) {
-        const int j = c * 32 + lane;
-        const uint4 pj = *reinterpret_cast<const uint4 *>(spm[j]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (stop_j != C) break;
+        const uint4 pj = pjv[c];
         const bool blocked = (pj.x & kept_m[0]) | (pj.y & kept_m[1]) | (pj.z & kept_m[2]) |
                              (pj.w & kept_m[3]);
         const uint32_t pjc = c == 0 ? pj.x : c == 1 ? pj.y : c == 2 ? pj.z : pj.w;
-        unsigned m = sex[c] & __ballot_sync(0xffffffffu, !blocked);
+        unsigned m = exv[c] & __ballot_sync(0xffffffffu, !blocked);
         uint32_t km = 0;
         while (m) {
           const int li = __ffs(m) - 1;  // next kept candidate, index c*32+li
@@ -374,8 +421,8 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         for (int c = 0; c < 4; ++c) {
           if ((kept_m[c] >> lane) & 1u) {
             const int pos = base + __popc(kept_m[c] & lanemask_lt());
-            out_ids[u * width + pos] = sid[c * 32 + lane];
-            out_dists[u * width + pos] = sdist[c * 32 + lane];
+            out_ids[u * width + pos] = idv[c];
+            out_dists[u * width + pos] = dsv[c];
           }
           base += __popc(kept_m[c]);
         }
@@ -387,9 +434,8 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int j = c * 32 + lane;
-        if (j > stop_j || !((sex[c] >> lane) & 1u)) continue;
-        const uint4 pj = *reinterpret_cast<const uint4 *>(spm[j]);
-        const uint32_t pw[4] = {pj.x, pj.y, pj.z, pj.w};
+        if (j > stop_j || !((exv[c] >> lane) & 1u)) continue;
+        const uint32_t pw[4] = {pjv[c].x, pjv[c].y, pjv[c].z, pjv[c].w};
         // the first kept candidate before j that dominates it
         int f = -1;
 #pragma unroll
@@ -405,7 +451,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         const uint32_t kw = ew == 0 ? kept_m[0] : ew == 1 ? kept_m[1] : ew == 2 ? kept_m[2] : kept_m[3];
         int ev = (ew == 0 ? 0 : ew == 1 ? kp1 : ew == 2 ? kp2 : kp3) +
                  __popc(kw & ((1u << (end & 31)) - 1u));
-        if (f >= 0 && sdist[f] != 0.0f) ev += 1;
+        if (f >= 0 && !((zu[f >> 5] >> (f & 31)) & 1u)) ev += 1;
         dsum += ev;
         if (STRATEGY == 1) {
           const uint4 aj = *reinterpret_cast<const uint4 *>(sam[j]);
@@ -437,9 +483,13 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&s.mempty[mb]);
-      if (++mb == GROUPS) { mb = 0; mphase ^= 1; }
     }
   }
+#if GRAM_STATS
+  if (lane == 0 && (warp <= 2 || warp == GREEDY_WARP))
+    atomicAdd(&g_gram_stats[7 + (warp == GREEDY_WARP ? 3 : warp)],
+              (unsigned long long)(clock64() - t_start));
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -461,14 +511,13 @@ int launch_prune_u8_rows(const uint8_t *xu8, const int32_t *norms, int64_t n,
 
 size_t gram_workspace(int64_t n) { return (size_t)(n + 64) * sizeof(int32_t); }
 
-// Opt-in (PGK_GRAM=1): exact and parity-tested, but on config 2 the per-warp
-// exact-integer kernel is faster today (12 vs 19 ms for phase A at 1M; the
-// full C x C predicate matrix costs more than the reference's lazy pairs).
+// Default selection path for exact-integer rows (PGK_GRAM=0 selects the
+// per-warp prune_u8_kernel instead, e.g. for A/B timing).
 bool gram_enabled() {
   static int env = -1;
   if (env < 0) {
     const char *e = getenv("PGK_GRAM");
-    env = (e && e[0] == '1') ? 1 : 0;
+    env = (e && e[0] == '0') ? 0 : 1;
   }
   return env == 1;
 }
@@ -508,6 +557,23 @@ int launch_prune_gram(const uint8_t *xu8, const int32_t *norms, int64_t n,
         cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals,
         long_rows, long_count);
   PGK_CHECK_LAUNCH("prune_gram_kernel");
+#if GRAM_STATS
+  {
+    unsigned long long h[16];
+    PGK_CUDA(cudaStreamSynchronize(stream));
+    PGK_CUDA(cudaMemcpyFromSymbol(h, gram::g_gram_stats, sizeof(h)));
+    const double ctas = (double)grid;
+    fprintf(stderr,
+            "[gram stats] per CTA, Mcycles: total gather %.2f mma %.2f mask(w2) %.2f greedy %.2f | "
+            "waits: gather-empty %.2f mma-full %.2f mma-tempty %.2f mask-full %.2f mask-tfull "
+            "%.2f mask-mempty %.2f (per mask warp) greedy-mfull %.2f\n",
+            h[7] / ctas / 1e6, h[8] / ctas / 1e6, h[9] / ctas / 1e6, h[10] / ctas / 1e6,
+            h[0] / ctas / 1e6, h[1] / ctas / 1e6, h[2] / ctas / 1e6, h[3] / ctas / 4e6,
+            h[4] / ctas / 4e6, h[5] / ctas / 4e6, h[6] / ctas / 1e6);
+    unsigned long long z[16] = {0};
+    PGK_CUDA(cudaMemcpyToSymbol(gram::g_gram_stats, z, sizeof(z)));
+  }
+#endif
   // hub rows (> 128 candidates): the per-warp exact-integer kernel, over the
   // device-side list (its length is read on the device)
   return launch_prune_u8_rows(xu8, norms, n, long_count, row_node, long_rows, cand_off,

@@ -328,8 +328,9 @@ def test_gram_selection_hub_rows_and_fallback():
 
 def test_tensor_core_cxc_gram_selection_path():
     """The batched per-point C x C Gram kernel (tcgen05 kind::i8 + bitmask scan,
-    opt-in via PGK_GRAM=1) gives the same phase A / B rows and counters as the
-    default path, in a fresh process."""
+    the default for exact-integer rows) and the per-warp lazy kernel
+    (PGK_GRAM=0) give the same phase A / B rows and counters, each in a fresh
+    process (the default path itself is checked against the oracle above)."""
     import os
     import subprocess
     import sys
@@ -359,7 +360,7 @@ for name, data in (("cfg2", synth.cfg2(6000)), ("hub", hub.astype(np.float32))):
 np.savez(sys.argv[1], **out)
 ''' % str(root)
     res = {}
-    for tag, env in (("gram", {"PGK_GRAM": "1"}), ("warp", {})):
+    for tag, env in (("gram", {"PGK_GRAM": "1"}), ("warp", {"PGK_GRAM": "0"})):
         path = f"/tmp/pgk_gram_{tag}.npz"
         subprocess.check_call([sys.executable, "-c", code, path],
                               env=dict(os.environ, **env), timeout=600)
