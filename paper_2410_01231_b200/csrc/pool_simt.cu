@@ -89,7 +89,14 @@ __global__ void __launch_bounds__(256, 1)
                     const float *__restrict__ Q, int64_t nq, int exclude_self,
                     const int32_t *__restrict__ xnorm,
                     const int32_t *__restrict__ qnorm, int S, int vec4,
-                    uint64_t *__restrict__ out_keys) {
+                    uint64_t *__restrict__ out_keys, const int32_t *__restrict__ tlist,
+                    const int32_t *__restrict__ tlen, int64_t tstride,
+                    const int32_t *__restrict__ perm) {
+  // Tile-list mode (tlist != null, pool_tiles.cu): X == Q are the tile-sorted
+  // rows, this block's 32 query rows belong to query tile blockIdx.x / 4 and
+  // only that tile's candidate column tiles are scanned; perm maps sorted rows
+  // to original ids (< 0: padding), keys carry original ids and rows are
+  // written at their original position.
   extern __shared__ __align__(16) unsigned char smem[];
   float(*sA)[TBM + 1] = reinterpret_cast<float(*)[TBM + 1]>(smem);
   float(*sB)[TBN + 1] =
@@ -98,9 +105,11 @@ __global__ void __launch_bounds__(256, 1)
   off = (off + 15) & ~size_t(15);
   uint64_t *sbuf = reinterpret_cast<uint64_t *>(smem + off);
   int32_t *sxn = reinterpret_cast<int32_t *>(sbuf + TBM * CAP);
+  int32_t *sperm = sxn + TBN;  // original ids of the current column tile (list mode)
 
   const int tid = threadIdx.x, ty = tid >> 5, tx = tid & 31;
   const int64_t row0 = (int64_t)blockIdx.x * TBM;
+  const int64_t qt = (int64_t)blockIdx.x / (TBN / TBM);  // query tile (list mode)
 
   int cnt[4];
   uint64_t tau[4];
@@ -111,6 +120,8 @@ __global__ void __launch_bounds__(256, 1)
     tau[i] = KEY_MAX;
     int64_t g = row0 + ty * 4 + i;
     qn[i] = (MODE == MODE_U8 && g < nq) ? qnorm[g] : 0;
+    // padding rows of the tile sort never take candidates
+    if (perm && g < nq && perm[g] < 0) tau[i] = 0;
   }
 
   // global -> register staging of one (column tile, k chunk)
@@ -151,7 +162,9 @@ __global__ void __launch_bounds__(256, 1)
   };
 
   const int nk = (d + TBK - 1) / TBK;
-  const int64_t ntiles = (n + TBN - 1) / TBN;
+  const int64_t ntiles = tlist ? tlen[qt] : (n + TBN - 1) / TBN;
+  const int32_t *tl = tlist ? tlist + qt * tstride : nullptr;
+  auto col_tile = [&](int64_t i) -> int64_t { return tl ? (int64_t)tl[i] : i; };
   const int64_t steps = ntiles * nk;
   float acc[4][4];
 #pragma unroll
@@ -159,11 +172,11 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
 
-  load_regs(0, 0);
+  if (steps > 0) load_regs(col_tile(0) * TBN, 0);
   for (int64_t st = 0; st < steps; ++st) {
     const int64_t ct = st / nk;
     const int kc = (int)(st - ct * nk);
-    const int64_t c0 = ct * TBN;
+    const int64_t c0 = col_tile(ct) * TBN;
     // registers -> shared (transposed: [k][row] / [k][col])
     sA[lk + 0][lr] = ra.x;
     sA[lk + 1][lr] = ra.y;
@@ -180,10 +193,14 @@ __global__ void __launch_bounds__(256, 1)
       int64_t c = c0 + tid;
       sxn[tid] = c < n ? xnorm[c] : 0;
     }
+    if (perm && kc == 0 && tid < TBN) {
+      int64_t c = c0 + tid;
+      sperm[tid] = c < n ? perm[c] : -1;
+    }
     __syncthreads();
     if (st + 1 < steps) {
       const int64_t ct1 = (st + 1) / nk;
-      load_regs(ct1 * TBN, (int)((st + 1) - ct1 * nk) * TBK);
+      load_regs(col_tile(ct1) * TBN, (int)((st + 1) - ct1 * nk) * TBK);
     }
 #pragma unroll 8
     for (int k = 0; k < TBK; ++k) {
@@ -214,7 +231,8 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int64_t c = c0 + tx + 32 * q;
-          bool valid = g < nq && c < n && !(exclude_self && c == g);
+          const int32_t cid = perm ? sperm[tx + 32 * q] : (int32_t)c;
+          bool valid = g < nq && c < n && cid >= 0 && !(exclude_self && c == g);
           float dist;
           if (MODE == MODE_U8) {
             int di = qn[i] + sxn[tx + 32 * q] - 2 * __float2int_rn(acc[i][q]);
@@ -222,7 +240,7 @@ __global__ void __launch_bounds__(256, 1)
           } else {
             dist = acc[i][q];
           }
-          uint64_t key = pack_key(dist, (int32_t)c);
+          uint64_t key = pack_key(dist, cid);
           bool pass = valid && key < tau[i];
           unsigned bal = __ballot_sync(0xffffffffu, pass);
           if (bal) {
@@ -250,8 +268,9 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t *b = sbuf + (size_t)r * CAP;
     __syncwarp();
     compact_row<CAP>(b, cnt[i], tau[i], S, tx);
-    if (g < nq)
-      for (int j = tx; j < S; j += 32) out_keys[g * S + j] = j < cnt[i] ? b[j] : KEY_MAX;
+    const int64_t og = (perm && g < nq) ? (int64_t)perm[g] : g;
+    if (g < nq && og >= 0)
+      for (int j = tx; j < S; j += 32) out_keys[og * S + j] = j < cnt[i] ? b[j] : KEY_MAX;
   }
 }
 
@@ -281,16 +300,44 @@ __device__ void write_pool_row(const float *__restrict__ X, const float *__restr
                                int32_t *__restrict__ gt_ids,
                                int32_t *__restrict__ pool_ids,
                                float *__restrict__ pool_dists, int lane) {
-  for (int j = lane; j < K2; j += 32) {
-    if (j < K) {
-      int32_t v = s_id[j];
-      if (gt_ids) gt_ids[row * K + j] = v;
-      float dist = v < 0 ? __int_as_float(0x7f800000)
-                         : (vec4 ? sql2_seq<true>(X + (int64_t)v * d, q, d)
-                                 : sql2_seq<false>(X + (int64_t)v * d, q, d));
-      s_key[j] = v < 0 ? KEY_MAX : pack_key(dist, v);
+  // the reference's sequential fp32 squared_l2 per (row, candidate): each
+  // chain is inherently serial, so a lane runs four candidates' chains
+  // interleaved (independent, bit-identical to one at a time)
+  for (int j0 = lane; j0 < K2; j0 += 128) {
+    int32_t v[4];
+    const float *xr[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + 32 * c;
+      v[c] = j < K ? s_id[j] : -1;
+      if (j < K && gt_ids) gt_ids[row * K + j] = v[c];
+      xr[c] = v[c] >= 0 ? X + (int64_t)v[c] * d : q;  // q: a harmless stand-in
+    }
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    if (vec4) {
+      const float4 *q4 = reinterpret_cast<const float4 *>(q);
+      for (int i = 0; i < (d >> 2); ++i) {
+        const float4 b = __ldg(q4 + i);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float4 a = __ldg(reinterpret_cast<const float4 *>(xr[c]) + i);
+          acc[c] = sq_step(acc[c], a.x, b.x);
+          acc[c] = sq_step(acc[c], a.y, b.y);
+          acc[c] = sq_step(acc[c], a.z, b.z);
+          acc[c] = sq_step(acc[c], a.w, b.w);
+        }
+      }
     } else {
-      s_key[j] = KEY_MAX;
+      for (int i = 0; i < d; ++i) {
+        const float b = __ldg(q + i);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[c] = sq_step(acc[c], __ldg(xr[c] + i), b);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + 32 * c;
+      if (j < K2) s_key[j] = v[c] < 0 ? KEY_MAX : pack_key(acc[c], v[c]);
     }
   }
   __syncwarp();
@@ -312,25 +359,56 @@ __global__ void __launch_bounds__(RR_WARPS * 32)
                   int64_t nq, const uint64_t *__restrict__ keys, int S, int K,
                   double gamma, int vec4, int32_t *__restrict__ gt_ids,
                   int32_t *__restrict__ pool_ids, float *__restrict__ pool_dists,
-                  int32_t *__restrict__ fb_list, int32_t *__restrict__ fb_count) {
+                  int32_t *__restrict__ fb_list, int32_t *__restrict__ fb_count,
+                  const int32_t *__restrict__ order) {
   __shared__ double s_d[RR_WARPS][RR_MAXS];
   __shared__ int32_t s_id[RR_WARPS][RR_MAXS];
   __shared__ uint64_t s_key[RR_WARPS][RR_MAXS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S2 = next_pow2(S), K2 = next_pow2(K);
-  for (int64_t r = (int64_t)blockIdx.x * RR_WARPS + warp; r < nq;
-       r += (int64_t)gridDim.x * RR_WARPS) {
+  for (int64_t ri = (int64_t)blockIdx.x * RR_WARPS + warp; ri < nq;
+       ri += (int64_t)gridDim.x * RR_WARPS) {
+    // rows in the tile order when pruned: a warp's neighbours share candidates (L2)
+    const int64_t r = order ? (int64_t)order[ri] : ri;
     const float *q = Q + r * d;
     __syncwarp();
     for (int j = lane; j < S2; j += 32) {
       uint64_t k = j < S ? keys[r * S + j] : KEY_MAX;
-      if (k != KEY_MAX) {
-        int32_t v = key_id(k);
-        s_id[warp][j] = v;
-        s_d[warp][j] = sql2_f64(X + (int64_t)v * d, q, d, vec4);
-      } else {
-        s_id[warp][j] = 0x7fffffff;
-        s_d[warp][j] = __longlong_as_double(0x7ff0000000000000ll);
+      s_id[warp][j] = k != KEY_MAX ? key_id(k) : 0x7fffffff;
+    }
+    __syncwarp();
+    // float64 distances of the survivors: lanes over dimensions (coalesced
+    // rows), four candidates at a time, warp-reduced.  The pool's float64
+    // ranking (oracle: BLAS norm expansion) fixes no summation order; any
+    // accurate order is within the proof's 1e-12 slack.
+    for (int j0 = 0; j0 < S2; j0 += 4) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      const float *xr[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int32_t v = s_id[warp][j0 + c];
+        xr[c] = v != 0x7fffffff ? X + (int64_t)v * d : q;
+      }
+      for (int k = lane; k < d; k += 32) {
+        const double qk = (double)__ldg(q + k);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double t = (double)__ldg(xr[c] + k) - qk;
+          acc[c] = fma(t, t, acc[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+      }
+      if (lane < 4) {
+        double a = acc[0];
+#pragma unroll
+        for (int c = 1; c < 4; ++c) a = lane == c ? acc[c] : a;
+        s_d[warp][j0 + lane] = s_id[warp][j0 + lane] != 0x7fffffff
+                                   ? a
+                                   : __longlong_as_double(0x7ff0000000000000ll);
       }
     }
     __syncwarp();
@@ -446,10 +524,10 @@ __global__ void __launch_bounds__(FB_THREADS)
 // ---------------------------------------------------------------------------
 struct KnnLayout {
   int *flag;
-  int32_t *xnorm, *qnorm, *fb_list, *fb_count;
+  int32_t *xnorm, *qnorm, *fb_list, *fb_count, *order;
   uint64_t *keys;
-  void *tc_ws, *tws;
-  size_t tc_bytes, tws_bytes;
+  void *tc_ws, *tws, *tws_f32;
+  size_t tc_bytes, tws_bytes, tws_f32_bytes;
   size_t total;
 };
 
@@ -458,6 +536,14 @@ bool tc_pool_supported(int64_t d, int64_t k);
 size_t tiles_workspace(int64_t n, int64_t d);
 int64_t tiles_rows(int64_t n);
 bool tiles_supported(int64_t n, int64_t d, int64_t k);
+bool tiles_f32_supported(int64_t n, int64_t d, int64_t k);
+size_t tiles_f32_workspace(int64_t n, int64_t d, int64_t k);
+int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64_t *keys,
+                          void *tws, size_t tws_bytes, cudaStream_t stream, bool *handled);
+int tiles_f32_order(void *tws, int64_t n, int64_t d, int64_t k, int32_t *out,
+                    cudaStream_t stream);
+int tiles_f32_work(const void *tws, int64_t n, int64_t d, int64_t k, unsigned long long out[4],
+                   cudaStream_t stream);
 
 int pool_S(int64_t k, int mode) {
   if (mode == PGK_POOL_U8) return (int)k;
@@ -476,8 +562,9 @@ static KnnLayout knn_layout(void *ws, size_t bytes, int64_t n, int64_t nq, int64
   L.qnorm = c.take<int32_t>(nq);
   L.fb_list = c.take<int32_t>(nq);
   L.keys = c.take<uint64_t>((size_t)nq * S);
-  L.tc_bytes = L.tws_bytes = 0;
-  L.tc_ws = L.tws = nullptr;
+  L.order = c.take<int32_t>(nq);
+  L.tc_bytes = L.tws_bytes = L.tws_f32_bytes = 0;
+  L.tc_ws = L.tws = L.tws_f32 = nullptr;
   if (mode != PGK_POOL_F32 && tc_pool_supported(d, k)) {
     const bool tiles = nq == n && tiles_supported(n, d, k);
     const int64_t rows = tiles ? std::max(nq, tiles_rows(n)) : nq;
@@ -487,6 +574,10 @@ static KnnLayout knn_layout(void *ws, size_t bytes, int64_t n, int64_t nq, int64
       L.tws_bytes = tiles_workspace(n, d);
       L.tws = c.take<char>(L.tws_bytes);
     }
+  }
+  if (mode != PGK_POOL_U8 && nq == n && tiles_f32_supported(n, d, k)) {
+    L.tws_f32_bytes = tiles_f32_workspace(n, d, k);
+    L.tws_f32 = c.take<char>(L.tws_f32_bytes);
   }
   L.total = c.off;
   return L;
@@ -508,6 +599,7 @@ int knn_work(const void *ws, int64_t n, int64_t nq, int64_t d, int64_t k, int mo
   KnnLayout L = knn_layout(const_cast<void *>(ws), ~size_t(0), n, nq, d, k, mode);
   out[0] = out[1] = out[2] = out[3] = 0;
   if (L.tws) return tiles_work(L.tws, n, d, out, stream);
+  if (L.tws_f32) return tiles_f32_work(L.tws_f32, n, d, k, out, stream);
   return PGK_OK;
 }
 
@@ -525,6 +617,7 @@ int knn_order(const void *ws, int64_t n, int64_t nq, int64_t d, int64_t k, int m
               int32_t *out, cudaStream_t stream) {
   KnnLayout L = knn_layout(const_cast<void *>(ws), ~size_t(0), n, nq, d, k, mode);
   if (L.tws) return tiles_order(L.tws, n, d, out, stream);
+  if (L.tws_f32) return tiles_f32_order(L.tws_f32, n, d, k, out, stream);
   iota_kernel<<<(unsigned)num_sms() * 4, 256, 0, stream>>>(out, n);
   PGK_CHECK_LAUNCH("iota_kernel");
   return PGK_OK;
@@ -561,10 +654,12 @@ int detect_u8(const float *X, int64_t n, int64_t d, int *is_u8, void *ws, size_t
 template <int MODE, int CAP>
 static int launch_tile(const float *X, int64_t n, int d, const float *Q, int64_t nq,
                        int exclude_self, const int32_t *xn, const int32_t *qn, int S,
-                       int vec4, uint64_t *keys, cudaStream_t stream) {
+                       int vec4, uint64_t *keys, cudaStream_t stream,
+                       const int32_t *tlist = nullptr, const int32_t *tlen = nullptr,
+                       int64_t tstride = 0, const int32_t *perm = nullptr) {
   size_t smem = (TBK * (TBM + 1) + TBK * (TBN + 1)) * sizeof(float);
   smem = (smem + 15) & ~size_t(15);
-  smem += (size_t)TBM * CAP * sizeof(uint64_t) + TBN * sizeof(int32_t);
+  smem += (size_t)TBM * CAP * sizeof(uint64_t) + 2 * TBN * sizeof(int32_t);
   static bool attr = false;
   if (!attr) {
     PGK_CUDA(cudaFuncSetAttribute(knn_tile_kernel<MODE, CAP>,
@@ -573,9 +668,25 @@ static int launch_tile(const float *X, int64_t n, int d, const float *Q, int64_t
   }
   const unsigned grid = (unsigned)((nq + TBM - 1) / TBM);
   knn_tile_kernel<MODE, CAP><<<grid, 256, smem, stream>>>(X, n, d, Q, nq, exclude_self, xn,
-                                                          qn, S, vec4, keys);
+                                                          qn, S, vec4, keys, tlist, tlen,
+                                                          tstride, perm);
   PGK_CHECK_LAUNCH("knn_tile_kernel");
   return PGK_OK;
+}
+
+// F32 tile-list pass over the tile-sorted rows xs (np rows): every row keeps
+// its S best (approximate, direct-difference fp32) keys, written at perm[row].
+int launch_pool_f32_lists(const float *xs, int64_t np, int d, int S, int vec4,
+                          const int32_t *tlist, const int32_t *tlen, int64_t tstride,
+                          const int32_t *perm, uint64_t *keys, cudaStream_t stream) {
+  if (S > 480) {
+    set_error("pool width S=%d unsupported in F32 mode", S);
+    return PGK_ERR_UNSUPPORTED;
+  }
+  return S <= 224 ? launch_tile<MODE_F32, 256>(xs, np, d, xs, np, 1, nullptr, nullptr, S, vec4,
+                                              keys, stream, tlist, tlen, tstride, perm)
+                  : launch_tile<MODE_F32, 512>(xs, np, d, xs, np, 1, nullptr, nullptr, S, vec4,
+                                              keys, stream, tlist, tlen, tstride, perm);
 }
 
 int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, int64_t nq,
@@ -670,18 +781,32 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
     PGK_CHECK_LAUNCH("finalize_exact_kernel");
     return PGK_OK;
   }
-  rc = S <= 224 ? launch_tile<MODE_F32, 256>(X, n, (int)d, Q, nq, exclude_self, nullptr,
-                                             nullptr, S, vec4, L.keys, stream)
-                : launch_tile<MODE_F32, 512>(X, n, (int)d, Q, nq, exclude_self, nullptr,
-                                             nullptr, S, vec4, L.keys, stream);
-  if (rc) return rc;
+  bool pruned = false;
+  if (L.tws_f32 && self && exclude_self) {
+    // exact tile pruning: S approximate survivors from the candidate tiles only
+    rc = launch_pool_tiles_f32(X, n, (int)d, (int)k, S, L.keys, L.tws_f32, L.tws_f32_bytes,
+                               stream, &pruned);
+    if (rc) return rc;
+    if (pruned) {
+      rc = tiles_f32_order(L.tws_f32, n, d, k, L.order, stream);
+      if (rc) return rc;
+    }
+  }
+  if (!pruned) {
+    rc = S <= 224 ? launch_tile<MODE_F32, 256>(X, n, (int)d, Q, nq, exclude_self, nullptr,
+                                               nullptr, S, vec4, L.keys, stream)
+                  : launch_tile<MODE_F32, 512>(X, n, (int)d, Q, nq, exclude_self, nullptr,
+                                               nullptr, S, vec4, L.keys, stream);
+    if (rc) return rc;
+  }
   // (1+u)^(d+2) <= 1 + gamma for u = 2^-24
   const double gamma = (double)(d + 2) * 5.9604644775390625e-08 * 1.001 + 1e-12;
   const unsigned rgrid =
       (unsigned)std::min<int64_t>((nq + RR_WARPS - 1) / RR_WARPS, (int64_t)sms * 16);
   rerank_kernel<<<rgrid, RR_WARPS * 32, 0, stream>>>(X, (int)d, Q, nq, L.keys, S, (int)k,
                                                      gamma, vec4, gt_ids, pool_ids,
-                                                     pool_dists, L.fb_list, L.fb_count);
+                                                     pool_dists, L.fb_list, L.fb_count,
+                                                     pruned ? L.order : nullptr);
   PGK_CHECK_LAUNCH("rerank_kernel");
   fallback_kernel<<<(unsigned)sms * 2, FB_THREADS, 0, stream>>>(
       X, n, (int)d, Q, exclude_self, (int)k, vec4, L.fb_list, L.fb_count, gt_ids, pool_ids,

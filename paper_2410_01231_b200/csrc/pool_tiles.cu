@@ -239,7 +239,7 @@ __global__ void tile_nearest_kernel(const float *__restrict__ dc, const int32_t 
 // U_Q = max over the tile's rows of the pass-1 K-th neighbour distance
 __global__ void tile_ubound_kernel(const uint64_t *__restrict__ keys, int K,
                                    const int32_t *__restrict__ perm, int64_t T,
-                                   double *__restrict__ U) {
+                                   double *__restrict__ U, double inflate = 1.0) {
   const int lane = threadIdx.x & 31;
   for (int64_t Q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; Q < T;
        Q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -254,7 +254,9 @@ __global__ void tile_ubound_kernel(const uint64_t *__restrict__ keys, int K,
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) U[Q] = sqrt(m) * (1.0 + MARGIN) + 1e-9;
+    // inflate: approximate pass-1 distances (F32 path) bound the exact K-th
+    // one from above only after dividing by (1 - gamma)
+    if (lane == 0) U[Q] = sqrt(m * inflate) * (1.0 + MARGIN) + 1e-9;
   }
 }
 
@@ -263,7 +265,8 @@ __global__ void tile_filter_kernel(const float *__restrict__ dc, const double *_
                                    const int32_t *__restrict__ size, const double *__restrict__ U,
                                    int64_t T, int32_t *__restrict__ lists,
                                    int32_t *__restrict__ lens,
-                                   unsigned long long *__restrict__ total) {
+                                   unsigned long long *__restrict__ total,
+                                   double dc_margin = DC_MARGIN) {
   const int lane = threadIdx.x & 31;
   for (int64_t Q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; Q < T;
        Q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -273,7 +276,7 @@ __global__ void tile_filter_kernel(const float *__restrict__ dc, const double *_
       const int64_t t = t0 + lane;
       bool keep = false;
       if (t < T && size[t] > 0) {
-        const double lb = (double)dc[Q * T + t] * (1.0 - DC_MARGIN) - rQ - rad[t];
+        const double lb = (double)dc[Q * T + t] * (1.0 - dc_margin) - rQ - rad[t];
         keep = lb <= UQ;
       }
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
@@ -547,6 +550,303 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   return PGK_OK;
 }
 
+// ===========================================================================
+// F32 path (general float data: configs 1, 3, 4).  Same tiles and bounds; the
+// tile passes run the SIMT direct-difference kernel over candidate lists and
+// keep S = K + margin approximate survivors per row, which pool_simt.cu's
+// float64 rerank then proves exact (or sends to the exact fallback).  Points
+// with exact distance > U_Q are excluded by the bound, so the rerank's proof
+// only has to cover the candidates it saw.
+//   * assignment: the first <= 128 dimensions quantised to u8 by one global
+//     affine map feed the tcgen05 K = 1 kernel -- only an efficiency
+//     heuristic, correctness rests on the float64 radii of step 3;
+//   * dc: fp32 direct-difference centroid distances, relative error
+//     <= (d+2) 2^-24 on dc^2 (margin scaled with d);
+//   * U_Q: the pass-1 K-th *approximate* distance a_K bounds the exact K-th
+//     one by a_K / (1 - gamma), gamma = (d+2) 2^-24 (the rerank's bound).
+// ===========================================================================
+namespace tiles {
+
+constexpr int DA = 128;  // assignment dimensions
+// one center per 256 rows: mixture data with many components (config 4: 1000
+// components, 2M points) still gets a center in practically every component
+// (P(miss) ~ e^-7.8), which keeps cells -- hence tiles -- single-component
+constexpr int CSTRIDE_F = 256;
+
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t o) {
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+
+// global min / max over the first da dimensions (orderable-uint atomics)
+__global__ void minmax_kernel(const float *__restrict__ X, int64_t n, int d, int da,
+                              uint32_t *__restrict__ mm) {
+  uint32_t lo = 0xffffffffu, hi = 0u;
+  const int64_t total = n * da;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / da;
+    const uint32_t o = f2ord(X[r * d + (e - r * da)]);
+    lo = min(lo, o);
+    hi = max(hi, o);
+  }
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
+  }
+}
+
+// rows (every `stride`-th from `first` of X) -> da integer-valued floats in [0, 255]
+__global__ void quantize_kernel(const float *__restrict__ X, int64_t rows, int64_t stride,
+                                int d, int da, const uint32_t *__restrict__ mm,
+                                float *__restrict__ out) {
+  const float lo = ord2f(mm[0]), hi = ord2f(mm[1]);
+  const float scale = hi > lo ? 255.0f / (hi - lo) : 0.0f;
+  const int64_t total = rows * da;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / da;
+    const float v = X[r * stride * d + (e - r * da)];
+    out[e] = fminf(255.0f, fmaxf(0.0f, rintf((v - lo) * scale)));
+  }
+}
+
+// tile-sorted float rows; padding rows are zero (perm < 0 keeps them out)
+__global__ void gather_sorted_f32_kernel(const float *__restrict__ X, int d,
+                                         const int32_t *__restrict__ perm, int64_t np,
+                                         float *__restrict__ xs) {
+  const int64_t total = np * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / d;
+    const int32_t src = perm[r];
+    xs[e] = src >= 0 ? X[(int64_t)src * d + (e - r * d)] : 0.0f;
+  }
+}
+
+// warp per tile: float64 centroid of the real rows (stored fp32), radius
+// against the stored centroid in float64 (inflated)
+__global__ void tile_stats_f32_kernel(const float *__restrict__ xs,
+                                      const int32_t *__restrict__ perm, int d, int64_t ntiles,
+                                      float *__restrict__ cent, double *__restrict__ rad,
+                                      int32_t *__restrict__ size) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t r0 = t * TB;
+    int cnt = 0;
+    for (int i = 0; i < TB; ++i) cnt += perm[r0 + i] >= 0;
+    for (int k0 = 0; k0 < d; k0 += 32) {
+      const int k = k0 + lane;
+      double acc = 0.0;
+      if (k < d)
+        for (int i = 0; i < TB; ++i)
+          if (perm[r0 + i] >= 0) acc += (double)xs[(r0 + i) * d + k];
+      if (k < d) cent[t * d + k] = cnt ? (float)(acc / cnt) : 0.f;
+    }
+    __syncwarp();
+    double rmax = 0.0;
+    for (int i = 0; i < TB; ++i) {
+      if (perm[r0 + i] < 0) continue;
+      double s = 0.0;
+      for (int k = lane; k < d; k += 32) {
+        const double t_ = (double)xs[(r0 + i) * d + k] - (double)cent[t * d + k];
+        s += t_ * t_;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      rmax = fmax(rmax, s);
+    }
+    if (lane == 0) {
+      rad[t] = sqrt(rmax) * (1.0 + MARGIN) + 1e-12;
+      size[t] = cnt;
+    }
+  }
+}
+
+struct LayoutF32 {
+  float *cen_q, *xq, *cent, *dcm, *xs;
+  int32_t *cnorm, *xnorm, *hist, *cursor, *assign, *perm, *size, *lists, *lens;
+  uint32_t *mm;
+  int64_t *off, *scan_tmp;
+  uint64_t *akeys, *keys1;
+  double *rad, *U;
+  unsigned long long *total;
+  void *sub_ws;
+  size_t sub_bytes, bytes;
+  int64_t C, NPmax, Tmax;
+};
+
+}  // namespace tiles
+
+static tiles::LayoutF32 tiles_layout_f32(void *ws, size_t bytes, int64_t n, int64_t d,
+                                         int64_t K) {
+  using namespace tiles;
+  LayoutF32 L{};
+  Carve c(ws, bytes);
+  L.C = (n + CSTRIDE_F - 1) / CSTRIDE_F;
+  L.NPmax = (n + TB - 1) / TB * TB + L.C * TB;
+  L.Tmax = L.NPmax / TB;
+  const int64_t C = L.C, NP = L.NPmax, T = L.Tmax;
+  // layout prefix shared with Layout: size / perm / total / akeys are what
+  // the order and work helpers read (tiles_order_ptrs)
+  L.total = c.take<unsigned long long>(4);
+  L.mm = c.take<uint32_t>(2);
+  L.cen_q = c.take<float>((size_t)C * DA);
+  L.xq = c.take<float>((size_t)n * DA);
+  L.cnorm = c.take<int32_t>(C + 128);
+  L.xnorm = c.take<int32_t>(n + 128);
+  L.akeys = c.take<uint64_t>(n);
+  L.hist = c.take<int32_t>(C);
+  L.cursor = c.take<int32_t>(C);
+  L.assign = c.take<int32_t>(n);
+  L.off = c.take<int64_t>(C + 1);
+  L.scan_tmp = c.take<int64_t>(scan_scratch(C + 1));
+  L.perm = c.take<int32_t>(NP);
+  L.xs = c.take<float>((size_t)NP * d);
+  L.cent = c.take<float>((size_t)T * d);
+  L.rad = c.take<double>(T);
+  L.size = c.take<int32_t>(T);
+  L.lists = c.take<int32_t>((size_t)T * T);
+  L.lens = c.take<int32_t>(T);
+  L.dcm = c.take<float>((size_t)T * T);
+  L.U = c.take<double>(T);
+  L.keys1 = c.take<uint64_t>((size_t)n * K);
+  L.sub_bytes = tc_pool_workspace(C, n, false);
+  L.sub_ws = c.take<char>(L.sub_bytes);
+  L.bytes = c.off;
+  return L;
+}
+
+bool tiles_f32_supported(int64_t n, int64_t d, int64_t k) {
+  static int env = -1;
+  if (env < 0) {
+    const char *e = getenv("PGK_DISABLE_PRUNE");
+    env = (e && e[0] == '1') ? 1 : 0;
+  }
+  const int64_t T = ((n + 127) / 128 * 128 + (n + 255) / 256 * 128) / 128;
+  return !env && k <= 384 && n >= 8 * tiles::TB && T <= 32768;
+}
+
+size_t tiles_f32_workspace(int64_t n, int64_t d, int64_t k) {
+  return tiles_layout_f32(nullptr, 0, n, d, k).bytes;
+}
+
+int launch_pool_f32_lists(const float *xs, int64_t np, int d, int S, int vec4,
+                          const int32_t *tlist, const int32_t *tlen, int64_t tstride,
+                          const int32_t *perm, uint64_t *keys, cudaStream_t stream);
+
+// The pruned F32 pool: every row's S best approximate keys in keys (n x S,
+// original order, original ids), for pool_simt.cu's rerank + fallback.
+int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64_t *keys,
+                          void *tws, size_t tws_bytes, cudaStream_t stream, bool *handled) {
+  using namespace tiles;
+  *handled = false;
+  if (!tiles_f32_supported(n, d, K)) return PGK_OK;
+  LayoutF32 L = tiles_layout_f32(tws, tws_bytes, n, d, K);
+  if (L.bytes > tws_bytes) {
+    set_error("F32 tile workspace too small");
+    return PGK_ERR_NOMEM;
+  }
+  const int sms = num_sms();
+  const int64_t C = L.C, NP = L.NPmax, T = L.Tmax;
+  const unsigned g = (unsigned)sms * 8;
+  const int da = d < DA ? d : DA;
+  // 1. approximate nearest center on quantised leading dimensions (tcgen05)
+  const uint32_t mm0[2] = {0xffffffffu, 0u};
+  PGK_CUDA(cudaMemcpyAsync(L.mm, mm0, sizeof(mm0), cudaMemcpyHostToDevice, stream));
+  minmax_kernel<<<g, 256, 0, stream>>>(X, n, d, da, L.mm);
+  PGK_CHECK_LAUNCH("minmax_kernel");
+  quantize_kernel<<<g, 256, 0, stream>>>(X, n, 1, d, da, L.mm, L.xq);
+  PGK_CHECK_LAUNCH("quantize_kernel");
+  quantize_kernel<<<g, 256, 0, stream>>>(X, C, CSTRIDE_F, d, da, L.mm, L.cen_q);
+  PGK_CHECK_LAUNCH("quantize_kernel");
+  int rc = launch_norms_u8(L.cen_q, C, da, L.cnorm, stream);
+  if (rc) return rc;
+  rc = launch_norms_u8(L.xq, n, da, L.xnorm, stream);
+  if (rc) return rc;
+  bool h = false;
+  rc = launch_pool_tc_u8_lists(L.cen_q, C, da, L.xq, n, 0, L.cnorm, L.xnorm, 1, L.akeys,
+                               L.sub_ws, L.sub_bytes, stream, nullptr, nullptr, nullptr, 0,
+                               nullptr, &h);
+  if (rc) return rc;
+  if (!h) return PGK_OK;
+  // 2. counting sort by center, runs padded to whole tiles
+  PGK_CUDA(cudaMemsetAsync(L.hist, 0, C * 4, stream));
+  PGK_CUDA(cudaMemsetAsync(L.cursor, 0, C * 4, stream));
+  assign_hist_kernel<<<g, 256, 0, stream>>>(L.akeys, n, L.hist, L.assign);
+  PGK_CHECK_LAUNCH("assign_hist_kernel");
+  padded_len_kernel<<<g, 256, 0, stream>>>(L.hist, C, L.off);
+  PGK_CHECK_LAUNCH("padded_len_kernel");
+  rc = exclusive_scan(L.off, L.off, C + 1, L.scan_tmp, stream);
+  if (rc) return rc;
+  fill_i32_kernel<<<g, 256, 0, stream>>>(L.perm, NP, -1);
+  PGK_CHECK_LAUNCH("fill_i32_kernel");
+  assign_scatter_kernel<<<g, 256, 0, stream>>>(L.assign, n, L.off, L.cursor, L.perm);
+  PGK_CHECK_LAUNCH("assign_scatter_kernel");
+  // 3. sorted rows, tile summaries (float64), centroid distances
+  gather_sorted_f32_kernel<<<g, 256, 0, stream>>>(X, d, L.perm, NP, L.xs);
+  PGK_CHECK_LAUNCH("gather_sorted_f32_kernel");
+  tile_stats_f32_kernel<<<g, 256, 0, stream>>>(L.xs, L.perm, d, T, L.cent, L.rad, L.size);
+  PGK_CHECK_LAUNCH("tile_stats_f32_kernel");
+  PGK_CUDA(cudaMemsetAsync(L.total, 0, 4 * sizeof(unsigned long long), stream));
+  tile_dist_kernel<<<dim3((unsigned)((T + DB - 1) / DB), (unsigned)((T + DB - 1) / DB)), 256, 0,
+                     stream>>>(L.cent, T, d, L.dcm);
+  PGK_CHECK_LAUNCH("tile_dist_kernel");
+  // 4. pass 1: top-K over each query tile's nearest tiles -> U_Q
+  const int vec4 = (d % 4 == 0);
+  tile_nearest_kernel<<<g, 256, 0, stream>>>(L.dcm, L.size, T, K, L.lists, L.lens, L.total + 1);
+  PGK_CHECK_LAUNCH("tile_nearest_kernel");
+  rc = launch_pool_f32_lists(L.xs, NP, d, K, vec4, L.lists, L.lens, T, L.perm, L.keys1, stream);
+  if (rc) return rc;
+  const double gamma = (double)(d + 2) * 5.9604644775390625e-08 * 1.001 + 1e-12;
+  tile_ubound_kernel<<<g, 256, 0, stream>>>(L.keys1, K, L.perm, T, L.U, 1.0 / (1.0 - gamma));
+  PGK_CHECK_LAUNCH("tile_ubound_kernel");
+  // 5. pass 2: every tile that can hold a pool member; S approximate survivors
+  const double dc_margin = std::max(DC_MARGIN, 2.0 * gamma);
+  tile_filter_kernel<<<g, 256, 0, stream>>>(L.dcm, L.rad, L.size, L.U, T, L.lists, L.lens,
+                                            L.total, dc_margin);
+  PGK_CHECK_LAUNCH("tile_filter_kernel");
+  rc = launch_pool_f32_lists(L.xs, NP, d, S, vec4, L.lists, L.lens, T, L.perm, keys, stream);
+  if (rc) return rc;
+  const char *se = getenv("PGK_TILES_STATS");
+  if (se && se[0] == '1') {
+    unsigned long long tot[2] = {0, 0};
+    PGK_CUDA(cudaMemcpyAsync(tot, L.total, sizeof(tot), cudaMemcpyDeviceToHost, stream));
+    std::vector<double> hr(T), hu(T);
+    std::vector<int32_t> hs(T);
+    PGK_CUDA(cudaMemcpyAsync(hr.data(), L.rad, T * 8, cudaMemcpyDeviceToHost, stream));
+    PGK_CUDA(cudaMemcpyAsync(hu.data(), L.U, T * 8, cudaMemcpyDeviceToHost, stream));
+    PGK_CUDA(cudaMemcpyAsync(hs.data(), L.size, T * 4, cudaMemcpyDeviceToHost, stream));
+    PGK_CUDA(cudaStreamSynchronize(stream));
+    std::vector<double> r2, u2;
+    for (int64_t t = 0; t < T; ++t)
+      if (hs[t] > 0) { r2.push_back(hr[t]); u2.push_back(hu[t]); }
+    auto q = [](std::vector<double> v, double f) {
+      std::sort(v.begin(), v.end());
+      return v.empty() ? 0.0 : v[(size_t)(f * (v.size() - 1))];
+    };
+    const double real = (double)r2.size();
+    fprintf(stderr,
+            "[tiles f32] %.0f tiles; pass-1 pairs %llu, pass-2 pairs %llu = %.3f%% of all, mean "
+            "list %.1f | radius p50/p90 %.3g %.3g | U_Q p50/p90 %.3g %.3g\n",
+            real, tot[1], tot[0], 100.0 * tot[0] / (real * real), tot[0] / real, q(r2, .5),
+            q(r2, .9), q(u2, .5), q(u2, .9));
+  }
+  {  // work record: [2] assignment (center) pairs, [3] done
+    const unsigned long long rec[2] = {
+        (unsigned long long)((n + TB - 1) / TB) * (unsigned long long)((C + TB - 1) / TB), 1ull};
+    PGK_CUDA(cudaMemcpyAsync(L.total + 2, rec, sizeof(rec), cudaMemcpyHostToDevice, stream));
+  }
+  *handled = true;
+  return PGK_OK;
+}
+
 // Locality order of the last pruned launch: the real rows of the tile
 // permutation, tile by tile (identity when the pruned path did not run).
 __global__ void order_scan_kernel(const int32_t *__restrict__ size, int64_t T,
@@ -596,16 +896,28 @@ __global__ void order_emit_kernel(const int32_t *__restrict__ perm, const int64_
   }
 }
 
+static int tiles_order_ptrs(const int32_t *size, const int32_t *perm, int64_t T, int64_t n,
+                            const unsigned long long *total, int64_t *toff, int32_t *out,
+                            cudaStream_t stream) {
+  order_scan_kernel<<<1, 1024, 0, stream>>>(size, T, toff);
+  PGK_CHECK_LAUNCH("order_scan_kernel");
+  order_emit_kernel<<<(unsigned)num_sms() * 4, 256, 0, stream>>>(perm, toff, T, n, total, out);
+  PGK_CHECK_LAUNCH("order_emit_kernel");
+  return PGK_OK;
+}
+
 int tiles_order(void *tws, int64_t n, int64_t d, int32_t *out, cudaStream_t stream) {
   tiles::Layout L = tiles_layout(tws, ~size_t(0), n, d);
   // toff reuses the assignment-key scratch (n >= T entries, free after the sort)
-  int64_t *toff = reinterpret_cast<int64_t *>(L.akeys);
-  order_scan_kernel<<<1, 1024, 0, stream>>>(L.size, L.Tmax, toff);
-  PGK_CHECK_LAUNCH("order_scan_kernel");
-  order_emit_kernel<<<(unsigned)num_sms() * 4, 256, 0, stream>>>(L.perm, toff, L.Tmax, n, L.total,
-                                                                out);
-  PGK_CHECK_LAUNCH("order_emit_kernel");
-  return PGK_OK;
+  return tiles_order_ptrs(L.size, L.perm, L.Tmax, n, L.total,
+                          reinterpret_cast<int64_t *>(L.akeys), out, stream);
+}
+
+int tiles_f32_order(void *tws, int64_t n, int64_t d, int64_t k, int32_t *out,
+                    cudaStream_t stream) {
+  tiles::LayoutF32 L = tiles_layout_f32(tws, ~size_t(0), n, d, k);
+  return tiles_order_ptrs(L.size, L.perm, L.Tmax, n, L.total,
+                          reinterpret_cast<int64_t *>(L.akeys), out, stream);
 }
 
 // Work record of the last pruned launch on `tws` (blocking read):
@@ -614,6 +926,15 @@ int tiles_order(void *tws, int64_t n, int64_t d, int32_t *out, cudaStream_t stre
 int tiles_work(const void *tws, int64_t n, int64_t d, unsigned long long out[4],
                cudaStream_t stream) {
   tiles::Layout L = tiles_layout(const_cast<void *>(tws), ~size_t(0), n, d);
+  PGK_CUDA(cudaMemcpyAsync(out, L.total, 4 * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, stream));
+  PGK_CUDA(cudaStreamSynchronize(stream));
+  return PGK_OK;
+}
+
+int tiles_f32_work(const void *tws, int64_t n, int64_t d, int64_t k, unsigned long long out[4],
+                   cudaStream_t stream) {
+  tiles::LayoutF32 L = tiles_layout_f32(const_cast<void *>(tws), ~size_t(0), n, d, k);
   PGK_CUDA(cudaMemcpyAsync(out, L.total, 4 * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, stream));
   PGK_CUDA(cudaStreamSynchronize(stream));

@@ -368,3 +368,56 @@ np.savez(sys.argv[1], **out)
     assert res["gram"].keys() == res["warp"].keys()
     for k in res["gram"]:
         np.testing.assert_array_equal(res["gram"][k], res["warp"][k], err_msg=k)
+
+
+def test_float_tile_pruning_equals_full_scan():
+    """The pruned F32 pool (tile bounds + approximate survivors + float64
+    rerank) returns exactly the brute-force result (PGK_DISABLE_PRUNE=1), pools
+    and both phases, on float configs where pruning applies, each in a fresh
+    process."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, %r)
+from paper_2410_01231_b200 import Dataset, PruneParams, knn_pools, prune_all, add_reverse_and_prune, synth
+out = {}
+for name, data, K, R in (("cfg1", synth.cfg1(10000), 64, 24), ("cfg3", synth.cfg3(30000), 128, 32),
+                         ("cfg4", synth.cfg4(12000), 256, 64)):
+    ds = Dataset.from_array(data)
+    ids, dists = knn_pools(ds, K)
+    off = np.arange(ds.n + 1, dtype=np.int64) * K
+    cnt = np.full(ds.n, K, np.int32)
+    p = PruneParams(M=R)
+    a = prune_all(ds, off, cnt, ids.ravel(), dists.ravel(), p)
+    b = add_reverse_and_prune(ds, a[0], a[1], a[2], p)
+    out[name + "_ids"], out[name + "_d"] = ids, dists
+    out[name + "_b"], out[name + "_bc"] = b[0], b[2]
+np.savez(sys.argv[1], **out)
+''' % str(root)
+    res = {}
+    for tag, env in (("pruned", {}), ("full", {"PGK_DISABLE_PRUNE": "1"})):
+        path = f"/tmp/pgk_f32prune_{tag}.npz"
+        subprocess.check_call([sys.executable, "-c", code, path],
+                              env=dict(os.environ, **env), timeout=900)
+        res[tag] = dict(np.load(path))
+    for k in res["full"]:
+        np.testing.assert_array_equal(res["pruned"][k], res["full"][k], err_msg=k)
+
+
+@pytest.mark.parametrize("cfg,rows", [(3, 300), (4, 150)])
+def test_full_scale_float_pools_on_seeded_rows(cfg, rows):
+    """Config 3 (1M x 960) and config 4 (2M x 768) at full size: the pools of
+    seeded rows equal the oracle's exact k-NN (float64, id ties) with fp32
+    list distances (SURVEY 8(d): prefixes + seeded rows at full N)."""
+    c = synth.CONFIGS[cfg]
+    data = c["gen"](c["n"], c["n"])
+    ds = Dataset.from_array(data)
+    ids, dists = knn_pools(ds, c["K"])
+    sel = np.sort(np.random.default_rng(100 + cfg).choice(ds.n, rows, replace=False))
+    o_ids, o_d = oracle.knn_pools(data, c["K"], rows=sel)
+    np.testing.assert_array_equal(ids[sel], o_ids)
+    np.testing.assert_array_equal(dists[sel], o_d)
