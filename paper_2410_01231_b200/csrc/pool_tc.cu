@@ -34,6 +34,8 @@ constexpr int BN = 128;   // data points per tile == MMA N
 constexpr int KB = 128;   // bytes per (padded) row
 constexpr int STAGES = 2;       // B-tile ring depth
 constexpr int ACC = 1;          // TMEM accumulator stages (128 columns each)
+constexpr int HALVES = 2;       // each accumulator is filled / drained in two 64-column halves
+constexpr int HN = BN / HALVES;
 constexpr int CTAS_PER_SM = 3;  // co-resident CTAs share the tensor core
 constexpr int TILE_BYTES = BN * KB;
 constexpr int CAP = 1024;  // per-row candidate buffer (keys, global memory)
@@ -45,17 +47,20 @@ struct __align__(1024) Smem {
   uint8_t a[BM * KB];
   uint8_t b[STAGES][TILE_BYTES];
   int32_t sv[4][32 * 36];  // per epilogue warp: one chunk of s values per lane
-  alignas(16) int32_t ny[ACC][BN];   // |x|^2 of the tile in each accumulator stage
-  alignas(16) int32_t pid[ACC][BN];  // original ids of the tile's columns (pruned path)
+  alignas(16) int32_t ny[2][BN];   // |x|^2 of the tile (double-buffered by tile parity)
+  alignas(16) int32_t pid[2][BN];  // original ids of the tile's columns (pruned path)
   uint64_t full[STAGES], empty[STAGES];
-  uint64_t tfull[ACC], tempty[ACC];
+  uint64_t tfull[HALVES], tempty[HALVES];  // per accumulator half
   uint64_t a_full, a_empty;
   uint32_t tmem_base;
   int32_t blk[2];  // dynamic schedule: block index per A-tile phase (-1 = done)
 };
 
 // kind::i8 instruction descriptor: D s32, A/B u8, K-major, M=128, N=BN
-constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// half-width (N = 64) MMAs: half h of a tile lands in TMEM columns h*64..h*64+63,
+// so the MMA of the next tile's first half overlaps the epilogue's second half
+constexpr uint32_t IDESC_H =
+    (2u << 4) | ((uint32_t)(HN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
 // Internal keys of this kernel: ((uint64)dist << 32) | id with dist the exact
 // integer distance (< 2^25), so key order == (dist, id) order.
@@ -241,8 +246,9 @@ __global__ void __maxnreg__(112)
     }                                           \
   } while (0)
   extern __shared__ uint8_t smem_raw[];
-  Smem &s = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                      ~uintptr_t(1023));
+  // 1024-B aligned view, derived from the shared array itself so every access
+  // compiles to LDS/STS (an integer round trip would leave generic LD/ST)
+  Smem &s = *reinterpret_cast<Smem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nblocks = (int)((nq + BM - 1) / BM);
   const int ntiles = (int)((n + BN - 1) / BN);
@@ -252,7 +258,7 @@ __global__ void __maxnreg__(112)
       mbar_init(&s.full[i], 1);
       mbar_init(&s.empty[i], 1);
     }
-    for (int i = 0; i < ACC; ++i) {
+    for (int i = 0; i < HALVES; ++i) {
       mbar_init(&s.tfull[i], 1);
       mbar_init(&s.tempty[i], 4);
     }
@@ -307,7 +313,7 @@ __global__ void __maxnreg__(112)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
-      int stage = 0, acc = 0;
+      int stage = 0, tpar = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int it = 0;; ++it) {
         mbar_wait(&s.a_full, it & 1);
@@ -318,22 +324,31 @@ __global__ void __maxnreg__(112)
         const uint64_t adesc = sw128_desc(s.a);
         for (int t = 0; t < len; ++t) {
           const int tid = tlist ? tlist[(int64_t)b * tstride + t] : t;
-          mbar_wait(&s.tempty[acc], acc_phase ^ 1);
-          // the tile's |x|^2 (xnorm is padded to a multiple of BN) lands with the
-          // accumulator: tfull completes on the commit AND these bytes
-          mbar_expect_tx_only(&s.tfull[acc], perm ? BN * 8 : BN * 4);
-          bulk_load(s.ny[acc], xnorm + (int64_t)tid * BN, BN * 4, &s.tfull[acc]);
-          if (perm) bulk_load(s.pid[acc], perm + (int64_t)tid * BN, BN * 4, &s.tfull[acc]);
-          mbar_wait(&s.full[stage], phase);
-          tc_fence_after();
-          const uint64_t bdesc = sw128_desc(s.b[stage]);
 #pragma unroll
-          for (int kk = 0; kk < KB / 32; ++kk)  // K = 32 bytes per MMA; +32 B = +2 (16 B units)
-            mma_i8(tmem + acc * BN, adesc + 2 * kk, bdesc + 2 * kk, IDESC, kk > 0);
+          for (int h = 0; h < HALVES; ++h) {
+            mbar_wait(&s.tempty[h], acc_phase ^ 1);
+            if (h == 0) {
+              // the tile's |x|^2 (xnorm is padded to a multiple of BN) and ids
+              // land with the first half: tfull[0] completes on the commit AND
+              // these bytes (buffer by tile parity: the epilogue may still read
+              // the previous tile's in its second half)
+              mbar_expect_tx_only(&s.tfull[0], perm ? BN * 8 : BN * 4);
+              bulk_load(s.ny[tpar], xnorm + (int64_t)tid * BN, BN * 4, &s.tfull[0]);
+              if (perm) bulk_load(s.pid[tpar], perm + (int64_t)tid * BN, BN * 4, &s.tfull[0]);
+              mbar_wait(&s.full[stage], phase);
+            }
+            tc_fence_after();
+            // rows h*64.. of the B tile: 8 SW128 atoms of 1024 B further on
+            const uint64_t bdesc = sw128_desc(s.b[stage] + h * HN * KB);
+#pragma unroll
+            for (int kk = 0; kk < KB / 32; ++kk)  // K = 32 bytes per MMA; +32 B = +2 (16 B units)
+              mma_i8(tmem + h * HN, adesc + 2 * kk, bdesc + 2 * kk, IDESC_H, kk > 0);
+            tc_commit(&s.tfull[h]);
+          }
           tc_commit(&s.empty[stage]);
-          tc_commit(&s.tfull[acc]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
-          if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+          acc_phase ^= 1;
+          tpar ^= 1;
         }
         tc_commit(&s.a_empty);
       }
@@ -343,7 +358,7 @@ __global__ void __maxnreg__(112)
     const int q = warp & 3;  // TMEM lane quarter this warp may access (warp % 4)
     int32_t *const svw = s.sv[warp - 2];  // this warp's staging: lane l at svw[l * 36]
     int32_t *sv = svw + lane * 36;
-    int acc = 0;
+    int tpar = 0;
     uint32_t acc_phase = 0;
     for (int it = 0;; ++it) {
       mbar_wait(&s.a_full, it & 1);
@@ -392,20 +407,27 @@ __global__ void __maxnreg__(112)
       for (int t = 0; t < len; ++t) {
         const int tid = tlist ? tid_next : t;
         if (tlist && t + 1 < len) tid_next = tlist[(int64_t)b * tstride + t + 1];
-        PGK_TICK(ST_MAIN);
-        mbar_wait(&s.tfull[acc], acc_phase);
-        tc_fence_after();
-        PGK_TICK(ST_WAIT);
         const int64_t col0 = (int64_t)tid * BN;
-        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
+          if ((c & 1) == 0) {  // entering half c/2: wait for its MMAs
+            if (c > 0) {  // the previous half is in registers: let the MMA reuse it
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&s.tempty[(c >> 1) - 1]);
+            }
+            PGK_TICK(ST_MAIN);
+            mbar_wait(&s.tfull[c >> 1], acc_phase);
+            tc_fence_after();
+            PGK_TICK(ST_WAIT);
+          }
           // (co-resident CTAs hide the TMEM-load latency; one chunk in flight)
           uint32_t r[32];
           tmem_ld32(tbase + c * 32, r);
           tmem_wait_ld();
           const int64_t cb = col0 + c * 32;
-          const int4 *nyp = reinterpret_cast<const int4 *>(s.ny[acc] + c * 32);
+          const int4 *nyp = reinterpret_cast<const int4 *>(s.ny[tpar] + c * 32);
           // s_j = |x_j|^2 - 2 q.x_j ; pass iff s_j <= tp
           uint32_t mask = 0;
 #pragma unroll
@@ -423,7 +445,7 @@ __global__ void __maxnreg__(112)
             // the data, not a padding slot of the tile sort), and a row never
             // keeps itself
             const int64_t colj = cb + lane;
-            const int32_t cidj = perm ? s.pid[acc][c * 32 + lane] : (int32_t)colj;
+            const int32_t cidj = perm ? s.pid[tpar][c * 32 + lane] : (int32_t)colj;
             mask &= __ballot_sync(0xffffffffu, colj < n && cidj >= 0);
             if (exclude_self && row >= cb && row < cb + 32) mask &= ~(1u << (int)(row - cb));
             const bool track = K > 1 && tau == KEY_MAX && mask;
@@ -448,7 +470,7 @@ __global__ void __maxnreg__(112)
                 const int j = __ffs(mask) - 1;
                 mask &= mask - 1;
                 const uint64_t key = ((uint64_t)(uint32_t)(sv[j] + nx) << 32) |
-                                     (uint32_t)(perm ? s.pid[acc][c * 32 + j] : (int32_t)(cb + j));
+                                     (uint32_t)(perm ? s.pid[tpar][c * 32 + j] : (int32_t)(cb + j));
                 if (key < tau) {
                   tau = key;
                   tp = tau_prefilter(tau, nx);
@@ -496,7 +518,7 @@ __global__ void __maxnreg__(112)
               while (mm) {
                 const int j = __ffs(mm) - 1;
                 mm &= mm - 1;
-                const int32_t cid = perm ? s.pid[acc][c * 32 + j] : (int32_t)(cb + j);
+                const int32_t cid = perm ? s.pid[tpar][c * 32 + j] : (int32_t)(cb + j);
                 *mybuf++ = ((uint64_t)(uint32_t)(sv[j] + nx) << 32) | (uint32_t)cid;
               }
             }
@@ -512,11 +534,12 @@ __global__ void __maxnreg__(112)
             PGK_TICK(ST_SLOW);
           }
         }
-        // accumulator and its norms fully consumed: hand the stage back
+        // last half and the tile's norms / ids consumed: hand them back
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&s.tempty[acc]);
-        if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+        if (lane == 0) mbar_arrive(&s.tempty[HALVES - 1]);
+        acc_phase ^= 1;
+        tpar ^= 1;
       }
       // block done: record each row's buffer fill and threshold; selection
       // and sorting run in the massively parallel finalize kernel

@@ -112,8 +112,9 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
                       int64_t *__restrict__ dist_evals, int64_t *__restrict__ angle_evals,
                       int32_t *__restrict__ long_rows, int32_t *__restrict__ long_count) {
   extern __shared__ uint8_t smem_raw[];
-  Smem &s = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                      ~uintptr_t(1023));
+  // 1024-B aligned view, derived from the shared array itself so every access
+  // compiles to LDS/STS (an integer round trip would leave generic LD/ST)
+  Smem &s = *reinterpret_cast<Smem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
