@@ -171,6 +171,42 @@ int pgk_knn_work(const void *ws, int64_t n, int64_t nq, int64_t d, int64_t k,
 int pgk_knn_order(const void *ws, int64_t n, int64_t d, int64_t k, int mode,
                   int32_t *order, void *stream);
 
+/* ---- beam search and phase C ----------------------
+ * Replaces the numba search core the reference binds from Python:
+ * _kernels.search_one / search_many (_kernels.py:209-245, called by
+ * search.kann_search / search_batch, search.py:43-94, and by prune._connect /
+ * entry_point, prune.py:154-199) and graph.reachable_from (graph.py:112-123).
+ *
+ * pgk_beam_search: per query (rows of `queries`, device f32[nq*d]) a beam
+ * search with pool width L (<= 256) from `ep` (or eps[qi] when eps != NULL)
+ * over the adjacency adj (device int32[n*width], -1 padded) with `counts`;
+ * writes the first k pool entries skipping `exclude` (out_ids / out_dists
+ * [nq*k], -1 / +inf padded) and, when non-NULL, dist_counts / n_expanded
+ * [nq] (int64).  ws: pgk_search_workspace(n, nq) bytes. */
+int pgk_search_workspace(int64_t n, int64_t nq, size_t *ws_bytes_host);
+int pgk_beam_search(const float *data, int64_t n, int64_t d, const int32_t *adj,
+                    int64_t width, const int32_t *counts, const float *queries, int64_t nq,
+                    int64_t k, int64_t L, const int32_t *eps, int32_t ep, int32_t exclude,
+                    int32_t *out_ids, float *out_dists, int64_t *dist_counts,
+                    int64_t *n_expanded, void *ws, size_t ws_bytes, void *stream);
+
+/* Reachability bitmap seen (device uint32[(n+31)/32], bit v = node v):
+ * pgk_mark_reachable adds every node reachable from `start` through nodes not
+ * yet marked (start included; one-CTA BFS enqueued on the stream).
+ * pgk_first_unseen writes the smallest unmarked id, or -1 (blocking).
+ * ws: pgk_reach_workspace(n) bytes. */
+int pgk_reach_workspace(int64_t n, size_t *ws_bytes_host);
+int pgk_mark_reachable(const int32_t *adj, int64_t width, const int32_t *counts, int64_t n,
+                       int32_t start, uint32_t *seen, void *ws, size_t ws_bytes, void *stream);
+int pgk_first_unseen(const uint32_t *seen, int64_t n, int32_t *out_host, void *ws,
+                     void *stream);
+
+/* core.centroid (core.py:153-155): float64 column means, written as f32[d]
+ * (deterministic two-level sum).  ws: pgk_centroid_workspace(n, d) bytes. */
+int pgk_centroid_workspace(int64_t n, int64_t d, size_t *ws_bytes_host);
+int pgk_centroid(const float *data, int64_t n, int64_t d, float *out, void *ws,
+                 size_t ws_bytes, void *stream);
+
 /* Cumulative number of kernel launches this library has issued since it was
  * loaded (process-wide; the bench reports the difference around its timed
  * region as gpu_launches). */

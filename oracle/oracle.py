@@ -67,6 +67,11 @@ def lib():
         L.orc_merge_with_reverse.argtypes = [P, P, P, I64, I64, P, P, P, P, P, P, P]
         L.orc_knn_pool.argtypes = [P, I64, I64, I64, I32, P, I64, P, P]
         L.orc_list_dists_sorted.argtypes = [P, I64, P, I64, I64, P, P]
+        L.orc_search_many.restype = None
+        L.orc_search_many.argtypes = [P, I64, I64, P, I64, P, P, I64, I64, I64, I32, I32, P,
+                                      P, P]
+        L.orc_mark_reachable.restype = None
+        L.orc_mark_reachable.argtypes = [P, I64, P, I64, I32, P]
         L.orc_num_threads.restype = I32
         _lib = L
     return _lib
@@ -217,3 +222,79 @@ def refine_ab(data, pool_ids, pool_dists, M: int, strategy: str = "rng",
     a = prune_all(data, off, cnt, pool_ids.ravel(), pool_dists.ravel(), M, strategy, alpha)
     b = add_reverse_and_prune(data, a[0], a[1], a[2], M, strategy, alpha)
     return a, b
+
+
+# ---------------------------------------------------------------------------
+# Beam search and phase C (search.py:43-94, prune.py:154-229) -- restated on
+# the C search core above; pinned by tests/golden/search.npz.
+# ---------------------------------------------------------------------------
+
+def search_batch(data, adj, counts, queries, k: int, L: int, ep: int, exclude: int = -1):
+    """search.py:81-94 / _kernels.search_many: (ids, dists, dist_counts)."""
+    data = _f32(data)
+    adj = np.ascontiguousarray(adj, np.int32)
+    counts = np.ascontiguousarray(counts, np.int32)
+    q = _f32(np.atleast_2d(queries))
+    nq = q.shape[0]
+    ids = np.full((nq, k), EMPTY, np.int32)
+    dists = np.full((nq, k), np.inf, np.float32)
+    dc = np.zeros(nq, np.int64)
+    lib().orc_search_many(_p(data), data.shape[0], data.shape[1], _p(adj), adj.shape[1],
+                          _p(counts), _p(q), nq, k, L, int(ep), int(exclude), _p(ids),
+                          _p(dists), _p(dc))
+    return ids, dists, dc
+
+
+def centroid(data) -> np.ndarray:
+    """core.py:153-155: float64 mean, returned float32."""
+    return np.asarray(data, np.float32).mean(axis=0, dtype=np.float64).astype(np.float32)
+
+
+def entry_point(data, adj, counts, k: int, L: int, seed: int = 0) -> int:
+    """prune.py:154-162: beam search for the centroid from a seeded random node."""
+    n = np.asarray(data).shape[0]
+    rn = int(np.random.default_rng(seed).integers(0, n))
+    ids, _, _ = search_batch(data, adj, counts, centroid(data), k, L, rn)
+    return int(ids[0, 0])
+
+
+def mark_reachable(adj, counts, start: int, seen=None) -> np.ndarray:
+    adj = np.ascontiguousarray(adj, np.int32)
+    counts = np.ascontiguousarray(counts, np.int32)
+    n = adj.shape[0]
+    seen = np.zeros(n, np.uint8) if seen is None else np.ascontiguousarray(seen, np.uint8)
+    lib().orc_mark_reachable(_p(adj), adj.shape[1], _p(counts), n, int(start), _p(seen))
+    return seen
+
+
+def connect(data, adj, counts, M: int, ep: int, connect_L: int):
+    """prune.py:165-199 (_connect): one edge per unreachable component head
+    (the first unreached id), from its nearest reachable node found by a
+    beam search from ep; widening by one column when that node's row is
+    full.  Returns (adj, counts, appended)."""
+    adj = np.array(adj, np.int32, copy=True)
+    counts = np.array(counts, np.int32, copy=True)
+    n = adj.shape[0]
+    seen = mark_reachable(adj, counts, ep)
+    appended = 0
+    while not seen.all():
+        v = int(np.flatnonzero(seen == 0)[0])
+        ids, _, _ = search_batch(data, adj, counts, np.asarray(data)[v], 1, connect_L, ep)
+        r = int(ids[0, 0])
+        if counts[r] == adj.shape[1]:
+            adj = np.hstack([adj, np.full((n, 1), EMPTY, np.int32)])
+        adj[r, counts[r]] = v
+        counts[r] += 1
+        appended += 1
+        seen = mark_reachable(adj, counts, v, seen)
+    return adj, counts, appended
+
+
+def finish_connect(data, b_ids, b_counts, M: int, ep=None, seed: int = 0, connect_L=None):
+    """The phase-C tail of prune.py:202-229 (finish_refine) on a phase-B graph:
+    (adj, counts, ep, over_cap)."""
+    L = max(M + 1, 32) if connect_L is None else connect_L
+    if ep is None:
+        ep = entry_point(data, b_ids, b_counts, 1, L, seed)
+    adj, counts, _ = connect(data, b_ids, b_counts, M, ep, L)
+    return adj, counts, int(ep), np.flatnonzero(counts > M).astype(np.int32)

@@ -56,11 +56,23 @@ def lib():
         L.pgk_knn_pools.argtypes = [P, I64, I64, P, I64, I64, I, I, P, P, P, P, SZ, P]
         L.pgk_knn_fallback_rows.argtypes = [P, P, P]
         L.pgk_knn_work.argtypes = [P, I64, I64, I64, I64, I, P, P]
+        I32 = ctypes.c_int32
+        L.pgk_search_workspace.argtypes = [I64, I64, P]
+        L.pgk_beam_search.argtypes = [P, I64, I64, P, I64, P, P, I64, I64, I64, P, I32, I32,
+                                      P, P, P, P, P, SZ, P]
+        L.pgk_reach_workspace.argtypes = [I64, P]
+        L.pgk_mark_reachable.argtypes = [P, I64, P, I64, I32, P, P, SZ, P]
+        L.pgk_first_unseen.argtypes = [P, I64, P, P, P]
+        L.pgk_centroid_workspace.argtypes = [I64, I64, P]
+        L.pgk_centroid.argtypes = [P, I64, I64, P, P, SZ, P]
         for f in ("pgk_device_check", "pgk_prune_batch", "pgk_prune_rows", "pgk_prune_rows_ex",
                   "pgk_prune_workspace",
                   "pgk_make_u8", "pgk_add_reverse_and_prune_ex", "pgk_reverse_workspace",
                   "pgk_add_reverse_and_prune", "pgk_detect_u8", "pgk_knn_workspace",
-                  "pgk_knn_pools", "pgk_knn_fallback_rows", "pgk_knn_work", "pgk_knn_order"):
+                  "pgk_knn_pools", "pgk_knn_fallback_rows", "pgk_knn_work", "pgk_knn_order",
+                  "pgk_search_workspace", "pgk_beam_search", "pgk_reach_workspace",
+                  "pgk_mark_reachable", "pgk_first_unseen", "pgk_centroid_workspace",
+                  "pgk_centroid"):
             getattr(L, f).restype = I
         _lib = L
     return _lib
@@ -70,7 +82,8 @@ EXPORTS = ("pgk_version", "pgk_last_error", "pgk_device_check", "pgk_prune_batch
            "pgk_prune_rows", "pgk_prune_rows_ex", "pgk_prune_workspace", "pgk_make_u8", "pgk_add_reverse_and_prune_ex",
            "pgk_reverse_workspace", "pgk_add_reverse_and_prune", "pgk_detect_u8",
            "pgk_knn_workspace", "pgk_knn_pools", "pgk_knn_fallback_rows", "pgk_knn_work",
-           "pgk_knn_order",
+           "pgk_knn_order", "pgk_search_workspace", "pgk_beam_search", "pgk_reach_workspace",
+           "pgk_mark_reachable", "pgk_first_unseen", "pgk_centroid_workspace", "pgk_centroid",
            "pgk_launch_count")
 
 

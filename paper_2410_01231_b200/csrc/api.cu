@@ -28,6 +28,16 @@ int num_sms() {
 }
 
 size_t prune_workspace(int64_t n_rows);
+size_t search_workspace(int64_t n, int64_t nq);
+int beam_search(const float *, int64_t, int64_t, const int32_t *, int64_t, const int32_t *,
+                const float *, int64_t, int64_t, int64_t, const int32_t *, int32_t, int32_t,
+                int32_t *, float *, int64_t *, int64_t *, void *, size_t, cudaStream_t);
+size_t reach_workspace(int64_t n);
+int mark_reachable(const int32_t *, int64_t, const int32_t *, int64_t, int32_t, uint32_t *,
+                   void *, size_t, cudaStream_t);
+int first_unseen(const uint32_t *, int64_t, int32_t *, void *, cudaStream_t);
+size_t centroid_workspace(int64_t n, int64_t d);
+int centroid(const float *, int64_t, int64_t, float *, void *, size_t, cudaStream_t);
 int launch_prune(const float *, const uint8_t *, const int32_t *, int64_t, int64_t,
                  const int32_t *, const int32_t *, void *, size_t, const int64_t *,
                  const int32_t *, const int32_t *,
@@ -214,6 +224,54 @@ int pgk_knn_order(const void *ws, int64_t n, int64_t d, int64_t k, int mode, int
 int pgk_knn_fallback_rows(const void *ws, int *rows_host, void *stream) {
   PGK_REQUIRE(ws && rows_host, "NULL argument");
   return fallback_rows(ws, rows_host, (cudaStream_t)stream);
+}
+
+int pgk_search_workspace(int64_t n, int64_t nq, size_t *ws_bytes_host) {
+  PGK_REQUIRE(ws_bytes_host, "NULL argument");
+  *ws_bytes_host = search_workspace(n, nq);
+  return PGK_OK;
+}
+
+int pgk_beam_search(const float *data, int64_t n, int64_t d, const int32_t *adj,
+                    int64_t width, const int32_t *counts, const float *queries, int64_t nq,
+                    int64_t k, int64_t L, const int32_t *eps, int32_t ep, int32_t exclude,
+                    int32_t *out_ids, float *out_dists, int64_t *dist_counts,
+                    int64_t *n_expanded, void *ws, size_t ws_bytes, void *stream) {
+  PGK_REQUIRE(data && adj && counts && out_ids && out_dists && ws, "NULL argument");
+  PGK_REQUIRE(nq == 0 || queries, "NULL queries");
+  return beam_search(data, n, d, adj, width, counts, queries, nq, k, L, eps, ep, exclude,
+                     out_ids, out_dists, dist_counts, n_expanded, ws, ws_bytes,
+                     (cudaStream_t)stream);
+}
+
+int pgk_reach_workspace(int64_t n, size_t *ws_bytes_host) {
+  PGK_REQUIRE(ws_bytes_host, "NULL argument");
+  *ws_bytes_host = reach_workspace(n);
+  return PGK_OK;
+}
+
+int pgk_mark_reachable(const int32_t *adj, int64_t width, const int32_t *counts, int64_t n,
+                       int32_t start, uint32_t *seen, void *ws, size_t ws_bytes, void *stream) {
+  PGK_REQUIRE(adj && counts && seen && ws, "NULL argument");
+  return mark_reachable(adj, width, counts, n, start, seen, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int pgk_first_unseen(const uint32_t *seen, int64_t n, int32_t *out_host, void *ws,
+                     void *stream) {
+  PGK_REQUIRE(seen && out_host && ws, "NULL argument");
+  return first_unseen(seen, n, out_host, ws, (cudaStream_t)stream);
+}
+
+int pgk_centroid_workspace(int64_t n, int64_t d, size_t *ws_bytes_host) {
+  PGK_REQUIRE(ws_bytes_host, "NULL argument");
+  *ws_bytes_host = centroid_workspace(n, d);
+  return PGK_OK;
+}
+
+int pgk_centroid(const float *data, int64_t n, int64_t d, float *out, void *ws,
+                 size_t ws_bytes, void *stream) {
+  PGK_REQUIRE(data && out && ws, "NULL argument");
+  return centroid(data, n, d, out, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 }  // extern "C"

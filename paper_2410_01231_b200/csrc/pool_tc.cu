@@ -263,7 +263,10 @@ __global__ void __maxnreg__(112)
       mbar_init(&s.tempty[i], 4);
     }
     mbar_init(&s.a_full, 1);
-    mbar_init(&s.a_empty, 1);
+    // the A tile / block slot is free once the MMA is done with it AND every
+    // epilogue warp has taken the block index: otherwise, with one-tile
+    // blocks, a_full could run two phases ahead of the epilogue (parity alias)
+    mbar_init(&s.a_empty, 1 + 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -364,6 +367,7 @@ __global__ void __maxnreg__(112)
       mbar_wait(&s.a_full, it & 1);
       const int b = s.blk[it & 1];
       if (b < 0) break;
+      if (lane == 0) mbar_arrive(&s.a_empty);  // block index taken
       const int64_t row = (int64_t)b * BM + q * 32 + lane;
       // padding rows (and, in a re-run, rows already finished): no pool
       const bool row_ok =

@@ -31,6 +31,18 @@ size_t scan_scratch(int64_t m);
 int exclusive_scan(const int64_t *in, int64_t *out, int64_t m, int64_t *scratch,
                    cudaStream_t stream);
 
+// PGK_DEBUG_SYNC=1: synchronise and report after every stage (hang hunting)
+static void dbg_stage(const char *what, cudaStream_t stream) {
+  static int env = -1;
+  if (env < 0) {
+    const char *e = getenv("PGK_DEBUG_SYNC");
+    env = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!env) return;
+  const cudaError_t err = cudaStreamSynchronize(stream);
+  fprintf(stderr, "[pgk debug] %s: %s\n", what, cudaGetErrorString(err));
+}
+
 namespace tiles {
 
 constexpr int TB = 128;  // tile size (== tc::BN == tc::BM)
@@ -414,20 +426,24 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   // 1. centers (every 512th row) + exact nearest center of every point (K = 1)
   gather_centers_kernel<<<g, 256, 0, stream>>>(X, n, d, C, L.cen);
   PGK_CHECK_LAUNCH("gather_centers_kernel");
+  dbg_stage("gather_centers_kernel", stream);
   int rc = launch_norms_u8(L.cen, C, d, L.cnorm, stream);
   if (rc) return rc;
   bool h = false;
   rc = launch_pool_tc_u8_lists(L.cen, C, d, X, n, 0, L.cnorm, xnorm, 1, L.akeys, L.sub_ws,
                                L.sub_bytes, stream, nullptr, nullptr, nullptr, 0, nullptr, &h);
   if (rc) return rc;
+  dbg_stage("assign tc", stream);
   if (!h) return PGK_OK;
   // 2. counting sort by center, every run padded to whole tiles (perm = -1)
   PGK_CUDA(cudaMemsetAsync(L.hist, 0, C * 4, stream));
   PGK_CUDA(cudaMemsetAsync(L.cursor, 0, C * 4, stream));
   assign_hist_kernel<<<g, 256, 0, stream>>>(L.akeys, n, L.hist, L.assign);
   PGK_CHECK_LAUNCH("assign_hist_kernel");
+  dbg_stage("assign_hist_kernel", stream);
   padded_len_kernel<<<g, 256, 0, stream>>>(L.hist, C, L.off);
   PGK_CHECK_LAUNCH("padded_len_kernel");
+  dbg_stage("padded_len_kernel", stream);
   rc = exclusive_scan(L.off, L.off, C + 1, L.scan_tmp, stream);
   if (rc) return rc;
   // the padded total lives on the device; kernels below run over the
@@ -436,31 +452,39 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   PGK_CHECK_LAUNCH("fill_i32_kernel");
   assign_scatter_kernel<<<g, 256, 0, stream>>>(L.assign, n, L.off, L.cursor, L.perm);
   PGK_CHECK_LAUNCH("assign_scatter_kernel");
+  dbg_stage("assign_scatter_kernel", stream);
   const int64_t NP = L.NPmax, T = L.Tmax;
   // 3. sorted u8 rows / norms, tile summaries, centroid distances
   gather_sorted_kernel<<<g, 256, 0, stream>>>(X, d, L.perm, xnorm, NP, L.xs, L.ns);
   PGK_CHECK_LAUNCH("gather_sorted_kernel");
+  dbg_stage("gather_sorted_kernel", stream);
   fill_i32_kernel<<<1, 128, 0, stream>>>(L.ns + NP, 128, 0x3f3f3f3f);
   PGK_CHECK_LAUNCH("fill_i32_kernel");
   tile_stats_kernel<<<g, 256, 0, stream>>>(L.xs, L.perm, d, T, L.cent, L.rad, L.size);
   PGK_CHECK_LAUNCH("tile_stats_kernel");
+  dbg_stage("tile_stats_kernel", stream);
   PGK_CUDA(cudaMemsetAsync(L.total, 0, 4 * sizeof(unsigned long long), stream));
   tile_dist_kernel<<<dim3((unsigned)((T + DB - 1) / DB), (unsigned)((T + DB - 1) / DB)), 256, 0,
                      stream>>>(L.cent, T, d, L.dcm);
   PGK_CHECK_LAUNCH("tile_dist_kernel");
+  dbg_stage("tile_dist_kernel", stream);
   // 4. pass 1: exact top-K over each query tile's NEAR nearest tiles -> U_Q
   tile_nearest_kernel<<<g, 256, 0, stream>>>(L.dcm, L.size, T, K, L.lists, L.lens, L.total + 1);
   PGK_CHECK_LAUNCH("tile_nearest_kernel");
+  dbg_stage("tile_nearest_kernel", stream);
   rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes, stream,
                                L.xs, L.lists, L.lens, T, L.perm, handled, nullptr, 1);
   if (rc) return rc;
+  dbg_stage("pass 1 tc", stream);
   if (!*handled) return PGK_OK;
   tile_ubound_kernel<<<g, 256, 0, stream>>>(keys, K, L.perm, T, L.U);
   PGK_CHECK_LAUNCH("tile_ubound_kernel");
+  dbg_stage("tile_ubound_kernel", stream);
   // 5. pass 2: every tile that can hold a pool member, then the full top-K
   tile_filter_kernel<<<g, 256, 0, stream>>>(L.dcm, L.rad, L.size, L.U, T, L.lists, L.lens,
                                             L.total);
   PGK_CHECK_LAUNCH("tile_filter_kernel");
+  dbg_stage("tile_filter_kernel", stream);
   const char *se = getenv("PGK_TILES_STATS");
   const bool stats = se && se[0] == '1';
   std::vector<uint64_t> seed_k;
@@ -476,11 +500,13 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
                                L.xs, L.lists, L.lens, T, L.perm, handled, keys, 0, shrink,
                                L.fail, out, L.fail_rows);
   if (rc) return rc;
+  dbg_stage("pass 2 tc", stream);
   if (shrink < 1.0f) {
     // 6. re-run the blocks holding a row whose guess was too tight, seeded by
     // its untouched pass-1 key (finished rows re-derive the same result)
     rerun_lens_kernel<<<g, 256, 0, stream>>>(L.fail, L.lens, T, L.lens2);
     PGK_CHECK_LAUNCH("rerun_lens_kernel");
+  dbg_stage("rerun_lens_kernel", stream);
     if (stats) {
       std::vector<int32_t> hf(T);
       PGK_CUDA(cudaMemcpyAsync(hf.data(), L.fail, T * 4, cudaMemcpyDeviceToHost, stream));
@@ -762,10 +788,13 @@ int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64
   PGK_CUDA(cudaMemcpyAsync(L.mm, mm0, sizeof(mm0), cudaMemcpyHostToDevice, stream));
   minmax_kernel<<<g, 256, 0, stream>>>(X, n, d, da, L.mm);
   PGK_CHECK_LAUNCH("minmax_kernel");
+  dbg_stage("minmax_kernel", stream);
   quantize_kernel<<<g, 256, 0, stream>>>(X, n, 1, d, da, L.mm, L.xq);
   PGK_CHECK_LAUNCH("quantize_kernel");
+  dbg_stage("quantize_kernel", stream);
   quantize_kernel<<<g, 256, 0, stream>>>(X, C, CSTRIDE_F, d, da, L.mm, L.cen_q);
   PGK_CHECK_LAUNCH("quantize_kernel");
+  dbg_stage("quantize_kernel", stream);
   int rc = launch_norms_u8(L.cen_q, C, da, L.cnorm, stream);
   if (rc) return rc;
   rc = launch_norms_u8(L.xq, n, da, L.xnorm, stream);
@@ -775,20 +804,24 @@ int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64
                                L.sub_ws, L.sub_bytes, stream, nullptr, nullptr, nullptr, 0,
                                nullptr, &h);
   if (rc) return rc;
+  dbg_stage("assign tc", stream);
   if (!h) return PGK_OK;
   // 2. counting sort by center, runs padded to whole tiles
   PGK_CUDA(cudaMemsetAsync(L.hist, 0, C * 4, stream));
   PGK_CUDA(cudaMemsetAsync(L.cursor, 0, C * 4, stream));
   assign_hist_kernel<<<g, 256, 0, stream>>>(L.akeys, n, L.hist, L.assign);
   PGK_CHECK_LAUNCH("assign_hist_kernel");
+  dbg_stage("assign_hist_kernel", stream);
   padded_len_kernel<<<g, 256, 0, stream>>>(L.hist, C, L.off);
   PGK_CHECK_LAUNCH("padded_len_kernel");
+  dbg_stage("padded_len_kernel", stream);
   rc = exclusive_scan(L.off, L.off, C + 1, L.scan_tmp, stream);
   if (rc) return rc;
   fill_i32_kernel<<<g, 256, 0, stream>>>(L.perm, NP, -1);
   PGK_CHECK_LAUNCH("fill_i32_kernel");
   assign_scatter_kernel<<<g, 256, 0, stream>>>(L.assign, n, L.off, L.cursor, L.perm);
   PGK_CHECK_LAUNCH("assign_scatter_kernel");
+  dbg_stage("assign_scatter_kernel", stream);
   // 3. sorted rows, tile summaries (float64), centroid distances
   gather_sorted_f32_kernel<<<g, 256, 0, stream>>>(X, d, L.perm, NP, L.xs);
   PGK_CHECK_LAUNCH("gather_sorted_f32_kernel");
@@ -798,20 +831,24 @@ int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64
   tile_dist_kernel<<<dim3((unsigned)((T + DB - 1) / DB), (unsigned)((T + DB - 1) / DB)), 256, 0,
                      stream>>>(L.cent, T, d, L.dcm);
   PGK_CHECK_LAUNCH("tile_dist_kernel");
+  dbg_stage("tile_dist_kernel", stream);
   // 4. pass 1: top-K over each query tile's nearest tiles -> U_Q
   const int vec4 = (d % 4 == 0);
   tile_nearest_kernel<<<g, 256, 0, stream>>>(L.dcm, L.size, T, K, L.lists, L.lens, L.total + 1);
   PGK_CHECK_LAUNCH("tile_nearest_kernel");
+  dbg_stage("tile_nearest_kernel", stream);
   rc = launch_pool_f32_lists(L.xs, NP, d, K, vec4, L.lists, L.lens, T, L.perm, L.keys1, stream);
   if (rc) return rc;
   const double gamma = (double)(d + 2) * 5.9604644775390625e-08 * 1.001 + 1e-12;
   tile_ubound_kernel<<<g, 256, 0, stream>>>(L.keys1, K, L.perm, T, L.U, 1.0 / (1.0 - gamma));
   PGK_CHECK_LAUNCH("tile_ubound_kernel");
+  dbg_stage("tile_ubound_kernel", stream);
   // 5. pass 2: every tile that can hold a pool member; S approximate survivors
   const double dc_margin = std::max(DC_MARGIN, 2.0 * gamma);
   tile_filter_kernel<<<g, 256, 0, stream>>>(L.dcm, L.rad, L.size, L.U, T, L.lists, L.lens,
                                             L.total, dc_margin);
   PGK_CHECK_LAUNCH("tile_filter_kernel");
+  dbg_stage("tile_filter_kernel", stream);
   rc = launch_pool_f32_lists(L.xs, NP, d, S, vec4, L.lists, L.lens, T, L.perm, keys, stream);
   if (rc) return rc;
   const char *se = getenv("PGK_TILES_STATS");

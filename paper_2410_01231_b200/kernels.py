@@ -188,3 +188,65 @@ def fallback_rows(ws: torch.Tensor) -> int:
     v = ctypes.c_int(0)
     check(_lib.lib().pgk_knn_fallback_rows(ptr(ws), ctypes.byref(v), _lib.stream_handle()))
     return int(v.value)
+
+
+# ---------------------------------------------------------------------------
+# beam search / phase C (search.cu)
+# ---------------------------------------------------------------------------
+
+def beam_search(X: torch.Tensor, adj: torch.Tensor, counts: torch.Tensor, queries, k: int,
+                L: int, ep: int = 0, exclude: int = -1, eps=None):
+    """Beam search per query row (search.cu); returns device tensors
+    (ids (nq, k), dists (nq, k), dist_counts (nq,), n_expanded (nq,))."""
+    dev = _lib.device()
+    n, d = X.shape
+    adj = _dev(adj, torch.int32)
+    counts = _dev(counts, torch.int32)
+    Q = _dev(queries, torch.float32).reshape(-1, d).contiguous()
+    nq = Q.shape[0]
+    eps_t = None if eps is None else _dev(eps, torch.int32)
+    ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    dc = torch.empty(nq, dtype=torch.int64, device=dev)
+    nexp = torch.empty(nq, dtype=torch.int64, device=dev)
+    sz = ctypes.c_size_t(0)
+    _lib.check(_lib.lib().pgk_search_workspace(n, nq, ctypes.byref(sz)))
+    ws = _lib.workspace(sz.value)
+    _lib.check(_lib.lib().pgk_beam_search(
+        _lib.ptr(X), n, d, _lib.ptr(adj), adj.shape[1], _lib.ptr(counts), _lib.ptr(Q), nq, k,
+        L, _lib.ptr(eps_t), int(ep), int(exclude), _lib.ptr(ids), _lib.ptr(dists),
+        _lib.ptr(dc), _lib.ptr(nexp), _lib.ptr(ws), ws.numel(), _lib.stream_handle()))
+    return ids, dists, dc, nexp
+
+
+def reach_workspace(n: int) -> torch.Tensor:
+    sz = ctypes.c_size_t(0)
+    _lib.check(_lib.lib().pgk_reach_workspace(n, ctypes.byref(sz)))
+    return _lib.workspace(sz.value)
+
+
+def mark_reachable(adj: torch.Tensor, counts: torch.Tensor, start: int, seen: torch.Tensor,
+                   ws: torch.Tensor) -> None:
+    """Extend the bitmap `seen` (int32 words viewed as uint32) from `start`."""
+    _lib.check(_lib.lib().pgk_mark_reachable(
+        _lib.ptr(adj), adj.shape[1], _lib.ptr(counts), adj.shape[0], int(start),
+        _lib.ptr(seen), _lib.ptr(ws), ws.numel(), _lib.stream_handle()))
+
+
+def first_unseen(seen: torch.Tensor, n: int, ws: torch.Tensor) -> int:
+    out = ctypes.c_int32(0)
+    _lib.check(_lib.lib().pgk_first_unseen(_lib.ptr(seen), n, ctypes.byref(out), _lib.ptr(ws),
+                                           _lib.stream_handle()))
+    return int(out.value)
+
+
+def centroid(X: torch.Tensor) -> torch.Tensor:
+    """float64 column means of the device dataset, as float32 (d,)."""
+    n, d = X.shape
+    sz = ctypes.c_size_t(0)
+    _lib.check(_lib.lib().pgk_centroid_workspace(n, d, ctypes.byref(sz)))
+    ws = _lib.workspace(sz.value)
+    out = torch.empty(d, dtype=torch.float32, device=X.device)
+    _lib.check(_lib.lib().pgk_centroid(_lib.ptr(X), n, d, _lib.ptr(out), _lib.ptr(ws),
+                                       ws.numel(), _lib.stream_handle()))
+    return out

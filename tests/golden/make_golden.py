@@ -37,7 +37,10 @@ from numba import njit, prange  # noqa: E402
 from pgann import _kernels  # noqa: E402  (reference)
 from pgann.core import Dataset  # noqa: E402
 from pgann.oracle import ground_truth_table  # noqa: E402
-from pgann.prune import PruneParams, add_reverse_and_prune, prune_all  # noqa: E402
+from pgann.prune import (PruneParams, add_reverse_and_prune, entry_point,  # noqa: E402
+                         finish_refine, prune_all)
+from pgann.graph import ProximityGraph, reachable_from  # noqa: E402
+from pgann.search import kann_search, search_batch  # noqa: E402
 
 from paper_2410_01231_b200 import synth  # noqa: E402
 
@@ -191,8 +194,75 @@ def save_cases() -> None:
     print("cases", names)
 
 
+# ---------------------------------------------------------------------------
+# Phase C and beam search: search_batch (search.py:81-94
+# -> _kernels.search_many / _search_core), entry_point (prune.py:154-162) and
+# finish_refine(connect=True) (prune.py:202-229, _connect :165-199).
+# ---------------------------------------------------------------------------
+
+def _phase_ab(data, K, R, strategy="rng", alpha=60.0):
+    ds = Dataset.from_array(data)
+    n = ds.n
+    truth = ground_truth_table(ds, None, k=K, exclude_self=True)
+    ids = truth.astype(np.int32).copy()
+    dists = _list_dists(ds.data, ids)
+    _resort(ids, dists)
+    off = (np.arange(n + 1, dtype=np.int64) * K)
+    cnt = np.full(n, K, np.int32)
+    params = PruneParams(M=R, alpha=alpha, strategy=strategy)
+    a = prune_all(ds, off, cnt, ids.ravel(), dists.ravel(), params)
+    return ds, params, a
+
+
+def save_search() -> None:
+    rec = {}
+    names = []
+    rng = np.random.default_rng(77)
+    # two far-apart blobs with a small pool: phase B leaves the graph split
+    blobs = np.vstack([rng.standard_normal((300, 8)), rng.standard_normal((300, 8)) + 40.0,
+                       rng.standard_normal((5, 8)) + 80.0]).astype(np.float32)
+    specs = [
+        ("cfg1_2k", synth.cfg1(2_000), 64, 24, "rng", 60.0),
+        ("cfg1_full", synth.cfg1(10_000), 64, 24, "rng", 60.0),
+        ("cfg1_a66", synth.cfg1(2_000), 64, 24, "alpha", 66.0),
+        ("blobs", blobs, 6, 4, "rng", 60.0),
+        ("blobs_a", blobs, 8, 3, "alpha", 120.0),
+    ]
+    for name, data, K, R, strategy, alpha in specs:
+        ds, params, a = _phase_ab(data, K, R, strategy, alpha)
+        g = finish_refine(ds, a[0], a[1], a[2], params, connect=True, ep=None, seed=0)
+        b_ids, b_d, b_c, _, _ = add_reverse_and_prune(ds, a[0], a[1], a[2], params)
+        interim = ProximityGraph(adj=b_ids, counts=b_c, M=params.M, ep=0)
+        L = max(params.M + 1, 32)
+        ep = entry_point(ds, interim, k=1, L=L, seed=0)
+        reach = reachable_from(interim, ep)
+        q = rng.standard_normal((64, data.shape[1])).astype(np.float32) * data.std() + \
+            data.mean(axis=0)
+        q = np.vstack([q, data[rng.choice(ds.n, 16, replace=False)]]).astype(np.float32)
+        for tag, kk, LL in (("k10L40", 10, 40), ("k1L16", 1, 16)):
+            s_ids, s_d, s_cnt = search_batch(ds, g, q, kk, LL)
+            rec[f"{name}_{tag}_ids"] = s_ids
+            rec[f"{name}_{tag}_dists"] = s_d
+            rec[f"{name}_{tag}_dcount"] = s_cnt
+        k_ids, k_d = kann_search(ds, g, q[0], 5, 24, ep=int(ds.n // 2))
+        rec.update({f"{name}_data": data, f"{name}_K": np.int64(K), f"{name}_R": np.int64(R),
+                    f"{name}_strategy": np.asarray(strategy), f"{name}_alpha": np.float64(alpha),
+                    f"{name}_b_ids": b_ids, f"{name}_b_counts": b_c, f"{name}_ep": np.int64(ep),
+                    f"{name}_reach": reach, f"{name}_c_adj": g.adj, f"{name}_c_counts": g.counts,
+                    f"{name}_c_ep": np.int64(g.ep), f"{name}_c_over": g.over_cap,
+                    f"{name}_queries": q, f"{name}_kann_ids": k_ids, f"{name}_kann_dists": k_d})
+        names.append(name)
+        print(name, "ep", ep, "unreached", int((~reach).sum()), "width", g.adj.shape[1],
+              "over", len(g.over_cap))
+    rec["names"] = np.array(names)
+    np.savez_compressed(HERE / "search.npz", **rec)
+
+
 def main() -> None:
     os.makedirs(HERE, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "search":
+        save_search()
+        return
     save_cases()
     save_config("cfg1_full", synth.cfg1(10_000), 64, 24,
                 dict(config=1, n=10_000, K=64, R=24), full=False)

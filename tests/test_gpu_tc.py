@@ -83,6 +83,10 @@ def _pools_subprocess(gen_code, K, env_extra):
     ("np.random.default_rng(3).integers(0, 256, (9000, 128)).astype(np.float32)", 64),
     ("np.repeat(np.random.default_rng(4).integers(0, 256, (300, 96)), 20, axis=0)"
      ".astype(np.float32)", 32),
+    # small K: pass-1 lists of a single tile (one-tile blocks stress the
+    # A-tile / block-index barrier of the dynamic schedule)
+    ("synth.cfg2(100000)", 16),
+    ("synth.cfg2(100000)", 32),
 ])
 def test_tile_pruned_pool_equals_full_scan(gen_code, K):
     """Exact tile pruning (default) vs the full tcgen05 scan (PGK_DISABLE_PRUNE=1):

@@ -91,3 +91,36 @@ def test_oracle_composition_matches_reference(name):
             assert sha(res[1]) == str(g[p + "dists__sha256"]), p
             assert sha(res[2]) == str(g[p + "counts__sha256"]), p
             assert res[3] == int(g[p + "de"]) and res[4] == int(g[p + "ae"]), p
+
+
+def _search_golden():
+    import numpy as np
+    from pathlib import Path
+    return np.load(Path(__file__).resolve().parent / "golden" / "search.npz", allow_pickle=False)
+
+
+def test_oracle_search_and_connect_match_reference():
+    """Beam search (search_batch, kann_search) and phase C (entry_point +
+    _connect via finish_refine) of the oracle restatement equal the reference's
+    outputs (tests/golden/search.npz, made by make_golden.py search)."""
+    import numpy as np
+    g = _search_golden()
+    for name in g["names"]:
+        data = g[f"{name}_data"]
+        M = int(g[f"{name}_R"])
+        adj, cnt, ep, over = oracle.finish_connect(data, g[f"{name}_b_ids"],
+                                                   g[f"{name}_b_counts"], M)
+        assert ep == int(g[f"{name}_c_ep"]), name
+        np.testing.assert_array_equal(adj, g[f"{name}_c_adj"], err_msg=name)
+        np.testing.assert_array_equal(cnt, g[f"{name}_c_counts"], err_msg=name)
+        np.testing.assert_array_equal(over, g[f"{name}_c_over"], err_msg=name)
+        q = g[f"{name}_queries"]
+        for tag, k, L in (("k10L40", 10, 40), ("k1L16", 1, 16)):
+            ids, d, dc = oracle.search_batch(data, adj, cnt, q, k, L, ep)
+            np.testing.assert_array_equal(ids, g[f"{name}_{tag}_ids"], err_msg=name)
+            np.testing.assert_array_equal(d, g[f"{name}_{tag}_dists"], err_msg=name)
+            np.testing.assert_array_equal(dc, g[f"{name}_{tag}_dcount"], err_msg=name)
+        ki, kd, _ = oracle.search_batch(data, adj, cnt, q[0], 5, 24, data.shape[0] // 2)
+        m = len(g[f"{name}_kann_ids"])
+        np.testing.assert_array_equal(ki[0, :m], g[f"{name}_kann_ids"])
+        np.testing.assert_array_equal(kd[0, :m], g[f"{name}_kann_dists"])
