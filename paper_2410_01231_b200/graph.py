@@ -29,6 +29,27 @@ class ProximityGraph:
     def mean_degree(self) -> float:
         return float(self.counts.mean())
 
+    def to_csr(self):
+        """(offsets int64 (n+1), neighbour ids int32) (graph.py:63-71)."""
+        counts = np.asarray(self.counts, np.int64)
+        offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        live = np.arange(self.adj.shape[1])[None, :] < counts[:, None]
+        return offsets, np.asarray(self.adj, np.int32)[live]
+
+    @classmethod
+    def from_csr(cls, offsets, nbrs, M: int, ep: int, over_cap=None) -> "ProximityGraph":
+        """Row-padded adjacency of width max(max degree, 1) (graph.py:73-85)."""
+        offsets = np.asarray(offsets, np.int64)
+        counts = np.diff(offsets).astype(np.int32)
+        n = counts.shape[0]
+        width = max(int(counts.max()) if n else 0, 1)
+        adj = np.full((n, width), EMPTY, dtype=np.int32)
+        rows = np.repeat(np.arange(n), counts)
+        cols = np.arange(int(offsets[-1])) - np.repeat(offsets[:-1], counts)
+        adj[rows, cols] = np.asarray(nbrs, np.int32)
+        over = np.empty(0, np.int32) if over_cap is None else np.asarray(over_cap, np.int32)
+        return cls(adj=adj, counts=counts, M=M, ep=ep, over_cap=over)
+
     def validate(self) -> None:
         """Structural checks (graph.py:41-61), vectorised; ValueError on violation."""
         n = self.n

@@ -258,10 +258,41 @@ def save_search() -> None:
     np.savez_compressed(HERE / "search.npz", **rec)
 
 
+def save_io() -> None:
+    """Files written by the reference's dataset_io (save_vecs / save_index,
+    dataset_io.py:67-84, 164-190) for byte-level format checks."""
+    from pgann import dataset_io
+    out = HERE / "io"
+    os.makedirs(out, exist_ok=True)
+    rng = np.random.default_rng(8)
+    f = rng.standard_normal((7, 5)).astype(np.float32)
+    i = rng.integers(-50, 50, size=(4, 9)).astype(np.int32)
+    b = rng.integers(0, 256, size=(6, 16)).astype(np.uint8)
+    dataset_io.save_vecs(out / "f.fvecs", f)
+    dataset_io.save_vecs(out / "i.ivecs", i)
+    dataset_io.save_vecs(out / "b.bvecs", b)
+    sg = np.load(HERE / "search.npz")
+    rec = dict(f=f, i=i, b=b)
+    for name in ("cfg1_2k", "blobs"):
+        g = ProximityGraph(adj=sg[f"{name}_c_adj"], counts=sg[f"{name}_c_counts"],
+                           M=int(sg[f"{name}_R"]), ep=int(sg[f"{name}_c_ep"]),
+                           over_cap=sg[f"{name}_c_over"])
+        dataset_io.save_index(out / f"{name}.pgix", g)
+        h = dataset_io.load_index(out / f"{name}.pgix")
+        rec[f"{name}_adj"], rec[f"{name}_counts"] = h.adj, h.counts
+        rec[f"{name}_ep"], rec[f"{name}_M"] = np.int64(h.ep), np.int64(h.M)
+        rec[f"{name}_over"] = h.over_cap
+    np.savez_compressed(out / "expect.npz", **rec)
+    print("io", sorted(p.name for p in out.iterdir()))
+
+
 def main() -> None:
     os.makedirs(HERE, exist_ok=True)
     if len(sys.argv) > 1 and sys.argv[1] == "search":
         save_search()
+        return
+    if len(sys.argv) > 1 and sys.argv[1] == "io":
+        save_io()
         return
     save_cases()
     save_config("cfg1_full", synth.cfg1(10_000), 64, 24,
