@@ -51,8 +51,18 @@ def test_graph_validate():
     assert off.tolist() == [0, 1, 2] and nbrs.tolist() == [1, 0]
 
 
-def test_phase_c_is_out_of_scope():
+def test_phase_c_has_no_cpu_fallback():
+    """Phase C (refine(connect=True)) and the beam search run on the GPU only:
+    without a CUDA device they raise instead of computing on the host."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check")
+    from paper_2410_01231_b200 import ProximityGraph, kann_search
     ds = Dataset.from_array(np.zeros((3, 2), np.float32))
-    with pytest.raises(NotImplementedError):
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
         refine(ds, np.zeros(4, np.int64), np.zeros(3, np.int32), np.zeros(0, np.int32),
                np.zeros(0, np.float32), PruneParams(M=2), connect=True)
+    g = ProximityGraph(adj=np.array([[1], [0], [0]], np.int32),
+                       counts=np.array([1, 1, 1], np.int32), M=2, ep=0)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        kann_search(ds, g, np.zeros(2, np.float32), 1, 4)
