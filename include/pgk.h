@@ -182,7 +182,9 @@ int pgk_knn_order(const void *ws, int64_t n, int64_t d, int64_t k, int mode,
  * over the adjacency adj (device int32[n*width], -1 padded) with `counts`;
  * writes the first k pool entries skipping `exclude` (out_ids / out_dists
  * [nq*k], -1 / +inf padded) and, when non-NULL, dist_counts / n_expanded
- * [nq] (int64).  ws: pgk_search_workspace(n, nq) bytes. */
+ * [nq] (int64).  exclude == -2 skips each query's own index (query row i is
+ * node i: _kernels.batch_self_search, _kernels.py:252-281).
+ * ws: pgk_search_workspace(n, nq) bytes. */
 int pgk_search_workspace(int64_t n, int64_t nq, size_t *ws_bytes_host);
 int pgk_beam_search(const float *data, int64_t n, int64_t d, const int32_t *adj,
                     int64_t width, const int32_t *counts, const float *queries, int64_t nq,
@@ -200,6 +202,30 @@ int pgk_mark_reachable(const int32_t *adj, int64_t width, const int32_t *counts,
                        int32_t start, uint32_t *seen, void *ws, size_t ws_bytes, void *stream);
 int pgk_first_unseen(const uint32_t *seen, int64_t n, int32_t *out_host, void *ws,
                      void *stream);
+
+/* ---- NN-Descent and FastNSG bookkeeping ---------------
+ * pgk_knng_init: knng.knng_init_random's row fill (_kernels.knng_init_rows,
+ * _kernels.py:764-798): draws (device int64[n*D], the host rng's draws) ->
+ * ids / dists (n*k0, sorted by (dist, id)); shortfall[u] > 0 marks rows
+ * with fewer than k0 distinct draws (the caller repairs them and re-sorts
+ * them with pgk_knng_sort_rows, which sorts the listed rows' given ids).
+ * pgk_knng_round: one NN-Descent round (knng.knng_descent_iterate,
+ * knng.py:64-101 with _kernels cap_reverse / _select_join / knng_join_round)
+ * from ids / dists / flags (uint8, n*k0) into the out arrays, with per-node
+ * accepted-update and distance counts.  ws: pgk_knng_round_workspace bytes.
+ * pgk_mark_fresh: fresh[u*cw+j] = cand[u*cw+j] absent from prev row u
+ * (_kernels.mark_fresh, _kernels.py:722-733). */
+int pgk_knng_init(const float *data, int64_t n, int64_t d, const int64_t *draws, int64_t D,
+                  int64_t k0, int32_t *ids, float *dists, int32_t *shortfall, void *stream);
+int pgk_knng_sort_rows(const float *data, int64_t d, const int32_t *rows, int64_t nrows,
+                       int64_t k0, int32_t *ids, float *dists, void *stream);
+int pgk_knng_round_workspace(int64_t n, int64_t k0, int64_t cap, size_t *ws_bytes_host);
+int pgk_knng_round(const float *data, int64_t n, int64_t d, int64_t k0, const int32_t *ids,
+                   const float *dists, const uint8_t *flags, int64_t cap_new, int64_t cap_old,
+                   int32_t *out_ids, float *out_dists, uint8_t *out_flags, int64_t *upd_counts,
+                   int64_t *dist_evals, void *ws, size_t ws_bytes, void *stream);
+int pgk_mark_fresh(const int32_t *cand, int64_t cw, const int32_t *ccnt, const int32_t *prev,
+                   int64_t pw, const int32_t *pcnt, int64_t n, uint8_t *fresh, void *stream);
 
 /* core.centroid (core.py:153-155): float64 column means, written as f32[d]
  * (deterministic two-level sum).  ws: pgk_centroid_workspace(n, d) bytes. */

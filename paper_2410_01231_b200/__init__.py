@@ -7,6 +7,7 @@ Drop-in for the reference pgann package's hot path (arXiv 2410.01231):
   * prune.refine / finish_refine, entry_point  -- phase C connectivity repair
   * search.kann_search / search_batch     -- beam search
   * io.load_vecs / save_vecs / load_index / save_index -- reference file formats
+  * knng / nsg / hnsw -- NN-Descent, NSG, FastNSG and FastHNSW builders
   * index.build_rng_index / RngBuilder   -- the whole path in one call
 All compute runs in libpgk.so (hand-written CUDA for sm_100a, C ABI in
 include/pgk.h); there is no CPU fallback.
@@ -18,7 +19,7 @@ from .pool import exact_knn, ground_truth_table, knn_pools, mean_recall, recall_
 from .prune import (PruneParams, RefineStats, add_reverse_and_prune, alpha_prune,
                     entry_point, finish_refine, prune_all, refine, rng_prune)
 from .search import kann_search, search_batch
-from . import io
+from . import hnsw, io, knng, nsg
 from .index import RngBuilder, build_rng_index
 
 __all__ = ["Dataset", "centroid", "EMPTY", "ProximityGraph", "exact_knn",

@@ -65,6 +65,12 @@ def lib():
         L.pgk_first_unseen.argtypes = [P, I64, P, P, P]
         L.pgk_centroid_workspace.argtypes = [I64, I64, P]
         L.pgk_centroid.argtypes = [P, I64, I64, P, P, SZ, P]
+        L.pgk_knng_init.argtypes = [P, I64, I64, P, I64, I64, P, P, P, P]
+        L.pgk_knng_sort_rows.argtypes = [P, I64, P, I64, I64, P, P, P]
+        L.pgk_knng_round_workspace.argtypes = [I64, I64, I64, P]
+        L.pgk_knng_round.argtypes = [P, I64, I64, I64, P, P, P, I64, I64, P, P, P, P, P, P, SZ,
+                                     P]
+        L.pgk_mark_fresh.argtypes = [P, I64, P, P, I64, P, I64, P, P]
         for f in ("pgk_device_check", "pgk_prune_batch", "pgk_prune_rows", "pgk_prune_rows_ex",
                   "pgk_prune_workspace",
                   "pgk_make_u8", "pgk_add_reverse_and_prune_ex", "pgk_reverse_workspace",
@@ -72,7 +78,8 @@ def lib():
                   "pgk_knn_pools", "pgk_knn_fallback_rows", "pgk_knn_work", "pgk_knn_order",
                   "pgk_search_workspace", "pgk_beam_search", "pgk_reach_workspace",
                   "pgk_mark_reachable", "pgk_first_unseen", "pgk_centroid_workspace",
-                  "pgk_centroid"):
+                  "pgk_centroid", "pgk_knng_init", "pgk_knng_sort_rows",
+                  "pgk_knng_round_workspace", "pgk_knng_round", "pgk_mark_fresh"):
             getattr(L, f).restype = I
         _lib = L
     return _lib
@@ -84,7 +91,8 @@ EXPORTS = ("pgk_version", "pgk_last_error", "pgk_device_check", "pgk_prune_batch
            "pgk_knn_workspace", "pgk_knn_pools", "pgk_knn_fallback_rows", "pgk_knn_work",
            "pgk_knn_order", "pgk_search_workspace", "pgk_beam_search", "pgk_reach_workspace",
            "pgk_mark_reachable", "pgk_first_unseen", "pgk_centroid_workspace", "pgk_centroid",
-           "pgk_launch_count")
+           "pgk_knng_init", "pgk_knng_sort_rows", "pgk_knng_round_workspace", "pgk_knng_round",
+           "pgk_mark_fresh", "pgk_launch_count")
 
 
 def check(rc: int) -> None:

@@ -37,6 +37,16 @@ int mark_reachable(const int32_t *, int64_t, const int32_t *, int64_t, int32_t, 
                    void *, size_t, cudaStream_t);
 int first_unseen(const uint32_t *, int64_t, int32_t *, void *, cudaStream_t);
 size_t centroid_workspace(int64_t n, int64_t d);
+int knng_init(const float *, int64_t, int64_t, const int64_t *, int64_t, int64_t, int32_t *,
+              float *, int32_t *, cudaStream_t);
+int knng_sort_rows(const float *, int64_t, const int32_t *, int64_t, int64_t, int32_t *, float *,
+                   cudaStream_t);
+size_t knng_round_workspace(int64_t n, int64_t k0, int64_t cap);
+int knng_round(const float *, int64_t, int64_t, int64_t, const int32_t *, const float *,
+               const uint8_t *, int64_t, int64_t, int32_t *, float *, uint8_t *, int64_t *,
+               int64_t *, void *, size_t, cudaStream_t);
+int mark_fresh(const int32_t *, int64_t, const int32_t *, const int32_t *, int64_t,
+               const int32_t *, int64_t, uint8_t *, cudaStream_t);
 int centroid(const float *, int64_t, int64_t, float *, void *, size_t, cudaStream_t);
 int launch_prune(const float *, const uint8_t *, const int32_t *, int64_t, int64_t,
                  const int32_t *, const int32_t *, void *, size_t, const int64_t *,
@@ -260,6 +270,42 @@ int pgk_first_unseen(const uint32_t *seen, int64_t n, int32_t *out_host, void *w
                      void *stream) {
   PGK_REQUIRE(seen && out_host && ws, "NULL argument");
   return first_unseen(seen, n, out_host, ws, (cudaStream_t)stream);
+}
+
+int pgk_knng_init(const float *data, int64_t n, int64_t d, const int64_t *draws, int64_t D,
+                  int64_t k0, int32_t *ids, float *dists, int32_t *shortfall, void *stream) {
+  PGK_REQUIRE(data && draws && ids && dists && shortfall, "NULL argument");
+  return knng_init(data, n, d, draws, D, k0, ids, dists, shortfall, (cudaStream_t)stream);
+}
+
+int pgk_knng_sort_rows(const float *data, int64_t d, const int32_t *rows, int64_t nrows,
+                       int64_t k0, int32_t *ids, float *dists, void *stream) {
+  PGK_REQUIRE(data && ids && dists && (nrows == 0 || rows), "NULL argument");
+  return knng_sort_rows(data, d, rows, nrows, k0, ids, dists, (cudaStream_t)stream);
+}
+
+int pgk_knng_round_workspace(int64_t n, int64_t k0, int64_t cap, size_t *ws_bytes_host) {
+  PGK_REQUIRE(ws_bytes_host, "NULL argument");
+  *ws_bytes_host = knng_round_workspace(n, k0, cap);
+  return PGK_OK;
+}
+
+int pgk_knng_round(const float *data, int64_t n, int64_t d, int64_t k0, const int32_t *ids,
+                   const float *dists, const uint8_t *flags, int64_t cap_new, int64_t cap_old,
+                   int32_t *out_ids, float *out_dists, uint8_t *out_flags, int64_t *upd_counts,
+                   int64_t *dist_evals, void *ws, size_t ws_bytes, void *stream) {
+  PGK_REQUIRE(data && ids && dists && flags && out_ids && out_dists && out_flags && upd_counts &&
+                  dist_evals && ws,
+              "NULL argument");
+  PGK_REQUIRE(cap_new >= 1 && cap_old >= 1, "caps must be >= 1");
+  return knng_round(data, n, d, k0, ids, dists, flags, cap_new, cap_old, out_ids, out_dists,
+                    out_flags, upd_counts, dist_evals, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int pgk_mark_fresh(const int32_t *cand, int64_t cw, const int32_t *ccnt, const int32_t *prev,
+                   int64_t pw, const int32_t *pcnt, int64_t n, uint8_t *fresh, void *stream) {
+  PGK_REQUIRE(cand && ccnt && prev && pcnt && fresh, "NULL argument");
+  return mark_fresh(cand, cw, ccnt, prev, pw, pcnt, n, fresh, (cudaStream_t)stream);
 }
 
 int pgk_centroid_workspace(int64_t n, int64_t d, size_t *ws_bytes_host) {

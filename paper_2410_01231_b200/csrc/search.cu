@@ -133,11 +133,13 @@ __global__ void __launch_bounds__(WARPS * 32)
         size = tot;
       }
     }
-    // results: the first k pool entries, skipping `exclude`
+    // results: the first k pool entries, skipping `exclude` (-2: the query's
+    // own index, batch_self_search, _kernels.py:252-281)
+    const int32_t ex = exclude == -2 ? (int32_t)qi : exclude;
     int m = 0;
     for (int b = 0; b < size && m < k; b += 32) {
       const int i = b + lane;
-      const bool take = i < size && kid(P.key[cur][i]) != exclude;
+      const bool take = i < size && kid(P.key[cur][i]) != ex;
       const unsigned bal = __ballot_sync(0xffffffffu, take);
       const int pos = m + __popc(bal & lanemask_lt());
       if (take && pos < k) {

@@ -250,3 +250,57 @@ def centroid(X: torch.Tensor) -> torch.Tensor:
     _lib.check(_lib.lib().pgk_centroid(_lib.ptr(X), n, d, _lib.ptr(out), _lib.ptr(ws),
                                        ws.numel(), _lib.stream_handle()))
     return out
+
+
+# ---------------------------------------------------------------------------
+# NN-Descent / FastNSG bookkeeping (nnd.cu)
+# ---------------------------------------------------------------------------
+
+def knng_init(X: torch.Tensor, draws: torch.Tensor, k0: int):
+    """Rows from the first k0 distinct draws, sorted by (dist, id); returns
+    (ids, dists, shortfall) device tensors."""
+    dev = X.device
+    n, d = X.shape
+    draws = _dev(draws, torch.int64).contiguous()
+    ids = torch.empty((n, k0), dtype=torch.int32, device=dev)
+    dists = torch.empty((n, k0), dtype=torch.float32, device=dev)
+    short = torch.empty(n, dtype=torch.int32, device=dev)
+    _lib.check(_lib.lib().pgk_knng_init(_lib.ptr(X), n, d, _lib.ptr(draws), draws.shape[1], k0,
+                                        _lib.ptr(ids), _lib.ptr(dists), _lib.ptr(short),
+                                        _lib.stream_handle()))
+    return ids, dists, short
+
+
+def knng_sort_rows(X: torch.Tensor, rows, ids: torch.Tensor, dists: torch.Tensor) -> None:
+    """Distances + (dist, id) sort of the listed rows' current ids (in place)."""
+    rows = _dev(rows, torch.int32).contiguous()
+    _lib.check(_lib.lib().pgk_knng_sort_rows(_lib.ptr(X), X.shape[1], _lib.ptr(rows),
+                                             rows.numel(), ids.shape[1], _lib.ptr(ids),
+                                             _lib.ptr(dists), _lib.stream_handle()))
+
+
+def knng_round(X: torch.Tensor, ids, dists, flags, cap_new: int, cap_old: int):
+    """One NN-Descent round -> (ids, dists, flags, upd (n,), evals (n,))."""
+    n, d = X.shape
+    k0 = ids.shape[1]
+    o_ids, o_d, o_f = torch.empty_like(ids), torch.empty_like(dists), torch.empty_like(flags)
+    upd = torch.empty(n, dtype=torch.int64, device=X.device)
+    ev = torch.empty(n, dtype=torch.int64, device=X.device)
+    sz = ctypes.c_size_t(0)
+    _lib.check(_lib.lib().pgk_knng_round_workspace(n, k0, cap_new + cap_old, ctypes.byref(sz)))
+    ws = _lib.workspace(sz.value)
+    _lib.check(_lib.lib().pgk_knng_round(
+        _lib.ptr(X), n, d, k0, _lib.ptr(ids), _lib.ptr(dists), _lib.ptr(flags), cap_new, cap_old,
+        _lib.ptr(o_ids), _lib.ptr(o_d), _lib.ptr(o_f), _lib.ptr(upd), _lib.ptr(ev),
+        _lib.ptr(ws), ws.numel(), _lib.stream_handle()))
+    return o_ids, o_d, o_f, upd, ev
+
+
+def mark_fresh(cand: torch.Tensor, ccnt: torch.Tensor, prev: torch.Tensor,
+               pcnt: torch.Tensor) -> torch.Tensor:
+    n, cw = cand.shape
+    fresh = torch.empty((n, cw), dtype=torch.uint8, device=cand.device)
+    _lib.check(_lib.lib().pgk_mark_fresh(_lib.ptr(cand), cw, _lib.ptr(ccnt), _lib.ptr(prev),
+                                         prev.shape[1], _lib.ptr(pcnt), n, _lib.ptr(fresh),
+                                         _lib.stream_handle()))
+    return fresh

@@ -286,8 +286,70 @@ def save_io() -> None:
     print("io", sorted(p.name for p in out.iterdir()))
 
 
+def save_f3() -> None:
+    """NN-Descent, FastNSG, NSG and FastHNSW outputs:
+    knng.py:40-125, nsg.py:319-430, hnsw.py:141-192, search.py:97-130."""
+    from pgann import hnsw as R_hnsw
+    from pgann import knng as R_knng
+    from pgann import nsg as R_nsg
+    from pgann.search import layered_search
+    rec = {}
+    names = []
+    for name, data in (("cfg1", synth.cfg1(2_500)), ("cfg2", synth.cfg2(3_000))):
+        ds = Dataset.from_array(data)
+        rec[f"{name}_data"] = data
+        # NN-Descent: init + every round's rows / flags / update counts
+        st = R_knng.knng_init_random(ds, 16, seed=5)
+        rec[f"{name}_knng0_ids"], rec[f"{name}_knng0_dists"] = st.ids, st.dists
+        for r in range(1, 4):
+            st = R_knng.knng_descent_iterate(ds, st, rho=1.0 if r != 2 else 0.5)
+            rec[f"{name}_knng{r}_ids"], rec[f"{name}_knng{r}_dists"] = st.ids, st.dists
+            rec[f"{name}_knng{r}_flags"] = st.flags
+            rec[f"{name}_knng{r}_upd"] = np.int64(st.last_updates)
+        kb = R_knng.build_knng(ds, 12, iters=10, seed=7)
+        rec[f"{name}_bknng_ids"], rec[f"{name}_bknng_iters"] = kb.ids, np.int64(kb.iterations)
+        g = R_nsg.build_nsg_original(ds, k0=12, k=24, L=32, M=12, seed=3)
+        rec[f"{name}_nsg_adj"], rec[f"{name}_nsg_counts"], rec[f"{name}_nsg_ep"] = \
+            g.adj, g.counts, np.int64(g.ep)
+        fst = R_nsg.FastNsgStats()
+        g = R_nsg.build_fastnsg(ds, k0=12, k=24, L=32, M=12, alpha=66.0, max_iters=2, seed=4,
+                                stats=fst)
+        rec[f"{name}_fnsg_adj"], rec[f"{name}_fnsg_counts"], rec[f"{name}_fnsg_ep"] = \
+            g.adj, g.counts, np.int64(g.ep)
+        rec[f"{name}_fnsg_over"] = g.over_cap
+        fs = fst.final_state
+        rec[f"{name}_fnsg_state_ids"], rec[f"{name}_fnsg_state_counts"] = fs.ids, fs.counts
+        rec[f"{name}_fnsg_state_fresh"] = fs.fresh
+        rec[f"{name}_fnsg_search_dists"] = np.array([s.search_dists for s in fst.per_iteration])
+        lg = R_hnsw.build_fasthnsw(ds, k0=12, ef=40, M=12, seed=6)
+        rec[f"{name}_hnsw_levels"], rec[f"{name}_hnsw_ep"] = lg.levels, np.int64(lg.ep)
+        rec[f"{name}_hnsw_nlayers"] = np.int64(len(lg.layers))
+        for i, layer in enumerate(lg.layers):
+            rec[f"{name}_hnsw_L{i}_members"] = layer.members
+            rec[f"{name}_hnsw_L{i}_adj"] = layer.graph.adj
+            rec[f"{name}_hnsw_L{i}_counts"] = layer.graph.counts
+            rec[f"{name}_hnsw_L{i}_ep"] = np.int64(layer.graph.ep)
+        rng = np.random.default_rng(31)
+        q = data[rng.choice(ds.n, 40, replace=False)] + rng.normal(0, 0.5, (40, data.shape[1]))
+        q = q.astype(np.float32)
+        res = [layered_search(ds, lg, qq, 10, 40) for qq in q]
+        rec[f"{name}_lq"] = q
+        rec[f"{name}_lq_ids"] = np.array([np.pad(r[0], (0, 10 - len(r[0])), constant_values=-1)
+                                          for r in res])
+        rec[f"{name}_lq_dists"] = np.array([np.pad(r[1], (0, 10 - len(r[1])),
+                                                   constant_values=np.inf) for r in res])
+        names.append(name)
+        print(name, "knng iters", kb.iterations, "hnsw layers", len(lg.layers),
+              "upd", [int(rec[f"{name}_knng{r}_upd"]) for r in range(1, 4)])
+    rec["names"] = np.array(names)
+    np.savez_compressed(HERE / "f3.npz", **rec)
+
+
 def main() -> None:
     os.makedirs(HERE, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "f3":
+        save_f3()
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "search":
         save_search()
         return

@@ -1,0 +1,80 @@
+"""GPU parity for SURVEY 8(f) f3 -- NN-Descent, the classic and the
+self-iterative (FastNSG) NSG builders and the layer-global FastHNSW -- against
+the reference's own outputs (tests/golden/f3.npz, make_golden.py f3), on a
+float (cfg1) and an exact-integer (cfg2) prefix.  Exact: rows, flags, the
+per-round accepted-update counts (they drive the early stop), entry points,
+adjacency, layer assignments and layered-search results."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2410_01231_b200 import Dataset
+from paper_2410_01231_b200 import hnsw, knng, nsg
+
+pytestmark = pytest.mark.gpu
+
+G = np.load(Path(__file__).resolve().parent / "golden" / "f3.npz", allow_pickle=False)
+NAMES = [str(x) for x in G["names"]]
+
+
+def _live_equal(adj, counts, ref_adj, ref_counts, tag):
+    np.testing.assert_array_equal(counts, ref_counts, err_msg=tag)
+    live = np.arange(adj.shape[1])[None, :] < counts[:, None]
+    assert adj.shape == ref_adj.shape, tag
+    np.testing.assert_array_equal(np.where(live, adj, -1), np.where(live, ref_adj, -1),
+                                  err_msg=tag)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_nn_descent_rounds_match_reference(name):
+    ds = Dataset.from_array(G[f"{name}_data"])
+    st = knng.knng_init_random(ds, 16, seed=5)
+    np.testing.assert_array_equal(st.ids, G[f"{name}_knng0_ids"])
+    np.testing.assert_array_equal(st.dists, G[f"{name}_knng0_dists"])
+    for r in range(1, 4):
+        st = knng.knng_descent_iterate(ds, st, rho=1.0 if r != 2 else 0.5)
+        np.testing.assert_array_equal(st.ids, G[f"{name}_knng{r}_ids"], err_msg=f"round {r}")
+        np.testing.assert_array_equal(st.dists, G[f"{name}_knng{r}_dists"])
+        np.testing.assert_array_equal(st.flags, G[f"{name}_knng{r}_flags"])
+        assert st.last_updates == int(G[f"{name}_knng{r}_upd"]), r
+    kb = knng.build_knng(ds, 12, iters=10, seed=7)
+    assert kb.iterations == int(G[f"{name}_bknng_iters"])
+    np.testing.assert_array_equal(kb.ids, G[f"{name}_bknng_ids"])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_nsg_builders_match_reference(name):
+    ds = Dataset.from_array(G[f"{name}_data"])
+    g = nsg.build_nsg_original(ds, k0=12, k=24, L=32, M=12, seed=3)
+    assert g.ep == int(G[f"{name}_nsg_ep"])
+    _live_equal(g.adj, g.counts, G[f"{name}_nsg_adj"], G[f"{name}_nsg_counts"], "nsg")
+    st = nsg.FastNsgStats()
+    g = nsg.build_fastnsg(ds, k0=12, k=24, L=32, M=12, alpha=66.0, max_iters=2, seed=4,
+                          stats=st)
+    assert g.ep == int(G[f"{name}_fnsg_ep"])
+    _live_equal(g.adj, g.counts, G[f"{name}_fnsg_adj"], G[f"{name}_fnsg_counts"], "fastnsg")
+    np.testing.assert_array_equal(g.over_cap, G[f"{name}_fnsg_over"])
+    fs = st.final_state
+    np.testing.assert_array_equal(fs.counts, G[f"{name}_fnsg_state_counts"])
+    np.testing.assert_array_equal(fs.ids, G[f"{name}_fnsg_state_ids"])
+    np.testing.assert_array_equal(fs.fresh, G[f"{name}_fnsg_state_fresh"])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_fasthnsw_and_layered_search_match_reference(name):
+    ds = Dataset.from_array(G[f"{name}_data"])
+    lg = hnsw.build_fasthnsw(ds, k0=12, ef=40, M=12, seed=6)
+    np.testing.assert_array_equal(lg.levels, G[f"{name}_hnsw_levels"])
+    assert lg.ep == int(G[f"{name}_hnsw_ep"])
+    assert len(lg.layers) == int(G[f"{name}_hnsw_nlayers"])
+    for i, layer in enumerate(lg.layers):
+        np.testing.assert_array_equal(layer.members, G[f"{name}_hnsw_L{i}_members"])
+        assert layer.graph.ep == int(G[f"{name}_hnsw_L{i}_ep"])
+        _live_equal(layer.graph.adj, layer.graph.counts, G[f"{name}_hnsw_L{i}_adj"],
+                    G[f"{name}_hnsw_L{i}_counts"], f"layer {i}")
+    for j, q in enumerate(G[f"{name}_lq"]):
+        ids, dists = hnsw.layered_search(ds, lg, q, 10, 40)
+        m = len(ids)
+        np.testing.assert_array_equal(ids, G[f"{name}_lq_ids"][j, :m])
+        np.testing.assert_array_equal(dists, G[f"{name}_lq_dists"][j, :m])
