@@ -192,6 +192,16 @@ int pgk_beam_search(const float *data, int64_t n, int64_t d, const int32_t *adj,
                     int32_t *out_ids, float *out_dists, int64_t *dist_counts,
                     int64_t *n_expanded, void *ws, size_t ws_bytes, void *stream);
 
+/* pgk_beam_search plus the expansion order of every query: expansions
+ * (device int32[nq*exp_cap]) receives the first exp_cap expanded nodes in
+ * order (n_expanded tells how many there were). */
+int pgk_beam_search_ex(const float *data, int64_t n, int64_t d, const int32_t *adj,
+                       int64_t width, const int32_t *counts, const float *queries, int64_t nq,
+                       int64_t k, int64_t L, const int32_t *eps, int32_t ep, int32_t exclude,
+                       int32_t *out_ids, float *out_dists, int64_t *dist_counts,
+                       int64_t *n_expanded, int32_t *expansions, int64_t exp_cap, void *ws,
+                       size_t ws_bytes, void *stream);
+
 /* Reachability bitmap seen (device uint32[(n+31)/32], bit v = node v):
  * pgk_mark_reachable adds every node reachable from `start` through nodes not
  * yet marked (start included; one-CTA BFS enqueued on the stream).
@@ -202,6 +212,12 @@ int pgk_mark_reachable(const int32_t *adj, int64_t width, const int32_t *counts,
                        int32_t start, uint32_t *seen, void *ws, size_t ws_bytes, void *stream);
 int pgk_first_unseen(const uint32_t *seen, int64_t n, int32_t *out_host, void *ws,
                      void *stream);
+/* Phase C's component heads, in order (prune.py:174-199: the first unreached
+ * id, all it reaches, the next first unreached id, ...) into heads (device
+ * int32[n]); marks them in seen; *n_heads_host = count (blocking). */
+int pgk_component_heads(const int32_t *adj, int64_t width, const int32_t *counts, int64_t n,
+                        uint32_t *seen, int32_t *heads, int32_t *n_heads_host, void *ws,
+                        size_t ws_bytes, void *stream);
 
 /* ---- NN-Descent and FastNSG bookkeeping ---------------
  * pgk_knng_init: knng.knng_init_random's row fill (_kernels.knng_init_rows,

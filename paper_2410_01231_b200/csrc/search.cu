@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(WARPS * 32)
                        int32_t exclude, int32_t *__restrict__ out_ids,
                        float *__restrict__ out_dists, int64_t *__restrict__ dist_counts,
                        int64_t *__restrict__ n_expanded, int32_t *__restrict__ stamps,
-                       int nslots) {
+                       int nslots, int32_t *__restrict__ exp_out, int exp_cap) {
   __shared__ WarpPool pools[WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.x * WARPS + warp;
@@ -89,7 +89,11 @@ __global__ void __launch_bounds__(WARPS * 32)
       }
       if (idx < 0) break;
       const int32_t u = kid(P.key[cur][idx]);
-      if (lane == 0) P.flag[cur][idx] = 1;
+      if (lane == 0) {
+        P.flag[cur][idx] = 1;
+        // expansion order record (phase-C speculation checks it)
+        if (exp_out && nexp < exp_cap) exp_out[qi * exp_cap + nexp] = u;
+      }
       ++nexp;
       __syncwarp();
       const int cu = counts[u];
@@ -162,6 +166,91 @@ __global__ void __launch_bounds__(WARPS * 32)
 }
 
 // ---- reachability -------------------------------------------------------
+// BFS body shared by the single-start and the component-heads kernels:
+// marks everything reachable from the nodes in cur[0..n_cur) through unseen
+// nodes (cur already marked).
+__device__ void bfs_from(const int32_t *__restrict__ adj, int width,
+                         const int32_t *__restrict__ counts, uint32_t *__restrict__ seen,
+                         int32_t *cur, int32_t *nxt, int *n_cur, int *n_next) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x / 32;
+  while (*n_cur > 0) {
+    if (threadIdx.x == 0) *n_next = 0;
+    __syncthreads();
+    const int nc = *n_cur;
+    for (int f = warp; f < nc; f += nwarps) {
+      const int32_t u = cur[f];
+      const int cu = counts[u];
+      for (int j = lane; j < cu; j += 32) {
+        const int32_t v = adj[(int64_t)u * width + j];
+        const uint32_t bit = 1u << (v & 31);
+        if (seen[v >> 5] & bit) continue;
+        const uint32_t old = atomicOr(seen + (v >> 5), bit);
+        if (!(old & bit)) nxt[atomicAdd(n_next, 1)] = v;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *n_cur = *n_next;
+    int32_t *t = cur;
+    cur = nxt;
+    nxt = t;
+    __syncthreads();
+  }
+}
+
+// Phase C's component heads in the reference's order (prune.py:174-199): the
+// first unreached id, everything it reaches, the next first unreached id...
+// The sequence does not depend on the repair edges (they leave nodes that are
+// already reached), so one CTA computes it up front.
+__global__ void __launch_bounds__(1024)
+    component_heads_kernel(const int32_t *__restrict__ adj, int width,
+                           const int32_t *__restrict__ counts, int64_t n,
+                           uint32_t *__restrict__ seen, int32_t *__restrict__ qa,
+                           int32_t *__restrict__ qb, int32_t *__restrict__ heads,
+                           int32_t *__restrict__ n_heads) {
+  __shared__ int n_cur, n_next, s_found;
+  __shared__ int64_t s_word;
+  const int64_t nwords = (n + 31) >> 5;
+  int64_t w0 = 0;
+  int m = 0;
+  for (;;) {
+    // first word at or after w0 with an unseen bit (blockwide scan)
+    if (threadIdx.x == 0) {
+      s_word = nwords;
+      s_found = 0;
+    }
+    __syncthreads();
+    for (int64_t base = w0; base < nwords && !s_found; base += blockDim.x) {
+      const int64_t w = base + threadIdx.x;
+      if (w < nwords) {
+        uint32_t miss = ~seen[w];
+        const int64_t hi = n - w * 32;
+        if (hi < 32) miss &= (1u << hi) - 1u;
+        if (miss) atomicMin((unsigned long long *)&s_word, (unsigned long long)w);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && s_word < nwords) s_found = 1;
+      __syncthreads();
+    }
+    if (!s_found) break;
+    const int64_t w = s_word;
+    w0 = w;
+    if (threadIdx.x == 0) {
+      uint32_t miss = ~seen[w];
+      const int64_t hi = n - w * 32;
+      if (hi < 32) miss &= (1u << hi) - 1u;
+      const int32_t v = (int32_t)(w * 32 + __ffs(miss) - 1);
+      heads[m] = v;
+      atomicOr(seen + (v >> 5), 1u << (v & 31));
+      qa[0] = v;
+      n_cur = 1;
+    }
+    ++m;
+    __syncthreads();
+    bfs_from(adj, width, counts, seen, qa, qb, &n_cur, &n_next);
+  }
+  if (threadIdx.x == 0) *n_heads = m;
+}
+
 // One CTA runs the whole BFS (device-side level loop over a global-memory
 // queue): no host round trip per level, so deep / chain-like components
 // (phase C on near-duplicate data) cost no more than their size.
@@ -249,7 +338,7 @@ int beam_search(const float *X, int64_t n, int64_t d, const int32_t *adj, int64_
                 const int32_t *counts, const float *Q, int64_t nq, int64_t k, int64_t L,
                 const int32_t *eps, int32_t ep, int32_t exclude, int32_t *out_ids,
                 float *out_dists, int64_t *dist_counts, int64_t *n_expanded, void *ws,
-                size_t ws_bytes, cudaStream_t stream) {
+                size_t ws_bytes, cudaStream_t stream, int32_t *exp_out, int64_t exp_cap) {
   PGK_REQUIRE(n >= 1 && d >= 1 && width >= 1, "empty graph");
   PGK_REQUIRE(k >= 1, "k must be >= 1");
   PGK_REQUIRE(k <= L, "k must not exceed the pool width L");
@@ -263,7 +352,7 @@ int beam_search(const float *X, int64_t n, int64_t d, const int32_t *adj, int64_
   const unsigned grid = (unsigned)((slots + srch::WARPS - 1) / srch::WARPS);
   srch::beam_search_kernel<<<grid, srch::WARPS * 32, 0, stream>>>(
       X, n, (int)d, adj, (int)width, counts, Q, nq, (int)k, (int)L, eps, ep, exclude, out_ids,
-      out_dists, dist_counts, n_expanded, stamps, (int)slots);
+      out_dists, dist_counts, n_expanded, stamps, (int)slots, exp_out, (int)exp_cap);
   PGK_CHECK_LAUNCH("beam_search_kernel");
   return PGK_OK;
 }
@@ -284,6 +373,23 @@ int mark_reachable(const int32_t *adj, int64_t width, const int32_t *counts, int
   srch::bfs_block_kernel<<<1, srch::BFS_THREADS, 0, stream>>>(adj, (int)width, counts, start,
                                                               seen, fa, fb);
   PGK_CHECK_LAUNCH("bfs_block_kernel");
+  return PGK_OK;
+}
+
+// All component heads of the unreached remainder, in order (marks them and
+// what they reach in `seen`); *n_heads_host receives the count (blocking).
+int component_heads(const int32_t *adj, int64_t width, const int32_t *counts, int64_t n,
+                    uint32_t *seen, int32_t *heads, int32_t *n_heads_host, void *ws,
+                    size_t ws_bytes, cudaStream_t stream) {
+  PGK_REQUIRE(ws_bytes >= reach_workspace(n), "reach workspace too small");
+  Carve c(ws, ws_bytes);
+  int32_t *cnt = c.take<int32_t>(64);
+  int32_t *fa = c.take<int32_t>(n), *fb = c.take<int32_t>(n);
+  srch::component_heads_kernel<<<1, 1024, 0, stream>>>(adj, (int)width, counts, n, seen, fa, fb,
+                                                       heads, cnt);
+  PGK_CHECK_LAUNCH("component_heads_kernel");
+  PGK_CUDA(cudaMemcpyAsync(n_heads_host, cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+  PGK_CUDA(cudaStreamSynchronize(stream));
   return PGK_OK;
 }
 

@@ -195,9 +195,11 @@ def fallback_rows(ws: torch.Tensor) -> int:
 # ---------------------------------------------------------------------------
 
 def beam_search(X: torch.Tensor, adj: torch.Tensor, counts: torch.Tensor, queries, k: int,
-                L: int, ep: int = 0, exclude: int = -1, eps=None):
+                L: int, ep: int = 0, exclude: int = -1, eps=None, exp_cap: int = 0):
     """Beam search per query row (search.cu); returns device tensors
-    (ids (nq, k), dists (nq, k), dist_counts (nq,), n_expanded (nq,))."""
+    (ids (nq, k), dists (nq, k), dist_counts (nq,), n_expanded (nq,)) and,
+    with exp_cap > 0, the first exp_cap expanded nodes of each query (nq,
+    exp_cap) as a fifth element."""
     dev = _lib.device()
     n, d = X.shape
     adj = _dev(adj, torch.int32)
@@ -209,14 +211,30 @@ def beam_search(X: torch.Tensor, adj: torch.Tensor, counts: torch.Tensor, querie
     dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
     dc = torch.empty(nq, dtype=torch.int64, device=dev)
     nexp = torch.empty(nq, dtype=torch.int64, device=dev)
+    exps = torch.empty((nq, exp_cap), dtype=torch.int32, device=dev) if exp_cap > 0 else None
     sz = ctypes.c_size_t(0)
     _lib.check(_lib.lib().pgk_search_workspace(n, nq, ctypes.byref(sz)))
     ws = _lib.workspace(sz.value)
-    _lib.check(_lib.lib().pgk_beam_search(
+    _lib.check(_lib.lib().pgk_beam_search_ex(
         _lib.ptr(X), n, d, _lib.ptr(adj), adj.shape[1], _lib.ptr(counts), _lib.ptr(Q), nq, k,
         L, _lib.ptr(eps_t), int(ep), int(exclude), _lib.ptr(ids), _lib.ptr(dists),
-        _lib.ptr(dc), _lib.ptr(nexp), _lib.ptr(ws), ws.numel(), _lib.stream_handle()))
+        _lib.ptr(dc), _lib.ptr(nexp), _lib.ptr(exps), int(exp_cap), _lib.ptr(ws), ws.numel(),
+        _lib.stream_handle()))
+    if exp_cap > 0:
+        return ids, dists, dc, nexp, exps
     return ids, dists, dc, nexp
+
+
+def component_heads(adj: torch.Tensor, counts: torch.Tensor, seen: torch.Tensor,
+                    ws: torch.Tensor) -> torch.Tensor:
+    """Phase C's component heads in order (device int32), marking `seen`."""
+    n = adj.shape[0]
+    heads = torch.empty(n, dtype=torch.int32, device=adj.device)
+    m = ctypes.c_int32(0)
+    _lib.check(_lib.lib().pgk_component_heads(
+        _lib.ptr(adj), adj.shape[1], _lib.ptr(counts), n, _lib.ptr(seen), _lib.ptr(heads),
+        ctypes.byref(m), _lib.ptr(ws), ws.numel(), _lib.stream_handle()))
+    return heads[: m.value]
 
 
 def reach_workspace(n: int) -> torch.Tensor:

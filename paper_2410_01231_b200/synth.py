@@ -68,6 +68,26 @@ def cfg2(n: int = 1_000_000, n_full: int = 1_000_000, seed: int = 1) -> np.ndarr
     return out
 
 
+def cfg5(n: int = 200_000, n_queries: int = 10_000, seed: int = 4):
+    """Config 5 (FastHNSW build): the config-2 recipe with seed 4 for the base
+    rows; the queries continue the same generator after the base draws (same
+    256 centres: a ~ U{0..255}, x = clip(rint(c[a] + 20 z), 0, 255)).
+    Returns (base (n, 128), queries (n_queries, 128)) float32."""
+    d, k = 128, 256
+    rng = np.random.default_rng(seed)
+    c = 255.0 * rng.random((k, d))
+    a = rng.integers(0, k, size=n)
+    base = np.empty((n, d), np.float32)
+
+    def put(lo, hi, z):
+        base[lo:hi] = np.clip(np.rint(c[a[lo:hi]] + 20.0 * z), 0.0, 255.0).astype(np.float32)
+
+    _normal_rows(rng, n, d, put)
+    qa = rng.integers(0, k, size=n_queries)
+    q = np.clip(np.rint(c[qa] + 20.0 * rng.standard_normal((n_queries, d))), 0.0, 255.0)
+    return base, q.astype(np.float32)
+
+
 def cfg3(n: int = 1_000_000, n_full: int = 1_000_000, seed: int = 2) -> np.ndarray:
     """Config 3 (Gist1M stand-in): gen_synthetic(n_full, 960, "clustered", seed=2,
     n_clusters=100, cluster_std=0.1), first ``n`` rows."""
