@@ -194,13 +194,19 @@ int pgk_beam_search(const float *data, int64_t n, int64_t d, const int32_t *adj,
 
 /* pgk_beam_search plus the expansion order of every query: expansions
  * (device int32[nq*exp_cap]) receives the first exp_cap expanded nodes in
- * order (n_expanded tells how many there were). */
+ * order (n_expanded tells how many there were) and exp_worst (device
+ * uint64[nq*exp_cap], optional) the pool's admission bound -- its last
+ * packed (dist, id) key, or ~0 while not full -- right after each expansion.
+ * pgk_pair_dists: out[i] = squared_l2(data[a[i]], data[b[i]]) (fp32,
+ * _kernels.py:17-24). */
 int pgk_beam_search_ex(const float *data, int64_t n, int64_t d, const int32_t *adj,
                        int64_t width, const int32_t *counts, const float *queries, int64_t nq,
                        int64_t k, int64_t L, const int32_t *eps, int32_t ep, int32_t exclude,
                        int32_t *out_ids, float *out_dists, int64_t *dist_counts,
-                       int64_t *n_expanded, int32_t *expansions, int64_t exp_cap, void *ws,
-                       size_t ws_bytes, void *stream);
+                       int64_t *n_expanded, int32_t *expansions, uint64_t *exp_worst,
+                       int64_t exp_cap, void *ws, size_t ws_bytes, void *stream);
+int pgk_pair_dists(const float *data, int64_t d, const int32_t *a, const int32_t *b, int64_t m,
+                   float *out, void *stream);
 
 /* Reachability bitmap seen (device uint32[(n+31)/32], bit v = node v):
  * pgk_mark_reachable adds every node reachable from `start` through nodes not

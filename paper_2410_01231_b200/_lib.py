@@ -61,7 +61,8 @@ def lib():
         L.pgk_beam_search.argtypes = [P, I64, I64, P, I64, P, P, I64, I64, I64, P, I32, I32,
                                       P, P, P, P, P, SZ, P]
         L.pgk_beam_search_ex.argtypes = [P, I64, I64, P, I64, P, P, I64, I64, I64, P, I32, I32,
-                                         P, P, P, P, P, I64, P, SZ, P]
+                                         P, P, P, P, P, P, I64, P, SZ, P]
+        L.pgk_pair_dists.argtypes = [P, I64, P, P, I64, P, P]
         L.pgk_component_heads.argtypes = [P, I64, P, I64, P, P, P, P, SZ, P]
         L.pgk_reach_workspace.argtypes = [I64, P]
         L.pgk_mark_reachable.argtypes = [P, I64, P, I64, I32, P, P, SZ, P]
@@ -80,7 +81,7 @@ def lib():
                   "pgk_add_reverse_and_prune", "pgk_detect_u8", "pgk_knn_workspace",
                   "pgk_knn_pools", "pgk_knn_fallback_rows", "pgk_knn_work", "pgk_knn_order",
                   "pgk_search_workspace", "pgk_beam_search", "pgk_reach_workspace",
-                  "pgk_beam_search_ex", "pgk_component_heads",
+                  "pgk_beam_search_ex", "pgk_component_heads", "pgk_pair_dists",
                   "pgk_mark_reachable", "pgk_first_unseen", "pgk_centroid_workspace",
                   "pgk_centroid", "pgk_knng_init", "pgk_knng_sort_rows",
                   "pgk_knng_round_workspace", "pgk_knng_round", "pgk_mark_fresh"):
@@ -95,7 +96,7 @@ EXPORTS = ("pgk_version", "pgk_last_error", "pgk_device_check", "pgk_prune_batch
            "pgk_knn_workspace", "pgk_knn_pools", "pgk_knn_fallback_rows", "pgk_knn_work",
            "pgk_knn_order", "pgk_search_workspace", "pgk_beam_search", "pgk_reach_workspace",
            "pgk_mark_reachable", "pgk_first_unseen", "pgk_centroid_workspace", "pgk_centroid",
-           "pgk_beam_search_ex", "pgk_component_heads", "pgk_knng_init", "pgk_knng_sort_rows", "pgk_knng_round_workspace", "pgk_knng_round",
+           "pgk_beam_search_ex", "pgk_component_heads", "pgk_pair_dists", "pgk_knng_init", "pgk_knng_sort_rows", "pgk_knng_round_workspace", "pgk_knng_round",
            "pgk_mark_fresh", "pgk_launch_count")
 
 

@@ -32,7 +32,9 @@ size_t search_workspace(int64_t n, int64_t nq);
 int beam_search(const float *, int64_t, int64_t, const int32_t *, int64_t, const int32_t *,
                 const float *, int64_t, int64_t, int64_t, const int32_t *, int32_t, int32_t,
                 int32_t *, float *, int64_t *, int64_t *, void *, size_t, cudaStream_t,
-                int32_t *, int64_t);
+                int32_t *, int64_t, uint64_t *);
+int pair_dists(const float *, int64_t, const int32_t *, const int32_t *, int64_t, float *,
+               cudaStream_t);
 int component_heads(const int32_t *, int64_t, const int32_t *, int64_t, uint32_t *, int32_t *,
                     int32_t *, void *, size_t, cudaStream_t);
 size_t reach_workspace(int64_t n);
@@ -254,21 +256,27 @@ int pgk_beam_search(const float *data, int64_t n, int64_t d, const int32_t *adj,
   PGK_REQUIRE(nq == 0 || queries, "NULL queries");
   return beam_search(data, n, d, adj, width, counts, queries, nq, k, L, eps, ep, exclude,
                      out_ids, out_dists, dist_counts, n_expanded, ws, ws_bytes,
-                     (cudaStream_t)stream, nullptr, 0);
+                     (cudaStream_t)stream, nullptr, 0, nullptr);
 }
 
 int pgk_beam_search_ex(const float *data, int64_t n, int64_t d, const int32_t *adj,
                        int64_t width, const int32_t *counts, const float *queries, int64_t nq,
                        int64_t k, int64_t L, const int32_t *eps, int32_t ep, int32_t exclude,
                        int32_t *out_ids, float *out_dists, int64_t *dist_counts,
-                       int64_t *n_expanded, int32_t *expansions, int64_t exp_cap, void *ws,
-                       size_t ws_bytes, void *stream) {
+                       int64_t *n_expanded, int32_t *expansions, uint64_t *exp_worst,
+                       int64_t exp_cap, void *ws, size_t ws_bytes, void *stream) {
   PGK_REQUIRE(data && adj && counts && out_ids && out_dists && ws, "NULL argument");
   PGK_REQUIRE(nq == 0 || queries, "NULL queries");
-  PGK_REQUIRE(!expansions || exp_cap >= 1, "exp_cap must be >= 1");
+  PGK_REQUIRE((!expansions && !exp_worst) || exp_cap >= 1, "exp_cap must be >= 1");
   return beam_search(data, n, d, adj, width, counts, queries, nq, k, L, eps, ep, exclude,
                      out_ids, out_dists, dist_counts, n_expanded, ws, ws_bytes,
-                     (cudaStream_t)stream, expansions, exp_cap);
+                     (cudaStream_t)stream, expansions, exp_cap, exp_worst);
+}
+
+int pgk_pair_dists(const float *data, int64_t d, const int32_t *a, const int32_t *b, int64_t m,
+                   float *out, void *stream) {
+  PGK_REQUIRE(data && out && (m == 0 || (a && b)), "NULL argument");
+  return pair_dists(data, d, a, b, m, out, (cudaStream_t)stream);
 }
 
 int pgk_component_heads(const int32_t *adj, int64_t width, const int32_t *counts, int64_t n,

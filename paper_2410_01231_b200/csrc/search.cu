@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(WARPS * 32)
                        int32_t exclude, int32_t *__restrict__ out_ids,
                        float *__restrict__ out_dists, int64_t *__restrict__ dist_counts,
                        int64_t *__restrict__ n_expanded, int32_t *__restrict__ stamps,
-                       int nslots, int32_t *__restrict__ exp_out, int exp_cap) {
+                       int nslots, int32_t *__restrict__ exp_out, int exp_cap,
+                       uint64_t *__restrict__ exp_worst) {
   __shared__ WarpPool pools[WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.x * WARPS + warp;
@@ -136,6 +137,11 @@ __global__ void __launch_bounds__(WARPS * 32)
         cur ^= 1;
         size = tot;
       }
+      // the pool's admission bound once u's neighbours are in (phase-C
+      // speculation: an extra neighbour offered last is rejected iff its
+      // key is >= this; KEY_MAX while the pool is not full)
+      if (exp_worst && lane == 0 && nexp - 1 < exp_cap)
+        exp_worst[qi * exp_cap + nexp - 1] = size == L ? P.key[cur][size - 1] : KEY_MAX;
     }
     // results: the first k pool entries, skipping `exclude` (-2: the query's
     // own index, batch_self_search, _kernels.py:252-281)
@@ -338,7 +344,8 @@ int beam_search(const float *X, int64_t n, int64_t d, const int32_t *adj, int64_
                 const int32_t *counts, const float *Q, int64_t nq, int64_t k, int64_t L,
                 const int32_t *eps, int32_t ep, int32_t exclude, int32_t *out_ids,
                 float *out_dists, int64_t *dist_counts, int64_t *n_expanded, void *ws,
-                size_t ws_bytes, cudaStream_t stream, int32_t *exp_out, int64_t exp_cap) {
+                size_t ws_bytes, cudaStream_t stream, int32_t *exp_out, int64_t exp_cap,
+                uint64_t *exp_worst) {
   PGK_REQUIRE(n >= 1 && d >= 1 && width >= 1, "empty graph");
   PGK_REQUIRE(k >= 1, "k must be >= 1");
   PGK_REQUIRE(k <= L, "k must not exceed the pool width L");
@@ -352,7 +359,8 @@ int beam_search(const float *X, int64_t n, int64_t d, const int32_t *adj, int64_
   const unsigned grid = (unsigned)((slots + srch::WARPS - 1) / srch::WARPS);
   srch::beam_search_kernel<<<grid, srch::WARPS * 32, 0, stream>>>(
       X, n, (int)d, adj, (int)width, counts, Q, nq, (int)k, (int)L, eps, ep, exclude, out_ids,
-      out_dists, dist_counts, n_expanded, stamps, (int)slots, exp_out, (int)exp_cap);
+      out_dists, dist_counts, n_expanded, stamps, (int)slots, exp_out, (int)exp_cap,
+      exp_worst);
   PGK_CHECK_LAUNCH("beam_search_kernel");
   return PGK_OK;
 }
@@ -405,6 +413,24 @@ int first_unseen(const uint32_t *seen, int64_t n, int32_t *out_host, void *ws,
   PGK_CUDA(cudaMemcpyAsync(&h, dv, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
   PGK_CUDA(cudaStreamSynchronize(stream));
   *out_host = h == big ? -1 : h;
+  return PGK_OK;
+}
+
+// squared_l2(data[a[i]], data[b[i]]) (the reference's sequential fp32)
+__global__ void pair_dists_kernel(const float *__restrict__ X, int d, const int32_t *__restrict__ a,
+                                  const int32_t *__restrict__ b, int64_t m,
+                                  float *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = sql2_seq<false>(X + (int64_t)a[i] * d, X + (int64_t)b[i] * d, d);
+}
+
+int pair_dists(const float *X, int64_t d, const int32_t *a, const int32_t *b, int64_t m,
+               float *out, cudaStream_t stream) {
+  if (m == 0) return PGK_OK;
+  pair_dists_kernel<<<(unsigned)std::min<int64_t>((m + 255) / 256, (int64_t)num_sms() * 8), 256,
+                      0, stream>>>(X, (int)d, a, b, m, out);
+  PGK_CHECK_LAUNCH("pair_dists_kernel");
   return PGK_OK;
 }
 

@@ -212,17 +212,28 @@ def beam_search(X: torch.Tensor, adj: torch.Tensor, counts: torch.Tensor, querie
     dc = torch.empty(nq, dtype=torch.int64, device=dev)
     nexp = torch.empty(nq, dtype=torch.int64, device=dev)
     exps = torch.empty((nq, exp_cap), dtype=torch.int32, device=dev) if exp_cap > 0 else None
+    worst = torch.empty((nq, exp_cap), dtype=torch.int64, device=dev) if exp_cap > 0 else None
     sz = ctypes.c_size_t(0)
     _lib.check(_lib.lib().pgk_search_workspace(n, nq, ctypes.byref(sz)))
     ws = _lib.workspace(sz.value)
     _lib.check(_lib.lib().pgk_beam_search_ex(
         _lib.ptr(X), n, d, _lib.ptr(adj), adj.shape[1], _lib.ptr(counts), _lib.ptr(Q), nq, k,
         L, _lib.ptr(eps_t), int(ep), int(exclude), _lib.ptr(ids), _lib.ptr(dists),
-        _lib.ptr(dc), _lib.ptr(nexp), _lib.ptr(exps), int(exp_cap), _lib.ptr(ws), ws.numel(),
-        _lib.stream_handle()))
+        _lib.ptr(dc), _lib.ptr(nexp), _lib.ptr(exps), _lib.ptr(worst), int(exp_cap),
+        _lib.ptr(ws), ws.numel(), _lib.stream_handle()))
     if exp_cap > 0:
-        return ids, dists, dc, nexp, exps
+        return ids, dists, dc, nexp, exps, worst
     return ids, dists, dc, nexp
+
+
+def pair_dists(X: torch.Tensor, a, b) -> torch.Tensor:
+    """squared_l2(X[a[i]], X[b[i]]) per pair (fp32, reference order)."""
+    a = _dev(a, torch.int32).contiguous()
+    b = _dev(b, torch.int32).contiguous()
+    out = torch.empty(a.numel(), dtype=torch.float32, device=X.device)
+    _lib.check(_lib.lib().pgk_pair_dists(_lib.ptr(X), X.shape[1], _lib.ptr(a), _lib.ptr(b),
+                                         a.numel(), _lib.ptr(out), _lib.stream_handle()))
+    return out
 
 
 def component_heads(adj: torch.Tensor, counts: torch.Tensor, seen: torch.Tensor,
