@@ -247,10 +247,10 @@ def run_ours(args):
             order = builder.order()
             e[2].record(stream)  # selection kernel(s) alone between e[2] and e[3]
             a = kernels.prune_batch(X, builder.cand_off, builder.cand_counts, pids, pd,
-                                    p.strategy_code, p.cos_alpha, p.M, p.M, out=builder.a_out,
+                                    p.strategy_code, p.kernel_param, p.M, p.M, out=builder.a_out,
                                     u8=u8, order=order, ws=builder.prune_ws)
             e[3].record(stream)
-            kernels.add_reverse_and_prune(X, a[0], a[1], a[2], p.strategy_code, p.cos_alpha,
+            kernels.add_reverse_and_prune(X, a[0], a[1], a[2], p.strategy_code, p.kernel_param,
                                           p.M, p.M, ws=builder.rev_ws, out=builder.b_out, u8=u8,
                                           order=order)
             e[4].record(stream)

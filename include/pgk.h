@@ -8,6 +8,8 @@
  *   data      float32 (n, d) row-major, row i == id i        (core.py:18-47)
  *   offsets   int64, counts int32, ids int32 (-1 = EMPTY), dists float32
  *   strategy  0 = "rng", 1 = "alpha"; cos_alpha float64      (prune.py:24-56)
+ *             2 = "slack" (extension, no reference equivalent: s^2 * dwv < dv,
+ *             with s^2 >= 1 passed in the cos_alpha argument)
  *
  * Conventions of this ABI:
  *   - every pointer argument is a DEVICE pointer unless the name says _host;

@@ -32,7 +32,13 @@ SRC = HERE / "pgk_oracle.c"
 LIB = HERE / "liboracle.so"
 
 EMPTY = -1
-_STRATEGIES = ("rng", "alpha")
+_STRATEGIES = ("rng", "alpha", "slack")
+
+
+def _param(strategy: str, alpha: float) -> float:
+    """The rule's float64 kernel parameter: cos(alpha) (prune.py:54-56), or
+    s^2 for the "slack" extension (no reference equivalent)."""
+    return float(alpha) * float(alpha) if strategy == "slack" else cos_alpha(alpha)
 
 
 def build(force: bool = False) -> Path:
@@ -115,7 +121,7 @@ def prune_all(data, cand_off, cand_counts, cand_ids, cand_dists, M: int,
     de = np.zeros(n, np.int64)
     ae = np.zeros(n, np.int64)
     lib().orc_prune_batch(_p(data), n, d, _p(cand_off), _p(cand_counts), _p(cand_ids),
-                          _p(cand_dists), _STRATEGIES.index(strategy), cos_alpha(alpha),
+                          _p(cand_dists), _STRATEGIES.index(strategy), _param(strategy, alpha),
                           M, width, _p(out_ids), _p(out_dists), _p(out_counts),
                           _p(de), _p(ae))
     return out_ids, out_dists, out_counts, int(de.sum()), int(ae.sum())

@@ -83,7 +83,8 @@ static int check_prune_args(const float *data, int64_t n, int64_t d, int strateg
                             int64_t M, int64_t width) {
   PGK_REQUIRE(n >= 0 && d >= 1, "bad shape n=%lld d=%lld", (long long)n, (long long)d);
   PGK_REQUIRE(n == 0 || data, "data is NULL");
-  PGK_REQUIRE(strategy == 0 || strategy == 1, "strategy must be 0 (rng) or 1 (alpha)");
+  PGK_REQUIRE(strategy == 0 || strategy == 1 || strategy == 2,
+              "strategy must be 0 (rng), 1 (alpha) or 2 (slack)");
   PGK_REQUIRE(M >= 1, "M must be >= 1");
   PGK_REQUIRE(width >= M, "row width %lld < M %lld", (long long)width, (long long)M);
   PGK_REQUIRE(n < 0x7fffffffLL && width < 0x7fffffffLL, "n / width exceed int32 ids");

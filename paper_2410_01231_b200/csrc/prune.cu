@@ -169,6 +169,8 @@ __device__ __forceinline__ int test_round(
       } else if (dwv < dv) {
         if (strategy == 0) {
           dom = true;
+        } else if (strategy == 2) {  // "slack" extension: s^2 * dwv < dv
+          dom = cos_alpha * (double)dwv < (double)dv;
         } else {
           double c = cos_angle_from_sq(duw, dwv, dv);
           s_ae[j] += 1;
@@ -352,6 +354,8 @@ __device__ __forceinline__ int test_round_u8(const uint4 (&wr)[8], int nw, float
       } else if (dwv < dv) {
         if (strategy == 0) {
           dom = true;
+        } else if (strategy == 2) {  // "slack" extension: s^2 * dwv < dv
+          dom = cos_alpha * (double)dwv < (double)dv;
         } else {
           const double c = cos_angle_from_sq(duw, dwv, dv);
           s_ae[j] += 1;

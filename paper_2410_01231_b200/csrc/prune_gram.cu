@@ -298,7 +298,18 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       // dwv = |c_i|^2 + |c_t|^2 - 2 G[t][i] an exact integer >= 0:
       //   dwv < dv  <=>  dwv <= ceil(dv) - 1;  dwv == 0  <=>  dwv <= 0
       // so with x = |c_i|^2 - 2 G[t][i]:  x <= max(ceil(dv) - 1, 0) - |c_t|^2
-      const int dle = dv >= 2.0e9f ? 0x7fffffff : max((int)ceilf(dv) - 1, 0);
+      // rng: dwv < dv; "slack" extension: s^2 * dwv < dv (s^2 = cos_alpha >= 1):
+      // the largest integer x with p * x < dv, in the same float64 arithmetic
+      int dle;
+      if (dv >= 2.0e9f) {
+        dle = 0x7fffffff;
+      } else {
+        const double p = strategy == 2 ? cos_alpha : 1.0;
+        int64_t x = (int64_t)floor((double)dv / p);
+        while (x >= 0 && !(p * (double)x < (double)dv)) --x;
+        while (p * (double)(x + 1) < (double)dv) ++x;
+        dle = (int)(x > 0 ? x : 0);
+      }
       const int thr = dle == 0x7fffffff ? 0x7fffffff : dle - nv;
       uint32_t pm[4] = {0, 0, 0, 0}, am[4] = {0, 0, 0, 0};
       GWAIT(4, mbar_wait(&s.tfull[grp], tphase));
@@ -547,9 +558,9 @@ int launch_prune_gram(const uint8_t *xu8, const int32_t *norms, int64_t n,
   }
   const unsigned grid =
       (unsigned)std::min<int64_t>(n, (int64_t)gram::CTAS_PER_SM * num_sms());
-  if (strategy == 0)
+  if (strategy == 0 || strategy == 2)  // slack: the rng masks with another threshold
     gram::prune_gram_kernel<0><<<grid, gram::THREADS, smem, stream>>>(
-        xu8, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, 0,
+        xu8, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
         cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals,
         long_rows, long_count);
   else

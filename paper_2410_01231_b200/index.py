@@ -81,9 +81,9 @@ class RngBuilder:
         u8 = self.u8_rows(X)
         order = self.order()
         a = kernels.prune_batch(X, self.cand_off, self.cand_counts, ids, dists,
-                                p.strategy_code, p.cos_alpha, p.M, p.M, out=self.a_out, u8=u8,
+                                p.strategy_code, p.kernel_param, p.M, p.M, out=self.a_out, u8=u8,
                                 order=order, ws=self.prune_ws)
-        b = kernels.add_reverse_and_prune(X, a[0], a[1], a[2], p.strategy_code, p.cos_alpha,
+        b = kernels.add_reverse_and_prune(X, a[0], a[1], a[2], p.strategy_code, p.kernel_param,
                                           p.M, p.M, ws=self.rev_ws, out=self.b_out, u8=u8,
                                           order=order)
         de = torch.stack([a[3].sum(), b[3].sum()])

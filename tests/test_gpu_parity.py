@@ -421,3 +421,31 @@ def test_full_scale_float_pools_on_seeded_rows(cfg, rows):
     o_ids, o_d = oracle.knn_pools(data, c["K"], rows=sel)
     np.testing.assert_array_equal(ids[sel], o_ids)
     np.testing.assert_array_equal(dists[sel], o_d)
+
+
+@pytest.mark.parametrize("gen,n,K,R", [(synth.cfg1, 3000, 64, 24), (synth.cfg2, 6000, 64, 24),
+                                       (synth.cfg4, 3000, 128, 32)])
+def test_slack_strategy_against_oracle(gen, n, K, R):
+    """The "slack" extension (BASELINE config 4's alpha=1.2; no reference
+    equivalent, parity pinned to the oracle restatement): phases A and B,
+    counters included, on float, exact-integer and unit-norm data; slack 1.0
+    reproduces "rng" exactly."""
+    data = gen(n)
+    ds = Dataset.from_array(data)
+    ids, dists = knn_pools(ds, K)
+    off = np.arange(ds.n + 1, dtype=np.int64) * K
+    cnt = np.full(ds.n, K, np.int32)
+    for s in (1.0, 1.2):
+        p = PruneParams(M=R, alpha=s, strategy="slack")
+        a = prune_all(ds, off, cnt, ids.ravel(), dists.ravel(), p)
+        b = add_reverse_and_prune(ds, a[0], a[1], a[2], p)
+        oa = oracle.prune_all(data, off, cnt, ids.ravel(), dists.ravel(), R, "slack", s)
+        ob = oracle.add_reverse_and_prune(data, oa[0], oa[1], oa[2], R, "slack", s)
+        for res, ref in ((a, oa), (b, ob)):
+            np.testing.assert_array_equal(res[0], ref[0])
+            np.testing.assert_array_equal(res[2], ref[2])
+            assert res[3] == ref[3] and res[4] == 0
+        if s == 1.0:
+            r = prune_all(ds, off, cnt, ids.ravel(), dists.ravel(), PruneParams(M=R))
+            np.testing.assert_array_equal(a[0], r[0])
+            assert a[3] == r[3]

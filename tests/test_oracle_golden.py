@@ -39,6 +39,28 @@ def test_oracle_prune_matches_reference_cases(golden_cases, name, strategy):
 
 
 @pytest.mark.parametrize("name", CASES)
+def test_oracle_slack_one_is_the_reference_rng_rule(golden_cases, name):
+    """The "slack" extension (no reference equivalent) anchors to the
+    reference at s = 1: it must give the reference's own "rng" outputs on
+    every edge case (ties, duplicates, self entries, empty rows); s > 1 keeps
+    a superset-leaning degree (more edges survive)."""
+    g = golden_cases
+    data = g[f"{name}_data"]
+    M = int(g[f"{name}_M"])
+    a = oracle.prune_all(data, g[f"{name}_off"], g[f"{name}_counts"], g[f"{name}_ids"],
+                         g[f"{name}_dists"], M, "slack", 1.0)
+    b = oracle.add_reverse_and_prune(data, a[0], a[1], a[2], M, "slack", 1.0)
+    for ph, res in (("a", a), ("b", b)):
+        p = f"{name}_rng_{ph}_"
+        np.testing.assert_array_equal(res[0], g[p + "ids"])
+        np.testing.assert_array_equal(res[2], g[p + "counts"])
+        assert res[3] == int(g[p + "de"])
+    a2 = oracle.prune_all(data, g[f"{name}_off"], g[f"{name}_counts"], g[f"{name}_ids"],
+                          g[f"{name}_dists"], M, "slack", 1.5)
+    assert a2[2].sum() >= a[2].sum()
+
+
+@pytest.mark.parametrize("name", CASES)
 def test_oracle_pool_matches_reference_cases(golden_cases, name):
     g = golden_cases
     data = g[f"{name}_data"]
