@@ -222,7 +222,18 @@ __device__ __forceinline__ int row_tp(uint64_t tau, int nx, int K) {
 enum { ST_WAIT, ST_MAIN, ST_SLOW, ST_COMPACT, ST_FINAL, ST_NSLOW, ST_NCOMPACT, ST_NAPPEND,
        ST_COUNT };
 
-template <bool STATS>
+// DENSE (pass-1 bound mode): no threshold, no survivor lists -- every row
+// stores the exact distance of every column it meets, densely (u32, at most
+// DENSE_TILES tiles per row in the row's CAP x 8-byte slot), for
+// tc_kth_dense_kernel's exact K-th selection.
+constexpr int DENSE_TILES = 2 * CAP / BN;
+
+__device__ __forceinline__ uint32_t dense_val(int dist, int64_t col, int64_t n, int32_t pid,
+                                              bool self) {
+  return (col < n && pid >= 0 && !self) ? (uint32_t)dist : 0xffffffffu;
+}
+
+template <bool STATS, bool DENSE>
 // 112 registers keeps CTAS_PER_SM = 3 resident (3 x 6 warps x 112 x 32 <= 64K)
 __global__ void __maxnreg__(112)
     tc_pool_u8_kernel(const __grid_constant__ CUtensorMap tmX,
@@ -432,6 +443,27 @@ __global__ void __maxnreg__(112)
           tmem_wait_ld();
           const int64_t cb = col0 + c * 32;
           const int4 *nyp = reinterpret_cast<const int4 *>(s.ny[tpar] + c * 32);
+          if (DENSE) {
+            if (row_ok && t < DENSE_TILES) {
+              const int4 *pp = reinterpret_cast<const int4 *>(s.pid[tpar] + c * 32);
+              uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<uint32_t *>(bufs + row * CAP) +
+                                                     t * BN + c * 32);
+              const bool es = exclude_self != 0;
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                const int4 w = nyp[v];
+                const int4 pd = perm ? pp[v] : make_int4(0, 0, 0, 0);
+                const int64_t cj = cb + 4 * v;
+                uint4 o;
+                o.x = dense_val(w.x - 2 * (int)r[4 * v] + nx, cj, n, pd.x, es && row == cj);
+                o.y = dense_val(w.y - 2 * (int)r[4 * v + 1] + nx, cj + 1, n, pd.y, es && row == cj + 1);
+                o.z = dense_val(w.z - 2 * (int)r[4 * v + 2] + nx, cj + 2, n, pd.z, es && row == cj + 2);
+                o.w = dense_val(w.w - 2 * (int)r[4 * v + 3] + nx, cj + 3, n, pd.w, es && row == cj + 3);
+                dst[v] = o;
+              }
+            }
+            continue;
+          }
           // s_j = |x_j|^2 - 2 q.x_j ; pass iff s_j <= tp
           uint32_t mask = 0;
 #pragma unroll
@@ -548,6 +580,7 @@ __global__ void __maxnreg__(112)
       // block done: record each row's buffer fill and threshold; selection
       // and sorting run in the massively parallel finalize kernel
       PGK_TICK(ST_MAIN);
+      if (DENSE) cnt = min(len, DENSE_TILES) * BN;
       if (row < nq) {
         row_cnt[row] = row_ok ? (cnt | (guessed ? GUESSED : 0)) : -1;
         row_tau[row] = tau;
@@ -890,6 +923,66 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, 4)
   }
 }
 
+// K-th smallest of a row's dense pass-1 distances (0xffffffff = invalid), to
+// within 1/1024 of the row's value range from above: a warp-wide binary
+// search over register-resident values (per step one compare per value and
+// one REDUX count), keeping count(v <= hi) >= K.  Returns hi.
+template <int VPL>
+__device__ __noinline__ uint32_t kth_dense(const uint32_t *__restrict__ buf, int cnt, int K,
+                                           int lane) {
+  uint32_t v[VPL];
+  int nv = 0;
+  uint32_t vmin = 0xffffffffu, vmax = 0;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int idx = i * 32 + lane;
+    v[i] = idx < cnt ? buf[idx] : 0xffffffffu;
+    if (v[i] != 0xffffffffu) {
+      ++nv;
+      vmin = min(vmin, v[i]);
+      vmax = max(vmax, v[i]);
+    }
+  }
+  if ((int)__reduce_add_sync(0xffffffffu, (unsigned)nv) < K) return 0xffffffffu;
+  uint32_t lo = __reduce_min_sync(0xffffffffu, vmin);
+  uint32_t hi = __reduce_max_sync(0xffffffffu, vmax);
+  const uint32_t tol = (hi - lo) >> 10;
+  while (hi - lo > tol) {
+    const uint32_t mid = lo + ((hi - lo) >> 1);
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) c += v[i] <= mid;
+    if ((int)__reduce_add_sync(0xffffffffu, (unsigned)c) >= K) hi = mid;
+    else lo = mid + 1;
+  }
+  return hi;
+}
+
+// Pass-1 bound of every row from its dense distances (warp per row): an
+// upper bound of the K-th smallest valid distance, itself an upper bound of
+// the true K-th neighbour distance (the row met real points only), in the library's key
+// format at out_keys[orig_row * K + K - 1].
+__global__ void __launch_bounds__(FIN_WARPS * 32)
+    tc_kth_dense_kernel(const uint64_t *__restrict__ bufs, const int32_t *__restrict__ row_cnt,
+                        int64_t nrows, int K, const int32_t *__restrict__ perm,
+                        uint64_t *__restrict__ out_keys) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t r = (int64_t)blockIdx.x * FIN_WARPS + warp; r < nrows;
+       r += (int64_t)gridDim.x * FIN_WARPS) {
+    const int cnt = row_cnt[r];
+    if (cnt < 0) continue;  // padding row
+    const uint32_t *b = reinterpret_cast<const uint32_t *>(bufs + r * CAP);
+    uint32_t kth;
+    if (cnt <= 512) kth = kth_dense<16>(b, cnt, K, lane);
+    else if (cnt <= 768) kth = kth_dense<24>(b, cnt, K, lane);
+    else if (cnt <= 1024) kth = kth_dense<32>(b, cnt, K, lane);
+    else kth = kth_dense<64>(b, cnt, K, lane);
+    const int64_t orow = perm ? (int64_t)perm[r] : r;
+    if (lane == 0)
+      out_keys[orow * K + K - 1] = kth == 0xffffffffu ? KEY_MAX : pack_key((float)kth, 0x7fffffff);
+  }
+}
+
 // float (integer-valued, d <= 128) -> u8 rows padded to 128 bytes
 __global__ void to_u8_kernel(const float *__restrict__ X, int64_t n, int d,
                              uint8_t *__restrict__ out) {
@@ -929,6 +1022,21 @@ static bool make_map(CUtensorMap *tm, const uint8_t *base, int64_t rows) {
 }
 
 }  // namespace tc
+
+// (128-byte rows x rows) u8 tensor map with a (128 x box_rows) box, SW128;
+// box_rows = 1 is the TMA gather4 form (prune_gram.cu)
+bool make_u8_row_map(CUtensorMap *tm, const uint8_t *base, int64_t rows, int box_rows) {
+  auto fn = tc::encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)tc::KB, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)tc::KB};
+  cuuint32_t box[2] = {(cuuint32_t)tc::KB, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void *)base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
 
 size_t tc_pool_workspace(int64_t n, int64_t nq, bool self) {
   const int sms = num_sms();
@@ -1005,21 +1113,38 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   const size_t smem = sizeof(tc::Smem) + 1024;
   static bool attr = false;
   if (!attr) {
-    PGK_CUDA(cudaFuncSetAttribute(tc::tc_pool_u8_kernel<false>,
+    PGK_CUDA(cudaFuncSetAttribute(tc::tc_pool_u8_kernel<false, false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    PGK_CUDA(cudaFuncSetAttribute(tc::tc_pool_u8_kernel<true>,
+    PGK_CUDA(cudaFuncSetAttribute(tc::tc_pool_u8_kernel<true, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PGK_CUDA(cudaFuncSetAttribute(tc::tc_pool_u8_kernel<false, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   const int nblocks = (int)((nq + tc::BM - 1) / tc::BM);
   const unsigned grid = (unsigned)std::min<int64_t>(nblocks, (int64_t)tc::CTAS_PER_SM * sms);
   PGK_CUDA(cudaMemsetAsync(sched, 0, sizeof(int32_t), stream));
+  // pass-1 bounds over tile lists: dense distances + exact K-th selection
+  const bool dense = kth_only && K > 1 && tlist;
   const char *se = getenv("PGK_TC_STATS");
+  if (dense) {
+    tc::tc_pool_u8_kernel<false, true><<<grid, tc::THREADS, smem, stream>>>(
+        tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
+        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask);
+    PGK_CHECK_LAUNCH("tc_pool_u8_kernel<dense>");
+    const unsigned fgrid =
+        (unsigned)std::min<int64_t>((nq + tc::FIN_WARPS - 1) / tc::FIN_WARPS, (int64_t)sms * 8);
+    tc::tc_kth_dense_kernel<<<fgrid, tc::FIN_WARPS * 32, 0, stream>>>(bufs, row_cnt, nq, K, perm,
+                                                                      keys);
+    PGK_CHECK_LAUNCH("tc_kth_dense_kernel");
+    *handled = true;
+    return PGK_OK;
+  }
   if (se && se[0] == '1') {
     unsigned long long *dstats = nullptr;
     PGK_CUDA(cudaMalloc(&dstats, sizeof(unsigned long long) * tc::ST_COUNT));
     PGK_CUDA(cudaMemsetAsync(dstats, 0, sizeof(unsigned long long) * tc::ST_COUNT, stream));
-    tc::tc_pool_u8_kernel<true><<<grid, tc::THREADS, smem, stream>>>(
+    tc::tc_pool_u8_kernel<true, false><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, dstats, tlist, tlen,
         tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel<stats>");
@@ -1034,7 +1159,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
             h[0] / warps, h[1] / warps, h[2] / warps, h[3] / warps, h[4] / warps, h[5] / warps,
             h[6] / warps, (double)h[7] / (double)nq);
   } else {
-    tc::tc_pool_u8_kernel<false><<<grid, tc::THREADS, smem, stream>>>(
+    tc::tc_pool_u8_kernel<false, false><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
         tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel");

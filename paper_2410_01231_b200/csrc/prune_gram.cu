@@ -19,11 +19,13 @@
 // kept neighbour is discarded).  Rows with more than 128 candidates (hubs in
 // phase B) are listed and left to prune_u8_kernel.
 //
-// CTA: warp 0 gathers (cp.async, zero-filled tails), warp 1 allocates TMEM and
+// CTA: warp 0 gathers (TMA gather4 rows, cp.async metadata), warp 1 allocates TMEM and
 // issues the MMA, warps 2-5 build the predicate masks (each its lower-
 // triangle chunks of the Gram rows), warp 6 runs the greedy scan and the
 // counters on double-buffered masks, overlapped with the next point's masks.
 // 4 CTAs per SM share the tensor core (128 TMEM columns each).
+#include <cuda.h>
+
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -100,7 +102,8 @@ __device__ unsigned long long g_gram_stats[16];
 
 template <int STRATEGY>  // 0 = rng, 1 = alpha (compile-time: no angle code for rng)
 __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
-    prune_gram_kernel(const uint8_t *__restrict__ xu8, const int32_t *__restrict__ norms,
+    prune_gram_kernel(const __grid_constant__ CUtensorMap tmX,
+                      const int32_t *__restrict__ norms,
                       int64_t n_rows, const int32_t *__restrict__ row_node,
                       const int32_t *__restrict__ row_order,
                       const int64_t *__restrict__ cand_off,
@@ -167,12 +170,14 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         boff = cand_off[bu];
       }
     };
-    int32_t pv[C / 32];
+    // lane l holds the ids of candidate rows 4l..4l+3 (-1 past cnt): its
+    // TMA gather4 fetches exactly those rows
+    int32_t pv[4];
     auto load_ids = [&](int64_t base, int cnt) {
 #pragma unroll
-      for (int kk = 0; kk < C / 32; ++kk) {
-        const int r = lane + 32 * kk;
-        pv[kk] = r < cnt ? cand_ids[base + r] : 0;
+      for (int i = 0; i < 4; ++i) {
+        const int r = 4 * lane + i;
+        pv[i] = r < cnt ? cand_ids[base + r] : -1;
       }
     };
     if (nb > 0) load_batch(0);
@@ -182,9 +187,9 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     for (int64_t k = 0; k < nb; ++k) {
       const int64_t u = cu, base = coff;
       const int cnt = ccnt;
-      int32_t v[C / 32];
+      int32_t v[4];
 #pragma unroll
-      for (int kk = 0; kk < C / 32; ++kk) v[kk] = pv[kk];
+      for (int i = 0; i < 4; ++i) v[i] = pv[i];
       const int64_t k1 = k + 1;
       if (k1 < nb) {
         if ((k1 & 31) == 0) load_batch(k1);
@@ -198,28 +203,29 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         continue;
       }
       GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
-      uint8_t *tile = s.tile[stage];
+      // candidate rows by TMA gather4 (4 rows of 128 B per instruction, SW128
+      // applied by the map; the 4 rows of lane l land at tile row 4l, i.e.
+      // atom l/2, half l%2).  Rows past cnt keep stale bytes: their Gram
+      // entries feed no mask bit that is ever read (t >= cnt is not
+      // examinable, i >= cnt > t unused).
+      const int ng = (cnt + 3) >> 2;
+      if (lane == 0) mbar_expect_tx_only(&s.full[stage], (uint32_t)ng * 512u);
+      __syncwarp();
+      if (lane < ng) {
+        const int32_t a = v[0];
+        tma_gather4(s.tile[stage] + (lane >> 1) * 1024 + (lane & 1) * 512, &tmX, &s.full[stage],
+                    0, a, v[1] >= 0 ? v[1] : a, v[2] >= 0 ? v[2] : a, v[3] >= 0 ? v[3] : a);
+      }
+      *reinterpret_cast<int4 *>(&s.id[stage][4 * lane]) = make_int4(v[0], v[1], v[2], v[3]);
 #pragma unroll
-      for (int kk = 0; kk < C / 32; ++kk) {
-        const int r = lane + 32 * kk;
+      for (int i = 0; i < 4; ++i) {
+        const int r = 4 * lane + i;
         if (r < cnt) {
-          s.id[stage][r] = v[kk];
           cp_async4(&s.dist[stage][r], cand_dists + base + r);
-          cp_async4(&s.nrm[stage][r], norms + v[kk]);
+          cp_async4(&s.nrm[stage][r], norms + v[i]);
         } else {
-          s.id[stage][r] = -1;
           s.dist[stage][r] = 0.f;
           s.nrm[stage][r] = 0;
-        }
-        // rows past cnt keep stale bytes: their Gram entries feed no mask bit
-        // that is ever read (t >= cnt is not examinable, i >= cnt > t unused)
-        if (32 * kk < cnt) {
-          const bool ok = r < cnt;
-          const uint8_t *src = xu8 + (int64_t)(ok ? v[kk] : 0) * 128;
-          uint8_t *dst = tile + (r >> 3) * 1024 + (r & 7) * 128;
-#pragma unroll
-          for (int ch = 0; ch < 8; ++ch)  // 128B swizzle: chunk ^ (row % 8)
-            cp_async16_zfill(dst + ((ch ^ (r & 7)) << 4), src + ch * 16, ok ? 16u : 0u);
         }
       }
       if (lane == 0) {
@@ -303,8 +309,12 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       int dle;
       if (dv >= 2.0e9f) {
         dle = 0x7fffffff;
+      } else if (strategy != 2) {  // rng: the largest integer below dv, exactly
+        const float fl = floorf(dv);
+        const int x = (int)fl - (fl == dv ? 1 : 0);
+        dle = x > 0 ? x : 0;
       } else {
-        const double p = strategy == 2 ? cos_alpha : 1.0;
+        const double p = cos_alpha;
         int64_t x = (int64_t)floor((double)dv / p);
         while (x >= 0 && !(p * (double)x < (double)dv)) --x;
         while (p * (double)(x + 1) < (double)dv) ++x;
@@ -314,7 +324,9 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       uint32_t pm[4] = {0, 0, 0, 0}, am[4] = {0, 0, 0, 0};
       GWAIT(4, mbar_wait(&s.tfull[grp], tphase));
       tc_fence_after();
-      const int clast = min(q, (cnt - 1) >> 5);  // lower-triangle chunks holding candidates
+      // lower-triangle chunks holding candidates; none when this warp's
+      // candidates are all past cnt (their masks are never read)
+      const int clast = q * 32 >= cnt ? -1 : min(q, (cnt - 1) >> 5);
 #pragma unroll 1
       for (int c = 0; c <= clast; ++c) {
         uint32_t g[32];
@@ -521,6 +533,8 @@ int launch_prune_u8_rows(const uint8_t *xu8, const int32_t *norms, int64_t n,
                          float *out_dists, int32_t *out_counts, int64_t *dist_evals,
                          int64_t *angle_evals, cudaStream_t stream);
 
+bool make_u8_row_map(CUtensorMap *tm, const uint8_t *base, int64_t rows, int box_rows);
+
 size_t gram_workspace(int64_t n) { return (size_t)(n + 64) * sizeof(int32_t); }
 
 // Default selection path for exact-integer rows (PGK_GRAM=0 selects the
@@ -547,6 +561,13 @@ int launch_prune_gram(const uint8_t *xu8, const int32_t *norms, int64_t n,
   int32_t *long_count = reinterpret_cast<int32_t *>(ws);
   int32_t *long_rows = long_count + 32;
   PGK_CUDA(cudaMemsetAsync(long_count, 0, sizeof(int32_t), stream));
+  // candidate ids index data rows (< 2^31 by the ABI); the gather map needs
+  // no tighter row bound
+  CUtensorMap tmX;
+  if (!make_u8_row_map(&tmX, xu8, 0x7fffffff, 1)) {
+    set_error("cuTensorMapEncodeTiled failed (gather4 map)");
+    return PGK_ERR_CUDA;
+  }
   const size_t smem = sizeof(gram::Smem) + 1024;
   static bool attr = false;
   if (!attr) {
@@ -560,12 +581,12 @@ int launch_prune_gram(const uint8_t *xu8, const int32_t *norms, int64_t n,
       (unsigned)std::min<int64_t>(n, (int64_t)gram::CTAS_PER_SM * num_sms());
   if (strategy == 0 || strategy == 2)  // slack: the rng masks with another threshold
     gram::prune_gram_kernel<0><<<grid, gram::THREADS, smem, stream>>>(
-        xu8, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
+        tmX, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
         cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals,
         long_rows, long_count);
   else
     gram::prune_gram_kernel<1><<<grid, gram::THREADS, smem, stream>>>(
-        xu8, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, 1,
+        tmX, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, 1,
         cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals,
         long_rows, long_count);
   PGK_CHECK_LAUNCH("prune_gram_kernel");
