@@ -34,9 +34,19 @@ constexpr int BN = 128;   // data points per tile == MMA N
 constexpr int KB = 128;   // bytes per (padded) row
 constexpr int STAGES = 2;       // B-tile ring depth
 constexpr int ACC = 1;          // TMEM accumulator stages (128 columns each)
-constexpr int HALVES = 2;       // each accumulator is filled / drained in two 64-column halves
+#ifndef TC_PAIRLD
+#define TC_PAIRLD 0
+#endif
+#ifndef TC_PARTS
+#define TC_PARTS 2
+#endif
+constexpr int HALVES = TC_PARTS;  // each accumulator is filled / drained in column parts
 constexpr int HN = BN / HALVES;
-constexpr int CTAS_PER_SM = 3;  // co-resident CTAs share the tensor core
+constexpr int CPP = HN / 32;      // 32-column epilogue chunks per part
+#ifndef TC_CTAS
+#define TC_CTAS 3
+#endif
+constexpr int CTAS_PER_SM = TC_CTAS;  // co-resident CTAs share the tensor core
 constexpr int TILE_BYTES = BN * KB;
 constexpr int CAP = 1024;  // per-row candidate buffer (keys, global memory)
 constexpr int THREADS = 192;  // warp 0 TMA, warp 1 TMEM alloc + MMA, warps 2-5 epilogue
@@ -235,7 +245,7 @@ __device__ __forceinline__ uint32_t dense_val(int dist, int64_t col, int64_t n, 
 
 template <bool STATS, bool DENSE>
 // 112 registers keeps CTAS_PER_SM = 3 resident (3 x 6 warps x 112 x 32 <= 64K)
-__global__ void __maxnreg__(112)
+__global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
     tc_pool_u8_kernel(const __grid_constant__ CUtensorMap tmX,
                       const __grid_constant__ CUtensorMap tmQ, int64_t n, int64_t nq,
                       int exclude_self, const int32_t *__restrict__ xnorm,
@@ -424,23 +434,40 @@ __global__ void __maxnreg__(112)
         if (tlist && t + 1 < len) tid_next = tlist[(int64_t)b * tstride + t + 1];
         const int64_t col0 = (int64_t)tid * BN;
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
+#if TC_PAIRLD
+        static_assert(CPP == 2, "paired TMEM loads need 2-chunk parts");
+        uint32_t rn[32];
+#endif
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
-          if ((c & 1) == 0) {  // entering half c/2: wait for its MMAs
+          if (c % CPP == 0) {  // entering part c/CPP: wait for its MMAs
             if (c > 0) {  // the previous half is in registers: let the MMA reuse it
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(&s.tempty[(c >> 1) - 1]);
+              if (lane == 0) mbar_arrive(&s.tempty[c / CPP - 1]);
             }
             PGK_TICK(ST_MAIN);
-            mbar_wait(&s.tfull[c >> 1], acc_phase);
+            mbar_wait(&s.tfull[c / CPP], acc_phase);
             tc_fence_after();
             PGK_TICK(ST_WAIT);
           }
-          // (co-resident CTAs hide the TMEM-load latency; one chunk in flight)
           uint32_t r[32];
+#if TC_PAIRLD
+          // both chunks of a part in one TMEM round trip
+          if ((c & 1) == 0) {
+            tmem_ld32(tbase + c * 32, r);
+            tmem_ld32(tbase + (c + 1) * 32, rn);
+            tmem_wait_ld_regs(r);
+            tmem_wait_ld_regs(rn);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = rn[i];
+          }
+#else
+          // (co-resident CTAs hide the TMEM-load latency; one chunk in flight)
           tmem_ld32(tbase + c * 32, r);
           tmem_wait_ld();
+#endif
           const int64_t cb = col0 + c * 32;
           const int4 *nyp = reinterpret_cast<const int4 *>(s.ny[tpar] + c * 32);
           if (DENSE) {

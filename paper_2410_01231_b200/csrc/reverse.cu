@@ -37,7 +37,7 @@ int launch_prune(const float *X, const uint8_t *xu8, const int32_t *norms, int64
                  cudaStream_t stream);
 
 constexpr int SORT_WARPS = 8;
-constexpr int SORT_SMEM_KEYS = 512;  // per-warp in-shared-memory sort capacity
+constexpr int SORT_SMEM_KEYS = 512;  // per-warp in-register sort capacity (16 keys per lane)
 
 __global__ void rev_count_kernel(const int32_t *__restrict__ ids,
                                  const int32_t *__restrict__ counts, int64_t n,
@@ -182,6 +182,68 @@ __device__ __forceinline__ int warp_dedupe(const uint64_t *s, int len,
   return m;
 }
 
+// Register bitonic sort of 32*NPL keys (element i = slot*32 + lane), then the
+// consecutive-duplicate-id removal of warp_dedupe on the sorted registers.
+template <int NPL>
+__device__ __forceinline__ int reg_sort_dedupe(const uint64_t *__restrict__ keys, int len,
+                                               int32_t *__restrict__ out_ids,
+                                               float *__restrict__ out_d, int lane) {
+  constexpr int SIZE = 32 * NPL;
+  uint64_t e[NPL];
+#pragma unroll
+  for (int s0 = 0; s0 < NPL; ++s0) {
+    const int i = s0 * 32 + lane;
+    e[s0] = i < len ? keys[i] : KEY_MAX;
+  }
+#pragma unroll
+  for (int k = 2; k <= SIZE; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int js = j >> 5;
+#pragma unroll
+        for (int s0 = 0; s0 < NPL; ++s0) {
+          if (s0 & js) continue;
+          const int s1 = s0 ^ js;
+          const bool up = (((s0 << 5) | lane) & k) == 0;
+          const uint64_t a = e[s0], b = e[s1];
+          const bool sw = (a > b) == up;
+          e[s0] = sw ? b : a;
+          e[s1] = sw ? a : b;
+        }
+      } else {
+        const bool lower = (lane & j) == 0;
+#pragma unroll
+        for (int s0 = 0; s0 < NPL; ++s0) {
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, e[s0], j);
+          const bool up = (((s0 << 5) | lane) & k) == 0;
+          const uint64_t mn = e[s0] < o ? e[s0] : o, mx = e[s0] < o ? o : e[s0];
+          e[s0] = (lower == up) ? mn : mx;
+        }
+      }
+    }
+  }
+  int m = 0;
+  uint64_t last = 0;  // previous slot's lane-31 key
+#pragma unroll
+  for (int s0 = 0; s0 < NPL; ++s0) {
+    if (s0 * 32 >= len) break;
+    uint64_t prev = __shfl_up_sync(0xffffffffu, e[s0], 1);
+    if (lane == 0) prev = last;
+    last = __shfl_sync(0xffffffffu, e[s0], 31);
+    const int i = s0 * 32 + lane;
+    const bool keep = i < len && (i == 0 || key_id(prev) != key_id(e[s0]));
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int p = m + __popc(bal & lanemask_lt());
+      out_ids[p] = key_id(e[s0]);
+      out_d[p] = key_dist(e[s0]);
+    }
+    m += __popc(bal);
+  }
+  return m;
+}
+
 __global__ void __launch_bounds__(SORT_WARPS * 32)
     merge_sort_kernel(const int64_t *__restrict__ mrg_off, int64_t n,
                       const uint64_t *__restrict__ keys,
@@ -189,9 +251,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32)
                       int32_t *__restrict__ mrg_counts,
                       int32_t *__restrict__ long_list,
                       int32_t *__restrict__ long_count) {
-  __shared__ uint64_t s[SORT_WARPS][SORT_SMEM_KEYS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t *sk = s[warp];
   for (int64_t u = (int64_t)blockIdx.x * SORT_WARPS + warp; u < n;
        u += (int64_t)gridDim.x * SORT_WARPS) {
     const int64_t lo = mrg_off[u];
@@ -200,12 +260,12 @@ __global__ void __launch_bounds__(SORT_WARPS * 32)
       if (lane == 0) long_list[atomicAdd(long_count, 1)] = (int32_t)u;
       continue;
     }
-    const int size = next_pow2(len < 2 ? 2 : len);
-    __syncwarp();
-    for (int i = lane; i < size; i += 32) sk[i] = i < len ? keys[lo + i] : KEY_MAX;
-    __syncwarp();
-    warp_bitonic_sort(sk, size, lane);
-    int m = warp_dedupe(sk, len, mrg_ids + lo, mrg_d + lo, lane);
+    int m;
+    if (len <= 32) m = reg_sort_dedupe<1>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
+    else if (len <= 64) m = reg_sort_dedupe<2>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
+    else if (len <= 128) m = reg_sort_dedupe<4>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
+    else if (len <= 256) m = reg_sort_dedupe<8>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
+    else m = reg_sort_dedupe<16>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
     if (lane == 0) mrg_counts[u] = m;
   }
 }
