@@ -48,6 +48,7 @@ constexpr int CPP = HN / 32;      // 32-column epilogue chunks per part
 #endif
 constexpr int CTAS_PER_SM = TC_CTAS;  // co-resident CTAs share the tensor core
 constexpr int TILE_BYTES = BN * KB;
+constexpr int NYBUF = 3;
 constexpr int CAP = 1024;  // per-row candidate buffer (keys, global memory)
 constexpr int THREADS = 192;  // warp 0 TMA, warp 1 TMEM alloc + MMA, warps 2-5 epilogue
 constexpr int TMEM_COLS = ACC * BN;
@@ -57,8 +58,12 @@ struct __align__(1024) Smem {
   uint8_t a[BM * KB];
   uint8_t b[STAGES][TILE_BYTES];
   int32_t sv[4][32 * 36];  // per epilogue warp: one chunk of s values per lane
-  alignas(16) int32_t ny[2][BN];   // |x|^2 of the tile (double-buffered by tile parity)
-  alignas(16) int32_t pid[2][BN];  // original ids of the tile's columns (pruned path)
+  // |x|^2 and original ids (pruned path) of the tile's columns, 3 buffers by
+  // running tile count: the MMA warp prefetches tile g+1's while the
+  // epilogue may still read tile g-1's
+  alignas(16) int32_t ny[NYBUF][BN];
+  alignas(16) int32_t pid[NYBUF][BN];
+  uint64_t nfull[NYBUF];
   uint64_t full[STAGES], empty[STAGES];
   uint64_t tfull[HALVES], tempty[HALVES];  // per accumulator half
   uint64_t a_full, a_empty;
@@ -283,6 +288,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
       mbar_init(&s.tfull[i], 1);
       mbar_init(&s.tempty[i], 4);
     }
+    for (int i = 0; i < NYBUF; ++i) mbar_init(&s.nfull[i], 1);
     mbar_init(&s.a_full, 1);
     // the A tile / block slot is free once the MMA is done with it AND every
     // epilogue warp has taken the block index: otherwise, with one-tile
@@ -337,8 +343,17 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
-      int stage = 0, tpar = 0;
+      int stage = 0;
       uint32_t phase = 0, acc_phase = 0;
+      uint32_t g = 0;  // tiles issued by this CTA (norm buffer g % NYBUF)
+      // the tile's |x|^2 (xnorm is padded to a multiple of BN) and ids into
+      // buffer gi % NYBUF, one tile ahead of the MMA
+      auto load_norms = [&](uint32_t gi, int tid) {
+        const int nb = (int)(gi % NYBUF);
+        mbar_expect_tx(&s.nfull[nb], perm ? BN * 8 : BN * 4);
+        bulk_load(s.ny[nb], xnorm + (int64_t)tid * BN, BN * 4, &s.nfull[nb]);
+        if (perm) bulk_load(s.pid[nb], perm + (int64_t)tid * BN, BN * 4, &s.nfull[nb]);
+      };
       for (int it = 0;; ++it) {
         mbar_wait(&s.a_full, it & 1);
         const int b = s.blk[it & 1];
@@ -346,19 +361,20 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
         const int len = tlist ? tlen[b] : ntiles;
         tc_fence_after();
         const uint64_t adesc = sw128_desc(s.a);
-        for (int t = 0; t < len; ++t) {
-          const int tid = tlist ? tlist[(int64_t)b * tstride + t] : t;
+        // buffer g % NYBUF last served tile g - 3, which the epilogue finished
+        // before releasing tile g - 1's first part (waited on below / before)
+        int tid_nx = tlist ? tlist[(int64_t)b * tstride] : 0;
+        load_norms(g, tid_nx);
+        for (int t = 0; t < len; ++t, ++g) {
+          const int tid = tid_nx;
+          if (t + 1 < len) tid_nx = tlist ? tlist[(int64_t)b * tstride + t + 1] : t + 1;
 #pragma unroll
           for (int h = 0; h < HALVES; ++h) {
             mbar_wait(&s.tempty[h], acc_phase ^ 1);
             if (h == 0) {
-              // the tile's |x|^2 (xnorm is padded to a multiple of BN) and ids
-              // land with the first half: tfull[0] completes on the commit AND
-              // these bytes (buffer by tile parity: the epilogue may still read
-              // the previous tile's in its second half)
-              mbar_expect_tx_only(&s.tfull[0], perm ? BN * 8 : BN * 4);
-              bulk_load(s.ny[tpar], xnorm + (int64_t)tid * BN, BN * 4, &s.tfull[0]);
-              if (perm) bulk_load(s.pid[tpar], perm + (int64_t)tid * BN, BN * 4, &s.tfull[0]);
+              // the epilogue has released tile t-1's first part, so it is done
+              // with tile t-2: its norm buffer takes tile t+1's
+              if (t + 1 < len) load_norms(g + 1, tid_nx);
               mbar_wait(&s.full[stage], phase);
             }
             tc_fence_after();
@@ -372,7 +388,6 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
           tc_commit(&s.empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           acc_phase ^= 1;
-          tpar ^= 1;
         }
         tc_commit(&s.a_empty);
       }
@@ -382,7 +397,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
     const int q = warp & 3;  // TMEM lane quarter this warp may access (warp % 4)
     int32_t *const svw = s.sv[warp - 2];  // this warp's staging: lane l at svw[l * 36]
     int32_t *sv = svw + lane * 36;
-    int tpar = 0;
+    uint32_t g = 0;  // tiles consumed by this CTA (norm buffer g % NYBUF)
     uint32_t acc_phase = 0;
     for (int it = 0;; ++it) {
       mbar_wait(&s.a_full, it & 1);
@@ -433,6 +448,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
         const int tid = tlist ? tid_next : t;
         if (tlist && t + 1 < len) tid_next = tlist[(int64_t)b * tstride + t + 1];
         const int64_t col0 = (int64_t)tid * BN;
+        const int tpar = (int)(g % NYBUF);
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
 #if TC_PAIRLD
         static_assert(CPP == 2, "paired TMEM loads need 2-chunk parts");
@@ -440,6 +456,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
 #endif
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
+          if (c == 0) mbar_wait(&s.nfull[tpar], (g / NYBUF) & 1);  // the tile's norms / ids
           if (c % CPP == 0) {  // entering part c/CPP: wait for its MMAs
             if (c > 0) {  // the previous half is in registers: let the MMA reuse it
               tc_fence_before();
@@ -602,7 +619,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
         __syncwarp();
         if (lane == 0) mbar_arrive(&s.tempty[HALVES - 1]);
         acc_phase ^= 1;
-        tpar ^= 1;
+        ++g;
       }
       // block done: record each row's buffer fill and threshold; selection
       // and sorting run in the massively parallel finalize kernel

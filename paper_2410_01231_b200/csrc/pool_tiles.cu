@@ -166,6 +166,10 @@ constexpr int DB = 64, DK = 32;
 __global__ void __launch_bounds__(256)
     tile_dist_kernel(const float *__restrict__ cent, int64_t T, int d, float *__restrict__ dc) {
   __shared__ float sa[DK][DB + 1], sb[DK][DB + 1];
+  __shared__ float st[DB][DB + 1];  // transposed block (mirror write)
+  // dc is symmetric bit for bit ((a-b)^2 == (b-a)^2, same FMA order): only
+  // blocks on or above the diagonal are computed, and mirrored
+  if (blockIdx.x < blockIdx.y) return;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int64_t q0 = (int64_t)blockIdx.y * DB, t0 = (int64_t)blockIdx.x * DB;
   float acc[4][4] = {};
@@ -196,8 +200,16 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t q = q0 + ty * 4 + i, t = t0 + tx + 16 * j;
-      if (q < T && t < T) dc[q * T + t] = sqrtf(acc[i][j]);
+      const float v = sqrtf(acc[i][j]);
+      st[tx + 16 * j][ty * 4 + i] = v;
+      if (q < T && t < T) dc[q * T + t] = v;
     }
+  if (blockIdx.x == blockIdx.y) return;
+  __syncthreads();
+  for (int e = threadIdx.x; e < DB * DB; e += 256) {
+    const int r = e / DB, c = e % DB;  // mirror row t0 + r, column q0 + c
+    if (t0 + r < T && q0 + c < T) dc[(t0 + r) * T + q0 + c] = st[r][c];
+  }
 }
 
 // pass-1 list: the nearest tiles of every query tile by centroid distance,
