@@ -8,18 +8,20 @@
 // all partial sums are integers < 2^24).  Top-K by packed (dist, id) key is
 // therefore the reference's (dist, id) order, no rerank needed.
 //
-// Kernel shape (persistent, 2 CTAs / SM, 256 threads):
-//   warp 0      TMA producer: the block's 128 query rows (A, once per block)
-//               and a ring of 128-point data tiles (B), 128 B/row, SW128
-//   warp 1      MMA issuer: D[128 x 128] (s32, TMEM) = A . B^T, 4 x K=32
-//               tcgen05.mma per tile, double-buffered accumulator
-//   warp 2      TMEM allocator (256 columns)
-//   warps 4..7  epilogue: warp q reads TMEM lanes 32q..32q+31, i.e. thread =
-//               query row; per 32 columns one IMAD + one compare per value
-//               against the row's running K-th best (fast reject), rare
-//               survivors appended to a per-row candidate buffer in global
-//               memory (L2); a full buffer is compacted by the whole warp
-//               (bitonic sort in shared memory, keep K, raise the threshold).
+// Kernel shape (persistent, TC_CTAS = 2 CTAs / SM, 192 threads):
+//   warp 0      TMA producer + dynamic block scheduler: the block's 128 query
+//               rows (A, once per block) and a 2-stage ring of 128-point data
+//               tiles (B), 128 B/row, SW128
+//   warp 1      TMEM allocator + MMA issuer: D[128 x 128] (s32) = A . B^T,
+//               4 x K=32 tcgen05.mma per 64-column part; TC_ACC = 2
+//               accumulators by tile parity, so the epilogue warps may drift
+//               a whole tile apart; bulk-loads each tile's |x|^2 and ids one
+//               tile ahead (NYBUF ring)
+//   warps 2..5  epilogue: warp q reads TMEM lanes 32q..32q+31, i.e. thread =
+//               query row; per 32 columns one IADD + one compare per value
+//               against the row's threshold (fast reject); survivors appended
+//               to a per-row candidate buffer in global memory; the
+//               massively parallel finalize kernel selects and sorts.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -33,7 +35,11 @@ constexpr int BM = 128;   // query rows per block == TMEM lanes
 constexpr int BN = 128;   // data points per tile == MMA N
 constexpr int KB = 128;   // bytes per (padded) row
 constexpr int STAGES = 2;       // B-tile ring depth
-constexpr int ACC = 1;          // TMEM accumulator stages (128 columns each)
+#ifndef TC_ACC
+#define TC_ACC 2
+#endif
+
+constexpr int ACC = TC_ACC;     // TMEM accumulator stages (128 columns each, by tile)
 #ifndef TC_PAIRLD
 #define TC_PAIRLD 0
 #endif
@@ -44,11 +50,11 @@ constexpr int HALVES = TC_PARTS;  // each accumulator is filled / drained in col
 constexpr int HN = BN / HALVES;
 constexpr int CPP = HN / 32;      // 32-column epilogue chunks per part
 #ifndef TC_CTAS
-#define TC_CTAS 3
+#define TC_CTAS 2
 #endif
 constexpr int CTAS_PER_SM = TC_CTAS;  // co-resident CTAs share the tensor core
 constexpr int TILE_BYTES = BN * KB;
-constexpr int NYBUF = 3;
+constexpr int NYBUF = ACC + 2;  // the MMA runs up to ACC tiles ahead of the epilogue
 constexpr int CAP = 1024;  // per-row candidate buffer (keys, global memory)
 constexpr int THREADS = 192;  // warp 0 TMA, warp 1 TMEM alloc + MMA, warps 2-5 epilogue
 constexpr int TMEM_COLS = ACC * BN;
@@ -65,7 +71,7 @@ struct __align__(1024) Smem {
   alignas(16) int32_t pid[NYBUF][BN];
   uint64_t nfull[NYBUF];
   uint64_t full[STAGES], empty[STAGES];
-  uint64_t tfull[HALVES], tempty[HALVES];  // per accumulator half
+  uint64_t tfull[ACC][HALVES], tempty[ACC][HALVES];  // per accumulator slot and part
   uint64_t a_full, a_empty;
   uint32_t tmem_base;
   int32_t blk[2];  // dynamic schedule: block index per A-tile phase (-1 = done)
@@ -285,8 +291,10 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
       mbar_init(&s.empty[i], 1);
     }
     for (int i = 0; i < HALVES; ++i) {
-      mbar_init(&s.tfull[i], 1);
-      mbar_init(&s.tempty[i], 4);
+      for (int a = 0; a < ACC; ++a) {
+        mbar_init(&s.tfull[a][i], 1);
+        mbar_init(&s.tempty[a][i], 4);
+      }
     }
     for (int i = 0; i < NYBUF; ++i) mbar_init(&s.nfull[i], 1);
     mbar_init(&s.a_full, 1);
@@ -344,8 +352,8 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
       int stage = 0;
-      uint32_t phase = 0, acc_phase = 0;
-      uint32_t g = 0;  // tiles issued by this CTA (norm buffer g % NYBUF)
+      uint32_t phase = 0;
+      uint32_t g = 0;  // tiles issued by this CTA (accumulator g % ACC, norm buffer g % NYBUF)
       // the tile's |x|^2 (xnorm is padded to a multiple of BN) and ids into
       // buffer gi % NYBUF, one tile ahead of the MMA
       auto load_norms = [&](uint32_t gi, int tid) {
@@ -361,8 +369,8 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
         const int len = tlist ? tlen[b] : ntiles;
         tc_fence_after();
         const uint64_t adesc = sw128_desc(s.a);
-        // buffer g % NYBUF last served tile g - 3, which the epilogue finished
-        // before releasing tile g - 1's first part (waited on below / before)
+        // buffer g % NYBUF last served tile g - NYBUF; the epilogue finished it
+        // before releasing tile g-1-ACC's last part (waited on for tile g-1)
         int tid_nx = tlist ? tlist[(int64_t)b * tstride] : 0;
         load_norms(g, tid_nx);
         for (int t = 0; t < len; ++t, ++g) {
@@ -370,10 +378,11 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
           if (t + 1 < len) tid_nx = tlist ? tlist[(int64_t)b * tstride + t + 1] : t + 1;
 #pragma unroll
           for (int h = 0; h < HALVES; ++h) {
-            mbar_wait(&s.tempty[h], acc_phase ^ 1);
+            mbar_wait(&s.tempty[g % ACC][h], ((g / ACC) & 1) ^ 1);
             if (h == 0) {
-              // the epilogue has released tile t-1's first part, so it is done
-              // with tile t-2: its norm buffer takes tile t+1's
+              // the epilogue has released tile g-ACC's first part (this slot's
+              // previous use), so it is done with tile g-ACC-1 = g+1-NYBUF:
+              // that norm buffer takes tile g+1's
               if (t + 1 < len) load_norms(g + 1, tid_nx);
               mbar_wait(&s.full[stage], phase);
             }
@@ -382,12 +391,11 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
             const uint64_t bdesc = sw128_desc(s.b[stage] + h * HN * KB);
 #pragma unroll
             for (int kk = 0; kk < KB / 32; ++kk)  // K = 32 bytes per MMA; +32 B = +2 (16 B units)
-              mma_i8(tmem + h * HN, adesc + 2 * kk, bdesc + 2 * kk, IDESC_H, kk > 0);
-            tc_commit(&s.tfull[h]);
+              mma_i8(tmem + (g % ACC) * BN + h * HN, adesc + 2 * kk, bdesc + 2 * kk, IDESC_H, kk > 0);
+            tc_commit(&s.tfull[g % ACC][h]);
           }
           tc_commit(&s.empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
-          acc_phase ^= 1;
         }
         tc_commit(&s.a_empty);
       }
@@ -397,8 +405,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
     const int q = warp & 3;  // TMEM lane quarter this warp may access (warp % 4)
     int32_t *const svw = s.sv[warp - 2];  // this warp's staging: lane l at svw[l * 36]
     int32_t *sv = svw + lane * 36;
-    uint32_t g = 0;  // tiles consumed by this CTA (norm buffer g % NYBUF)
-    uint32_t acc_phase = 0;
+    uint32_t g = 0;  // tiles consumed by this CTA (accumulator g % ACC, norm buffer g % NYBUF)
     for (int it = 0;; ++it) {
       mbar_wait(&s.a_full, it & 1);
       const int b = s.blk[it & 1];
@@ -449,7 +456,9 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
         if (tlist && t + 1 < len) tid_next = tlist[(int64_t)b * tstride + t + 1];
         const int64_t col0 = (int64_t)tid * BN;
         const int tpar = (int)(g % NYBUF);
-        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
+        const int aslot = (int)(g % ACC);
+        const uint32_t acc_phase = (g / ACC) & 1;
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + aslot * BN;
 #if TC_PAIRLD
         static_assert(CPP == 2, "paired TMEM loads need 2-chunk parts");
         uint32_t rn[32];
@@ -461,10 +470,10 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
             if (c > 0) {  // the previous half is in registers: let the MMA reuse it
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(&s.tempty[c / CPP - 1]);
+              if (lane == 0) mbar_arrive(&s.tempty[aslot][c / CPP - 1]);
             }
             PGK_TICK(ST_MAIN);
-            mbar_wait(&s.tfull[c / CPP], acc_phase);
+            mbar_wait(&s.tfull[aslot][c / CPP], acc_phase);
             tc_fence_after();
             PGK_TICK(ST_WAIT);
           }
@@ -617,8 +626,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
         // last half and the tile's norms / ids consumed: hand them back
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&s.tempty[HALVES - 1]);
-        acc_phase ^= 1;
+        if (lane == 0) mbar_arrive(&s.tempty[aslot][HALVES - 1]);
         ++g;
       }
       // block done: record each row's buffer fill and threshold; selection
@@ -1009,7 +1017,7 @@ __device__ __noinline__ uint32_t kth_dense(const uint32_t *__restrict__ buf, int
 __global__ void __launch_bounds__(FIN_WARPS * 32)
     tc_kth_dense_kernel(const uint64_t *__restrict__ bufs, const int32_t *__restrict__ row_cnt,
                         int64_t nrows, int K, const int32_t *__restrict__ perm,
-                        uint64_t *__restrict__ out_keys) {
+                        uint64_t *__restrict__ out_keys, uint32_t *__restrict__ ostat) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t r = (int64_t)blockIdx.x * FIN_WARPS + warp; r < nrows;
        r += (int64_t)gridDim.x * FIN_WARPS) {
@@ -1024,6 +1032,13 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
     const int64_t orow = perm ? (int64_t)perm[r] : r;
     if (lane == 0)
       out_keys[orow * K + K - 1] = kth == 0xffffffffu ? KEY_MAX : pack_key((float)kth, 0x7fffffff);
+    if (ostat) {  // instrumentation: order statistics K/8, K/4, K/2, K (PGK_TILES_STATS)
+      for (int j = 0; j < 4; ++j) {
+        const int kj = max(1, K >> (3 - j));
+        const uint32_t x = cnt <= 1024 ? kth_dense<32>(b, cnt, kj, lane) : kth_dense<64>(b, cnt, kj, lane);
+        if (lane == 0) ostat[orow * 4 + j] = x;
+      }
+    }
   }
 }
 
@@ -1081,6 +1096,9 @@ bool make_u8_row_map(CUtensorMap *tm, const uint8_t *base, int64_t rows, int box
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+
+// instrumentation (PGK_TILES_STATS): pass-1 order statistics per row
+uint32_t *g_dense_ostat = nullptr;
 
 size_t tc_pool_workspace(int64_t n, int64_t nq, bool self) {
   const int sms = num_sms();
@@ -1179,7 +1197,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
     const unsigned fgrid =
         (unsigned)std::min<int64_t>((nq + tc::FIN_WARPS - 1) / tc::FIN_WARPS, (int64_t)sms * 8);
     tc::tc_kth_dense_kernel<<<fgrid, tc::FIN_WARPS * 32, 0, stream>>>(bufs, row_cnt, nq, K, perm,
-                                                                      keys);
+                                                                      keys, g_dense_ostat);
     PGK_CHECK_LAUNCH("tc_kth_dense_kernel");
     *handled = true;
     return PGK_OK;

@@ -284,17 +284,23 @@ __global__ void tile_ubound_kernel(const uint64_t *__restrict__ keys, int K,
   }
 }
 
-// pass-2 list: every tile T with lb(Q,T) <= U_Q, ascending T
+// pass-2 list: every tile T with lb(Q,T) <= scale * U_Q (+1e-9), ascending T;
+// with `only`, just the tiles Q with only[Q] != 0 (the others get no list)
 __global__ void tile_filter_kernel(const float *__restrict__ dc, const double *__restrict__ rad,
                                    const int32_t *__restrict__ size, const double *__restrict__ U,
                                    int64_t T, int32_t *__restrict__ lists,
                                    int32_t *__restrict__ lens,
                                    unsigned long long *__restrict__ total,
-                                   double dc_margin = DC_MARGIN) {
+                                   double dc_margin = DC_MARGIN, double scale = 1.0,
+                                   const int32_t *__restrict__ only = nullptr) {
   const int lane = threadIdx.x & 31;
   for (int64_t Q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; Q < T;
        Q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const double rQ = rad[Q], UQ = U[Q];
+    if (only && only[Q] == 0) {
+      if (lane == 0) lens[Q] = 0;
+      continue;
+    }
+    const double rQ = rad[Q], UQ = U[Q] * scale + 1e-9;
     int base = 0;
     for (int64_t t0 = 0; size[Q] > 0 && t0 < T; t0 += 32) {
       const int64_t t = t0 + lane;
@@ -309,19 +315,9 @@ __global__ void tile_filter_kernel(const float *__restrict__ dc, const double *_
     }
     if (lane == 0) {
       lens[Q] = base;
-      atomicAdd(total, (unsigned long long)base);
+      if (total) atomicAdd(total, (unsigned long long)base);
     }
   }
-}
-
-// Blocks whose guessed pass-2 threshold failed somewhere keep their list for
-// the re-run; every other block gets an empty list (skipped).
-__global__ void rerun_lens_kernel(const int32_t *__restrict__ fail,
-                                  const int32_t *__restrict__ lens, int64_t T,
-                                  int32_t *__restrict__ lens2) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T;
-       t += (int64_t)gridDim.x * blockDim.x)
-    lens2[t] = fail[t] ? lens[t] : 0;
 }
 
 // Pass-2 threshold guess: seed * SHRINK (exclusive squared-distance bound).
@@ -420,6 +416,8 @@ size_t tiles_workspace(int64_t n, int64_t d) { return tiles_layout(nullptr, 0, n
 int64_t tiles_rows(int64_t n) { return tiles_layout(nullptr, 0, n, 1).NPmax; }
 
 // Runs the whole pruned pool.  *handled = false when pruning does not apply.
+extern uint32_t *g_dense_ostat;
+
 int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm, int K,
                          uint64_t *keys, void *tc_ws, size_t tc_bytes, void *tws,
                          size_t tws_bytes, cudaStream_t stream, bool *handled,
@@ -484,17 +482,30 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   tile_nearest_kernel<<<g, 256, 0, stream>>>(L.dcm, L.size, T, K, L.lists, L.lens, L.total + 1);
   PGK_CHECK_LAUNCH("tile_nearest_kernel");
   dbg_stage("tile_nearest_kernel", stream);
+  const char *se0 = getenv("PGK_TILES_STATS");
+  uint32_t *ostat = nullptr;
+  if (se0 && se0[0] == '1') {  // pass-1 order statistics for the guess analysis
+    PGK_CUDA(cudaMalloc(&ostat, (size_t)n * 4 * sizeof(uint32_t)));
+    g_dense_ostat = ostat;
+  }
   rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes, stream,
                                L.xs, L.lists, L.lens, T, L.perm, handled, nullptr, 1);
+  g_dense_ostat = nullptr;
   if (rc) return rc;
   dbg_stage("pass 1 tc", stream);
   if (!*handled) return PGK_OK;
   tile_ubound_kernel<<<g, 256, 0, stream>>>(keys, K, L.perm, T, L.U);
   PGK_CHECK_LAUNCH("tile_ubound_kernel");
   dbg_stage("tile_ubound_kernel", stream);
-  // 5. pass 2: every tile that can hold a pool member, then the full top-K
+  // 5. pass 2: every tile that can hold a pool member, then the full top-K.
+  // With a guessed threshold g <= shrink * seed a row is exact only when it
+  // finds >= K points below g (verified), and every point below g lies
+  // within sqrt(shrink) * U_Q of the tile: the list can be cut to that
+  // radius; rows failing the guess re-run on the full-radius list (step 6).
+  const float shrink = seed_shrink();
   tile_filter_kernel<<<g, 256, 0, stream>>>(L.dcm, L.rad, L.size, L.U, T, L.lists, L.lens,
-                                            L.total);
+                                            L.total, DC_MARGIN,
+                                            shrink < 1.0f ? sqrt((double)shrink) : 1.0);
   PGK_CHECK_LAUNCH("tile_filter_kernel");
   dbg_stage("tile_filter_kernel", stream);
   const char *se = getenv("PGK_TILES_STATS");
@@ -505,7 +516,6 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
     PGK_CUDA(cudaMemcpy2DAsync(seed_k.data(), 8, keys + K - 1, (size_t)K * 8, 8, n,
                                cudaMemcpyDeviceToHost, stream));
   }
-  const float shrink = seed_shrink();
   PGK_CUDA(cudaMemsetAsync(L.fail, 0, T * 4, stream));
   PGK_CUDA(cudaMemsetAsync(L.fail_rows, 0, NP, stream));
   rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes, stream,
@@ -514,11 +524,12 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   if (rc) return rc;
   dbg_stage("pass 2 tc", stream);
   if (shrink < 1.0f) {
-    // 6. re-run the blocks holding a row whose guess was too tight, seeded by
-    // its untouched pass-1 key (finished rows re-derive the same result)
-    rerun_lens_kernel<<<g, 256, 0, stream>>>(L.fail, L.lens, T, L.lens2);
-    PGK_CHECK_LAUNCH("rerun_lens_kernel");
-  dbg_stage("rerun_lens_kernel", stream);
+    // 6. re-run the rows whose guess was too tight (their blocks, row mask),
+    // seeded by their untouched pass-1 key, on the full-radius list
+    tile_filter_kernel<<<g, 256, 0, stream>>>(L.dcm, L.rad, L.size, L.U, T, L.lists, L.lens2,
+                                              nullptr, DC_MARGIN, 1.0, L.fail);
+    PGK_CHECK_LAUNCH("tile_filter_kernel (re-run)");
+  dbg_stage("tile_filter_kernel (re-run)", stream);
     if (stats) {
       std::vector<int32_t> hf(T);
       PGK_CUDA(cudaMemcpyAsync(hf.data(), L.fail, T * 4, cudaMemcpyDeviceToHost, stream));
@@ -552,6 +563,24 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
     for (double f : {0.90, 0.92, 0.93, 0.94, 0.95, 0.96}) {
       const size_t above = ratio.end() - std::lower_bound(ratio.begin(), ratio.end(), f);
       fprintf(stderr, "[tiles]   rows with ratio >= %.2f: %zu\n", f, above);
+    }
+    if (ostat) {  // predictors: pass-1 order statistics K/8, K/4, K/2, K
+      std::vector<uint32_t> os((size_t)n * 4);
+      PGK_CUDA(cudaMemcpy(os.data(), ostat, os.size() * 4, cudaMemcpyDeviceToHost));
+      for (int j = 0; j < 4; ++j) {
+        std::vector<double> rr;
+        for (int64_t i = 0; i < n; ++i)
+          if (os[i * 4 + j] > 0 && os[i * 4 + j] != 0xffffffffu)
+            rr.push_back(final_d[i] / (double)os[i * 4 + j]);
+        std::sort(rr.begin(), rr.end());
+        auto q = [&](double f) { return rr.empty() ? 0.0 : rr[(size_t)(f * (rr.size() - 1))]; };
+        const double f = q(0.998);  // guess factor failing 0.2 % of rows
+        double surv = 0;  // mean (guess / final)^12.9: relative buffered survivors
+        for (double x : rr) surv += pow(f / x, 12.9);
+        fprintf(stderr, "[tiles] predictor rank K>>%d: final/pred p1 %.3f p50 %.3f p99.8 %.3f "
+                "-> survivors x%.2f of exact\n", 3 - j, q(0.01), q(0.5), f, surv / rr.size());
+      }
+      cudaFree(ostat);
     }
   }
   {  // work record: [0] pass-2 tile pairs, [1] pass-1 pairs, [2] assignment pairs, [3] done

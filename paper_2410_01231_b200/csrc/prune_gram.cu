@@ -19,7 +19,7 @@
 // kept neighbour is discarded).  Rows with more than 128 candidates (hubs in
 // phase B) are listed and left to prune_u8_kernel.
 //
-// CTA: warp 0 gathers (TMA gather4 rows, cp.async metadata), warp 1 allocates TMEM and
+// CTA: warp 0 gathers (TMA gather4 rows, register-pipelined metadata), warp 1 allocates TMEM and
 // issues the MMA, warps 2-5 build the predicate masks (each its lower-
 // triangle chunks of the Gram rows), warp 6 runs the greedy scan and the
 // counters on double-buffered masks, overlapped with the next point's masks.
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&s.full[i], 32);   // every gather lane arrives (cp.async.mbarrier)
+      mbar_init(&s.full[i], 1);    // gather lane 0 (after the stage's STS), + TMA bytes
       mbar_init(&s.empty[i], 4);   // released by the 4 mask warps
     }
     for (int i = 0; i < GROUPS; ++i) {
@@ -149,101 +149,126 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   if (warp == 0) {
     // ---------------- gather: rows, ids, dists, norms of one point --------
     // This CTA's points are i = blockIdx.x + k * gridDim.x; their (u, cnt,
-    // off) are loaded 32 at a time (lane j: point k0 + j) and the next
-    // point's candidate ids are prefetched while the current one lands, so
-    // the warp waits on one L2 round trip per batch, not per point.  The
-    // other roles follow the stream published in s.u / s.cnt / s.self.
+    // off, self) are loaded 32 at a time (lane j: point k0 + j).  Software
+    // pipeline, all in registers, so no dependent global round trip sits
+    // between a free stage and its publication:
+    //   point k+2: candidate ids in flight
+    //   point k+1: candidate dists + norms in flight
+    //   point k  : published into a free stage (TMA gather4 rows, STS rest)
+    // Lane l holds candidates 4l..4l+3 (id -1, dist 0, norm 0 past cnt); its
+    // gather4 fetches exactly those rows.  The other roles follow the stream
+    // published in s.u / s.cnt / s.self.
     int stage = 0;
     uint32_t phase = 0;
     const int64_t nb = blockIdx.x < n_rows ? (n_rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     int64_t bu = 0, boff = 0;
-    int bcnt = 0;
+    int bcnt = 0, bself = 0;
     auto load_batch = [&](int64_t k0) {
       const int64_t k = k0 + lane;
       bu = 0;
       bcnt = 0;
       boff = 0;
+      bself = 0;
       if (k < nb) {
         const int64_t i = blockIdx.x + k * gridDim.x;
         bu = row_order ? row_order[i] : i;
         bcnt = cand_counts[bu];
         boff = cand_off[bu];
+        bself = row_node ? row_node[bu] : (int32_t)bu;
       }
     };
-    // lane l holds the ids of candidate rows 4l..4l+3 (-1 past cnt): its
-    // TMA gather4 fetches exactly those rows
-    int32_t pv[4];
-    auto load_ids = [&](int64_t base, int cnt) {
+    struct PM {
+      int64_t u, off;
+      int cnt, self;  // cnt -1: past the stream
+    };
+    auto meta = [&](int64_t j) {
+      PM m{0, 0, -1, 0};
+      if (j < nb) {
+        if ((j & 31) == 0) load_batch(j);
+        const int src = (int)(j & 31);
+        m.u = __shfl_sync(0xffffffffu, bu, src);
+        m.off = __shfl_sync(0xffffffffu, boff, src);
+        m.cnt = __shfl_sync(0xffffffffu, bcnt, src);
+        m.self = __shfl_sync(0xffffffffu, bself, src);
+      }
+      return m;
+    };
+    auto ids_of = [&](const PM &m, int32_t (&o)[4]) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int r = 4 * lane + i;
-        pv[i] = r < cnt ? cand_ids[base + r] : -1;
+        o[i] = (m.cnt <= C && r < m.cnt) ? cand_ids[m.off + r] : -1;
       }
     };
-    if (nb > 0) load_batch(0);
-    int64_t cu = __shfl_sync(0xffffffffu, bu, 0), coff = __shfl_sync(0xffffffffu, boff, 0);
-    int ccnt = __shfl_sync(0xffffffffu, bcnt, 0);
-    if (nb > 0 && ccnt <= C) load_ids(coff, ccnt);
+    auto dn_of = [&](const PM &m, const int32_t (&id)[4], float (&dd)[4], int32_t (&nn)[4]) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = 4 * lane + i;
+        const bool ok = m.cnt <= C && r < m.cnt;
+        dd[i] = ok ? cand_dists[m.off + r] : 0.f;
+        nn[i] = ok ? norms[id[i]] : 0;
+      }
+    };
+    PM m0 = meta(0), m1 = meta(1);
+    int32_t i0[4], i1[4];
+    float d0[4];
+    int32_t n0[4];
+    ids_of(m0, i0);
+    ids_of(m1, i1);
+    dn_of(m0, i0, d0, n0);
     for (int64_t k = 0; k < nb; ++k) {
-      const int64_t u = cu, base = coff;
-      const int cnt = ccnt;
-      int32_t v[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = pv[i];
-      const int64_t k1 = k + 1;
-      if (k1 < nb) {
-        if ((k1 & 31) == 0) load_batch(k1);
-        cu = __shfl_sync(0xffffffffu, bu, (int)(k1 & 31));
-        coff = __shfl_sync(0xffffffffu, boff, (int)(k1 & 31));
-        ccnt = __shfl_sync(0xffffffffu, bcnt, (int)(k1 & 31));
+      const PM m2 = meta(k + 2);
+      int32_t i2[4];
+      ids_of(m2, i2);
+      float d1[4];
+      int32_t n1[4];
+      dn_of(m1, i1, d1, n1);
+      if (m0.cnt > C) {  // hub row: left to the per-warp kernel
+        if (lane == 0) long_rows[atomicAdd(long_count, 1)] = (int32_t)m0.u;
+      } else {
+        GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
+        // candidate rows by TMA gather4 (4 rows of 128 B per instruction,
+        // SW128 applied by the map; lane l's rows land at tile row 4l, i.e.
+        // atom l/2, half l%2).  Rows past cnt keep stale bytes: their Gram
+        // entries feed no mask bit that is ever read (t >= cnt is not
+        // examinable, i >= cnt > t unused).
+        const int ng = (m0.cnt + 3) >> 2;
+        if (lane == 0) mbar_expect_tx_only(&s.full[stage], (uint32_t)ng * 512u);
+        __syncwarp();
+        if (lane < ng) {
+          const int32_t a = i0[0];
+          tma_gather4(s.tile[stage] + (lane >> 1) * 1024 + (lane & 1) * 512, &tmX,
+                      &s.full[stage], 0, a, i0[1] >= 0 ? i0[1] : a, i0[2] >= 0 ? i0[2] : a,
+                      i0[3] >= 0 ? i0[3] : a);
+        }
+        *reinterpret_cast<int4 *>(&s.id[stage][4 * lane]) = make_int4(i0[0], i0[1], i0[2], i0[3]);
+        *reinterpret_cast<float4 *>(&s.dist[stage][4 * lane]) = make_float4(d0[0], d0[1], d0[2], d0[3]);
+        *reinterpret_cast<int4 *>(&s.nrm[stage][4 * lane]) = make_int4(n0[0], n0[1], n0[2], n0[3]);
+        if (lane == 0) {
+          s.u[stage] = m0.u;
+          s.cnt[stage] = m0.cnt;
+          s.self[stage] = m0.self;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s.full[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (cnt > C) {  // hub row: left to the per-warp kernel
-        if (lane == 0) long_rows[atomicAdd(long_count, 1)] = (int32_t)u;
-        if (k1 < nb && ccnt <= C) load_ids(coff, ccnt);
-        continue;
-      }
-      GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
-      // candidate rows by TMA gather4 (4 rows of 128 B per instruction, SW128
-      // applied by the map; the 4 rows of lane l land at tile row 4l, i.e.
-      // atom l/2, half l%2).  Rows past cnt keep stale bytes: their Gram
-      // entries feed no mask bit that is ever read (t >= cnt is not
-      // examinable, i >= cnt > t unused).
-      const int ng = (cnt + 3) >> 2;
-      if (lane == 0) mbar_expect_tx_only(&s.full[stage], (uint32_t)ng * 512u);
-      __syncwarp();
-      if (lane < ng) {
-        const int32_t a = v[0];
-        tma_gather4(s.tile[stage] + (lane >> 1) * 1024 + (lane & 1) * 512, &tmX, &s.full[stage],
-                    0, a, v[1] >= 0 ? v[1] : a, v[2] >= 0 ? v[2] : a, v[3] >= 0 ? v[3] : a);
-      }
-      *reinterpret_cast<int4 *>(&s.id[stage][4 * lane]) = make_int4(v[0], v[1], v[2], v[3]);
+      m0 = m1;
+      m1 = m2;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int r = 4 * lane + i;
-        if (r < cnt) {
-          cp_async4(&s.dist[stage][r], cand_dists + base + r);
-          cp_async4(&s.nrm[stage][r], norms + v[i]);
-        } else {
-          s.dist[stage][r] = 0.f;
-          s.nrm[stage][r] = 0;
-        }
+        i0[i] = i1[i];
+        d0[i] = d1[i];
+        n0[i] = n1[i];
+        i1[i] = i2[i];
       }
-      if (lane == 0) {
-        s.u[stage] = u;
-        s.cnt[stage] = cnt;
-        s.self[stage] = row_node ? row_node[u] : (int32_t)u;
-      }
-      if (k1 < nb && ccnt <= C) load_ids(coff, ccnt);  // next point, in flight meanwhile
-      __syncwarp();
-      cp_async_mbar_arrive(&s.full[stage]);
-      if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
     // end of stream: one sentinel per mask group (each reads every other point)
     for (int g = 0; g < GROUPS; ++g) {
       GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
       if (lane == 0) s.cnt[stage] = g == 0 ? -1 : -2;
       __syncwarp();
-      cp_async_mbar_arrive(&s.full[stage]);
+      if (lane == 0) mbar_arrive(&s.full[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
   } else if (warp == 1) {
