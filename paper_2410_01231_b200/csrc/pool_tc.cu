@@ -537,6 +537,31 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
             const int32_t cidj = perm ? s.pid[tpar][c * 32 + lane] : (int32_t)colj;
             mask &= __ballot_sync(0xffffffffu, colj < n && cidj >= 0);
             if (exclude_self && row >= cb && row < cb + 32) mask &= ~(1u << (int)(row - cb));
+            if (K == 1) {  // nearest neighbour only: the threshold IS the answer
+              // branch-free minimum (dist, id) key over the chunk's survivors
+              uint64_t best = KEY_MAX;
+              const int4 *pp = reinterpret_cast<const int4 *>(s.pid[tpar] + c * 32);
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                const int4 w = nyp[v];
+                const int4 pd = perm ? pp[v] : make_int4((int)(cb + 4 * v), (int)(cb + 4 * v + 1),
+                                                         (int)(cb + 4 * v + 2), (int)(cb + 4 * v + 3));
+                const int wv[4] = {w.x, w.y, w.z, w.w};
+                const int pv[4] = {pd.x, pd.y, pd.z, pd.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int j = 4 * v + e;
+                  const uint64_t key = ((uint64_t)(uint32_t)(wv[e] - 2 * (int)r[j] + nx) << 32) |
+                                       (uint32_t)pv[e];
+                  best = ((mask >> j) & 1u) && key < best ? key : best;
+                }
+              }
+              if (best < tau) {
+                tau = best;
+                tp = tau_prefilter(tau, nx);
+              }
+              continue;
+            }
             const bool track = K > 1 && tau == KEY_MAX && mask;
             if (mask) {
 #pragma unroll
@@ -553,20 +578,6 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
             __syncwarp();
             if (track) {  // rare: rows still without a threshold
               for (unsigned mm = mask; mm; mm &= mm - 1) smax = max(smax, sv[__ffs(mm) - 1]);
-            }
-            if (K == 1) {  // nearest neighbour only: the threshold IS the answer
-              while (mask) {
-                const int j = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const uint64_t key = ((uint64_t)(uint32_t)(sv[j] + nx) << 32) |
-                                     (uint32_t)(perm ? s.pid[tpar][c * 32 + j] : (int32_t)(cb + j));
-                if (key < tau) {
-                  tau = key;
-                  tp = tau_prefilter(tau, nx);
-                }
-              }
-              __syncwarp();
-              continue;
             }
             // room for this chunk's survivors in every row of the warp
             unsigned need = __ballot_sync(0xffffffffu, cnt + __popc(mask) > CAP);
