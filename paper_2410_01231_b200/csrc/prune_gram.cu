@@ -463,17 +463,29 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         }
         kept_m[c] = km;
       }
-      // the kept candidates in scan order, written once, coalesced
+      // the kept candidates in scan order, staged in this point's (already
+      // register-resident) candidate buffer, then written as whole padded
+      // rows: one fully coalesced store sequence per row (whole 128-byte
+      // lines also when the output is pinned host memory)
       {
+        int32_t *oid = s.gid[mb];
+        float *od = s.gdist[mb];
+        __syncwarp();
         int base = 0;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           if ((kept_m[c] >> lane) & 1u) {
             const int pos = base + __popc(kept_m[c] & lanemask_lt());
-            out_ids[u * width + pos] = idv[c];
-            out_dists[u * width + pos] = dsv[c];
+            oid[pos] = idv[c];
+            od[pos] = dsv[c];
           }
           base += __popc(kept_m[c]);
+        }
+        __syncwarp();
+        for (int j = lane; j < width; j += 32) {
+          const bool k = j < kept;
+          out_ids[u * width + j] = k ? oid[j] : -1;
+          out_dists[u * width + j] = k ? od[j] : __int_as_float(0x7f800000);
         }
       }
       // ---- exact lazy counters of every examined candidate ----
@@ -520,10 +532,6 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       for (int o = 16; o > 0; o >>= 1) {
         dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
         if (STRATEGY == 1) asum += __shfl_xor_sync(0xffffffffu, asum, o);
-      }
-      for (int j = kept + lane; j < width; j += 32) {
-        out_ids[u * width + j] = -1;
-        out_dists[u * width + j] = __int_as_float(0x7f800000);
       }
       if (lane == 0) {
         dist_evals[u] = dsum;

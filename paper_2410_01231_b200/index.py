@@ -74,9 +74,25 @@ class RngBuilder:
                                           _lib.ptr(norms), _lib.stream_handle()))
         return self.u8_out
 
-    def build(self, X: torch.Tensor) -> BuildOutput:
-        """Enqueue the whole path on the current stream (no host sync)."""
+    def build(self, X: torch.Tensor, host_out=None) -> BuildOutput:
+        """Enqueue the whole path on the current stream (no host sync).
+
+        host_out: optional (ids, counts) pinned host tensors ((n, R) and (n,)
+        int32).  The final re-prune kernel then writes the adjacency rows
+        straight into `ids` over PCIe (pinned memory is device-addressable
+        under UVA; whole 128-byte rows per store sequence), so that transfer
+        overlaps the kernel instead of following it; the degrees follow with
+        one 4-byte-per-row copy.  Both are complete once the stream reaches
+        the end of the build."""
         p = self.params
+        b_out = self.b_out
+        if host_out is not None:
+            h_ids, h_cnt = host_out
+            for t, shape in ((h_ids, (self.n, p.M)), (h_cnt, (self.n,))):
+                if t.device.type != "cpu" or not t.is_pinned() or t.dtype != torch.int32 \
+                        or tuple(t.shape) != shape or not t.is_contiguous():
+                    raise ValueError(f"host_out tensors must be pinned contiguous int32 {shape}")
+            b_out = (h_ids,) + b_out[1:]
         ids, dists = self.pools(X)
         u8 = self.u8_rows(X)
         order = self.order()
@@ -84,8 +100,10 @@ class RngBuilder:
                                 p.strategy_code, p.kernel_param, p.M, p.M, out=self.a_out, u8=u8,
                                 order=order, ws=self.prune_ws)
         b = kernels.add_reverse_and_prune(X, a[0], a[1], a[2], p.strategy_code, p.kernel_param,
-                                          p.M, p.M, ws=self.rev_ws, out=self.b_out, u8=u8,
+                                          p.M, p.M, ws=self.rev_ws, out=b_out, u8=u8,
                                           order=order)
+        if host_out is not None:
+            host_out[1].copy_(b[2], non_blocking=True)
         de = torch.stack([a[3].sum(), b[3].sum()])
         ae = torch.stack([a[4].sum(), b[4].sum()])
         return BuildOutput(b[0], b[1], b[2], a[2], de, ae)

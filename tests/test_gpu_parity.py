@@ -247,6 +247,23 @@ def test_device_resident_api_keeps_tensors_on_gpu():
     assert a[0].is_cuda and int(a[3]) > 0
 
 
+def test_builder_host_outputs_equal_device_outputs():
+    """RngBuilder.build(host_out=...): the final kernel writes adjacency and
+    degrees straight into pinned host memory; identical to the device build."""
+    from paper_2410_01231_b200.index import RngBuilder, pool_mode
+    X = torch.from_numpy(synth.cfg2(20000)).cuda()
+    b = RngBuilder(20000, 128, 64, PruneParams(M=24), pool_mode(X))
+    dev = b.build(X)
+    ids, cnt = dev.ids.cpu(), dev.counts.cpu()
+    h_ids = torch.full((20000, 24), 7, dtype=torch.int32).pin_memory()
+    h_cnt = torch.zeros(20000, dtype=torch.int32).pin_memory()
+    b.build(X, host_out=(h_ids, h_cnt))
+    torch.cuda.synchronize()
+    assert torch.equal(h_ids, ids) and torch.equal(h_cnt, cnt)
+    with pytest.raises(ValueError):
+        b.build(X, host_out=(torch.zeros((20000, 24), dtype=torch.int32), h_cnt))
+
+
 @pytest.mark.parametrize("strategy,alpha", [("rng", 60.0), ("alpha", 66.0)])
 def test_exact_integer_selection_equals_fp32_path(strategy, alpha):
     """Integer-valued [0,255] data: the u8 dp4a selection path (pgk_prune_rows_ex
