@@ -153,6 +153,15 @@ int pgk_knn_pools(const float *data, int64_t n, int64_t d,
                   int mode, int32_t *gt_ids, int32_t *pool_ids,
                   float *pool_dists, void *ws, size_t ws_bytes, void *stream);
 
+/* pgk_knn_pools for the self pool (queries == data, exclude_self, mode
+ * PGK_POOL_U8) from the caller's exact-integer copy: data_u8 (n rows of 128
+ * bytes) and norms (int32 squared norms), as pgk_make_u8 writes them, so the
+ * pool does not convert `data` again.  The caller guarantees (e.g. by
+ * pgk_detect_u8) that every value of `data` is an integer in [0, 255] and d <= 128. */
+int pgk_knn_pools_u8(const float *data, const uint8_t *data_u8, const int32_t *norms, int64_t n,
+                     int64_t d, int64_t k, int32_t *gt_ids, int32_t *pool_ids, float *pool_dists,
+                     void *ws, size_t ws_bytes, void *stream);
+
 /* Number of query rows that needed the exact float64 fallback scan in the most
  * recent pgk_knn_pools call on this workspace (device int32 inside ws; this
  * helper performs a blocking read). */

@@ -68,7 +68,8 @@ int add_reverse_and_prune(const float *, const uint8_t *, const int32_t *, const
                           size_t, cudaStream_t);
 int knn_workspace(int64_t, int64_t, int64_t, int64_t, int, size_t *);
 int knn_pools(const float *, int64_t, int64_t, const float *, int64_t, int64_t, int, int,
-              int32_t *, int32_t *, float *, void *, size_t, cudaStream_t);
+              int32_t *, int32_t *, float *, void *, size_t, cudaStream_t,
+              const uint8_t *xu8_in = nullptr, const int32_t *norms_in = nullptr);
 int detect_u8(const float *, int64_t, int64_t, int *, void *, size_t, cudaStream_t);
 int fallback_rows(const void *, int *, cudaStream_t);
 int knn_work(const void *, int64_t, int64_t, int64_t, int64_t, int, unsigned long long *,
@@ -222,6 +223,15 @@ int pgk_knn_pools(const float *data, int64_t n, int64_t d, const float *queries,
   PGK_REQUIRE(data && pool_ids && pool_dists && ws, "NULL argument");
   return knn_pools(data, n, d, queries, nq, k, exclude_self, mode, gt_ids, pool_ids,
                    pool_dists, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int pgk_knn_pools_u8(const float *data, const uint8_t *data_u8, const int32_t *norms, int64_t n,
+                     int64_t d, int64_t k, int32_t *gt_ids, int32_t *pool_ids, float *pool_dists,
+                     void *ws, size_t ws_bytes, void *stream) {
+  PGK_REQUIRE(data && data_u8 && norms && pool_ids && pool_dists && ws, "NULL argument");
+  PGK_REQUIRE(d <= 128, "exact-integer rows need d <= 128");
+  return knn_pools(data, n, d, nullptr, n, k, 1, PGK_POOL_U8, gt_ids, pool_ids, pool_dists, ws,
+                   ws_bytes, (cudaStream_t)stream, data_u8, norms);
 }
 
 int pgk_knn_work(const void *ws, int64_t n, int64_t nq, int64_t d, int64_t k, int mode,

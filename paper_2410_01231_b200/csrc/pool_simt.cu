@@ -698,15 +698,20 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             const uint64_t *init_keys = nullptr, int kth_only = 0,
                             float shrink = 1.0f, int32_t *fail_blocks = nullptr,
                             const PoolOut *out = nullptr, uint8_t *fail_rows = nullptr,
-                            const uint8_t *row_mask = nullptr);
+                            const uint8_t *row_mask = nullptr, const uint8_t *qu8_in = nullptr);
 int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm, int K,
                          uint64_t *keys, void *tc_ws, size_t tc_bytes, void *tws,
                          size_t tws_bytes, cudaStream_t stream, bool *handled,
-                         unsigned long long *pairs_out, const PoolOut *out);
+                         unsigned long long *pairs_out, const PoolOut *out,
+                         const uint8_t *xu8_in);
 
+// xu8_in / norms_in (optional, U8 mode with queries == data): the caller's
+// exact-integer rows (128 B each) and squared norms (pgk_make_u8), used
+// instead of converting X again.
 int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, int64_t k,
               int exclude_self, int mode, int32_t *gt_ids, int32_t *pool_ids,
-              float *pool_dists, void *ws, size_t bytes, cudaStream_t stream) {
+              float *pool_dists, void *ws, size_t bytes, cudaStream_t stream,
+              const uint8_t *xu8_in, const int32_t *norms_in) {
   PGK_REQUIRE(k >= 1, "k must be >= 1");
   PGK_REQUIRE(n >= 1 && d >= 1, "dataset must be non-empty");
   const bool self = (Q == nullptr);
@@ -745,8 +750,13 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
   PGK_CUDA(cudaMemsetAsync(L.fb_count, 0, sizeof(int32_t), stream));
   int rc;
   if (mode == PGK_POOL_U8) {
-    norms_u8_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(X, n, (int)d, L.xnorm);
-    PGK_CHECK_LAUNCH("norms_u8_kernel");
+    if (!self || d > 128) xu8_in = nullptr, norms_in = nullptr;
+    if (norms_in) {
+      PGK_CUDA(cudaMemcpyAsync(L.xnorm, norms_in, (size_t)n * 4, cudaMemcpyDeviceToDevice, stream));
+    } else {
+      norms_u8_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(X, n, (int)d, L.xnorm);
+      PGK_CHECK_LAUNCH("norms_u8_kernel");
+    }
     const int32_t *qn = L.xnorm;
     if (!self) {
       norms_u8_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(Q, nq, (int)d, L.qnorm);
@@ -758,7 +768,7 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
     const PoolOut po{gt_ids, pool_ids, pool_dists};
     if (L.tc_ws && L.tws && self && exclude_self) {
       rc = launch_pool_tiles_u8(X, n, (int)d, L.xnorm, (int)k, L.keys, L.tc_ws, L.tc_bytes,
-                                L.tws, L.tws_bytes, stream, &handled, nullptr, &po);
+                                L.tws, L.tws_bytes, stream, &handled, nullptr, &po, xu8_in);
       if (rc) return rc;
     }
     if (L.tc_ws && !handled) {

@@ -1126,7 +1126,8 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             const int32_t *tlist, const int32_t *tlen, int64_t tstride,
                             const int32_t *perm, bool *handled, const uint64_t *init_keys,
                             int kth_only, float shrink, int32_t *fail_blocks,
-                            const PoolOut *out, uint8_t *fail_rows, const uint8_t *row_mask) {
+                            const PoolOut *out, uint8_t *fail_rows, const uint8_t *row_mask,
+                            const uint8_t *qu8_in) {
   *handled = false;
   if (shrink < 1.0f && (!fail_blocks || !fail_rows)) {
     set_error("guessed thresholds need a fail-block array");
@@ -1154,7 +1155,9 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
     tc::to_u8_kernel<<<cg, 256, 0, stream>>>(X, n, d, xu8);
     PGK_CHECK_LAUNCH("to_u8_kernel");
   }
-  if (!self) {
+  if (!self && qu8_in) {
+    qu8 = const_cast<uint8_t *>(qu8_in);  // the caller's u8 rows (128 B each)
+  } else if (!self) {
     tc::to_u8_kernel<<<cg, 256, 0, stream>>>(Q, nq, d, qu8);
     PGK_CHECK_LAUNCH("to_u8_kernel");
   }

@@ -102,6 +102,7 @@ __global__ void gather_sorted_kernel(const float *__restrict__ X, int d,
                                      const int32_t *__restrict__ perm,
                                      const int32_t *__restrict__ xnorm, int64_t np,
                                      uint8_t *__restrict__ xs, int32_t *__restrict__ ns) {
+  // (from fp32 rows; gather_sorted_u8_kernel below copies existing u8 rows)
   const int64_t total = np * 128;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -109,6 +110,23 @@ __global__ void gather_sorted_kernel(const float *__restrict__ X, int d,
     const int c = (int)(e & 127);
     const int32_t src = perm[r];
     xs[e] = (src >= 0 && c < d) ? (uint8_t)__float2int_rn(X[(int64_t)src * d + c]) : (uint8_t)0;
+    if (c == 0) ns[r] = src >= 0 ? xnorm[src] : 0x3f3f3f3f;
+  }
+}
+
+// the same from the caller's u8 rows (128 B each): 16-byte copies
+__global__ void gather_sorted_u8_kernel(const uint8_t *__restrict__ xu8,
+                                        const int32_t *__restrict__ perm,
+                                        const int32_t *__restrict__ xnorm, int64_t np,
+                                        uint8_t *__restrict__ xs, int32_t *__restrict__ ns) {
+  const int64_t total = np * 8;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e >> 3;
+    const int c = (int)(e & 7);
+    const int32_t src = perm[r];
+    reinterpret_cast<uint4 *>(xs)[e] =
+        src >= 0 ? reinterpret_cast<const uint4 *>(xu8)[(int64_t)src * 8 + c] : make_uint4(0, 0, 0, 0);
     if (c == 0) ns[r] = src >= 0 ? xnorm[src] : 0x3f3f3f3f;
   }
 }
@@ -361,7 +379,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             const uint64_t *init_keys = nullptr, int kth_only = 0,
                             float shrink = 1.0f, int32_t *fail_blocks = nullptr,
                             const PoolOut *out = nullptr, uint8_t *fail_rows = nullptr,
-                            const uint8_t *row_mask = nullptr);
+                            const uint8_t *row_mask = nullptr, const uint8_t *qu8_in = nullptr);
 
 static tiles::Layout tiles_layout(void *ws, size_t bytes, int64_t n, int64_t d) {
   using namespace tiles;
@@ -421,7 +439,8 @@ extern uint32_t *g_dense_ostat;
 int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm, int K,
                          uint64_t *keys, void *tc_ws, size_t tc_bytes, void *tws,
                          size_t tws_bytes, cudaStream_t stream, bool *handled,
-                         unsigned long long *pairs_out, const PoolOut *out) {
+                         unsigned long long *pairs_out, const PoolOut *out,
+                         const uint8_t *xu8_in) {
   using namespace tiles;
   *handled = false;
   if (!tiles_supported(n, d, K)) return PGK_OK;
@@ -441,7 +460,8 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   if (rc) return rc;
   bool h = false;
   rc = launch_pool_tc_u8_lists(L.cen, C, d, X, n, 0, L.cnorm, xnorm, 1, L.akeys, L.sub_ws,
-                               L.sub_bytes, stream, nullptr, nullptr, nullptr, 0, nullptr, &h);
+                               L.sub_bytes, stream, nullptr, nullptr, nullptr, 0, nullptr, &h,
+                               nullptr, 0, 1.0f, nullptr, nullptr, nullptr, nullptr, xu8_in);
   if (rc) return rc;
   dbg_stage("assign tc", stream);
   if (!h) return PGK_OK;
@@ -465,8 +485,13 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   dbg_stage("assign_scatter_kernel", stream);
   const int64_t NP = L.NPmax, T = L.Tmax;
   // 3. sorted u8 rows / norms, tile summaries, centroid distances
-  gather_sorted_kernel<<<g, 256, 0, stream>>>(X, d, L.perm, xnorm, NP, L.xs, L.ns);
-  PGK_CHECK_LAUNCH("gather_sorted_kernel");
+  if (xu8_in) {
+    gather_sorted_u8_kernel<<<g, 256, 0, stream>>>(xu8_in, L.perm, xnorm, NP, L.xs, L.ns);
+    PGK_CHECK_LAUNCH("gather_sorted_u8_kernel");
+  } else {
+    gather_sorted_kernel<<<g, 256, 0, stream>>>(X, d, L.perm, xnorm, NP, L.xs, L.ns);
+    PGK_CHECK_LAUNCH("gather_sorted_kernel");
+  }
   dbg_stage("gather_sorted_kernel", stream);
   fill_i32_kernel<<<1, 128, 0, stream>>>(L.ns + NP, 128, 0x3f3f3f3f);
   PGK_CHECK_LAUNCH("fill_i32_kernel");

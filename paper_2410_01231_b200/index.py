@@ -60,9 +60,9 @@ class RngBuilder:
         return kernels.knn_order(self.pool_ws, self.n, self.d, self.K, self.mode,
                                  self.order_out)
 
-    def pools(self, X: torch.Tensor):
+    def pools(self, X: torch.Tensor, u8=None):
         r = kernels.knn_pools(X, self.K, None, True, self.mode, False, self.pool_ws,
-                              self.pool_out)
+                              self.pool_out, u8=u8)
         return r.pool_ids, r.pool_dists
 
     def u8_rows(self, X: torch.Tensor):
@@ -93,8 +93,8 @@ class RngBuilder:
                         or tuple(t.shape) != shape or not t.is_contiguous():
                     raise ValueError(f"host_out tensors must be pinned contiguous int32 {shape}")
             b_out = (h_ids,) + b_out[1:]
-        ids, dists = self.pools(X)
-        u8 = self.u8_rows(X)
+        u8 = self.u8_rows(X)  # exact-integer rows once, for the pool and the selection
+        ids, dists = self.pools(X, u8)
         order = self.order()
         a = kernels.prune_batch(X, self.cand_off, self.cand_counts, ids, dists,
                                 p.strategy_code, p.kernel_param, p.M, p.M, out=self.a_out, u8=u8,

@@ -99,3 +99,17 @@ def test_tile_pruned_pool_equals_full_scan(gen_code, K):
     rows = np.random.default_rng(1).choice(len(data), 150, replace=False)
     o_ids, o_d = oracle.knn_pools(data, K, rows)
     np.testing.assert_array_equal(ids[rows], o_ids)
+
+
+@pytest.mark.parametrize("n,d,K", [(30000, 128, 128), (12000, 100, 64)])
+def test_pool_from_callers_u8_rows_equals_fp32_input(n, d, K):
+    """pgk_knn_pools_u8 (the caller's make_u8 rows and norms feed the center
+    assignment and the tile gather) equals pgk_knn_pools on the fp32 rows."""
+    import torch
+    from paper_2410_01231_b200 import _lib, kernels
+    rng = np.random.default_rng(7)
+    data = synth.cfg2(n) if d == 128 else rng.integers(0, 256, (n, d)).astype(np.float32)
+    X = torch.from_numpy(data).cuda()
+    a = kernels.knn_pools(X, K, mode=_lib.POOL_U8, want_gt=False)
+    b = kernels.knn_pools(X, K, mode=_lib.POOL_U8, want_gt=False, u8=kernels.make_u8(X))
+    assert torch.equal(a.pool_ids, b.pool_ids) and torch.equal(a.pool_dists, b.pool_dists)

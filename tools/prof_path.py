@@ -38,9 +38,9 @@ def main():
             prof = torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA])
             prof.__enter__()
         t0 = time.perf_counter()
-        if a.stage in ("pool", "all"):
-            ids, d = b.pools(X)
         u8 = b.u8_rows(X)
+        if a.stage in ("pool", "all"):
+            ids, d = b.pools(X, u8)
         order = b.order()
         if a.stage in ("prune", "all"):
             r = kernels.prune_batch(X, b.cand_off, b.cand_counts, ids, d, p.strategy_code,
