@@ -266,7 +266,8 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
                       int64_t tstride, const int32_t *__restrict__ perm,
                       const uint64_t *__restrict__ init_keys, float shrink,
                       int32_t *__restrict__ row_cnt, uint64_t *__restrict__ row_tau,
-                      int32_t *__restrict__ sched, const uint8_t *__restrict__ row_mask) {
+                      int32_t *__restrict__ sched, const uint8_t *__restrict__ row_mask,
+                      int k1_direct) {
   unsigned long long st[ST_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t_prev = STATS ? clock64() : 0;
 #define PGK_TICK(slot)                          \
@@ -632,6 +633,13 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
       if (row < nq) {
         row_cnt[row] = row_ok ? (cnt | (guessed ? GUESSED : 0)) : -1;
         row_tau[row] = tau;
+        // K == 1: the threshold is the answer; each lane writes its own row
+        // (no finalize pass)
+        if (K == 1 && k1_direct && row_ok) {
+          const int64_t orow = perm ? (int64_t)perm[row] : row;
+          out_keys[orow] =
+              tau == KEY_MAX ? KEY_MAX : pack_key((float)khi(tau), (int32_t)(uint32_t)tau);
+        }
       }
       PGK_TICK(ST_FINAL);
     }
@@ -1188,10 +1196,12 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   // pass-1 bounds over tile lists: dense distances + exact K-th selection
   const bool dense = kth_only && K > 1 && tlist;
   const char *se = getenv("PGK_TC_STATS");
+  // K == 1 into keys (not the pool arrays): the epilogue writes the answer
+  const int k1_direct = (K == 1 && !(out && !kth_only)) ? 1 : 0;
   if (dense) {
     tc::tc_pool_u8_kernel<false, true><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
-        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask);
+        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, 0);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel<dense>");
     const unsigned fgrid =
         (unsigned)std::min<int64_t>((nq + tc::FIN_WARPS - 1) / tc::FIN_WARPS, (int64_t)sms * 8);
@@ -1207,7 +1217,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
     PGK_CUDA(cudaMemsetAsync(dstats, 0, sizeof(unsigned long long) * tc::ST_COUNT, stream));
     tc::tc_pool_u8_kernel<true, false><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, dstats, tlist, tlen,
-        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask);
+        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, 0);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel<stats>");
     unsigned long long h[tc::ST_COUNT];
     PGK_CUDA(cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, stream));
@@ -1222,8 +1232,12 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   } else {
     tc::tc_pool_u8_kernel<false, false><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
-        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask);
+        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, k1_direct);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel");
+    if (k1_direct) {
+      *handled = true;
+      return PGK_OK;
+    }
   }
   tc::FinOut fo{nullptr, nullptr, nullptr};
   if (out && !kth_only) fo = tc::FinOut{out->gt_ids, out->ids, out->dists};
