@@ -433,6 +433,175 @@ __global__ void __launch_bounds__(RR_WARPS * 32)
   }
 }
 
+// F32 mode pass 2, staged (d % 4 == 0, 16-byte aligned rows): one pass over
+// the S survivors' rows computes, per candidate (one lane each), both the
+// oracle's float64 sequential distance (t = (double)x - (double)q; acc +=
+// t*t, index order, no FMA: bit-identical to the restatement's ranking) and
+// the reference's fp32 squared_l2 chain for the list distance.  Rows are
+// staged 32 dimensions at a time through shared memory by cp.async, 8 lanes
+// per row (coalesced), double-buffered; rows are read once instead of twice
+// (float64 pass + fp32 pass of the selected K).
+constexpr int RS_WARPS = 4;
+constexpr int RS_DC = 32;
+constexpr int RS_ROW = RS_DC + 4;  // staged row stride (floats): LDS.128 conflict-free
+
+struct RerankSmem {
+  double d[RS_WARPS][RR_MAXS];
+  int32_t id[RS_WARPS][RR_MAXS];
+  float f[RS_WARPS][RR_MAXS];
+  uint64_t key[RS_WARPS][RR_MAXS];
+  double qd[RS_WARPS][2][RS_DC];                         // the query chunk as doubles
+  alignas(16) float stage[RS_WARPS][2][32 * RS_ROW];    // 32 candidate rows x 2 chunks
+};
+
+__device__ __forceinline__ void rs_cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
+// (d64, id) pairs with an fp32 payload, ascending by (d64, id)
+__device__ __forceinline__ void warp_bitonic_sort_triples(double *d, int32_t *id, float *f,
+                                                          int size, int lane) {
+  for (int k = 2; k <= size; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < size; i += 32) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const double da = d[i], db = d[ixj];
+          const int32_t ia = id[i], ib = id[ixj];
+          const bool up = (i & k) == 0;
+          if (pair_gt(da, ia, db, ib) == up) {
+            d[i] = db; d[ixj] = da; id[i] = ib; id[ixj] = ia;
+            const float t = f[i]; f[i] = f[ixj]; f[ixj] = t;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(RS_WARPS * 32)
+    rerank_staged_kernel(const float *__restrict__ X, int d, const float *__restrict__ Q,
+                         int64_t nq, const uint64_t *__restrict__ keys, int S, int K,
+                         double gamma, int32_t *__restrict__ gt_ids,
+                         int32_t *__restrict__ pool_ids, float *__restrict__ pool_dists,
+                         int32_t *__restrict__ fb_list, int32_t *__restrict__ fb_count,
+                         const int32_t *__restrict__ order) {
+  extern __shared__ __align__(16) unsigned char rs_raw[];
+  RerankSmem &sm = *reinterpret_cast<RerankSmem *>(rs_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double *s_d = sm.d[warp];
+  int32_t *s_id = sm.id[warp];
+  float *s_f = sm.f[warp];
+  uint64_t *s_key = sm.key[warp];
+  const int S2 = next_pow2(S), K2 = next_pow2(K);
+  const int l8 = lane & 7, rsub = lane >> 3;
+  for (int64_t ri = (int64_t)blockIdx.x * RS_WARPS + warp; ri < nq;
+       ri += (int64_t)gridDim.x * RS_WARPS) {
+    const int64_t r = order ? (int64_t)order[ri] : ri;
+    const float *q = Q + r * d;
+    __syncwarp();
+    for (int j = lane; j < S2; j += 32) {
+      const uint64_t k = j < S ? keys[r * S + j] : KEY_MAX;
+      s_id[j] = k != KEY_MAX ? key_id(k) : 0x7fffffff;
+      s_d[j] = __longlong_as_double(0x7ff0000000000000ll);
+      s_f[j] = __int_as_float(0x7f800000);
+    }
+    __syncwarp();
+    for (int b0 = 0; b0 < S; b0 += 32) {
+      const int nb = min(32, S - b0);
+      const int32_t v = lane < nb ? s_id[b0 + lane] : 0x7fffffff;
+      const bool act = v != 0x7fffffff;
+      // stage chunk c0 of the batch's rows (8 lanes per row, 4 rows per
+      // instruction) and the query chunk as doubles
+      auto issue = [&](int c0, int buf) {
+        float *st = sm.stage[warp][buf];
+#pragma unroll
+        for (int e0 = 0; e0 < 32; e0 += 4) {
+          const int e = e0 + rsub;
+          const int32_t ve = __shfl_sync(0xffffffffu, v, e);
+          if (ve != 0x7fffffff && c0 + 4 * l8 < d)
+            rs_cp_async16(st + e * RS_ROW + 4 * l8, X + (int64_t)ve * d + c0 + 4 * l8);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (c0 + lane < d) sm.qd[warp][buf][lane] = (double)__ldg(q + c0 + lane);
+      };
+      double a64 = 0.0;
+      float a32 = 0.0f;
+      __syncwarp();
+      issue(0, 0);
+      int cur = 0;
+      for (int c0 = 0; c0 < d; c0 += RS_DC) {
+        if (c0 + RS_DC < d) {
+          issue(c0 + RS_DC, cur ^ 1);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncwarp();
+        if (act) {
+          const int dc = min(RS_DC, d - c0);
+          const float *srow = sm.stage[warp][cur] + lane * RS_ROW;
+          const double *qd = sm.qd[warp][cur];
+          const float *qf = q + c0;
+#pragma unroll 4
+          for (int k = 0; k < dc; k += 4) {
+            const float4 x = *reinterpret_cast<const float4 *>(srow + k);
+            const float4 y = __ldg(reinterpret_cast<const float4 *>(qf + k));
+            a32 = sq_step(a32, x.x, y.x);  // squared_l2(candidate, query) as write_pool_row
+            a32 = sq_step(a32, x.y, y.y);
+            a32 = sq_step(a32, x.z, y.z);
+            a32 = sq_step(a32, x.w, y.w);
+            double t;
+            t = __dsub_rn((double)x.x, qd[k]);     a64 = __dadd_rn(a64, __dmul_rn(t, t));
+            t = __dsub_rn((double)x.y, qd[k + 1]); a64 = __dadd_rn(a64, __dmul_rn(t, t));
+            t = __dsub_rn((double)x.z, qd[k + 2]); a64 = __dadd_rn(a64, __dmul_rn(t, t));
+            t = __dsub_rn((double)x.w, qd[k + 3]); a64 = __dadd_rn(a64, __dmul_rn(t, t));
+          }
+        }
+        __syncwarp();
+        cur ^= 1;
+      }
+      if (act) {
+        s_d[b0 + lane] = a64;
+        s_f[b0 + lane] = a32;
+      }
+    }
+    __syncwarp();
+    warp_bitonic_sort_triples(s_d, s_id, s_f, S2, lane);
+    const uint64_t klast = keys[r * S + S - 1];
+    bool safe = true;
+    if (klast != KEY_MAX) {
+      // every non-survivor has approx >= approx_S, hence true distance
+      // >= approx_S / (1 + gamma); its float64 value is within 1e-12 of that
+      const double lb = (double)key_dist(klast) / (1.0 + gamma) * (1.0 - 1e-12);
+      safe = s_d[K - 1] < lb;
+    }
+    if (!safe) {
+      if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = (int32_t)r;
+      continue;
+    }
+    // the K members in (float64 dist, id) order; the list re-sorted by its
+    // fp32 distances (ties by id)
+    for (int j = lane; j < K2; j += 32) {
+      const int32_t v = j < K ? s_id[j] : 0x7fffffff;
+      if (j < K && gt_ids) gt_ids[r * K + j] = v == 0x7fffffff ? -1 : v;
+      s_key[j] = v == 0x7fffffff ? KEY_MAX : pack_key(s_f[j], v);
+    }
+    __syncwarp();
+    warp_bitonic_sort(s_key, K2, lane);
+    for (int j = lane; j < K; j += 32) {
+      const uint64_t k = s_key[j];
+      pool_ids[r * K + j] = k == KEY_MAX ? -1 : key_id(k);
+      pool_dists[r * K + j] = k == KEY_MAX ? __int_as_float(0x7f800000) : key_dist(k);
+    }
+    __syncwarp();
+  }
+}
+
 // Exact float64 full scan for rows whose boundary proof failed.  One CTA per
 // listed row: 256 columns per round, survivors of the (d64, id) threshold are
 // appended to a shared buffer that is block-sorted when it could overflow.
@@ -813,11 +982,32 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
   const double gamma = (double)(d + 2) * 5.9604644775390625e-08 * 1.001 + 1e-12;
   const unsigned rgrid =
       (unsigned)std::min<int64_t>((nq + RR_WARPS - 1) / RR_WARPS, (int64_t)sms * 16);
-  rerank_kernel<<<rgrid, RR_WARPS * 32, 0, stream>>>(X, (int)d, Q, nq, L.keys, S, (int)k,
-                                                     gamma, vec4, gt_ids, pool_ids,
-                                                     pool_dists, L.fb_list, L.fb_count,
-                                                     pruned ? L.order : nullptr);
-  PGK_CHECK_LAUNCH("rerank_kernel");
+  static int staged_env = -1;
+  if (staged_env < 0) {
+    const char *e = getenv("PGK_RERANK_STAGED");
+    staged_env = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (vec4 && staged_env) {
+    const size_t rsm = sizeof(RerankSmem);
+    static bool attr = false;
+    if (!attr) {
+      PGK_CUDA(cudaFuncSetAttribute(rerank_staged_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+      attr = true;
+    }
+    const unsigned sgrid =
+        (unsigned)std::min<int64_t>((nq + RS_WARPS - 1) / RS_WARPS, (int64_t)sms * 8);
+    rerank_staged_kernel<<<sgrid, RS_WARPS * 32, rsm, stream>>>(
+        X, (int)d, Q, nq, L.keys, S, (int)k, gamma, gt_ids, pool_ids, pool_dists, L.fb_list,
+        L.fb_count, pruned ? L.order : nullptr);
+    PGK_CHECK_LAUNCH("rerank_staged_kernel");
+  } else {
+    rerank_kernel<<<rgrid, RR_WARPS * 32, 0, stream>>>(X, (int)d, Q, nq, L.keys, S, (int)k,
+                                                       gamma, vec4, gt_ids, pool_ids,
+                                                       pool_dists, L.fb_list, L.fb_count,
+                                                       pruned ? L.order : nullptr);
+    PGK_CHECK_LAUNCH("rerank_kernel");
+  }
   fallback_kernel<<<(unsigned)sms * 2, FB_THREADS, 0, stream>>>(
       X, n, (int)d, Q, exclude_self, (int)k, vec4, L.fb_list, L.fb_count, gt_ids, pool_ids,
       pool_dists);
