@@ -189,6 +189,182 @@ __device__ __forceinline__ int test_round(
   return new_n;
 }
 
+// Speculative in-window rounds (MODE 1, fp32 rows).  The next kept
+// neighbours can only be the first alive entries, so one staged pass over the
+// alive rows computes every alive entry's distance to each of the first SPEC
+// alive entries (SPEC independent sequential fp32 chains per lane: bit-
+// identical values, SPEC x fewer row reads, SPEC-way ILP), and the rounds are
+// then resolved in order from registers.  A distance is counted (s_de / s_ae)
+// only when its round happens, i.e. for kept neighbours, so verdicts, the kept
+// set and the lazy counters are exactly the sequential rounds'.  Returns the
+// new alive count; kept / stop / stop_j are updated as the caller's loop does.
+constexpr int SPEC = 4;
+constexpr int SB = PRUNE_W / 32;
+
+__device__ __forceinline__ int spec_block(const float *__restrict__ X, int d, int strategy,
+                                          double cos_alpha, int n_alive, int32_t *s_id,
+                                          float *s_dist, int32_t *s_de, int32_t *s_ae,
+                                          int16_t *s_alive, float *stage, int32_t *orow,
+                                          float *odrow, int &kept, int M, bool &stop,
+                                          int &stop_j, int lane) {
+  const int nw = min(SPEC, n_alive);
+  int32_t wid[SPEC];
+  float wdu[SPEC];
+#pragma unroll
+  for (int i = 0; i < SPEC; ++i) {
+    const int e = s_alive[i < nw ? i : 0];
+    wid[i] = s_id[e];
+    wdu[i] = s_dist[e];
+  }
+  float dr[SB][SPEC];
+  const int l8 = lane & 7, rsub = lane >> 3;
+#pragma unroll
+  for (int b = 0; b < SB; ++b) {
+#pragma unroll
+    for (int i = 0; i < SPEC; ++i) dr[b][i] = 0.0f;
+    const int base = b * 32;
+    if (base >= n_alive) continue;
+    const int nb = min(32, n_alive - base);
+    const bool act = lane < nb;
+    const int32_t v = s_id[s_alive[act ? base + lane : base]];
+    auto issue = [&](int c0, float *buf) {
+      const int dc = min(DC, d - c0);
+#pragma unroll
+      for (int e0 = 0; e0 < 32; e0 += 4) {
+        const int e = e0 + rsub;
+        const int32_t ve = __shfl_sync(0xffffffffu, v, e);
+        if (e < nb && 4 * l8 < dc)
+          cp_async16(buf + e * SROW + 4 * l8, X + (int64_t)ve * d + c0 + 4 * l8);
+      }
+      cp_async_commit();
+    };
+    float acc[SPEC];
+#pragma unroll
+    for (int i = 0; i < SPEC; ++i) acc[i] = 0.0f;
+    __syncwarp();
+    issue(0, stage);
+    int cur = 0;
+    for (int c0 = 0; c0 < d; c0 += DC) {
+      if (c0 + DC < d) {
+        issue(c0 + DC, stage + (cur ^ 1) * 32 * SROW);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      if (act) {
+        const int dc = min(DC, d - c0);
+        const float *srow = stage + cur * 32 * SROW + lane * SROW;
+#pragma unroll 2
+        for (int k = 0; k < dc; k += 4) {
+          const float4 y = *reinterpret_cast<const float4 *>(srow + k);
+#pragma unroll
+          for (int i = 0; i < SPEC; ++i) {
+            if (i < nw) {
+              // squared_l2(data[w], data[v]) (_kernels.py:390)
+              const float4 x =
+                  __ldg(reinterpret_cast<const float4 *>(X + (int64_t)wid[i] * d + c0 + k));
+              acc[i] = sq_step(acc[i], x.x, y.x);
+              acc[i] = sq_step(acc[i], x.y, y.y);
+              acc[i] = sq_step(acc[i], x.z, y.z);
+              acc[i] = sq_step(acc[i], x.w, y.w);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      cur ^= 1;
+    }
+#pragma unroll
+    for (int i = 0; i < SPEC; ++i) dr[b][i] = acc[i];
+  }
+  // resolve the rounds in order
+  unsigned am[SB];
+#pragma unroll
+  for (int b = 0; b < SB; ++b) am[b] = __ballot_sync(0xffffffffu, b * 32 + lane < n_alive);
+  int pos = 0, last = 0;
+#pragma unroll
+  for (int i = 0; i < SPEC; ++i) {
+    if (i >= nw) break;
+    if (pos != i) continue;  // entry i was dominated: the next kept lies further on
+    // alive entry i is the next kept neighbour (_kernels.py:396-399)
+    if (lane == 0) {
+      orow[kept] = wid[i];
+      odrow[kept] = wdu[i];
+    }
+    ++kept;
+    last = i;
+    if (kept == M) {  // _kernels.py:378: later candidates never examined
+      stop = true;
+      stop_j = s_alive[i];
+      return 0;
+    }
+    const float duw = wdu[i];
+#pragma unroll
+    for (int b = 0; b < SB; ++b) {
+      const int p = b * 32 + lane;
+      bool live = (am[b] >> lane) & 1u;
+      if (live && p > i) {
+        if (duw == 0.0f) {  // _kernels.py:387-389: dominated, no evaluation
+          live = false;
+        } else {
+          const int j = s_alive[p];
+          const float dv = s_dist[j];
+          const float dwv = dr[b][i];
+          s_de[j] += 1;
+          bool dom;
+          if (dwv == 0.0f) {
+            dom = true;
+          } else if (dwv < dv) {
+            if (strategy == 0) {
+              dom = true;
+            } else if (strategy == 2) {  // "slack" extension: s^2 * dwv < dv
+              dom = cos_alpha * (double)dwv < (double)dv;
+            } else {
+              double c = cos_angle_from_sq(duw, dwv, dv);
+              s_ae[j] += 1;
+              dom = c < cos_alpha;
+            }
+          } else {
+            dom = false;
+          }
+          live = !dom;
+        }
+      }
+      am[b] = __ballot_sync(0xffffffffu, live);
+    }
+    // next kept: the first alive entry after i
+    int nxt = n_alive;
+#pragma unroll
+    for (int b = SB - 1; b >= 0; --b) {
+      const int sh = i - b * 32;  // bits 0..sh of batch b are at or before entry i
+      const unsigned after = sh < 0 ? 0xffffffffu : (sh >= 31 ? 0u : ~((2u << sh) - 1u));
+      const unsigned m = am[b] & after;
+      if (m) nxt = b * 32 + __ffs(m) - 1;
+    }
+    pos = nxt;
+  }
+  // compact: alive entries after the last kept one, order kept
+  int16_t keep_e[SB];
+#pragma unroll
+  for (int b = 0; b < SB; ++b) {
+    const int p = b * 32 + lane;
+    keep_e[b] = p < n_alive ? s_alive[p] : (int16_t)0;
+  }
+  __syncwarp();
+  int new_n = 0;
+#pragma unroll
+  for (int b = 0; b < SB; ++b) {
+    const int p = b * 32 + lane;
+    const bool k = ((am[b] >> lane) & 1u) && p > last;
+    const unsigned bb = __ballot_sync(0xffffffffu, k);
+    if (k) s_alive[new_n + __popc(bb & lanemask_lt())] = keep_e[b];
+    new_n += __popc(bb);
+  }
+  __syncwarp();
+  return new_n;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(PRUNE_WARPS * 32, 2)
     prune_kernel(const float *__restrict__ X, const uint8_t *__restrict__ xu8,
@@ -253,7 +429,12 @@ __global__ void __launch_bounds__(PRUNE_WARPS * 32, 2)
       }
       // in-window greedy: the first alive entry is the next kept neighbour
       int stop_j = wn - 1;
-      while (n_alive > 0) {
+      if (MODE == 1) {  // speculative rounds (same verdicts, counters, order)
+        while (n_alive > 0 && !stop)
+          n_alive = spec_block(X, d, strategy, cos_alpha, n_alive, s_id, s_dist, s_de, s_ae,
+                               s_alive, stage, orow, odrow, kept, M, stop, stop_j, lane);
+      }
+      while (MODE != 1 && n_alive > 0) {
         const int e = s_alive[0];
         const int32_t w = s_id[e];
         const float duw = s_dist[e];
