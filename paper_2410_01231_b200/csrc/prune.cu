@@ -192,13 +192,16 @@ __device__ __forceinline__ int test_round(
 // Speculative in-window rounds (MODE 1, fp32 rows).  The next kept
 // neighbours can only be the first alive entries, so one staged pass over the
 // alive rows computes every alive entry's distance to each of the first SPEC
-// alive entries (SPEC independent sequential fp32 chains per lane: bit-
+// alive entries (SPEC = 3 independent sequential fp32 chains per lane: bit-
 // identical values, SPEC x fewer row reads, SPEC-way ILP), and the rounds are
 // then resolved in order from registers.  A distance is counted (s_de / s_ae)
 // only when its round happens, i.e. for kept neighbours, so verdicts, the kept
 // set and the lazy counters are exactly the sequential rounds'.  Returns the
 // new alive count; kept / stop / stop_j are updated as the caller's loop does.
-constexpr int SPEC = 4;
+#ifndef PRUNE_SPEC
+#define PRUNE_SPEC 3
+#endif
+constexpr int SPEC = PRUNE_SPEC;
 constexpr int SB = PRUNE_W / 32;
 
 __device__ __forceinline__ int spec_block(const float *__restrict__ X, int d, int strategy,
