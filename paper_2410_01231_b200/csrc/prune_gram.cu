@@ -48,7 +48,7 @@ constexpr int C = 128;          // candidates per point (TMEM lanes)
 #define GRAM_GREEDY 2
 #endif
 #ifndef GRAM_NBUF
-#define GRAM_NBUF 3
+#define GRAM_NBUF 2  // measured: 3 buffers cost 5 % (less shared memory left to L1)
 #endif
 constexpr int STAGES = GRAM_STAGES;  // gathered points in flight
 constexpr int GROUPS = GRAM_GROUPS;  // mask warpgroups = TMEM accumulators (point parity)
@@ -61,6 +61,7 @@ constexpr int CTAS_PER_SM = GRAM_CTAS;
 constexpr int TMEM_COLS = C * GROUPS;
 constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(C >> 3) << 17) | ((uint32_t)(C >> 4) << 24);
 
+template <int STRATEGY>
 struct __align__(1024) Smem {
   uint8_t tile[STAGES][C * 128];  // SW128 K-major: 8-row x 128-byte atoms
   int32_t id[STAGES][C];
@@ -70,7 +71,8 @@ struct __align__(1024) Smem {
   int32_t self[STAGES];
   int64_t u[STAGES];
   alignas(16) uint32_t pm[NBUF][C][4];  // pm[j]: candidates i < j that dominate c_j if kept
-  alignas(16) uint32_t am[NBUF][C][4];  // am[j]: candidates i whose test of c_j evaluates the angle
+  // am[j]: candidates i whose test of c_j evaluates the angle (alpha only)
+  alignas(16) uint32_t am[STRATEGY == 1 ? NBUF : 1][STRATEGY == 1 ? C : 1][4];
   uint32_t ex[NBUF][4];     // examinable candidates (in range, not u itself)
   int32_t gid[NBUF][C];     // the greedy warp's copy of the point (the gather
   float gdist[NBUF][C];     // stage is released as soon as the masks are built)
@@ -117,7 +119,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned view, derived from the shared array itself so every access
   // compiles to LDS/STS (an integer round trip would leave generic LD/ST)
-  Smem &s = *reinterpret_cast<Smem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  Smem<STRATEGY> &s = *reinterpret_cast<Smem<STRATEGY> *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       for (;;) {
         GWAIT(1, mbar_wait(&s.full[stage], phase));
         if (s.cnt[stage] < 0) break;
-        fence_proxy_async_smem();  // cp.async (generic proxy) -> tensor-core reads
+        fence_proxy_async_smem();  // generic-proxy smem writes -> tensor-core reads
         GWAIT(2, mbar_wait(&s.tempty[acc], tphase ^ 1));
         tc_fence_after();
         const uint64_t desc = sw128_desc(s.tile[stage]);
@@ -395,7 +397,8 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       if (lane == 0) mbar_arrive(&s.tempty[grp]);
       GWAIT(5, mbar_wait(&s.mempty[mb], mphase ^ 1));  // the greedy warp is done with buffer mb
       *reinterpret_cast<uint4 *>(s.pm[mb][t]) = make_uint4(pm[0], pm[1], pm[2], pm[3]);
-      *reinterpret_cast<uint4 *>(s.am[mb][t]) = make_uint4(am[0], am[1], am[2], am[3]);
+      if (STRATEGY == 1)
+        *reinterpret_cast<uint4 *>(s.am[mb][t]) = make_uint4(am[0], am[1], am[2], am[3]);
       const unsigned exm = __ballot_sync(0xffffffffu, t < cnt && sid[t] != self);
       if (lane == 0) s.ex[mb][q] = exm;
       s.gid[mb][t] = sid[t];
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       const int32_t *sid = s.gid[mb];
       const float *sdist = s.gdist[mb];
       const uint32_t(*spm)[4] = s.pm[mb];
-      const uint32_t(*sam)[4] = s.am[mb];
+      const uint32_t(*sam)[4] = s.am[STRATEGY == 1 ? mb : 0];
       const uint32_t *sex = s.ex[mb];
       // everything this lane needs, loaded at once (one shared-memory latency)
       uint4 pjv[4];
@@ -601,24 +604,24 @@ int launch_prune_gram(const uint8_t *xu8, const int32_t *norms, int64_t n,
     set_error("cuTensorMapEncodeTiled failed (gather4 map)");
     return PGK_ERR_CUDA;
   }
-  const size_t smem = sizeof(gram::Smem) + 1024;
+  const size_t smem0 = sizeof(gram::Smem<0>) + 1024, smem1 = sizeof(gram::Smem<1>) + 1024;
   static bool attr = false;
   if (!attr) {
     PGK_CUDA(cudaFuncSetAttribute(gram::prune_gram_kernel<0>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem0));
     PGK_CUDA(cudaFuncSetAttribute(gram::prune_gram_kernel<1>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
     attr = true;
   }
   const unsigned grid =
       (unsigned)std::min<int64_t>(n, (int64_t)gram::CTAS_PER_SM * num_sms());
   if (strategy == 0 || strategy == 2)  // slack: the rng masks with another threshold
-    gram::prune_gram_kernel<0><<<grid, gram::THREADS, smem, stream>>>(
+    gram::prune_gram_kernel<0><<<grid, gram::THREADS, smem0, stream>>>(
         tmX, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
         cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals,
         long_rows, long_count);
   else
-    gram::prune_gram_kernel<1><<<grid, gram::THREADS, smem, stream>>>(
+    gram::prune_gram_kernel<1><<<grid, gram::THREADS, smem1, stream>>>(
         tmX, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, 1,
         cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals,
         long_rows, long_count);
