@@ -48,7 +48,10 @@ namespace tiles {
 constexpr int TB = 128;  // tile size (== tc::BN == tc::BM)
 constexpr double MARGIN = 1e-9;
 
-constexpr int CSTRIDE = 512;  // one center per 512 rows
+#ifndef TILES_CSTRIDE
+#define TILES_CSTRIDE 512
+#endif
+constexpr int CSTRIDE = TILES_CSTRIDE;  // one center per CSTRIDE rows
 
 __global__ void gather_centers_kernel(const float *__restrict__ X, int64_t n, int d, int64_t C,
                                       float *__restrict__ cen) {
@@ -423,7 +426,7 @@ bool tiles_supported(int64_t n, int64_t d, int64_t k) {
     const char *e = getenv("PGK_DISABLE_PRUNE");
     env = (e && e[0] == '1') ? 1 : 0;
   }
-  const int64_t T = ((n + 127) / 128 * 128 + (n + 511) / 512 * 128) / 128;
+  const int64_t T = ((n + 127) / 128 * 128 + (n + tiles::CSTRIDE - 1) / tiles::CSTRIDE * 128) / 128;
   // the T x T centroid-distance matrix and lists (8 B / pair) stay modest
   return !env && d <= 128 && k <= 256 && n >= 8 * tiles::TB && T <= 32768;
 }
