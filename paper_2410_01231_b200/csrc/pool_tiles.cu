@@ -241,8 +241,7 @@ __global__ void tile_nearest_kernel(const float *__restrict__ dc, const int32_t 
                                     int64_t T, int K, int32_t *__restrict__ lists,
                                     int32_t *__restrict__ lens,
                                     unsigned long long *__restrict__ total) {
-  __shared__ uint64_t sk[8][32 * NEAR];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   for (int64_t Q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; Q < T;
        Q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     // per-lane best NEAR (sorted insertion), then a warp sort of 32*NEAR keys
@@ -250,29 +249,51 @@ __global__ void tile_nearest_kernel(const float *__restrict__ dc, const int32_t 
 #pragma unroll
     for (int i = 0; i < NEAR; ++i) best[i] = KEY_MAX;
     const bool qreal = size[Q] > 0;
-    for (int64_t t = lane; qreal && t < T; t += 32) {
-      if (size[t] <= 0) continue;
-      uint64_t k = ((uint64_t)__float_as_uint(dc[Q * T + t]) << 32) | (uint32_t)t;
-      if (k < best[NEAR - 1]) {  // sorted insertion (branch-free shift)
+    // four columns per lane per trip, loads issued together
+    for (int64_t t0 = lane; qreal && t0 < T; t0 += 128) {
+      uint64_t kq[4];
 #pragma unroll
-        for (int i = NEAR - 1; i > 0; --i)
-          best[i] = k < best[i - 1] ? best[i - 1] : (k < best[i] ? k : best[i]);
-        best[0] = k < best[0] ? k : best[0];
+      for (int u = 0; u < 4; ++u) {
+        const int64_t t = t0 + 32 * u;
+        kq[u] = (t < T && size[t] > 0)
+                    ? ((uint64_t)__float_as_uint(dc[Q * T + t]) << 32) | (uint32_t)t
+                    : KEY_MAX;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint64_t k = kq[u];
+        if (k < best[NEAR - 1]) {  // sorted insertion (branch-free shift)
+#pragma unroll
+          for (int i = NEAR - 1; i > 0; --i)
+            best[i] = k < best[i - 1] ? best[i - 1] : (k < best[i] ? k : best[i]);
+          best[0] = k < best[0] ? k : best[0];
+        }
       }
     }
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < NEAR; ++i) sk[w][i * 32 + lane] = best[i];
-    __syncwarp();
-    warp_bitonic_sort(sk[w], 32 * NEAR, lane);
-    // prefix of tiles until they hold P1_MULT * K points
+    // the warp's NEAR smallest keys in order: each lane's list is sorted, so
+    // the next one is the warp minimum of the lanes' heads (keys are unique);
+    // stop once the tiles hold P1_MULT * K points
     int m = 0, pts = 0;
-    for (int i = 0; i < NEAR && sk[w][i] != KEY_MAX; ++i) {
-      pts += size[(uint32_t)sk[w][i]];
+    uint32_t mine = 0;  // lane i: the i-th nearest tile
+    for (int i = 0; i < NEAR; ++i) {
+      uint64_t mn = best[0];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t y = __shfl_xor_sync(0xffffffffu, mn, o);
+        mn = y < mn ? y : mn;
+      }
+      if (mn == KEY_MAX) break;
+      if (best[0] == mn) {  // pop the owner's head
+#pragma unroll
+        for (int j = 0; j + 1 < NEAR; ++j) best[j] = best[j + 1];
+        best[NEAR - 1] = KEY_MAX;
+      }
+      if (lane == i) mine = (uint32_t)mn;
+      pts += size[(uint32_t)mn];
       m = i + 1;
       if (pts >= P1_MULT * K) break;
     }
-    if (lane < m) lists[Q * T + lane] = (int32_t)(uint32_t)sk[w][lane];
+    if (lane < m) lists[Q * T + lane] = (int32_t)mine;
     if (lane == 0) {
       lens[Q] = m;
       atomicAdd(total, (unsigned long long)m);
@@ -323,16 +344,27 @@ __global__ void tile_filter_kernel(const float *__restrict__ dc, const double *_
     }
     const double rQ = rad[Q], UQ = U[Q] * scale + 1e-9;
     int base = 0;
-    for (int64_t t0 = 0; size[Q] > 0 && t0 < T; t0 += 32) {
-      const int64_t t = t0 + lane;
-      bool keep = false;
-      if (t < T && size[t] > 0) {
-        const double lb = (double)dc[Q * T + t] * (1.0 - dc_margin) - rQ - rad[t];
-        keep = lb <= UQ;
+    const bool qreal = size[Q] > 0;
+    // four 32-column chunks per trip, their loads issued together (the
+    // per-chunk ballot chain would otherwise expose one global latency each)
+    for (int64_t t0 = 0; qreal && t0 < T; t0 += 128) {
+      bool keep[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t t = t0 + 32 * u + lane;
+        keep[u] = false;
+        if (t < T) {
+          const int32_t sz = size[t];
+          const double lb = (double)dc[Q * T + t] * (1.0 - dc_margin) - rQ - rad[t];
+          keep[u] = sz > 0 && lb <= UQ;
+        }
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (keep) lists[Q * T + base + __popc(bal & lanemask_lt())] = (int32_t)t;
-      base += __popc(bal);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned bal = __ballot_sync(0xffffffffu, keep[u]);
+        if (keep[u]) lists[Q * T + base + __popc(bal & lanemask_lt())] = (int32_t)(t0 + 32 * u + lane);
+        base += __popc(bal);
+      }
     }
     if (lane == 0) {
       lens[Q] = base;
