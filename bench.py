@@ -75,10 +75,19 @@ class Clocks:
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,utilization.gpu,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
+            return self
+        # the timed region is short (~25 ms per step): start timing only once
+        # the sampler is producing rows
+        t0 = time.time()
+        while time.time() - t0 < 5.0 and self.proc.poll() is None:
+            self.f.flush()
+            if self.path.exists() and self.path.stat().st_size > 0:
+                break
+            time.sleep(0.02)
         return self
 
     def __exit__(self, *a):
