@@ -57,7 +57,7 @@ int launch_prune(const float *, const uint8_t *, const int32_t *, int64_t, int64
                  const int32_t *, const int32_t *, void *, size_t, const int64_t *,
                  const int32_t *, const int32_t *,
                  const float *, int, double, int64_t, int64_t, int32_t *, float *, int32_t *,
-                 int64_t *, int64_t *, cudaStream_t);
+                 int64_t *, int64_t *, cudaStream_t, bool short_rows = false);
 int make_u8(const float *, int64_t, int64_t, uint8_t *, int32_t *, cudaStream_t);
 int reverse_workspace(int64_t n, int64_t width, size_t *bytes);
 int add_reverse_and_prune(const float *, const uint8_t *, const int32_t *, const int32_t *,

@@ -747,7 +747,7 @@ int launch_prune_gram(const uint8_t *xu8, const int32_t *norms, int64_t n,
                       const int32_t *cand_ids, const float *cand_dists, int strategy,
                       double cos_alpha, int64_t M, int64_t width, int32_t *out_ids,
                       float *out_dists, int32_t *out_counts, int64_t *dist_evals,
-                      int64_t *angle_evals, void *ws, cudaStream_t stream);
+                      int64_t *angle_evals, void *ws, cudaStream_t stream, bool pair);
 
 size_t prune_workspace(int64_t n_rows) { return gram_workspace(n_rows); }
 
@@ -757,12 +757,12 @@ int launch_prune(const float *X, const uint8_t *xu8, const int32_t *norms, int64
                  const int32_t *cand_counts, const int32_t *cand_ids, const float *cand_dists,
                  int strategy, double cos_alpha, int64_t M, int64_t width, int32_t *out_ids,
                  float *out_dists, int32_t *out_counts, int64_t *dist_evals,
-                 int64_t *angle_evals, cudaStream_t stream) {
+                 int64_t *angle_evals, cudaStream_t stream, bool short_rows) {
   if (n == 0) return PGK_OK;
   if (xu8 && norms && d <= 128 && ws && ws_bytes >= gram_workspace(n) && gram_enabled())
     return launch_prune_gram(xu8, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids,
                              cand_dists, strategy, cos_alpha, M, width, out_ids, out_dists,
-                             out_counts, dist_evals, angle_evals, ws, stream);
+                             out_counts, dist_evals, angle_evals, ws, stream, short_rows);
   if (xu8 && norms && d <= 128)
     return launch_prune_u8_rows(xu8, norms, n, nullptr, row_node, row_order, cand_off,
                      cand_counts, cand_ids, cand_dists,

@@ -67,17 +67,19 @@ struct __align__(1024) Smem {
   int32_t id[STAGES][C];
   float dist[STAGES][C];
   alignas(16) int32_t nrm[STAGES][C];
-  int32_t cnt[STAGES];   // -1: end of this CTA's stream
-  int32_t self[STAGES];
-  int64_t u[STAGES];
+  // per stage, per point slot (PAIR mode: two points share a stage, rows
+  // 0..63 and 64..127; otherwise slot 0 only)
+  int32_t cnt[STAGES][2];   // [0] -1: end of this CTA's stream; 0: empty slot
+  int32_t self[STAGES][2];
+  int64_t u[STAGES][2];
   alignas(16) uint32_t pm[NBUF][C][4];  // pm[j]: candidates i < j that dominate c_j if kept
   // am[j]: candidates i whose test of c_j evaluates the angle (alpha only)
   alignas(16) uint32_t am[STRATEGY == 1 ? NBUF : 1][STRATEGY == 1 ? C : 1][4];
   uint32_t ex[NBUF][4];     // examinable candidates (in range, not u itself)
   int32_t gid[NBUF][C];     // the greedy warp's copy of the point (the gather
   float gdist[NBUF][C];     // stage is released as soon as the masks are built)
-  int64_t gu[NBUF];
-  int32_t gcnt[NBUF];       // -1: end of stream
+  int64_t gu[NBUF][2];     // -1: empty slot
+  int32_t gcnt[NBUF][2];    // [0] -1: end of stream
   uint64_t full[STAGES], empty[STAGES];
   uint64_t tfull[GROUPS], tempty[GROUPS];
   uint64_t mfull[NBUF], mempty[NBUF];
@@ -102,7 +104,12 @@ __device__ unsigned long long g_gram_stats[16];
 #define GWAIT(slot, expr) expr
 #endif
 
-template <int STRATEGY>  // 0 = rng, 1 = alpha (compile-time: no angle code for rng)
+// PAIR: two points of <= 64 candidates per stage / MMA (rows 0..63 and
+// 64..127 of the tile; the diagonal 64 x 64 blocks of the Gram matrix are the
+// two points' own): the phase-B re-prune, whose rows hold ~38 candidates, is
+// bound by the per-point pipeline cost, which pairing halves.  Rows with more
+// than 64 candidates are listed for the single-point kernel.
+template <int STRATEGY, bool PAIR>  // 0 = rng, 1 = alpha (compile-time: no angle code for rng)
 __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     prune_gram_kernel(const __grid_constant__ CUtensorMap tmX,
                       const int32_t *__restrict__ norms,
@@ -115,7 +122,11 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
                       int M, int width, int32_t *__restrict__ out_ids,
                       float *__restrict__ out_dists, int32_t *__restrict__ out_counts,
                       int64_t *__restrict__ dist_evals, int64_t *__restrict__ angle_evals,
-                      int32_t *__restrict__ long_rows, int32_t *__restrict__ long_count) {
+                      int32_t *__restrict__ long_rows, int32_t *__restrict__ long_count,
+                      const int32_t *__restrict__ n_rows_dev) {
+  static_assert(!PAIR || (GROUPS == 1 && NG == 2), "PAIR: one mask group, one greedy warp per slot");
+  constexpr int PC = PAIR ? C / 2 : C;  // candidates per point
+  if (n_rows_dev) n_rows = *n_rows_dev;  // rows listed on the device (a previous launch)
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned view, derived from the shared array itself so every access
   // compiles to LDS/STS (an integer round trip would leave generic LD/ST)
@@ -132,7 +143,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     }
     for (int i = 0; i < NBUF; ++i) {
       mbar_init(&s.mfull[i], 4);
-      mbar_init(&s.mempty[i], 1);
+      mbar_init(&s.mempty[i], PAIR ? 2 : 1);  // PAIR: each greedy warp frees its slot
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -160,7 +171,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     // Lane l holds candidates 4l..4l+3 (id -1, dist 0, norm 0 past cnt); its
     // gather4 fetches exactly those rows.  The other roles follow the stream
     // published in s.u / s.cnt / s.self.
-    int stage = 0;
+    int stage = 0, half = 0;
     uint32_t phase = 0;
     const int64_t nb = blockIdx.x < n_rows ? (n_rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     int64_t bu = 0, boff = 0;
@@ -199,14 +210,14 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int r = 4 * lane + i;
-        o[i] = (m.cnt <= C && r < m.cnt) ? cand_ids[m.off + r] : -1;
+        o[i] = (m.cnt <= PC && r < m.cnt) ? cand_ids[m.off + r] : -1;
       }
     };
     auto dn_of = [&](const PM &m, const int32_t (&id)[4], float (&dd)[4], int32_t (&nn)[4]) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int r = 4 * lane + i;
-        const bool ok = m.cnt <= C && r < m.cnt;
+        const bool ok = m.cnt <= PC && r < m.cnt;
         dd[i] = ok ? cand_dists[m.off + r] : 0.f;
         nn[i] = ok ? norms[id[i]] : 0;
       }
@@ -225,35 +236,44 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       float d1[4];
       int32_t n1[4];
       dn_of(m1, i1, d1, n1);
-      if (m0.cnt > C) {  // hub row: left to the per-warp kernel
+      if (m0.cnt > PC) {  // hub row (PAIR: > 64): left to the next kernel
         if (lane == 0) long_rows[atomicAdd(long_count, 1)] = (int32_t)m0.u;
       } else {
-        GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
+        if (half == 0) GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
         // candidate rows by TMA gather4 (4 rows of 128 B per instruction,
-        // SW128 applied by the map; lane l's rows land at tile row 4l, i.e.
-        // atom l/2, half l%2).  Rows past cnt keep stale bytes: their Gram
-        // entries feed no mask bit that is ever read (t >= cnt is not
+        // SW128 applied by the map; lane l's rows land at tile row r0 + 4l,
+        // i.e. atom (r0 + 4l) / 8).  Rows past cnt keep stale bytes: their
+        // Gram entries feed no mask bit that is ever read (t >= cnt is not
         // examinable, i >= cnt > t unused).
+        const int r0 = half * 64;
         const int ng = (m0.cnt + 3) >> 2;
         if (lane == 0) mbar_expect_tx_only(&s.full[stage], (uint32_t)ng * 512u);
         __syncwarp();
         if (lane < ng) {
           const int32_t a = i0[0];
-          tma_gather4(s.tile[stage] + (lane >> 1) * 1024 + (lane & 1) * 512, &tmX,
+          tma_gather4(s.tile[stage] + ((r0 + 4 * lane) >> 3) * 1024 + (lane & 1) * 512, &tmX,
                       &s.full[stage], 0, a, i0[1] >= 0 ? i0[1] : a, i0[2] >= 0 ? i0[2] : a,
                       i0[3] >= 0 ? i0[3] : a);
         }
-        *reinterpret_cast<int4 *>(&s.id[stage][4 * lane]) = make_int4(i0[0], i0[1], i0[2], i0[3]);
-        *reinterpret_cast<float4 *>(&s.dist[stage][4 * lane]) = make_float4(d0[0], d0[1], d0[2], d0[3]);
-        *reinterpret_cast<int4 *>(&s.nrm[stage][4 * lane]) = make_int4(n0[0], n0[1], n0[2], n0[3]);
-        if (lane == 0) {
-          s.u[stage] = m0.u;
-          s.cnt[stage] = m0.cnt;
-          s.self[stage] = m0.self;
+        if (4 * lane < PC) {
+          *reinterpret_cast<int4 *>(&s.id[stage][r0 + 4 * lane]) = make_int4(i0[0], i0[1], i0[2], i0[3]);
+          *reinterpret_cast<float4 *>(&s.dist[stage][r0 + 4 * lane]) =
+              make_float4(d0[0], d0[1], d0[2], d0[3]);
+          *reinterpret_cast<int4 *>(&s.nrm[stage][r0 + 4 * lane]) = make_int4(n0[0], n0[1], n0[2], n0[3]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s.full[stage]);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (lane == 0) {
+          s.u[stage][half] = m0.u;
+          s.cnt[stage][half] = m0.cnt;
+          s.self[stage][half] = m0.self;
+        }
+        if (PAIR && half == 0) {
+          half = 1;  // the next point fills the other half of this stage
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s.full[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          half = 0;
+        }
       }
       m0 = m1;
       m1 = m2;
@@ -265,10 +285,24 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         i1[i] = i2[i];
       }
     }
+    if (PAIR && half == 1) {  // a half-filled last stage: the second slot is empty
+      if (lane == 0) {
+        s.u[stage][1] = -1;
+        s.cnt[stage][1] = 0;
+      }
+      if (4 * lane < PC) {
+        *reinterpret_cast<int4 *>(&s.id[stage][64 + 4 * lane]) = make_int4(-1, -1, -1, -1);
+        *reinterpret_cast<float4 *>(&s.dist[stage][64 + 4 * lane]) = make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<int4 *>(&s.nrm[stage][64 + 4 * lane]) = make_int4(0, 0, 0, 0);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s.full[stage]);
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    }
     // end of stream: one sentinel per mask group (each reads every other point)
     for (int g = 0; g < GROUPS; ++g) {
       GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
-      if (lane == 0) s.cnt[stage] = g == 0 ? -1 : -2;
+      if (lane == 0) s.cnt[stage][0] = g == 0 ? -1 : -2;
       __syncwarp();
       if (lane == 0) mbar_arrive(&s.full[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -280,7 +314,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       uint32_t phase = 0, tphase = 0;
       for (;;) {
         GWAIT(1, mbar_wait(&s.full[stage], phase));
-        if (s.cnt[stage] < 0) break;
+        if (s.cnt[stage][0] < 0) break;
         fence_proxy_async_smem();  // generic-proxy smem writes -> tensor-core reads
         GWAIT(2, mbar_wait(&s.tempty[acc], tphase ^ 1));
         tc_fence_after();
@@ -310,18 +344,23 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       const int mb = (int)(k % NBUF);  // greedy buffer of point k
       const uint32_t mphase = (uint32_t)((k / NBUF) & 1);
       GWAIT(3, mbar_wait(&s.full[stage], phase));
-      const int cnt = s.cnt[stage];
-      if (cnt < 0) {  // end of stream: the first group to see it tells every greedy warp
-        for (int64_t kk = k; cnt == -1 && kk < k + NG; ++kk) {
+      const int cnt0 = s.cnt[stage][0];
+      if (cnt0 < 0) {  // end of stream: the first group to see it tells every greedy warp
+        // (PAIR: both greedy warps read every buffer, one sentinel serves both)
+        for (int64_t kk = k; cnt0 == -1 && kk < k + (PAIR ? 1 : NG); ++kk) {
           const int b = (int)(kk % NBUF);
           GWAIT(5, mbar_wait(&s.mempty[b], ((uint32_t)((kk / NBUF) & 1)) ^ 1));
-          if (t == 0) s.gcnt[b] = -1;
+          if (t == 0) s.gcnt[b][0] = -1;
           __syncwarp();
           if (lane == 0) mbar_arrive(&s.mfull[b]);
         }
         break;
       }
-      const int32_t self = s.self[stage];
+      const int P = PAIR ? (q >> 1) : 0;  // this warp's point slot
+      const int ql = PAIR ? (q & 1) : q;  // its quarter within the point
+      const int cb = PAIR ? 2 * P : 0;    // the point's first column chunk
+      const int cnt = s.cnt[stage][P];
+      const int32_t self = s.self[stage][P];
       const int32_t *sid = s.id[stage];
       const float *sdist = s.dist[stage];
       const int32_t *snrm = s.nrm[stage];
@@ -353,17 +392,18 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       tc_fence_after();
       // lower-triangle chunks holding candidates; none when this warp's
       // candidates are all past cnt (their masks are never read)
-      const int clast = q * 32 >= cnt ? -1 : min(q, (cnt - 1) >> 5);
+      const int clast = ql * 32 >= cnt ? -1 : min(ql, (cnt - 1) >> 5);
 #pragma unroll 1
       for (int c = 0; c <= clast; ++c) {
+        const int gc = cb + c;  // column chunk of the tile
         uint32_t g[32];
-        tmem_ld32(tl + (uint32_t)(c * 32), g);
-        const uint32_t zu = __ballot_sync(0xffffffffu, sdist[c * 32 + lane] == 0.0f);
-        const uint32_t valid = c < q ? 0xffffffffu : ((1u << lane) - 1u);
+        tmem_ld32(tl + (uint32_t)(gc * 32), g);
+        const uint32_t zu = __ballot_sync(0xffffffffu, sdist[gc * 32 + lane] == 0.0f);
+        const uint32_t valid = c < ql ? 0xffffffffu : ((1u << lane) - 1u);
         tmem_wait_ld();
         uint32_t dm = 0, need = 0;
         if (STRATEGY == 0) {
-          const int4 *np = reinterpret_cast<const int4 *>(snrm + c * 32);
+          const int4 *np = reinterpret_cast<const int4 *>(snrm + gc * 32);
 #pragma unroll
           for (int v = 0; v < 8; ++v) {
             const int4 w = np[v];
@@ -376,7 +416,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         } else {
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
-            const int ci = c * 32 + k;
+            const int ci = gc * 32 + k;
             const float duw = sdist[ci];
             const float dwv = (float)(snrm[ci] + nv - 2 * (int)g[k]);  // == squared_l2
             const bool z = (duw == 0.0f) | (dwv == 0.0f);
@@ -399,13 +439,13 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       *reinterpret_cast<uint4 *>(s.pm[mb][t]) = make_uint4(pm[0], pm[1], pm[2], pm[3]);
       if (STRATEGY == 1)
         *reinterpret_cast<uint4 *>(s.am[mb][t]) = make_uint4(am[0], am[1], am[2], am[3]);
-      const unsigned exm = __ballot_sync(0xffffffffu, t < cnt && sid[t] != self);
+      const unsigned exm = __ballot_sync(0xffffffffu, ql * 32 + lane < cnt && sid[t] != self);
       if (lane == 0) s.ex[mb][q] = exm;
       s.gid[mb][t] = sid[t];
       s.gdist[mb][t] = dv;
-      if (t == 0) {
-        s.gu[mb] = s.u[stage];
-        s.gcnt[mb] = cnt;
+      if (ql == 0 && lane == 0) {
+        s.gu[mb][P] = s.u[stage][P];
+        s.gcnt[mb][P] = cnt;
       }
       __syncwarp();
       if (lane == 0) {
@@ -417,11 +457,18 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   } else {
     // ---------------- greedy scan + exact lazy counters (NG warps) ---------
     const int gw = warp - GREEDY_WARP;
-    for (int64_t k = gw;; k += NG) {
+    const int P = PAIR ? gw : 0;        // PAIR: greedy warp w takes slot w of every buffer
+    const int base = P * PC;            // the slot's first tile row
+    for (int64_t k = PAIR ? 0 : gw;; k += PAIR ? 1 : NG) {
       const int mb = (int)(k % NBUF);
       GWAIT(6, mbar_wait(&s.mfull[mb], (uint32_t)((k / NBUF) & 1)));
-      if (s.gcnt[mb] < 0) break;
-      const int64_t u = s.gu[mb];
+      if (s.gcnt[mb][0] < 0) break;
+      const int64_t u = s.gu[mb][P];
+      if (PAIR && u < 0) {  // empty slot (odd point count)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s.mempty[mb]);
+        continue;
+      }
       const int32_t *sid = s.gid[mb];
       const float *sdist = s.gdist[mb];
       const uint32_t(*spm)[4] = s.pm[mb];
@@ -434,10 +481,17 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       float dsv[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        pjv[c] = *reinterpret_cast<const uint4 *>(spm[c * 32 + lane]);
-        exv[c] = sex[c];
-        idv[c] = sid[c * 32 + lane];
-        dsv[c] = sdist[c * 32 + lane];
+        if (c * 32 < PC) {
+          pjv[c] = *reinterpret_cast<const uint4 *>(spm[base + c * 32 + lane]);
+          exv[c] = sex[(PAIR ? 2 * P : 0) + c];
+          idv[c] = sid[base + c * 32 + lane];
+          dsv[c] = sdist[base + c * 32 + lane];
+        } else {  // PAIR: chunks 2, 3 are the other slot's
+          pjv[c] = make_uint4(0, 0, 0, 0);
+          exv[c] = 0;
+          idv[c] = -1;
+          dsv[c] = 0.0f;
+        }
       }
       uint32_t zu[4];  // candidates with duw == 0 (no distance computed against them)
 #pragma unroll
@@ -471,8 +525,8 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       // rows: one fully coalesced store sequence per row (whole 128-byte
       // lines also when the output is pinned host memory)
       {
-        int32_t *oid = s.gid[mb];
-        float *od = s.gdist[mb];
+        int32_t *oid = s.gid[mb] + base;
+        float *od = s.gdist[mb] + base;
         __syncwarp();
         int base = 0;
 #pragma unroll
@@ -518,7 +572,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         if (f >= 0 && !((zu[f >> 5] >> (f & 31)) & 1u)) ev += 1;
         dsum += ev;
         if (STRATEGY == 1) {
-          const uint4 aj = *reinterpret_cast<const uint4 *>(sam[j]);
+          const uint4 aj = *reinterpret_cast<const uint4 *>(sam[base + j]);
           const uint32_t aw[4] = {aj.x, aj.y, aj.z, aj.w};
           int an = 0;
 #pragma unroll
@@ -571,7 +625,7 @@ int launch_prune_u8_rows(const uint8_t *xu8, const int32_t *norms, int64_t n,
 
 bool make_u8_row_map(CUtensorMap *tm, const uint8_t *base, int64_t rows, int box_rows);
 
-size_t gram_workspace(int64_t n) { return (size_t)(n + 64) * sizeof(int32_t); }
+size_t gram_workspace(int64_t n) { return (size_t)(2 * n + 128) * sizeof(int32_t); }
 
 // Default selection path for exact-integer rows (PGK_GRAM=0 selects the
 // per-warp prune_u8_kernel instead, e.g. for A/B timing).
@@ -586,17 +640,46 @@ bool gram_enabled() {
 
 // Phase-A / re-prune selection through the tensor-core Gram kernel; rows with
 // more than 128 candidates go to prune_u8_kernel.  ws: gram_workspace(n) bytes.
+// pair: rows of <= 64 candidates two per MMA first (the phase-B re-prune),
+// the longer ones listed on the device for the single-point kernel.
+template <int STRATEGY, bool PAIR>
+static int launch_gram_kernel(const CUtensorMap &tmX, const int32_t *norms, int64_t n,
+                              const int32_t *n_dev, const int32_t *row_node,
+                              const int32_t *row_order, const int64_t *cand_off,
+                              const int32_t *cand_counts, const int32_t *cand_ids,
+                              const float *cand_dists, int strategy, double cos_alpha, int64_t M,
+                              int64_t width, int32_t *out_ids, float *out_dists,
+                              int32_t *out_counts, int64_t *dist_evals, int64_t *angle_evals,
+                              int32_t *long_rows, int32_t *long_count, cudaStream_t stream) {
+  const size_t smem = sizeof(gram::Smem<STRATEGY>) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    PGK_CUDA(cudaFuncSetAttribute(gram::prune_gram_kernel<STRATEGY, PAIR>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)gram::CTAS_PER_SM * num_sms());
+  gram::prune_gram_kernel<STRATEGY, PAIR><<<grid, gram::THREADS, smem, stream>>>(
+      tmX, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
+      cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals,
+      long_rows, long_count, n_dev);
+  PGK_CHECK_LAUNCH("prune_gram_kernel");
+  return PGK_OK;
+}
+
 int launch_prune_gram(const uint8_t *xu8, const int32_t *norms, int64_t n,
                       const int32_t *row_node, const int32_t *row_order,
                       const int64_t *cand_off, const int32_t *cand_counts,
                       const int32_t *cand_ids, const float *cand_dists, int strategy,
                       double cos_alpha, int64_t M, int64_t width, int32_t *out_ids,
                       float *out_dists, int32_t *out_counts, int64_t *dist_evals,
-                      int64_t *angle_evals, void *ws, cudaStream_t stream) {
+                      int64_t *angle_evals, void *ws, cudaStream_t stream, bool pair) {
   if (n == 0) return PGK_OK;
-  int32_t *long_count = reinterpret_cast<int32_t *>(ws);
+  int32_t *long_count = reinterpret_cast<int32_t *>(ws);  // rows past the single kernel
+  int32_t *pair_count = long_count + 1;                   // rows past the pair kernel
   int32_t *long_rows = long_count + 32;
-  PGK_CUDA(cudaMemsetAsync(long_count, 0, sizeof(int32_t), stream));
+  int32_t *pair_rows = long_rows + n + 32;
+  PGK_CUDA(cudaMemsetAsync(long_count, 0, 2 * sizeof(int32_t), stream));
   // candidate ids index data rows (< 2^31 by the ABI); the gather map needs
   // no tighter row bound
   CUtensorMap tmX;
@@ -604,28 +687,34 @@ int launch_prune_gram(const uint8_t *xu8, const int32_t *norms, int64_t n,
     set_error("cuTensorMapEncodeTiled failed (gather4 map)");
     return PGK_ERR_CUDA;
   }
-  const size_t smem0 = sizeof(gram::Smem<0>) + 1024, smem1 = sizeof(gram::Smem<1>) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    PGK_CUDA(cudaFuncSetAttribute(gram::prune_gram_kernel<0>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem0));
-    PGK_CUDA(cudaFuncSetAttribute(gram::prune_gram_kernel<1>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
-    attr = true;
+  const bool rng = strategy == 0 || strategy == 2;  // slack: the rng masks, another threshold
+  const int sa = rng ? strategy : 1;
+  int rc;
+  if (pair) {
+    rc = rng ? launch_gram_kernel<0, true>(tmX, norms, n, nullptr, row_node, row_order, cand_off,
+                                           cand_counts, cand_ids, cand_dists, sa, cos_alpha, M,
+                                           width, out_ids, out_dists, out_counts, dist_evals,
+                                           angle_evals, pair_rows, pair_count, stream)
+             : launch_gram_kernel<1, true>(tmX, norms, n, nullptr, row_node, row_order, cand_off,
+                                           cand_counts, cand_ids, cand_dists, sa, cos_alpha, M,
+                                           width, out_ids, out_dists, out_counts, dist_evals,
+                                           angle_evals, pair_rows, pair_count, stream);
+    if (rc) return rc;
   }
-  const unsigned grid =
-      (unsigned)std::min<int64_t>(n, (int64_t)gram::CTAS_PER_SM * num_sms());
-  if (strategy == 0 || strategy == 2)  // slack: the rng masks with another threshold
-    gram::prune_gram_kernel<0><<<grid, gram::THREADS, smem0, stream>>>(
-        tmX, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
-        cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals,
-        long_rows, long_count);
-  else
-    gram::prune_gram_kernel<1><<<grid, gram::THREADS, smem1, stream>>>(
-        tmX, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, 1,
-        cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals,
-        long_rows, long_count);
-  PGK_CHECK_LAUNCH("prune_gram_kernel");
+  // single-point kernel: every row, or (pair) the rows listed above
+  const int32_t *order1 = pair ? pair_rows : row_order;
+  const int32_t *n1_dev = pair ? pair_count : nullptr;
+  rc = rng ? launch_gram_kernel<0, false>(tmX, norms, n, n1_dev, row_node, order1, cand_off,
+                                          cand_counts, cand_ids, cand_dists, sa, cos_alpha, M,
+                                          width, out_ids, out_dists, out_counts, dist_evals,
+                                          angle_evals, long_rows, long_count, stream)
+           : launch_gram_kernel<1, false>(tmX, norms, n, n1_dev, row_node, order1, cand_off,
+                                          cand_counts, cand_ids, cand_dists, sa, cos_alpha, M,
+                                          width, out_ids, out_dists, out_counts, dist_evals,
+                                          angle_evals, long_rows, long_count, stream);
+  if (rc) return rc;
+  const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)gram::CTAS_PER_SM * num_sms());
+  (void)grid;
 #if GRAM_STATS
   {
     unsigned long long h[16];

@@ -34,7 +34,7 @@ int launch_prune(const float *X, const uint8_t *xu8, const int32_t *norms, int64
                  const float *cand_dists, int strategy, double cos_alpha,
                  int64_t M, int64_t width, int32_t *out_ids, float *out_dists,
                  int32_t *out_counts, int64_t *dist_evals, int64_t *angle_evals,
-                 cudaStream_t stream);
+                 cudaStream_t stream, bool short_rows = false);
 
 constexpr int SORT_WARPS = 8;
 constexpr int SORT_SMEM_KEYS = 512;  // per-warp in-register sort capacity (16 keys per lane)
@@ -399,7 +399,7 @@ int add_reverse_and_prune(const float *X, const uint8_t *xu8, const int32_t *nor
   return launch_prune(X, xu8, norms, n, d, nullptr, row_order, L.prune_ws, L.prune_bytes,
                       L.mrg_off, L.mrg_counts, L.mrg_ids, L.mrg_d, strategy,
                       cos_alpha, M, out_width, out_ids, out_dists, out_counts,
-                      dist_evals, angle_evals, stream);
+                      dist_evals, angle_evals, stream, /*short_rows=*/true);
 }
 
 }  // namespace pgk
