@@ -353,11 +353,14 @@ def run_ours(args):
                    "l2": "256 MB buffer written between timed steps (L2 flush); inputs "
                          f"{data.nbytes >> 20} MB"},
         "stages_ms": {"pool": pool_ms, "prep": prep_ms, "select_A": a_ms, "reverse_B": b_ms},
-        # dominant kernel by time per step: the selection kernel (phase A launch;
-        # phase B re-runs it over the unions, see roofline_reverse)
+        # the largest single launch per step: the phase-A selection kernel (phase
+        # B re-runs it over the unions, see roofline_reverse).  The tcgen05 pool
+        # kernel's three launches (center assignment, pass 2, re-run) sum to a
+        # little more per step; the pool stage has its own line, roofline_pool.
         "roofline": {"bound": "hbm", "achieved": sel_gbs, "peak": hbm, "unit": "GB/s",
                      "frac": sel_gbs / hbm, "traffic": traffic,
-                     "kernel": ("prune_gram_kernel (tcgen05 C x C Gram + greedy scan)"
+                     "kernel": ("prune_gram_kernel (tcgen05 C x C Gram + greedy scan), "
+                                "phase-A launch: the largest single launch of the step"
                                 if u8_path else "prune_kernel (fp32 lazy scan)"),
                      "algorithmic": f"N*({e}dK+{e}d+8K+8R+4) bytes per launch"
                                     + (" (u8 exact-integer rows)" if u8_path else ""),
