@@ -285,19 +285,19 @@ def run_ours(args):
     # ---- e2e: host buffers through the public API ---------------------------
     ids_host = torch.empty((N, R), dtype=torch.int32).pin_memory()
     cnt_host = torch.empty(N, dtype=torch.int32).pin_memory()
-    Xe = torch.empty_like(X)
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
+    for _ in range(args.warmup):  # the host pipeline's buffers and stream, untimed
+        builder.build_host(host, host_out=(ids_host, cnt_host))
     barrier()
     for s in range(args.steps):
         flush.fill_(s & 0xff)
         e2e_ev[s][0].record(stream)
-        Xe.copy_(host, non_blocking=True)
-        m = pool_mode(Xe)  # the public call detects the exact-integer mode per dataset
-        assert m == mode
-        # adjacency + degrees land in pinned host memory, written by the final
-        # re-prune kernel itself (the transfer overlaps that kernel)
-        builder.build(Xe, host_out=(ids_host, cnt_host))
+        # host data in chunks on a side stream, each chunk's u8 rows, exact-
+        # integer check and tile-center assignment as it lands; adjacency +
+        # degrees land in pinned host memory, written by the final re-prune
+        # kernel itself (the transfer overlaps that kernel)
+        builder.build_host(host, host_out=(ids_host, cnt_host))
         e2e_ev[s][1].record(stream)
     barrier()
     e2e_s = sum(a.elapsed_time(b) for a, b in e2e_ev) / 1e3

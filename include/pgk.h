@@ -159,8 +159,28 @@ int pgk_knn_pools(const float *data, int64_t n, int64_t d,
  * pool does not convert `data` again.  The caller guarantees (e.g. by
  * pgk_detect_u8) that every value of `data` is an integer in [0, 255] and d <= 128. */
 int pgk_knn_pools_u8(const float *data, const uint8_t *data_u8, const int32_t *norms, int64_t n,
-                     int64_t d, int64_t k, int32_t *gt_ids, int32_t *pool_ids, float *pool_dists,
-                     void *ws, size_t ws_bytes, void *stream);
+                     int64_t d, int64_t k, int assigned, int32_t *gt_ids, int32_t *pool_ids,
+                     float *pool_dists, void *ws, size_t ws_bytes, void *stream);
+
+/* Host-data pipeline pieces (package: RngBuilder.build_host): the rows of a
+ * pinned host array reach the device in chunks, and the tile pruning's
+ * center assignment runs per chunk as it lands instead of after the whole
+ * copy.  pgk_tiles_u8_prepare takes the centers (rows 0, s, 2s, ... of the
+ * data, s = pgk_tiles_center_stride(), fp32 on the device, e.g. by
+ * pgk_copy_rows_h2d with a pitch of s rows); pgk_tiles_u8_assign then assigns
+ * rows [row0, row0 + nrows) from their pgk_make_u8 rows and norms; a final
+ * pgk_knn_pools_u8(..., assigned = 1, ...) on the same workspace continues
+ * from there.  pgk_detect_u8_async clears *flag (device int, caller sets it to
+ * 1) when a value of the rows is not an integer in [0, 255]. */
+int64_t pgk_tiles_center_stride(void);
+int pgk_tiles_u8_prepare(void *ws, size_t ws_bytes, int64_t n, int64_t d, int64_t k,
+                         const float *centers, void *stream);
+int pgk_tiles_u8_assign(void *ws, size_t ws_bytes, int64_t n, int64_t d, int64_t k,
+                        const uint8_t *rows_u8, const int32_t *norms, int64_t row0, int64_t nrows,
+                        void *stream);
+int pgk_detect_u8_async(const float *data, int64_t n, int64_t d, int *flag, void *stream);
+int pgk_copy_rows_h2d(void *dst, const void *src_host, int64_t rows, int64_t row_bytes,
+                      int64_t src_pitch, void *stream);
 
 /* Number of query rows that needed the exact float64 fallback scan in the most
  * recent pgk_knn_pools call on this workspace (device int32 inside ws; this

@@ -53,7 +53,7 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None,
             raise RuntimeError(f"nvcc failed on {s}")
         objs.append(obj)
     tmp = lib.with_suffix(".so.tmp")
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs,
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xlinker", "--no-undefined", *objs,
            "-o", str(tmp)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

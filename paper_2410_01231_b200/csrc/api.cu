@@ -69,7 +69,13 @@ int add_reverse_and_prune(const float *, const uint8_t *, const int32_t *, const
 int knn_workspace(int64_t, int64_t, int64_t, int64_t, int, size_t *);
 int knn_pools(const float *, int64_t, int64_t, const float *, int64_t, int64_t, int, int,
               int32_t *, int32_t *, float *, void *, size_t, cudaStream_t,
-              const uint8_t *xu8_in = nullptr, const int32_t *norms_in = nullptr);
+              const uint8_t *xu8_in = nullptr, const int32_t *norms_in = nullptr,
+              bool assigned = false);
+int knn_tiles_prepare(void *, size_t, int64_t, int64_t, int64_t, const float *, cudaStream_t);
+int knn_tiles_assign(void *, size_t, int64_t, int64_t, int64_t, const uint8_t *, const int32_t *,
+                     int64_t, int64_t, cudaStream_t);
+int detect_u8_async(const float *, int64_t, int64_t, int *, cudaStream_t);
+int64_t tiles_center_stride();
 int detect_u8(const float *, int64_t, int64_t, int *, void *, size_t, cudaStream_t);
 int fallback_rows(const void *, int *, cudaStream_t);
 int knn_work(const void *, int64_t, int64_t, int64_t, int64_t, int, unsigned long long *,
@@ -226,12 +232,44 @@ int pgk_knn_pools(const float *data, int64_t n, int64_t d, const float *queries,
 }
 
 int pgk_knn_pools_u8(const float *data, const uint8_t *data_u8, const int32_t *norms, int64_t n,
-                     int64_t d, int64_t k, int32_t *gt_ids, int32_t *pool_ids, float *pool_dists,
-                     void *ws, size_t ws_bytes, void *stream) {
+                     int64_t d, int64_t k, int assigned, int32_t *gt_ids, int32_t *pool_ids,
+                     float *pool_dists, void *ws, size_t ws_bytes, void *stream) {
   PGK_REQUIRE(data && data_u8 && norms && pool_ids && pool_dists && ws, "NULL argument");
   PGK_REQUIRE(d <= 128, "exact-integer rows need d <= 128");
   return knn_pools(data, n, d, nullptr, n, k, 1, PGK_POOL_U8, gt_ids, pool_ids, pool_dists, ws,
-                   ws_bytes, (cudaStream_t)stream, data_u8, norms);
+                   ws_bytes, (cudaStream_t)stream, data_u8, norms, assigned != 0);
+}
+
+int64_t pgk_tiles_center_stride(void) { return tiles_center_stride(); }
+
+int pgk_tiles_u8_prepare(void *ws, size_t ws_bytes, int64_t n, int64_t d, int64_t k,
+                         const float *centers, void *stream) {
+  PGK_REQUIRE(ws && centers, "NULL argument");
+  return knn_tiles_prepare(ws, ws_bytes, n, d, k, centers, (cudaStream_t)stream);
+}
+
+int pgk_tiles_u8_assign(void *ws, size_t ws_bytes, int64_t n, int64_t d, int64_t k,
+                        const uint8_t *rows_u8, const int32_t *norms, int64_t row0, int64_t nrows,
+                        void *stream) {
+  PGK_REQUIRE(ws && rows_u8 && norms, "NULL argument");
+  return knn_tiles_assign(ws, ws_bytes, n, d, k, rows_u8, norms, row0, nrows,
+                          (cudaStream_t)stream);
+}
+
+int pgk_detect_u8_async(const float *data, int64_t n, int64_t d, int *flag, void *stream) {
+  PGK_REQUIRE(data && flag, "NULL argument");
+  return detect_u8_async(data, n, d, flag, (cudaStream_t)stream);
+}
+
+int pgk_copy_rows_h2d(void *dst, const void *src_host, int64_t rows, int64_t row_bytes,
+                      int64_t src_pitch, void *stream) {
+  PGK_REQUIRE(dst && src_host && rows >= 0 && row_bytes > 0 && src_pitch >= row_bytes,
+              "bad strided copy");
+  if (rows == 0) return PGK_OK;
+  PGK_CUDA(cudaMemcpy2DAsync(dst, (size_t)row_bytes, src_host, (size_t)src_pitch,
+                             (size_t)row_bytes, (size_t)rows, cudaMemcpyHostToDevice,
+                             (cudaStream_t)stream));
+  return PGK_OK;
 }
 
 int pgk_knn_work(const void *ws, int64_t n, int64_t nq, int64_t d, int64_t k, int mode,

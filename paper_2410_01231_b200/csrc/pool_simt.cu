@@ -872,7 +872,11 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
                          uint64_t *keys, void *tc_ws, size_t tc_bytes, void *tws,
                          size_t tws_bytes, cudaStream_t stream, bool *handled,
                          unsigned long long *pairs_out, const PoolOut *out,
-                         const uint8_t *xu8_in);
+                         const uint8_t *xu8_in, bool assigned);
+int tiles_u8_prepare(void *tws, size_t tws_bytes, int64_t n, int d, int K, const float *centers,
+                     cudaStream_t stream);
+int tiles_u8_assign(void *tws, size_t tws_bytes, int64_t n, int d, int K, const uint8_t *rows_u8,
+                    const int32_t *norms, int64_t row0, int64_t nrows, cudaStream_t stream);
 
 // xu8_in / norms_in (optional, U8 mode with queries == data): the caller's
 // exact-integer rows (128 B each) and squared norms (pgk_make_u8), used
@@ -880,7 +884,7 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
 int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, int64_t k,
               int exclude_self, int mode, int32_t *gt_ids, int32_t *pool_ids,
               float *pool_dists, void *ws, size_t bytes, cudaStream_t stream,
-              const uint8_t *xu8_in, const int32_t *norms_in) {
+              const uint8_t *xu8_in, const int32_t *norms_in, bool assigned) {
   PGK_REQUIRE(k >= 1, "k must be >= 1");
   PGK_REQUIRE(n >= 1 && d >= 1, "dataset must be non-empty");
   const bool self = (Q == nullptr);
@@ -937,7 +941,8 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
     const PoolOut po{gt_ids, pool_ids, pool_dists};
     if (L.tc_ws && L.tws && self && exclude_self) {
       rc = launch_pool_tiles_u8(X, n, (int)d, L.xnorm, (int)k, L.keys, L.tc_ws, L.tc_bytes,
-                                L.tws, L.tws_bytes, stream, &handled, nullptr, &po, xu8_in);
+                                L.tws, L.tws_bytes, stream, &handled, nullptr, &po, xu8_in,
+                                assigned && xu8_in != nullptr);
       if (rc) return rc;
     }
     if (L.tc_ws && !handled) {
@@ -1012,6 +1017,33 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
       X, n, (int)d, Q, exclude_self, (int)k, vec4, L.fb_list, L.fb_count, gt_ids, pool_ids,
       pool_dists);
   PGK_CHECK_LAUNCH("fallback_kernel");
+  return PGK_OK;
+}
+
+// The staged (chunked) center assignment on the tile workspace inside a
+// pgk_knn_pools workspace (U8 mode, self pool).
+int knn_tiles_prepare(void *ws, size_t bytes, int64_t n, int64_t d, int64_t k,
+                      const float *centers, cudaStream_t stream) {
+  KnnLayout L = knn_layout(ws, bytes, n, n, d, k, PGK_POOL_U8);
+  PGK_REQUIRE(L.total <= bytes && L.tws, "knn workspace has no tile pruning for this shape");
+  return tiles_u8_prepare(L.tws, L.tws_bytes, n, (int)d, (int)k, centers, stream);
+}
+
+int knn_tiles_assign(void *ws, size_t bytes, int64_t n, int64_t d, int64_t k,
+                     const uint8_t *rows_u8, const int32_t *norms, int64_t row0, int64_t nrows,
+                     cudaStream_t stream) {
+  KnnLayout L = knn_layout(ws, bytes, n, n, d, k, PGK_POOL_U8);
+  PGK_REQUIRE(L.total <= bytes && L.tws, "knn workspace has no tile pruning for this shape");
+  return tiles_u8_assign(L.tws, L.tws_bytes, n, (int)d, (int)k, rows_u8, norms, row0, nrows,
+                         stream);
+}
+
+int detect_u8_async(const float *X, int64_t n, int64_t d, int *flag, cudaStream_t stream) {
+  const int64_t total = n * d;
+  if (total == 0) return PGK_OK;
+  unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+  detect_u8_kernel<<<blocks, 256, 0, stream>>>(X, total, flag);
+  PGK_CHECK_LAUNCH("detect_u8_kernel");
   return PGK_OK;
 }
 

@@ -468,6 +468,42 @@ size_t tiles_workspace(int64_t n, int64_t d) { return tiles_layout(nullptr, 0, n
 // rows of the padded, tile-sorted problem (the tc workspace must cover them)
 int64_t tiles_rows(int64_t n) { return tiles_layout(nullptr, 0, n, 1).NPmax; }
 
+// Staged center assignment for rows that arrive in chunks: the centers
+// (rows 0, CSTRIDE, 2 CSTRIDE, ... of the data, fp32, device) first, then each
+// chunk of exact-integer rows (128 B each) with its norms as it lands.
+int64_t tiles_center_stride() { return tiles::CSTRIDE; }
+
+int tiles_u8_prepare(void *tws, size_t tws_bytes, int64_t n, int d, int K, const float *centers,
+                     cudaStream_t stream) {
+  using namespace tiles;
+  PGK_REQUIRE(tiles_supported(n, d, K), "tile pruning does not apply to this shape");
+  Layout L = tiles_layout(tws, tws_bytes, n, d);
+  PGK_REQUIRE(L.bytes <= tws_bytes, "tile workspace too small");
+  PGK_CUDA(cudaMemcpyAsync(L.cen, centers, (size_t)L.C * d * sizeof(float),
+                           cudaMemcpyDeviceToDevice, stream));
+  return launch_norms_u8(L.cen, L.C, d, L.cnorm, stream);
+}
+
+int tiles_u8_assign(void *tws, size_t tws_bytes, int64_t n, int d, int K, const uint8_t *rows_u8,
+                    const int32_t *norms, int64_t row0, int64_t nrows, cudaStream_t stream) {
+  using namespace tiles;
+  PGK_REQUIRE(tiles_supported(n, d, K), "tile pruning does not apply to this shape");
+  PGK_REQUIRE(row0 >= 0 && nrows >= 0 && row0 + nrows <= n, "row range out of bounds");
+  if (nrows == 0) return PGK_OK;
+  Layout L = tiles_layout(tws, tws_bytes, n, d);
+  PGK_REQUIRE(L.bytes <= tws_bytes, "tile workspace too small");
+  bool h = false;
+  // queries = the chunk's u8 rows (the fp32 query pointer is never read)
+  const int rc = launch_pool_tc_u8_lists(L.cen, L.C, d, reinterpret_cast<const float *>(rows_u8),
+                                         nrows, 0, L.cnorm, norms, 1, L.akeys + row0, L.sub_ws,
+                                         L.sub_bytes, stream, nullptr, nullptr, nullptr, 0,
+                                         nullptr, &h, nullptr, 0, 1.0f, nullptr, nullptr, nullptr,
+                                         nullptr, rows_u8);
+  if (rc) return rc;
+  PGK_REQUIRE(h, "tensor-core assignment unavailable");
+  return PGK_OK;
+}
+
 // Runs the whole pruned pool.  *handled = false when pruning does not apply.
 extern uint32_t *g_dense_ostat;
 
@@ -475,7 +511,7 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
                          uint64_t *keys, void *tc_ws, size_t tc_bytes, void *tws,
                          size_t tws_bytes, cudaStream_t stream, bool *handled,
                          unsigned long long *pairs_out, const PoolOut *out,
-                         const uint8_t *xu8_in) {
+                         const uint8_t *xu8_in, bool assigned) {
   using namespace tiles;
   *handled = false;
   if (!tiles_supported(n, d, K)) return PGK_OK;
@@ -487,11 +523,15 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   const int sms = num_sms();
   const int64_t C = L.C;
   const unsigned g = (unsigned)sms * 8;
-  // 1. centers (every 512th row) + exact nearest center of every point (K = 1)
+  // 1. centers (every CSTRIDE-th row) + exact nearest center of every point
+  // (K = 1); `assigned`: already done chunk by chunk (tiles_u8_prepare /
+  // tiles_u8_assign, the host-data pipeline)
+  int rc = PGK_OK;
+  if (!assigned) {
   gather_centers_kernel<<<g, 256, 0, stream>>>(X, n, d, C, L.cen);
   PGK_CHECK_LAUNCH("gather_centers_kernel");
   dbg_stage("gather_centers_kernel", stream);
-  int rc = launch_norms_u8(L.cen, C, d, L.cnorm, stream);
+  rc = launch_norms_u8(L.cen, C, d, L.cnorm, stream);
   if (rc) return rc;
   bool h = false;
   rc = launch_pool_tc_u8_lists(L.cen, C, d, X, n, 0, L.cnorm, xnorm, 1, L.akeys, L.sub_ws,
@@ -500,6 +540,7 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   if (rc) return rc;
   dbg_stage("assign tc", stream);
   if (!h) return PGK_OK;
+  }
   // 2. counting sort by center, every run padded to whole tiles (perm = -1)
   PGK_CUDA(cudaMemsetAsync(L.hist, 0, C * 4, stream));
   PGK_CUDA(cudaMemsetAsync(L.cursor, 0, C * 4, stream));

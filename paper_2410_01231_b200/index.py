@@ -54,6 +54,7 @@ class RngBuilder:
                        torch.empty(n, dtype=I32, device=dev))
         self.order_out = torch.empty(n, dtype=I32, device=dev)
         self.prune_ws = _lib.workspace(kernels.prune_workspace_bytes(n))
+        self._pipe = None  # build_host's buffers, made on first use
 
     def order(self):
         """Locality order of the last pools() call (selection passes only)."""
@@ -84,17 +85,33 @@ class RngBuilder:
         overlaps the kernel instead of following it; the degrees follow with
         one 4-byte-per-row copy.  Both are complete once the stream reaches
         the end of the build."""
+        _check_host_out(host_out, self.n, self.params.M)
+        u8 = self.u8_rows(X)  # exact-integer rows once, for the pool and the selection
+        return self._finish(X, u8, host_out)
+
+    def build_host(self, host: torch.Tensor, host_out=None, chunks: int = 8) -> BuildOutput:
+        """The whole path from a pinned host array (n, d) float32: the rows are
+        copied in `chunks` pieces on a side stream while the current stream
+        converts each landed chunk to exact-integer rows and assigns it to its
+        tile center, so the pool's center assignment no longer waits for the
+        whole copy.  The exact-integer check runs on the device per chunk; if
+        the data turn out not to qualify, the result is recomputed through the
+        float path (one 4-byte read at the end: this call returns with the
+        build complete).  Non-U8 builders copy, then build."""
+        if self.mode != _lib.POOL_U8 or self.d > 128 or self.n < 8 * 128:
+            out = self.build(host.to(_lib.device(), non_blocking=True), host_out)
+            torch.cuda.current_stream().synchronize()
+            return out
+        return _build_host(self, host, host_out, chunks)
+
+    def _finish(self, X, u8, host_out, assigned: bool = False) -> BuildOutput:
         p = self.params
         b_out = self.b_out
         if host_out is not None:
-            h_ids, h_cnt = host_out
-            for t, shape in ((h_ids, (self.n, p.M)), (h_cnt, (self.n,))):
-                if t.device.type != "cpu" or not t.is_pinned() or t.dtype != torch.int32 \
-                        or tuple(t.shape) != shape or not t.is_contiguous():
-                    raise ValueError(f"host_out tensors must be pinned contiguous int32 {shape}")
-            b_out = (h_ids,) + b_out[1:]
-        u8 = self.u8_rows(X)  # exact-integer rows once, for the pool and the selection
-        ids, dists = self.pools(X, u8)
+            b_out = (host_out[0],) + b_out[1:]
+        r = kernels.knn_pools(X, self.K, None, True, self.mode, False, self.pool_ws,
+                              self.pool_out, u8=u8, assigned=assigned)
+        ids, dists = r.pool_ids, r.pool_dists
         order = self.order()
         a = kernels.prune_batch(X, self.cand_off, self.cand_counts, ids, dists,
                                 p.strategy_code, p.kernel_param, p.M, p.M, out=self.a_out, u8=u8,
@@ -107,6 +124,81 @@ class RngBuilder:
         de = torch.stack([a[3].sum(), b[3].sum()])
         ae = torch.stack([a[4].sum(), b[4].sum()])
         return BuildOutput(b[0], b[1], b[2], a[2], de, ae)
+
+
+def _check_host_out(host_out, n: int, M: int) -> None:
+    if host_out is None:
+        return
+    h_ids, h_cnt = host_out
+    for t, shape in ((h_ids, (n, M)), (h_cnt, (n,))):
+        if t.device.type != "cpu" or not t.is_pinned() or t.dtype != torch.int32 \
+                or tuple(t.shape) != shape or not t.is_contiguous():
+            raise ValueError(f"host_out tensors must be pinned contiguous int32 {shape}")
+
+
+class HostPipeline:
+    """RngBuilder.build_host's device buffers and copy stream (one per builder)."""
+
+    def __init__(self, b: "RngBuilder"):
+        dev = _lib.device()
+        self.stride = int(_lib.lib().pgk_tiles_center_stride())
+        self.C = (b.n + self.stride - 1) // self.stride
+        self.X = torch.empty((b.n, b.d), dtype=torch.float32, device=dev)
+        self.cen = torch.empty((self.C, b.d), dtype=torch.float32, device=dev)
+        self.flag = torch.ones(1, dtype=torch.int32, device=dev)
+        self.stream = torch.cuda.Stream(device=dev)
+        self.f32 = None  # float-path builder, made if a dataset is not exact-integer
+
+
+def _build_host(b: "RngBuilder", host: torch.Tensor, host_out, chunks: int):
+    if host.device.type != "cpu" or not host.is_pinned() or host.dtype != torch.float32 \
+            or tuple(host.shape) != (b.n, b.d) or not host.is_contiguous():
+        raise ValueError(f"host data must be a pinned contiguous float32 ({b.n}, {b.d}) tensor")
+    _check_host_out(host_out, b.n, b.params.M)
+    if b._pipe is None:
+        b._pipe = HostPipeline(b)
+    pp, L = b._pipe, _lib.lib()
+    main, cs = torch.cuda.current_stream(), pp.stream
+    n, d, K = b.n, b.d, b.K
+    bounds = [round(i * n / chunks) for i in range(chunks + 1)]
+    spans = list(zip(bounds[:-1], bounds[1:]))
+    # copy stream: the centers (one strided copy), then the rows chunk by chunk
+    cs.wait_stream(main)  # earlier work on these buffers is done
+    ev_c = torch.cuda.Event()
+    evs = []
+    with torch.cuda.stream(cs):
+        _lib.check(L.pgk_copy_rows_h2d(_lib.ptr(pp.cen), _lib.ptr(host), pp.C, d * 4,
+                                       pp.stride * d * 4, _lib.stream_handle()))
+        ev_c.record(cs)
+        for r0, r1 in spans:
+            pp.X[r0:r1].copy_(host[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            evs.append(ev)
+    # current stream: per landed chunk, exact-integer rows + detection + the
+    # chunk's center assignment
+    pp.flag.fill_(1)
+    main.wait_event(ev_c)
+    ws, stream = b.pool_ws, _lib.stream_handle()
+    _lib.check(L.pgk_tiles_u8_prepare(_lib.ptr(ws), ws.numel(), n, d, K, _lib.ptr(pp.cen), stream))
+    xu8, norms = b.u8_out
+    for (r0, r1), ev in zip(spans, evs):
+        main.wait_event(ev)
+        rows = r1 - r0
+        _lib.check(L.pgk_make_u8(_lib.ptr(pp.X[r0:r1]), rows, d, _lib.ptr(xu8[r0:r1]),
+                                 _lib.ptr(norms[r0:r1]), stream))
+        _lib.check(L.pgk_detect_u8_async(_lib.ptr(pp.X[r0:r1]), rows, d, _lib.ptr(pp.flag),
+                                         stream))
+        _lib.check(L.pgk_tiles_u8_assign(_lib.ptr(ws), ws.numel(), n, d, K,
+                                         _lib.ptr(xu8[r0:r1]), _lib.ptr(norms[r0:r1]), r0, rows,
+                                         stream))
+    out = b._finish(pp.X, b.u8_out, host_out, assigned=True)
+    if int(pp.flag.item()) == 0:  # not exact-integer after all: the float path
+        if pp.f32 is None:
+            pp.f32 = RngBuilder(n, d, K, b.params, _lib.POOL_F32)
+        out = pp.f32.build(pp.X, host_out)
+        torch.cuda.current_stream().synchronize()
+    return out
 
 
 def pool_mode(X: torch.Tensor) -> int:

@@ -143,7 +143,7 @@ class PoolResult:
 
 def knn_pools(X: torch.Tensor, k: int, queries=None, exclude_self: bool = True,
               mode: int = _lib.POOL_AUTO, want_gt: bool = True, ws=None,
-              out=None, u8=None) -> PoolResult:
+              out=None, u8=None, assigned: bool = False) -> PoolResult:
     """Exact k-NN pools (pgk_knn_pools); device tensors, no sync (unless
     mode == AUTO, which reads one flag).  u8: optional (rows, norms) from
     make_u8 for the exact-integer self pool (pgk_knn_pools_u8): the pool
@@ -163,8 +163,8 @@ def knn_pools(X: torch.Tensor, k: int, queries=None, exclude_self: bool = True,
     if u8 is not None and Q is None and exclude_self and mode == _lib.POOL_U8:
         xu8, norms = u8
         check(_lib.lib().pgk_knn_pools_u8(
-            ptr(X), ptr(xu8), ptr(norms), n, d, int(k), ptr(gt), ptr(pool_ids), ptr(pool_dists),
-            ptr(ws), ws.numel(), _lib.stream_handle()))
+            ptr(X), ptr(xu8), ptr(norms), n, d, int(k), int(bool(assigned)), ptr(gt),
+            ptr(pool_ids), ptr(pool_dists), ptr(ws), ws.numel(), _lib.stream_handle()))
         return PoolResult(pool_ids, pool_dists, gt, ws)
     check(_lib.lib().pgk_knn_pools(
         ptr(X), n, d, ptr(Q), nq, int(k), int(bool(exclude_self)), int(mode), ptr(gt),

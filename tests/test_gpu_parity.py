@@ -466,3 +466,26 @@ def test_slack_strategy_against_oracle(gen, n, K, R):
             r = prune_all(ds, off, cnt, ids.ravel(), dists.ravel(), PruneParams(M=R))
             np.testing.assert_array_equal(a[0], r[0])
             assert a[3] == r[3]
+
+
+@pytest.mark.parametrize("n,chunks,integer", [(20000, 8, True), (12345, 5, True), (9000, 3, False)])
+def test_build_host_pipeline_equals_device_build(n, chunks, integer):
+    """RngBuilder.build_host (chunked copy, per-chunk u8 rows, device-side
+    exact-integer check, per-chunk tile-center assignment) equals the device
+    build; data that are not exact-integer fall back to the float path."""
+    from paper_2410_01231_b200 import _lib
+    from paper_2410_01231_b200.index import RngBuilder, pool_mode
+    data = synth.cfg2(n)
+    if not integer:
+        data = data + np.float32(0.25)  # same shape, no longer integer-valued
+    X = torch.from_numpy(data).cuda()
+    ref = RngBuilder(n, 128, 64, PruneParams(M=24), pool_mode(X)).build(X)
+    ids, cnt = ref.ids.cpu(), ref.counts.cpu()
+    b = RngBuilder(n, 128, 64, PruneParams(M=24), _lib.POOL_U8)
+    host = torch.from_numpy(data).pin_memory()
+    h_ids = torch.full((n, 24), 7, dtype=torch.int32).pin_memory()
+    h_cnt = torch.zeros(n, dtype=torch.int32).pin_memory()
+    for _ in range(2):  # the second call reuses the pipeline's buffers
+        b.build_host(host, host_out=(h_ids, h_cnt), chunks=chunks)
+        torch.cuda.synchronize()
+        assert torch.equal(h_ids, ids) and torch.equal(h_cnt, cnt)
