@@ -244,14 +244,18 @@ enum { ST_WAIT, ST_MAIN, ST_SLOW, ST_COMPACT, ST_FINAL, ST_NSLOW, ST_NCOMPACT, S
        ST_COUNT };
 
 // DENSE (pass-1 bound mode): no threshold, no survivor lists -- every row
-// stores the exact distance of every column it meets, densely (u32, at most
-// DENSE_TILES tiles per row in the row's CAP x 8-byte slot), for
-// tc_kth_dense_kernel's exact K-th selection.
+// stores every column's distance, densely, as u16 ceil(dist / 128) (exact
+// u8 distances are < 2^23, so < 0xfffe; 0xffff = invalid), at most
+// DENSE_TILES tiles per row in the row's CAP x 8-byte slot, for
+// tc_kth_dense_kernel.  128 x the K-th smallest stored value bounds the K-th
+// smallest distance from above (within 128 of it): half the bytes of u32.
 constexpr int DENSE_TILES = 2 * CAP / BN;
+constexpr int DENSE_Q = 7;  // quantisation: dist / 2^7, rounded up
 
 __device__ __forceinline__ uint32_t dense_val(int dist, int64_t col, int64_t n, int32_t pid,
                                               bool self) {
-  return (col < n && pid >= 0 && !self) ? (uint32_t)dist : 0xffffffffu;
+  return (col < n && pid >= 0 && !self) ? min(((uint32_t)dist + 127u) >> DENSE_Q, 0xfffeu)
+                                        : 0xffffu;
 }
 
 template <bool STATS, bool DENSE>
@@ -500,7 +504,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
           if (DENSE) {
             if (row_ok && t < DENSE_TILES) {
               const int4 *pp = reinterpret_cast<const int4 *>(s.pid[tpar] + c * 32);
-              uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<uint32_t *>(bufs + row * CAP) +
+              uint2 *dst = reinterpret_cast<uint2 *>(reinterpret_cast<uint16_t *>(bufs + row * CAP) +
                                                      t * BN + c * 32);
               const bool es = exclude_self != 0;
 #pragma unroll
@@ -508,12 +512,11 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
                 const int4 w = nyp[v];
                 const int4 pd = perm ? pp[v] : make_int4(0, 0, 0, 0);
                 const int64_t cj = cb + 4 * v;
-                uint4 o;
-                o.x = dense_val(w.x - 2 * (int)r[4 * v] + nx, cj, n, pd.x, es && row == cj);
-                o.y = dense_val(w.y - 2 * (int)r[4 * v + 1] + nx, cj + 1, n, pd.y, es && row == cj + 1);
-                o.z = dense_val(w.z - 2 * (int)r[4 * v + 2] + nx, cj + 2, n, pd.z, es && row == cj + 2);
-                o.w = dense_val(w.w - 2 * (int)r[4 * v + 3] + nx, cj + 3, n, pd.w, es && row == cj + 3);
-                dst[v] = o;
+                const uint32_t a0 = dense_val(w.x - 2 * (int)r[4 * v] + nx, cj, n, pd.x, es && row == cj);
+                const uint32_t a1 = dense_val(w.y - 2 * (int)r[4 * v + 1] + nx, cj + 1, n, pd.y, es && row == cj + 1);
+                const uint32_t a2 = dense_val(w.z - 2 * (int)r[4 * v + 2] + nx, cj + 2, n, pd.z, es && row == cj + 2);
+                const uint32_t a3 = dense_val(w.w - 2 * (int)r[4 * v + 3] + nx, cj + 3, n, pd.w, es && row == cj + 3);
+                dst[v] = make_uint2(a0 | (a1 << 16), a2 | (a3 << 16));
               }
             }
             continue;
@@ -979,20 +982,27 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, 4)
   }
 }
 
-// K-th smallest of a row's dense pass-1 distances (0xffffffff = invalid), to
+// K-th smallest of a row's dense pass-1 values (u16; 0xffff = invalid), to
 // within 1/1024 of the row's value range from above: a warp-wide binary
 // search over register-resident values (per step one compare per value and
 // one REDUX count), keeping count(v <= hi) >= K.  Returns hi.
 template <int VPL>
-__device__ __noinline__ uint32_t kth_dense(const uint32_t *__restrict__ buf, int cnt, int K,
+__device__ __noinline__ uint32_t kth_dense(const uint16_t *__restrict__ buf, int cnt, int K,
                                            int lane) {
+  static_assert(VPL % 2 == 0, "values are loaded in u16 pairs");
   uint32_t v[VPL];
   int nv = 0;
   uint32_t vmin = 0xffffffffu, vmax = 0;
+  const uint32_t *buf2 = reinterpret_cast<const uint32_t *>(buf);  // cnt is a multiple of 128
+#pragma unroll
+  for (int i = 0; i < VPL / 2; ++i) {
+    const int idx = i * 32 + lane;  // word: values 2 idx, 2 idx + 1 (order is irrelevant)
+    const uint32_t w = 2 * idx < cnt ? buf2[idx] : 0xffffffffu;
+    v[2 * i] = (w & 0xffffu) == 0xffffu ? 0xffffffffu : (w & 0xffffu);
+    v[2 * i + 1] = (w >> 16) == 0xffffu ? 0xffffffffu : (w >> 16);
+  }
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
-    const int idx = i * 32 + lane;
-    v[i] = idx < cnt ? buf[idx] : 0xffffffffu;
     if (v[i] != 0xffffffffu) {
       ++nv;
       vmin = min(vmin, v[i]);
@@ -1018,7 +1028,7 @@ __device__ __noinline__ uint32_t kth_dense(const uint32_t *__restrict__ buf, int
 // upper bound of the K-th smallest valid distance, itself an upper bound of
 // the true K-th neighbour distance (the row met real points only), in the library's key
 // format at out_keys[orig_row * K + K - 1].
-__global__ void __launch_bounds__(FIN_WARPS * 32)
+__global__ void __launch_bounds__(FIN_WARPS * 32, 4)
     tc_kth_dense_kernel(const uint64_t *__restrict__ bufs, const int32_t *__restrict__ row_cnt,
                         int64_t nrows, int K, const int32_t *__restrict__ perm,
                         uint64_t *__restrict__ out_keys, uint32_t *__restrict__ ostat) {
@@ -1027,7 +1037,7 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
        r += (int64_t)gridDim.x * FIN_WARPS) {
     const int cnt = row_cnt[r];
     if (cnt < 0) continue;  // padding row
-    const uint32_t *b = reinterpret_cast<const uint32_t *>(bufs + r * CAP);
+    const uint16_t *b = reinterpret_cast<const uint16_t *>(bufs + r * CAP);
     uint32_t kth;
     if (cnt <= 512) kth = kth_dense<16>(b, cnt, K, lane);
     else if (cnt <= 768) kth = kth_dense<24>(b, cnt, K, lane);
@@ -1035,12 +1045,13 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
     else kth = kth_dense<64>(b, cnt, K, lane);
     const int64_t orow = perm ? (int64_t)perm[r] : r;
     if (lane == 0)
-      out_keys[orow * K + K - 1] = kth == 0xffffffffu ? KEY_MAX : pack_key((float)kth, 0x7fffffff);
+      out_keys[orow * K + K - 1] =
+          kth == 0xffffffffu ? KEY_MAX : pack_key((float)(kth << DENSE_Q), 0x7fffffff);
     if (ostat) {  // instrumentation: order statistics K/8, K/4, K/2, K (PGK_TILES_STATS)
       for (int j = 0; j < 4; ++j) {
         const int kj = max(1, K >> (3 - j));
         const uint32_t x = cnt <= 1024 ? kth_dense<32>(b, cnt, kj, lane) : kth_dense<64>(b, cnt, kj, lane);
-        if (lane == 0) ostat[orow * 4 + j] = x;
+        if (lane == 0) ostat[orow * 4 + j] = x == 0xffffffffu ? x : x << DENSE_Q;
       }
     }
   }
