@@ -35,9 +35,13 @@ def ncu(args):
     return subprocess.run(["ncu", "-i", *args], capture_output=True, text=True).stdout
 
 
-def full(path):
+def full(path, kid=None):
+    """Summary of one kernel of a --set full report (kid: its ID, default the first)."""
     det = list(csv.reader(io.StringIO(ncu([path, "--page", "details", "--csv"]))))
     h = det[0]
+    if kid is not None:
+        ii = h.index("ID")
+        det = [h] + [r for r in det[1:] if len(r) > ii and r[ii] == str(kid)]
     print("kernel:", dict(zip(h, det[1])).get("Kernel Name", "")[:120])
     keep = {"Duration", "DRAM Throughput", "Memory Throughput", "L1/TEX Cache Throughput",
             "L2 Cache Throughput", "L2 Hit Rate", "L1/TEX Hit Rate", "Compute (SM) Throughput",
@@ -50,7 +54,11 @@ def full(path):
         if d.get("Metric Name") in keep:
             print(f"  {d['Metric Name']:<40} {d['Metric Value']:>14} {d['Metric Unit']}")
     raw = list(csv.reader(io.StringIO(ncu([path, "--page", "raw", "--csv"]))))
-    rh, rv = raw[0], raw[2] if len(raw) > 2 else raw[1]
+    rh = raw[0]
+    rows = raw[2:] if len(raw) > 2 else raw[1:]
+    if kid is not None and "ID" in rh:
+        rows = [r for r in rows if r[rh.index("ID")] == str(kid)] or rows
+    rv = rows[0]
     for a, b in zip(rh, rv):
         if a in ("dram__bytes_read.sum", "dram__bytes_write.sum",
                  "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
@@ -90,4 +98,4 @@ def full(path):
 
 
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full}[sys.argv[1]](*sys.argv[2:])
