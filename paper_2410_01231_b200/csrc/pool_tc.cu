@@ -40,9 +40,6 @@ constexpr int STAGES = 2;       // B-tile ring depth
 #endif
 
 constexpr int ACC = TC_ACC;     // TMEM accumulator stages (128 columns each, by tile)
-#ifndef TC_PAIRLD
-#define TC_PAIRLD 0
-#endif
 #ifndef TC_PARTS
 #define TC_PARTS 2
 #endif
@@ -464,10 +461,6 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
         const int aslot = (int)(g % ACC);
         const uint32_t acc_phase = (g / ACC) & 1;
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + aslot * BN;
-#if TC_PAIRLD
-        static_assert(CPP == 2, "paired TMEM loads need 2-chunk parts");
-        uint32_t rn[32];
-#endif
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           if (c == 0) mbar_wait(&s.nfull[tpar], (g / NYBUF) & 1);  // the tile's norms / ids
@@ -483,22 +476,10 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
             PGK_TICK(ST_WAIT);
           }
           uint32_t r[32];
-#if TC_PAIRLD
-          // both chunks of a part in one TMEM round trip
-          if ((c & 1) == 0) {
-            tmem_ld32(tbase + c * 32, r);
-            tmem_ld32(tbase + (c + 1) * 32, rn);
-            tmem_wait_ld_regs(r);
-            tmem_wait_ld_regs(rn);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = rn[i];
-          }
-#else
-          // (co-resident CTAs hide the TMEM-load latency; one chunk in flight)
+          // (co-resident CTAs hide the TMEM-load latency; one chunk in flight;
+          // two loads per round trip measured no faster)
           tmem_ld32(tbase + c * 32, r);
           tmem_wait_ld();
-#endif
           const int64_t cb = col0 + c * 32;
           const int4 *nyp = reinterpret_cast<const int4 *>(s.ny[tpar] + c * 32);
           if (DENSE) {
