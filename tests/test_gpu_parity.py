@@ -489,3 +489,33 @@ def test_build_host_pipeline_equals_device_build(n, chunks, integer):
         b.build_host(host, host_out=(h_ids, h_cnt), chunks=chunks)
         torch.cuda.synchronize()
         assert torch.equal(h_ids, ids) and torch.equal(h_cnt, cnt)
+
+
+@pytest.mark.parametrize("strategy,alpha", [("rng", 60.0), ("alpha", 66.0)])
+def test_reverse_pass_union_sizes_through_pair_single_and_hub_paths(strategy, alpha):
+    """Phase B on exact-integer rows whose unions span 0..~400 candidates: the
+    paired Gram kernel (<= 64), the single-point Gram kernel (65..128) and the
+    per-warp hub kernel (> 128), against the oracle (rows, counters)."""
+    rng = np.random.default_rng(21)
+    n, M = 4000, 32
+    data = synth.cfg2(n)
+    ds = Dataset.from_array(data)
+    # phase-A-like rows: per-row degree 0..M, targets Zipf-skewed (hubs)
+    counts = rng.integers(0, M + 1, n).astype(np.int32)
+    ids = np.full((n, M), -1, np.int32)
+    dists = np.full((n, M), np.inf, np.float32)
+    for u in range(n):
+        c = counts[u]
+        cand = np.unique(np.minimum(rng.zipf(1.6, 3 * M) - 1, n - 1))
+        cand = cand[cand != u][:c]
+        counts[u] = len(cand)
+        d = ((data[cand].astype(np.float64) - data[u]) ** 2).sum(1).astype(np.float32)
+        o = np.lexsort((cand, d))
+        ids[u, :len(cand)] = cand[o]
+        dists[u, :len(cand)] = d[o]
+    params = PruneParams(M=M, alpha=alpha, strategy=strategy)
+    got = add_reverse_and_prune(ds, ids, dists, counts, params)
+    want = oracle.add_reverse_and_prune(data, ids, dists, counts, M, strategy, alpha)
+    for i in range(3):
+        np.testing.assert_array_equal(got[i], want[i])
+    assert got[3] == want[3] and got[4] == want[4]
