@@ -60,7 +60,7 @@ constexpr int GUESSED = 1 << 30;  // row_cnt flag: the row ran under a guessed t
 struct __align__(1024) Smem {
   uint8_t a[BM * KB];
   uint8_t b[STAGES][TILE_BYTES];
-  int32_t sv[4][32 * 36];  // per epilogue warp: one chunk of s values per lane
+  int32_t sv[4][32 * 36];  // per epilogue warp: one chunk of dot products per lane
   // |x|^2 and original ids (pruned path) of the tile's columns, 3 buffers by
   // running tile count: the MMA warp prefetches tile g+1's while the
   // epilogue may still read tile g-1's
@@ -548,21 +548,21 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
               continue;
             }
             const bool track = K > 1 && tau == KEY_MAX && mask;
+            // stage the raw dot products (s_j = |x_j|^2 - 2 sv[j] is formed
+            // per survivor from the tile's norms)
             if (mask) {
 #pragma unroll
-              for (int v = 0; v < 8; ++v) {
-                const int4 w = nyp[v];
-                int4 o;
-                o.x = w.x - 2 * (int)r[4 * v];
-                o.y = w.y - 2 * (int)r[4 * v + 1];
-                o.z = w.z - 2 * (int)r[4 * v + 2];
-                o.w = w.w - 2 * (int)r[4 * v + 3];
-                reinterpret_cast<int4 *>(sv)[v] = o;
-              }
+              for (int v = 0; v < 8; ++v)
+                reinterpret_cast<int4 *>(sv)[v] =
+                    make_int4((int)r[4 * v], (int)r[4 * v + 1], (int)r[4 * v + 2], (int)r[4 * v + 3]);
             }
             __syncwarp();
+            const int32_t *tny = s.ny[tpar] + c * 32;
             if (track) {  // rare: rows still without a threshold
-              for (unsigned mm = mask; mm; mm &= mm - 1) smax = max(smax, sv[__ffs(mm) - 1]);
+              for (unsigned mm = mask; mm; mm &= mm - 1) {
+                const int j = __ffs(mm) - 1;
+                smax = max(smax, tny[j] - 2 * sv[j]);
+              }
             }
             // room for this chunk's survivors in every row of the warp
             unsigned need = __ballot_sync(0xffffffffu, cnt + __popc(mask) > CAP);
@@ -589,7 +589,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
               for (unsigned mm = mask; mm; mm &= mm - 1) {
                 const int j = __ffs(mm) - 1;
                 const int32_t cid = perm ? s.pid[tpar][c * 32 + j] : (int32_t)(cb + j);
-                *mybuf++ = ((uint64_t)(uint32_t)(sv[j] + nx) << 32) | (uint32_t)cid;
+                *mybuf++ = ((uint64_t)(uint32_t)(tny[j] - 2 * sv[j] + nx) << 32) | (uint32_t)cid;
               }
             }
             cnt += __popc(mask);
