@@ -518,9 +518,14 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
             // exact survivor masks: lane j vouches for column cb + j (inside
             // the data, not a padding slot of the tile sort), and a row never
             // keeps itself
-            const int64_t colj = cb + lane;
-            const int32_t cidj = perm ? s.pid[tpar][c * 32 + lane] : (int32_t)colj;
-            mask &= __ballot_sync(0xffffffffu, colj < n && cidj >= 0);
+            // padding slots and columns past n carry a huge |x|^2 (0x3f3f3f3f),
+            // so no finite threshold passes them; only rows still without one
+            // need the explicit column check
+            if (__any_sync(0xffffffffu, tp >= 0x3f000000)) {
+              const int64_t colj = cb + lane;
+              const int32_t cidj = perm ? s.pid[tpar][c * 32 + lane] : (int32_t)colj;
+              mask &= __ballot_sync(0xffffffffu, colj < n && cidj >= 0);
+            }
             if (exclude_self && row >= cb && row < cb + 32) mask &= ~(1u << (int)(row - cb));
             if (K == 1) {  // nearest neighbour only: the threshold IS the answer
               // branch-free minimum (dist, id) key over the chunk's survivors
