@@ -180,12 +180,19 @@ __global__ void tile_stats_kernel(const uint8_t *__restrict__ xs, const int32_t 
   }
 }
 
-// dc[Q][T] = |c_Q - c_T| for all tile pairs: register-tiled fp32 direct
-// difference (FMA), relative error <= (d+2) 2^-24 on dc^2, covered by DC_MARGIN.
+// dc[Q][T] = |c_Q - c_T| for all tile pairs, register-tiled fp32.
+//  * direct difference (GRAM = false): FSUB + FFMA per term, relative error
+//    <= (d+2) 2^-24 on dc^2, covered by DC_MARGIN;
+//  * norm expansion (GRAM = true; u8 centroids, whose norms are only ~25x the
+//    distances): one FFMA per term, |approx - dc^2| <= (d+8) 2^-24 (|c_Q|^2 +
+//    |c_T|^2) (the dot, the norms' and the final roundings), subtracted before
+//    the square root, so dc is a lower bound (DC_MARGIN covers the sqrt).
 constexpr double DC_MARGIN = 2e-5;
 constexpr int DB = 64, DK = 32;
+template <bool GRAM>
 __global__ void __launch_bounds__(256)
-    tile_dist_kernel(const float *__restrict__ cent, int64_t T, int d, float *__restrict__ dc) {
+    tile_dist_kernel(const float *__restrict__ cent, int64_t T, int d, float *__restrict__ dc,
+                     const float *__restrict__ cn) {
   __shared__ float sa[DK][DB + 1], sb[DK][DB + 1];
   __shared__ float st[DB][DB + 1];  // transposed block (mirror write)
   // dc is symmetric bit for bit ((a-b)^2 == (b-a)^2, same FMA order): only
@@ -210,8 +217,12 @@ __global__ void __launch_bounds__(256)
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float t_ = a[i] - b[j];
-          acc[i][j] = fmaf(t_, t_, acc[i][j]);
+          if (GRAM) {
+            acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+          } else {
+            const float t_ = a[i] - b[j];
+            acc[i][j] = fmaf(t_, t_, acc[i][j]);
+          }
         }
     }
     __syncthreads();
@@ -221,7 +232,14 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t q = q0 + ty * 4 + i, t = t0 + tx + 16 * j;
-      const float v = sqrtf(acc[i][j]);
+      float v;
+      if (GRAM) {
+        const double nn = (q < T && t < T) ? (double)cn[q] + (double)cn[t] : 0.0;
+        const double e = (double)(d + 8) * 5.9604644775390625e-08 * 1.01 * nn;
+        v = (float)sqrt(fmax(nn - 2.0 * (double)acc[i][j] - e, 0.0));
+      } else {
+        v = sqrtf(acc[i][j]);
+      }
       st[tx + 16 * j][ty * 4 + i] = v;
       if (q < T && t < T) dc[q * T + t] = v;
     }
@@ -230,6 +248,23 @@ __global__ void __launch_bounds__(256)
   for (int e = threadIdx.x; e < DB * DB; e += 256) {
     const int r = e / DB, c = e % DB;  // mirror row t0 + r, column q0 + c
     if (t0 + r < T && q0 + c < T) dc[(t0 + r) * T + q0 + c] = st[r][c];
+  }
+}
+
+// fp32 squared norms of the (fp32) centroids, float64 sums rounded once
+__global__ void cent_norms_kernel(const float *__restrict__ cent, int64_t T, int d,
+                                  float *__restrict__ cn) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < T;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double s = 0.0;
+    for (int k = lane; k < d; k += 32) {
+      const double v = (double)cent[t * d + k];
+      s += v * v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) cn[t] = (float)s;
   }
 }
 
@@ -388,7 +423,7 @@ static float seed_shrink() {
 }
 
 struct Layout {
-  float *cen, *cent, *dcm;
+  float *cen, *cent, *dcm, *cn;
   int32_t *cnorm, *hist, *cursor, *assign, *perm, *ns, *size, *lists, *lens, *fail, *lens2;
   uint8_t *fail_rows;
   int64_t *off, *scan_tmp;
@@ -436,6 +471,7 @@ static tiles::Layout tiles_layout(void *ws, size_t bytes, int64_t n, int64_t d) 
   L.xs = c.take<uint8_t>((size_t)NP * 128);
   L.ns = c.take<int32_t>(NP + 128);
   L.cent = c.take<float>((size_t)T * d);
+  L.cn = c.take<float>(T);
   L.rad = c.take<double>(T);
   L.size = c.take<int32_t>(T);
   L.lists = c.take<int32_t>((size_t)T * T);
@@ -575,8 +611,10 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   PGK_CHECK_LAUNCH("tile_stats_kernel");
   dbg_stage("tile_stats_kernel", stream);
   PGK_CUDA(cudaMemsetAsync(L.total, 0, 4 * sizeof(unsigned long long), stream));
-  tile_dist_kernel<<<dim3((unsigned)((T + DB - 1) / DB), (unsigned)((T + DB - 1) / DB)), 256, 0,
-                     stream>>>(L.cent, T, d, L.dcm);
+  cent_norms_kernel<<<g, 256, 0, stream>>>(L.cent, T, d, L.cn);
+  PGK_CHECK_LAUNCH("cent_norms_kernel");
+  tile_dist_kernel<true><<<dim3((unsigned)((T + DB - 1) / DB), (unsigned)((T + DB - 1) / DB)),
+                            256, 0, stream>>>(L.cent, T, d, L.dcm, L.cn);
   PGK_CHECK_LAUNCH("tile_dist_kernel");
   dbg_stage("tile_dist_kernel", stream);
   // 4. pass 1: exact top-K over each query tile's NEAR nearest tiles -> U_Q
@@ -970,8 +1008,8 @@ int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64
   tile_stats_f32_kernel<<<g, 256, 0, stream>>>(L.xs, L.perm, d, T, L.cent, L.rad, L.size);
   PGK_CHECK_LAUNCH("tile_stats_f32_kernel");
   PGK_CUDA(cudaMemsetAsync(L.total, 0, 4 * sizeof(unsigned long long), stream));
-  tile_dist_kernel<<<dim3((unsigned)((T + DB - 1) / DB), (unsigned)((T + DB - 1) / DB)), 256, 0,
-                     stream>>>(L.cent, T, d, L.dcm);
+  tile_dist_kernel<false><<<dim3((unsigned)((T + DB - 1) / DB), (unsigned)((T + DB - 1) / DB)),
+                            256, 0, stream>>>(L.cent, T, d, L.dcm, nullptr);
   PGK_CHECK_LAUNCH("tile_dist_kernel");
   dbg_stage("tile_dist_kernel", stream);
   // 4. pass 1: top-K over each query tile's nearest tiles -> U_Q
