@@ -193,7 +193,10 @@ template <bool GRAM>
 __global__ void __launch_bounds__(256)
     tile_dist_kernel(const float *__restrict__ cent, int64_t T, int d, float *__restrict__ dc,
                      const float *__restrict__ cn) {
-  __shared__ float sa[DK][DB + 1], sb[DK][DB + 1];
+  // rows padded to 68 floats: 16-byte aligned, so each thread's 4 rows and 4
+  // columns of a k-step are one LDS.128 each
+  __shared__ __align__(16) float sa[DK][DB + 4];
+  __shared__ __align__(16) float sb[DK][DB + 4];
   __shared__ float st[DB][DB + 1];  // transposed block (mirror write)
   // dc is symmetric bit for bit ((a-b)^2 == (b-a)^2, same FMA order): only
   // blocks on or above the diagonal are computed, and mirrored
@@ -210,9 +213,9 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
 #pragma unroll 8
     for (int k = 0; k < DK; ++k) {
-      float a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) { a[i] = sa[k][ty * 4 + i]; b[i] = sb[k][tx + 16 * i]; }
+      const float4 a4 = *reinterpret_cast<const float4 *>(&sa[k][ty * 4]);
+      const float4 b4 = *reinterpret_cast<const float4 *>(&sb[k][tx * 4]);
+      const float a[4] = {a4.x, a4.y, a4.z, a4.w}, b[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(256)
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int64_t q = q0 + ty * 4 + i, t = t0 + tx + 16 * j;
+      const int64_t q = q0 + ty * 4 + i, t = t0 + tx * 4 + j;
       float v;
       if (GRAM) {
         const double nn = (q < T && t < T) ? (double)cn[q] + (double)cn[t] : 0.0;
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(256)
       } else {
         v = sqrtf(acc[i][j]);
       }
-      st[tx + 16 * j][ty * 4 + i] = v;
+      st[tx * 4 + j][ty * 4 + i] = v;
       if (q < T && t < T) dc[q * T + t] = v;
     }
   if (blockIdx.x == blockIdx.y) return;
