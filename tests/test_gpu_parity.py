@@ -519,3 +519,55 @@ def test_reverse_pass_union_sizes_through_pair_single_and_hub_paths(strategy, al
     for i in range(3):
         np.testing.assert_array_equal(got[i], want[i])
     assert got[3] == want[3] and got[4] == want[4]
+
+
+@pytest.mark.parametrize("strategy,alpha", [("rng", 60.0), ("alpha", 66.0)])
+def test_full_scale_cfg2_build_through_the_bench_path(strategy, alpha):
+    """Config 2 at its full size (1M x 128, K=128, R=32, rng) through the bench's
+    RngBuilder: the pools of 300 seeded rows equal the oracle's exact k-NN;
+    every pool row is sorted by (dist, id), self-free, duplicate-free and its
+    fp32 distances equal a direct recomputation; phases A and B over ALL 1M
+    rows equal the oracle's (ids, dists, degrees, dist_evals) when fed the
+    GPU's pools (SURVEY 8(d): full-N phases A+B beside seeded pool rows);
+    the alpha case covers the angle counters too."""
+    from paper_2410_01231_b200.index import RngBuilder, pool_mode
+    c = synth.CONFIGS[2]
+    n, K, R = c["n"], c["K"], c["R"]
+    data = c["gen"](n, n)
+    X = torch.from_numpy(data).cuda()
+    b = RngBuilder(n, data.shape[1], K, PruneParams(M=R, alpha=alpha, strategy=strategy),
+                   pool_mode(X))
+    out = b.build(X)
+    torch.cuda.synchronize()
+    p_ids, p_d = (t.cpu().numpy() for t in b.pool_out[:2])
+    # pool properties on every row (direct-difference fp32 sums of integers
+    # below 2^24 are exact, so the recomputation is the reference's value)
+    for r0 in range(0, n, 8192):
+        r1 = min(n, r0 + 8192)
+        ii = b.pool_out[0][r0:r1].long()
+        dd = ((X[ii] - X[r0:r1, None, :]) ** 2).sum(-1)
+        assert torch.equal(dd, b.pool_out[1][r0:r1]), r0
+    rows = np.arange(n)[:, None]
+    assert (p_ids != rows).all() and (p_ids >= 0).all()
+    key_sorted = (p_d[:, 1:] > p_d[:, :-1]) | ((p_d[:, 1:] == p_d[:, :-1]) & (p_ids[:, 1:] > p_ids[:, :-1]))
+    assert key_sorted.all()
+    sel = np.sort(np.random.default_rng(202).choice(n, 300, replace=False))
+    o_ids, o_d = oracle.knn_pools(data, K, rows=sel)
+    np.testing.assert_array_equal(p_ids[sel], o_ids)
+    np.testing.assert_array_equal(p_d[sel], o_d)
+    # phases A and B over all rows against the oracle on the same pools
+    off = np.arange(n + 1, dtype=np.int64) * K
+    cnt = np.full(n, K, np.int32)
+    oa = oracle.prune_all(data, off, cnt, p_ids.ravel(), p_d.ravel(), R, strategy, alpha)
+    np.testing.assert_array_equal(b.a_out[0].cpu().numpy(), oa[0])
+    np.testing.assert_array_equal(b.a_out[1].cpu().numpy(), oa[1])
+    np.testing.assert_array_equal(out.a_counts.cpu().numpy(), oa[2])
+    ob = oracle.add_reverse_and_prune(data, oa[0], oa[1], oa[2], R, strategy, alpha)
+    np.testing.assert_array_equal(out.ids.cpu().numpy(), ob[0])
+    np.testing.assert_array_equal(out.dists.cpu().numpy(), ob[1])
+    np.testing.assert_array_equal(out.counts.cpu().numpy(), ob[2])
+    de = out.dist_evals.cpu().numpy()
+    assert int(de[0]) == oa[3] and int(de[1]) == ob[3]
+    ae = out.angle_evals.cpu().numpy()
+    assert int(ae[0]) == oa[4] and int(ae[1]) == ob[4]
+    assert strategy == "alpha" or oa[4] == ob[4] == 0
