@@ -134,49 +134,58 @@ __global__ void gather_sorted_u8_kernel(const uint8_t *__restrict__ xu8,
   }
 }
 
-// warp per tile: float64 centroid of the real rows (stored fp32) and radius
-// against the stored centroid (float64, inflated)
-__global__ void tile_stats_kernel(const uint8_t *__restrict__ xs, const int32_t *__restrict__ perm,
-                                  int d, int64_t ntiles, float *__restrict__ cent,
-                                  double *__restrict__ rad, int32_t *__restrict__ size) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
-       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+// block (TB threads) per tile: centroid of the real rows (thread = dimension:
+// an exact integer column sum, divided in float64 and stored fp32) and the
+// radius against the stored centroid (thread = row: float64 squared distance,
+// block max, inflated).  Padding rows are all-zero bytes.
+__global__ void __launch_bounds__(TB) tile_stats_kernel(const uint8_t *__restrict__ xs,
+                                                        const int32_t *__restrict__ perm, int d,
+                                                        int64_t ntiles, float *__restrict__ cent,
+                                                        double *__restrict__ rad,
+                                                        int32_t *__restrict__ size) {
+  __shared__ float c_s[TB];
+  __shared__ uint8_t ok_s[TB];
+  __shared__ double wmax[TB / 32];
+  const int j = threadIdx.x, lane = j & 31;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t r0 = t * TB;
-    double acc[4] = {0, 0, 0, 0};
-    int cnt = 0;
-    for (int i = 0; i < TB; ++i) {
-      if (perm[r0 + i] < 0) continue;
-      ++cnt;
-      const uint8_t *row = xs + (r0 + i) * 128;
+    const bool ok = perm[r0 + j] >= 0;
+    ok_s[j] = ok;
+    const int cnt = __syncthreads_count(ok);
+    int sum = 0;
+#pragma unroll 8
+    for (int i = 0; i < TB; ++i)
+      if (ok_s[i]) sum += xs[(r0 + i) * 128 + j];
+    const float c = (cnt && j < d) ? (float)((double)sum / cnt) : 0.f;
+    if (j < d) cent[t * d + j] = c;
+    c_s[j] = c;
+    __syncthreads();
+    double s = 0.0;
+    if (ok) {
+      const uint4 *row = reinterpret_cast<const uint4 *>(xs + (r0 + j) * 128);
+#pragma unroll 2
+      for (int v = 0; v < 8; ++v) {
+        const uint4 w = row[v];
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-      for (int k = 0; k < 4; ++k) acc[k] += (double)row[lane + 32 * k];
-    }
-    float c[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      c[k] = cnt ? (float)(acc[k] / cnt) : 0.f;
-      if (lane + 32 * k < d) cent[t * d + lane + 32 * k] = c[k];
-      if (lane + 32 * k >= d) c[k] = 0.f;
-    }
-    double rmax = 0.0;
-    for (int i = 0; i < TB; ++i) {
-      if (perm[r0 + i] < 0) continue;
-      const uint8_t *row = xs + (r0 + i) * 128;
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double t_ = (double)row[lane + 32 * k] - (double)c[k];
-        s += t_ * t_;
+        for (int q = 0; q < 16; ++q) {
+          const double t_ = (double)((ww[q >> 2] >> (8 * (q & 3))) & 0xffu) - (double)c_s[16 * v + q];
+          s += t_ * t_;
+        }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      rmax = fmax(rmax, s);
     }
-    if (lane == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+    if (lane == 0) wmax[j >> 5] = s;
+    __syncthreads();
+    if (j == 0) {
+      double rmax = 0.0;
+#pragma unroll
+      for (int w = 0; w < TB / 32; ++w) rmax = fmax(rmax, wmax[w]);
       rad[t] = sqrt(rmax) * (1.0 + MARGIN) + 1e-12;
       size[t] = cnt;
     }
+    __syncthreads();
   }
 }
 
@@ -610,7 +619,8 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   dbg_stage("gather_sorted_kernel", stream);
   fill_i32_kernel<<<1, 128, 0, stream>>>(L.ns + NP, 128, 0x3f3f3f3f);
   PGK_CHECK_LAUNCH("fill_i32_kernel");
-  tile_stats_kernel<<<g, 256, 0, stream>>>(L.xs, L.perm, d, T, L.cent, L.rad, L.size);
+  tile_stats_kernel<<<(unsigned)std::min<int64_t>(T, (int64_t)sms * 16), TB, 0, stream>>>(
+      L.xs, L.perm, d, T, L.cent, L.rad, L.size);
   PGK_CHECK_LAUNCH("tile_stats_kernel");
   dbg_stage("tile_stats_kernel", stream);
   PGK_CUDA(cudaMemsetAsync(L.total, 0, 4 * sizeof(unsigned long long), stream));
