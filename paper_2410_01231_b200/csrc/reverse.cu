@@ -39,15 +39,15 @@ int launch_prune(const float *X, const uint8_t *xu8, const int32_t *norms, int64
 constexpr int SORT_WARPS = 8;
 constexpr int SORT_SMEM_KEYS = 512;  // per-warp in-register sort capacity (16 keys per lane)
 
+// warp per phase-A row, lane per entry (no per-element division)
 __global__ void rev_count_kernel(const int32_t *__restrict__ ids,
                                  const int32_t *__restrict__ counts, int64_t n,
                                  int width, int32_t *__restrict__ rev_cnt) {
-  const int64_t total = n * width;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t u = e / width;
-    int j = (int)(e - u * width);
-    if (j < counts[u]) atomicAdd(rev_cnt + ids[e], 1);
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += nw) {
+    const int c = counts[u];
+    for (int j = lane; j < c; j += 32) atomicAdd(rev_cnt + ids[u * width + j], 1);
   }
 }
 
@@ -137,23 +137,38 @@ int exclusive_scan(const int64_t *in, int64_t *out, int64_t m, int64_t *scratch,
   return PGK_OK;
 }
 
+// own entries and reverse entries into the merged slices: warp per two
+// phase-A rows (lane per entry), so each lane has two slot atomics in flight
 __global__ void scatter_kernel(const int32_t *__restrict__ ids,
                                const float *__restrict__ dists,
                                const int32_t *__restrict__ counts, int64_t n,
                                int width, const int64_t *__restrict__ mrg_off,
                                int32_t *__restrict__ rev_left,
                                uint64_t *__restrict__ keys) {
-  const int64_t total = n * width;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t u = e / width;
-    int j = (int)(e - u * width);
-    if (j >= counts[u]) continue;
-    int32_t v = ids[e];
-    float dd = dists[e];
-    keys[mrg_off[u] + j] = pack_key(dd, v);  // own entry
-    int slot = atomicSub(rev_left + v, 1) - 1;
-    keys[mrg_off[v] + counts[v] + slot] = pack_key(dd, (int32_t)u);  // reverse
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += 2 * nw) {
+    const int64_t u2 = u + nw;
+    const int c1 = counts[u], c2 = u2 < n ? counts[u2] : 0;
+    const int64_t o1 = mrg_off[u], o2 = u2 < n ? mrg_off[u2] : 0;
+    for (int j = lane; j < max(c1, c2); j += 32) {
+      const bool p1 = j < c1, p2 = j < c2;
+      const int32_t v1 = p1 ? ids[u * width + j] : 0, v2 = p2 ? ids[u2 * width + j] : 0;
+      const float d1 = p1 ? dists[u * width + j] : 0.f, d2 = p2 ? dists[u2 * width + j] : 0.f;
+      int s1 = 0, s2 = 0;
+      if (p1) s1 = atomicSub(rev_left + v1, 1) - 1;
+      if (p2) s2 = atomicSub(rev_left + v2, 1) - 1;
+      const int64_t b1 = p1 ? mrg_off[v1] + counts[v1] : 0;
+      const int64_t b2 = p2 ? mrg_off[v2] + counts[v2] : 0;
+      if (p1) {
+        keys[o1 + j] = pack_key(d1, v1);                  // own entry
+        keys[b1 + s1] = pack_key(d1, (int32_t)u);         // reverse
+      }
+      if (p2) {
+        keys[o2 + j] = pack_key(d2, v2);
+        keys[b2 + s2] = pack_key(d2, (int32_t)u2);
+      }
+    }
   }
 }
 
@@ -368,10 +383,12 @@ int add_reverse_and_prune(const float *X, const uint8_t *xu8, const int32_t *nor
   const int sms = num_sms();
   const int64_t edges = n * a_width;
   const unsigned eblocks = (unsigned)std::min<int64_t>((edges + 255) / 256, (int64_t)sms * 16);
+  // warp-per-row kernels (rev_count, scatter): one warp per 2 rows at most
+  const unsigned rblocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 15) / 16, (int64_t)sms * 16));
 
   PGK_CUDA(cudaMemsetAsync(L.rev_cnt, 0, sizeof(int32_t) * n, stream));
   PGK_CUDA(cudaMemsetAsync(L.long_count, 0, sizeof(int32_t), stream));
-  rev_count_kernel<<<eblocks, 256, 0, stream>>>(a_ids, a_counts, n, (int)a_width, L.rev_cnt);
+  rev_count_kernel<<<rblocks, 256, 0, stream>>>(a_ids, a_counts, n, (int)a_width, L.rev_cnt);
   PGK_CHECK_LAUNCH("rev_count_kernel");
 
   // mrg_off[u] = sum_{t<u} (counts[t] + rev_cnt[t]); mrg_off[n] = total
@@ -382,7 +399,7 @@ int add_reverse_and_prune(const float *X, const uint8_t *xu8, const int32_t *nor
   PGK_CUDA(cudaMemcpyAsync(L.rev_left, L.rev_cnt, sizeof(int32_t) * n,
                            cudaMemcpyDeviceToDevice, stream));
 
-  scatter_kernel<<<eblocks, 256, 0, stream>>>(a_ids, a_dists, a_counts, n, (int)a_width,
+  scatter_kernel<<<rblocks, 256, 0, stream>>>(a_ids, a_dists, a_counts, n, (int)a_width,
                                               L.mrg_off, L.rev_left, L.keys);
   PGK_CHECK_LAUNCH("scatter_kernel");
 
