@@ -24,6 +24,7 @@ import os
 import statistics
 import subprocess
 import sys
+import threading
 import time
 from pathlib import Path
 
@@ -60,14 +61,60 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region."""
+    """SM clock and throttle-reason sampling during the timed region: an NVML
+    thread every 2 ms (the region is ~200 ms), else nvidia-smi -lms 20."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.proc = None
+        self.nvml = None
         self.index = index
+        self.rows = []
         self.path = Path(f"/tmp/pgk_clocks_{os.getpid()}.csv")
 
+    def _nvml_index(self) -> int:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            ids = [x.strip() for x in vis.split(",") if x.strip()]
+            if self.index < len(ids) and ids[self.index].isdigit():
+                return int(ids[self.index])
+        return self.index
+
+    def _nvml_start(self) -> bool:
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self._nvml_index())
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        except Exception:
+            return False
+        masks = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                 N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+        self.stop = threading.Event()
+
+        def run():
+            while not self.stop.is_set():
+                try:
+                    sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                    util = N.nvmlDeviceGetUtilizationRates(h).gpu
+                    r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((float(sm), float(mx), float(util),
+                                      ["Active" if r & m else "Not Active" for m in masks]))
+                except Exception:
+                    pass
+                time.sleep(0.002)
+
+        self.nvml = threading.Thread(target=run, daemon=True)
+        self.nvml.start()
+        t0 = time.time()
+        while not self.rows and time.time() - t0 < 2.0:
+            time.sleep(0.002)
+        return True
+
     def __enter__(self):
+        if self._nvml_start():
+            return self
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(
@@ -91,6 +138,9 @@ class Clocks:
         return self
 
     def __exit__(self, *a):
+        if self.nvml is not None:
+            self.stop.set()
+            self.nvml.join(timeout=1.0)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -100,26 +150,28 @@ class Clocks:
             self.f.close()
 
     def summary(self):
-        if self.proc is None or not self.path.exists():
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        rows = []
-        for line in self.path.read_text().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                rows.append((float(parts[0]), float(parts[1]), float(parts[3]), parts[4:8]))
-            except ValueError:
-                continue
+        rows = list(self.rows)
+        source = "nvml"
+        if self.nvml is None:
+            source = "nvidia-smi"
+            if self.proc is None or not self.path.exists():
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            for line in self.path.read_text().splitlines():
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 8:
+                    continue
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), float(parts[3]), parts[4:8]))
+                except ValueError:
+                    continue
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         loaded = [r for r in rows if r[2] >= 50] or rows
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[3])
+        reasons = sorted({self.NAMES[i] for r in loaded for i, v in enumerate(r[3])
                           if v.lower() == "active"})
         return {"sm_mhz": statistics.median(r[0] for r in loaded),
                 "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
-                "samples": len(loaded)}
+                "samples": len(loaded), "source": source}
 
 
 def measured_traffic(kernel: str, cfg: int, n: int):
