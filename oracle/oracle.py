@@ -128,8 +128,11 @@ def prune_all(data, cand_off, cand_counts, cand_ids, cand_dists, M: int,
 
 
 def add_reverse_and_prune(data, ids, dists, counts, M: int, strategy: str = "rng",
-                          alpha: float = 60.0):
-    """prune.py:129-151 (phase B)."""
+                          alpha: float = 60.0, rows=None):
+    """prune.py:129-151 (phase B).  rows: re-prune only these rows (the merged
+    lists still take reverse edges from every row; other rows come back empty)
+    -- the per-row independence of the re-prune, used for seeded-row checks
+    at sizes where the full CPU re-prune is too slow."""
     data = _f32(data)
     n = data.shape[0]
     ids = np.ascontiguousarray(ids, np.int32)
@@ -154,6 +157,10 @@ def add_reverse_and_prune(data, ids, dists, counts, M: int, strategy: str = "rng
     lib().orc_merge_with_reverse(_p(ids), _p(dists), _p(counts), n, width, _p(rev_off),
                                  _p(rev_ids), _p(rev_dists), _p(mrg_off), _p(mrg_ids),
                                  _p(mrg_dists), _p(mrg_counts))
+    if rows is not None:
+        keep = np.zeros(n, bool)
+        keep[np.asarray(rows)] = True
+        mrg_counts[~keep] = 0
     return prune_all(data, mrg_off, mrg_counts, mrg_ids, mrg_dists, M, strategy, alpha)
 
 

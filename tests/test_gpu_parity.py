@@ -571,3 +571,43 @@ def test_full_scale_cfg2_build_through_the_bench_path(strategy, alpha):
     ae = out.angle_evals.cpu().numpy()
     assert int(ae[0]) == oa[4] and int(ae[1]) == ob[4]
     assert strategy == "alpha" or oa[4] == ob[4] == 0
+
+
+@pytest.mark.parametrize("cfg,strategy,alpha,nrows", [(3, "rng", 60.0, 2000),
+                                                       (4, "slack", 1.2, 1000)])
+def test_full_scale_float_build_on_seeded_rows(cfg, strategy, alpha, nrows):
+    """Configs 3 (1M x 960, rng) and 4 (2M x 768, K=256, R=64, BASELINE's
+    alpha=1.2 as the slack rule) at full size through RngBuilder: phase A of
+    seeded rows and the phase-B re-prune of seeded rows (fed the GPU's
+    phase-A rows of ALL points, so the reverse edges are complete) equal the
+    oracle's rows and per-row counters bit for bit; the pools of the first
+    100 seeded rows equal the oracle's exact k-NN."""
+    from paper_2410_01231_b200.index import RngBuilder, pool_mode
+    c = synth.CONFIGS[cfg]
+    n, K, R = c["n"], c["K"], c["R"]
+    data = c["gen"](n, n)
+    X = torch.from_numpy(data).cuda()
+    b = RngBuilder(n, data.shape[1], K, PruneParams(M=R, alpha=alpha, strategy=strategy),
+                   pool_mode(X))
+    out = b.build(X)
+    torch.cuda.synchronize()
+    del X
+    p_ids, p_d = (t.cpu().numpy() for t in b.pool_out[:2])
+    sel = np.sort(np.random.default_rng(300 + cfg).choice(n, nrows, replace=False))
+    o_ids, o_d = oracle.knn_pools(data, K, rows=sel[:100])
+    np.testing.assert_array_equal(p_ids[sel[:100]], o_ids)
+    np.testing.assert_array_equal(p_d[sel[:100]], o_d)
+    off = np.arange(n + 1, dtype=np.int64) * K
+    cnt = np.zeros(n, np.int32)
+    cnt[sel] = K
+    oa = oracle.prune_all(data, off, cnt, p_ids.ravel(), p_d.ravel(), R, strategy, alpha)
+    a_ids, a_d, a_cnt, a_de = (t.cpu().numpy() for t in b.a_out[:4])
+    np.testing.assert_array_equal(a_ids[sel], oa[0][sel])
+    np.testing.assert_array_equal(a_d[sel], oa[1][sel])
+    np.testing.assert_array_equal(a_cnt[sel], oa[2][sel])
+    assert int(a_de[sel].sum()) == oa[3]
+    ob = oracle.add_reverse_and_prune(data, a_ids, a_d, a_cnt, R, strategy, alpha, rows=sel)
+    np.testing.assert_array_equal(out.ids.cpu().numpy()[sel], ob[0][sel])
+    np.testing.assert_array_equal(out.dists.cpu().numpy()[sel], ob[1][sel])
+    np.testing.assert_array_equal(out.counts.cpu().numpy()[sel], ob[2][sel])
+    assert int(b.b_out[3].cpu().numpy()[sel].sum()) == ob[3]

@@ -146,3 +146,26 @@ def test_oracle_search_and_connect_match_reference():
         m = len(g[f"{name}_kann_ids"])
         np.testing.assert_array_equal(ki[0, :m], g[f"{name}_kann_ids"])
         np.testing.assert_array_equal(kd[0, :m], g[f"{name}_kann_dists"])
+
+
+def test_oracle_row_subset_reprune_equals_full():
+    """add_reverse_and_prune(rows=...) (the seeded-row check used at full
+    config sizes) returns exactly the full re-prune's rows for those rows, and
+    phase A on a masked CSR exactly the full phase A's."""
+    data = synth.cfg1(3000)
+    ids, dists = oracle.knn_pools(data, 32)
+    n = data.shape[0]
+    off = np.arange(n + 1, dtype=np.int64) * 32
+    cnt = np.full(n, 32, np.int32)
+    a = oracle.prune_all(data, off, cnt, ids.ravel(), dists.ravel(), 16, "alpha", 66.0)
+    sel = np.sort(np.random.default_rng(5).choice(n, 300, replace=False))
+    masked = np.zeros(n, np.int32)
+    masked[sel] = 32
+    a_sel = oracle.prune_all(data, off, masked, ids.ravel(), dists.ravel(), 16, "alpha", 66.0)
+    for k in range(3):
+        np.testing.assert_array_equal(a_sel[k][sel], a[k][sel])
+    full = oracle.add_reverse_and_prune(data, a[0], a[1], a[2], 16, "alpha", 66.0)
+    part = oracle.add_reverse_and_prune(data, a[0], a[1], a[2], 16, "alpha", 66.0, rows=sel)
+    for k in range(3):
+        np.testing.assert_array_equal(part[k][sel], full[k][sel])
+    assert part[3] < full[3] and (part[2][np.setdiff1d(np.arange(n), sel)] == 0).all()
