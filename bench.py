@@ -386,8 +386,16 @@ def run_ours(args):
     sel_bytes_fp32 = N * (4 * d * K + 4 * d + 8 * K + 8 * R + 4)
     sel_gbs = sel_bytes / (a_ms / 1e3) / 1e9
     # reverse bytes B_B = 2(8R+4) + 16 deg_A + (8+e*d)|U| per point, |U| from the run
-    union = float((a_cnt + torch.bincount(builder.a_out[0][builder.a_out[0] >= 0].long(),
-                                          minlength=N)).float().mean().item())
+    # |U| = |own ∪ reverse| after the duplicate drop: a reverse edge v -> u
+    # duplicates an own entry exactly when u -> v is also a phase-A edge
+    a_ids = builder.a_out[0]
+    live = a_ids >= 0
+    src = torch.arange(N, device=a_ids.device)[:, None].expand_as(a_ids)[live]
+    dst = a_ids[live].long()
+    recip = torch.isin(dst * N + src, src * N + dst)
+    union = float((a_cnt.long() + torch.bincount(dst, minlength=N)
+                   - torch.bincount(src[recip], minlength=N)).float().mean().item())
+    del src, dst, recip
     rev_bytes = N * (2 * (8 * R + 4) + 16 * deg_a + (8 + e * d) * union)
     rev_gbs = rev_bytes / (b_ms / 1e3) / 1e9
     traffic = measured_traffic("select_A", cfg, N)

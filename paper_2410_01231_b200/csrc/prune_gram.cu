@@ -106,7 +106,7 @@ __device__ unsigned long long g_gram_stats[16];
 
 // PAIR: two points of <= 64 candidates per stage / MMA (rows 0..63 and
 // 64..127 of the tile; the diagonal 64 x 64 blocks of the Gram matrix are the
-// two points' own): the phase-B re-prune, whose rows hold ~38 candidates, is
+// two points' own): the phase-B re-prune, whose rows hold ~27 candidates, is
 // bound by the per-point pipeline cost, which pairing halves.  Rows with more
 // than 64 candidates are listed for the single-point kernel.
 template <int STRATEGY, bool PAIR>  // 0 = rng, 1 = alpha (compile-time: no angle code for rng)
