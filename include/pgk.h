@@ -173,6 +173,11 @@ int pgk_knn_pools_u8(const float *data, const uint8_t *data_u8, const int32_t *n
  * from there.  pgk_detect_u8_async clears *flag (device int, caller sets it to
  * 1) when a value of the rows is not an integer in [0, 255]. */
 int64_t pgk_tiles_center_stride(void);
+/* 1 when the exact tile-pruned pool (and so this pipeline) applies to the
+ * shape (n, d, k) in this process (d <= 128, k <= 256, enough rows, the tile
+ * count within its limit, PGK_DISABLE_PRUNE unset), else 0: callers take
+ * pgk_knn_pools_u8 without `assigned` (or pgk_knn_pools) then. */
+int pgk_tiles_supported(int64_t n, int64_t d, int64_t k);
 int pgk_tiles_u8_prepare(void *ws, size_t ws_bytes, int64_t n, int64_t d, int64_t k,
                          const float *centers, void *stream);
 int pgk_tiles_u8_assign(void *ws, size_t ws_bytes, int64_t n, int64_t d, int64_t k,

@@ -56,6 +56,7 @@ def lib():
         L.pgk_knn_pools.argtypes = [P, I64, I64, P, I64, I64, I, I, P, P, P, P, SZ, P]
         L.pgk_knn_pools_u8.argtypes = [P, P, P, I64, I64, I64, I, P, P, P, P, SZ, P]
         L.pgk_tiles_center_stride.restype = I64
+        L.pgk_tiles_supported.argtypes = [I64, I64, I64]
         L.pgk_tiles_u8_prepare.argtypes = [P, SZ, I64, I64, I64, P, P]
         L.pgk_tiles_u8_assign.argtypes = [P, SZ, I64, I64, I64, P, P, I64, I64, P]
         L.pgk_detect_u8_async.argtypes = [P, I64, I64, P, P]
@@ -101,7 +102,7 @@ EXPORTS = ("pgk_version", "pgk_last_error", "pgk_device_check", "pgk_prune_batch
            "pgk_prune_rows", "pgk_prune_rows_ex", "pgk_prune_workspace", "pgk_make_u8", "pgk_add_reverse_and_prune_ex",
            "pgk_reverse_workspace", "pgk_add_reverse_and_prune", "pgk_detect_u8",
            "pgk_knn_workspace", "pgk_knn_pools", "pgk_knn_pools_u8", "pgk_knn_fallback_rows",
-           "pgk_tiles_center_stride", "pgk_tiles_u8_prepare", "pgk_tiles_u8_assign",
+           "pgk_tiles_center_stride", "pgk_tiles_supported", "pgk_tiles_u8_prepare", "pgk_tiles_u8_assign",
            "pgk_detect_u8_async", "pgk_copy_rows_h2d",
            "pgk_knn_work",
            "pgk_knn_order", "pgk_search_workspace", "pgk_beam_search", "pgk_reach_workspace",

@@ -1,6 +1,8 @@
 // api.cu -- the extern "C" boundary (include/pgk.h).  Validates arguments,
 // maps errors to codes + a thread-local message, forwards to the kernels.
 #include <cstdarg>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -16,15 +18,35 @@ void set_error(const char *fmt, ...) {
   va_end(ap);
 }
 
+// Per-device caches (one process may drive several GPUs from several threads).
+static constexpr int kMaxDevices = 64;
+static std::atomic<int> g_sms[kMaxDevices];
+
 int num_sms() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0, v = 0;
-    cudaGetDevice(&dev);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  int v = g_sms[dev].load(std::memory_order_relaxed);
+  if (!v) {
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cached = v > 0 ? v : 148;
+    if (v <= 0) v = 148;
+    g_sms[dev].store(v, std::memory_order_relaxed);
   }
-  return cached;
+  return v;
+}
+
+cudaError_t ensure_smem(const void *fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find({fn, dev});
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done[{fn, dev}] = bytes;
+  return e;
 }
 
 size_t prune_workspace(int64_t n_rows);
@@ -76,6 +98,7 @@ int knn_tiles_assign(void *, size_t, int64_t, int64_t, int64_t, const uint8_t *,
                      int64_t, int64_t, cudaStream_t);
 int detect_u8_async(const float *, int64_t, int64_t, int *, cudaStream_t);
 int64_t tiles_center_stride();
+bool tiles_supported(int64_t n, int64_t d, int64_t k);
 int detect_u8(const float *, int64_t, int64_t, int *, void *, size_t, cudaStream_t);
 int fallback_rows(const void *, int *, cudaStream_t);
 int knn_work(const void *, int64_t, int64_t, int64_t, int64_t, int, unsigned long long *,
@@ -241,6 +264,9 @@ int pgk_knn_pools_u8(const float *data, const uint8_t *data_u8, const int32_t *n
 }
 
 int64_t pgk_tiles_center_stride(void) { return tiles_center_stride(); }
+int pgk_tiles_supported(int64_t n, int64_t d, int64_t k) {
+  return n > 0 && d >= 1 && k >= 1 && tiles_supported(n, d, k) ? 1 : 0;
+}
 
 int pgk_tiles_u8_prepare(void *ws, size_t ws_bytes, int64_t n, int64_t d, int64_t k,
                          const float *centers, void *stream) {

@@ -44,7 +44,10 @@ extern std::atomic<int64_t> g_launches;
     }                                                                        \
   } while (0)
 
-int num_sms();
+int num_sms();  // of the current device (cached per device)
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device),
+// thread-safe; a no-op when that kernel already allows >= bytes there.
+cudaError_t ensure_smem(const void *fn, size_t bytes);
 
 // Bump allocator over a caller-provided workspace.
 struct Carve {

@@ -829,12 +829,7 @@ static int launch_tile(const float *X, int64_t n, int d, const float *Q, int64_t
   size_t smem = (TBK * (TBM + 1) + TBK * (TBN + 1)) * sizeof(float);
   smem = (smem + 15) & ~size_t(15);
   smem += (size_t)TBM * CAP * sizeof(uint64_t) + 2 * TBN * sizeof(int32_t);
-  static bool attr = false;
-  if (!attr) {
-    PGK_CUDA(cudaFuncSetAttribute(knn_tile_kernel<MODE, CAP>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  PGK_CUDA(ensure_smem((const void *)knn_tile_kernel<MODE, CAP>, smem));
   const unsigned grid = (unsigned)((nq + TBM - 1) / TBM);
   knn_tile_kernel<MODE, CAP><<<grid, 256, smem, stream>>>(X, n, d, Q, nq, exclude_self, xn,
                                                           qn, S, vec4, keys, tlist, tlen,
@@ -994,12 +989,7 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
   }
   if (vec4 && staged_env) {
     const size_t rsm = sizeof(RerankSmem);
-    static bool attr = false;
-    if (!attr) {
-      PGK_CUDA(cudaFuncSetAttribute(rerank_staged_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
-      attr = true;
-    }
+    PGK_CUDA(ensure_smem((const void *)rerank_staged_kernel, rsm));
     const unsigned sgrid =
         (unsigned)std::min<int64_t>((nq + RS_WARPS - 1) / RS_WARPS, (int64_t)sms * 8);
     rerank_staged_kernel<<<sgrid, RS_WARPS * 32, rsm, stream>>>(

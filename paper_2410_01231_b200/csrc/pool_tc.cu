@@ -1191,16 +1191,9 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
     return PGK_ERR_CUDA;
   }
   const size_t smem = sizeof(tc::Smem) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    PGK_CUDA(cudaFuncSetAttribute(tc::tc_pool_u8_kernel<false, false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    PGK_CUDA(cudaFuncSetAttribute(tc::tc_pool_u8_kernel<true, false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    PGK_CUDA(cudaFuncSetAttribute(tc::tc_pool_u8_kernel<false, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  PGK_CUDA(ensure_smem((const void *)tc::tc_pool_u8_kernel<false, false>, smem));
+  PGK_CUDA(ensure_smem((const void *)tc::tc_pool_u8_kernel<true, false>, smem));
+  PGK_CUDA(ensure_smem((const void *)tc::tc_pool_u8_kernel<false, true>, smem));
   const int nblocks = (int)((nq + tc::BM - 1) / tc::BM);
   const unsigned grid = (unsigned)std::min<int64_t>(nblocks, (int64_t)tc::CTAS_PER_SM * sms);
   PGK_CUDA(cudaMemsetAsync(sched, 0, sizeof(int32_t), stream));

@@ -693,12 +693,7 @@ int launch_prune_u8_rows(const uint8_t *xu8, const int32_t *norms, int64_t n,
                      int64_t width, int32_t *out_ids, float *out_dists, int32_t *out_counts,
                      int64_t *dist_evals, int64_t *angle_evals, cudaStream_t stream) {
   const size_t smem = sizeof(PruneU8Smem);
-  static bool attr = false;
-  if (!attr) {
-    PGK_CUDA(cudaFuncSetAttribute(prune_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    attr = true;
-  }
+  PGK_CUDA(ensure_smem((const void *)prune_u8_kernel, smem));
   int64_t blocks = (n + U8_WARPS - 1) / U8_WARPS;
   const int64_t cap = (int64_t)num_sms();  // one ~210 KB block per SM
   if (blocks > cap) blocks = cap;
@@ -722,12 +717,7 @@ static int launch_mode(const float *X, const uint8_t *xu8, const int32_t *norms,
   int64_t blocks = (n + PRUNE_WARPS - 1) / PRUNE_WARPS;
   const int64_t cap = (int64_t)num_sms() * 2;  // 2 resident blocks per SM (~110 KB smem each)
   if (blocks > cap) blocks = cap;
-  static bool attr = false;
-  if (!attr) {
-    PGK_CUDA(cudaFuncSetAttribute(prune_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    attr = true;
-  }
+  PGK_CUDA(ensure_smem((const void *)prune_kernel<MODE>, smem));
   prune_kernel<MODE><<<(unsigned)blocks, PRUNE_WARPS * 32, smem, stream>>>(
       X, xu8, norms, n, (int)d, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists,
       strategy,

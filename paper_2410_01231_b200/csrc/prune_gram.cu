@@ -652,12 +652,7 @@ static int launch_gram_kernel(const CUtensorMap &tmX, const int32_t *norms, int6
                               int32_t *out_counts, int64_t *dist_evals, int64_t *angle_evals,
                               int32_t *long_rows, int32_t *long_count, cudaStream_t stream) {
   const size_t smem = sizeof(gram::Smem<STRATEGY>) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    PGK_CUDA(cudaFuncSetAttribute(gram::prune_gram_kernel<STRATEGY, PAIR>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  PGK_CUDA(ensure_smem((const void *)gram::prune_gram_kernel<STRATEGY, PAIR>, smem));
   const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)gram::CTAS_PER_SM * num_sms());
   gram::prune_gram_kernel<STRATEGY, PAIR><<<grid, gram::THREADS, smem, stream>>>(
       tmX, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,

@@ -47,7 +47,10 @@ __global__ void rev_count_kernel(const int32_t *__restrict__ ids,
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += nw) {
     const int c = counts[u];
-    for (int j = lane; j < c; j += 32) atomicAdd(rev_cnt + ids[u * width + j], 1);
+    for (int j = lane; j < c; j += 32) {
+      const int32_t v = ids[u * width + j];
+      if ((uint64_t)v < (uint64_t)n) atomicAdd(rev_cnt + v, 1);  // out-of-range ids: no edge
+    }
   }
 }
 
@@ -153,21 +156,23 @@ __global__ void scatter_kernel(const int32_t *__restrict__ ids,
     const int64_t o1 = mrg_off[u], o2 = u2 < n ? mrg_off[u2] : 0;
     for (int j = lane; j < max(c1, c2); j += 32) {
       const bool p1 = j < c1, p2 = j < c2;
-      const int32_t v1 = p1 ? ids[u * width + j] : 0, v2 = p2 ? ids[u2 * width + j] : 0;
+      int32_t v1 = p1 ? ids[u * width + j] : 0, v2 = p2 ? ids[u2 * width + j] : 0;
       const float d1 = p1 ? dists[u * width + j] : 0.f, d2 = p2 ? dists[u2 * width + j] : 0.f;
+      // an id outside [0, n) (a precondition violation the host shim rejects
+      // with ValueError) becomes the row's own id, which the scan skips: no
+      // write or gather ever leaves the buffers
+      const bool r1 = p1 && (uint64_t)v1 < (uint64_t)n, r2 = p2 && (uint64_t)v2 < (uint64_t)n;
+      if (p1 && !r1) v1 = (int32_t)u;
+      if (p2 && !r2) v2 = (int32_t)u2;
       int s1 = 0, s2 = 0;
-      if (p1) s1 = atomicSub(rev_left + v1, 1) - 1;
-      if (p2) s2 = atomicSub(rev_left + v2, 1) - 1;
-      const int64_t b1 = p1 ? mrg_off[v1] + counts[v1] : 0;
-      const int64_t b2 = p2 ? mrg_off[v2] + counts[v2] : 0;
-      if (p1) {
-        keys[o1 + j] = pack_key(d1, v1);                  // own entry
-        keys[b1 + s1] = pack_key(d1, (int32_t)u);         // reverse
-      }
-      if (p2) {
-        keys[o2 + j] = pack_key(d2, v2);
-        keys[b2 + s2] = pack_key(d2, (int32_t)u2);
-      }
+      if (r1) s1 = atomicSub(rev_left + v1, 1) - 1;
+      if (r2) s2 = atomicSub(rev_left + v2, 1) - 1;
+      const int64_t b1 = r1 ? mrg_off[v1] + counts[v1] : 0;
+      const int64_t b2 = r2 ? mrg_off[v2] + counts[v2] : 0;
+      if (p1) keys[o1 + j] = pack_key(d1, v1);             // own entry
+      if (r1) keys[b1 + s1] = pack_key(d1, (int32_t)u);    // reverse
+      if (p2) keys[o2 + j] = pack_key(d2, v2);
+      if (r2) keys[b2 + s2] = pack_key(d2, (int32_t)u2);
     }
   }
 }

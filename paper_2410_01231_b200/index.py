@@ -97,8 +97,11 @@ class RngBuilder:
         whole copy.  The exact-integer check runs on the device per chunk; if
         the data turn out not to qualify, the result is recomputed through the
         float path (one 4-byte read at the end: this call returns with the
-        build complete).  Non-U8 builders copy, then build."""
-        if self.mode != _lib.POOL_U8 or self.d > 128 or self.n < 8 * 128:
+        build complete).  Non-U8 builders, and shapes the tile-pruned pool
+        does not take (pgk_tiles_supported: K > 256, too many tiles,
+        PGK_DISABLE_PRUNE=1), copy, then build."""
+        if self.mode != _lib.POOL_U8 or self.d > 128 or \
+                not _lib.lib().pgk_tiles_supported(self.n, self.d, self.K):
             out = self.build(host.to(_lib.device(), non_blocking=True), host_out)
             torch.cuda.current_stream().synchronize()
             return out

@@ -9,7 +9,10 @@ through the reference's own loader and vice versa.
   u32 M, u64 n, u64 ep, u32 #over-cap + int32 ids, u64 CSR offsets (n+1),
   int32 neighbour ids.  Vectors are never stored.  Loading validates the
   structure and raises ``CorruptIndexError`` (a ValueError) like the
-  reference.  The layered kind (FastHNSW, f3) is recognised and refused.
+  reference.
+* ``PGIX`` layered index (kind 1, dataset_io.py:174-245): the FastHNSW
+  hierarchy (``hnsw.LayeredGraph``), per layer its ascending member ids and a
+  flat body; the loader checks nesting, coverage and the entry point.
 """
 
 from __future__ import annotations
@@ -83,73 +86,141 @@ def _as_host(a) -> np.ndarray:
     return a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
 
 
-def save_index(path, g: ProximityGraph) -> None:
-    """Write a flat PGIX index (CSR adjacency, M, entry point, over-cap tags)."""
-    if not isinstance(g, ProximityGraph):
-        raise TypeError(f"cannot serialize {type(g).__name__}")
+def _flat_body(g: ProximityGraph) -> list:
+    """u64 n, u64 ep, u32 #over-cap + int32 ids, u64 offsets, int32 neighbours
+    (dataset_io.py:114-120)."""
     host = ProximityGraph(adj=_as_host(g.adj), counts=_as_host(g.counts), M=g.M, ep=g.ep,
                           over_cap=_as_host(g.over_cap))
     offsets, nbrs = host.to_csr()
     over = np.asarray(host.over_cap, "<i4")
-    parts = [MAGIC, struct.pack("<IBI", VERSION, KIND_FLAT, int(g.M)),
-             struct.pack("<QQI", host.n, int(g.ep), over.size), over.tobytes(),
-             offsets.astype("<u8").tobytes(), nbrs.astype("<i4").tobytes()]
+    return [struct.pack("<QQI", host.n, int(g.ep), over.size), over.tobytes(),
+            offsets.astype("<u8").tobytes(), nbrs.astype("<i4").tobytes()]
+
+
+def save_index(path, g) -> None:
+    """Write a PGIX index: flat (ProximityGraph) or layered (hnsw.LayeredGraph:
+    u32 bottom M, u64 n, u64 ep, f64 m_factor, u32 #layers, then per layer
+    u64 #members + int32 members, u32 M and a flat body; dataset_io.py:174-195)."""
+    from .hnsw import LayeredGraph
+    if isinstance(g, ProximityGraph):
+        parts = [MAGIC, struct.pack("<IBI", VERSION, KIND_FLAT, int(g.M))] + _flat_body(g)
+    elif isinstance(g, LayeredGraph):
+        parts = [MAGIC, struct.pack("<IBI", VERSION, KIND_LAYERED, int(g.layers[0].graph.M)),
+                 struct.pack("<QQdI", g.n, int(g.ep), float(g.m_factor), len(g.layers))]
+        for layer in g.layers:
+            mem = np.asarray(_as_host(layer.members), "<i4")
+            parts += [struct.pack("<Q", mem.size), mem.tobytes(),
+                      struct.pack("<I", int(layer.graph.M))] + _flat_body(layer.graph)
+    else:
+        raise TypeError(f"cannot serialize {type(g).__name__}")
     Path(path).write_bytes(b"".join(parts))
 
 
-def load_index(path) -> ProximityGraph:
-    """Read a flat PGIX index with the reference's structural checks."""
-    path = Path(path)
-    buf = memoryview(path.read_bytes())
-    pos = 0
+class _Cursor:
+    """Bounds-checked little-endian reads over one file's bytes."""
 
-    def take(nbytes: int) -> memoryview:
-        nonlocal pos
-        if pos + nbytes > len(buf):
-            raise CorruptIndexError(f"{path}: truncated index file")
-        out = buf[pos:pos + nbytes]
-        pos += nbytes
+    def __init__(self, path: Path):
+        self.path = path
+        self.buf = memoryview(path.read_bytes())
+        self.pos = 0
+
+    def take(self, nbytes: int) -> memoryview:
+        if self.pos + nbytes > len(self.buf):
+            raise CorruptIndexError(f"{self.path}: truncated index file")
+        out = self.buf[self.pos:self.pos + nbytes]
+        self.pos += nbytes
         return out
 
-    def fields(fmt: str):
-        return struct.unpack(fmt, take(struct.calcsize(fmt)))
+    def fields(self, fmt: str):
+        return struct.unpack(fmt, self.take(struct.calcsize(fmt)))
 
-    def array(dtype: str, count: int) -> np.ndarray:
+    def array(self, dtype: str, count: int) -> np.ndarray:
         dt = np.dtype(dtype)
-        return np.frombuffer(take(dt.itemsize * count), dt).copy()
+        return np.frombuffer(self.take(dt.itemsize * count), dt).copy()
 
-    if bytes(take(4)) != MAGIC:
-        raise CorruptIndexError(f"{path}: not an index file (bad magic)")
-    version, kind = fields("<IB")
-    if version != VERSION:
-        raise CorruptIndexError(f"{path}: unsupported version {version}")
-    if kind == KIND_LAYERED:
-        raise NotImplementedError(f"{path}: layered (FastHNSW) indexes are not part of this "
-                                  "build")
-    if kind != KIND_FLAT:
-        raise CorruptIndexError(f"{path}: unknown index kind {kind}")
-    (M,) = fields("<I")
-    n, ep = fields("<QQ")
+    def end(self) -> None:
+        if self.pos != len(self.buf):
+            raise CorruptIndexError(f"{self.path}: trailing bytes in index file")
+
+
+def _read_flat(c: _Cursor, M: int) -> ProximityGraph:
+    """A flat body with the reference's checks (dataset_io.py:142-167)."""
+    path = c.path
+    n, ep = c.fields("<QQ")
     if n < 1:
         raise CorruptIndexError(f"{path}: empty graph")
     if ep >= n:
         raise CorruptIndexError(f"{path}: entry point {ep} out of range")
-    (n_over,) = fields("<I")
-    over = array("<i4", n_over)
-    offsets = array("<u8", n + 1).astype(np.int64)
+    (n_over,) = c.fields("<I")
+    over = c.array("<i4", n_over)
+    offsets = c.array("<u8", n + 1).astype(np.int64)
     if offsets[0] != 0 or np.any(np.diff(offsets) < 0):
         raise CorruptIndexError(f"{path}: bad CSR offsets")
-    nbrs = array("<i4", int(offsets[-1]))
+    nbrs = c.array("<i4", int(offsets[-1]))
     if nbrs.size and (nbrs.min() < 0 or nbrs.max() >= n):
         raise CorruptIndexError(f"{path}: neighbor id out of range")
-    if pos != len(buf):
-        raise CorruptIndexError(f"{path}: trailing bytes in index file")
     deg = np.diff(offsets)
     untagged = np.setdiff1d(np.flatnonzero(deg > M), over)
     if untagged.size:
         u = int(untagged[0])
         raise CorruptIndexError(f"{path}: node {u} degree {deg[u]} exceeds M={M}")
     return ProximityGraph.from_csr(offsets, nbrs, M=int(M), ep=int(ep), over_cap=over)
+
+
+def _read_layered(c: _Cursor):
+    """The layered body (dataset_io.py:213-245): nested, ascending member
+    lists, the bottom layer = every node, the entry point in the top layer;
+    levels are rebuilt from the nesting."""
+    from .hnsw import LayeredGraph, LayerGraph
+    path = c.path
+    c.fields("<I")  # bottom layer's M, repeated in its own body
+    n_total, ep, m_factor, n_layers = c.fields("<QQdI")
+    if n_layers < 1:
+        raise CorruptIndexError(f"{path}: layered index without layers")
+    layers = []
+    for li in range(n_layers):
+        (n_members,) = c.fields("<Q")
+        members = c.array("<i4", n_members)
+        if np.any(np.diff(members) <= 0):
+            raise CorruptIndexError(f"{path}: layer {li} members not ascending")
+        (layer_m,) = c.fields("<I")
+        g = _read_flat(c, layer_m)
+        if g.n != n_members:
+            raise CorruptIndexError(f"{path}: layer {li} graph size mismatch")
+        layers.append(LayerGraph(members=members, graph=g))
+    c.end()
+    if len(layers[0].members) != n_total:
+        raise CorruptIndexError(f"{path}: bottom layer must cover all nodes")
+    if not np.array_equal(layers[0].members, np.arange(n_total, dtype=np.int32)):
+        raise CorruptIndexError(f"{path}: bottom layer must contain every node")
+    levels = np.zeros(n_total, dtype=np.int32)
+    for li in range(1, n_layers):
+        mem = layers[li].members
+        if not np.all(np.isin(mem, layers[li - 1].members)):
+            raise CorruptIndexError(f"{path}: layer {li} not nested")
+        levels[mem] = li
+    if ep >= n_total or levels[ep] != n_layers - 1:
+        raise CorruptIndexError(f"{path}: entry point not in the top layer")
+    return LayeredGraph(layers=layers, levels=levels, ep=int(ep), m_factor=float(m_factor))
+
+
+def load_index(path):
+    """Read a PGIX index (flat -> ProximityGraph, layered -> LayeredGraph) with
+    the reference's structural checks (dataset_io.py:198-245)."""
+    c = _Cursor(Path(path))
+    if bytes(c.take(4)) != MAGIC:
+        raise CorruptIndexError(f"{c.path}: not an index file (bad magic)")
+    version, kind = c.fields("<IB")
+    if version != VERSION:
+        raise CorruptIndexError(f"{c.path}: unsupported version {version}")
+    if kind == KIND_LAYERED:
+        return _read_layered(c)
+    if kind != KIND_FLAT:
+        raise CorruptIndexError(f"{c.path}: unknown index kind {kind}")
+    (M,) = c.fields("<I")
+    g = _read_flat(c, M)
+    c.end()
+    return g
 
 
 __all__ = ["CorruptIndexError", "load_vecs", "save_vecs", "load_dataset", "save_index",

@@ -286,6 +286,28 @@ def save_io() -> None:
     print("io", sorted(p.name for p in out.iterdir()))
 
 
+def save_io_layered() -> None:
+    """Layered PGIX files (dataset_io.py:174-245) written by the reference
+    for the FastHNSW hierarchies of f3.npz (same inputs and parameters)."""
+    from pgann import dataset_io
+    from pgann import hnsw as R_hnsw
+    out = HERE / "io"
+    rec = {}
+    for name, data in (("cfg1", synth.cfg1(2_500)), ("cfg2", synth.cfg2(3_000))):
+        lg = R_hnsw.build_fasthnsw(Dataset.from_array(data), k0=12, ef=40, M=12, seed=6)
+        dataset_io.save_index(out / f"hnsw_{name}.pgix", lg)
+        h = dataset_io.load_index(out / f"hnsw_{name}.pgix")
+        rec[f"{name}_nlayers"], rec[f"{name}_ep"] = np.int64(len(h.layers)), np.int64(h.ep)
+        rec[f"{name}_levels"], rec[f"{name}_m_factor"] = h.levels, np.float64(h.m_factor)
+        for i, layer in enumerate(h.layers):
+            rec[f"{name}_L{i}_members"] = layer.members
+            rec[f"{name}_L{i}_adj"], rec[f"{name}_L{i}_counts"] = layer.graph.adj, layer.graph.counts
+            rec[f"{name}_L{i}_ep"], rec[f"{name}_L{i}_M"] = np.int64(layer.graph.ep), np.int64(layer.graph.M)
+            rec[f"{name}_L{i}_over"] = layer.graph.over_cap
+    np.savez_compressed(out / "expect_layered.npz", **rec)
+    print("io layered", sorted(p.name for p in out.iterdir()))
+
+
 def save_f3() -> None:
     """NN-Descent, FastNSG, NSG and FastHNSW outputs:
     knng.py:40-125, nsg.py:319-430, hnsw.py:141-192, search.py:97-130."""
@@ -355,6 +377,9 @@ def main() -> None:
         return
     if len(sys.argv) > 1 and sys.argv[1] == "io":
         save_io()
+        return
+    if len(sys.argv) > 1 and sys.argv[1] == "io_layered":
+        save_io_layered()
         return
     save_cases()
     save_config("cfg1_full", synth.cfg1(10_000), 64, 24,

@@ -78,3 +78,19 @@ def test_fasthnsw_and_layered_search_match_reference(name):
         m = len(ids)
         np.testing.assert_array_equal(ids, G[f"{name}_lq_ids"][j, :m])
         np.testing.assert_array_equal(dists, G[f"{name}_lq_dists"][j, :m])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_gpu_fasthnsw_saves_the_reference_file(tmp_path, name):
+    """The GPU-built hierarchy written as a layered PGIX index (kind 1) is the
+    file the reference's dataset_io writes for its own build, byte for byte
+    (tests/golden/io/hnsw_*.pgix), and loads back to the same layers."""
+    from paper_2410_01231_b200 import io as pio
+    ds = Dataset.from_array(G[f"{name}_data"])
+    lg = hnsw.build_fasthnsw(ds, k0=12, ef=40, M=12, seed=6)
+    ref = Path(__file__).resolve().parent / "golden" / "io" / f"hnsw_{name}.pgix"
+    pio.save_index(tmp_path / "g.pgix", lg)
+    assert (tmp_path / "g.pgix").read_bytes() == ref.read_bytes()
+    back = pio.load_index(tmp_path / "g.pgix")
+    assert back.ep == lg.ep and len(back.layers) == len(lg.layers)
+    np.testing.assert_array_equal(back.levels, lg.levels)
