@@ -43,6 +43,10 @@ extern "C" {
 #define PGK_POOL_AUTO 0 /* detect (one small device->host read)              */
 #define PGK_POOL_U8 1   /* every value an integer in [0,255], d <= 258: exact */
 #define PGK_POOL_F32 2  /* general fp32 data: approximate pass + fp64 rerank  */
+/* OR-ed into a mode (same value for the workspace query and the call): skip
+ * the exact tile pruning and scan every pair (the brute-force kernels) --
+ * the reference result by a second route, for verification. */
+#define PGK_POOL_NO_PRUNE 0x10
 
 const char *pgk_version(void);
 const char *pgk_last_error(void);

@@ -19,6 +19,7 @@ LIB_PATH = Path(os.environ.get("PGK_LIB_PATH", PKG / "libpgk.so"))
 
 OK, ERR_INVALID, ERR_CUDA, ERR_NOMEM, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 POOL_AUTO, POOL_U8, POOL_F32 = 0, 1, 2
+POOL_NO_PRUNE = 0x10  # OR into a mode: brute-force kernels, no tile pruning
 
 _lib = None
 

@@ -724,6 +724,8 @@ static KnnLayout knn_layout(void *ws, size_t bytes, int64_t n, int64_t nq, int64
                             int64_t k, int mode) {
   KnnLayout L{};
   Carve c(ws, bytes);
+  const bool prune = !(mode & PGK_POOL_NO_PRUNE);
+  mode &= ~PGK_POOL_NO_PRUNE;
   const int S = pool_S(k, mode == PGK_POOL_AUTO ? PGK_POOL_F32 : mode);
   L.flag = c.take<int>(4);
   L.fb_count = c.take<int32_t>(4);
@@ -735,7 +737,7 @@ static KnnLayout knn_layout(void *ws, size_t bytes, int64_t n, int64_t nq, int64
   L.tc_bytes = L.tws_bytes = L.tws_f32_bytes = 0;
   L.tc_ws = L.tws = L.tws_f32 = nullptr;
   if (mode != PGK_POOL_F32 && tc_pool_supported(d, k)) {
-    const bool tiles = nq == n && tiles_supported(n, d, k);
+    const bool tiles = prune && nq == n && tiles_supported(n, d, k);
     const int64_t rows = tiles ? std::max(nq, tiles_rows(n)) : nq;
     L.tc_bytes = tc_pool_workspace(tiles ? rows : n, rows, false);
     L.tc_ws = c.take<char>(L.tc_bytes);
@@ -744,7 +746,7 @@ static KnnLayout knn_layout(void *ws, size_t bytes, int64_t n, int64_t nq, int64
       L.tws = c.take<char>(L.tws_bytes);
     }
   }
-  if (mode != PGK_POOL_U8 && nq == n && tiles_f32_supported(n, d, k)) {
+  if (prune && mode != PGK_POOL_U8 && nq == n && tiles_f32_supported(n, d, k)) {
     L.tws_f32_bytes = tiles_f32_workspace(n, d, k);
     L.tws_f32 = c.take<char>(L.tws_f32_bytes);
   }
@@ -887,6 +889,8 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
   PGK_REQUIRE(!exclude_self || self, "exclude_self requires queries=None");
   PGK_REQUIRE(k <= (exclude_self ? n - 1 : n), "k=%lld exceeds the number of candidates",
               (long long)k);
+  const int noprune = mode & PGK_POOL_NO_PRUNE;
+  mode &= ~PGK_POOL_NO_PRUNE;
   if (mode == PGK_POOL_AUTO) {
     int a = 0, b = 1;
     int rc = detect_u8(X, n, d, &a, ws, bytes, stream);
@@ -902,7 +906,7 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
     set_error("U8 pool mode needs d <= 258");
     return PGK_ERR_UNSUPPORTED;
   }
-  KnnLayout L = knn_layout(ws, bytes, n, nq, d, k, mode);
+  KnnLayout L = knn_layout(ws, bytes, n, nq, d, k, mode | noprune);
   if (L.total > bytes) {
     set_error("knn workspace too small: need %zu, got %zu", L.total, bytes);
     return PGK_ERR_NOMEM;

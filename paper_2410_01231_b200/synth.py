@@ -68,6 +68,19 @@ def cfg2(n: int = 1_000_000, n_full: int = 1_000_000, seed: int = 1) -> np.ndarr
     return out
 
 
+def cfg2_queries(n_queries: int = 10_000, seed: int = 1, query_seed: int = 1001) -> np.ndarray:
+    """Recall queries for config 2 (BASELINE gives none; same
+    recipe, distinct documented seed): the SAME 256 centres (the first draw
+    of default_rng(seed)), then a ~ U{0..255} and the noise from
+    default_rng(query_seed): x = clip(rint(c[a] + 20 z), 0, 255)."""
+    d, k = 128, 256
+    c = 255.0 * np.random.default_rng(seed).random((k, d))
+    rng = np.random.default_rng(query_seed)
+    qa = rng.integers(0, k, size=n_queries)
+    q = np.clip(np.rint(c[qa] + 20.0 * rng.standard_normal((n_queries, d))), 0.0, 255.0)
+    return q.astype(np.float32)
+
+
 def cfg5(n: int = 200_000, n_queries: int = 10_000, seed: int = 4):
     """Config 5 (FastHNSW build): the config-2 recipe with seed 4 for the base
     rows; the queries continue the same generator after the base draws (same

@@ -1,0 +1,45 @@
+"""GPU parity at the benchmarked sizes (SURVEY 8(d) parity checks; north_star's
+figures): the tile-pruned pools equal the brute-force kernels on every row and
+the oracle on 2,000 seeded rows per config; the GPU graph agrees edge for edge
+with the oracle-built graph and the reference's greedy search has the same
+recall@10 on both (tests/_fullscale.py holds the computations)."""
+import os
+
+import pytest
+
+from _fullscale import graph_recall, pool_exactness
+
+pytestmark = pytest.mark.gpu
+
+# configs 3 (1M x 960) and 4 (2M x 768): the brute-force SIMT scans take minutes
+FULL = os.environ.get("PGK_FULL_PARITY", "1") == "1"
+
+
+def _check_pool(r):
+    assert r["pruned_path_ran"], r
+    assert r["rows_equal_bruteforce"] == r["rows"], r
+    assert r["oracle_rows_equal"] == r["oracle_rows"], r
+
+
+def test_cfg2_pruned_pools_equal_bruteforce_on_every_row():
+    _check_pool(pool_exactness(2))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_float_pruned_pools_equal_bruteforce_on_every_row(cfg):
+    if not FULL:
+        pytest.skip("PGK_FULL_PARITY=0")
+    _check_pool(pool_exactness(cfg))
+
+
+@pytest.mark.parametrize("strategy,alpha", [("rng", 60.0), ("alpha", 66.0)])
+def test_graph_edge_agreement_and_recall_vs_oracle_graph(strategy, alpha):
+    """north_star: >= 99.9 % edge agreement, recall@10 within 0.2 points of the
+    reference-built graph (here: identical graphs, identical recall)."""
+    r = graph_recall(50_000, 10_000, strategy=strategy, alpha=alpha)
+    assert r["edge_agreement"] >= 0.999, r
+    assert r["graphs_identical"], r
+    for row in r["search"]:
+        assert row["gpu_search_equals_oracle_search"], row
+        assert abs(row["recall_at_10_gpu_graph"] - row["recall_at_10_oracle_graph"]) <= 0.002, row
