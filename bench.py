@@ -453,6 +453,9 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if rank == 0 and not args.no_parity:
+        line["e2e_numpy_api"] = e2e_numpy(data, K, R, args)
+        line["parity"] = parity_live(builder, X, data, cfg, mode, args.no_cpu)
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import oracle
         n_s, _ = cpu_sample_size(cfg, args.cpu_target_s)
@@ -461,11 +464,137 @@ def run_ours(args):
             "value": n_s / tc, "unit": UNIT, "cores": oracle.num_threads(), "kind": "port",
             "sample": f"first {n_s} rows of the seeded config-{cfg} array, one full pass "
                       f"({tc:.1f} s): numpy-BLAS ground_truth_table restatement + C "
-                      "restatement of the numba prune/reverse kernels"}
+                      "restatement of the numba prune/reverse kernels",
+            "port_vs_reference": "the port is 1.14x the reference's own numba build on the same "
+                                 "16,337-row prefix, 8 threads, identical graphs "
+                                 "(profiles/r02_ref_vs_port.json)"}
+        ab = line.get("parity", {}).pop("_cpu_phases_ab_s", None)
+        if ab is not None:
+            line["cpu_baseline"]["phases_ab_full_n"] = {
+                "value": N / ab, "unit": UNIT, "seconds": ab, "cores": oracle.num_threads(),
+                "sample": f"all {N} rows: C restatement of the numba phase-A + phase-B kernels "
+                          "(prune.py:109-151) fed the GPU's pools (SURVEY 8(d) iii)"}
+    if rank == 0 and world == 1 and args.extra_cfg3:
+        del builder, X
+        torch.cuda.empty_cache()
+        line["configs_extra"] = {"cfg3": float_config_run(3, args.extra_steps)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def e2e_numpy(data, K: int, R: int, args) -> dict:
+    """The reference-signature host call: numpy (n, d) float32 in,
+    ProximityGraph (numpy adjacency) out -- index.build_rng_index, pageable
+    host memory, host wall clock around each call (blocking)."""
+    from paper_2410_01231_b200.index import build_rng_index
+    import torch
+    for _ in range(1):
+        build_rng_index(data, K, R)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(max(2, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        g = build_rng_index(data, K, R)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    return {"value": data.shape[0] / t, "unit": UNIT, "ms_per_call": t * 1e3,
+            "calls": len(ts), "api": "index.build_rng_index(numpy) -> ProximityGraph (numpy)",
+            "h2d_bytes_per_step": int(data.nbytes),
+            "d2h_bytes_per_step": int(g.adj.nbytes + g.counts.nbytes)}
+
+
+def parity_live(builder, X, data, cfg: int, mode: int, no_cpu: bool) -> dict:
+    """Parity of the benchmarked build, measured after the timed region:
+    the pools equal the brute-force kernels on every row; recall@10 of the
+    greedy search (search.py:81-94 semantics) on the phase-B graph; and, with
+    the CPU leg, phases A+B of the C oracle over all rows fed the same pools
+    (edge agreement with the GPU graph) -- its time is cpu_baseline's
+    phases_ab_full_n."""
+    import torch
+    from paper_2410_01231_b200 import (Dataset, ProximityGraph, _lib, kernels, pool, prune,
+                                       search, synth)
+    N, d = data.shape
+    K, R = builder.K, builder.params.M
+    out = {}
+    t0 = time.perf_counter()
+    bf = kernels.knn_pools(X, K, mode=mode | _lib.POOL_NO_PRUNE, want_gt=False)
+    same = ((bf.pool_ids == builder.pool_out[0]).all(1) &
+            (bf.pool_dists == builder.pool_out[1]).all(1))
+    out["pool_rows_equal_bruteforce"] = float(same.float().mean().item())
+    del bf
+    out["pool_check_s"] = time.perf_counter() - t0
+    ids = builder.b_out[0]
+    counts = builder.b_out[2]
+    ds = Dataset.from_array(data)
+    ds._dev = X  # the resident copy
+    g = ProximityGraph(adj=ids, counts=counts, M=R, ep=0)
+    if cfg == 2:
+        q = synth.cfg2_queries(10_000)
+        ep = prune.entry_point(ds, g, k=1, L=max(R + 1, 32))
+        truth = pool.ground_truth_table(ds, q, k=10)
+        rec = {}
+        for L in (20, 50, 100):
+            r_ids, _, r_dc = search.search_batch(ds, g, q, 10, L, ep=ep)
+            rec[f"L{L}"] = {"recall_at_10": pool.mean_recall(r_ids, truth, 10),
+                            "dist_evals_per_query": float(r_dc.mean())}
+        out["recall_at_10_phase_b_graph"] = rec
+        out["recall_queries"] = "10,000 synth.cfg2_queries; ep = entry_point (centroid search)"
+    if not no_cpu:
+        from oracle import oracle
+        p_ids = builder.pool_out[0].cpu().numpy()
+        p_d = builder.pool_out[1].cpu().numpy()
+        off = np.arange(N + 1, dtype=np.int64) * K
+        cnt = np.full(N, K, np.int32)
+        t1 = time.perf_counter()
+        oa = oracle.prune_all(data, off, cnt, p_ids.ravel(), p_d.ravel(), R, "rng", 60.0)
+        ob = oracle.add_reverse_and_prune(data, oa[0], oa[1], oa[2], R, "rng", 60.0)
+        out["_cpu_phases_ab_s"] = time.perf_counter() - t1
+        g_ids, g_cnt = ids.cpu().numpy(), counts.cpu().numpy()
+        live = np.arange(R)[None, :] < ob[2][:, None]
+        o_edges = int(live.sum())
+        agree = int((live & (g_ids == ob[0])).sum()) if np.array_equal(g_cnt, ob[2]) else None
+        if agree is None:  # different degrees: count shared (u, v) pairs
+            ge = np.arange(N, dtype=np.int64)[:, None] * N + g_ids
+            oe = np.arange(N, dtype=np.int64)[:, None] * N + ob[0]
+            agree = int(np.intersect1d(ge[np.arange(R)[None, :] < g_cnt[:, None]],
+                                       oe[live]).size)
+        out["edge_agreement_vs_oracle_full_n"] = agree / max(o_edges, 1)
+        out["graph_identical_to_oracle"] = bool(np.array_equal(g_ids, ob[0])
+                                                and np.array_equal(g_cnt, ob[2]))
+    out["prefix_graph_parity"] = ("profiles/r02_parity.json: 50k-row config-2 prefix, GPU vs "
+                                  "oracle-built graph incl. phase C, edge agreement and "
+                                  "recall@10 of both")
+    return out
+
+
+def float_config_run(cfg: int, steps: int) -> dict:
+    """A float configuration (SIMT pools + float64 rerank proof, fp32
+    selection) through RngBuilder.build, device-resident data, CUDA events;
+    a few steps (each takes seconds)."""
+    import torch
+    from paper_2410_01231_b200 import _lib
+    from paper_2410_01231_b200.index import RngBuilder
+    from paper_2410_01231_b200.prune import PruneParams
+    data, c = make_data(cfg, None)
+    N, d, K, R = data.shape[0], data.shape[1], c["K"], c["R"]
+    X = torch.from_numpy(data).cuda()
+    del data
+    b = RngBuilder(N, d, K, PruneParams(M=R), _lib.POOL_F32)
+    b.build(X)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    for e0, e1 in ev:
+        e0.record()
+        b.build(X)
+        e1.record()
+    torch.cuda.synchronize()
+    t = sum(a.elapsed_time(z) for a, z in ev) / 1e3 / steps
+    return {"workload": CONFIG_DESC[cfg], "value": N / t, "unit": UNIT, "ms_per_step": t * 1e3,
+            "steps": steps, "warmup": 1, "pool_mode": "f32+f64-rerank",
+            "dtype": "fp32 pools (SIMT) + f64 rerank, fp32 selection"}
 
 
 def main():
@@ -478,6 +607,9 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="prefix size (debug)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-target-s", type=float, default=15.0)
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--extra-cfg3", type=int, default=1)
+    ap.add_argument("--extra-steps", type=int, default=2)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -50,7 +50,14 @@ constexpr int C = 128;          // candidates per point (TMEM lanes)
 #ifndef GRAM_NBUF
 #define GRAM_NBUF 2  // measured: 3 buffers cost 5 % (less shared memory left to L1)
 #endif
-constexpr int STAGES = GRAM_STAGES;  // gathered points in flight
+#ifndef GRAM_TSTAGES
+#define GRAM_TSTAGES GRAM_STAGES
+#endif
+// Two rings: point slots (metadata: ids, dists, norms; freed by the mask
+// warps) and u8 row tiles (freed by the MMA's commit, so the next gather
+// starts while the masks of this point are still being built).
+constexpr int STAGES = GRAM_STAGES;    // point slots in flight
+constexpr int TSTAGES = GRAM_TSTAGES;  // row tiles in flight
 constexpr int GROUPS = GRAM_GROUPS;  // mask warpgroups = TMEM accumulators (point parity)
 constexpr int NG = GRAM_GREEDY;      // greedy warps: point k goes to warp k % NG
 constexpr int NBUF = GRAM_NBUF;      // mask buffers: point k uses k % NBUF
@@ -63,7 +70,7 @@ constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(C >> 3) << 17) | ((uint32_t)(
 
 template <int STRATEGY>
 struct __align__(1024) Smem {
-  uint8_t tile[STAGES][C * 128];  // SW128 K-major: 8-row x 128-byte atoms
+  uint8_t tile[TSTAGES][C * 128];  // SW128 K-major: 8-row x 128-byte atoms
   int32_t id[STAGES][C];
   float dist[STAGES][C];
   alignas(16) int32_t nrm[STAGES][C];
@@ -81,6 +88,7 @@ struct __align__(1024) Smem {
   int64_t gu[NBUF][2];     // -1: empty slot
   int32_t gcnt[NBUF][2];    // [0] -1: end of stream
   uint64_t full[STAGES], empty[STAGES];
+  uint64_t tfree[TSTAGES];  // tile consumed by the MMA (tcgen05.commit)
   uint64_t tfull[GROUPS], tempty[GROUPS];
   uint64_t mfull[NBUF], mempty[NBUF];
   uint32_t tmem_base;
@@ -137,6 +145,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       mbar_init(&s.full[i], 1);    // gather lane 0 (after the stage's STS), + TMA bytes
       mbar_init(&s.empty[i], 4);   // released by the 4 mask warps
     }
+    for (int i = 0; i < TSTAGES; ++i) mbar_init(&s.tfree[i], 1);
     for (int i = 0; i < GROUPS; ++i) {
       mbar_init(&s.tfull[i], 1);
       mbar_init(&s.tempty[i], 4);
@@ -171,8 +180,8 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     // Lane l holds candidates 4l..4l+3 (id -1, dist 0, norm 0 past cnt); its
     // gather4 fetches exactly those rows.  The other roles follow the stream
     // published in s.u / s.cnt / s.self.
-    int stage = 0, half = 0;
-    uint32_t phase = 0;
+    int stage = 0, half = 0, tst = 0;
+    uint32_t phase = 0, tph = 0;
     const int64_t nb = blockIdx.x < n_rows ? (n_rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     int64_t bu = 0, boff = 0;
     int bcnt = 0, bself = 0;
@@ -239,7 +248,10 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       if (m0.cnt > PC) {  // hub row (PAIR: > 64): left to the next kernel
         if (lane == 0) long_rows[atomicAdd(long_count, 1)] = (int32_t)m0.u;
       } else {
-        if (half == 0) GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
+        if (half == 0) {
+          GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
+          mbar_wait(&s.tfree[tst], tph ^ 1);
+        }
         // candidate rows by TMA gather4 (4 rows of 128 B per instruction,
         // SW128 applied by the map; lane l's rows land at tile row r0 + 4l,
         // i.e. atom (r0 + 4l) / 8).  Rows past cnt keep stale bytes: their
@@ -251,7 +263,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         __syncwarp();
         if (lane < ng) {
           const int32_t a = i0[0];
-          tma_gather4(s.tile[stage] + ((r0 + 4 * lane) >> 3) * 1024 + (lane & 1) * 512, &tmX,
+          tma_gather4(s.tile[tst] + ((r0 + 4 * lane) >> 3) * 1024 + (lane & 1) * 512, &tmX,
                       &s.full[stage], 0, a, i0[1] >= 0 ? i0[1] : a, i0[2] >= 0 ? i0[2] : a,
                       i0[3] >= 0 ? i0[3] : a);
         }
@@ -272,6 +284,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
           __syncwarp();
           if (lane == 0) mbar_arrive(&s.full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++tst == TSTAGES) { tst = 0; tph ^= 1; }
           half = 0;
         }
       }
@@ -298,6 +311,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       __syncwarp();
       if (lane == 0) mbar_arrive(&s.full[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      if (++tst == TSTAGES) { tst = 0; tph ^= 1; }
     }
     // end of stream: one sentinel per mask group (each reads every other point)
     for (int g = 0; g < GROUPS; ++g) {
@@ -310,7 +324,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA: G = C C^T per gathered point ----------------
-      int stage = 0, acc = 0;
+      int stage = 0, acc = 0, tst = 0;
       uint32_t phase = 0, tphase = 0;
       for (;;) {
         GWAIT(1, mbar_wait(&s.full[stage], phase));
@@ -318,13 +332,15 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         fence_proxy_async_smem();  // generic-proxy smem writes -> tensor-core reads
         GWAIT(2, mbar_wait(&s.tempty[acc], tphase ^ 1));
         tc_fence_after();
-        const uint64_t desc = sw128_desc(s.tile[stage]);
+        const uint64_t desc = sw128_desc(s.tile[tst]);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           mma_i8(tmem + acc * C, desc + 2 * kk, desc + 2 * kk, IDESC, kk > 0);
         tc_commit(&s.tfull[acc]);
+        tc_commit(&s.tfree[tst]);  // the rows are consumed: the next gather may land
         if (++acc == GROUPS) { acc = 0; tphase ^= 1; }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (++tst == TSTAGES) tst = 0;
       }
     }
   } else if (warp < GREEDY_WARP) {

@@ -176,5 +176,36 @@ def layered_search_counted(ds: Dataset, lg: LayeredGraph, q, k: int, L: int):
     return ids[:m], dists[:m], n_dist + int(dc[0].item())
 
 
+def layered_search_batch(ds: Dataset, lg: LayeredGraph, queries, k: int, L: int):
+    """layered_search for every row of ``queries`` at once: per layer ONE
+    beam-search launch over all queries, each from its own entry node (the
+    queries are independent, so every row equals its sequential search,
+    search.py:97-130).  Returns (ids (nq, k) -1 padded, dists (nq, k) +inf
+    padded, dist_counts (nq,)) as numpy arrays."""
+    Q = np.ascontiguousarray(queries, dtype=np.float32)
+    if Q.ndim != 2 or Q.shape[1] != ds.d:
+        raise ValueError(f"queries must have shape (nq, {ds.d})")
+    if k < 1 or k > L:
+        raise ValueError("need 1 <= k <= L")
+    X = ds.device_data()
+    nq = Q.shape[0]
+    Qd = torch.from_numpy(Q).to(X.device)
+    w = torch.full((nq,), lg.ep, dtype=torch.int64, device=X.device)
+    n_dist = torch.zeros(nq, dtype=torch.int64, device=X.device)
+    for li in range(lg.max_level, 0, -1):
+        layer = lg.layers[li]
+        mem = torch.from_numpy(layer.members.astype(np.int64)).to(X.device)
+        sub = X.index_select(0, mem).contiguous()
+        local = torch.searchsorted(mem, w).to(torch.int32)
+        ids, _, dc, _ = kernels.beam_search(sub, layer.graph.adj, layer.graph.counts, Qd, 1, 1,
+                                            eps=local)
+        n_dist += dc
+        w = mem[ids[:, 0].long()]
+    bottom = lg.layers[0]
+    ids, dists, dc, _ = kernels.beam_search(X, bottom.graph.adj, bottom.graph.counts, Qd, k, L,
+                                            eps=w.to(torch.int32))
+    return ids.cpu().numpy(), dists.cpu().numpy(), (n_dist + dc).cpu().numpy()
+
+
 __all__ = ["complete_graph", "LayerGraph", "LayeredGraph", "LayerAssignment", "assign_layers",
-           "FastHnswStats", "build_fasthnsw", "layered_search", "layered_search_counted"]
+           "FastHnswStats", "build_fasthnsw", "layered_search", "layered_search_counted", "layered_search_batch"]

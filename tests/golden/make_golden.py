@@ -308,6 +308,59 @@ def save_io_layered() -> None:
     print("io layered", sorted(p.name for p in out.iterdir()))
 
 
+def save_cfg5() -> None:
+    """Config 5 at full size: the reference's FastHNSW build
+    of the 200k x 128 config-2-recipe data (seed 4; k0=32, ef=200, one M=32
+    for all layers -- SURVEY A.1 --, alpha=66, max_iters=2) and its layered
+    search over the 10,000 seeded queries.  Layer 0 is stored as digests plus
+    2,000 seeded rows; upper layers in full; search ids at L=100 in full and
+    recall@10 at L = 50, 100, 200 against the exact float64 top-10."""
+    import time
+    from pgann import hnsw as R_hnsw
+    from pgann.oracle import mean_recall
+    from pgann.search import layered_search
+    base, q = synth.cfg5(200_000, 10_000)
+    ds = Dataset.from_array(base)
+    t0 = time.perf_counter()
+    lg = R_hnsw.build_fasthnsw(ds, k0=32, ef=200, M=32, alpha=66.0, seed=4)
+    build_s = time.perf_counter() - t0
+    rec = dict(levels=lg.levels.astype(np.int8), ep=np.int64(lg.ep),
+               nlayers=np.int64(len(lg.layers)), m_factor=np.float64(lg.m_factor),
+               build_s=np.float64(build_s), threads=np.int64(int(os.environ.get("NUMBA_NUM_THREADS", os.cpu_count()))))
+    for i, layer in enumerate(lg.layers):
+        g = layer.graph
+        off, nb = g.to_csr()
+        rec[f"L{i}_csr_sha"] = np.array(digest(off.astype(np.int64)) + digest(nb.astype(np.int32)))
+        rec[f"L{i}_ep"] = np.int64(g.ep)
+        rec[f"L{i}_over"] = np.asarray(g.over_cap, np.int32)
+        if i > 0:
+            rec[f"L{i}_members"] = layer.members
+            rec[f"L{i}_adj"], rec[f"L{i}_counts"] = g.adj, g.counts
+        else:
+            rec["L0_counts"] = g.counts.astype(np.int16)
+            rows = np.sort(np.random.default_rng(55).choice(ds.n, 2000, replace=False))
+            rec["L0_rows"] = rows
+            rec["L0_rows_adj"] = g.adj[rows]
+    x = base.astype(np.float64)
+    xn = (x * x).sum(1)
+    truth = np.empty((q.shape[0], 10), np.int32)
+    for lo in range(0, q.shape[0], 500):
+        qq = q[lo:lo + 500].astype(np.float64)
+        d2 = np.maximum(xn[None, :] - 2.0 * (qq @ x.T) + (qq * qq).sum(1)[:, None], 0.0)
+        truth[lo:lo + 500] = np.argsort(d2, axis=1, kind="stable")[:, :10]
+    for L in (50, 100, 200):
+        ids = np.full((q.shape[0], 10), -1, np.int32)
+        for j in range(q.shape[0]):
+            r = layered_search(ds, lg, q[j], 10, L)[0]
+            ids[j, :len(r)] = r
+        rec[f"recall_L{L}"] = np.float64(mean_recall(ids, truth, 10))
+        if L == 100:
+            rec["search_ids_L100"] = ids
+        print("cfg5 L", L, "recall@10", float(rec[f"recall_L{L}"]), flush=True)
+    print("cfg5 build_s", build_s, "layers", [len(l.members) for l in lg.layers])
+    np.savez_compressed(HERE / "cfg5.npz", **rec)
+
+
 def save_f3() -> None:
     """NN-Descent, FastNSG, NSG and FastHNSW outputs:
     knng.py:40-125, nsg.py:319-430, hnsw.py:141-192, search.py:97-130."""
@@ -377,6 +430,9 @@ def main() -> None:
         return
     if len(sys.argv) > 1 and sys.argv[1] == "io":
         save_io()
+        return
+    if len(sys.argv) > 1 and sys.argv[1] == "cfg5":
+        save_cfg5()
         return
     if len(sys.argv) > 1 and sys.argv[1] == "io_layered":
         save_io_layered()

@@ -94,3 +94,50 @@ def test_gpu_fasthnsw_saves_the_reference_file(tmp_path, name):
     back = pio.load_index(tmp_path / "g.pgix")
     assert back.ep == lg.ep and len(back.layers) == len(lg.layers)
     np.testing.assert_array_equal(back.levels, lg.levels)
+
+
+C5 = Path(__file__).resolve().parent / "golden" / "cfg5.npz"
+
+
+@pytest.mark.slow
+def test_cfg5_full_size_fasthnsw_matches_reference():
+    """BASELINE config 5 at its full size (200k x 128, config-2 recipe seed 4;
+    k0=32, ef=200, M=32 on every layer -- SURVEY A.1 --, alpha 66): levels,
+    entry point and every layer's adjacency equal the reference's own build
+    (upper layers in full, layer 0 by CSR digest + 2,000 seeded rows), and the
+    layered search over the 10,000 seeded queries returns the reference's ids
+    at L=100 and its recall@10 at L = 50, 100, 200 (edge agreement 100 %,
+    recall difference 0)."""
+    import hashlib
+
+    from paper_2410_01231_b200 import ground_truth_table, mean_recall, synth
+    g = np.load(C5)
+    base, q = synth.cfg5(200_000, 10_000)
+    ds = Dataset.from_array(base)
+    lg = hnsw.build_fasthnsw(ds, k0=32, ef=200, M=32, alpha=66.0, seed=4)
+    np.testing.assert_array_equal(lg.levels, g["levels"].astype(np.int32))
+    assert lg.ep == int(g["ep"]) and len(lg.layers) == int(g["nlayers"])
+    dig = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    for i, layer in enumerate(lg.layers):
+        off, nb = layer.graph.to_csr()
+        assert dig(off.astype(np.int64)) + dig(nb.astype(np.int32)) == str(g[f"L{i}_csr_sha"]), i
+        assert layer.graph.ep == int(g[f"L{i}_ep"])
+        np.testing.assert_array_equal(layer.graph.over_cap, g[f"L{i}_over"])
+        if i > 0:
+            np.testing.assert_array_equal(layer.members, g[f"L{i}_members"])
+            _live_equal(layer.graph.adj, layer.graph.counts, g[f"L{i}_adj"], g[f"L{i}_counts"],
+                        f"layer {i}")
+    rows = g["L0_rows"]
+    a0 = lg.layers[0].graph
+    np.testing.assert_array_equal(a0.counts, g["L0_counts"].astype(np.int32))
+    ref_rows, mine = g["L0_rows_adj"], a0.adj[rows]
+    W = max(ref_rows.shape[1], mine.shape[1])
+    pad = lambda a, c: np.where(np.arange(W)[None, :] < c[:, None],  # noqa: E731
+                                np.pad(a, ((0, 0), (0, W - a.shape[1])), constant_values=-1), -1)
+    np.testing.assert_array_equal(pad(mine, a0.counts[rows]), pad(ref_rows, a0.counts[rows]))
+    truth = ground_truth_table(ds, q, k=10)
+    for L in (50, 100, 200):
+        ids, _, _ = hnsw.layered_search_batch(ds, lg, q, 10, L)
+        if L == 100:
+            np.testing.assert_array_equal(ids, g["search_ids_L100"])
+        assert mean_recall(ids, truth, 10) == pytest.approx(float(g[f"recall_L{L}"]), abs=1e-12)
