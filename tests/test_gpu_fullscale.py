@@ -11,8 +11,11 @@ from _fullscale import graph_recall, pool_exactness
 
 pytestmark = pytest.mark.gpu
 
-# configs 3 (1M x 960) and 4 (2M x 768): the brute-force SIMT scans take minutes
-FULL = os.environ.get("PGK_FULL_PARITY", "1") == "1"
+# config 3's brute-force SIMT scan takes ~90 s, config 4's ~340 s (+ the
+# oracle rows: 2,000 take 93 s / 147 s on 16 host threads): the default run
+# checks config 3 with 500 oracle rows; PGK_FULL_PARITY=1 adds config 4 and
+# 2,000 rows each (tools/parity_report.py -> profiles/r02_parity.json ran both)
+FULL = os.environ.get("PGK_FULL_PARITY", "0") == "1"
 
 
 def _check_pool(r):
@@ -28,9 +31,9 @@ def test_cfg2_pruned_pools_equal_bruteforce_on_every_row():
 @pytest.mark.slow
 @pytest.mark.parametrize("cfg", [3, 4])
 def test_float_pruned_pools_equal_bruteforce_on_every_row(cfg):
-    if not FULL:
-        pytest.skip("PGK_FULL_PARITY=0")
-    _check_pool(pool_exactness(cfg))
+    if cfg == 4 and not FULL:
+        pytest.skip("config 4 (2M x 768 brute force, ~8 min): PGK_FULL_PARITY=1")
+    _check_pool(pool_exactness(cfg, oracle_rows=2000 if FULL else 500))
 
 
 @pytest.mark.parametrize("strategy,alpha", [("rng", 60.0), ("alpha", 66.0)])
