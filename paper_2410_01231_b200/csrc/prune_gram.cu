@@ -50,14 +50,7 @@ constexpr int C = 128;          // candidates per point (TMEM lanes)
 #ifndef GRAM_NBUF
 #define GRAM_NBUF 2  // measured: 3 buffers cost 5 % (less shared memory left to L1)
 #endif
-#ifndef GRAM_TSTAGES
-#define GRAM_TSTAGES GRAM_STAGES
-#endif
-// Two rings: point slots (metadata: ids, dists, norms; freed by the mask
-// warps) and u8 row tiles (freed by the MMA's commit, so the next gather
-// starts while the masks of this point are still being built).
-constexpr int STAGES = GRAM_STAGES;    // point slots in flight
-constexpr int TSTAGES = GRAM_TSTAGES;  // row tiles in flight
+constexpr int STAGES = GRAM_STAGES;  // gathered points in flight
 constexpr int GROUPS = GRAM_GROUPS;  // mask warpgroups = TMEM accumulators (point parity)
 constexpr int NG = GRAM_GREEDY;      // greedy warps: point k goes to warp k % NG
 constexpr int NBUF = GRAM_NBUF;      // mask buffers: point k uses k % NBUF
@@ -70,7 +63,7 @@ constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(C >> 3) << 17) | ((uint32_t)(
 
 template <int STRATEGY>
 struct __align__(1024) Smem {
-  uint8_t tile[TSTAGES][C * 128];  // SW128 K-major: 8-row x 128-byte atoms
+  uint8_t tile[STAGES][C * 128];  // SW128 K-major: 8-row x 128-byte atoms
   int32_t id[STAGES][C];
   float dist[STAGES][C];
   alignas(16) int32_t nrm[STAGES][C];
@@ -88,7 +81,6 @@ struct __align__(1024) Smem {
   int64_t gu[NBUF][2];     // -1: empty slot
   int32_t gcnt[NBUF][2];    // [0] -1: end of stream
   uint64_t full[STAGES], empty[STAGES];
-  uint64_t tfree[TSTAGES];  // tile consumed by the MMA (tcgen05.commit)
   uint64_t tfull[GROUPS], tempty[GROUPS];
   uint64_t mfull[NBUF], mempty[NBUF];
   uint32_t tmem_base;
@@ -142,10 +134,9 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&s.full[i], 1);    // gather lane 0 (after the stage's STS), + TMA bytes
+      mbar_init(&s.full[i], 33);   // gather: 32 cp.async arrivals + lane 0 (after the STS), + TMA bytes
       mbar_init(&s.empty[i], 4);   // released by the 4 mask warps
     }
-    for (int i = 0; i < TSTAGES; ++i) mbar_init(&s.tfree[i], 1);
     for (int i = 0; i < GROUPS; ++i) {
       mbar_init(&s.tfull[i], 1);
       mbar_init(&s.tempty[i], 4);
@@ -171,33 +162,41 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   if (warp == 0) {
     // ---------------- gather: rows, ids, dists, norms of one point --------
     // This CTA's points are i = blockIdx.x + k * gridDim.x; their (u, cnt,
-    // off, self) are loaded 32 at a time (lane j: point k0 + j).  Software
-    // pipeline, all in registers, so no dependent global round trip sits
-    // between a free stage and its publication:
-    //   point k+2: candidate ids in flight
-    //   point k+1: candidate dists + norms in flight
-    //   point k  : published into a free stage (TMA gather4 rows, STS rest)
-    // Lane l holds candidates 4l..4l+3 (id -1, dist 0, norm 0 past cnt); its
-    // gather4 fetches exactly those rows.  The other roles follow the stream
-    // published in s.u / s.cnt / s.self.
-    int stage = 0, half = 0, tst = 0;
-    uint32_t phase = 0, tph = 0;
+    // off, self) are loaded 32 at a time (lane j: point 32b + j), two
+    // batches resident, the next one fetched in two steps (node ids, then
+    // their counts / offsets) well before it is needed.  The only values
+    // the warp itself waits for are each point's candidate ids (the TMA
+    // gather's row coordinates), loaded GD points ahead; dists and norms go
+    // global -> shared by cp.async, completed on the stage's full barrier
+    // (32 asynchronous arrivals + lane 0's), so no dependent global round
+    // trip sits in this loop.  Lane l holds candidates 4l..4l+3 (id -1 past
+    // cnt); its gather4 fetches exactly those rows.
+    constexpr int GD = 3;
+    int stage = 0, half = 0;
+    uint32_t phase = 0;
     const int64_t nb = blockIdx.x < n_rows ? (n_rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    int64_t bu = 0, boff = 0;
-    int bcnt = 0, bself = 0;
-    auto load_batch = [&](int64_t k0) {
-      const int64_t k = k0 + lane;
-      bu = 0;
-      bcnt = 0;
-      boff = 0;
-      bself = 0;
-      if (k < nb) {
-        const int64_t i = blockIdx.x + k * gridDim.x;
-        bu = row_order ? row_order[i] : i;
-        bcnt = cand_counts[bu];
-        boff = cand_off[bu];
-        bself = row_node ? row_node[bu] : (int32_t)bu;
+    int64_t bu0 = 0, bu1 = 0, bo0 = 0, bo1 = 0;
+    int bc0 = 0, bc1 = 0, bs0 = 0, bs1 = 0;
+    auto fetch_u = [&](int64_t b) {  // batch b, step 1: node ids
+      const int64_t kk = b * 32 + lane;
+      int64_t u = 0;
+      if (kk < nb) {
+        const int64_t i = blockIdx.x + kk * gridDim.x;
+        u = row_order ? row_order[i] : i;
       }
+      if (b & 1) bu1 = u; else bu0 = u;
+    };
+    auto fetch_rest = [&](int64_t b) {  // step 2: counts, offsets, self ids
+      const int64_t kk = b * 32 + lane;
+      const int64_t u = (b & 1) ? bu1 : bu0;
+      int c = 0, sf = 0;
+      int64_t o = 0;
+      if (kk < nb) {
+        c = cand_counts[u];
+        o = cand_off[u];
+        sf = row_node ? row_node[u] : (int32_t)u;
+      }
+      if (b & 1) { bc1 = c; bo1 = o; bs1 = sf; } else { bc0 = c; bo0 = o; bs0 = sf; }
     };
     struct PM {
       int64_t u, off;
@@ -206,52 +205,52 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     auto meta = [&](int64_t j) {
       PM m{0, 0, -1, 0};
       if (j < nb) {
-        if ((j & 31) == 0) load_batch(j);
+        const bool odd = (j >> 5) & 1;
         const int src = (int)(j & 31);
-        m.u = __shfl_sync(0xffffffffu, bu, src);
-        m.off = __shfl_sync(0xffffffffu, boff, src);
-        m.cnt = __shfl_sync(0xffffffffu, bcnt, src);
-        m.self = __shfl_sync(0xffffffffu, bself, src);
+        m.u = __shfl_sync(0xffffffffu, odd ? bu1 : bu0, src);
+        m.off = __shfl_sync(0xffffffffu, odd ? bo1 : bo0, src);
+        m.cnt = __shfl_sync(0xffffffffu, odd ? bc1 : bc0, src);
+        m.self = __shfl_sync(0xffffffffu, odd ? bs1 : bs0, src);
       }
       return m;
     };
     auto ids_of = [&](const PM &m, int32_t (&o)[4]) {
+      const int r = 4 * lane;
+      if (m.cnt <= PC && r + 3 < m.cnt && (m.off & 3) == 0) {
+        const int4 v = *reinterpret_cast<const int4 *>(cand_ids + m.off + r);
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+      } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = 4 * lane + i;
-        o[i] = (m.cnt <= PC && r < m.cnt) ? cand_ids[m.off + r] : -1;
+        for (int i = 0; i < 4; ++i)
+          o[i] = (m.cnt <= PC && r + i < m.cnt) ? cand_ids[m.off + r + i] : -1;
       }
     };
-    auto dn_of = [&](const PM &m, const int32_t (&id)[4], float (&dd)[4], int32_t (&nn)[4]) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = 4 * lane + i;
-        const bool ok = m.cnt <= PC && r < m.cnt;
-        dd[i] = ok ? cand_dists[m.off + r] : 0.f;
-        nn[i] = ok ? norms[id[i]] : 0;
-      }
+    auto publish_end = [&]() {  // the stage is complete: 32 async + 1 arrivals
+      cp_async_mbar_arrive(&s.full[stage]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s.full[stage]);
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
     };
-    PM m0 = meta(0), m1 = meta(1);
-    int32_t i0[4], i1[4];
-    float d0[4];
-    int32_t n0[4];
-    ids_of(m0, i0);
-    ids_of(m1, i1);
-    dn_of(m0, i0, d0, n0);
+    fetch_u(0);
+    fetch_rest(0);
+    fetch_u(1);
+    fetch_rest(1);
+    int32_t i0[4], i1[4], i2[4];
+    ids_of(meta(0), i0);
+    ids_of(meta(1), i1);
+    ids_of(meta(2), i2);
+    static_assert(GD == 3, "the id registers below hold three points");
     for (int64_t k = 0; k < nb; ++k) {
-      const PM m2 = meta(k + 2);
-      int32_t i2[4];
-      ids_of(m2, i2);
-      float d1[4];
-      int32_t n1[4];
-      dn_of(m1, i1, d1, n1);
+      const int64_t b = k >> 5;
+      if (b >= 1 && (k & 31) == 0) fetch_u(b + 1);
+      if (b >= 1 && (k & 31) == 16) fetch_rest(b + 1);
+      int32_t i3[4];
+      ids_of(meta(k + GD), i3);
+      const PM m0 = meta(k);
       if (m0.cnt > PC) {  // hub row (PAIR: > 64): left to the next kernel
         if (lane == 0) long_rows[atomicAdd(long_count, 1)] = (int32_t)m0.u;
       } else {
-        if (half == 0) {
-          GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
-          mbar_wait(&s.tfree[tst], tph ^ 1);
-        }
+        if (half == 0) GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
         // candidate rows by TMA gather4 (4 rows of 128 B per instruction,
         // SW128 applied by the map; lane l's rows land at tile row r0 + 4l,
         // i.e. atom (r0 + 4l) / 8).  Rows past cnt keep stale bytes: their
@@ -263,15 +262,24 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         __syncwarp();
         if (lane < ng) {
           const int32_t a = i0[0];
-          tma_gather4(s.tile[tst] + ((r0 + 4 * lane) >> 3) * 1024 + (lane & 1) * 512, &tmX,
+          tma_gather4(s.tile[stage] + ((r0 + 4 * lane) >> 3) * 1024 + (lane & 1) * 512, &tmX,
                       &s.full[stage], 0, a, i0[1] >= 0 ? i0[1] : a, i0[2] >= 0 ? i0[2] : a,
                       i0[3] >= 0 ? i0[3] : a);
         }
         if (4 * lane < PC) {
-          *reinterpret_cast<int4 *>(&s.id[stage][r0 + 4 * lane]) = make_int4(i0[0], i0[1], i0[2], i0[3]);
-          *reinterpret_cast<float4 *>(&s.dist[stage][r0 + 4 * lane]) =
-              make_float4(d0[0], d0[1], d0[2], d0[3]);
-          *reinterpret_cast<int4 *>(&s.nrm[stage][r0 + 4 * lane]) = make_int4(n0[0], n0[1], n0[2], n0[3]);
+          const int rb = r0 + 4 * lane;
+          *reinterpret_cast<int4 *>(&s.id[stage][rb]) = make_int4(i0[0], i0[1], i0[2], i0[3]);
+          // dists and norms: asynchronous copies (id -1 past cnt: zeros)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (i0[i] >= 0) {
+              cp_async4(&s.dist[stage][rb + i], cand_dists + m0.off + 4 * lane + i);
+              cp_async4(&s.nrm[stage][rb + i], norms + i0[i]);
+            } else {
+              s.dist[stage][rb + i] = 0.f;
+              s.nrm[stage][rb + i] = 0;
+            }
+          }
         }
         if (lane == 0) {
           s.u[stage][half] = m0.u;
@@ -281,21 +289,15 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         if (PAIR && half == 0) {
           half = 1;  // the next point fills the other half of this stage
         } else {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&s.full[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-          if (++tst == TSTAGES) { tst = 0; tph ^= 1; }
+          publish_end();
           half = 0;
         }
       }
-      m0 = m1;
-      m1 = m2;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         i0[i] = i1[i];
-        d0[i] = d1[i];
-        n0[i] = n1[i];
         i1[i] = i2[i];
+        i2[i] = i3[i];
       }
     }
     if (PAIR && half == 1) {  // a half-filled last stage: the second slot is empty
@@ -308,23 +310,18 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         *reinterpret_cast<float4 *>(&s.dist[stage][64 + 4 * lane]) = make_float4(0.f, 0.f, 0.f, 0.f);
         *reinterpret_cast<int4 *>(&s.nrm[stage][64 + 4 * lane]) = make_int4(0, 0, 0, 0);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s.full[stage]);
-      if (++stage == STAGES) { stage = 0; phase ^= 1; }
-      if (++tst == TSTAGES) { tst = 0; tph ^= 1; }
+      publish_end();
     }
     // end of stream: one sentinel per mask group (each reads every other point)
     for (int g = 0; g < GROUPS; ++g) {
       GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
       if (lane == 0) s.cnt[stage][0] = g == 0 ? -1 : -2;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s.full[stage]);
-      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      publish_end();
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA: G = C C^T per gathered point ----------------
-      int stage = 0, acc = 0, tst = 0;
+      int stage = 0, acc = 0;
       uint32_t phase = 0, tphase = 0;
       for (;;) {
         GWAIT(1, mbar_wait(&s.full[stage], phase));
@@ -332,15 +329,13 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         fence_proxy_async_smem();  // generic-proxy smem writes -> tensor-core reads
         GWAIT(2, mbar_wait(&s.tempty[acc], tphase ^ 1));
         tc_fence_after();
-        const uint64_t desc = sw128_desc(s.tile[tst]);
+        const uint64_t desc = sw128_desc(s.tile[stage]);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           mma_i8(tmem + acc * C, desc + 2 * kk, desc + 2 * kk, IDESC, kk > 0);
         tc_commit(&s.tfull[acc]);
-        tc_commit(&s.tfree[tst]);  // the rows are consumed: the next gather may land
         if (++acc == GROUPS) { acc = 0; tphase ^= 1; }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        if (++tst == TSTAGES) tst = 0;
       }
     }
   } else if (warp < GREEDY_WARP) {
