@@ -1099,6 +1099,9 @@ static bool make_map(CUtensorMap *tm, const uint8_t *base, int64_t rows) {
 
 // (128-byte rows x rows) u8 tensor map with a (128 x box_rows) box, SW128;
 // box_rows = 1 is the TMA gather4 form (prune_gram.cu)
+#ifndef GRAM_L2_PROMO
+#define GRAM_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 bool make_u8_row_map(CUtensorMap *tm, const uint8_t *base, int64_t rows, int box_rows) {
   auto fn = tc::encode_fn();
   if (!fn) return false;
@@ -1108,7 +1111,7 @@ bool make_u8_row_map(CUtensorMap *tm, const uint8_t *base, int64_t rows, int box
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void *)base, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  GRAM_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 

@@ -47,6 +47,15 @@ constexpr int C = 128;          // candidates per point (TMEM lanes)
 #ifndef GRAM_GREEDY
 #define GRAM_GREEDY 2
 #endif
+#ifndef GRAM_ROWS_CPASYNC
+#define GRAM_ROWS_CPASYNC 0  // candidate rows by 16-byte cp.async instead of TMA gather4
+#endif
+#ifndef GRAM_TMA_ROWS
+#define GRAM_TMA_ROWS 64  // with GRAM_ROWS_CPASYNC: rows per point left to TMA gather4
+#endif
+#ifndef GRAM_NORMS_GATHER
+#define GRAM_NORMS_GATHER 1  // 1: the gather warp fetches |c|^2 (cp.async); 0: mask warps compute it
+#endif
 #ifndef GRAM_NBUF
 #define GRAM_NBUF 2  // measured: 3 buffers cost 5 % (less shared memory left to L1)
 #endif
@@ -100,8 +109,15 @@ __device__ unsigned long long g_gram_stats[16];
     expr;                                                   \
     if (lane == 0) atomicAdd(&g_gram_stats[slot], (unsigned long long)(clock64() - t0_)); \
   } while (0)
+#define GMARK(acc)                                            \
+  do {                                                      \
+    const long long t_ = clock64();                         \
+    acc += t_ - gmark_;                                     \
+    gmark_ = t_;                                            \
+  } while (0)
 #else
 #define GWAIT(slot, expr) expr
+#define GMARK(acc) do { } while (0)
 #endif
 
 // PAIR: two points of <= 64 candidates per stage / MMA (rows 0..63 and
@@ -112,7 +128,7 @@ __device__ unsigned long long g_gram_stats[16];
 template <int STRATEGY, bool PAIR>  // 0 = rng, 1 = alpha (compile-time: no angle code for rng)
 __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     prune_gram_kernel(const __grid_constant__ CUtensorMap tmX,
-                      const int32_t *__restrict__ norms,
+                      const uint8_t *__restrict__ xrows, const int32_t *__restrict__ norms,
                       int64_t n_rows, const int32_t *__restrict__ row_node,
                       const int32_t *__restrict__ row_order,
                       const int64_t *__restrict__ cand_off,
@@ -240,7 +256,11 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     ids_of(meta(1), i1);
     ids_of(meta(2), i2);
     static_assert(GD == 3, "the id registers below hold three points");
+#if GRAM_STATS
+    long long gmark_ = clock64(), g_meta = 0, g_tma = 0, g_cpa = 0, g_pub = 0, g_wait = 0;
+#endif
     for (int64_t k = 0; k < nb; ++k) {
+      GMARK(g_pub);
       const int64_t b = k >> 5;
       if (b >= 1 && (k & 31) == 0) fetch_u(b + 1);
       if (b >= 1 && (k & 31) == 16) fetch_rest(b + 1);
@@ -250,7 +270,9 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       if (m0.cnt > PC) {  // hub row (PAIR: > 64): left to the next kernel
         if (lane == 0) long_rows[atomicAdd(long_count, 1)] = (int32_t)m0.u;
       } else {
+        GMARK(g_meta);
         if (half == 0) GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
+        GMARK(g_wait);
         // candidate rows by TMA gather4 (4 rows of 128 B per instruction,
         // SW128 applied by the map; lane l's rows land at tile row r0 + 4l,
         // i.e. atom (r0 + 4l) / 8).  Rows past cnt keep stale bytes: their
@@ -258,26 +280,53 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         // examinable, i >= cnt > t unused).
         const int r0 = half * 64;
         const int ng = (m0.cnt + 3) >> 2;
-        if (lane == 0) mbar_expect_tx_only(&s.full[stage], (uint32_t)ng * 512u);
+        // GRAM_ROWS_CPASYNC: rows [ncp0, cnt) by 16-byte cp.async (instruction m
+        // moves 4 rows, 8 lanes per row: lane l takes row 4m + l/8, chunk
+        // l%8 at SW128 position chunk ^ (row % 8); ids read back from the
+        // stage), rows [0, ncp0) by TMA gather4: the two paths in parallel
+        const int ncp0 = GRAM_ROWS_CPASYNC ? GRAM_TMA_ROWS : 4 * ng;
+        const int ngt = min(ng, ncp0 >> 2);  // TMA gather4 instructions
+        if (lane == 0 && ngt > 0) mbar_expect_tx_only(&s.full[stage], (uint32_t)ngt * 512u);
+        if (GRAM_ROWS_CPASYNC && 4 * lane < PC)
+          *reinterpret_cast<int4 *>(&s.id[stage][r0 + 4 * lane]) = make_int4(i0[0], i0[1], i0[2], i0[3]);
         __syncwarp();
-        if (lane < ng) {
+        if (lane < ngt) {
           const int32_t a = i0[0];
           tma_gather4(s.tile[stage] + ((r0 + 4 * lane) >> 3) * 1024 + (lane & 1) * 512, &tmX,
                       &s.full[stage], 0, a, i0[1] >= 0 ? i0[1] : a, i0[2] >= 0 ? i0[2] : a,
                       i0[3] >= 0 ? i0[3] : a);
         }
+        if (GRAM_ROWS_CPASYNC) {
+          const int j = lane & 7, rq = lane >> 3;
+          for (int m = ngt; m < ng; ++m) {
+            const int ra = r0 + 4 * m + rq;  // tile row
+            const int32_t id = s.id[stage][ra];
+            if (id >= 0)
+              cp_async16_zfill(s.tile[stage] + (ra >> 3) * 1024 + (ra & 7) * 128 + ((j ^ (ra & 7)) << 4),
+                               xrows + (int64_t)id * 128 + j * 16, 16);
+          }
+        }
+        GMARK(g_tma);
         if (4 * lane < PC) {
           const int rb = r0 + 4 * lane;
           *reinterpret_cast<int4 *>(&s.id[stage][rb]) = make_int4(i0[0], i0[1], i0[2], i0[3]);
-          // dists and norms: asynchronous copies (id -1 past cnt: zeros)
+          // dists: asynchronous copies (id -1 past cnt: zeros); the norms
+          // are computed by the mask warps from the gathered rows
+#if GRAM_NORMS_GATHER
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            if (i0[i] >= 0) {
-              cp_async4(&s.dist[stage][rb + i], cand_dists + m0.off + 4 * lane + i);
-              cp_async4(&s.nrm[stage][rb + i], norms + i0[i]);
-            } else {
-              s.dist[stage][rb + i] = 0.f;
-              s.nrm[stage][rb + i] = 0;
+            if (i0[i] >= 0) cp_async4(&s.nrm[stage][rb + i], norms + i0[i]);
+            else s.nrm[stage][rb + i] = 0;
+          }
+#endif
+          const float *dsrc = cand_dists + m0.off + 4 * lane;
+          if (i0[3] >= 0 && ((uintptr_t)dsrc & 15) == 0) {
+            cp_async16_zfill(&s.dist[stage][rb], dsrc, 16);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (i0[i] >= 0) cp_async4(&s.dist[stage][rb + i], dsrc + i);
+              else s.dist[stage][rb + i] = 0.f;
             }
           }
         }
@@ -286,6 +335,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
           s.cnt[stage][half] = m0.cnt;
           s.self[stage][half] = m0.self;
         }
+        GMARK(g_cpa);
         if (PAIR && half == 0) {
           half = 1;  // the next point fills the other half of this stage
         } else {
@@ -312,6 +362,15 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       }
       publish_end();
     }
+#if GRAM_STATS
+    if (lane == 0) {
+      atomicAdd(&g_gram_stats[11], (unsigned long long)g_meta);
+      atomicAdd(&g_gram_stats[12], (unsigned long long)g_tma);
+      atomicAdd(&g_gram_stats[13], (unsigned long long)g_cpa);
+      atomicAdd(&g_gram_stats[14], (unsigned long long)g_pub);
+      atomicAdd(&g_gram_stats[15], (unsigned long long)g_wait);
+    }
+#endif
     // end of stream: one sentinel per mask group (each reads every other point)
     for (int g = 0; g < GROUPS; ++g) {
       GWAIT(0, mbar_wait(&s.empty[stage], phase ^ 1));
@@ -374,9 +433,32 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       const int32_t self = s.self[stage][P];
       const int32_t *sid = s.id[stage];
       const float *sdist = s.dist[stage];
-      const int32_t *snrm = s.nrm[stage];
+      int32_t *snrm = s.nrm[stage];
       const float dv = sdist[t];
+      // |c_t|^2 from the gathered row itself (SW128: 16-byte chunk j of tile
+      // row t sits at atom t/8, row t%8, position j ^ (t%8)), published for
+      // the other mask warps: no norm gather in the gather warp's loop.
+      // Rows past cnt hold stale bytes; their norms feed no mask bit read.
+#if GRAM_NORMS_GATHER
       const int nv = snrm[t];
+#else
+      unsigned nvu = 0;
+      {
+        const uint8_t *rowp = s.tile[stage] + (t >> 3) * 1024 + (t & 7) * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 w = *reinterpret_cast<const uint4 *>(rowp + ((j ^ (t & 7)) << 4));
+          nvu = __dp4a(w.x, w.x, nvu);
+          nvu = __dp4a(w.y, w.y, nvu);
+          nvu = __dp4a(w.z, w.z, nvu);
+          nvu = __dp4a(w.w, w.w, nvu);
+        }
+        snrm[t] = (int)nvu;
+        if (GROUPS == 1) asm volatile("bar.sync 1, 128;" ::: "memory");
+        else named_bar_sync(1 + grp, 128);
+      }
+      const int nv = (int)nvu;
+#endif
       // c_i dominates c_t (rng) iff duw == 0 or dwv == 0 or dwv < dv, with
       // dwv = |c_i|^2 + |c_t|^2 - 2 G[t][i] an exact integer >= 0:
       //   dwv < dv  <=>  dwv <= ceil(dv) - 1;  dwv == 0  <=>  dwv <= 0
@@ -654,7 +736,8 @@ bool gram_enabled() {
 // pair: rows of <= 64 candidates two per MMA first (the phase-B re-prune),
 // the longer ones listed on the device for the single-point kernel.
 template <int STRATEGY, bool PAIR>
-static int launch_gram_kernel(const CUtensorMap &tmX, const int32_t *norms, int64_t n,
+static int launch_gram_kernel(const CUtensorMap &tmX, const uint8_t *xu8, const int32_t *norms,
+                              int64_t n,
                               const int32_t *n_dev, const int32_t *row_node,
                               const int32_t *row_order, const int64_t *cand_off,
                               const int32_t *cand_counts, const int32_t *cand_ids,
@@ -666,7 +749,7 @@ static int launch_gram_kernel(const CUtensorMap &tmX, const int32_t *norms, int6
   PGK_CUDA(ensure_smem((const void *)gram::prune_gram_kernel<STRATEGY, PAIR>, smem));
   const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)gram::CTAS_PER_SM * num_sms());
   gram::prune_gram_kernel<STRATEGY, PAIR><<<grid, gram::THREADS, smem, stream>>>(
-      tmX, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
+      tmX, xu8, norms, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
       cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals,
       long_rows, long_count, n_dev);
   PGK_CHECK_LAUNCH("prune_gram_kernel");
@@ -697,11 +780,11 @@ int launch_prune_gram(const uint8_t *xu8, const int32_t *norms, int64_t n,
   const int sa = rng ? strategy : 1;
   int rc;
   if (pair) {
-    rc = rng ? launch_gram_kernel<0, true>(tmX, norms, n, nullptr, row_node, row_order, cand_off,
+    rc = rng ? launch_gram_kernel<0, true>(tmX, xu8, norms, n, nullptr, row_node, row_order, cand_off,
                                            cand_counts, cand_ids, cand_dists, sa, cos_alpha, M,
                                            width, out_ids, out_dists, out_counts, dist_evals,
                                            angle_evals, pair_rows, pair_count, stream)
-             : launch_gram_kernel<1, true>(tmX, norms, n, nullptr, row_node, row_order, cand_off,
+             : launch_gram_kernel<1, true>(tmX, xu8, norms, n, nullptr, row_node, row_order, cand_off,
                                            cand_counts, cand_ids, cand_dists, sa, cos_alpha, M,
                                            width, out_ids, out_dists, out_counts, dist_evals,
                                            angle_evals, pair_rows, pair_count, stream);
@@ -710,11 +793,11 @@ int launch_prune_gram(const uint8_t *xu8, const int32_t *norms, int64_t n,
   // single-point kernel: every row, or (pair) the rows listed above
   const int32_t *order1 = pair ? pair_rows : row_order;
   const int32_t *n1_dev = pair ? pair_count : nullptr;
-  rc = rng ? launch_gram_kernel<0, false>(tmX, norms, n, n1_dev, row_node, order1, cand_off,
+  rc = rng ? launch_gram_kernel<0, false>(tmX, xu8, norms, n, n1_dev, row_node, order1, cand_off,
                                           cand_counts, cand_ids, cand_dists, sa, cos_alpha, M,
                                           width, out_ids, out_dists, out_counts, dist_evals,
                                           angle_evals, long_rows, long_count, stream)
-           : launch_gram_kernel<1, false>(tmX, norms, n, n1_dev, row_node, order1, cand_off,
+           : launch_gram_kernel<1, false>(tmX, xu8, norms, n, n1_dev, row_node, order1, cand_off,
                                           cand_counts, cand_ids, cand_dists, sa, cos_alpha, M,
                                           width, out_ids, out_dists, out_counts, dist_evals,
                                           angle_evals, long_rows, long_count, stream);
@@ -734,6 +817,9 @@ int launch_prune_gram(const uint8_t *xu8, const int32_t *norms, int64_t n,
             h[7] / ctas / 1e6, h[8] / ctas / 1e6, h[9] / ctas / 1e6, h[10] / ctas / 1e6,
             h[0] / ctas / 1e6, h[1] / ctas / 1e6, h[2] / ctas / 1e6, h[3] / ctas / 4e6,
             h[4] / ctas / 4e6, h[5] / ctas / 4e6, h[6] / ctas / 1e6);
+    fprintf(stderr, "[gram stats] gather loop per CTA, Mcycles: meta+ids %.2f empty-wait %.2f tma-issue %.2f "
+            "cp.async+sts %.2f publish %.2f\n", h[11] / ctas / 1e6, h[15] / ctas / 1e6,
+            h[12] / ctas / 1e6, h[13] / ctas / 1e6, h[14] / ctas / 1e6);
     unsigned long long z[16] = {0};
     PGK_CUDA(cudaMemcpyToSymbol(gram::g_gram_stats, z, sizeof(z)));
   }
