@@ -50,6 +50,9 @@ constexpr int C = 128;          // candidates per point (TMEM lanes)
 #ifndef GRAM_ROWS_CPASYNC
 #define GRAM_ROWS_CPASYNC 0  // candidate rows by 16-byte cp.async instead of TMA gather4
 #endif
+#ifndef GRAM_TMA_SINGLE
+#define GRAM_TMA_SINGLE 0  // 1: lane 0 issues all gather4 ops from shared-memory ids
+#endif
 #ifndef GRAM_TMA_ROWS
 #define GRAM_TMA_ROWS 64  // with GRAM_ROWS_CPASYNC: rows per point left to TMA gather4
 #endif
@@ -290,12 +293,34 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         if (GRAM_ROWS_CPASYNC && 4 * lane < PC)
           *reinterpret_cast<int4 *>(&s.id[stage][r0 + 4 * lane]) = make_int4(i0[0], i0[1], i0[2], i0[3]);
         __syncwarp();
+#if GRAM_TMA_SINGLE
+        // one thread issues every gather4 (row ids staged in shared memory:
+        // no per-lane ELECT / R2UR serialisation loop)
+        if (4 * lane < PC) {
+          const int32_t a = i0[0];
+          *reinterpret_cast<int4 *>(&s.id[stage][r0 + 4 * lane]) =
+              make_int4(a, i0[1] >= 0 ? i0[1] : a, i0[2] >= 0 ? i0[2] : a, i0[3] >= 0 ? i0[3] : a);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          const int4 *idv = reinterpret_cast<const int4 *>(&s.id[stage][r0]);
+          uint8_t *tb = s.tile[stage] + (r0 >> 3) * 1024;
+#pragma unroll 4
+          for (int g = 0; g < ngt; ++g) {
+            const int4 v = idv[g];
+            tma_gather4(tb + (g >> 1) * 1024 + (g & 1) * 512, &tmX, &s.full[stage], 0, v.x, v.y,
+                        v.z, v.w);
+          }
+        }
+        __syncwarp();
+#else
         if (lane < ngt) {
           const int32_t a = i0[0];
           tma_gather4(s.tile[stage] + ((r0 + 4 * lane) >> 3) * 1024 + (lane & 1) * 512, &tmX,
                       &s.full[stage], 0, a, i0[1] >= 0 ? i0[1] : a, i0[2] >= 0 ? i0[2] : a,
                       i0[3] >= 0 ? i0[3] : a);
         }
+#endif
         if (GRAM_ROWS_CPASYNC) {
           const int j = lane & 7, rq = lane >> 3;
           for (int m = ngt; m < ng; ++m) {
