@@ -588,13 +588,22 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
             PGK_TICK(ST_COMPACT);
             {
               // every lane appends its own survivors (per-row serial loops
-              // across the warp measured 2.8x slower than these divergent
-              // per-lane appends)
+              // across the warp measured 2.8x slower than these per-lane
+              // appends), in a warp-uniform loop of max-over-lanes trips with
+              // predicated stores: no divergent branch to resolve per survivor
               uint64_t *mybuf = wbuf + (size_t)lane * CAP + cnt;
-              for (unsigned mm = mask; mm; mm &= mm - 1) {
-                const int j = __ffs(mm) - 1;
+              const int trips = (int)__reduce_max_sync(0xffffffffu, (unsigned)__popc(mask));
+              unsigned mm = mask;
+#pragma unroll 2
+              for (int it = 0; it < trips; ++it) {
+                const bool act = mm != 0;
+                const int j = act ? __ffs(mm) - 1 : 0;
                 const int32_t cid = perm ? s.pid[tpar][c * 32 + j] : (int32_t)(cb + j);
-                *mybuf++ = ((uint64_t)(uint32_t)(tny[j] - 2 * sv[j] + nx) << 32) | (uint32_t)cid;
+                const uint64_t key =
+                    ((uint64_t)(uint32_t)(tny[j] - 2 * sv[j] + nx) << 32) | (uint32_t)cid;
+                if (act) *mybuf = key;
+                mybuf += act ? 1 : 0;
+                mm &= mm - 1;
               }
             }
             cnt += __popc(mask);
@@ -676,7 +685,8 @@ struct FinOut {          // optional direct pool output (pool_simt's arrays)
 template <int KPL, bool ON_ID>
 __device__ __forceinline__ uint32_t radix_pick(const uint64_t (&kk)[KPL], int cnt, uint32_t tie_d,
                                                int &need, uint32_t *hist, int lane,
-                                               int max_passes, bool &exact) {
+                                               int max_passes, bool &exact,
+                                               uint32_t *lo_edge = nullptr) {
   uint32_t vmin = 0xffffffffu, vmax = 0;
 #pragma unroll
   for (int i = 0; i < KPL; ++i) {
@@ -737,10 +747,52 @@ __device__ __forceinline__ uint32_t radix_pick(const uint64_t (&kk)[KPL], int cn
     __syncwarp();
   }
   exact = shift == 0;
+  if (lo_edge) *lo_edge = vmin + (prefix << shift);
   return exact ? vmin + prefix : vmin + (((prefix + 1) << shift) - 1);
 }
 
 // exact K-th smallest (dist, id) key of cnt > K register-resident keys
+template <int KPL>
+__device__ __forceinline__ uint64_t radix_kth(const uint64_t (&kk)[KPL], int cnt, int K,
+                                              uint32_t *hist, int lane);
+
+// The same, faster in the common case: ONE 8-bit radix pass over the row's
+// distance range isolates the bucket holding the K-th key; when that bucket
+// holds at most 32 keys (a few, typically) they are compacted into `scratch`
+// and the K-th is found by ranking them against each other -- full (dist, id)
+// keys, so distance ties need no separate id pass.  Otherwise the full radix.
+template <int KPL>
+__device__ __forceinline__ uint64_t radix_kth_fast(const uint64_t (&kk)[KPL], int cnt, int K,
+                                                   uint32_t *hist, uint64_t *scratch, int lane) {
+  int need = K;
+  bool exact;
+  uint32_t lo = 0;
+  const uint32_t hi = radix_pick<KPL, false>(kk, cnt, 0, need, hist, lane, 1, exact, &lo);
+  int bc = 0;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const uint32_t dv = khi(kk[i]);
+    bc += __popc(__ballot_sync(0xffffffffu, i * 32 + lane < cnt && dv >= lo && dv <= hi));
+  }
+  if (bc > 32) return radix_kth<KPL>(kk, cnt, K, hist, lane);
+  int base = 0;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const uint32_t dv = khi(kk[i]);
+    const bool in = i * 32 + lane < cnt && dv >= lo && dv <= hi;
+    const unsigned b = __ballot_sync(0xffffffffu, in);
+    if (in) scratch[base + __popc(b & lanemask_lt())] = kk[i];
+    base += __popc(b);
+  }
+  __syncwarp();
+  const uint64_t mine = lane < bc ? scratch[lane] : KEY_MAX;
+  int rank = 0;
+  for (int o = 0; o < bc; ++o) rank += scratch[o] < mine;
+  const unsigned hit = __ballot_sync(0xffffffffu, lane < bc && rank == need - 1);
+  __syncwarp();
+  return __shfl_sync(0xffffffffu, mine, __ffs(hit) - 1);
+}
+
 template <int KPL>
 __device__ __forceinline__ uint64_t radix_kth(const uint64_t (&kk)[KPL], int cnt, int K,
                                               uint32_t *hist, int lane) {
@@ -897,7 +949,7 @@ __device__ __noinline__ bool select_stage(const uint64_t *__restrict__ buf, int 
     if (lane == 0) out_keys[orow * K + K - 1] = kth;
     return false;
   }
-  const uint64_t tau = cnt > K ? radix_kth<KPL>(kk, cnt, K, hist, lane) : KEY_MAX;
+  const uint64_t tau = cnt > K ? radix_kth_fast<KPL>(kk, cnt, K, hist, stage, lane) : KEY_MAX;
   int base = 0;
 #pragma unroll
   for (int i = 0; i < KPL; ++i) {
