@@ -255,7 +255,9 @@ __device__ __forceinline__ uint32_t dense_val(int dist, int64_t col, int64_t n, 
                                         : 0xffffu;
 }
 
-template <bool STATS, bool DENSE>
+// K1: the K = 1 (nearest neighbour) instantiation; the K > 1 one carries no
+// K = 1 code (registers and scheduling of the pass-2 epilogue).
+template <bool STATS, bool DENSE, bool K1 = false>
 // 112 registers keeps CTAS_PER_SM = 3 resident (3 x 6 warps x 112 x 32 <= 64K)
 __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
     tc_pool_u8_kernel(const __grid_constant__ CUtensorMap tmX,
@@ -269,6 +271,8 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
                       int32_t *__restrict__ row_cnt, uint64_t *__restrict__ row_tau,
                       int32_t *__restrict__ sched, const uint8_t *__restrict__ row_mask,
                       int k1_direct) {
+  // K == 1 paths: compiled in for the K1 instantiation (and the STATS one)
+  const bool isk1 = K1 ? true : (STATS ? K == 1 : false);
   unsigned long long st[ST_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t_prev = STATS ? clock64() : 0;
 #define PGK_TICK(slot)                          \
@@ -434,7 +438,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
         const uint64_t k0 = init_keys[(perm ? (int64_t)perm[row] : row) * K + K - 1];
         if (k0 != KEY_MAX) {
           const uint32_t d0 = (uint32_t)key_dist(k0);
-          if (K == 1) {
+          if (isk1) {
             tau = (((uint64_t)d0 << 32) | (uint32_t)key_id(k0)) + 1;
           } else {
             // optionally a GUESS below the bound (shrink < 1): exact iff the
@@ -502,6 +506,57 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
             }
             continue;
           }
+          if (isk1) {
+            // nearest neighbour only (the center assignment): the chunk's
+            // minimum s_j (3-input min tree), then -- only when some row
+            // improves -- the smallest id among the columns at that minimum.
+            // Same result as the survivor-mask path below, ~half the work.
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const int4 w = nyp[v];
+              r[4 * v] = (uint32_t)(w.x - 2 * (int)r[4 * v]);
+              r[4 * v + 1] = (uint32_t)(w.y - 2 * (int)r[4 * v + 1]);
+              r[4 * v + 2] = (uint32_t)(w.z - 2 * (int)r[4 * v + 2]);
+              r[4 * v + 3] = (uint32_t)(w.w - 2 * (int)r[4 * v + 3]);
+            }
+            if (__any_sync(0xffffffffu, tp >= 0x3f000000)) {  // rows without a threshold yet
+              const int64_t colj = cb + lane;
+              const int32_t cidj = perm ? s.pid[tpar][c * 32 + lane] : (int32_t)colj;
+              const uint32_t ok = __ballot_sync(0xffffffffu, colj < n && cidj >= 0);
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (!((ok >> j) & 1u)) r[j] = 0x7fffffffu;
+            }
+            if (exclude_self && __any_sync(0xffffffffu, row >= cb && row < cb + 32)) {
+              const int sj = (row >= cb && row < cb + 32) ? (int)(row - cb) : -1;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j == sj) r[j] = 0x7fffffffu;
+            }
+            int smin = 0x7fffffff;
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) smin = min(smin, min((int)r[j], (int)r[j + 1]));
+            const bool imp = smin <= tp;
+            if (__any_sync(0xffffffffu, imp)) {
+              uint32_t idm = 0xffffffffu;
+              const int4 *pp = reinterpret_cast<const int4 *>(s.pid[tpar] + c * 32);
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                const int4 pd = perm ? pp[v] : make_int4((int)(cb + 4 * v), (int)(cb + 4 * v + 1),
+                                                         (int)(cb + 4 * v + 2), (int)(cb + 4 * v + 3));
+                idm = (int)r[4 * v] == smin ? min(idm, (uint32_t)pd.x) : idm;
+                idm = (int)r[4 * v + 1] == smin ? min(idm, (uint32_t)pd.y) : idm;
+                idm = (int)r[4 * v + 2] == smin ? min(idm, (uint32_t)pd.z) : idm;
+                idm = (int)r[4 * v + 3] == smin ? min(idm, (uint32_t)pd.w) : idm;
+              }
+              const uint64_t key = ((uint64_t)(uint32_t)(smin + nx) << 32) | idm;
+              if (imp && key < tau) {
+                tau = key;
+                tp = tau_prefilter(tau, nx);
+              }
+            }
+            continue;
+          }
           // s_j = |x_j|^2 - 2 q.x_j ; pass iff s_j <= tp
           uint32_t mask = 0;
 #pragma unroll
@@ -527,7 +582,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
               mask &= __ballot_sync(0xffffffffu, colj < n && cidj >= 0);
             }
             if (exclude_self && row >= cb && row < cb + 32) mask &= ~(1u << (int)(row - cb));
-            if (K == 1) {  // nearest neighbour only: the threshold IS the answer
+            if (isk1) {  // nearest neighbour only: the threshold IS the answer
               // branch-free minimum (dist, id) key over the chunk's survivors
               uint64_t best = KEY_MAX;
               const int4 *pp = reinterpret_cast<const int4 *>(s.pid[tpar] + c * 32);
@@ -552,7 +607,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
               }
               continue;
             }
-            const bool track = K > 1 && tau == KEY_MAX && mask;
+            const bool track = !isk1 && tau == KEY_MAX && mask;
             // stage the raw dot products (s_j = |x_j|^2 - 2 sv[j] is formed
             // per survivor from the tile's norms)
             if (mask) {
@@ -633,7 +688,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
         row_tau[row] = tau;
         // K == 1: the threshold is the answer; each lane writes its own row
         // (no finalize pass)
-        if (K == 1 && k1_direct && row_ok) {
+        if (isk1 && k1_direct && row_ok) {
           const int64_t orow = perm ? (int64_t)perm[row] : row;
           out_keys[orow] =
               tau == KEY_MAX ? KEY_MAX : pack_key((float)khi(tau), (int32_t)(uint32_t)tau);
@@ -1249,6 +1304,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   PGK_CUDA(ensure_smem((const void *)tc::tc_pool_u8_kernel<false, false>, smem));
   PGK_CUDA(ensure_smem((const void *)tc::tc_pool_u8_kernel<true, false>, smem));
   PGK_CUDA(ensure_smem((const void *)tc::tc_pool_u8_kernel<false, true>, smem));
+  PGK_CUDA(ensure_smem((const void *)tc::tc_pool_u8_kernel<false, false, true>, smem));
   const int nblocks = (int)((nq + tc::BM - 1) / tc::BM);
   const unsigned grid = (unsigned)std::min<int64_t>(nblocks, (int64_t)tc::CTAS_PER_SM * sms);
   PGK_CUDA(cudaMemsetAsync(sched, 0, sizeof(int32_t), stream));
@@ -1289,9 +1345,14 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
             h[0] / warps, h[1] / warps, h[2] / warps, h[3] / warps, h[4] / warps, h[5] / warps,
             h[6] / warps, (double)h[7] / (double)nq);
   } else {
-    tc::tc_pool_u8_kernel<false, false><<<grid, tc::THREADS, smem, stream>>>(
-        tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
-        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, k1_direct);
+    if (K == 1)
+      tc::tc_pool_u8_kernel<false, false, true><<<grid, tc::THREADS, smem, stream>>>(
+          tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
+          tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, k1_direct);
+    else
+      tc::tc_pool_u8_kernel<false, false><<<grid, tc::THREADS, smem, stream>>>(
+          tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
+          tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, k1_direct);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel");
     if (k1_direct) {
       *handled = true;

@@ -113,3 +113,27 @@ def test_pool_from_callers_u8_rows_equals_fp32_input(n, d, K):
     a = kernels.knn_pools(X, K, mode=_lib.POOL_U8, want_gt=False)
     b = kernels.knn_pools(X, K, mode=_lib.POOL_U8, want_gt=False, u8=kernels.make_u8(X))
     assert torch.equal(a.pool_ids, b.pool_ids) and torch.equal(a.pool_dists, b.pool_dists)
+
+
+@pytest.mark.parametrize("n,nq", [(5000, 700), (20000, 0)])
+def test_nearest_neighbour_k1_path(n, nq):
+    """K = 1 (the epilogue's nearest-neighbour path, which also assigns points
+    to tile centers): query tables and the self pool equal the oracle's exact
+    (float64 dist, id) nearest neighbour, ties on duplicates included."""
+    from paper_2410_01231_b200 import ground_truth_table
+    rng = np.random.default_rng(17)
+    data = synth.cfg2(n)
+    data[rng.choice(n, 200, replace=False)] = data[rng.choice(n, 200, replace=False)]  # dups
+    ds = Dataset.from_array(data)
+    if nq:
+        q = synth.cfg2(n + nq)[n:]
+        got = ground_truth_table(ds, q, k=1)
+        for i in range(0, nq, 13):
+            d64 = ((data.astype(np.float64) - q[i].astype(np.float64)) ** 2).sum(1)
+            assert got[i, 0] == np.lexsort((np.arange(n), d64))[0]
+    else:
+        ids, dists = knn_pools(ds, 1)
+        rows = rng.choice(n, 300, replace=False)
+        o_ids, o_d = oracle.knn_pools(data, 1, rows)
+        np.testing.assert_array_equal(ids[rows], o_ids)
+        np.testing.assert_array_equal(dists[rows], o_d)
