@@ -420,6 +420,255 @@ __global__ void tile_filter_kernel(const float *__restrict__ dc, const double *_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cell-level bounds (sparse tile lists, no T x T centroid-distance matrix).
+// Tiles come in cells (every tile lies inside one center's run), so a cell
+// is a ball around g_A (the size-weighted mean of its tile centroids, fp32)
+// of radius R_A = max_{T in A} (|g_A - c_T| + r_T), and every tile Q of A is
+// inside the ball around g_A of radius rho_Q = |c_Q - g_A| + r_Q.  For
+// q in Q and x in any tile of cell B:
+//     |q - x| >= |g_A - g_B| - rho_Q - R_B =: lbC(Q, B)
+// so a whole cell is skipped when lbC > U_Q; only the tiles of the remaining
+// cells get their centroid distance (computed on the fly, the same fp32
+// norm-expansion lower bound as tile_dist_kernel) and the tile test.
+// ---------------------------------------------------------------------------
+
+// tile -> cell map (cells own contiguous tile runs: off is in padded rows)
+__global__ void tile_cell_kernel(const int64_t *__restrict__ off, int64_t C,
+                                 int32_t *__restrict__ tcell) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
+       c += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t t = off[c] / TB; t < off[c + 1] / TB; ++t) tcell[t] = (int32_t)c;
+}
+
+// block (TB threads, thread = dimension) per cell: g_A, then (warp 0) the
+// cell radius and every tile's radius around g_A, in float64 from the fp32
+// centroids, inflated by a relative margin
+__global__ void __launch_bounds__(TB) cell_stats_kernel(const float *__restrict__ cent,
+                                                        const double *__restrict__ rad,
+                                                        const int32_t *__restrict__ size,
+                                                        const int64_t *__restrict__ off,
+                                                        int64_t C, int d, float *__restrict__ g,
+                                                        double *__restrict__ Rc,
+                                                        double *__restrict__ rho) {
+  __shared__ float gs[TB];
+  const int j = threadIdx.x, lane = j & 31;
+  for (int64_t c = blockIdx.x; c < C; c += gridDim.x) {
+    const int64_t t0 = off[c] / TB, t1 = off[c + 1] / TB;
+    double acc = 0.0, w = 0.0;
+    for (int64_t t = t0; t < t1; ++t) {
+      const int sz = size[t];
+      if (sz > 0 && j < d) acc += (double)sz * (double)cent[t * d + j];
+      w += sz;
+    }
+    const float gj = (w > 0 && j < d) ? (float)(acc / w) : 0.f;
+    if (j < d) g[c * d + j] = gj;
+    gs[j] = gj;
+    __syncthreads();
+    if (j < 32) {
+      double R = w > 0 ? 0.0 : -1.0;  // -1: an empty cell, never a candidate
+      for (int64_t t = t0; t < t1; ++t) {
+        double s2 = 0.0;
+        for (int k = lane; k < d; k += 32) {
+          const double dd = (double)cent[t * d + k] - (double)gs[k];
+          s2 += dd * dd;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        const double rr = sqrt(s2) * (1.0 + 1e-9) + 1e-12 + rad[t];
+        if (lane == 0) rho[t] = rr;
+        if (size[t] > 0) R = fmax(R, rr);
+      }
+      if (lane == 0) Rc[c] = R;
+    }
+    __syncthreads();
+  }
+}
+
+// lower bound of |c_Q - c_T| from the fp32 centroids (tile_dist_kernel<true>'s
+// formula: FMA dot in dimension order, error <= (d+8) 2^-24 (|c_Q|^2+|c_T|^2))
+__device__ __forceinline__ float dc_lower(const float *__restrict__ cq, const float *__restrict__ ct,
+                                          float cnq, float cnt, int d) {
+  float acc = 0.f;
+  if ((d & 3) == 0) {
+    for (int k = 0; k < d; k += 4) {
+      const float4 a = *reinterpret_cast<const float4 *>(cq + k);
+      const float4 b = *reinterpret_cast<const float4 *>(ct + k);
+      acc = fmaf(a.x, b.x, acc);
+      acc = fmaf(a.y, b.y, acc);
+      acc = fmaf(a.z, b.z, acc);
+      acc = fmaf(a.w, b.w, acc);
+    }
+  } else {
+    for (int k = 0; k < d; ++k) acc = fmaf(cq[k], ct[k], acc);
+  }
+  const double nn = (double)cnq + (double)cnt;
+  const double e = (double)(d + 8) * 5.9604644775390625e-08 * 1.01 * nn;
+  return (float)sqrt(fmax(nn - 2.0 * (double)acc - e, 0.0));
+}
+
+// pass-1 lists from cells: Q's own cell and its nearest cells (by the cell
+// centroid distance) supply the candidate tiles; the nearest of those by
+// centroid distance, as many as hold >= P1_MULT * K points (<= NEAR tiles).
+// Any real points bound the K-th distance from above, so this is an
+// efficiency choice only.  Lists stride NEAR.
+constexpr int P1_CELLS = 6;
+__global__ void tile_nearest_cells_kernel(const float *__restrict__ cent,
+                                          const float *__restrict__ cn,
+                                          const int32_t *__restrict__ size,
+                                          const int32_t *__restrict__ tcell,
+                                          const int64_t *__restrict__ off,
+                                          const float *__restrict__ dcc,
+                                          const double *__restrict__ Rc, int64_t C, int64_t T,
+                                          int d, int K, int32_t *__restrict__ lists,
+                                          int32_t *__restrict__ lens,
+                                          unsigned long long *__restrict__ total) {
+  __shared__ uint64_t ck[8][64];  // 256 threads: per-warp candidate slots
+  const int lane = threadIdx.x & 31;
+  for (int64_t Q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; Q < T;
+       Q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    if (size[Q] <= 0) {
+      if (lane == 0) lens[Q] = 0;
+      continue;
+    }
+    const int32_t A = tcell[Q];
+    // the P1_CELLS nearest non-empty cells (A itself at distance 0 first):
+    // per-lane best list, then warp minima
+    uint64_t best[P1_CELLS];
+#pragma unroll
+    for (int i = 0; i < P1_CELLS; ++i) best[i] = KEY_MAX;
+    for (int64_t b = lane; b < C; b += 32) {
+      if (Rc[b] < 0.0) continue;
+      const float v = b == A ? 0.f : dcc[(int64_t)A * C + b];
+      const uint64_t k = ((uint64_t)__float_as_uint(v) << 32) | (uint32_t)b;
+      if (k < best[P1_CELLS - 1]) {
+#pragma unroll
+        for (int i = P1_CELLS - 1; i > 0; --i)
+          best[i] = k < best[i - 1] ? best[i - 1] : (k < best[i] ? k : best[i]);
+        best[0] = k < best[0] ? k : best[0];
+      }
+    }
+    // candidate tiles (<= 64): (dc, tile) keys staged in this warp's slots
+    uint64_t *mk = ck[threadIdx.x >> 5];
+    int nc = 0;
+    for (int i = 0; i < P1_CELLS; ++i) {
+      uint64_t mn = best[0];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t y = __shfl_xor_sync(0xffffffffu, mn, o);
+        mn = y < mn ? y : mn;
+      }
+      if (mn == KEY_MAX) break;
+      if (best[0] == mn) {
+#pragma unroll
+        for (int j = 0; j + 1 < P1_CELLS; ++j) best[j] = best[j + 1];
+        best[P1_CELLS - 1] = KEY_MAX;
+      }
+      const int64_t bc = (uint32_t)mn;
+      const int64_t ta = off[bc] / TB, tb = off[bc + 1] / TB;
+      for (int64_t t0 = ta; t0 < tb && nc < 64; t0 += 32) {
+        const int64_t t = t0 + lane;
+        const bool ok = t < tb && size[t] > 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        const int pos = nc + __popc(bal & ((1u << lane) - 1u));
+        if (ok && pos < 64) {
+          const float v = dc_lower(cent + Q * d, cent + t * d, cn[Q], cn[t], d);
+          mk[pos] = ((uint64_t)__float_as_uint(v) << 32) | (uint32_t)t;
+        }
+        nc = min(64, nc + __popc(bal));
+      }
+    }
+    __syncwarp();
+    uint64_t cand[2] = {lane < nc ? mk[lane] : KEY_MAX, lane + 32 < nc ? mk[lane + 32] : KEY_MAX};
+    __syncwarp();
+    // the nearest candidates in order until P1_MULT * K points
+    int m = 0, pts = 0;
+    uint32_t mine = 0;
+    for (int i = 0; i < NEAR; ++i) {
+      uint64_t a = cand[0] < cand[1] ? cand[0] : cand[1];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t y = __shfl_xor_sync(0xffffffffu, a, o);
+        a = y < a ? y : a;
+      }
+      if (a == KEY_MAX) break;
+      if (cand[0] == a) cand[0] = KEY_MAX;
+      else if (cand[1] == a) cand[1] = KEY_MAX;
+      if (lane == i) mine = (uint32_t)a;
+      pts += size[(uint32_t)a];
+      m = i + 1;
+      if (pts >= P1_MULT * K) break;
+    }
+    if (lane < m) lists[Q * NEAR + lane] = (int32_t)mine;
+    if (lane == 0) {
+      lens[Q] = m;
+      atomicAdd(total, (unsigned long long)m);
+    }
+    __syncwarp();
+  }
+}
+
+// pass-2 lists from cells: every tile T with lb(Q,T) <= scale * U_Q, ascending
+// T (cells in order, tiles in order), skipping whole cells by lbC; lists
+// stride T as before.  `only`: just the tiles Q with only[Q] != 0.
+__global__ void tile_filter_cells_kernel(const float *__restrict__ cent,
+                                         const float *__restrict__ cn,
+                                         const double *__restrict__ rad,
+                                         const double *__restrict__ rho,
+                                         const int32_t *__restrict__ size,
+                                         const int32_t *__restrict__ tcell,
+                                         const int64_t *__restrict__ off,
+                                         const float *__restrict__ dcc,
+                                         const double *__restrict__ Rc,
+                                         const double *__restrict__ U, int64_t C, int64_t T,
+                                         int d, int32_t *__restrict__ lists,
+                                         int32_t *__restrict__ lens,
+                                         unsigned long long *__restrict__ total,
+                                         double dc_margin, double scale,
+                                         const int32_t *__restrict__ only) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t Q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; Q < T;
+       Q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    if ((only && only[Q] == 0) || size[Q] <= 0) {
+      if (lane == 0) lens[Q] = 0;
+      continue;
+    }
+    const int32_t A = tcell[Q];
+    const double rQ = rad[Q], rhoQ = rho[Q], UQ = U[Q] * scale + 1e-9;
+    int base = 0;
+    for (int64_t b0 = 0; b0 < C; b0 += 32) {
+      const int64_t b = b0 + lane;
+      bool cell = false;
+      if (b < C && Rc[b] >= 0.0) {
+        const double lbc = (b == A ? 0.0 : (double)dcc[(int64_t)A * C + b] * (1.0 - dc_margin)) -
+                           rhoQ - Rc[b];
+        cell = lbc <= UQ;
+      }
+      unsigned cm = __ballot_sync(0xffffffffu, cell);
+      while (cm) {  // candidate cells in ascending order
+        const int64_t bb = b0 + __ffs(cm) - 1;
+        cm &= cm - 1;
+        const int64_t ta = off[bb] / TB, tb = off[bb + 1] / TB;
+        for (int64_t t0 = ta; t0 < tb; t0 += 32) {
+          const int64_t t = t0 + lane;
+          bool keep = false;
+          if (t < tb && size[t] > 0) {
+            const float v = dc_lower(cent + Q * d, cent + t * d, cn[Q], cn[t], d);
+            keep = (double)v * (1.0 - dc_margin) - rQ - rad[t] <= UQ;
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, keep);
+          if (keep) lists[Q * T + base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)t;
+          base += __popc(bal);
+        }
+      }
+    }
+    if (lane == 0) {
+      lens[Q] = base;
+      if (total) atomicAdd(total, (unsigned long long)base);
+    }
+  }
+}
+
 // Pass-2 threshold guess: seed * SHRINK (exclusive squared-distance bound).
 // In high dimension the final K-th distance is a near-constant fraction of
 // the pass-1 seed (config 2: 0.86-0.92), so the guess cuts the buffered
@@ -435,7 +684,9 @@ static float seed_shrink() {
 }
 
 struct Layout {
-  float *cen, *cent, *dcm, *cn;
+  float *cen, *cent, *cn, *gcell, *gcn, *dcc;
+  double *Rc, *rho;
+  int32_t *tcell;
   int32_t *cnorm, *hist, *cursor, *assign, *perm, *ns, *size, *lists, *lens, *fail, *lens2;
   uint8_t *fail_rows;
   int64_t *off, *scan_tmp;
@@ -491,7 +742,12 @@ static tiles::Layout tiles_layout(void *ws, size_t bytes, int64_t n, int64_t d) 
   L.fail = c.take<int32_t>(T);
   L.lens2 = c.take<int32_t>(T);
   L.fail_rows = c.take<uint8_t>(NP);
-  L.dcm = c.take<float>((size_t)T * T);
+  L.gcell = c.take<float>((size_t)C * d);
+  L.gcn = c.take<float>(C);
+  L.Rc = c.take<double>(C);
+  L.rho = c.take<double>(T);
+  L.tcell = c.take<int32_t>(T);
+  L.dcc = c.take<float>((size_t)C * C);
   L.U = c.take<double>(T);
   L.total = c.take<unsigned long long>(4);
   L.sub_bytes = tc_pool_workspace(C, n, false);
@@ -626,14 +882,25 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   PGK_CUDA(cudaMemsetAsync(L.total, 0, 4 * sizeof(unsigned long long), stream));
   cent_norms_kernel<<<g, 256, 0, stream>>>(L.cent, T, d, L.cn);
   PGK_CHECK_LAUNCH("cent_norms_kernel");
-  tile_dist_kernel<true><<<dim3((unsigned)((T + DB - 1) / DB), (unsigned)((T + DB - 1) / DB)),
-                            256, 0, stream>>>(L.cent, T, d, L.dcm, L.cn);
-  PGK_CHECK_LAUNCH("tile_dist_kernel");
-  dbg_stage("tile_dist_kernel", stream);
-  // 4. pass 1: exact top-K over each query tile's NEAR nearest tiles -> U_Q
-  tile_nearest_kernel<<<g, 256, 0, stream>>>(L.dcm, L.size, T, K, L.lists, L.lens, L.total + 1);
-  PGK_CHECK_LAUNCH("tile_nearest_kernel");
-  dbg_stage("tile_nearest_kernel", stream);
+  // cells as balls (g_A, R_A), tiles' radii around their cell, and the C x C
+  // cell-centroid distances: the bounds of the sparse tile lists
+  tile_cell_kernel<<<g, 256, 0, stream>>>(L.off, C, L.tcell);
+  PGK_CHECK_LAUNCH("tile_cell_kernel");
+  cell_stats_kernel<<<(unsigned)std::min<int64_t>(C, (int64_t)sms * 16), TB, 0, stream>>>(
+      L.cent, L.rad, L.size, L.off, C, d, L.gcell, L.Rc, L.rho);
+  PGK_CHECK_LAUNCH("cell_stats_kernel");
+  cent_norms_kernel<<<g, 256, 0, stream>>>(L.gcell, C, d, L.gcn);
+  PGK_CHECK_LAUNCH("cent_norms_kernel");
+  tile_dist_kernel<true><<<dim3((unsigned)((C + DB - 1) / DB), (unsigned)((C + DB - 1) / DB)),
+                            256, 0, stream>>>(L.gcell, C, d, L.dcc, L.gcn);
+  PGK_CHECK_LAUNCH("tile_dist_kernel (cells)");
+  dbg_stage("cell bounds", stream);
+  // 4. pass 1: exact top-K over each query tile's nearest tiles (from its
+  // own and the nearest cells) -> U_Q; lists of stride NEAR
+  tile_nearest_cells_kernel<<<g, 256, 0, stream>>>(L.cent, L.cn, L.size, L.tcell, L.off, L.dcc,
+                                                   L.Rc, C, T, d, K, L.lists, L.lens, L.total + 1);
+  PGK_CHECK_LAUNCH("tile_nearest_cells_kernel");
+  dbg_stage("tile_nearest_cells_kernel", stream);
   const char *se0 = getenv("PGK_TILES_STATS");
   uint32_t *ostat = nullptr;
   if (se0 && se0[0] == '1') {  // pass-1 order statistics for the guess analysis
@@ -641,7 +908,7 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
     g_dense_ostat = ostat;
   }
   rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes, stream,
-                               L.xs, L.lists, L.lens, T, L.perm, handled, nullptr, 1);
+                               L.xs, L.lists, L.lens, NEAR, L.perm, handled, nullptr, 1);
   g_dense_ostat = nullptr;
   if (rc) return rc;
   dbg_stage("pass 1 tc", stream);
@@ -655,10 +922,10 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   // within sqrt(shrink) * U_Q of the tile: the list can be cut to that
   // radius; rows failing the guess re-run on the full-radius list (step 6).
   const float shrink = seed_shrink();
-  tile_filter_kernel<<<g, 256, 0, stream>>>(L.dcm, L.rad, L.size, L.U, T, L.lists, L.lens,
-                                            L.total, DC_MARGIN,
-                                            shrink < 1.0f ? sqrt((double)shrink) : 1.0);
-  PGK_CHECK_LAUNCH("tile_filter_kernel");
+  tile_filter_cells_kernel<<<g, 256, 0, stream>>>(
+      L.cent, L.cn, L.rad, L.rho, L.size, L.tcell, L.off, L.dcc, L.Rc, L.U, C, T, d, L.lists,
+      L.lens, L.total, DC_MARGIN, shrink < 1.0f ? sqrt((double)shrink) : 1.0, nullptr);
+  PGK_CHECK_LAUNCH("tile_filter_cells_kernel");
   dbg_stage("tile_filter_kernel", stream);
   const char *se = getenv("PGK_TILES_STATS");
   const bool stats = se && se[0] == '1';
@@ -678,9 +945,10 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
   if (shrink < 1.0f) {
     // 6. re-run the rows whose guess was too tight (their blocks, row mask),
     // seeded by their untouched pass-1 key, on the full-radius list
-    tile_filter_kernel<<<g, 256, 0, stream>>>(L.dcm, L.rad, L.size, L.U, T, L.lists, L.lens2,
-                                              nullptr, DC_MARGIN, 1.0, L.fail);
-    PGK_CHECK_LAUNCH("tile_filter_kernel (re-run)");
+    tile_filter_cells_kernel<<<g, 256, 0, stream>>>(
+        L.cent, L.cn, L.rad, L.rho, L.size, L.tcell, L.off, L.dcc, L.Rc, L.U, C, T, d, L.lists,
+        L.lens2, nullptr, DC_MARGIN, 1.0, L.fail);
+    PGK_CHECK_LAUNCH("tile_filter_cells_kernel (re-run)");
   dbg_stage("tile_filter_kernel (re-run)", stream);
     if (stats) {
       std::vector<int32_t> hf(T);
