@@ -763,8 +763,9 @@ bool tiles_supported(int64_t n, int64_t d, int64_t k) {
     env = (e && e[0] == '1') ? 1 : 0;
   }
   const int64_t T = ((n + 127) / 128 * 128 + (n + tiles::CSTRIDE - 1) / tiles::CSTRIDE * 128) / 128;
-  // the T x T centroid-distance matrix and lists (8 B / pair) stay modest
-  return !env && d <= 128 && k <= 256 && n >= 8 * tiles::TB && T <= 32768;
+  // the T x T list storage (4 B / tile pair: 6 GB at 4M points) stays
+  // bounded; the bounds themselves are per cell pair (no T x T matrix)
+  return !env && d <= 128 && k <= 256 && n >= 8 * tiles::TB && T <= 65536;
 }
 
 size_t tiles_workspace(int64_t n, int64_t d) { return tiles_layout(nullptr, 0, n, d).bytes; }

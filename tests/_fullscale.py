@@ -28,11 +28,13 @@ def _equal_rows(a_ids, a_d, b_ids, b_d) -> int:
     return int(same.sum().item())
 
 
-def pool_exactness(cfg: int, oracle_rows: int = 2000, seed: int = 7) -> dict:
+def pool_exactness(cfg: int, oracle_rows: int = 2000, seed: int = 7, n: int = 0) -> dict:
     """Pruned pools vs the brute-force pools on all rows, and vs the oracle on
-    `oracle_rows` seeded rows, at config `cfg`'s full size."""
+    `oracle_rows` seeded rows, at config `cfg`'s full size (or n rows of the
+    config's recipe drawn as an n-row array: the scale test)."""
     c = synth.CONFIGS[cfg]
-    n, K = c["n"], c["K"]
+    K = c["K"]
+    n = n or c["n"]
     data = c["gen"](n, n)
     X = torch.from_numpy(data).cuda()
     mode = _lib.POOL_U8 if kernels.detect_u8(X) else _lib.POOL_F32

@@ -36,6 +36,16 @@ def test_float_pruned_pools_equal_bruteforce_on_every_row(cfg):
     _check_pool(pool_exactness(cfg, oracle_rows=2000 if FULL else 500))
 
 
+@pytest.mark.slow
+def test_pruned_pool_at_4m_points_equals_bruteforce():
+    """Scale: 4,000,000 x 128 (the config-2 recipe drawn at 4M rows, ~39k
+    tiles -- beyond round 1's 32,768-tile cap, which fell back to the O(N^2)
+    scan): the tile-pruned pool runs and equals the brute force on every row."""
+    if not FULL:
+        pytest.skip("4M x 128 brute force (~10 s) and ~80 GB of workspaces: PGK_FULL_PARITY=1")
+    _check_pool(pool_exactness(2, oracle_rows=300, n=4_000_000))
+
+
 @pytest.mark.parametrize("strategy,alpha", [("rng", 60.0), ("alpha", 66.0)])
 def test_graph_edge_agreement_and_recall_vs_oracle_graph(strategy, alpha):
     """north_star: >= 99.9 % edge agreement, recall@10 within 0.2 points of the

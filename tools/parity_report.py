@@ -22,10 +22,15 @@ def main():
     ap.add_argument("--configs", default="2,3,4")
     ap.add_argument("--n", type=int, default=50_000)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--scale-n", type=int, default=0, help="also config 2's recipe at this size")
     a = ap.parse_args()
     out = {"pools": [], "graphs": []}
     for cfg in [int(x) for x in a.configs.split(",") if x]:
         r = pool_exactness(cfg)
+        print(json.dumps(r), file=sys.stderr, flush=True)
+        out["pools"].append(r)
+    if a.scale_n:
+        r = pool_exactness(2, oracle_rows=300, n=a.scale_n)
         print(json.dumps(r), file=sys.stderr, flush=True)
         out["pools"].append(r)
     if not a.no_graph:
