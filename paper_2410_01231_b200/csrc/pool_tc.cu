@@ -1164,6 +1164,128 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, 4)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Rows whose guessed pass-2 threshold proved too tight (fail_rows != 0, ~0.2 %
+// of the rows): an exact rescan on the SIMT cores instead of re-running their
+// whole 128-row blocks on the tensor cores.  Block per failing row: the 8
+// warps share the full-radius tile list of the row's block; every key with
+// dist <= the row's pass-1 seed (an upper bound of its true K-th distance,
+// the seed is the row's untouched pass-1 key) goes to the row's buffer, which
+// is compacted to the K best (select_k) whenever the next round could
+// overflow it; warp 0 then finalizes the row (finalize_row).  Distances are
+// the same exact integers as the tensor-core path (dp4a on the u8 rows).
+// ---------------------------------------------------------------------------
+__global__ void fail_list_kernel(const uint8_t *__restrict__ fail_rows, int64_t nrows,
+                                 int32_t *__restrict__ list, int32_t *__restrict__ count) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x)
+    if (fail_rows[r]) list[atomicAdd(count, 1)] = (int32_t)r;
+}
+
+constexpr int RR_THREADS = FIN_WARPS * 32;
+constexpr int RR_ROUND = FIN_WARPS * BN;  // keys one round (a tile per warp) can produce
+__global__ void __launch_bounds__(RR_THREADS, 2)
+    rerun_rows_kernel(const uint8_t *__restrict__ xs, const int32_t *__restrict__ ns,
+                      const int32_t *__restrict__ perm, const int32_t *__restrict__ list,
+                      const int32_t *__restrict__ count, const int32_t *__restrict__ tlist,
+                      const int32_t *__restrict__ tlen, int64_t tstride,
+                      const uint64_t *__restrict__ seeds, int K, uint64_t *__restrict__ bufs,
+                      uint64_t *__restrict__ out_keys, FinOut fo) {
+  __shared__ uint32_t s_hist[256];
+  __shared__ uint64_t s_stage[FIN_STAGE];
+  __shared__ uint64_t s_round[RR_ROUND];  // this round's survivors
+  __shared__ int s_rc, s_cnt;
+  __shared__ uint32_t s_t;  // exclusive distance bound
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nl = *count;
+  for (int li = blockIdx.x; li < nl; li += gridDim.x) {
+    const int64_t r = list[li];
+    const int64_t orow = perm[r];
+    uint64_t *buf = bufs + r * CAP;
+    // the query row (u8, 128 B) in registers, word w = bytes 4w..4w+3
+    uint32_t q[32];
+    const uint4 *qr = reinterpret_cast<const uint4 *>(xs + r * KB);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const uint4 w = qr[v];
+      q[4 * v] = w.x; q[4 * v + 1] = w.y; q[4 * v + 2] = w.z; q[4 * v + 3] = w.w;
+    }
+    const int nq = ns[r];
+    if (threadIdx.x == 0) {
+      const uint64_t k0 = seeds[orow * K + K - 1];
+      s_t = k0 == KEY_MAX ? 0xffffffffu : (uint32_t)key_dist(k0) + 1u;
+      s_cnt = 0;
+      s_rc = 0;
+    }
+    __syncthreads();
+    const int64_t b = r / BM;
+    const int len = tlen[b];
+    const int32_t *tl = tlist + b * tstride;
+    for (int t0 = 0; t0 < len; t0 += FIN_WARPS) {
+      const int ti = t0 + warp;
+      const uint32_t tb = s_t;
+      if (ti < len) {
+        const int64_t tile = tl[ti];
+#pragma unroll 1
+        for (int i = 0; i < 4; ++i) {
+          const int64_t col = tile * BN + i * 32 + lane;
+          const int32_t id = perm[col];
+          const uint4 *xr = reinterpret_cast<const uint4 *>(xs + col * KB);
+          uint32_t dot = 0;
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const uint4 w = xr[v];
+            dot = __dp4a(w.x, q[4 * v], dot);
+            dot = __dp4a(w.y, q[4 * v + 1], dot);
+            dot = __dp4a(w.z, q[4 * v + 2], dot);
+            dot = __dp4a(w.w, q[4 * v + 3], dot);
+          }
+          const uint32_t dist = (uint32_t)(ns[col] + nq - 2 * (int)dot);
+          const bool keep = id >= 0 && id != (int32_t)orow && dist < tb;
+          const unsigned bal = __ballot_sync(0xffffffffu, keep);
+          int base = 0;
+          if (lane == 0 && bal) base = atomicAdd(&s_rc, __popc(bal));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (keep) s_round[base + __popc(bal & lanemask_lt())] = ((uint64_t)dist << 32) | (uint32_t)id;
+        }
+      }
+      __syncthreads();
+      if (warp == 0) {  // move the round into the row's buffer, compacting when full
+        int cnt = s_cnt;
+        uint32_t t = s_t;
+        const int rc = s_rc;
+        for (int i0 = 0; i0 < rc; i0 += 32) {
+          if (cnt + 32 > CAP) {
+            const uint64_t nt = select_k(buf, cnt, K, t, lane);
+            cnt = K;
+            t = min(t, khi(nt) + 1u);
+          }
+          const uint64_t key = i0 + lane < rc ? s_round[i0 + lane] : KEY_MAX;
+          const bool keep = key != KEY_MAX && khi(key) < t;
+          const unsigned bal = __ballot_sync(0xffffffffu, keep);
+          if (keep) buf[cnt + __popc(bal & lanemask_lt())] = key;
+          cnt += __popc(bal);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          s_cnt = cnt;
+          s_t = t;
+          s_rc = 0;
+        }
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {
+      const int cnt = s_cnt;
+      if (K <= 32) finalize_row<1>(buf, cnt, K, false, orow, out_keys, fo, s_hist, s_stage, lane);
+      else if (K <= 64) finalize_row<2>(buf, cnt, K, false, orow, out_keys, fo, s_hist, s_stage, lane);
+      else if (K <= 128) finalize_row<4>(buf, cnt, K, false, orow, out_keys, fo, s_hist, s_stage, lane);
+      else finalize_row<8>(buf, cnt, K, false, orow, out_keys, fo, s_hist, s_stage, lane);
+    }
+    __syncthreads();
+  }
+}
+
 // float (integer-valued, d <= 128) -> u8 rows padded to 128 bytes
 __global__ void to_u8_kernel(const float *__restrict__ X, int64_t n, int d,
                              uint8_t *__restrict__ out) {
@@ -1368,6 +1490,31 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
       tlist ? tlen : nullptr, fo);
   PGK_CHECK_LAUNCH("tc_finalize_kernel");
   *handled = true;
+  return PGK_OK;
+}
+
+// The failing rows of the last guessed pass 2 (see rerun_rows_kernel), on
+// the same tc workspace (its per-row buffers), xs / ns / perm the tile-sorted
+// rows, norms and permutation, tlist / tlen / tstride their full-radius lists.
+int launch_rerun_rows(int64_t np, void *tc_ws, size_t tc_bytes, const uint8_t *xs,
+                      const int32_t *ns, const int32_t *perm, const uint8_t *fail_rows,
+                      const int32_t *tlist, const int32_t *tlen, int64_t tstride,
+                      const uint64_t *seeds, int K, uint64_t *keys, const PoolOut *out,
+                      int32_t *scratch, cudaStream_t stream) {
+  Carve c(tc_ws, tc_bytes);
+  c.take<uint8_t>((size_t)np * tc::KB);  // the tc launcher's u8 copy (unused with xs)
+  const int64_t rows = (np + tc::BM - 1) / tc::BM * tc::BM;
+  uint64_t *bufs = c.take<uint64_t>((size_t)rows * tc::CAP);
+  int32_t *count = scratch, *list = scratch + 32;
+  const int sms = num_sms();
+  PGK_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), stream));
+  tc::fail_list_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(fail_rows, np, list, count);
+  PGK_CHECK_LAUNCH("fail_list_kernel");
+  tc::FinOut fo{nullptr, nullptr, nullptr};
+  if (out) fo = tc::FinOut{out->gt_ids, out->ids, out->dists};
+  tc::rerun_rows_kernel<<<(unsigned)sms * 8, tc::RR_THREADS, 0, stream>>>(
+      xs, ns, perm, list, count, tlist, tlen, tstride, seeds, K, bufs, keys, fo);
+  PGK_CHECK_LAUNCH("rerun_rows_kernel");
   return PGK_OK;
 }
 

@@ -686,7 +686,7 @@ static float seed_shrink() {
 struct Layout {
   float *cen, *cent, *cn, *gcell, *gcn, *dcc;
   double *Rc, *rho;
-  int32_t *tcell;
+  int32_t *tcell, *rr;
   int32_t *cnorm, *hist, *cursor, *assign, *perm, *ns, *size, *lists, *lens, *fail, *lens2;
   uint8_t *fail_rows;
   int64_t *off, *scan_tmp;
@@ -748,6 +748,7 @@ static tiles::Layout tiles_layout(void *ws, size_t bytes, int64_t n, int64_t d) 
   L.rho = c.take<double>(T);
   L.tcell = c.take<int32_t>(T);
   L.dcc = c.take<float>((size_t)C * C);
+  L.rr = c.take<int32_t>(NP + 32);
   L.U = c.take<double>(T);
   L.total = c.take<unsigned long long>(4);
   L.sub_bytes = tc_pool_workspace(C, n, false);
@@ -808,6 +809,12 @@ int tiles_u8_assign(void *tws, size_t tws_bytes, int64_t n, int d, int K, const 
   PGK_REQUIRE(h, "tensor-core assignment unavailable");
   return PGK_OK;
 }
+
+int launch_rerun_rows(int64_t np, void *tc_ws, size_t tc_bytes, const uint8_t *xs,
+                      const int32_t *ns, const int32_t *perm, const uint8_t *fail_rows,
+                      const int32_t *tlist, const int32_t *tlen, int64_t tstride,
+                      const uint64_t *seeds, int K, uint64_t *keys, const PoolOut *out,
+                      int32_t *scratch, cudaStream_t stream);
 
 // Runs the whole pruned pool.  *handled = false when pruning does not apply.
 extern uint32_t *g_dense_ostat;
@@ -960,9 +967,10 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
       fprintf(stderr, "[tiles] guess %.3f: %lld of %lld blocks re-run\n", shrink, (long long)nf,
               (long long)T);
     }
-    rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes,
-                                 stream, L.xs, L.lists, L.lens2, T, L.perm, handled, keys, 0,
-                                 1.0f, nullptr, out, nullptr, L.fail_rows);
+    // the failing rows alone, exact SIMT rescans over their full-radius
+    // lists (their whole blocks on the tensor cores cost ~4x more)
+    rc = launch_rerun_rows(NP, tc_ws, tc_bytes, L.xs, L.ns, L.perm, L.fail_rows, L.lists,
+                           L.lens2, T, keys, K, keys, out, L.rr, stream);
     if (rc) return rc;
   }
   if (stats && out) {  // final K-th distance (pool output) over the pass-2 seed
