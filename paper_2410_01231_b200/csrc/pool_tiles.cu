@@ -283,7 +283,10 @@ __global__ void cent_norms_kernel(const float *__restrict__ cent, int64_t T, int
 // pass-1 list: the nearest tiles of every query tile by centroid distance,
 // as many as needed to hold >= P1_MULT * K points (at most NEAR tiles)
 constexpr int NEAR = 16;
-constexpr int P1_MULT = 4;
+#ifndef TILES_P1_MULT
+#define TILES_P1_MULT 4
+#endif
+constexpr int P1_MULT = TILES_P1_MULT;
 __global__ void tile_nearest_kernel(const float *__restrict__ dc, const int32_t *__restrict__ size,
                                     int64_t T, int K, int32_t *__restrict__ lists,
                                     int32_t *__restrict__ lens,

@@ -264,8 +264,66 @@ __device__ __forceinline__ int reg_sort_dedupe(const uint64_t *__restrict__ keys
   return m;
 }
 
+// A slice of own <= 32 entries (the phase-A row, already ascending) and
+// rev <= 32 reverse entries (arrival order): sort only the reverse part (one
+// key per lane), then one bitonic merge with the own part -- 26 shuffle
+// stages against 40 for sorting all 64 -- and the same duplicate drop.
+__device__ __forceinline__ int merge_own_rev(const uint64_t *__restrict__ keys, int own, int rev,
+                                             int32_t *__restrict__ out_ids,
+                                             float *__restrict__ out_d, int lane) {
+  uint64_t e0 = lane < own ? keys[lane] : KEY_MAX;
+  uint64_t r = lane < rev ? keys[own + lane] : KEY_MAX;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t o = __shfl_xor_sync(0xffffffffu, r, j);
+      const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      const uint64_t mn = r < o ? r : o, mx = r < o ? o : r;
+      r = (lower == up) ? mn : mx;
+    }
+  }
+  // own ascending ++ reverse descending is bitonic (64 keys, slot*32 + lane)
+  uint64_t e1 = __shfl_sync(0xffffffffu, r, 31 - lane);
+  {
+    const uint64_t mn = e0 < e1 ? e0 : e1, mx = e0 < e1 ? e1 : e0;
+    e0 = mn;
+    e1 = mx;
+  }
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    const bool lower = (lane & j) == 0;
+    const uint64_t o0 = __shfl_xor_sync(0xffffffffu, e0, j);
+    const uint64_t o1 = __shfl_xor_sync(0xffffffffu, e1, j);
+    e0 = lower ? (e0 < o0 ? e0 : o0) : (e0 < o0 ? o0 : e0);
+    e1 = lower ? (e1 < o1 ? e1 : o1) : (e1 < o1 ? o1 : e1);
+  }
+  const int len = own + rev;
+  int m = 0;
+  uint64_t last = 0;
+#pragma unroll
+  for (int s0 = 0; s0 < 2; ++s0) {
+    const uint64_t v = s0 == 0 ? e0 : e1;
+    if (s0 * 32 >= len) break;
+    uint64_t prev = __shfl_up_sync(0xffffffffu, v, 1);
+    if (lane == 0) prev = last;
+    last = __shfl_sync(0xffffffffu, v, 31);
+    const int i = s0 * 32 + lane;
+    const bool keep = i < len && (i == 0 || key_id(prev) != key_id(v));
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int p = m + __popc(bal & lanemask_lt());
+      out_ids[p] = key_id(v);
+      out_d[p] = key_dist(v);
+    }
+    m += __popc(bal);
+  }
+  return m;
+}
+
 __global__ void __launch_bounds__(SORT_WARPS * 32)
     merge_sort_kernel(const int64_t *__restrict__ mrg_off, int64_t n,
+                      const int32_t *__restrict__ own_counts,
                       const uint64_t *__restrict__ keys,
                       int32_t *__restrict__ mrg_ids, float *__restrict__ mrg_d,
                       int32_t *__restrict__ mrg_counts,
@@ -281,7 +339,10 @@ __global__ void __launch_bounds__(SORT_WARPS * 32)
       continue;
     }
     int m;
-    if (len <= 32) m = reg_sort_dedupe<1>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
+    const int own = own_counts[u];
+    if (len > 32 && own <= 32 && len - own <= 32)
+      m = merge_own_rev(keys + lo, own, len - own, mrg_ids + lo, mrg_d + lo, lane);
+    else if (len <= 32) m = reg_sort_dedupe<1>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
     else if (len <= 64) m = reg_sort_dedupe<2>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
     else if (len <= 128) m = reg_sort_dedupe<4>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
     else if (len <= 256) m = reg_sort_dedupe<8>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
@@ -411,7 +472,7 @@ int add_reverse_and_prune(const float *X, const uint8_t *xu8, const int32_t *nor
   const unsigned sblocks =
       (unsigned)std::min<int64_t>((n + SORT_WARPS - 1) / SORT_WARPS, (int64_t)sms * 8);
   merge_sort_kernel<<<sblocks, SORT_WARPS * 32, 0, stream>>>(
-      L.mrg_off, n, L.keys, L.mrg_ids, L.mrg_d, L.mrg_counts, L.long_list, L.long_count);
+      L.mrg_off, n, a_counts, L.keys, L.mrg_ids, L.mrg_d, L.mrg_counts, L.long_list, L.long_count);
   PGK_CHECK_LAUNCH("merge_sort_kernel");
   long_sort_kernel<<<(unsigned)sms, 512, 0, stream>>>(L.mrg_off, L.keys, L.scratch,
                                                       L.long_list, L.long_count,
