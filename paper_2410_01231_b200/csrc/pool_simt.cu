@@ -864,7 +864,8 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             const uint64_t *init_keys = nullptr, int kth_only = 0,
                             float shrink = 1.0f, int32_t *fail_blocks = nullptr,
                             const PoolOut *out = nullptr, uint8_t *fail_rows = nullptr,
-                            const uint8_t *row_mask = nullptr, const uint8_t *qu8_in = nullptr);
+                            const uint8_t *row_mask = nullptr, const uint8_t *qu8_in = nullptr,
+                            const int32_t *gate = nullptr, int gate_min = 0);
 int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm, int K,
                          uint64_t *keys, void *tc_ws, size_t tc_bytes, void *tws,
                          size_t tws_bytes, cudaStream_t stream, bool *handled,

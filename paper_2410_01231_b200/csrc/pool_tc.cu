@@ -270,7 +270,11 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
                       const uint64_t *__restrict__ init_keys, float shrink,
                       int32_t *__restrict__ row_cnt, uint64_t *__restrict__ row_tau,
                       int32_t *__restrict__ sched, const uint8_t *__restrict__ row_mask,
-                      int k1_direct) {
+                      int k1_direct, const int32_t *__restrict__ gate, int gate_min) {
+  // a device-side switch: run only when *gate >= gate_min (the re-run of
+  // failing rows on the tensor cores, taken when they are too many for the
+  // SIMT rescan)
+  if (gate && *gate < gate_min) return;
   // K == 1 paths: compiled in for the K1 instantiation (and the STATS one)
   const bool isk1 = K1 ? true : (STATS ? K == 1 : false);
   unsigned long long st[ST_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1045,7 +1049,9 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, FIN_MINB)
                        const int32_t *__restrict__ perm, int kth_only,
                        uint64_t *__restrict__ out_keys, int32_t *__restrict__ fail_blocks,
                        uint8_t *__restrict__ fail_rows, const int32_t *__restrict__ tlen,
-                       FinOut fo) {
+                       FinOut fo, const int32_t *__restrict__ gate = nullptr,
+                       int gate_min = 0) {
+  if (gate && *gate < gate_min) return;
   __shared__ uint32_t s_hist[FIN_WARPS][256];
   __shared__ uint64_t s_stage[FIN_WARPS][FIN_STAGE];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1190,10 +1196,11 @@ __global__ void __launch_bounds__(RR_THREADS, 2)
                       const int32_t *__restrict__ count, const int32_t *__restrict__ tlist,
                       const int32_t *__restrict__ tlen, int64_t tstride,
                       const uint64_t *__restrict__ seeds, int K, uint64_t *__restrict__ bufs,
-                      uint64_t *__restrict__ out_keys, FinOut fo) {
+                      uint64_t *__restrict__ out_keys, FinOut fo, int max_rows) {
   __shared__ uint32_t s_hist[256];
   __shared__ uint64_t s_stage[FIN_STAGE];
-  __shared__ uint64_t s_round[RR_ROUND];  // this round's survivors
+  __shared__ uint64_t s_round[RR_ROUND];
+  if (*count > max_rows) return;  // too many: the tensor-core block re-run takes them  // this round's survivors
   __shared__ int s_rc, s_cnt;
   __shared__ uint32_t s_t;  // exclusive distance bound
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1378,7 +1385,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             const int32_t *perm, bool *handled, const uint64_t *init_keys,
                             int kth_only, float shrink, int32_t *fail_blocks,
                             const PoolOut *out, uint8_t *fail_rows, const uint8_t *row_mask,
-                            const uint8_t *qu8_in) {
+                            const uint8_t *qu8_in, const int32_t *gate, int gate_min) {
   *handled = false;
   if (shrink < 1.0f && (!fail_blocks || !fail_rows)) {
     set_error("guessed thresholds need a fail-block array");
@@ -1438,7 +1445,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   if (dense) {
     tc::tc_pool_u8_kernel<false, true><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
-        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, 0);
+        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, 0, gate, gate_min);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel<dense>");
     const unsigned fgrid =
         (unsigned)std::min<int64_t>((nq + tc::FIN_WARPS - 1) / tc::FIN_WARPS, (int64_t)sms * 8);
@@ -1454,7 +1461,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
     PGK_CUDA(cudaMemsetAsync(dstats, 0, sizeof(unsigned long long) * tc::ST_COUNT, stream));
     tc::tc_pool_u8_kernel<true, false><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, dstats, tlist, tlen,
-        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, 0);
+        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, 0, gate, gate_min);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel<stats>");
     unsigned long long h[tc::ST_COUNT];
     PGK_CUDA(cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, stream));
@@ -1470,11 +1477,13 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
     if (K == 1)
       tc::tc_pool_u8_kernel<false, false, true><<<grid, tc::THREADS, smem, stream>>>(
           tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
-          tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, k1_direct);
+          tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, k1_direct, gate,
+          gate_min);
     else
       tc::tc_pool_u8_kernel<false, false><<<grid, tc::THREADS, smem, stream>>>(
           tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
-          tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, k1_direct);
+          tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, k1_direct, gate,
+          gate_min);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel");
     if (k1_direct) {
       *handled = true;
@@ -1487,7 +1496,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
       (unsigned)std::min<int64_t>((nq + tc::FIN_WARPS - 1) / tc::FIN_WARPS, (int64_t)sms * 8);
   tc::tc_finalize_kernel<<<fgrid, tc::FIN_WARPS * 32, 0, stream>>>(
       bufs, row_cnt, row_tau, nq, K, perm, kth_only, keys, fail_blocks, fail_rows,
-      tlist ? tlen : nullptr, fo);
+      tlist ? tlen : nullptr, fo, gate, gate_min);
   PGK_CHECK_LAUNCH("tc_finalize_kernel");
   *handled = true;
   return PGK_OK;
@@ -1500,7 +1509,7 @@ int launch_rerun_rows(int64_t np, void *tc_ws, size_t tc_bytes, const uint8_t *x
                       const int32_t *ns, const int32_t *perm, const uint8_t *fail_rows,
                       const int32_t *tlist, const int32_t *tlen, int64_t tstride,
                       const uint64_t *seeds, int K, uint64_t *keys, const PoolOut *out,
-                      int32_t *scratch, cudaStream_t stream) {
+                      int32_t *scratch, int max_rows, cudaStream_t stream) {
   Carve c(tc_ws, tc_bytes);
   c.take<uint8_t>((size_t)np * tc::KB);  // the tc launcher's u8 copy (unused with xs)
   const int64_t rows = (np + tc::BM - 1) / tc::BM * tc::BM;
@@ -1513,7 +1522,7 @@ int launch_rerun_rows(int64_t np, void *tc_ws, size_t tc_bytes, const uint8_t *x
   tc::FinOut fo{nullptr, nullptr, nullptr};
   if (out) fo = tc::FinOut{out->gt_ids, out->ids, out->dists};
   tc::rerun_rows_kernel<<<(unsigned)sms * 8, tc::RR_THREADS, 0, stream>>>(
-      xs, ns, perm, list, count, tlist, tlen, tstride, seeds, K, bufs, keys, fo);
+      xs, ns, perm, list, count, tlist, tlen, tstride, seeds, K, bufs, keys, fo, max_rows);
   PGK_CHECK_LAUNCH("rerun_rows_kernel");
   return PGK_OK;
 }

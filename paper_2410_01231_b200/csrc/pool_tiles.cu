@@ -715,7 +715,8 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
                             const uint64_t *init_keys = nullptr, int kth_only = 0,
                             float shrink = 1.0f, int32_t *fail_blocks = nullptr,
                             const PoolOut *out = nullptr, uint8_t *fail_rows = nullptr,
-                            const uint8_t *row_mask = nullptr, const uint8_t *qu8_in = nullptr);
+                            const uint8_t *row_mask = nullptr, const uint8_t *qu8_in = nullptr,
+                            const int32_t *gate = nullptr, int gate_min = 0);
 
 static tiles::Layout tiles_layout(void *ws, size_t bytes, int64_t n, int64_t d) {
   using namespace tiles;
@@ -817,7 +818,7 @@ int launch_rerun_rows(int64_t np, void *tc_ws, size_t tc_bytes, const uint8_t *x
                       const int32_t *ns, const int32_t *perm, const uint8_t *fail_rows,
                       const int32_t *tlist, const int32_t *tlen, int64_t tstride,
                       const uint64_t *seeds, int K, uint64_t *keys, const PoolOut *out,
-                      int32_t *scratch, cudaStream_t stream);
+                      int32_t *scratch, int max_rows, cudaStream_t stream);
 
 // Runs the whole pruned pool.  *handled = false when pruning does not apply.
 extern uint32_t *g_dense_ostat;
@@ -972,8 +973,17 @@ int launch_pool_tiles_u8(const float *X, int64_t n, int d, const int32_t *xnorm,
     }
     // the failing rows alone, exact SIMT rescans over their full-radius
     // lists (their whole blocks on the tensor cores cost ~4x more)
+    // (when they are more than 1/32 of the rows -- a dataset the 0.93 guess
+    // does not fit -- their blocks re-run on the tensor cores instead: both
+    // launches read the failing-row count on the device and one exits)
+    const int max_rows = (int)std::max<int64_t>(1024, n / 32);
     rc = launch_rerun_rows(NP, tc_ws, tc_bytes, L.xs, L.ns, L.perm, L.fail_rows, L.lists,
-                           L.lens2, T, keys, K, keys, out, L.rr, stream);
+                           L.lens2, T, keys, K, keys, out, L.rr, max_rows, stream);
+    if (rc) return rc;
+    rc = launch_pool_tc_u8_lists(X, NP, d, X, NP, 1, L.ns, L.ns, K, keys, tc_ws, tc_bytes,
+                                 stream, L.xs, L.lists, L.lens2, T, L.perm, handled, keys, 0,
+                                 1.0f, nullptr, out, nullptr, L.fail_rows, nullptr, L.rr,
+                                 max_rows + 1);
     if (rc) return rc;
   }
   if (stats && out) {  // final K-th distance (pool output) over the pass-2 seed

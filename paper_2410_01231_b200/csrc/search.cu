@@ -312,24 +312,24 @@ __global__ void first_unseen_kernel(const uint32_t *__restrict__ seen, int64_t n
 }
 
 // ---- centroid: deterministic float64 column means ---------------------
-constexpr int CROWS = 2048;  // rows per partial
-__global__ void centroid_partial_kernel(const float *__restrict__ X, int64_t n, int d,
-                                        double *__restrict__ part) {
-  const int64_t chunk = blockIdx.y;
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= d) return;
-  const int64_t r0 = chunk * CROWS, r1 = min(n, r0 + CROWS);
-  double s = 0.0;
-  for (int64_t r = r0; r < r1; ++r) s += (double)X[r * d + col];
-  part[chunk * d + col] = s;
-}
-
-__global__ void centroid_final_kernel(const double *__restrict__ part, int64_t nchunks, int64_t n,
-                                      int d, float *__restrict__ out) {
+// numpy's mean(axis=0, dtype=float64) on a C-contiguous (n, d) array adds the
+// rows to the float64 accumulator in order (core.py:153-155): one thread per
+// column does exactly that, rows loaded 8 ahead (the adds are a dependent
+// chain; the loads are not).
+__global__ void centroid_seq_kernel(const float *__restrict__ X, int64_t n, int d,
+                                    float *__restrict__ out) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= d) return;
   double s = 0.0;
-  for (int64_t c = 0; c < nchunks; ++c) s += part[c * d + col];
+  int64_t r = 0;
+  for (; r + 8 <= n; r += 8) {
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = X[(r + i) * d + col];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += (double)v[i];
+  }
+  for (; r < n; ++r) s += (double)X[r * d + col];
   out[col] = (float)(s / (double)n);
 }
 
@@ -435,21 +435,18 @@ int pair_dists(const float *X, int64_t d, const int32_t *a, const int32_t *b, in
 }
 
 size_t centroid_workspace(int64_t n, int64_t d) {
-  return (size_t)((n + srch::CROWS - 1) / srch::CROWS) * d * sizeof(double) + 256;
+  (void)n;
+  (void)d;
+  return 256;  // (kept in the ABI: the sequential kernel needs none)
 }
 
 int centroid(const float *X, int64_t n, int64_t d, float *out, void *ws, size_t ws_bytes,
              cudaStream_t stream) {
   PGK_REQUIRE(n >= 1 && d >= 1, "empty dataset");
   PGK_REQUIRE(ws_bytes >= centroid_workspace(n, d), "centroid workspace too small");
-  const int64_t nch = (n + srch::CROWS - 1) / srch::CROWS;
-  double *part = reinterpret_cast<double *>(ws);
-  dim3 g1((unsigned)((d + 127) / 128), (unsigned)nch);
-  srch::centroid_partial_kernel<<<g1, 128, 0, stream>>>(X, n, (int)d, part);
-  PGK_CHECK_LAUNCH("centroid_partial_kernel");
-  srch::centroid_final_kernel<<<(unsigned)((d + 127) / 128), 128, 0, stream>>>(part, nch, n,
-                                                                               (int)d, out);
-  PGK_CHECK_LAUNCH("centroid_final_kernel");
+  (void)ws;
+  srch::centroid_seq_kernel<<<(unsigned)((d + 63) / 64), 64, 0, stream>>>(X, n, (int)d, out);
+  PGK_CHECK_LAUNCH("centroid_seq_kernel");
   return PGK_OK;
 }
 

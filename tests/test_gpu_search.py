@@ -105,3 +105,17 @@ def test_phase_c_and_search_at_scale_against_oracle():
         np.testing.assert_array_equal(s_ids, o_ids)
         np.testing.assert_array_equal(s_d, o_d)
         np.testing.assert_array_equal(s_dc, o_dc)
+
+
+@pytest.mark.parametrize("n,d", [(100_000, 33), (20_000, 960)])
+def test_centroid_equals_numpy_mean_bit_for_bit(n, d):
+    """core.centroid (core.py:153-155): numpy's float64 mean over axis 0 (rows
+    added in order), cast to fp32 -- on heavy-tailed float data, where a
+    different summation order would change the last ulp."""
+    import torch
+    from paper_2410_01231_b200 import kernels
+    rng = np.random.default_rng(5)
+    x = (rng.standard_normal((n, d)) * rng.uniform(0.1, 1000, (n, 1))).astype(np.float32)
+    got = kernels.centroid(torch.from_numpy(x).cuda()).cpu().numpy()
+    want = x.mean(axis=0, dtype=np.float64).astype(np.float32)
+    np.testing.assert_array_equal(got, want)
