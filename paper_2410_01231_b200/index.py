@@ -89,7 +89,8 @@ class RngBuilder:
         u8 = self.u8_rows(X)  # exact-integer rows once, for the pool and the selection
         return self._finish(X, u8, host_out)
 
-    def build_host(self, host: torch.Tensor, host_out=None, chunks: int = 8) -> BuildOutput:
+    def build_host(self, host: torch.Tensor, host_out=None, chunks: int = 8,
+                   registered: bool = False) -> BuildOutput:
         """The whole path from a pinned host array (n, d) float32: the rows are
         copied in `chunks` pieces on a side stream while the current stream
         converts each landed chunk to exact-integer rows and assigns it to its
@@ -97,7 +98,9 @@ class RngBuilder:
         whole copy.  The exact-integer check runs on the device per chunk; if
         the data turn out not to qualify, the result is recomputed through the
         float path (one 4-byte read at the end: this call returns with the
-        build complete).  Non-U8 builders, and shapes the tile-pruned pool
+        build complete).  registered: `host` is page-locked by the caller
+        (pgk_host_register) rather than torch-pinned.  Non-U8 builders, and
+        shapes the tile-pruned pool
         does not take (pgk_tiles_supported: K > 256, too many tiles,
         PGK_DISABLE_PRUNE=1), copy, then build."""
         if self.mode != _lib.POOL_U8 or self.d > 128 or \
@@ -105,7 +108,7 @@ class RngBuilder:
             out = self.build(host.to(_lib.device(), non_blocking=True), host_out)
             torch.cuda.current_stream().synchronize()
             return out
-        return _build_host(self, host, host_out, chunks)
+        return _build_host(self, host, host_out, chunks, registered)
 
     def _finish(self, X, u8, host_out, assigned: bool = False) -> BuildOutput:
         p = self.params
@@ -153,8 +156,10 @@ class HostPipeline:
         self.f32 = None  # float-path builder, made if a dataset is not exact-integer
 
 
-def _build_host(b: "RngBuilder", host: torch.Tensor, host_out, chunks: int):
-    if host.device.type != "cpu" or not host.is_pinned() or host.dtype != torch.float32 \
+def _build_host(b: "RngBuilder", host: torch.Tensor, host_out, chunks: int,
+                registered: bool = False):
+    if host.device.type != "cpu" or not (registered or host.is_pinned()) \
+            or host.dtype != torch.float32 \
             or tuple(host.shape) != (b.n, b.d) or not host.is_contiguous():
         raise ValueError(f"host data must be a pinned contiguous float32 ({b.n}, {b.d}) tensor")
     _check_host_out(host_out, b.n, b.params.M)
@@ -208,13 +213,40 @@ def pool_mode(X: torch.Tensor) -> int:
     return _lib.POOL_U8 if kernels.detect_u8(X) else _lib.POOL_F32
 
 
+_CACHE: dict = {}  # the last shape's builder and its pinned output buffers
+
+
 def build_rng_index(data, K: int, R: int, strategy: str = "rng", alpha: float = 60.0,
                     ep: int = 0) -> ProximityGraph:
     """Host-buffer entry point: numpy (n, d) float32 in, ProximityGraph out
-    (phases A+B, connect=False, as prune.refine(..., connect=False, ep=ep))."""
+    (phases A+B, connect=False, as prune.refine(..., connect=False, ep=ep)).
+
+    The caller's array is page-locked in place for the call
+    (pgk_host_register) and fed to the chunked host pipeline
+    (RngBuilder.build_host: copy overlapped with the per-row work); the
+    builder and its pinned output buffers are kept for the next call of the
+    same shape."""
     data = np.ascontiguousarray(data, dtype=np.float32)
-    X = torch.from_numpy(data).to(_lib.device())
+    if data.ndim != 2 or data.shape[0] < 1 or data.shape[1] < 1:
+        raise ValueError("data must be a non-empty (n, d) array")
+    n, d = data.shape
     params = PruneParams(M=R, alpha=alpha, strategy=strategy)
-    b = RngBuilder(data.shape[0], data.shape[1], K, params, pool_mode(X)).build(X)
-    return ProximityGraph(adj=b.ids.cpu().numpy(), counts=b.counts.cpu().numpy(), M=R,
-                          ep=ep)
+    key = (n, d, K, params.M, params.strategy_code, params.kernel_param)
+    ent = _CACHE.get(key)
+    if ent is None:
+        _CACHE.clear()
+        mode = _lib.POOL_U8 if d <= 128 else _lib.POOL_F32  # build_host re-checks on device
+        b = RngBuilder(n, d, K, params, mode)
+        ent = (b, torch.empty((n, R), dtype=torch.int32).pin_memory(),
+               torch.empty(n, dtype=torch.int32).pin_memory())
+        _CACHE[key] = ent
+    b, h_ids, h_cnt = ent
+    host = torch.from_numpy(data)
+    L = _lib.lib()
+    _lib.check(L.pgk_host_register(_lib.ptr(host), data.nbytes))
+    try:
+        b.build_host(host, host_out=(h_ids, h_cnt), registered=True)
+        torch.cuda.current_stream().synchronize()
+    finally:
+        _lib.check(L.pgk_host_unregister(_lib.ptr(host)))
+    return ProximityGraph(adj=h_ids.numpy().copy(), counts=h_cnt.numpy().copy(), M=R, ep=ep)

@@ -491,6 +491,23 @@ def test_build_host_pipeline_equals_device_build(n, chunks, integer):
         assert torch.equal(h_ids, ids) and torch.equal(h_cnt, cnt)
 
 
+@pytest.mark.parametrize("n,d,integer", [(20000, 128, True), (20000, 128, False), (3000, 32, False)])
+def test_numpy_api_build_rng_index(n, d, integer):
+    """index.build_rng_index (numpy in, ProximityGraph out; the caller's array
+    page-locked in place for the chunked pipeline, builder cached per shape)
+    equals the oracle's phases A+B on the oracle's pools, twice in a row."""
+    from paper_2410_01231_b200.index import build_rng_index
+    data = synth.cfg2(n) if d == 128 else synth.cfg1(n)
+    if not integer and d == 128:
+        data = data + np.float32(0.25)
+    o_ids, o_d = oracle.knn_pools(data, 64)
+    _, ob = oracle.refine_ab(data, o_ids, o_d, 24, "rng", 60.0)
+    for _ in range(2):
+        g = build_rng_index(data, 64, 24)
+        np.testing.assert_array_equal(g.counts, ob[2])
+        np.testing.assert_array_equal(g.adj, ob[0])
+
+
 @pytest.mark.parametrize("strategy,alpha", [("rng", 60.0), ("alpha", 66.0)])
 def test_reverse_pass_union_sizes_through_pair_single_and_hub_paths(strategy, alpha):
     """Phase B on exact-integer rows whose unions span 0..~400 candidates: the
