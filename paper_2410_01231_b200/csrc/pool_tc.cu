@@ -1040,6 +1040,9 @@ __device__ __forceinline__ void finalize_row(const uint64_t *buf, int cnt, int K
   __syncwarp();
 }
 
+#ifndef FIN_PREFETCH
+#define FIN_PREFETCH 1
+#endif
 #ifndef FIN_MINB
 #define FIN_MINB 2  // 128 registers, no spills: 2.96 -> 2.83 ms at config 2
 #endif
@@ -1055,8 +1058,20 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, FIN_MINB)
   __shared__ uint32_t s_hist[FIN_WARPS][256];
   __shared__ uint64_t s_stage[FIN_WARPS][FIN_STAGE];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t r = (int64_t)blockIdx.x * FIN_WARPS + warp; r < nrows;
-       r += (int64_t)gridDim.x * FIN_WARPS) {
+  const int64_t step = (int64_t)gridDim.x * FIN_WARPS;
+  for (int64_t r = (int64_t)blockIdx.x * FIN_WARPS + warp; r < nrows; r += step) {
+#if FIN_PREFETCH
+    // pull the next row's keys (and its metadata) into L2 while this row is
+    // worked on: the buffers (~2 KB per row, 2 GB in all) stream from DRAM
+    if (r + step < nrows) {
+      if (lane < 16)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(bufs + (r + step) * CAP + lane * 16));
+      else if (lane == 16)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(row_cnt + r + step));
+      else if (lane == 17 && perm)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(perm + r + step));
+    }
+#endif
     if (tlen && tlen[r / BM] == 0) continue;  // block not scheduled in this launch
     const int raw = row_cnt[r];
     if (raw < 0) continue;  // padding row
