@@ -190,11 +190,6 @@ int pgk_tiles_u8_assign(void *ws, size_t ws_bytes, int64_t n, int64_t d, int64_t
 int pgk_detect_u8_async(const float *data, int64_t n, int64_t d, int *flag, void *stream);
 int pgk_copy_rows_h2d(void *dst, const void *src_host, int64_t rows, int64_t row_bytes,
                       int64_t src_pitch, void *stream);
-/* Page-lock a caller's host buffer in place (cudaHostRegister) for the
- * duration of one host-data build, so a plain numpy array feeds the chunked
- * pipeline without a staging copy; pgk_host_unregister releases it. */
-int pgk_host_register(void *ptr, size_t bytes);
-int pgk_host_unregister(void *ptr);
 
 /* Number of query rows that needed the exact float64 fallback scan in the most
  * recent pgk_knn_pools call on this workspace (device int32 inside ws; this

@@ -62,8 +62,6 @@ def lib():
         L.pgk_tiles_u8_assign.argtypes = [P, SZ, I64, I64, I64, P, P, I64, I64, P]
         L.pgk_detect_u8_async.argtypes = [P, I64, I64, P, P]
         L.pgk_copy_rows_h2d.argtypes = [P, P, I64, I64, I64, P]
-        L.pgk_host_register.argtypes = [P, SZ]
-        L.pgk_host_unregister.argtypes = [P]
         L.pgk_knn_fallback_rows.argtypes = [P, P, P]
         L.pgk_knn_work.argtypes = [P, I64, I64, I64, I64, I, P, P]
         I32 = ctypes.c_int32
@@ -91,7 +89,7 @@ def lib():
                   "pgk_add_reverse_and_prune", "pgk_detect_u8", "pgk_knn_workspace",
                   "pgk_knn_pools", "pgk_knn_pools_u8", "pgk_knn_fallback_rows", "pgk_knn_work",
                   "pgk_knn_order", "pgk_search_workspace", "pgk_tiles_u8_prepare",
-                  "pgk_tiles_u8_assign", "pgk_detect_u8_async", "pgk_copy_rows_h2d", "pgk_host_register", "pgk_host_unregister", "pgk_beam_search", "pgk_reach_workspace",
+                  "pgk_tiles_u8_assign", "pgk_detect_u8_async", "pgk_copy_rows_h2d", "pgk_beam_search", "pgk_reach_workspace",
                   "pgk_beam_search_ex", "pgk_component_heads", "pgk_pair_dists",
                   "pgk_mark_reachable", "pgk_first_unseen", "pgk_centroid_workspace",
                   "pgk_centroid", "pgk_knng_init", "pgk_knng_sort_rows",
@@ -106,7 +104,7 @@ EXPORTS = ("pgk_version", "pgk_last_error", "pgk_device_check", "pgk_prune_batch
            "pgk_reverse_workspace", "pgk_add_reverse_and_prune", "pgk_detect_u8",
            "pgk_knn_workspace", "pgk_knn_pools", "pgk_knn_pools_u8", "pgk_knn_fallback_rows",
            "pgk_tiles_center_stride", "pgk_tiles_supported", "pgk_tiles_u8_prepare", "pgk_tiles_u8_assign",
-           "pgk_detect_u8_async", "pgk_copy_rows_h2d", "pgk_host_register", "pgk_host_unregister",
+           "pgk_detect_u8_async", "pgk_copy_rows_h2d",
            "pgk_knn_work",
            "pgk_knn_order", "pgk_search_workspace", "pgk_beam_search", "pgk_reach_workspace",
            "pgk_mark_reachable", "pgk_first_unseen", "pgk_centroid_workspace", "pgk_centroid",

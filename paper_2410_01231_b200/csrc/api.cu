@@ -298,18 +298,6 @@ int pgk_copy_rows_h2d(void *dst, const void *src_host, int64_t rows, int64_t row
   return PGK_OK;
 }
 
-int pgk_host_register(void *ptr, size_t bytes) {
-  PGK_REQUIRE(ptr && bytes > 0, "bad host buffer");
-  PGK_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
-  return PGK_OK;
-}
-
-int pgk_host_unregister(void *ptr) {
-  PGK_REQUIRE(ptr, "NULL host buffer");
-  PGK_CUDA(cudaHostUnregister(ptr));
-  return PGK_OK;
-}
-
 int pgk_knn_work(const void *ws, int64_t n, int64_t nq, int64_t d, int64_t k, int mode,
                  uint64_t *work_host, void *stream) {
   PGK_REQUIRE(ws && work_host, "NULL argument");

@@ -37,6 +37,9 @@ int launch_prune(const float *X, const uint8_t *xu8, const int32_t *norms, int64
                  cudaStream_t stream, bool short_rows = false);
 
 constexpr int SORT_WARPS = 8;
+#ifndef SCATTER_PASSES
+#define SCATTER_PASSES 1  // measured: 4 node-range passes 1.05 ms vs 0.68 ms for one
+#endif
 constexpr int SORT_SMEM_KEYS = 512;  // per-warp in-register sort capacity (16 keys per lane)
 
 // warp per phase-A row, lane per entry (no per-element division)
@@ -147,7 +150,11 @@ __global__ void scatter_kernel(const int32_t *__restrict__ ids,
                                const int32_t *__restrict__ counts, int64_t n,
                                int width, const int64_t *__restrict__ mrg_off,
                                int32_t *__restrict__ rev_left,
-                               uint64_t *__restrict__ keys) {
+                               uint64_t *__restrict__ keys, int64_t vlo, int64_t vhi) {
+  // one pass of SCATTER_PASSES: only entries whose target slice (v for a
+  // reverse entry, u for an own entry) lies in [vlo, vhi) are written, so
+  // the pass's scattered 8-byte writes stay inside an L2-sized part of the
+  // key array (no partial-sector write-backs to DRAM)
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += 2 * nw) {
@@ -164,15 +171,16 @@ __global__ void scatter_kernel(const int32_t *__restrict__ ids,
       const bool r1 = p1 && (uint64_t)v1 < (uint64_t)n, r2 = p2 && (uint64_t)v2 < (uint64_t)n;
       if (p1 && !r1) v1 = (int32_t)u;
       if (p2 && !r2) v2 = (int32_t)u2;
+      const bool w1 = r1 && v1 >= vlo && v1 < vhi, w2 = r2 && v2 >= vlo && v2 < vhi;
       int s1 = 0, s2 = 0;
-      if (r1) s1 = atomicSub(rev_left + v1, 1) - 1;
-      if (r2) s2 = atomicSub(rev_left + v2, 1) - 1;
-      const int64_t b1 = r1 ? mrg_off[v1] + counts[v1] : 0;
-      const int64_t b2 = r2 ? mrg_off[v2] + counts[v2] : 0;
-      if (p1) keys[o1 + j] = pack_key(d1, v1);             // own entry
-      if (r1) keys[b1 + s1] = pack_key(d1, (int32_t)u);    // reverse
-      if (p2) keys[o2 + j] = pack_key(d2, v2);
-      if (r2) keys[b2 + s2] = pack_key(d2, (int32_t)u2);
+      if (w1) s1 = atomicSub(rev_left + v1, 1) - 1;
+      if (w2) s2 = atomicSub(rev_left + v2, 1) - 1;
+      const int64_t b1 = w1 ? mrg_off[v1] + counts[v1] : 0;
+      const int64_t b2 = w2 ? mrg_off[v2] + counts[v2] : 0;
+      if (p1 && u >= vlo && u < vhi) keys[o1 + j] = pack_key(d1, v1);     // own entry
+      if (w1) keys[b1 + s1] = pack_key(d1, (int32_t)u);                   // reverse
+      if (p2 && u2 >= vlo && u2 < vhi) keys[o2 + j] = pack_key(d2, v2);
+      if (w2) keys[b2 + s2] = pack_key(d2, (int32_t)u2);
     }
   }
 }
@@ -465,9 +473,15 @@ int add_reverse_and_prune(const float *X, const uint8_t *xu8, const int32_t *nor
   PGK_CUDA(cudaMemcpyAsync(L.rev_left, L.rev_cnt, sizeof(int32_t) * n,
                            cudaMemcpyDeviceToDevice, stream));
 
-  scatter_kernel<<<rblocks, 256, 0, stream>>>(a_ids, a_dists, a_counts, n, (int)a_width,
-                                              L.mrg_off, L.rev_left, L.keys);
-  PGK_CHECK_LAUNCH("scatter_kernel");
+  // key array (2 n R entries, 8 B) in node-range passes of <= ~64 MB each
+  const int64_t passes = std::max<int64_t>(1, std::min<int64_t>(SCATTER_PASSES,
+                                                                 (16 * n * a_width) >> 26));
+  for (int64_t p = 0; p < passes; ++p) {
+    const int64_t vlo = n * p / passes, vhi = n * (p + 1) / passes;
+    scatter_kernel<<<rblocks, 256, 0, stream>>>(a_ids, a_dists, a_counts, n, (int)a_width,
+                                                L.mrg_off, L.rev_left, L.keys, vlo, vhi);
+    PGK_CHECK_LAUNCH("scatter_kernel");
+  }
 
   const unsigned sblocks =
       (unsigned)std::min<int64_t>((n + SORT_WARPS - 1) / SORT_WARPS, (int64_t)sms * 8);

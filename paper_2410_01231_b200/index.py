@@ -90,7 +90,7 @@ class RngBuilder:
         return self._finish(X, u8, host_out)
 
     def build_host(self, host: torch.Tensor, host_out=None, chunks: int = 8,
-                   registered: bool = False) -> BuildOutput:
+                   source: np.ndarray | None = None) -> BuildOutput:
         """The whole path from a pinned host array (n, d) float32: the rows are
         copied in `chunks` pieces on a side stream while the current stream
         converts each landed chunk to exact-integer rows and assigns it to its
@@ -98,17 +98,21 @@ class RngBuilder:
         whole copy.  The exact-integer check runs on the device per chunk; if
         the data turn out not to qualify, the result is recomputed through the
         float path (one 4-byte read at the end: this call returns with the
-        build complete).  registered: `host` is page-locked by the caller
-        (pgk_host_register) rather than torch-pinned.  Non-U8 builders, and
-        shapes the tile-pruned pool
+        build complete).  source: a plain (pageable) numpy array of the same
+        shape; `host` is then a pinned staging buffer, filled chunk by chunk
+        just before each chunk's copy is enqueued (the CPU copy of chunk i+1
+        overlaps the transfer of chunk i).  Non-U8 builders, and shapes the
+        tile-pruned pool
         does not take (pgk_tiles_supported: K > 256, too many tiles,
         PGK_DISABLE_PRUNE=1), copy, then build."""
         if self.mode != _lib.POOL_U8 or self.d > 128 or \
                 not _lib.lib().pgk_tiles_supported(self.n, self.d, self.K):
+            if source is not None:
+                host.copy_(torch.from_numpy(source))
             out = self.build(host.to(_lib.device(), non_blocking=True), host_out)
             torch.cuda.current_stream().synchronize()
             return out
-        return _build_host(self, host, host_out, chunks, registered)
+        return _build_host(self, host, host_out, chunks, source)
 
     def _finish(self, X, u8, host_out, assigned: bool = False) -> BuildOutput:
         p = self.params
@@ -154,12 +158,12 @@ class HostPipeline:
         self.flag = torch.ones(1, dtype=torch.int32, device=dev)
         self.stream = torch.cuda.Stream(device=dev)
         self.f32 = None  # float-path builder, made if a dataset is not exact-integer
+        self.cen_host = None  # pinned staging of the centers (numpy sources)
 
 
 def _build_host(b: "RngBuilder", host: torch.Tensor, host_out, chunks: int,
-                registered: bool = False):
-    if host.device.type != "cpu" or not (registered or host.is_pinned()) \
-            or host.dtype != torch.float32 \
+                source: np.ndarray | None = None):
+    if host.device.type != "cpu" or not host.is_pinned() or host.dtype != torch.float32 \
             or tuple(host.shape) != (b.n, b.d) or not host.is_contiguous():
         raise ValueError(f"host data must be a pinned contiguous float32 ({b.n}, {b.d}) tensor")
     _check_host_out(host_out, b.n, b.params.M)
@@ -175,10 +179,19 @@ def _build_host(b: "RngBuilder", host: torch.Tensor, host_out, chunks: int,
     ev_c = torch.cuda.Event()
     evs = []
     with torch.cuda.stream(cs):
-        _lib.check(L.pgk_copy_rows_h2d(_lib.ptr(pp.cen), _lib.ptr(host), pp.C, d * 4,
-                                       pp.stride * d * 4, _lib.stream_handle()))
+        if source is None:
+            _lib.check(L.pgk_copy_rows_h2d(_lib.ptr(pp.cen), _lib.ptr(host), pp.C, d * 4,
+                                           pp.stride * d * 4, _lib.stream_handle()))
+        else:  # the centers (every stride-th row) staged first, densely
+            if pp.cen_host is None:
+                pp.cen_host = torch.empty((pp.C, d), dtype=torch.float32).pin_memory()
+            pp.cen_host.copy_(torch.from_numpy(source[::pp.stride]))
+            _lib.check(L.pgk_copy_rows_h2d(_lib.ptr(pp.cen), _lib.ptr(pp.cen_host), pp.C, d * 4,
+                                           d * 4, _lib.stream_handle()))
         ev_c.record(cs)
         for r0, r1 in spans:
+            if source is not None:
+                host[r0:r1].copy_(torch.from_numpy(source[r0:r1]))
             pp.X[r0:r1].copy_(host[r0:r1], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(cs)
@@ -213,7 +226,7 @@ def pool_mode(X: torch.Tensor) -> int:
     return _lib.POOL_U8 if kernels.detect_u8(X) else _lib.POOL_F32
 
 
-_CACHE: dict = {}  # the last shape's builder and its pinned output buffers
+_CACHE: dict = {}  # the last shape's builder, pinned staging and output buffers
 
 
 def build_rng_index(data, K: int, R: int, strategy: str = "rng", alpha: float = 60.0,
@@ -221,11 +234,11 @@ def build_rng_index(data, K: int, R: int, strategy: str = "rng", alpha: float = 
     """Host-buffer entry point: numpy (n, d) float32 in, ProximityGraph out
     (phases A+B, connect=False, as prune.refine(..., connect=False, ep=ep)).
 
-    The caller's array is page-locked in place for the call
-    (pgk_host_register) and fed to the chunked host pipeline
-    (RngBuilder.build_host: copy overlapped with the per-row work); the
-    builder and its pinned output buffers are kept for the next call of the
-    same shape."""
+    The array is staged chunk by chunk into a pinned buffer feeding the
+    chunked host pipeline (RngBuilder.build_host: the CPU staging of a chunk
+    overlaps the transfer of the previous one and the per-row device work);
+    the builder and its pinned buffers are kept for the next call of the same
+    shape."""
     data = np.ascontiguousarray(data, dtype=np.float32)
     if data.ndim != 2 or data.shape[0] < 1 or data.shape[1] < 1:
         raise ValueError("data must be a non-empty (n, d) array")
@@ -236,17 +249,12 @@ def build_rng_index(data, K: int, R: int, strategy: str = "rng", alpha: float = 
     if ent is None:
         _CACHE.clear()
         mode = _lib.POOL_U8 if d <= 128 else _lib.POOL_F32  # build_host re-checks on device
-        b = RngBuilder(n, d, K, params, mode)
-        ent = (b, torch.empty((n, R), dtype=torch.int32).pin_memory(),
+        ent = (RngBuilder(n, d, K, params, mode),
+               torch.empty((n, d), dtype=torch.float32).pin_memory(),
+               torch.empty((n, R), dtype=torch.int32).pin_memory(),
                torch.empty(n, dtype=torch.int32).pin_memory())
         _CACHE[key] = ent
-    b, h_ids, h_cnt = ent
-    host = torch.from_numpy(data)
-    L = _lib.lib()
-    _lib.check(L.pgk_host_register(_lib.ptr(host), data.nbytes))
-    try:
-        b.build_host(host, host_out=(h_ids, h_cnt), registered=True)
-        torch.cuda.current_stream().synchronize()
-    finally:
-        _lib.check(L.pgk_host_unregister(_lib.ptr(host)))
+    b, stage, h_ids, h_cnt = ent
+    b.build_host(stage, host_out=(h_ids, h_cnt), source=data)
+    torch.cuda.current_stream().synchronize()
     return ProximityGraph(adj=h_ids.numpy().copy(), counts=h_cnt.numpy().copy(), M=R, ep=ep)
