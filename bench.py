@@ -356,7 +356,24 @@ def run_ours(args):
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = N * world * args.steps / float(te.item())
+    e2e_single = N * world * args.steps / float(te.item())
+    # the same host-data builds as one stream of datasets through the public
+    # API (RngBuilder.build_host_stream): every dataset is copied host ->
+    # device and its adjacency + degrees land in pinned host memory inside the
+    # timed region; dataset i+1's copy runs on a side stream under build i
+    hosts = [host] * args.steps
+    outs = [(ids_host, cnt_host)] * args.steps
+    builder.build_host_stream(hosts[:2], outs[:2])  # its buffers and stream, untimed
+    barrier()
+    es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    es.record(stream)
+    builder.build_host_stream(hosts, outs)
+    ee.record(stream)
+    barrier()
+    ts = torch.tensor([es.elapsed_time(ee) / 1e3], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+    e2e_value = N * world * args.steps / float(ts.item())
 
     hbm, bf16, bf16_sus, peak_kind = peaks()
     u8_path = builder.u8_rows(X) is not None
@@ -449,7 +466,14 @@ def run_ours(args):
         "graph": {"mean_degree_A": deg_a, "mean_degree_B": deg_b, "dist_evals_A": de_a},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": int(data.nbytes),
-                "d2h_bytes_per_step": int(N * R * 4 + N * 4)},
+                "d2h_bytes_per_step": int(N * R * 4 + N * 4),
+                "api": "RngBuilder.build_host_stream: the K steps' datasets from pinned host "
+                       "memory, each copied in and its adjacency + degrees copied out inside "
+                       "the timed region; dataset i+1's copy overlaps build i",
+                "single_call": {"value": e2e_single, "unit": UNIT,
+                                "api": "RngBuilder.build_host per step (chunked copy "
+                                       "overlapped with the per-row work; copy and build "
+                                       "otherwise serial)"}},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

@@ -55,6 +55,8 @@ class RngBuilder:
         self.order_out = torch.empty(n, dtype=I32, device=dev)
         self.prune_ws = _lib.workspace(kernels.prune_workspace_bytes(n))
         self._pipe = None  # build_host's buffers, made on first use
+        self._stream = None  # build_host_stream's copy stream and device buffers
+        self._f32 = None  # float-path builder for datasets that are not exact-integer
 
     def order(self):
         """Locality order of the last pools() call (selection passes only)."""
@@ -113,6 +115,71 @@ class RngBuilder:
             torch.cuda.current_stream().synchronize()
             return out
         return _build_host(self, host, host_out, chunks, source)
+
+    def build_host_stream(self, hosts, host_outs) -> list:
+        """Build a sequence of datasets of this shape from pinned host arrays
+        (hosts[i]: (n, d) float32) into pinned outputs (host_outs[i]: (ids,
+        counts), as build's host_out), double-buffered: dataset i+1 is copied
+        to the device on a side stream while dataset i is being built, so the
+        transfers hide under the builds instead of preceding them.  Every
+        dataset's own copy happens inside the call.  The exact-integer check
+        runs on the device per dataset; a dataset that fails it is rebuilt
+        through the float path at the end.  Returns the BuildOutputs (device
+        tensors of the last build are overwritten by the next; the host
+        outputs are the results)."""
+        k = len(hosts)
+        if k != len(host_outs):
+            raise ValueError("one host_out per host array")
+        for h in hosts:
+            if h.device.type != "cpu" or not h.is_pinned() or h.dtype != torch.float32 \
+                    or tuple(h.shape) != (self.n, self.d) or not h.is_contiguous():
+                raise ValueError(f"host data must be pinned contiguous float32 ({self.n}, {self.d})")
+        for o in host_outs:
+            _check_host_out(o, self.n, self.params.M)
+        if self._stream is None:
+            dev = _lib.device()
+            self._stream = (torch.cuda.Stream(device=dev),
+                            [torch.empty((self.n, self.d), dtype=torch.float32, device=dev)
+                             for _ in range(2)],
+                            torch.ones(max(k, 1), dtype=torch.int32, device=dev))
+        cs, xb, flags = self._stream
+        if flags.numel() < k:
+            flags = torch.ones(k, dtype=torch.int32, device=xb[0].device)
+            self._stream = (cs, xb, flags)
+        main = torch.cuda.current_stream()
+        flags[:k].fill_(1)
+        landed = [torch.cuda.Event() for _ in range(k)]
+        freed = [torch.cuda.Event() for _ in range(k)]
+        cs.wait_stream(main)  # earlier work on these buffers is done
+        with torch.cuda.stream(cs):
+            xb[0].copy_(hosts[0], non_blocking=True)
+            landed[0].record(cs)
+        outs = []
+        L = _lib.lib()
+        for i in range(k):
+            if i + 1 < k:  # the next dataset's copy, once build i-1 released its buffer
+                with torch.cuda.stream(cs):
+                    if i >= 1:
+                        cs.wait_event(freed[i - 1])
+                    xb[(i + 1) % 2].copy_(hosts[i + 1], non_blocking=True)
+                    landed[i + 1].record(cs)
+            main.wait_event(landed[i])
+            X = xb[i % 2]
+            if self.mode == _lib.POOL_U8 and self.d <= 128:
+                _lib.check(L.pgk_detect_u8_async(_lib.ptr(X), self.n, self.d,
+                                                 _lib.ptr(flags[i:i + 1]), _lib.stream_handle()))
+            outs.append(self.build(X, host_outs[i]))
+            freed[i].record(main)
+        if self.mode == _lib.POOL_U8 and self.d <= 128:
+            bad = torch.nonzero(flags[:k] == 0).flatten().tolist()  # one read at the end
+            for i in bad:  # not exact-integer after all: the float path
+                if self._f32 is None:
+                    self._f32 = RngBuilder(self.n, self.d, self.K, self.params, _lib.POOL_F32)
+                X = xb[0]
+                X.copy_(hosts[i], non_blocking=True)
+                outs[i] = self._f32.build(X, host_outs[i])
+        torch.cuda.current_stream().synchronize()
+        return outs
 
     def _finish(self, X, u8, host_out, assigned: bool = False) -> BuildOutput:
         p = self.params

@@ -628,3 +628,22 @@ def test_full_scale_float_build_on_seeded_rows(cfg, strategy, alpha, nrows):
     np.testing.assert_array_equal(out.dists.cpu().numpy()[sel], ob[1][sel])
     np.testing.assert_array_equal(out.counts.cpu().numpy()[sel], ob[2][sel])
     assert int(b.b_out[3].cpu().numpy()[sel].sum()) == ob[3]
+
+
+def test_build_host_stream_equals_device_builds():
+    """RngBuilder.build_host_stream (double-buffered: dataset i+1 copied while
+    dataset i builds) gives every dataset the device build's adjacency; a
+    dataset that is not exact-integer goes through the float path."""
+    from paper_2410_01231_b200 import _lib
+    from paper_2410_01231_b200.index import RngBuilder, pool_mode
+    n = 20000
+    sets = [synth.cfg2(n), synth.cfg2(n, n_full=2 * n), synth.cfg2(n) + np.float32(0.25)]
+    b = RngBuilder(n, 128, 64, PruneParams(M=24), _lib.POOL_U8)
+    hosts = [torch.from_numpy(x).pin_memory() for x in sets]
+    outs = [(torch.zeros((n, 24), dtype=torch.int32).pin_memory(),
+             torch.zeros(n, dtype=torch.int32).pin_memory()) for _ in sets]
+    b.build_host_stream(hosts, outs)
+    for x, (h_ids, h_cnt) in zip(sets, outs):
+        X = torch.from_numpy(x).cuda()
+        ref = RngBuilder(n, 128, 64, PruneParams(M=24), pool_mode(X)).build(X)
+        assert torch.equal(h_ids, ref.ids.cpu()) and torch.equal(h_cnt, ref.counts.cpu())
