@@ -708,7 +708,8 @@ bool tiles_supported(int64_t n, int64_t d, int64_t k);
 bool tiles_f32_supported(int64_t n, int64_t d, int64_t k);
 size_t tiles_f32_workspace(int64_t n, int64_t d, int64_t k);
 int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64_t *keys,
-                          void *tws, size_t tws_bytes, cudaStream_t stream, bool *handled);
+                          void *tws, size_t tws_bytes, cudaStream_t stream, bool *handled,
+                          bool *lb_keys);
 int tiles_f32_order(void *tws, int64_t n, int64_t d, int64_t k, int32_t *out,
                     cudaStream_t stream);
 int tiles_f32_work(const void *tws, int64_t n, int64_t d, int64_t k, unsigned long long out[4],
@@ -965,11 +966,11 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
     PGK_CHECK_LAUNCH("finalize_exact_kernel");
     return PGK_OK;
   }
-  bool pruned = false;
+  bool pruned = false, lb_keys = false;
   if (L.tws_f32 && self && exclude_self) {
     // exact tile pruning: S approximate survivors from the candidate tiles only
     rc = launch_pool_tiles_f32(X, n, (int)d, (int)k, S, L.keys, L.tws_f32, L.tws_f32_bytes,
-                               stream, &pruned);
+                               stream, &pruned, &lb_keys);
     if (rc) return rc;
     if (pruned) {
       rc = tiles_f32_order(L.tws_f32, n, d, k, L.order, stream);
@@ -984,7 +985,9 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
     if (rc) return rc;
   }
   // (1+u)^(d+2) <= 1 + gamma for u = 2^-24
-  const double gamma = (double)(d + 2) * 5.9604644775390625e-08 * 1.001 + 1e-12;
+  // (the tensor-core passes hand over proven lower bounds: nothing to inflate)
+  const double gamma =
+      lb_keys ? 0.0 : (double)(d + 2) * 5.9604644775390625e-08 * 1.001 + 1e-12;
   const unsigned rgrid =
       (unsigned)std::min<int64_t>((nq + RR_WARPS - 1) / RR_WARPS, (int64_t)sms * 16);
   static int staged_env = -1;

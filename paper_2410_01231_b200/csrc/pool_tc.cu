@@ -27,6 +27,7 @@
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
+#include "tc_select.cuh"
 
 namespace pgk {
 namespace tc {
@@ -79,96 +80,6 @@ struct __align__(1024) Smem {
 // so the MMA of the next tile's first half overlaps the epilogue's second half
 constexpr uint32_t IDESC_H =
     (2u << 4) | ((uint32_t)(HN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-
-// Internal keys of this kernel: ((uint64)dist << 32) | id with dist the exact
-// integer distance (< 2^25), so key order == (dist, id) order.
-__device__ __forceinline__ uint32_t khi(uint64_t k) { return (uint32_t)(k >> 32); }
-
-__device__ __forceinline__ int warp_sum(int v) {
-  return (int)__reduce_add_sync(0xffffffffu, (unsigned)v);
-}
-
-// Warp-cooperative selection on one row's candidate buffer (cnt > K keys in
-// global memory): keep exactly the K smallest keys (unordered) at buf[0..K)
-// and return the K-th smallest key.  Binary searches over the register-
-// resident keys (distance within [min, max], then id among distance ties;
-// REDUX warp sums); no sort.
-template <int KPL>
-__device__ __noinline__ uint64_t select_kt(uint64_t *buf, int cnt, int K, uint32_t hi_bound,
-                                           int lane) {
-  static_assert(KPL <= 32, "selection holds the whole buffer in registers");
-  uint64_t kk[KPL];
-  uint32_t dmin = 0xffffffffu, dmax = 0;
-#pragma unroll
-  for (int i = 0; i < KPL; ++i) {
-    const int idx = i * 32 + lane;
-    kk[i] = idx < cnt ? buf[idx] : KEY_MAX;
-    if (idx < cnt) {
-      dmin = min(dmin, khi(kk[i]));
-      dmax = max(dmax, khi(kk[i]));
-    }
-  }
-  // smallest td with #{dist <= td} >= K, searched in [min, max]
-  uint32_t lo = __reduce_min_sync(0xffffffffu, dmin);
-  uint32_t hi = min(__reduce_max_sync(0xffffffffu, dmax), hi_bound);
-  while (lo < hi) {
-    const uint32_t mid = lo + ((hi - lo) >> 1);
-    int c = 0;
-#pragma unroll
-    for (int i = 0; i < KPL; ++i) c += khi(kk[i]) <= mid;
-    if (warp_sum(c) >= K) hi = mid;
-    else lo = mid + 1;
-  }
-  const uint32_t td = lo;
-  int c_lt = 0, c_eq = 0;
-  uint32_t id_max = 0;
-#pragma unroll
-  for (int i = 0; i < KPL; ++i) {
-    c_lt += khi(kk[i]) < td;
-    if (khi(kk[i]) == td) {
-      ++c_eq;
-      id_max = max(id_max, (uint32_t)kk[i]);
-    }
-  }
-  c_lt = warp_sum(c_lt);
-  c_eq = warp_sum(c_eq);
-  const int need = K - c_lt;
-  uint32_t tid;
-  if (c_eq == need) {
-    tid = __reduce_max_sync(0xffffffffu, id_max);
-  } else {  // distance ties straddle the boundary: smallest ids win
-    uint32_t a = 0, b = 0x7fffffffu;
-    while (a < b) {
-      const uint32_t mid = a + ((b - a) >> 1);
-      int c = 0;
-#pragma unroll
-      for (int i = 0; i < KPL; ++i) c += khi(kk[i]) == td && (uint32_t)kk[i] <= mid;
-      if (warp_sum(c) >= need) b = mid;
-      else a = mid + 1;
-    }
-    tid = a;
-  }
-  const uint64_t tau = ((uint64_t)td << 32) | tid;
-  __syncwarp();
-  int p = 0;
-#pragma unroll
-  for (int i = 0; i < KPL; ++i) {
-    const bool keep = kk[i] <= tau;
-    const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    if (keep) buf[p + __popc(bal & lanemask_lt())] = kk[i];
-    p += __popc(bal);
-  }
-  __syncwarp();
-  return tau;
-}
-
-// cnt <= 32*KPL keys per call
-__device__ __forceinline__ uint64_t select_k(uint64_t *buf, int cnt, int K, uint32_t hi_bound,
-                                             int lane) {
-  if (cnt <= 256) return select_kt<8>(buf, cnt, K, hi_bound, lane);
-  if (cnt <= 512) return select_kt<16>(buf, cnt, K, hi_bound, lane);
-  return select_kt<CAP / 32>(buf, cnt, K, hi_bound, lane);
-}
 
 // Register bitonic sort of 32*NPL keys (element i = slot*32 + lane).
 template <int NPL>
@@ -1366,6 +1277,21 @@ bool make_u8_row_map(CUtensorMap *tm, const uint8_t *base, int64_t rows, int box
   return r == CUDA_SUCCESS;
 }
 
+// (rows x cols) bf16 row-major tensor map with a (64 x 128) box, SW128: the
+// operand blocks of the float pool (pool_tc_f32.cu)
+bool make_bf16_tile_map(CUtensorMap *tm, const void *base, int64_t rows, int64_t cols) {
+  auto fn = tc::encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // instrumentation (PGK_TILES_STATS): pass-1 order statistics per row
 uint32_t *g_dense_ostat = nullptr;
 
@@ -1382,7 +1308,7 @@ size_t tc_pool_workspace(int64_t n, int64_t nq, bool self) {
 
 bool tc_pool_supported(int64_t d, int64_t k) {
   static_assert(tc::CAP >= 256 + 32, "CAP must leave room for K <= 256 plus one chunk");
-  static_assert(tc::CAP <= 1024, "select_k holds CAP keys in registers");
+  static_assert(tc::CAP <= tc::SEL_CAP, "select_k holds CAP keys in registers");
   static_assert(tc::FIN_STAGE >= 256, "finalize stages up to K = 256 keys");
   static int env = -1;
   if (env < 0) {

@@ -1,0 +1,753 @@
+// pool_tc_f32.cu -- float k-NN pool passes on the 5th-gen tensor cores
+// (tcgen05 kind::f16, bf16 operands, fp32 accumulation in TMEM) for general
+// fp32 data (configs 1, 3, 4; reference oracle.py:31-65 ranks by float64).
+//
+// What the tensor cores deliver is a PREFILTER with a proven error bound; the
+// float64 rerank (pool_simt.cu) stays the judge of the K members.
+//
+//   * Centred operands.  Every 128-row tile T of the tile-sorted rows is
+//     assigned one of G <= 128 reference vectors m_g (greedy k-center over the
+//     tile centroids) and stores x' = fl32(x - m_ref(T)), split into two bf16
+//     terms x' = h + l + r, |r_i| <= 2^-18 |x'_i|.  For q in tile Q (ref a) and
+//     x in tile T (ref b), Delta = m_b - m_a:
+//         |q - x|^2 = |q'|^2 + |x'|^2 + |Delta|^2 - 2 q'.x' - 2 q'.Delta + 2 x'.Delta
+//     q'.x' ~ h_q.h_x + h_q.l_x + l_q.h_x on the tensor cores (3 MMAs per
+//     K = 16 step); the cross terms come from a float64 table
+//     P[row][g] = row'.(m_g - m_ref(row)) (exactly zero when a == b), so large
+//     common offsets (config 3: norms ~17x the neighbour distances) never
+//     enter the fp32 accumulation.
+//   * Error bound (a = |q'|, b = |x'|, delta = |Delta|):
+//       - dropped operand terms          <= 3.1 * 2^-18 a b
+//       - fp32 accumulation of 3 dp products per pair, truncating adder
+//         (every addend and every partial sum rounded toward zero at the
+//         accumulator's precision)       <= 4 (dp + 16) 2^-23 a b
+//       - rounding of the stored x', q'  <= 2^-23 (a + b)(a + b + delta)
+//       - rounding of the stored P       <= 2^-23 (a + b) delta
+//     folded into per-row, per-column and per-pair slack terms; the epilogue
+//     evaluates them with directed rounding (FFMA.RM / FADD.RM), so a stored
+//     key is a true LOWER bound of the pair's squared distance (pass 2) or a
+//     true UPPER bound (pass 1, whose K-th smallest value bounds the row's
+//     K-th neighbour distance from above).
+//   * Pass 2 keeps every pair whose lower bound is <= the row's pass-1 bound
+//     (nothing else can be among the K nearest), then the S smallest lower
+//     bounds go to the rerank, whose proof needs gamma = 0: every pair not
+//     handed over has true distance >= its lower bound >= the S-th one.
+//
+// Kernel shape (persistent, 1 CTA / SM, 192 threads): warp 0 TMA producer +
+// dynamic block scheduler (3-stage ring of 64-element k-blocks: A hi/lo and B
+// hi/lo, SW128), warp 1 MMA issuer (2 accumulators of 128 TMEM columns by tile
+// parity), warps 2-5 epilogue (thread = query row = TMEM lane; per-row
+// candidate buffers in global memory, select_k compaction when full).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+#include "tc_select.cuh"
+
+namespace pgk {
+
+bool make_bf16_tile_map(CUtensorMap *tm, const void *base, int64_t rows, int64_t cols);
+
+namespace tcf {
+
+using namespace tc;
+
+constexpr int BM = 128;      // query rows per block == TMEM lanes
+constexpr int BN = 128;      // candidate rows per tile == MMA N
+constexpr int KBLK = 64;     // bf16 elements per k-block (one 128-byte SW128 row)
+constexpr int STAGES = 3;    // k-block ring depth (4 x 16 KB per stage)
+constexpr int ACC = 2;       // TMEM accumulators (128 columns each, by tile parity)
+constexpr int CAP = 1024;    // per-row candidate buffer (keys, global memory)
+constexpr int THREADS = 192;
+constexpr int TILE_B = BN * 128;  // bytes of one (128 rows x 64 bf16) operand block
+constexpr int TMEM_COLS = ACC * BN;
+constexpr int GMAX = 128;    // reference vectors
+constexpr float TAU_MAX = 1e29f;   // "no bound yet"
+constexpr float PAD_CX = 1e30f;    // column term of padding slots: never passes
+
+// kind::f16: D fp32, A/B bf16, K-major, M = 128, N = 128
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+struct __align__(1024) Smem {
+  uint8_t st[STAGES][4][TILE_B];  // A hi, A lo, B hi, B lo
+  float sv[4][32 * 36];           // per epilogue warp: one chunk of dot products per lane
+  alignas(16) float cx[2][BN];    // per tile (parity): column term
+  alignas(16) float kb[2][BN];    // kappa * |x'|
+  alignas(16) int32_t pid[2][BN]; // original ids (-1 = padding)
+  uint64_t full[STAGES], empty[STAGES];
+  uint64_t tfull[ACC], tempty[ACC];
+  uint64_t blk_full, blk_empty;
+  uint32_t tmem_base;
+  int32_t blk[2];
+};
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// directed-rounding helpers: UB = upper bounds (round up), else lower bounds
+template <bool UB>
+__device__ __forceinline__ float fma_dir(float a, float b, float c) {
+  return UB ? __fmaf_ru(a, b, c) : __fmaf_rd(a, b, c);
+}
+template <bool UB>
+__device__ __forceinline__ float add_dir(float a, float b) {
+  return UB ? __fadd_ru(a, b) : __fadd_rd(a, b);
+}
+template <bool UB>
+__device__ __forceinline__ float d2f_dir(double v) {
+  return UB ? __double2float_ru(v) : __double2float_rd(v);
+}
+
+struct Args {
+  int64_t np;              // tile-sorted rows (multiple of 128)
+  int nkb;                 // k-blocks per row (dp / 64)
+  int dp;                  // padded dimension
+  int G;                   // reference vectors
+  int K;                   // selection size of this pass (pass 1: K, pass 2: S)
+  float kappa;             // pair slack factor
+  const int32_t *tlist, *tlen;
+  int64_t tstride;
+  const int32_t *perm;     // sorted row -> original id (-1 = padding)
+  const int32_t *tref;     // tile -> reference
+  const float *P;          // np x G cross terms
+  const double *D2;        // G x G squared reference distances
+  const float *nbnd;       // np: |x'|^2 bound (pass 1: upper, pass 2: lower; slack included)
+  const float *na;         // np: |x'| rounded up
+  const float *tau_in;     // np: row thresholds (pass 2); null = none yet
+  uint64_t *bufs;          // np x CAP keys
+  int32_t *row_cnt;        // np
+  float *row_tau;          // np
+  int32_t *sched;
+};
+
+template <bool UB>
+__global__ void __launch_bounds__(THREADS, 1)
+    tc_pool_f32_kernel(const __grid_constant__ CUtensorMap tmH, const Args g_) {
+  const Args &A = g_;
+  extern __shared__ uint8_t smem_raw[];
+  Smem &s = *reinterpret_cast<Smem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nblocks = (int)(A.np / BM);
+  const int nkb = A.nkb;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&s.full[i], 1);
+      mbar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < ACC; ++i) {
+      mbar_init(&s.tfull[i], 1);
+      mbar_init(&s.tempty[i], 4);
+    }
+    mbar_init(&s.blk_full, 1);
+    mbar_init(&s.blk_empty, 1 + 4);  // MMA thread + one lane per epilogue warp
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&s.tmem_base)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer + block scheduler ----------------
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmH) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int it = 0;; ++it) {
+        int b, len = 0;
+        do {
+          b = atomicAdd(A.sched, 1);
+          if (b < nblocks) len = A.tlen[b];
+        } while (b < nblocks && len == 0);
+        mbar_wait(&s.blk_empty, (it & 1) ^ 1);
+        s.blk[it & 1] = b < nblocks ? b : -1;
+        mbar_arrive(&s.blk_full);
+        if (b >= nblocks) break;
+        for (int t = 0; t < len; ++t) {
+          const int tid = A.tlist[(int64_t)b * A.tstride + t];
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&s.empty[stage], phase ^ 1);
+            mbar_expect_tx(&s.full[stage], 4 * TILE_B);
+            tma_load_2d(s.st[stage][0], &tmH, &s.full[stage], kb * KBLK, b * BM);
+            tma_load_2d(s.st[stage][1], &tmH, &s.full[stage], A.dp + kb * KBLK, b * BM);
+            tma_load_2d(s.st[stage][2], &tmH, &s.full[stage], kb * KBLK, tid * BN);
+            tma_load_2d(s.st[stage][3], &tmH, &s.full[stage], A.dp + kb * KBLK, tid * BN);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t g = 0;  // tiles issued by this CTA
+      for (int it = 0;; ++it) {
+        mbar_wait(&s.blk_full, it & 1);
+        const int b = s.blk[it & 1];
+        mbar_arrive(&s.blk_empty);
+        if (b < 0) break;
+        const int len = A.tlen[b];
+        for (int t = 0; t < len; ++t, ++g) {
+          mbar_wait(&s.tempty[g % ACC], ((g / ACC) & 1) ^ 1);
+          const uint32_t dcol = tmem + (g % ACC) * BN;
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&s.full[stage], phase);
+            tc_fence_after();
+            const uint64_t ah = sw128_desc(s.st[stage][0]), al = sw128_desc(s.st[stage][1]);
+            const uint64_t bh = sw128_desc(s.st[stage][2]), bl = sw128_desc(s.st[stage][3]);
+#pragma unroll
+            for (int kk = 0; kk < KBLK / 16; ++kk)  // K = 16 bf16 = 32 B per MMA
+              mma_bf16(dcol, ah + 2 * kk, bh + 2 * kk, IDESC, (kb | kk) != 0);
+#pragma unroll
+            for (int kk = 0; kk < KBLK / 16; ++kk) mma_bf16(dcol, ah + 2 * kk, bl + 2 * kk, IDESC, 1);
+#pragma unroll
+            for (int kk = 0; kk < KBLK / 16; ++kk) mma_bf16(dcol, al + 2 * kk, bh + 2 * kk, IDESC, 1);
+            tc_commit(&s.empty[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          tc_commit(&s.tfull[g % ACC]);
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue ----------------
+    const int q = warp & 3;        // TMEM lane quarter of this warp
+    const int et = threadIdx.x - 64;  // 0..127: the column this thread prepares
+    float *sv = s.sv[warp - 2] + lane * 36;
+    uint32_t g = 0;
+    for (int it = 0;; ++it) {
+      mbar_wait(&s.blk_full, it & 1);
+      const int b = s.blk[it & 1];
+      if (lane == 0) mbar_arrive(&s.blk_empty);
+      if (b < 0) break;
+      const int64_t row = (int64_t)b * BM + q * 32 + lane;
+      const bool row_ok = A.perm[row] >= 0;
+      uint64_t *wbuf = A.bufs + ((int64_t)b * BM + q * 32) * CAP;  // this warp's rows
+      const int len = A.tlen[b];
+      const int aref = A.tref[b];
+      const float a_q = A.na[row];
+      const double nq = (double)A.nbnd[row];
+      float tau = A.tau_in ? fminf(A.tau_in[row], TAU_MAX) : TAU_MAX;
+      int cnt = 0;
+      int tid_next = A.tlist[(int64_t)b * A.tstride];
+      for (int t = 0; t < len; ++t, ++g) {
+        const int tid = tid_next;
+        if (t + 1 < len) tid_next = A.tlist[(int64_t)b * A.tstride + t + 1];
+        const int par = (int)(g & 1);
+        // ---- per-tile terms: column j = et (all 128 epilogue threads), row = this lane ----
+        const int bref = A.tref[tid];
+        double d2 = 0.0, delta = 0.0;
+        if (bref != aref) {
+          d2 = A.D2[(int64_t)aref * A.G + bref];
+          delta = sqrt(d2) * (1.0 + 1e-12);
+        }
+        {
+          const int64_t col = (int64_t)tid * BN + et;
+          const int32_t pj = A.perm[col];
+          const double bj = (double)A.na[col];
+          const double pc = bref != aref ? (double)A.P[col * A.G + aref] : 0.0;
+          // column term: |x'|^2 + 2 x'.Delta = nbnd - 2 P[x][a], slack 2^-21 b delta
+          const double sl = 4.76837158203125e-07 * bj * delta;  // 2^-21
+          const double v = (double)A.nbnd[col] - 2.0 * pc + (UB ? sl : -sl);
+          const double rs = 1e-12 * (fabs((double)A.nbnd[col]) + 2.0 * fabs(pc));
+          s.cx[par][et] = pj >= 0 ? d2f_dir<UB>(v + (UB ? rs : -rs)) : PAD_CX;
+          s.kb[par][et] = __fmul_ru(A.kappa, A.na[col]);
+          s.pid[par][et] = pj;
+        }
+        // row term: |q'|^2 + |Delta|^2 - 2 q'.Delta = nbnd + D2 - 2 P[q][b]
+        float rq;
+        {
+          const double pr = bref != aref ? (double)A.P[row * A.G + bref] : 0.0;
+          const double sl = 4.76837158203125e-07 * (double)a_q * delta;
+          const double rs = 1e-12 * (fabs(nq) + d2 + 2.0 * fabs(pr));
+          const double v = nq + d2 - 2.0 * pr;
+          rq = d2f_dir<UB>(UB ? v + sl + rs : v - sl - rs);
+        }
+        // pairs pass iff t2 = (cx -/+ kappa a b - 2 D) <= thr, thr >= tau - rq
+        float thr = row_ok ? __fsub_ru(tau, rq) : -3e38f;
+        const float ka = UB ? a_q : -a_q;
+        named_bar_sync(1, 128);  // the tile's column terms are in place
+        mbar_wait(&s.tfull[g % ACC], (g / ACC) & 1);
+        tc_fence_after();
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (g % ACC) * BN;
+        const int64_t col0 = (int64_t)tid * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c * 32, r);
+          tmem_wait_ld();
+          const float4 *cxp = reinterpret_cast<const float4 *>(s.cx[par] + c * 32);
+          const float4 *kbp = reinterpret_cast<const float4 *>(s.kb[par] + c * 32);
+          uint32_t mask = 0;
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const float4 cxv = cxp[v], kbv = kbp[v];
+            const float t0 = fma_dir<UB>(ka, kbv.x, fma_dir<UB>(-2.0f, __uint_as_float(r[4 * v]), cxv.x));
+            const float t1 = fma_dir<UB>(ka, kbv.y, fma_dir<UB>(-2.0f, __uint_as_float(r[4 * v + 1]), cxv.y));
+            const float t2 = fma_dir<UB>(ka, kbv.z, fma_dir<UB>(-2.0f, __uint_as_float(r[4 * v + 2]), cxv.z));
+            const float t3 = fma_dir<UB>(ka, kbv.w, fma_dir<UB>(-2.0f, __uint_as_float(r[4 * v + 3]), cxv.w));
+            mask |= (t0 <= thr) ? (1u << (4 * v)) : 0u;
+            mask |= (t1 <= thr) ? (1u << (4 * v + 1)) : 0u;
+            mask |= (t2 <= thr) ? (1u << (4 * v + 2)) : 0u;
+            mask |= (t3 <= thr) ? (1u << (4 * v + 3)) : 0u;
+          }
+          const int64_t cb = col0 + c * 32;
+          if (row >= cb && row < cb + 32) mask &= ~(1u << (int)(row - cb));  // never itself
+          if (__any_sync(0xffffffffu, mask != 0)) {
+            if (mask) {
+#pragma unroll
+              for (int v = 0; v < 8; ++v)
+                reinterpret_cast<float4 *>(sv)[v] =
+                    make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+            }
+            __syncwarp();
+            // room for this chunk's survivors in every row of the warp: a full
+            // buffer is cut to its K smallest bounds, whose largest becomes
+            // the row's threshold
+            unsigned need = __ballot_sync(0xffffffffu, cnt + __popc(mask) > CAP);
+            while (need) {
+              const int src = __ffs(need) - 1;
+              need &= need - 1;
+              const int c_src = __shfl_sync(0xffffffffu, cnt, src);
+              const uint64_t nt = select_k(wbuf + (size_t)src * CAP, c_src, A.K, 0xffffffffu, lane);
+              if (lane == src) {
+                cnt = A.K;
+                tau = fminf(tau, key_dist(nt));
+                thr = __fsub_ru(tau, rq);
+                // re-test this chunk under the tighter threshold
+                unsigned m2 = 0;
+                for (unsigned mm = mask; mm; mm &= mm - 1) {
+                  const int j = __ffs(mm) - 1;
+                  const float tv = fma_dir<UB>(ka, s.kb[par][c * 32 + j],
+                                               fma_dir<UB>(-2.0f, sv[j], s.cx[par][c * 32 + j]));
+                  if (tv <= thr) m2 |= 1u << j;
+                }
+                mask = m2;
+              }
+            }
+            {
+              uint64_t *mybuf = wbuf + (size_t)lane * CAP + cnt;
+              const int trips = (int)__reduce_max_sync(0xffffffffu, (unsigned)__popc(mask));
+              unsigned mm = mask;
+#pragma unroll 2
+              for (int i = 0; i < trips; ++i) {
+                const bool act = mm != 0;
+                const int j = act ? __ffs(mm) - 1 : 0;
+                const float tv = fma_dir<UB>(ka, s.kb[par][c * 32 + j],
+                                             fma_dir<UB>(-2.0f, sv[j], s.cx[par][c * 32 + j]));
+                const uint64_t key = pack_key(add_dir<UB>(tv, rq), s.pid[par][c * 32 + j]);
+                if (act) *mybuf = key;
+                mybuf += act ? 1 : 0;
+                mm &= mm - 1;
+              }
+            }
+            cnt += __popc(mask);
+            __syncwarp();
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s.tempty[g % ACC]);
+      }
+      A.row_cnt[row] = row_ok ? cnt : -1;
+      A.row_tau[row] = tau;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Selection after a pass, warp per tile-sorted row.
+//   pass 1 (keys_out == null): tau_out[row] = the K-th smallest upper bound
+//   pass 2: the S smallest lower-bound keys at keys_out[perm[row] * S ..], the
+//           largest of them last (the rerank's proof reads that slot)
+// ---------------------------------------------------------------------------
+constexpr int FIN_WARPS = 8;
+
+__global__ void __launch_bounds__(FIN_WARPS * 32)
+    f32_select_kernel(uint64_t *__restrict__ bufs, const int32_t *__restrict__ row_cnt,
+                      const int32_t *__restrict__ perm, int64_t np, int K,
+                      float *__restrict__ tau_out, uint64_t *__restrict__ keys_out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < np;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int cnt = row_cnt[p];
+    const int32_t orow = perm[p];
+    if (orow < 0 || cnt < 0) {
+      if (tau_out && lane == 0) tau_out[p] = TAU_MAX;
+      continue;
+    }
+    uint64_t *buf = bufs + p * CAP;
+    uint64_t kth = KEY_MAX;
+    if (cnt > K) {
+      kth = select_k(buf, cnt, K, 0xffffffffu, lane);
+    } else if (cnt == K) {
+      uint64_t m = 0;
+      for (int j = lane; j < K; j += 32) m = max(m, buf[j]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      kth = m;
+    }
+    if (tau_out) {
+      if (lane == 0) tau_out[p] = kth == KEY_MAX ? TAU_MAX : fminf(key_dist(kth), TAU_MAX);
+      continue;
+    }
+    uint64_t *out = keys_out + (int64_t)orow * K;
+    const uint64_t last = cnt >= K ? buf[K - 1] : KEY_MAX;
+    for (int j = lane; j < K; j += 32) {
+      uint64_t k = j < cnt ? buf[j] : KEY_MAX;
+      if (kth != KEY_MAX) {
+        if (k == kth) k = last;       // the K-th smallest swaps into the last slot
+        if (j == K - 1) k = kth;
+      }
+      out[j] = k;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Operand preparation
+// ---------------------------------------------------------------------------
+// One greedy k-center step over the tile centroids: distances to reference g
+// (= centroid of tile *pick), nearest reference per tile, and the farthest
+// tile -> next pick.  Block 0 also copies the reference vector.
+__global__ void kcenter_step_kernel(const float *__restrict__ cent, const int32_t *__restrict__ size,
+                                    int64_t T, int d, int g, const unsigned long long *pick_in,
+                                    unsigned long long *pick_out, float *__restrict__ mind,
+                                    int32_t *__restrict__ tref, float *__restrict__ refs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t pick = g == 0 ? 0 : (int64_t)(uint32_t)(*pick_in);
+  const float *cp = cent + pick * d;
+  if (blockIdx.x == 0)
+    for (int k = threadIdx.x; k < d; k += blockDim.x) refs[(int64_t)g * d + k] = cp[k];
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < T;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    float acc = 0.f;
+    for (int k = lane; k < d; k += 32) {
+      const float v = cent[t * d + k] - cp[k];
+      acc = fmaf(v, v, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      float m = g == 0 ? 3e38f : mind[t];
+      if (acc < m) {
+        m = acc;
+        mind[t] = acc;
+        tref[t] = g;
+      }
+      if (size[t] > 0)
+        atomicMax(pick_out, ((unsigned long long)__float_as_uint(m) << 32) | (uint32_t)t);
+    }
+  }
+}
+
+// warp per row: x' = fl32(x - m_ref), bf16 hi / lo split into H (row: dp hi
+// values then dp lo values), |x'|^2 bounds with the row's own slack, |x'|
+__global__ void f32_split_kernel(const float *__restrict__ xs, const int32_t *__restrict__ perm,
+                                 const int32_t *__restrict__ tref, const float *__restrict__ refs,
+                                 int64_t np, int d, int dp, __nv_bfloat16 *__restrict__ H,
+                                 float *__restrict__ nlo, float *__restrict__ nhi,
+                                 float *__restrict__ na) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < np;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const bool real = perm[p] >= 0;
+    const float *m = refs + (int64_t)tref[p / BN] * d;
+    __nv_bfloat16 *h = H + p * 2 * dp;
+    double acc = 0.0;
+    for (int k = lane; k < dp; k += 32) {
+      float v = 0.f;
+      if (real && k < d) v = __fsub_rn(xs[p * d + k], m[k]);
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      const __nv_bfloat16 lo = __float2bfloat16_rn(__fsub_rn(v, __bfloat162float(hi)));
+      h[k] = hi;
+      h[dp + k] = lo;
+      acc = fma((double)v, (double)v, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const double a = sqrt(acc) * (1.0 + 1e-9);
+      // storage rounding of x' (2^-23 (a + b)(a + b + delta)): the row's own
+      // a^2 share, doubled for safety; the a*delta share is added per tile
+      const double sl = 2.384185791015625e-07 * a * a + 1e-12 * acc;  // 2^-22 a^2
+      nlo[p] = __double2float_rd(acc - sl);
+      nhi[p] = __double2float_ru(acc + sl);
+      na[p] = __double2float_ru(a);
+    }
+  }
+}
+
+// P[p][g] = x'_p . (m_g - m_ref(p)) in float64 (stored fp32), block per 8 rows
+constexpr int PX_WARPS = 8;
+__global__ void __launch_bounds__(PX_WARPS * 32)
+    f32_cross_kernel(const float *__restrict__ xs, const int32_t *__restrict__ perm,
+                     const int32_t *__restrict__ tref, const float *__restrict__ refs,
+                     int64_t np, int d, int G, float *__restrict__ P) {
+  extern __shared__ float px_s[];  // PX_WARPS x d centred rows
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float *xr = px_s + (size_t)warp * d;
+  for (int64_t p0 = (int64_t)blockIdx.x * PX_WARPS; p0 < np; p0 += (int64_t)gridDim.x * PX_WARPS) {
+    const int64_t p = p0 + warp;  // np is a multiple of 128: always in range
+    const int a = tref[p / BN];
+    const bool real = perm[p] >= 0;
+    const float *ma = refs + (int64_t)a * d;
+    __syncthreads();
+    double xa = 0.0;  // x'.m_a
+    for (int k = lane; k < d; k += 32) {
+      const float v = real ? __fsub_rn(xs[p * d + k], ma[k]) : 0.f;
+      xr[k] = v;
+      xa = fma((double)v, (double)ma[k], xa);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) xa += __shfl_xor_sync(0xffffffffu, xa, o);
+    __syncwarp();
+    for (int g = 0; g < G; ++g) {
+      float out = 0.f;
+      if (g != a && real) {
+        const float *mg = refs + (int64_t)g * d;
+        double acc = 0.0;
+        for (int k = lane; k < d; k += 32) acc = fma((double)xr[k], (double)mg[k], acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        out = (float)(acc - xa);
+      }
+      if (lane == 0) P[p * G + g] = out;
+    }
+  }
+}
+
+// D2[a][b] = |m_b - m_a|^2 (float64), warp per pair
+__global__ void ref_dist_kernel(const float *__restrict__ refs, int G, int d,
+                                double *__restrict__ D2) {
+  const int lane = threadIdx.x & 31;
+  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < G * G;
+       e += (gridDim.x * blockDim.x) >> 5) {
+    const int a = e / G, b = e - a * G;
+    double acc = 0.0;
+    for (int k = lane; k < d; k += 32) {
+      const double v = (double)refs[(int64_t)b * d + k] - (double)refs[(int64_t)a * d + k];
+      acc = fma(v, v, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) D2[e] = acc;
+  }
+}
+
+// pass-1 K-th keys of the SIMT kernel (original row order, relative error
+// gamma) -> per sorted row upper bounds
+__global__ void tau_from_keys_kernel(const uint64_t *__restrict__ keys1, int K,
+                                     const int32_t *__restrict__ perm, int64_t np, double inflate,
+                                     float *__restrict__ tau) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t o = perm[p];
+    float t = TAU_MAX;
+    if (o >= 0) {
+      const uint64_t k = keys1[(int64_t)o * K + K - 1];
+      if (k != KEY_MAX) t = fminf(__double2float_ru((double)key_dist(k) * inflate), TAU_MAX);
+    }
+    tau[p] = t;
+  }
+}
+
+// U_Q = max over the tile's real rows of the pass-1 bounds (as a distance,
+// like tile_ubound_kernel)
+__global__ void tile_umax_kernel(const float *__restrict__ tau, const int32_t *__restrict__ perm,
+                                 int64_t T, double *__restrict__ U) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t Q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; Q < T;
+       Q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    float m = 0.f;
+    for (int i = lane; i < BN; i += 32)
+      if (perm[Q * BN + i] >= 0) m = fmaxf(m, tau[Q * BN + i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) U[Q] = m >= TAU_MAX ? 1e150 : sqrt((double)m) * (1.0 + 1e-9) + 1e-9;
+  }
+}
+
+struct Layout {
+  __nv_bfloat16 *H;
+  float *refs, *P, *nlo, *nhi, *na, *tau, *rtau, *mind;
+  double *D2;
+  int32_t *tref, *row_cnt, *sched;
+  unsigned long long *pick;
+  uint64_t *bufs;
+  size_t bytes;
+  int dp;
+};
+
+static Layout layout(void *ws, size_t bytes, int64_t np, int64_t T, int64_t d) {
+  Layout L{};
+  Carve c(ws, bytes);
+  L.dp = (int)((d + KBLK - 1) / KBLK * KBLK);
+  L.H = c.take<__nv_bfloat16>((size_t)np * 2 * L.dp);
+  L.refs = c.take<float>((size_t)GMAX * d);
+  L.P = c.take<float>((size_t)np * GMAX);
+  L.nlo = c.take<float>(np);
+  L.nhi = c.take<float>(np);
+  L.na = c.take<float>(np);
+  L.tau = c.take<float>(np);
+  L.rtau = c.take<float>(np);
+  L.mind = c.take<float>(T);
+  L.D2 = c.take<double>((size_t)GMAX * GMAX);
+  L.tref = c.take<int32_t>(T);
+  L.row_cnt = c.take<int32_t>(np);
+  L.sched = c.take<int32_t>(4);
+  L.pick = c.take<unsigned long long>(GMAX + 1);
+  L.bufs = c.take<uint64_t>((size_t)np * CAP);
+  L.bytes = c.off;
+  return L;
+}
+
+}  // namespace tcf
+
+bool tcf32_supported(int64_t d, int64_t k) {
+  static int env = -1;
+  if (env < 0) {
+    const char *e = getenv("PGK_F32_TC");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env && d >= 64 && d <= 8192 && k >= 2 && k <= 384;
+}
+
+size_t tcf32_workspace(int64_t np, int64_t T, int64_t d) {
+  return tcf::layout(nullptr, 0, np, T, d).bytes;
+}
+
+// References, centred bf16 operands, cross-term table (once per build; np
+// tile-sorted rows xs with centroids cent / sizes of the T tiles).
+int tcf32_prepare(const float *xs, const int32_t *perm, const float *cent, const int32_t *size,
+                  int64_t np, int64_t T, int d, void *ws, size_t bytes, cudaStream_t stream) {
+  using namespace tcf;
+  Layout L = layout(ws, bytes, np, T, d);
+  if (L.bytes > bytes) {
+    set_error("float tensor-core pool workspace too small");
+    return PGK_ERR_NOMEM;
+  }
+  const int sms = num_sms();
+  const int G = (int)std::min<int64_t>(GMAX, T);
+  PGK_CUDA(cudaMemsetAsync(L.pick, 0, (GMAX + 1) * sizeof(unsigned long long), stream));
+  for (int g = 0; g < G; ++g) {
+    kcenter_step_kernel<<<(unsigned)sms * 2, 256, 0, stream>>>(
+        cent, size, T, d, g, g ? L.pick + g - 1 : nullptr, L.pick + g, L.mind, L.tref, L.refs);
+    PGK_CHECK_LAUNCH("kcenter_step_kernel");
+  }
+  ref_dist_kernel<<<(unsigned)sms * 2, 256, 0, stream>>>(L.refs, G, d, L.D2);
+  PGK_CHECK_LAUNCH("ref_dist_kernel");
+  f32_split_kernel<<<(unsigned)sms * 16, 256, 0, stream>>>(xs, perm, L.tref, L.refs, np, d, L.dp,
+                                                          L.H, L.nlo, L.nhi, L.na);
+  PGK_CHECK_LAUNCH("f32_split_kernel");
+  const size_t psm = (size_t)PX_WARPS * d * sizeof(float);
+  PGK_CUDA(ensure_smem((const void *)f32_cross_kernel, psm));
+  f32_cross_kernel<<<(unsigned)sms * 4, PX_WARPS * 32, psm, stream>>>(xs, perm, L.tref, L.refs, np,
+                                                                     d, G, L.P);
+  PGK_CHECK_LAUNCH("f32_cross_kernel");
+  return PGK_OK;
+}
+
+// Row thresholds of pass 2 from the SIMT pass-1 keys (original order).
+int tcf32_tau_from_keys(const uint64_t *keys1, int K, const int32_t *perm, int64_t np, int64_t T,
+                        int d, double inflate, void *ws, size_t bytes, cudaStream_t stream) {
+  using namespace tcf;
+  Layout L = layout(ws, bytes, np, T, d);
+  tau_from_keys_kernel<<<(unsigned)num_sms() * 4, 256, 0, stream>>>(keys1, K, perm, np, inflate,
+                                                                   L.tau);
+  PGK_CHECK_LAUNCH("tau_from_keys_kernel");
+  return PGK_OK;
+}
+
+// One pass over the tile lists.  ub = 1: pass 1 (upper bounds; the row
+// thresholds land in the workspace and, as tile maxima, in U).  ub = 0: pass 2
+// (the S smallest lower-bound keys per row into keys, original order).
+int tcf32_pass(int64_t np, int64_t T, int d, const int32_t *perm, const int32_t *tlist,
+               const int32_t *tlen, int64_t tstride, int K, int ub, double *U, uint64_t *keys,
+               void *ws, size_t bytes, cudaStream_t stream) {
+  using namespace tcf;
+  Layout L = layout(ws, bytes, np, T, d);
+  const int sms = num_sms();
+  CUtensorMap tmH;
+  if (!make_bf16_tile_map(&tmH, L.H, np, 2 * (int64_t)L.dp)) {
+    set_error("cuTensorMapEncodeTiled failed (bf16 tile map)");
+    return PGK_ERR_CUDA;
+  }
+  Args a{};
+  a.np = np;
+  a.dp = L.dp;
+  a.nkb = L.dp / KBLK;
+  a.G = (int)std::min<int64_t>(GMAX, T);
+  a.K = K;
+  // pair slack: 2 x (dropped operand terms + truncating fp32 accumulation of
+  // 3 dp products) + the 2 a b share of the storage rounding
+  a.kappa = (float)(2.0 * (3.1 / 262144.0 + 4.0 * (L.dp + 16) / 8388608.0) + 1.0 / 2097152.0);
+  a.tlist = tlist;
+  a.tlen = tlen;
+  a.tstride = tstride;
+  a.perm = perm;
+  a.tref = L.tref;
+  a.P = L.P;
+  a.D2 = L.D2;
+  a.nbnd = ub ? L.nhi : L.nlo;
+  a.na = L.na;
+  a.tau_in = ub ? nullptr : L.tau;
+  a.bufs = L.bufs;
+  a.row_cnt = L.row_cnt;
+  a.row_tau = L.rtau;
+  a.sched = L.sched;
+  PGK_CUDA(cudaMemsetAsync(L.sched, 0, sizeof(int32_t), stream));
+  const size_t smem = sizeof(Smem) + 1024;
+  PGK_CUDA(ensure_smem((const void *)tc_pool_f32_kernel<false>, smem));
+  PGK_CUDA(ensure_smem((const void *)tc_pool_f32_kernel<true>, smem));
+  const unsigned grid = (unsigned)std::min<int64_t>(np / BM, (int64_t)sms);
+  if (ub)
+    tc_pool_f32_kernel<true><<<grid, THREADS, smem, stream>>>(tmH, a);
+  else
+    tc_pool_f32_kernel<false><<<grid, THREADS, smem, stream>>>(tmH, a);
+  PGK_CHECK_LAUNCH("tc_pool_f32_kernel");
+  const unsigned fgrid = (unsigned)std::min<int64_t>((np + FIN_WARPS - 1) / FIN_WARPS,
+                                                     (int64_t)sms * 8);
+  f32_select_kernel<<<fgrid, FIN_WARPS * 32, 0, stream>>>(L.bufs, L.row_cnt, perm, np, K,
+                                                         ub ? L.tau : nullptr, ub ? nullptr : keys);
+  PGK_CHECK_LAUNCH("f32_select_kernel");
+  if (ub && U) {
+    tile_umax_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(L.tau, perm, T, U);
+    PGK_CHECK_LAUNCH("tile_umax_kernel");
+  }
+  return PGK_OK;
+}
+
+}  // namespace pgk

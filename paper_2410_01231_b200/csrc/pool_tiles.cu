@@ -1186,12 +1186,22 @@ struct LayoutF32 {
   uint64_t *akeys, *keys1;
   double *rad, *U;
   unsigned long long *total;
-  void *sub_ws;
-  size_t sub_bytes, bytes;
+  void *sub_ws, *tcf_ws;
+  size_t sub_bytes, tcf_bytes, bytes;
   int64_t C, NPmax, Tmax;
 };
 
 }  // namespace tiles
+
+bool tcf32_supported(int64_t d, int64_t k);
+size_t tcf32_workspace(int64_t np, int64_t T, int64_t d);
+int tcf32_prepare(const float *xs, const int32_t *perm, const float *cent, const int32_t *size,
+                  int64_t np, int64_t T, int d, void *ws, size_t bytes, cudaStream_t stream);
+int tcf32_tau_from_keys(const uint64_t *keys1, int K, const int32_t *perm, int64_t np, int64_t T,
+                        int d, double inflate, void *ws, size_t bytes, cudaStream_t stream);
+int tcf32_pass(int64_t np, int64_t T, int d, const int32_t *perm, const int32_t *tlist,
+               const int32_t *tlen, int64_t tstride, int K, int ub, double *U, uint64_t *keys,
+               void *ws, size_t bytes, cudaStream_t stream);
 
 static tiles::LayoutF32 tiles_layout_f32(void *ws, size_t bytes, int64_t n, int64_t d,
                                          int64_t K) {
@@ -1228,6 +1238,8 @@ static tiles::LayoutF32 tiles_layout_f32(void *ws, size_t bytes, int64_t n, int6
   L.keys1 = c.take<uint64_t>((size_t)n * K);
   L.sub_bytes = tc_pool_workspace(C, n, false);
   L.sub_ws = c.take<char>(L.sub_bytes);
+  L.tcf_bytes = tcf32_supported(d, K) ? tcf32_workspace(NP, T, d) : 0;
+  L.tcf_ws = L.tcf_bytes ? c.take<char>(L.tcf_bytes) : nullptr;
   L.bytes = c.off;
   return L;
 }
@@ -1253,9 +1265,11 @@ int launch_pool_f32_lists(const float *xs, int64_t np, int d, int S, int vec4,
 // The pruned F32 pool: every row's S best approximate keys in keys (n x S,
 // original order, original ids), for pool_simt.cu's rerank + fallback.
 int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64_t *keys,
-                          void *tws, size_t tws_bytes, cudaStream_t stream, bool *handled) {
+                          void *tws, size_t tws_bytes, cudaStream_t stream, bool *handled,
+                          bool *lb_keys) {
   using namespace tiles;
   *handled = false;
+  *lb_keys = false;
   if (!tiles_f32_supported(n, d, K)) return PGK_OK;
   LayoutF32 L = tiles_layout_f32(tws, tws_bytes, n, d, K);
   if (L.bytes > tws_bytes) {
@@ -1320,20 +1334,53 @@ int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64
   tile_nearest_kernel<<<g, 256, 0, stream>>>(L.dcm, L.size, T, K, L.lists, L.lens, L.total + 1);
   PGK_CHECK_LAUNCH("tile_nearest_kernel");
   dbg_stage("tile_nearest_kernel", stream);
-  rc = launch_pool_f32_lists(L.xs, NP, d, K, vec4, L.lists, L.lens, T, L.perm, L.keys1, stream);
-  if (rc) return rc;
+  // float pools on the tensor cores (pool_tc_f32.cu): centred bf16 operands,
+  // proven bounds.  PGK_F32_TC=1: pass 2 only (SIMT pass 1), 2 (default): both
+  static int tc_mode = -1;
+  if (tc_mode < 0) {
+    const char *e = getenv("PGK_F32_TC");
+    tc_mode = e ? atoi(e) : 2;
+  }
+  const bool use_tc = L.tcf_ws != nullptr && tc_mode > 0;
+  if (use_tc) {
+    rc = tcf32_prepare(L.xs, L.perm, L.cent, L.size, NP, T, d, L.tcf_ws, L.tcf_bytes, stream);
+    if (rc) return rc;
+    dbg_stage("tcf32_prepare", stream);
+  }
   const double gamma = (double)(d + 2) * 5.9604644775390625e-08 * 1.001 + 1e-12;
-  tile_ubound_kernel<<<g, 256, 0, stream>>>(L.keys1, K, L.perm, T, L.U, 1.0 / (1.0 - gamma));
-  PGK_CHECK_LAUNCH("tile_ubound_kernel");
-  dbg_stage("tile_ubound_kernel", stream);
+  if (use_tc && tc_mode >= 2) {
+    rc = tcf32_pass(NP, T, d, L.perm, L.lists, L.lens, T, K, 1, L.U, nullptr, L.tcf_ws,
+                    L.tcf_bytes, stream);
+    if (rc) return rc;
+    dbg_stage("tcf32 pass 1", stream);
+  } else {
+    rc = launch_pool_f32_lists(L.xs, NP, d, K, vec4, L.lists, L.lens, T, L.perm, L.keys1, stream);
+    if (rc) return rc;
+    tile_ubound_kernel<<<g, 256, 0, stream>>>(L.keys1, K, L.perm, T, L.U, 1.0 / (1.0 - gamma));
+    PGK_CHECK_LAUNCH("tile_ubound_kernel");
+    dbg_stage("tile_ubound_kernel", stream);
+    if (use_tc) {
+      rc = tcf32_tau_from_keys(L.keys1, K, L.perm, NP, T, d, 1.0 / (1.0 - gamma), L.tcf_ws,
+                               L.tcf_bytes, stream);
+      if (rc) return rc;
+    }
+  }
   // 5. pass 2: every tile that can hold a pool member; S approximate survivors
   const double dc_margin = std::max(DC_MARGIN, 2.0 * gamma);
   tile_filter_kernel<<<g, 256, 0, stream>>>(L.dcm, L.rad, L.size, L.U, T, L.lists, L.lens,
                                             L.total, dc_margin);
   PGK_CHECK_LAUNCH("tile_filter_kernel");
   dbg_stage("tile_filter_kernel", stream);
-  rc = launch_pool_f32_lists(L.xs, NP, d, S, vec4, L.lists, L.lens, T, L.perm, keys, stream);
-  if (rc) return rc;
+  if (use_tc) {
+    rc = tcf32_pass(NP, T, d, L.perm, L.lists, L.lens, T, S, 0, nullptr, keys, L.tcf_ws,
+                    L.tcf_bytes, stream);
+    if (rc) return rc;
+    *lb_keys = true;
+    dbg_stage("tcf32 pass 2", stream);
+  } else {
+    rc = launch_pool_f32_lists(L.xs, NP, d, S, vec4, L.lists, L.lens, T, L.perm, keys, stream);
+    if (rc) return rc;
+  }
   const char *se = getenv("PGK_TILES_STATS");
   if (se && se[0] == '1') {
     unsigned long long tot[2] = {0, 0};
