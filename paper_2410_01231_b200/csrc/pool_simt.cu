@@ -602,11 +602,23 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
   }
 }
 
-// Exact float64 full scan for rows whose boundary proof failed.  One CTA per
+// Exact float64 scan for rows whose boundary proof failed.  One CTA per
 // listed row: 256 columns per round, survivors of the (d64, id) threshold are
 // appended to a shared buffer that is block-sorted when it could overflow.
+// Without tile lists the scan covers all n rows; with them (the pruned
+// pools) only the row's pass-2 candidate tiles -- every point outside them is
+// farther than the row's K-th neighbour (pool_tiles.cu), so the result is the
+// same exact pool at a fraction of the reads.
 constexpr int FB_THREADS = 256;
 constexpr int FB_CAP = 1024;
+
+struct FbTiles {           // null lists = full scan
+  const int32_t *lists, *lens;
+  int64_t stride;
+  const int32_t *perm;     // tile-sorted position -> original id (-1 = padding)
+  const int32_t *ipos;     // original id -> tile-sorted position
+  const float *xs;         // tile-sorted rows
+};
 
 __global__ void __launch_bounds__(FB_THREADS)
     fallback_kernel(const float *__restrict__ X, int64_t n, int d,
@@ -614,7 +626,7 @@ __global__ void __launch_bounds__(FB_THREADS)
                     const int32_t *__restrict__ fb_list,
                     const int32_t *__restrict__ fb_count,
                     int32_t *__restrict__ gt_ids, int32_t *__restrict__ pool_ids,
-                    float *__restrict__ pool_dists) {
+                    float *__restrict__ pool_dists, const FbTiles ft) {
   __shared__ double s_d[FB_CAP];
   __shared__ int32_t s_id[FB_CAP];
   __shared__ uint64_t s_key[FB_CAP];
@@ -632,21 +644,32 @@ __global__ void __launch_bounds__(FB_THREADS)
       s_tid = 0x7fffffff;
     }
     __syncthreads();
-    for (int64_t c0 = 0; c0 < n; c0 += FB_THREADS) {
+    const int64_t qt = ft.lists ? (int64_t)ft.ipos[r] / 128 : 0;
+    const int64_t ncand = ft.lists ? (int64_t)ft.lens[qt] * 128 : n;
+    for (int64_t c0 = 0; c0 < ncand; c0 += FB_THREADS) {
       const int64_t c = c0 + tid;
       bool pass = false;
       double dd = 0.0;
-      if (c < n && !(exclude_self && c == r)) {
-        dd = sql2_f64(X + c * d, q, d, vec4);
-        pass = dd < s_td || (dd == s_td && (int32_t)c < s_tid);
+      int32_t cid = (int32_t)c;
+      const float *xr = X + c * d;
+      bool valid = c < ncand;
+      if (ft.lists && valid) {
+        const int64_t col = (int64_t)ft.lists[qt * ft.stride + (c >> 7)] * 128 + (c & 127);
+        cid = ft.perm[col];
+        xr = ft.xs + col * d;
+        valid = cid >= 0;
+      }
+      if (valid && !(exclude_self && cid == r)) {
+        dd = sql2_f64(xr, q, d, vec4);
+        pass = dd < s_td || (dd == s_td && cid < s_tid);
       }
       if (pass) {
         int p = atomicAdd(&s_cnt, 1);
         s_d[p] = dd;
-        s_id[p] = (int32_t)c;
+        s_id[p] = cid;
       }
       __syncthreads();
-      if (s_cnt > FB_CAP - FB_THREADS || c0 + FB_THREADS >= n) {
+      if (s_cnt > FB_CAP - FB_THREADS || c0 + FB_THREADS >= ncand) {
         // block bitonic sort of (d, id) pairs, keep K
         const int cnt = s_cnt;
         for (int i = cnt + tid; i < FB_CAP; i += FB_THREADS) {
@@ -709,7 +732,7 @@ bool tiles_f32_supported(int64_t n, int64_t d, int64_t k);
 size_t tiles_f32_workspace(int64_t n, int64_t d, int64_t k);
 int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64_t *keys,
                           void *tws, size_t tws_bytes, cudaStream_t stream, bool *handled,
-                          bool *lb_keys);
+                          bool *lb_keys, FbTiles *ft);
 int tiles_f32_order(void *tws, int64_t n, int64_t d, int64_t k, int32_t *out,
                     cudaStream_t stream);
 int tiles_f32_work(const void *tws, int64_t n, int64_t d, int64_t k, unsigned long long out[4],
@@ -967,10 +990,11 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
     return PGK_OK;
   }
   bool pruned = false, lb_keys = false;
+  FbTiles ft{};
   if (L.tws_f32 && self && exclude_self) {
     // exact tile pruning: S approximate survivors from the candidate tiles only
     rc = launch_pool_tiles_f32(X, n, (int)d, (int)k, S, L.keys, L.tws_f32, L.tws_f32_bytes,
-                               stream, &pruned, &lb_keys);
+                               stream, &pruned, &lb_keys, &ft);
     if (rc) return rc;
     if (pruned) {
       rc = tiles_f32_order(L.tws_f32, n, d, k, L.order, stream);
@@ -1011,9 +1035,9 @@ int knn_pools(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq, 
                                                        pruned ? L.order : nullptr);
     PGK_CHECK_LAUNCH("rerank_kernel");
   }
-  fallback_kernel<<<(unsigned)sms * 2, FB_THREADS, 0, stream>>>(
+  fallback_kernel<<<(unsigned)sms * 8, FB_THREADS, 0, stream>>>(
       X, n, (int)d, Q, exclude_self, (int)k, vec4, L.fb_list, L.fb_count, gt_ids, pool_ids,
-      pool_dists);
+      pool_dists, pruned ? ft : FbTiles{});
   PGK_CHECK_LAUNCH("fallback_kernel");
   return PGK_OK;
 }

@@ -66,7 +66,8 @@ constexpr int CAP = 1024;    // per-row candidate buffer (keys, global memory)
 constexpr int THREADS = 192;
 constexpr int TILE_B = BN * 128;  // bytes of one (128 rows x 64 bf16) operand block
 constexpr int TMEM_COLS = ACC * BN;
-constexpr int GMAX = 128;    // reference vectors
+constexpr int GMAX = 1024;   // reference vectors at most
+constexpr int MW = GMAX / 32;  // words of a per-tile reference bit set
 constexpr float TAU_MAX = 1e29f;   // "no bound yet"
 constexpr float PAD_CX = 1e30f;    // column term of padding slots: never passes
 
@@ -189,11 +190,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int tid = A.tlist[(int64_t)b * A.tstride + t];
           for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(&s.empty[stage], phase ^ 1);
+#ifdef TCF_EXP_NOLO  // timing experiment: half the operand bytes (wrong results)
+            mbar_expect_tx(&s.full[stage], 2 * TILE_B);
+            tma_load_2d(s.st[stage][0], &tmH, &s.full[stage], kb * KBLK, b * BM);
+            tma_load_2d(s.st[stage][2], &tmH, &s.full[stage], kb * KBLK, tid * BN);
+#else
             mbar_expect_tx(&s.full[stage], 4 * TILE_B);
             tma_load_2d(s.st[stage][0], &tmH, &s.full[stage], kb * KBLK, b * BM);
             tma_load_2d(s.st[stage][1], &tmH, &s.full[stage], A.dp + kb * KBLK, b * BM);
             tma_load_2d(s.st[stage][2], &tmH, &s.full[stage], kb * KBLK, tid * BN);
             tma_load_2d(s.st[stage][3], &tmH, &s.full[stage], A.dp + kb * KBLK, tid * BN);
+#endif
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
         }
@@ -222,10 +229,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int kk = 0; kk < KBLK / 16; ++kk)  // K = 16 bf16 = 32 B per MMA
               mma_bf16(dcol, ah + 2 * kk, bh + 2 * kk, IDESC, (kb | kk) != 0);
+#ifndef TCF_EXP_ONEMMA  // timing experiment: one product of three (wrong results)
 #pragma unroll
             for (int kk = 0; kk < KBLK / 16; ++kk) mma_bf16(dcol, ah + 2 * kk, bl + 2 * kk, IDESC, 1);
 #pragma unroll
             for (int kk = 0; kk < KBLK / 16; ++kk) mma_bf16(dcol, al + 2 * kk, bh + 2 * kk, IDESC, 1);
+#endif
             tc_commit(&s.empty[stage]);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
@@ -295,6 +304,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (g % ACC) * BN;
         const int64_t col0 = (int64_t)tid * BN;
+#ifdef TCF_EXP_NOEPI  // timing experiment: no epilogue work (wrong results)
+        if (false)
+#endif
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t r[32];
@@ -510,42 +522,76 @@ __global__ void f32_split_kernel(const float *__restrict__ xs, const int32_t *__
   }
 }
 
-// P[p][g] = x'_p . (m_g - m_ref(p)) in float64 (stored fp32), block per 8 rows
+// Which cross terms a pass reads: the row term of q in Q against tile T needs
+// P[q][ref(T)], the column term of x in T needs P[x][ref(Q)].  need[T] = bit
+// set of the references of every tile paired with T by the lists (MW words).
+__global__ void need_mask_kernel(const int32_t *__restrict__ tlist, const int32_t *__restrict__ tlen,
+                                 int64_t tstride, const int32_t *__restrict__ tref, int64_t T,
+                                 uint32_t *__restrict__ need) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t Q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; Q < T;
+       Q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int len = tlen[Q];
+    const int a = tref[Q];
+    for (int j = lane; j < len; j += 32) {
+      const int t = tlist[Q * tstride + j];
+      const int b = tref[t];
+      if (b != a) {
+        atomicOr(need + Q * MW + (b >> 5), 1u << (b & 31));
+        atomicOr(need + (int64_t)t * MW + (a >> 5), 1u << (a & 31));
+      }
+    }
+  }
+}
+
+__global__ void mask_done_kernel(const uint32_t *__restrict__ need, uint32_t *__restrict__ done,
+                                 int64_t words) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < words;
+       i += (int64_t)gridDim.x * blockDim.x)
+    done[i] |= need[i];
+}
+
+// P[p][g] = x'_p . (m_g - m_ref(p)) in float64 (stored fp32) for the
+// references in need & ~done of the row's tile; block per 8 rows
 constexpr int PX_WARPS = 8;
 __global__ void __launch_bounds__(PX_WARPS * 32)
     f32_cross_kernel(const float *__restrict__ xs, const int32_t *__restrict__ perm,
                      const int32_t *__restrict__ tref, const float *__restrict__ refs,
+                     const uint32_t *__restrict__ need, const uint32_t *__restrict__ done,
                      int64_t np, int d, int G, float *__restrict__ P) {
   extern __shared__ float px_s[];  // PX_WARPS x d centred rows
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float *xr = px_s + (size_t)warp * d;
   for (int64_t p0 = (int64_t)blockIdx.x * PX_WARPS; p0 < np; p0 += (int64_t)gridDim.x * PX_WARPS) {
     const int64_t p = p0 + warp;  // np is a multiple of 128: always in range
-    const int a = tref[p / BN];
-    const bool real = perm[p] >= 0;
+    const int64_t tile = p / BN;
+    bool any = false;
+    for (int w = lane; w < MW; w += 32) any |= (need[tile * MW + w] & ~done[tile * MW + w]) != 0;
+    if (!__any_sync(0xffffffffu, any) || perm[p] < 0) continue;
+    const int a = tref[tile];
     const float *ma = refs + (int64_t)a * d;
-    __syncthreads();
     double xa = 0.0;  // x'.m_a
     for (int k = lane; k < d; k += 32) {
-      const float v = real ? __fsub_rn(xs[p * d + k], ma[k]) : 0.f;
+      const float v = __fsub_rn(xs[p * d + k], ma[k]);
       xr[k] = v;
       xa = fma((double)v, (double)ma[k], xa);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) xa += __shfl_xor_sync(0xffffffffu, xa, o);
     __syncwarp();
-    for (int g = 0; g < G; ++g) {
-      float out = 0.f;
-      if (g != a && real) {
+    for (int w = 0; w < MW; ++w) {
+      for (uint32_t mm = need[tile * MW + w] & ~done[tile * MW + w]; mm; mm &= mm - 1) {
+        const int g = w * 32 + __ffs(mm) - 1;
+        if (g >= G) break;
         const float *mg = refs + (int64_t)g * d;
         double acc = 0.0;
         for (int k = lane; k < d; k += 32) acc = fma((double)xr[k], (double)mg[k], acc);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        out = (float)(acc - xa);
+        if (lane == 0) P[p * G + g] = (float)(acc - xa);
       }
-      if (lane == 0) P[p * G + g] = out;
     }
+    __syncwarp();
   }
 }
 
@@ -605,11 +651,18 @@ struct Layout {
   float *refs, *P, *nlo, *nhi, *na, *tau, *rtau, *mind;
   double *D2;
   int32_t *tref, *row_cnt, *sched;
+  uint32_t *need, *done;
   unsigned long long *pick;
   uint64_t *bufs;
   size_t bytes;
   int dp;
 };
+
+// one reference per ~8 tiles (1,024 points), a multiple of 32 in [32, GMAX]
+static int num_refs(int64_t T) {
+  const int64_t g = std::min<int64_t>(GMAX, std::max<int64_t>(32, (T / 8 + 31) / 32 * 32));
+  return (int)std::min<int64_t>(g, std::max<int64_t>(T, 1));
+}
 
 static Layout layout(void *ws, size_t bytes, int64_t np, int64_t T, int64_t d) {
   Layout L{};
@@ -617,7 +670,7 @@ static Layout layout(void *ws, size_t bytes, int64_t np, int64_t T, int64_t d) {
   L.dp = (int)((d + KBLK - 1) / KBLK * KBLK);
   L.H = c.take<__nv_bfloat16>((size_t)np * 2 * L.dp);
   L.refs = c.take<float>((size_t)GMAX * d);
-  L.P = c.take<float>((size_t)np * GMAX);
+  L.P = c.take<float>((size_t)np * num_refs(T));
   L.nlo = c.take<float>(np);
   L.nhi = c.take<float>(np);
   L.na = c.take<float>(np);
@@ -629,6 +682,8 @@ static Layout layout(void *ws, size_t bytes, int64_t np, int64_t T, int64_t d) {
   L.row_cnt = c.take<int32_t>(np);
   L.sched = c.take<int32_t>(4);
   L.pick = c.take<unsigned long long>(GMAX + 1);
+  L.need = c.take<uint32_t>((size_t)T * MW);
+  L.done = c.take<uint32_t>((size_t)T * MW);
   L.bufs = c.take<uint64_t>((size_t)np * CAP);
   L.bytes = c.off;
   return L;
@@ -660,7 +715,7 @@ int tcf32_prepare(const float *xs, const int32_t *perm, const float *cent, const
     return PGK_ERR_NOMEM;
   }
   const int sms = num_sms();
-  const int G = (int)std::min<int64_t>(GMAX, T);
+  const int G = num_refs(T);
   PGK_CUDA(cudaMemsetAsync(L.pick, 0, (GMAX + 1) * sizeof(unsigned long long), stream));
   for (int g = 0; g < G; ++g) {
     kcenter_step_kernel<<<(unsigned)sms * 2, 256, 0, stream>>>(
@@ -672,11 +727,8 @@ int tcf32_prepare(const float *xs, const int32_t *perm, const float *cent, const
   f32_split_kernel<<<(unsigned)sms * 16, 256, 0, stream>>>(xs, perm, L.tref, L.refs, np, d, L.dp,
                                                           L.H, L.nlo, L.nhi, L.na);
   PGK_CHECK_LAUNCH("f32_split_kernel");
-  const size_t psm = (size_t)PX_WARPS * d * sizeof(float);
-  PGK_CUDA(ensure_smem((const void *)f32_cross_kernel, psm));
-  f32_cross_kernel<<<(unsigned)sms * 4, PX_WARPS * 32, psm, stream>>>(xs, perm, L.tref, L.refs, np,
-                                                                     d, G, L.P);
-  PGK_CHECK_LAUNCH("f32_cross_kernel");
+  PGK_CUDA(cudaMemsetAsync(L.need, 0, (size_t)T * MW * sizeof(uint32_t), stream));
+  PGK_CUDA(cudaMemsetAsync(L.done, 0, (size_t)T * MW * sizeof(uint32_t), stream));
   return PGK_OK;
 }
 
@@ -694,7 +746,7 @@ int tcf32_tau_from_keys(const uint64_t *keys1, int K, const int32_t *perm, int64
 // One pass over the tile lists.  ub = 1: pass 1 (upper bounds; the row
 // thresholds land in the workspace and, as tile maxima, in U).  ub = 0: pass 2
 // (the S smallest lower-bound keys per row into keys, original order).
-int tcf32_pass(int64_t np, int64_t T, int d, const int32_t *perm, const int32_t *tlist,
+int tcf32_pass(const float *xs, int64_t np, int64_t T, int d, const int32_t *perm, const int32_t *tlist,
                const int32_t *tlen, int64_t tstride, int K, int ub, double *U, uint64_t *keys,
                void *ws, size_t bytes, cudaStream_t stream) {
   using namespace tcf;
@@ -709,7 +761,7 @@ int tcf32_pass(int64_t np, int64_t T, int d, const int32_t *perm, const int32_t 
   a.np = np;
   a.dp = L.dp;
   a.nkb = L.dp / KBLK;
-  a.G = (int)std::min<int64_t>(GMAX, T);
+  a.G = num_refs(T);
   a.K = K;
   // pair slack: 2 x (dropped operand terms + truncating fp32 accumulation of
   // 3 dp products) + the 2 a b share of the storage rounding
@@ -729,6 +781,16 @@ int tcf32_pass(int64_t np, int64_t T, int d, const int32_t *perm, const int32_t 
   a.row_tau = L.rtau;
   a.sched = L.sched;
   PGK_CUDA(cudaMemsetAsync(L.sched, 0, sizeof(int32_t), stream));
+  // the cross terms this pass's lists read (those not computed yet)
+  need_mask_kernel<<<(unsigned)sms * 4, 256, 0, stream>>>(tlist, tlen, tstride, L.tref, T, L.need);
+  PGK_CHECK_LAUNCH("need_mask_kernel");
+  const size_t psm = (size_t)PX_WARPS * d * sizeof(float);
+  PGK_CUDA(ensure_smem((const void *)f32_cross_kernel, psm));
+  f32_cross_kernel<<<(unsigned)sms * 4, PX_WARPS * 32, psm, stream>>>(
+      xs, perm, L.tref, L.refs, L.need, L.done, np, d, a.G, L.P);
+  PGK_CHECK_LAUNCH("f32_cross_kernel");
+  mask_done_kernel<<<(unsigned)sms * 2, 256, 0, stream>>>(L.need, L.done, T * MW);
+  PGK_CHECK_LAUNCH("mask_done_kernel");
   const size_t smem = sizeof(Smem) + 1024;
   PGK_CUDA(ensure_smem((const void *)tc_pool_f32_kernel<false>, smem));
   PGK_CUDA(ensure_smem((const void *)tc_pool_f32_kernel<true>, smem));

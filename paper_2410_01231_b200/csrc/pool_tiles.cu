@@ -1199,7 +1199,7 @@ int tcf32_prepare(const float *xs, const int32_t *perm, const float *cent, const
                   int64_t np, int64_t T, int d, void *ws, size_t bytes, cudaStream_t stream);
 int tcf32_tau_from_keys(const uint64_t *keys1, int K, const int32_t *perm, int64_t np, int64_t T,
                         int d, double inflate, void *ws, size_t bytes, cudaStream_t stream);
-int tcf32_pass(int64_t np, int64_t T, int d, const int32_t *perm, const int32_t *tlist,
+int tcf32_pass(const float *xs, int64_t np, int64_t T, int d, const int32_t *perm, const int32_t *tlist,
                const int32_t *tlen, int64_t tstride, int K, int ub, double *U, uint64_t *keys,
                void *ws, size_t bytes, cudaStream_t stream);
 
@@ -1264,9 +1264,26 @@ int launch_pool_f32_lists(const float *xs, int64_t np, int d, int S, int vec4,
 
 // The pruned F32 pool: every row's S best approximate keys in keys (n x S,
 // original order, original ids), for pool_simt.cu's rerank + fallback.
+struct FbTiles {  // pool_simt.cu: the exact rescan's view of the pass-2 lists
+  const int32_t *lists, *lens;
+  int64_t stride;
+  const int32_t *perm, *ipos;
+  const float *xs;
+};
+
+namespace tiles {
+// original id -> tile-sorted position
+__global__ void inverse_perm_kernel(const int32_t *__restrict__ perm, int64_t np,
+                                    int32_t *__restrict__ ipos) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np;
+       p += (int64_t)gridDim.x * blockDim.x)
+    if (perm[p] >= 0) ipos[perm[p]] = (int32_t)p;
+}
+}  // namespace tiles
+
 int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64_t *keys,
                           void *tws, size_t tws_bytes, cudaStream_t stream, bool *handled,
-                          bool *lb_keys) {
+                          bool *lb_keys, FbTiles *ft) {
   using namespace tiles;
   *handled = false;
   *lb_keys = false;
@@ -1349,7 +1366,7 @@ int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64
   }
   const double gamma = (double)(d + 2) * 5.9604644775390625e-08 * 1.001 + 1e-12;
   if (use_tc && tc_mode >= 2) {
-    rc = tcf32_pass(NP, T, d, L.perm, L.lists, L.lens, T, K, 1, L.U, nullptr, L.tcf_ws,
+    rc = tcf32_pass(L.xs, NP, T, d, L.perm, L.lists, L.lens, T, K, 1, L.U, nullptr, L.tcf_ws,
                     L.tcf_bytes, stream);
     if (rc) return rc;
     dbg_stage("tcf32 pass 1", stream);
@@ -1372,7 +1389,7 @@ int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64
   PGK_CHECK_LAUNCH("tile_filter_kernel");
   dbg_stage("tile_filter_kernel", stream);
   if (use_tc) {
-    rc = tcf32_pass(NP, T, d, L.perm, L.lists, L.lens, T, S, 0, nullptr, keys, L.tcf_ws,
+    rc = tcf32_pass(L.xs, NP, T, d, L.perm, L.lists, L.lens, T, S, 0, nullptr, keys, L.tcf_ws,
                     L.tcf_bytes, stream);
     if (rc) return rc;
     *lb_keys = true;
@@ -1410,6 +1427,11 @@ int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64
         (unsigned long long)((n + TB - 1) / TB) * (unsigned long long)((C + TB - 1) / TB), 1ull};
     PGK_CUDA(cudaMemcpyAsync(L.total + 2, rec, sizeof(rec), cudaMemcpyHostToDevice, stream));
   }
+  // the exact rescan of rows whose proof fails reads only their pass-2 tiles
+  // (assign is free after the counting sort: it takes the inverse permutation)
+  inverse_perm_kernel<<<g, 256, 0, stream>>>(L.perm, NP, L.assign);
+  PGK_CHECK_LAUNCH("inverse_perm_kernel");
+  *ft = FbTiles{L.lists, L.lens, T, L.perm, L.assign, L.xs};
   *handled = true;
   return PGK_OK;
 }
