@@ -605,9 +605,9 @@ def parity_live(builder, X, data, cfg: int, mode: int, no_cpu: bool) -> dict:
 
 
 def float_config_run(cfg: int, steps: int) -> dict:
-    """A float configuration (SIMT pools + float64 rerank proof, fp32
-    selection) through RngBuilder.build, device-resident data, CUDA events;
-    a few steps (each takes seconds)."""
+    """A float configuration (tcgen05 bf16x3 pool passes with proven bounds +
+    float64 rerank, fp32 selection) through RngBuilder.build, device-resident
+    data, CUDA events; a few steps (each takes about a second)."""
     import torch
     from paper_2410_01231_b200 import _lib
     from paper_2410_01231_b200.index import RngBuilder
@@ -629,7 +629,8 @@ def float_config_run(cfg: int, steps: int) -> dict:
     t = sum(a.elapsed_time(z) for a, z in ev) / 1e3 / steps
     return {"workload": CONFIG_DESC[cfg], "value": N / t, "unit": UNIT, "ms_per_step": t * 1e3,
             "steps": steps, "warmup": 1, "pool_mode": "f32+f64-rerank",
-            "dtype": "fp32 pools (SIMT) + f64 rerank, fp32 selection"}
+            "dtype": "fp32 data: tcgen05 bf16x3 pool passes (proven bounds) + f64 rerank, "
+                     "fp32 selection"}
 
 
 def main():

@@ -416,13 +416,17 @@ for name, data, K, R in (("cfg1", synth.cfg1(10000), 64, 24), ("cfg3", synth.cfg
 np.savez(sys.argv[1], **out)
 ''' % str(root)
     res = {}
-    for tag, env in (("pruned", {}), ("full", {"PGK_DISABLE_PRUNE": "1"})):
+    # pruned = the default: tensor-core passes (pool_tc_f32.cu) where d >= 64;
+    # tc_pass2 = SIMT pass 1 + tensor-core pass 2; simt = both passes SIMT
+    for tag, env in (("pruned", {}), ("tc_pass2", {"PGK_F32_TC": "1"}),
+                     ("simt", {"PGK_F32_TC": "0"}), ("full", {"PGK_DISABLE_PRUNE": "1"})):
         path = f"/tmp/pgk_f32prune_{tag}.npz"
         subprocess.check_call([sys.executable, "-c", code, path],
                               env=dict(os.environ, **env), timeout=900)
         res[tag] = dict(np.load(path))
-    for k in res["full"]:
-        np.testing.assert_array_equal(res["pruned"][k], res["full"][k], err_msg=k)
+    for tag in ("pruned", "tc_pass2", "simt"):
+        for k in res["full"]:
+            np.testing.assert_array_equal(res[tag][k], res["full"][k], err_msg=f"{tag}:{k}")
 
 
 @pytest.mark.parametrize("cfg,rows", [(3, 300), (4, 150)])
