@@ -13,7 +13,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libpgk.so"
 SOURCES = ["api.cu", "prune.cu", "reverse.cu", "pool_simt.cu", "pool_tc.cu", "pool_tc_f32.cu",
            "pool_tiles.cu",
-           "prune_gram.cu", "search.cu", "nnd.cu"]
+           "prune_gram.cu", "prune_gram_f32.cu", "search.cu", "nnd.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
          "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -380,7 +380,8 @@ __global__ void __launch_bounds__(PRUNE_WARPS * 32, 2)
                  double cos_alpha, int M, int width, int32_t *__restrict__ out_ids,
                  float *__restrict__ out_dists, int32_t *__restrict__ out_counts,
                  int64_t *__restrict__ dist_evals,
-                 int64_t *__restrict__ angle_evals) {
+                 int64_t *__restrict__ angle_evals, const int32_t *__restrict__ n_dev) {
+  if (n_dev) n = *n_dev;  // rows listed on the device (a previous launch)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PruneSmem &sm = *reinterpret_cast<PruneSmem *>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -712,7 +713,8 @@ static int launch_mode(const float *X, const uint8_t *xu8, const int32_t *norms,
                        const int32_t *cand_counts, const int32_t *cand_ids,
                        const float *cand_dists, int strategy, double cos_alpha, int64_t M,
                        int64_t width, int32_t *out_ids, float *out_dists, int32_t *out_counts,
-                       int64_t *dist_evals, int64_t *angle_evals, cudaStream_t stream) {
+                       int64_t *dist_evals, int64_t *angle_evals, cudaStream_t stream,
+                       const int32_t *n_dev = nullptr) {
   const size_t smem = sizeof(PruneSmem);
   int64_t blocks = (n + PRUNE_WARPS - 1) / PRUNE_WARPS;
   const int64_t cap = (int64_t)num_sms() * 2;  // 2 resident blocks per SM (~110 KB smem each)
@@ -721,7 +723,8 @@ static int launch_mode(const float *X, const uint8_t *xu8, const int32_t *norms,
   prune_kernel<MODE><<<(unsigned)blocks, PRUNE_WARPS * 32, smem, stream>>>(
       X, xu8, norms, n, (int)d, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists,
       strategy,
-      cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals);
+      cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals,
+      n_dev);
   PGK_CHECK_LAUNCH("prune_kernel");
   return PGK_OK;
 }
@@ -738,6 +741,15 @@ int launch_prune_gram(const uint8_t *xu8, const int32_t *norms, int64_t n,
                       double cos_alpha, int64_t M, int64_t width, int32_t *out_ids,
                       float *out_dists, int32_t *out_counts, int64_t *dist_evals,
                       int64_t *angle_evals, void *ws, cudaStream_t stream, bool pair);
+
+bool gram_f32_supported(const float *X, int64_t d, int strategy);
+int launch_prune_gram_f32(const float *X, int64_t d, int64_t n, const int32_t *row_node,
+                          const int32_t *row_order, const int64_t *cand_off,
+                          const int32_t *cand_counts, const int32_t *cand_ids,
+                          const float *cand_dists, int strategy, double cos_alpha, int64_t M,
+                          int64_t width, int32_t *out_ids, float *out_dists,
+                          int32_t *out_counts, int64_t *dist_evals, int64_t *angle_evals,
+                          int32_t *long_rows, int32_t *long_count, cudaStream_t stream);
 
 size_t prune_workspace(int64_t n_rows) { return gram_workspace(n_rows); }
 
@@ -758,6 +770,22 @@ int launch_prune(const float *X, const uint8_t *xu8, const int32_t *norms, int64
                      cand_counts, cand_ids, cand_dists,
                      strategy, cos_alpha, M, width, out_ids, out_dists, out_counts, dist_evals,
                      angle_evals, stream);
+  if (ws && ws_bytes >= gram_workspace(n) && gram_f32_supported(X, d, strategy)) {
+    // fp32 rows: the candidate Gram matrix on the tensor cores, exact chains
+    // only for undecided pairs (prune_gram_f32.cu); rows with more than 128
+    // candidates are listed for prune_kernel
+    int32_t *long_count = reinterpret_cast<int32_t *>(ws);
+    int32_t *long_rows = long_count + 32;
+    PGK_CUDA(cudaMemsetAsync(long_count, 0, sizeof(int32_t), stream));
+    int rc = launch_prune_gram_f32(X, d, n, row_node, row_order, cand_off, cand_counts, cand_ids,
+                                   cand_dists, strategy, cos_alpha, M, width, out_ids, out_dists,
+                                   out_counts, dist_evals, angle_evals, long_rows, long_count,
+                                   stream);
+    if (rc) return rc;
+    return launch_mode<1>(X, nullptr, nullptr, n, d, row_node, long_rows, cand_off, cand_counts,
+                          cand_ids, cand_dists, strategy, cos_alpha, M, width, out_ids, out_dists,
+                          out_counts, dist_evals, angle_evals, stream, long_count);
+  }
   if ((d % 4 == 0) && ((uintptr_t)X % 16 == 0))
     return launch_mode<1>(X, nullptr, nullptr, n, d, row_node, row_order, cand_off, cand_counts,
                           cand_ids,

@@ -62,7 +62,7 @@ def prune_batch(X: torch.Tensor, cand_off, cand_counts, cand_ids, cand_dists,
     ids, dists, counts, de, ae = out
     rn = None if row_node is None else _dev(row_node, _I32)
     xu8, norms = (None, None) if u8 is None else u8
-    if ws is None and u8 is not None:
+    if ws is None:  # row lists of the tensor-core selection kernels (u8 and fp32)
         ws = _lib.workspace(prune_workspace_bytes(rows))
     check(_lib.lib().pgk_prune_rows_ex(
         ptr(X), ptr(xu8), ptr(norms), n, d, rows, ptr(rn), ptr(order), ptr(cand_off),
