@@ -47,8 +47,7 @@ using namespace tc;
 
 constexpr int C = 128;        // candidates per point (TMEM lanes)
 constexpr int KBLK = 64;      // dimensions per k-block (128 B of bf16)
-constexpr int STAGES = 2;     // operand ring (hi + lo tiles, 32 KB per stage)
-constexpr int RAW = 3;        // raw fp32 k-block ring (cp.async, 32 KB per slot)
+constexpr int STAGES = 3;     // operand ring (hi + lo tiles, 32 KB per stage)
 constexpr int PW = 8;         // producer warps (16 candidate rows each)
 constexpr int NBUF = 3;       // mask buffers (point k uses k % NBUF)
 constexpr int NG = 3;         // greedy warps (point k goes to warp k % NG)
@@ -62,7 +61,6 @@ constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(C >>
 
 struct __align__(1024) Smem {
   uint8_t tile[STAGES][2][TILE_B];  // [stage][hi / lo], SW128 K-major
-  alignas(16) float raw[RAW][C][KBLK];  // fp32 k-blocks of the candidate rows, as loaded
   alignas(16) float urow[2][DMAX];  // the point's own row, by point parity
   int32_t id[2][C];
   float dist[2][C];
@@ -177,49 +175,49 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp < PW) {
     // ---------------- producers (PW warps) ----------------
-    // Warp w owns candidate rows 16w .. 16w+15.  The raw fp32 k-blocks stream
-    // global -> shared by cp.async (one instruction moves 128 contiguous bytes
-    // of each of 4 rows: lane l takes row 4m + l/8 of the warp, 16-byte chunk
-    // l%8 of the line), two k-blocks ahead of the conversion and across point
-    // boundaries; every thread later converts exactly the pieces it fetched
-    // (cp.async.wait_group is the only synchronisation): centred on u, split
-    // into bf16 hi / lo, stored into the SW128 operand tiles; 4 partial row
-    // norms per thread, reduced over the row's 8 lanes at the end of a point.
+    // Warp w owns candidate rows 16w .. 16w+15.  Per k-block a thread centres
+    // and splits 4 pieces of 8 dimensions: lane l takes 16-byte bf16 chunk
+    // l%4 of each line of rows g + 4*((l/4)%2) + 8*rg (g = l/8, rg = 0, 1), so
+    // one STS.128 of a quarter warp covers two rows whose SW128 positions fall
+    // into disjoint halves of the 128-byte bank span (conflict free), and the
+    // 32-byte global reads of four lanes cover one 128-byte line.  The next
+    // k-block's 8 float4 (the next point's first block at the end of a point)
+    // are in flight while the current one is converted; 4 partial row norms
+    // per thread, reduced over the row's 4 lanes at the end of a point.
     // Metadata pipeline over this CTA's points (i = blockIdx.x + k gridDim.x):
     // the node of point k+2 and the counts / offsets of point k+1 at the top
     // of point k, its candidate ids and own-row slice half way through it.
     const int t = threadIdx.x;
-    const int sub = lane >> 3, ch = lane & 7;
+    const int c16 = lane & 3;
+    const int rl = (lane >> 3) + 4 * ((lane >> 2) & 1);  // row within a group of 8
     const int wrow0 = warp * 16;
     const int d4 = d >> 2;
     const float4 *X4 = reinterpret_cast<const float4 *>(X);
     int stage = 0;
     uint32_t phase = 0;
-    int64_t kp = 0;       // points published by this CTA
-    uint32_t rslot = 0;   // raw-ring slot of the next block to convert
+    int64_t kp = 0;  // points published by this CTA
     const int64_t nb = blockIdx.x < n_rows ? (n_rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     auto rowu = [&](int64_t k) -> int64_t {
       if (k >= nb) return -1;
       const int64_t i = blockIdx.x + k * gridDim.x;
       return row_order ? (int64_t)row_order[i] : i;
     };
-    // raw k-block kb of this thread's 4 rows into ring slot sl (one group)
-    auto issue = [&](const int32_t (&rid)[4], int kb, uint32_t sl) {
+    // k-block kb of this thread's 4 pieces (piece i: row group i/2, line i%2)
+    auto load_kb = [&](const int32_t (&rid)[2], int kb, float4 (&dst)[8]) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int m = j >> 1, line = j & 1;
-        const int e4 = kb * 16 + line * 8 + ch;
-        const bool ok = rid[m] >= 0 && e4 < d4;
-        float *dst = &s.raw[sl][wrow0 + 4 * m + sub][line * 32 + ch * 4];
-        cp_async16_zfill(dst, X4 + (ok ? (int64_t)rid[m] * d4 + e4 : 0), ok ? 16u : 0u);
+      for (int i = 0; i < 4; ++i) {
+        const int e4 = kb * 16 + (i & 1) * 8 + c16 * 2;
+        const float4 *src = X4 + (int64_t)(rid[i >> 1] < 0 ? 0 : rid[i >> 1]) * d4 + e4;
+        const bool ok = rid[i >> 1] >= 0;
+        dst[2 * i] = (ok && e4 < d4) ? __ldg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+        dst[2 * i + 1] = (ok && e4 + 1 < d4) ? __ldg(src + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    auto load_ids = [&](int64_t off, int cnt, int32_t (&rid)[4]) {
+    auto load_ids = [&](int64_t off, int cnt, int32_t (&rid)[2]) {
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int r = wrow0 + 4 * m + sub;
-        rid[m] = r < cnt ? cand_ids[off + r] : -1;
+      for (int g = 0; g < 2; ++g) {
+        const int r = wrow0 + 8 * g + rl;
+        rid[g] = r < cnt ? cand_ids[off + r] : -1;
       }
     };
     int64_t u0 = rowu(0), u1 = rowu(1);
@@ -227,8 +225,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     int64_t off0 = 0, off1 = 0;
     int32_t self0 = 0, self1 = 0, cid0 = -1, cid1 = -1;
     float dist0 = __int_as_float(0x7f800000), dist1 = dist0;
-    int32_t rid0[4] = {-1, -1, -1, -1}, rid1[4] = {-1, -1, -1, -1};
+    int32_t rid0[2] = {-1, -1}, rid1[2] = {-1, -1};
     float4 us0 = make_float4(0.f, 0.f, 0.f, 0.f), us1 = us0;  // own-row slice (d4 <= 256)
+    float4 xn[8];
     if (u0 >= 0) {
       cnt0 = cand_counts[u0];
       off0 = cand_off[u0];
@@ -242,10 +241,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (t < d4) us0 = __ldg(X4 + (int64_t)self0 * d4 + t);
       }
     }
-    // two blocks in flight ahead of the conversion, from here on
-    issue(rid0, 0, 0);
-    issue(rid0, 1, 1);
-    uint32_t islot = 2;  // raw-ring slot of the next block to issue
+    load_kb(rid0, 0, xn);
     for (int64_t k = 0; k < nb; ++k) {
       const int64_t u2 = rowu(k + 2);
       cnt1 = -1;
@@ -259,8 +255,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       bool have1 = false;
       auto fetch1 = [&]() {  // the second half of point k+1's metadata
         have1 = true;
-#pragma unroll
-        for (int m = 0; m < 4; ++m) rid1[m] = -1;
+        rid1[0] = rid1[1] = -1;
         us1 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (cnt1 >= 0 && cnt1 <= C) {
           if (t < cnt1) {
@@ -271,14 +266,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (t < d4) us1 = __ldg(X4 + (int64_t)self1 * d4 + t);
         }
       };
-      if (cnt0 > C) {  // hub row: left to prune_kernel (its two empty blocks are skipped)
+      if (cnt0 > C) {  // hub row: left to prune_kernel
         if (t == 0) long_rows[atomicAdd(long_count, 1)] = (int32_t)u0;
         fetch1();
-        issue(rid1, 0, islot);
-        islot = islot + 1 == RAW ? 0 : islot + 1;
-        issue(rid1, 1, islot);
-        islot = islot + 1 == RAW ? 0 : islot + 1;
-        rslot = (rslot + 2) % RAW;
+        load_kb(rid1, 0, xn);
       } else {
         const int par = (int)(kp & 1);
         GFWAIT(0, mbar_wait(&s.pempty[par], (uint32_t)(((kp >> 1) & 1) ^ 1)));
@@ -294,63 +285,64 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (t < nkb * (KBLK / 4)) reinterpret_cast<float4 *>(s.urow[par])[t] = us0;
         named_bar_sync(2, PW * 32);
         const bool wact = wrow0 < cnt0;  // this warp has rows
-        float nacc[4] = {0.f, 0.f, 0.f, 0.f};
+        float nacc[2] = {0.f, 0.f};
         for (int kb = 0; kb < nkb; ++kb) {
-          // keep two blocks in flight: this point's kb+2, or the next point's
-          if (kb + 2 < nkb) {
-            issue(rid0, kb + 2, islot);
-          } else {
+          float4 xv[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) xv[j] = xn[j];
+          if (kb + 1 < nkb) {
+            if (wact) load_kb(rid0, kb + 1, xn);
+          } else {  // the next point's first k-block
             if (!have1) fetch1();
-            issue(rid1, kb + 2 - nkb, islot);
+            load_kb(rid1, 0, xn);
           }
-          islot = islot + 1 == RAW ? 0 : islot + 1;
           if (kb == (nkb >> 1) - 1 && !have1) fetch1();
-          asm volatile("cp.async.wait_group 2;" ::: "memory");
           GFWAIT(1, mbar_wait(&s.empty[stage], phase ^ 1));
           if (t == 0) s.stage_end[stage] = 0;
           if (wact) {
             const float4 *us = reinterpret_cast<const float4 *>(s.urow[par] + kb * KBLK);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const int m = j >> 1, line = j & 1;
-              if (rid0[m] < 0) continue;
-              const int r = wrow0 + 4 * m + sub;
-              const float4 xv =
-                  *reinterpret_cast<const float4 *>(&s.raw[rslot][r][line * 32 + ch * 4]);
-              const float4 ua = us[line * 8 + ch];
-              const float v0 = __fsub_rn(xv.x, ua.x), v1 = __fsub_rn(xv.y, ua.y),
-                          v2 = __fsub_rn(xv.z, ua.z), v3 = __fsub_rn(xv.w, ua.w);
-              nacc[m] = fmaf(v0, v0, nacc[m]);
-              nacc[m] = fmaf(v1, v1, nacc[m]);
-              nacc[m] = fmaf(v2, v2, nacc[m]);
-              nacc[m] = fmaf(v3, v3, nacc[m]);
-              const uint32_t h0 = pack_bf16x2(v0, v1), h1 = pack_bf16x2(v2, v3);
-              const uint32_t l0 = pack_bf16x2(__fsub_rn(v0, __uint_as_float(h0 << 16)),
-                                              __fsub_rn(v1, __uint_as_float(h0 & 0xffff0000u)));
-              const uint32_t l1 = pack_bf16x2(__fsub_rn(v2, __uint_as_float(h1 << 16)),
-                                              __fsub_rn(v3, __uint_as_float(h1 & 0xffff0000u)));
-              // 16-byte chunk line*4 + ch/2 of tile row r, its half ch%2
+            for (int i = 0; i < 4; ++i) {
+              const int g = i >> 1, line = i & 1;
+              if (rid0[g] < 0) continue;
+              const int r = wrow0 + 8 * g + rl;
+              const float4 ua = us[line * 8 + c16 * 2], ub = us[line * 8 + c16 * 2 + 1];
+              const float4 xa = xv[2 * i], xb = xv[2 * i + 1];
+              const float v[8] = {__fsub_rn(xa.x, ua.x), __fsub_rn(xa.y, ua.y),
+                                  __fsub_rn(xa.z, ua.z), __fsub_rn(xa.w, ua.w),
+                                  __fsub_rn(xb.x, ub.x), __fsub_rn(xb.y, ub.y),
+                                  __fsub_rn(xb.z, ub.z), __fsub_rn(xb.w, ub.w)};
+              uint32_t hw[4], lw[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float a = v[2 * e], b = v[2 * e + 1];
+                nacc[g] = fmaf(a, a, nacc[g]);
+                nacc[g] = fmaf(b, b, nacc[g]);
+                hw[e] = pack_bf16x2(a, b);
+                lw[e] = pack_bf16x2(__fsub_rn(a, __uint_as_float(hw[e] << 16)),
+                                    __fsub_rn(b, __uint_as_float(hw[e] & 0xffff0000u)));
+              }
+              // 16-byte chunk line*4 + c16 of tile row r
               const uint32_t pos = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128) +
-                                   ((((uint32_t)(line * 4 + (ch >> 1))) ^ (uint32_t)(r & 7)) << 4) +
-                                   (uint32_t)((ch & 1) * 8);
-              *reinterpret_cast<uint2 *>(s.tile[stage][0] + pos) = make_uint2(h0, h1);
-              *reinterpret_cast<uint2 *>(s.tile[stage][1] + pos) = make_uint2(l0, l1);
+                                   ((((uint32_t)(line * 4 + c16)) ^ (uint32_t)(r & 7)) << 4);
+              *reinterpret_cast<uint4 *>(s.tile[stage][0] + pos) =
+                  make_uint4(hw[0], hw[1], hw[2], hw[3]);
+              *reinterpret_cast<uint4 *>(s.tile[stage][1] + pos) =
+                  make_uint4(lw[0], lw[1], lw[2], lw[3]);
             }
           }
-          rslot = rslot + 1 == RAW ? 0 : rslot + 1;
           fence_proxy_async_smem();  // generic-proxy smem writes -> tensor-core reads
           __syncwarp();
           if (lane == 0) mbar_arrive(&s.full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        // row norms: the 8 lanes of a row's group hold its partial sums
+        // row norms: the 4 lanes of a row hold its partial sums
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          float v = nacc[m];
+        for (int g = 0; g < 2; ++g) {
+          float v = nacc[g];
           v += __shfl_xor_sync(0xffffffffu, v, 1);
           v += __shfl_xor_sync(0xffffffffu, v, 2);
-          v += __shfl_xor_sync(0xffffffffu, v, 4);
-          if (ch == 0) s.nrm[par][wrow0 + 4 * m + sub] = v;
+          if (c16 == 0) s.nrm[par][wrow0 + 8 * g + rl] = v;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&s.pfull[par]);
@@ -358,11 +350,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       u0 = u1; cnt0 = cnt1; off0 = off1; self0 = self1; cid0 = cid1; dist0 = dist1;
       us0 = us1;
-#pragma unroll
-      for (int m = 0; m < 4; ++m) rid0[m] = rid1[m];
+      rid0[0] = rid1[0];
+      rid0[1] = rid1[1];
       u1 = u2;
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
     // end of stream: one sentinel stage for the MMA warp, one sentinel point
     // for the mask warps
     GFWAIT(1, mbar_wait(&s.empty[stage], phase ^ 1));

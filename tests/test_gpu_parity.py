@@ -651,3 +651,63 @@ def test_build_host_stream_equals_device_builds():
         X = torch.from_numpy(x).cuda()
         ref = RngBuilder(n, 128, 64, PruneParams(M=24), pool_mode(X)).build(X)
         assert torch.equal(h_ids, ref.ids.cpu()) and torch.equal(h_cnt, ref.counts.cpu())
+
+
+def _lattice_float(n, d, seed):
+    """Integer-valued float data above the exact-integer range (values up to
+    1000): distance ties and exact duplicates everywhere, so many pair tests
+    sit exactly on their threshold."""
+    rng = np.random.default_rng(seed)
+    base = rng.integers(0, 4, size=(n, d)).astype(np.float32) * 250.0
+    base[n // 2:] = base[: n - n // 2]          # every row has an exact duplicate
+    base[: n // 8, 0] += 1.0                    # ... some of them one step apart
+    return np.ascontiguousarray(base)
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "lattice"])
+def test_gram_f32_selection_against_oracle(name):
+    """The tensor-core float selection (prune_gram_f32.cu: bf16 hi/lo Gram on
+    rows centred on the point, proven pair classification, float64 / exact
+    fp32 chains for undecided pairs) equals the oracle's phases A and B, ids,
+    dists, degrees and dist_evals, for rng and the slack rule; the lattice
+    data put most pair tests exactly on their threshold (zero distances,
+    F == dv ties), which forces the exact-chain path."""
+    if name == "cfg3":
+        data, K, R = synth.cfg3(5000), 128, 32
+    elif name == "cfg4":
+        data, K, R = synth.cfg4(4000), 120, 32
+    else:
+        data, K, R = _lattice_float(3000, 128, 5), 96, 24
+    ds = Dataset.from_array(data)
+    ids, dists = knn_pools(ds, K)
+    o_ids, o_dists = oracle.knn_pools(data, K)
+    np.testing.assert_array_equal(ids, o_ids)
+    off = np.arange(ds.n + 1, dtype=np.int64) * K
+    cnt = np.full(ds.n, K, np.int32)
+    for strategy, s in (("rng", 60.0), ("slack", 1.2)):
+        p = PruneParams(M=R, alpha=s, strategy=strategy)
+        a = prune_all(ds, off, cnt, ids.ravel(), dists.ravel(), p)
+        b = add_reverse_and_prune(ds, a[0], a[1], a[2], p)
+        oa = oracle.prune_all(data, off, cnt, ids.ravel(), dists.ravel(), R, strategy, s)
+        ob = oracle.add_reverse_and_prune(data, oa[0], oa[1], oa[2], R, strategy, s)
+        for res, ref in ((a, oa), (b, ob)):
+            for i in range(3):
+                np.testing.assert_array_equal(res[i], ref[i], err_msg=f"{name} {strategy} [{i}]")
+            assert res[3] == ref[3], (name, strategy)
+
+
+def test_gram_f32_equals_prune_kernel_on_larger_prefixes():
+    """PGK_GRAM_F32=0 (per-warp prune_kernel) and the default tensor-core
+    selection give identical phases A and B, counters included, on 60k-row
+    prefixes of configs 3 and 4 (fresh processes: the switch is read once)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    for cfg, k in ((3, 0), (4, 128)):
+        out = subprocess.run([sys.executable, str(root / "tools" / "gram_f32_check.py"), "--config",
+                              str(cfg), "--n", "60000", "--k", str(k), "--reps", "1"],
+                             capture_output=True, text=True, timeout=1200, check=True).stdout
+        cmp_line = [json.loads(l) for l in out.splitlines() if l.startswith('{"compare"')]
+        assert cmp_line and all(v == 0 for v in cmp_line[0]["differing_entries"].values()), out
