@@ -380,8 +380,7 @@ __global__ void __launch_bounds__(PRUNE_WARPS * 32, 2)
                  double cos_alpha, int M, int width, int32_t *__restrict__ out_ids,
                  float *__restrict__ out_dists, int32_t *__restrict__ out_counts,
                  int64_t *__restrict__ dist_evals,
-                 int64_t *__restrict__ angle_evals, const int32_t *__restrict__ n_dev) {
-  if (n_dev) n = *n_dev;  // rows listed on the device (a previous launch)
+                 int64_t *__restrict__ angle_evals, int min_cnt) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PruneSmem &sm = *reinterpret_cast<PruneSmem *>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -395,8 +394,9 @@ __global__ void __launch_bounds__(PRUNE_WARPS * 32, 2)
   for (int64_t i = (int64_t)blockIdx.x * PRUNE_WARPS + warp; i < n;
        i += (int64_t)gridDim.x * PRUNE_WARPS) {
     const int64_t u = row_order ? row_order[i] : i;
-    const int64_t base = cand_off[u];
     const int cnt = cand_counts[u];
+    if (cnt <= min_cnt) continue;  // rows the tensor-core kernel has done
+    const int64_t base = cand_off[u];
     const int32_t self = row_node ? row_node[u] : (int32_t)u;
     int32_t *orow = out_ids + u * width;
     float *odrow = out_dists + u * width;
@@ -586,8 +586,8 @@ __global__ void __launch_bounds__(U8_WARPS * 32, 1)
   for (int64_t i = (int64_t)blockIdx.x * U8_WARPS + warp; i < n;
        i += (int64_t)gridDim.x * U8_WARPS) {
     const int64_t u = row_order ? row_order[i] : i;
-    const int64_t base = cand_off[u];
     const int cnt = cand_counts[u];
+    const int64_t base = cand_off[u];
     const int32_t self = row_node ? row_node[u] : (int32_t)u;
     int32_t *orow = out_ids + u * width;
     float *odrow = out_dists + u * width;
@@ -714,7 +714,7 @@ static int launch_mode(const float *X, const uint8_t *xu8, const int32_t *norms,
                        const float *cand_dists, int strategy, double cos_alpha, int64_t M,
                        int64_t width, int32_t *out_ids, float *out_dists, int32_t *out_counts,
                        int64_t *dist_evals, int64_t *angle_evals, cudaStream_t stream,
-                       const int32_t *n_dev = nullptr) {
+                       int min_cnt = -1) {
   const size_t smem = sizeof(PruneSmem);
   int64_t blocks = (n + PRUNE_WARPS - 1) / PRUNE_WARPS;
   const int64_t cap = (int64_t)num_sms() * 2;  // 2 resident blocks per SM (~110 KB smem each)
@@ -724,7 +724,7 @@ static int launch_mode(const float *X, const uint8_t *xu8, const int32_t *norms,
       X, xu8, norms, n, (int)d, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists,
       strategy,
       cos_alpha, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals, angle_evals,
-      n_dev);
+      min_cnt);
   PGK_CHECK_LAUNCH("prune_kernel");
   return PGK_OK;
 }
@@ -749,7 +749,7 @@ int launch_prune_gram_f32(const float *X, int64_t d, int64_t n, const int32_t *r
                           const float *cand_dists, int strategy, double cos_alpha, int64_t M,
                           int64_t width, int32_t *out_ids, float *out_dists,
                           int32_t *out_counts, int64_t *dist_evals, int64_t *angle_evals,
-                          int32_t *long_rows, int32_t *long_count, cudaStream_t stream);
+                          cudaStream_t stream);
 
 size_t prune_workspace(int64_t n_rows) { return gram_workspace(n_rows); }
 
@@ -773,18 +773,15 @@ int launch_prune(const float *X, const uint8_t *xu8, const int32_t *norms, int64
   if (ws && ws_bytes >= gram_workspace(n) && gram_f32_supported(X, d, strategy)) {
     // fp32 rows: the candidate Gram matrix on the tensor cores, exact chains
     // only for undecided pairs (prune_gram_f32.cu); rows with more than 128
-    // candidates are listed for prune_kernel
-    int32_t *long_count = reinterpret_cast<int32_t *>(ws);
-    int32_t *long_rows = long_count + 32;
-    PGK_CUDA(cudaMemsetAsync(long_count, 0, sizeof(int32_t), stream));
+    // candidates are skipped there and taken by prune_kernel, in the same
+    // (locality) order
     int rc = launch_prune_gram_f32(X, d, n, row_node, row_order, cand_off, cand_counts, cand_ids,
                                    cand_dists, strategy, cos_alpha, M, width, out_ids, out_dists,
-                                   out_counts, dist_evals, angle_evals, long_rows, long_count,
-                                   stream);
+                                   out_counts, dist_evals, angle_evals, stream);
     if (rc) return rc;
-    return launch_mode<1>(X, nullptr, nullptr, n, d, row_node, long_rows, cand_off, cand_counts,
+    return launch_mode<1>(X, nullptr, nullptr, n, d, row_node, row_order, cand_off, cand_counts,
                           cand_ids, cand_dists, strategy, cos_alpha, M, width, out_ids, out_dists,
-                          out_counts, dist_evals, angle_evals, stream, long_count);
+                          out_counts, dist_evals, angle_evals, stream, 128);
   }
   if ((d % 4 == 0) && ((uintptr_t)X % 16 == 0))
     return launch_mode<1>(X, nullptr, nullptr, n, d, row_node, row_order, cand_off, cand_counts,

@@ -98,6 +98,14 @@ struct __align__(1024) Smem {
   uint32_t tmem_base;
 };
 
+#ifndef GRAM_SLEEP
+#define GRAM_SLEEP 0  // ns between polls of the roles waiting on the gather stream (0: spin)
+#endif
+#if GRAM_SLEEP > 0
+#define GRAM_IDLE_WAIT(bar, par) mbar_wait_sleep(bar, par, GRAM_SLEEP)
+#else
+#define GRAM_IDLE_WAIT(bar, par) mbar_wait(bar, par)
+#endif
 #ifndef GRAM_STATS
 #define GRAM_STATS 0
 #endif
@@ -408,7 +416,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       int stage = 0, acc = 0;
       uint32_t phase = 0, tphase = 0;
       for (;;) {
-        GWAIT(1, mbar_wait(&s.full[stage], phase));
+        GWAIT(1, GRAM_IDLE_WAIT(&s.full[stage], phase));
         if (s.cnt[stage][0] < 0) break;
         fence_proxy_async_smem();  // generic-proxy smem writes -> tensor-core reads
         GWAIT(2, mbar_wait(&s.tempty[acc], tphase ^ 1));
@@ -438,7 +446,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       const uint32_t phase = (uint32_t)((k / STAGES) & 1);
       const int mb = (int)(k % NBUF);  // greedy buffer of point k
       const uint32_t mphase = (uint32_t)((k / NBUF) & 1);
-      GWAIT(3, mbar_wait(&s.full[stage], phase));
+      GWAIT(3, GRAM_IDLE_WAIT(&s.full[stage], phase));
       const int cnt0 = s.cnt[stage][0];
       if (cnt0 < 0) {  // end of stream: the first group to see it tells every greedy warp
         // (PAIR: both greedy warps read every buffer, one sentinel serves both)
@@ -579,7 +587,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     const int base = P * PC;            // the slot's first tile row
     for (int64_t k = PAIR ? 0 : gw;; k += PAIR ? 1 : NG) {
       const int mb = (int)(k % NBUF);
-      GWAIT(6, mbar_wait(&s.mfull[mb], (uint32_t)((k / NBUF) & 1)));
+      GWAIT(6, GRAM_IDLE_WAIT(&s.mfull[mb], (uint32_t)((k / NBUF) & 1)));
       if (s.gcnt[mb][0] < 0) break;
       const int64_t u = s.gu[mb][P];
       if (PAIR && u < 0) {  // empty slot (odd point count)

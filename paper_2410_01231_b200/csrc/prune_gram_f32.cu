@@ -29,7 +29,7 @@
 //     counters (popcounts of the final masks) are then exactly the
 //     reference's; about 5 of the ~8,000 pairs of a config-3 point need the
 //     exact chain.
-// Rows with more than 128 candidates are listed for prune_kernel.  rng and
+// Rows with more than 128 candidates are left to prune_kernel.  rng and
 // the slack rule only (the alpha rule's float64 angle stays on prune_kernel).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -137,7 +137,6 @@ __global__ void __launch_bounds__(THREADS, 1)
                           float ee, double gseq, int M, int width, int32_t *__restrict__ out_ids,
                           float *__restrict__ out_dists, int32_t *__restrict__ out_counts,
                           int64_t *__restrict__ dist_evals, int64_t *__restrict__ angle_evals,
-                          int32_t *__restrict__ long_rows, int32_t *__restrict__ long_count,
                           unsigned long long *__restrict__ stats) {
   extern __shared__ uint8_t smem_raw[];
   Smem &s = *reinterpret_cast<Smem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
@@ -266,8 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (t < d4) us1 = __ldg(X4 + (int64_t)self1 * d4 + t);
         }
       };
-      if (cnt0 > C) {  // hub row: left to prune_kernel
-        if (t == 0) long_rows[atomicAdd(long_count, 1)] = (int32_t)u0;
+      if (cnt0 > C) {  // hub row: skipped here, taken by prune_kernel
         fetch1();
         load_kb(rid1, 0, xn);
       } else {
@@ -742,16 +740,15 @@ bool gram_f32_supported(const float *X, int64_t d, int strategy) {
          ((uintptr_t)X % 16 == 0);
 }
 
-// ws: gram_workspace(n) bytes ([0] long-row count, rows from +32).  The rows
-// with more than 128 candidates are listed at long_rows / *long_count for the
-// caller's prune_kernel launch.
+// Rows with more than 128 candidates are skipped (the caller's prune_kernel
+// launch takes exactly those).
 int launch_prune_gram_f32(const float *X, int64_t d, int64_t n, const int32_t *row_node,
                           const int32_t *row_order, const int64_t *cand_off,
                           const int32_t *cand_counts, const int32_t *cand_ids,
                           const float *cand_dists, int strategy, double cos_alpha, int64_t M,
                           int64_t width, int32_t *out_ids, float *out_dists,
                           int32_t *out_counts, int64_t *dist_evals, int64_t *angle_evals,
-                          int32_t *long_rows, int32_t *long_count, cudaStream_t stream) {
+                          cudaStream_t stream) {
   using namespace gramf;
   const int nkb = (int)((d + KBLK - 1) / KBLK);
   const double dp = (double)nkb * KBLK;
@@ -779,7 +776,7 @@ int launch_prune_gram_f32(const float *X, int64_t d, int64_t n, const int32_t *r
   prune_gram_f32_kernel<<<grid, THREADS, smem, stream>>>(
       X, (int)d, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
       cos_alpha, (float)ee, gseq, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals,
-      angle_evals, long_rows, long_count, dstats);
+      angle_evals, dstats);
   PGK_CHECK_LAUNCH("prune_gram_f32_kernel");
   if (stats_env) {
     unsigned long long h[20];
