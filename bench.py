@@ -627,7 +627,26 @@ def float_config_run(cfg: int, steps: int) -> dict:
         e1.record()
     torch.cuda.synchronize()
     t = sum(a.elapsed_time(z) for a, z in ev) / 1e3 / steps
+    # one more pass, stage by stage (the same calls RngBuilder.build makes)
+    from paper_2410_01231_b200 import kernels
+    p = b.params
+    se = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    se[0].record()
+    r = kernels.knn_pools(X, K, None, True, b.mode, False, b.pool_ws, b.pool_out)
+    order = b.order()
+    se[1].record()
+    a = kernels.prune_batch(X, b.cand_off, b.cand_counts, r.pool_ids, r.pool_dists,
+                            p.strategy_code, p.kernel_param, p.M, p.M, out=b.a_out, order=order,
+                            ws=b.prune_ws)
+    se[2].record()
+    kernels.add_reverse_and_prune(X, a[0], a[1], a[2], p.strategy_code, p.kernel_param, p.M, p.M,
+                                  ws=b.rev_ws, out=b.b_out, order=order)
+    se[3].record()
+    torch.cuda.synchronize()
+    stages = {"pool": se[0].elapsed_time(se[1]), "select_A": se[1].elapsed_time(se[2]),
+              "reverse_B": se[2].elapsed_time(se[3])}
     return {"workload": CONFIG_DESC[cfg], "value": N / t, "unit": UNIT, "ms_per_step": t * 1e3,
+            "stages_ms": stages,
             "steps": steps, "warmup": 1, "pool_mode": "f32+f64-rerank",
             "dtype": "fp32 data: tcgen05 bf16x3 pool passes (proven bounds) + f64 rerank, "
                      "fp32 selection"}

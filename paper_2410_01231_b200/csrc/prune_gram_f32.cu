@@ -56,8 +56,9 @@ constexpr int THREADS = 32 * (PW + 4 + 1 + NG);  // 16 warps
 constexpr int MASK_WARP = PW, MMA_WARP = PW + 4, GREEDY_WARP = PW + 5;
 constexpr int TILE_B = C * 128;
 constexpr int TMEM_COLS = 2 * C;
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(C >> 3) << 17) |
-                           ((uint32_t)(C >> 4) << 24);
+// kind::f16: D fp32, A/B bf16, K-major, M = 128; N = the point's candidate
+// count rounded up to 16 (the re-prune's unions hold ~30 candidates)
+constexpr uint32_t IDESC_BASE = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(C >> 4) << 24);
 
 struct __align__(1024) Smem {
   uint8_t tile[STAGES][2][TILE_B];  // [stage][hi / lo], SW128 K-major
@@ -68,7 +69,8 @@ struct __align__(1024) Smem {
   int32_t cnt[2];                   // -1: end of this CTA's stream
   int32_t self[2];
   int64_t u[2];
-  int32_t stage_end[STAGES];
+  int32_t stage_end[STAGES];        // 1: end of stream; else 0
+  int32_t stage_n[STAGES];          // MMA N of the stage's point
   alignas(16) uint32_t pm[NBUF][C][4];  // pm[t]: candidates i < t that certainly dominate c_t
   alignas(16) uint32_t qm[NBUF][C][4];  // qm[t]: undecided pairs
   uint32_t ex[NBUF][4];
@@ -296,7 +298,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           if (kb == (nkb >> 1) - 1 && !have1) fetch1();
           GFWAIT(1, mbar_wait(&s.empty[stage], phase ^ 1));
-          if (t == 0) s.stage_end[stage] = 0;
+          if (t == 0) {
+            s.stage_end[stage] = 0;
+            s.stage_n[stage] = max(16, (cnt0 + 15) & ~15);
+          }
           if (wact) {
             const float4 *us = reinterpret_cast<const float4 *>(s.urow[par] + kb * KBLK);
 #pragma unroll
@@ -380,6 +385,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (s.stage_end[stage]) break;
         GFWAIT(4, mbar_wait(&s.tempty[par], (uint32_t)(((kp >> 1) & 1) ^ 1)));
         const uint32_t dcol = tmem + par * C;
+        const uint32_t idesc = IDESC_BASE | ((uint32_t)(s.stage_n[stage] >> 3) << 17);
         for (int kb = 0; kb < nkb; ++kb) {
           if (kb > 0) GFWAIT(3, mbar_wait_sleep(&s.full[stage], phase, 100));
           fence_proxy_async_smem();
@@ -387,11 +393,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint64_t dh = sw128_desc(s.tile[stage][0]), dl = sw128_desc(s.tile[stage][1]);
 #pragma unroll
           for (int kk = 0; kk < KBLK / 16; ++kk)
-            mma_bf16(dcol, dh + 2 * kk, dh + 2 * kk, IDESC, (kb | kk) != 0);
+            mma_bf16(dcol, dh + 2 * kk, dh + 2 * kk, idesc, (kb | kk) != 0);
 #pragma unroll
-          for (int kk = 0; kk < KBLK / 16; ++kk) mma_bf16(dcol, dh + 2 * kk, dl + 2 * kk, IDESC, 1);
+          for (int kk = 0; kk < KBLK / 16; ++kk) mma_bf16(dcol, dh + 2 * kk, dl + 2 * kk, idesc, 1);
 #pragma unroll
-          for (int kk = 0; kk < KBLK / 16; ++kk) mma_bf16(dcol, dl + 2 * kk, dh + 2 * kk, IDESC, 1);
+          for (int kk = 0; kk < KBLK / 16; ++kk) mma_bf16(dcol, dl + 2 * kk, dh + 2 * kk, idesc, 1);
           tc_commit(&s.empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
