@@ -49,6 +49,10 @@ constexpr int C = 128;        // candidates per point (TMEM lanes)
 constexpr int KBLK = 64;      // dimensions per k-block (128 B of bf16)
 constexpr int STAGES = 3;     // operand ring (hi + lo tiles, 32 KB per stage)
 constexpr int PW = 8;         // producer warps (16 candidate rows each)
+#ifndef GRAMF_PF_AHEAD
+#define GRAMF_PF_AHEAD 0  // measured: no gain in phase A, slower re-prune (3 / 5 blocks ahead)
+#endif
+constexpr int PF_AHEAD = GRAMF_PF_AHEAD;  // L1 prefetch distance in k-blocks
 constexpr int NBUF = 3;       // mask buffers (point k uses k % NBUF)
 constexpr int NG = 3;         // greedy warps (point k goes to warp k % NG)
 constexpr int DMAX = 1024;    // largest dimension (u's row is staged in shared memory)
@@ -297,6 +301,19 @@ __global__ void __launch_bounds__(THREADS, 1)
             load_kb(rid1, 0, xn);
           }
           if (kb == (nkb >> 1) - 1 && !have1) fetch1();
+          {
+            // L1 prefetch PF_AHEAD blocks ahead (the register prefetch covers one
+            // block, less than the L2 latency when a point has few rows):
+            // lane l of a row's 4 lanes takes the 128-byte line of piece l
+            const int pk = kb + PF_AHEAD;
+            const bool nxt = pk >= nkb;
+            const int pb = nxt ? pk - nkb : pk;
+            const int32_t ra = nxt ? rid1[0] : rid0[0], rb = nxt ? rid1[1] : rid0[1];
+            const int32_t rr = (c16 >> 1) ? rb : ra;
+            const int e4 = pb * 16 + (c16 & 1) * 8;
+            if (PF_AHEAD > 0 && (!nxt || have1) && pb < nkb && rr >= 0 && e4 < d4)
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(X4 + (int64_t)rr * d4 + e4));
+          }
           GFWAIT(1, mbar_wait(&s.empty[stage], phase ^ 1));
           if (t == 0) {
             s.stage_end[stage] = 0;
