@@ -451,15 +451,50 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
 // ---------------------------------------------------------------------------
 // Operand preparation
 // ---------------------------------------------------------------------------
+// Stop criterion of the k-center pass: once every tile centroid lies within
+// half a (mean) tile radius of its reference, further references no longer
+// shrink |x'| -- thr = 0.25 * mean(rad^2) over the non-empty tiles.
+__global__ void kcenter_thr_kernel(const double *__restrict__ rad, const int32_t *__restrict__ size,
+                                   int64_t T, float *__restrict__ thr) {
+  __shared__ double ssum[256];
+  __shared__ int scnt[256];
+  double a = 0.0;
+  int c = 0;
+  for (int64_t t = threadIdx.x; t < T; t += blockDim.x)
+    if (size[t] > 0) {
+      a += rad[t] * rad[t];
+      ++c;
+    }
+  ssum[threadIdx.x] = a;
+  scnt[threadIdx.x] = c;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      ssum[threadIdx.x] += ssum[threadIdx.x + o];
+      scnt[threadIdx.x] += scnt[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *thr = scnt[0] ? (float)(0.25 * ssum[0] / scnt[0]) : 0.f;
+}
+
 // One greedy k-center step over the tile centroids: distances to reference g
 // (= centroid of tile *pick), nearest reference per tile, and the farthest
-// tile -> next pick.  Block 0 also copies the reference vector.
+// tile -> next pick.  Block 0 also copies the reference vector.  Once the
+// farthest tile is within thr of its reference the pass is over: this and
+// every later launch return at once (pick_out stays 0).
 __global__ void kcenter_step_kernel(const float *__restrict__ cent, const int32_t *__restrict__ size,
                                     int64_t T, int d, int g, const unsigned long long *pick_in,
                                     unsigned long long *pick_out, float *__restrict__ mind,
-                                    int32_t *__restrict__ tref, float *__restrict__ refs) {
+                                    int32_t *__restrict__ tref, float *__restrict__ refs,
+                                    const float *__restrict__ thr) {
   const int lane = threadIdx.x & 31;
-  const int64_t pick = g == 0 ? 0 : (int64_t)(uint32_t)(*pick_in);
+  int64_t pick = 0;
+  if (g > 0) {
+    const unsigned long long pk = *pick_in;
+    if (__uint_as_float((uint32_t)(pk >> 32)) <= *thr) return;  // converged (or no tile left)
+    pick = (int64_t)(uint32_t)pk;
+  }
   const float *cp = cent + pick * d;
   if (blockIdx.x == 0)
     for (int k = threadIdx.x; k < d; k += blockDim.x) refs[(int64_t)g * d + k] = cp[k];
@@ -648,7 +683,7 @@ __global__ void tile_umax_kernel(const float *__restrict__ tau, const int32_t *_
 
 struct Layout {
   __nv_bfloat16 *H;
-  float *refs, *P, *nlo, *nhi, *na, *tau, *rtau, *mind;
+  float *refs, *P, *nlo, *nhi, *na, *tau, *rtau, *mind, *kthr;
   double *D2;
   int32_t *tref, *row_cnt, *sched;
   uint32_t *need, *done;
@@ -677,6 +712,7 @@ static Layout layout(void *ws, size_t bytes, int64_t np, int64_t T, int64_t d) {
   L.tau = c.take<float>(np);
   L.rtau = c.take<float>(np);
   L.mind = c.take<float>(T);
+  L.kthr = c.take<float>(4);
   L.D2 = c.take<double>((size_t)GMAX * GMAX);
   L.tref = c.take<int32_t>(T);
   L.row_cnt = c.take<int32_t>(np);
@@ -706,8 +742,9 @@ size_t tcf32_workspace(int64_t np, int64_t T, int64_t d) {
 
 // References, centred bf16 operands, cross-term table (once per build; np
 // tile-sorted rows xs with centroids cent / sizes of the T tiles).
-int tcf32_prepare(const float *xs, const int32_t *perm, const float *cent, const int32_t *size,
-                  int64_t np, int64_t T, int d, void *ws, size_t bytes, cudaStream_t stream) {
+int tcf32_prepare(const float *xs, const int32_t *perm, const float *cent, const double *rad,
+                  const int32_t *size, int64_t np, int64_t T, int d, void *ws, size_t bytes,
+                  cudaStream_t stream) {
   using namespace tcf;
   Layout L = layout(ws, bytes, np, T, d);
   if (L.bytes > bytes) {
@@ -717,9 +754,12 @@ int tcf32_prepare(const float *xs, const int32_t *perm, const float *cent, const
   const int sms = num_sms();
   const int G = num_refs(T);
   PGK_CUDA(cudaMemsetAsync(L.pick, 0, (GMAX + 1) * sizeof(unsigned long long), stream));
+  kcenter_thr_kernel<<<1, 256, 0, stream>>>(rad, size, T, L.kthr);
+  PGK_CHECK_LAUNCH("kcenter_thr_kernel");
   for (int g = 0; g < G; ++g) {
     kcenter_step_kernel<<<(unsigned)sms * 2, 256, 0, stream>>>(
-        cent, size, T, d, g, g ? L.pick + g - 1 : nullptr, L.pick + g, L.mind, L.tref, L.refs);
+        cent, size, T, d, g, g ? L.pick + g - 1 : nullptr, L.pick + g, L.mind, L.tref, L.refs,
+        L.kthr);
     PGK_CHECK_LAUNCH("kcenter_step_kernel");
   }
   ref_dist_kernel<<<(unsigned)sms * 2, 256, 0, stream>>>(L.refs, G, d, L.D2);

@@ -1195,8 +1195,9 @@ struct LayoutF32 {
 
 bool tcf32_supported(int64_t d, int64_t k);
 size_t tcf32_workspace(int64_t np, int64_t T, int64_t d);
-int tcf32_prepare(const float *xs, const int32_t *perm, const float *cent, const int32_t *size,
-                  int64_t np, int64_t T, int d, void *ws, size_t bytes, cudaStream_t stream);
+int tcf32_prepare(const float *xs, const int32_t *perm, const float *cent, const double *rad,
+                  const int32_t *size, int64_t np, int64_t T, int d, void *ws, size_t bytes,
+                  cudaStream_t stream);
 int tcf32_tau_from_keys(const uint64_t *keys1, int K, const int32_t *perm, int64_t np, int64_t T,
                         int d, double inflate, void *ws, size_t bytes, cudaStream_t stream);
 int tcf32_pass(const float *xs, int64_t np, int64_t T, int d, const int32_t *perm, const int32_t *tlist,
@@ -1360,7 +1361,7 @@ int launch_pool_tiles_f32(const float *X, int64_t n, int d, int K, int S, uint64
   }
   const bool use_tc = L.tcf_ws != nullptr && tc_mode > 0;
   if (use_tc) {
-    rc = tcf32_prepare(L.xs, L.perm, L.cent, L.size, NP, T, d, L.tcf_ws, L.tcf_bytes, stream);
+    rc = tcf32_prepare(L.xs, L.perm, L.cent, L.rad, L.size, NP, T, d, L.tcf_ws, L.tcf_bytes, stream);
     if (rc) return rc;
     dbg_stage("tcf32_prepare", stream);
   }
