@@ -77,6 +77,7 @@ struct __align__(1024) Smem {
   int32_t stage_n[STAGES];          // MMA N of the stage's point
   alignas(16) uint32_t pm[NBUF][C][4];  // pm[t]: candidates i < t that certainly dominate c_t
   alignas(16) uint32_t qm[NBUF][C][4];  // qm[t]: undecided pairs
+  alignas(16) uint32_t am[NBUF][C][4];  // am[t] (alpha rule): pairs whose test evaluates the angle
   uint32_t ex[NBUF][4];
   int32_t gid[NBUF][C];
   float gdist[NBUF][C];
@@ -117,6 +118,20 @@ __device__ __forceinline__ bool dominates_exact(float F, float dv, int strategy,
   return strategy == 0 ? true : p * (double)F < (double)dv;
 }
 
+// The alpha rule on an exact F (prune.cu's test_round): bit 0 = dominates,
+// bit 1 = the angle was evaluated.
+__device__ __forceinline__ int alpha_exact(float duw, float F, float dv, double cos_alpha) {
+  if (F == 0.0f) return 1;
+  if (!(F < dv)) return 0;
+  return 2 | (cos_angle_from_sq(duw, F, dv) < cos_alpha ? 1 : 0);
+}
+
+// sign of duw + x - dv - 2 cos(alpha) sqrt(duw x): negative iff the angle test
+// dominates (the cosine is increasing in x = dwv for x > duw - dv)
+__device__ __forceinline__ double alpha_f(double duw, double x, double dv, double k2) {
+  return (duw - dv) + x - k2 * sqrt(duw * x);
+}
+
 // PGK_GRAM_F32_STATS=1: cycles each role spends in its barrier waits
 // (stats[4 + slot]); slots: 0 producer-pempty 1 producer-empty 2 producer-total
 // 3 mma-full 4 mma-tempty 5 mma-total 6 mask-pfull 7 mask-tfull 8 mask-mempty
@@ -132,6 +147,7 @@ __device__ __forceinline__ bool dominates_exact(float F, float dv, int strategy,
     }                                                                           \
   } while (0)
 
+template <bool ALPHA>  // the alpha rule (strategy 1): angle masks and counters compiled in
 __global__ void __launch_bounds__(THREADS, 1)
     prune_gram_f32_kernel(const float *__restrict__ X, int d, int64_t n_rows,
                           const int32_t *__restrict__ row_node,
@@ -449,7 +465,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const float dv = s.dist[par][t];
       const float nt = s.nrm[par][t];
       const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + par * C;
-      uint32_t pm[4] = {0, 0, 0, 0}, qm[4] = {0, 0, 0, 0};
+      uint32_t pm[4] = {0, 0, 0, 0}, qm[4] = {0, 0, 0, 0}, gmm[4] = {0, 0, 0, 0};
       GFWAIT(7, mbar_wait_sleep(&s.tfull[par], pph, 100));
       tc_fence_after();
       const int clast = q * 32 >= cnt ? -1 : min(q, (cnt - 1) >> 5);
@@ -460,12 +476,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t zu = __ballot_sync(0xffffffffu, s.dist[par][c * 32 + lane] == 0.0f);
         const uint32_t valid = c < q ? 0xffffffffu : ((1u << lane) - 1u);
         tmem_wait_ld();
-        uint32_t dm = 0, am = 0;
+        uint32_t dm = 0, am = 0, gm = 0;  // dominates / undecided / angle evaluated
         const float4 *np = reinterpret_cast<const float4 *>(s.nrm[par] + c * 32);
+        const float4 *dp4 = reinterpret_cast<const float4 *>(s.dist[par] + c * 32);
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
           const float4 w = np[v];
           const float ni[4] = {w.x, w.y, w.z, w.w};
+          float du[4] = {0.f, 0.f, 0.f, 0.f};
+          if (ALPHA) {
+            const float4 dq = dp4[v];
+            du[0] = dq.x; du[1] = dq.y; du[2] = dq.z; du[3] = dq.w;
+          }
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int k = 4 * v + e;
@@ -473,7 +495,20 @@ __global__ void __launch_bounds__(THREADS, 1)
             const float A = fmaf(-2.0f, __uint_as_float(g[k]), S);
             const float hi = fmaf(ee, S, A), lo = fmaf(-ee, S, A);
             bool cd, cn;
-            if (strategy == 0) {
+            if (ALPHA) {
+              // F < dv and F > 0 certain: the angle is evaluated; its verdict
+              // from the sign of f at the interval's ends (fp32, with slack)
+              const bool lt = hi < dv && lo > 0.0f;
+              const float duw = du[e];
+              const float base = duw - dv, kk = (float)(2.0 * p_slack);
+              const float fhi = base + hi - kk * sqrtf(duw * hi);
+              const float flo = base + lo - kk * sqrtf(duw * lo);
+              const float eps = 2e-6f * (duw + dv + hi);
+              const bool mono = lo > base;  // (always, for sorted rows: duw <= dv)
+              cd = lt && mono && fhi < -eps;
+              cn = (lo >= dv && lo > 0.0f) || (lt && mono && flo > eps);
+              gm |= (lt && (cd || cn)) ? (1u << k) : 0u;
+            } else if (strategy == 0) {
               cd = hi < dv;
               cn = lo >= dv && lo > 0.0f;
             } else {
@@ -486,6 +521,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         pm[c] = (dm | zu) & valid;
         qm[c] = am & ~zu & valid;
+        if (ALPHA) gmm[c] = gm & ~zu & valid;
       }
       tc_fence_before();
       __syncwarp();
@@ -493,6 +529,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       GFWAIT(8, mbar_wait(&s.mempty[mb], mphase ^ 1));
       *reinterpret_cast<uint4 *>(s.pm[mb][t]) = make_uint4(pm[0], pm[1], pm[2], pm[3]);
       *reinterpret_cast<uint4 *>(s.qm[mb][t]) = make_uint4(qm[0], qm[1], qm[2], qm[3]);
+      if (ALPHA)
+        *reinterpret_cast<uint4 *>(s.am[mb][t]) = make_uint4(gmm[0], gmm[1], gmm[2], gmm[3]);
       const int32_t myid = s.id[par][t];
       const unsigned exm = __ballot_sync(0xffffffffu, t < cnt && myid != s.self[par]);
       if (lane == 0) s.ex[mb][q] = exm;
@@ -524,6 +562,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int32_t *sid = s.gid[mb];
       const float *sdist = s.gdist[mb];
       uint32_t pw[4][4], qw[4][4];  // this lane's candidates c*32+lane: pm / qm rows
+      uint32_t aw[ALPHA ? 4 : 1][4];  // ... and the angle-evaluated masks (alpha rule)
       uint32_t exv[4];
       int32_t idv[4];
       float dsv[4];
@@ -533,6 +572,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint4 b = *reinterpret_cast<const uint4 *>(s.qm[mb][c * 32 + lane]);
         pw[c][0] = a.x; pw[c][1] = a.y; pw[c][2] = a.z; pw[c][3] = a.w;
         qw[c][0] = b.x; qw[c][1] = b.y; qw[c][2] = b.z; qw[c][3] = b.w;
+        if (ALPHA) {
+          const uint4 g4 = *reinterpret_cast<const uint4 *>(s.am[mb][c * 32 + lane]);
+          aw[ALPHA ? c : 0][0] = g4.x; aw[ALPHA ? c : 0][1] = g4.y;
+          aw[ALPHA ? c : 0][2] = g4.z; aw[ALPHA ? c : 0][3] = g4.w;
+        }
         exv[c] = s.ex[mb][c];
         idv[c] = sid[c * 32 + lane];
         dsv[c] = sdist[c * 32 + lane];
@@ -632,9 +676,19 @@ __global__ void __launch_bounds__(THREADS, 1)
               for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
               const double dlo = acc * (1.0 - gseq), dhi = acc * (1.0 + gseq);
               const double dvd = (double)dvb;
-              int verdict = -1;  // 1 dominates, 0 does not, -1 undecided
+              const float duwf = sdist[w * 32 + ib];  // d(u, c_i)
+              int verdict = -1;  // bit 0 dominates, bit 1 angle evaluated; -1 undecided
               if (acc > 1e-30) {
-                if (strategy == 0) {
+                if (ALPHA) {
+                  if (dlo >= dvd) {
+                    verdict = 0;
+                  } else if (dhi < dvd && dlo > (double)duwf - dvd) {
+                    const double k2 = 2.0 * p_slack, du = (double)duwf;
+                    const double tol = 1e-11 * (du + dvd + dhi);
+                    if (alpha_f(du, dhi, dvd, k2) < -tol) verdict = 3;
+                    else if (alpha_f(du, dlo, dvd, k2) > tol) verdict = 2;
+                  }
+                } else if (strategy == 0) {
                   if (dhi < dvd) verdict = 1;
                   else if (dlo >= dvd) verdict = 0;
                 } else {
@@ -653,12 +707,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                   for (int e = 0; e < d; ++e) F = sq_step(F, ra[e], rb[e]);
                 }
                 F = __shfl_sync(0xffffffffu, F, 0);
-                verdict = dominates_exact(F, dvb, strategy, p_slack) ? 1 : 0;
+                verdict = ALPHA ? alpha_exact(duwf, F, dvb, p_slack)
+                                : (dominates_exact(F, dvb, strategy, p_slack) ? 1 : 0);
                 if (stats) ++st_chain;
               }
               __syncwarp();
               if (lane == src) {
-                if (verdict) pw[c][w] |= 1u << ib;
+                if (verdict & 1) pw[c][w] |= 1u << ib;
+                if (ALPHA && (verdict & 2)) aw[ALPHA ? c : 0][w] |= 1u << ib;
                 qw[c][w] &= ~(1u << ib);
                 rel &= rel - 1;
               }
@@ -697,7 +753,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // exact lazy counters of every examined candidate
       const int kp1 = __popc(kept_m[0]), kp2 = kp1 + __popc(kept_m[1]),
                 kp3 = kp2 + __popc(kept_m[2]);
-      long long dsum = 0;
+      long long dsum = 0, asum = 0;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int j = c * 32 + lane;
@@ -715,12 +771,26 @@ __global__ void __launch_bounds__(THREADS, 1)
                  __popc(kw & ((1u << (end & 31)) - 1u));
         if (f >= 0 && !((zu[f >> 5] >> (f & 31)) & 1u)) ev += 1;
         dsum += ev;
+        if (ALPHA) {  // angle evaluations among the pairs the scan looked at
+          int an = 0;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            uint32_t lim = end >= (w + 1) * 32 ? 0xffffffffu
+                                               : (end <= w * 32 ? 0u : ((1u << (end - w * 32)) - 1u));
+            if (f >= 0 && (f >> 5) == w) lim |= 1u << (f & 31);
+            an += __popc(aw[ALPHA ? c : 0][w] & kept_m[w] & lim);
+          }
+          asum += an;
+        }
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+        if (ALPHA) asum += __shfl_xor_sync(0xffffffffu, asum, o);
+      }
       if (lane == 0) {
         dist_evals[u] = dsum;
-        angle_evals[u] = 0;
+        angle_evals[u] = asum;
         out_counts[u] = kept;
       }
       __syncwarp();
@@ -752,14 +822,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 }  // namespace gramf
 
-// fp32 rows, d % 4 == 0, 16-byte aligned, 128 <= d <= 1024, rng / slack
+// fp32 rows, d % 4 == 0, 16-byte aligned, 128 <= d <= 1024; rng, alpha and slack
 bool gram_f32_supported(const float *X, int64_t d, int strategy) {
   static int env = -1;
   if (env < 0) {
     const char *e = getenv("PGK_GRAM_F32");
     env = (e && e[0] == '0') ? 0 : 1;
   }
-  return env && (strategy == 0 || strategy == 2) && d >= 128 && d <= gramf::DMAX && d % 4 == 0 &&
+  return env && strategy >= 0 && strategy <= 2 && d >= 128 && d <= gramf::DMAX && d % 4 == 0 &&
          ((uintptr_t)X % 16 == 0);
 }
 
@@ -782,7 +852,8 @@ int launch_prune_gram_f32(const float *X, int64_t d, int64_t n, const int32_t *r
   const double ee = (dp + 2.0 * (double)d + 16.0) * u24 * 1.02 +
                     (3.1 / 262144.0 + 4.0 * (dp + 16.0) / 8388608.0) + 8.0 * u24;
   const size_t smem = sizeof(Smem) + 1024;
-  PGK_CUDA(ensure_smem((const void *)prune_gram_f32_kernel, smem));
+  PGK_CUDA(ensure_smem((const void *)prune_gram_f32_kernel<false>, smem));
+  PGK_CUDA(ensure_smem((const void *)prune_gram_f32_kernel<true>, smem));
   const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)num_sms());
   // F = D (1 + theta): t = fl(a - b), t * t and d - 1 additions, each rounded
   const double gseq = ((double)d + 3.0) * u24 * 1.0001;
@@ -796,10 +867,16 @@ int launch_prune_gram_f32(const float *X, int64_t d, int64_t n, const int32_t *r
     PGK_CUDA(cudaMalloc(&dstats, 20 * sizeof(unsigned long long)));
     PGK_CUDA(cudaMemsetAsync(dstats, 0, 20 * sizeof(unsigned long long), stream));
   }
-  prune_gram_f32_kernel<<<grid, THREADS, smem, stream>>>(
-      X, (int)d, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
-      cos_alpha, (float)ee, gseq, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals,
-      angle_evals, dstats);
+  if (strategy == 1)
+    prune_gram_f32_kernel<true><<<grid, THREADS, smem, stream>>>(
+        X, (int)d, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
+        cos_alpha, (float)ee, gseq, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals,
+        angle_evals, dstats);
+  else
+    prune_gram_f32_kernel<false><<<grid, THREADS, smem, stream>>>(
+        X, (int)d, n, row_node, row_order, cand_off, cand_counts, cand_ids, cand_dists, strategy,
+        cos_alpha, (float)ee, gseq, (int)M, (int)width, out_ids, out_dists, out_counts, dist_evals,
+        angle_evals, dstats);
   PGK_CHECK_LAUNCH("prune_gram_f32_kernel");
   if (stats_env) {
     unsigned long long h[20];

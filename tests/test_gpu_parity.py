@@ -669,7 +669,8 @@ def test_gram_f32_selection_against_oracle(name):
     """The tensor-core float selection (prune_gram_f32.cu: bf16 hi/lo Gram on
     rows centred on the point, proven pair classification, float64 / exact
     fp32 chains for undecided pairs) equals the oracle's phases A and B, ids,
-    dists, degrees and dist_evals, for rng and the slack rule; the lattice
+    dists, degrees, dist_evals and angle_evals, for rng, the alpha rule (66 and
+    95 degrees) and the slack rule; the lattice
     data put most pair tests exactly on their threshold (zero distances,
     F == dv ties), which forces the exact-chain path."""
     if name == "cfg3":
@@ -684,7 +685,7 @@ def test_gram_f32_selection_against_oracle(name):
     np.testing.assert_array_equal(ids, o_ids)
     off = np.arange(ds.n + 1, dtype=np.int64) * K
     cnt = np.full(ds.n, K, np.int32)
-    for strategy, s in (("rng", 60.0), ("slack", 1.2)):
+    for strategy, s in (("rng", 60.0), ("slack", 1.2), ("alpha", 66.0), ("alpha", 95.0)):
         p = PruneParams(M=R, alpha=s, strategy=strategy)
         a = prune_all(ds, off, cnt, ids.ravel(), dists.ravel(), p)
         b = add_reverse_and_prune(ds, a[0], a[1], a[2], p)
@@ -693,7 +694,7 @@ def test_gram_f32_selection_against_oracle(name):
         for res, ref in ((a, oa), (b, ob)):
             for i in range(3):
                 np.testing.assert_array_equal(res[i], ref[i], err_msg=f"{name} {strategy} [{i}]")
-            assert res[3] == ref[3], (name, strategy)
+            assert res[3] == ref[3] and res[4] == ref[4], (name, strategy, s)
 
 
 def test_gram_f32_equals_prune_kernel_on_larger_prefixes():
