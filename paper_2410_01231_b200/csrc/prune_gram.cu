@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     // (32 asynchronous arrivals + lane 0's), so no dependent global round
     // trip sits in this loop.  Lane l holds candidates 4l..4l+3 (id -1 past
     // cnt); its gather4 fetches exactly those rows.
-    constexpr int GD = 3;
+    constexpr int GD = 4;
     int stage = 0, half = 0;
     uint32_t phase = 0;
     const int64_t nb = blockIdx.x < n_rows ? (n_rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -262,23 +262,29 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     fetch_rest(0);
     fetch_u(1);
     fetch_rest(1);
-    int32_t i0[4], i1[4], i2[4];
-    ids_of(meta(0), i0);
-    ids_of(meta(1), i1);
-    ids_of(meta(2), i2);
-    static_assert(GD == 3, "the id registers below hold three points");
+    // The id registers of GD points are NOT rotated (a rotation reads the
+    // newest load's destination at the top of the next iteration, which
+    // stalls the warp on a load issued one iteration earlier): the loop is
+    // unrolled GD times over GD named register sets, and a set is reloaded
+    // with point k + GD's ids right after point k has used it.
+    int32_t ia[4], ib[4], ic[4], id4[4];
+    ids_of(meta(0), ia);
+    ids_of(meta(1), ib);
+    ids_of(meta(2), ic);
+    ids_of(meta(3), id4);
+    static_assert(GD == 4, "four named id register sets below");
 #if GRAM_STATS
     long long gmark_ = clock64(), g_meta = 0, g_tma = 0, g_cpa = 0, g_pub = 0, g_wait = 0;
 #endif
-    for (int64_t k = 0; k < nb; ++k) {
+    auto point = [&](const int64_t k, int32_t (&i0)[4]) {
       GMARK(g_pub);
       const int64_t b = k >> 5;
       if (b >= 1 && (k & 31) == 0) fetch_u(b + 1);
       if (b >= 1 && (k & 31) == 16) fetch_rest(b + 1);
-      int32_t i3[4];
-      ids_of(meta(k + GD), i3);
       const PM m0 = meta(k);
-      if (m0.cnt > PC) {  // hub row (PAIR: > 64): left to the next kernel
+      if (m0.cnt < 0) {
+        // a row the fused merge kernel (reverse.cu) has already pruned
+      } else if (m0.cnt > PC) {  // hub row (PAIR: > 64): left to the next kernel
         if (lane == 0) long_rows[atomicAdd(long_count, 1)] = (int32_t)m0.u;
       } else {
         GMARK(g_meta);
@@ -376,12 +382,13 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
           half = 0;
         }
       }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        i0[i] = i1[i];
-        i1[i] = i2[i];
-        i2[i] = i3[i];
-      }
+      ids_of(meta(k + GD), i0);  // this set's next point
+    };
+    for (int64_t k = 0; k < nb; k += GD) {
+      point(k, ia);
+      if (k + 1 < nb) point(k + 1, ib);
+      if (k + 2 < nb) point(k + 2, ic);
+      if (k + 3 < nb) point(k + 3, id4);
     }
     if (PAIR && half == 1) {  // a half-filled last stage: the second slot is empty
       if (lane == 0) {

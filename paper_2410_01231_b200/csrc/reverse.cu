@@ -36,6 +36,19 @@ int launch_prune(const float *X, const uint8_t *xu8, const int32_t *norms, int64
                  int32_t *out_counts, int64_t *dist_evals, int64_t *angle_evals,
                  cudaStream_t stream, bool short_rows = false);
 
+size_t gram_workspace(int64_t n);
+bool gram_enabled();
+
+// PGK_REV_FUSED=0: every merged row goes to the tcgen05 kernels (A/B timing)
+static bool rev_fused_enabled() {
+  static int env = -1;
+  if (env < 0) {
+    const char *e = getenv("PGK_REV_FUSED");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env == 1;
+}
+
 constexpr int SORT_WARPS = 8;
 #ifndef SCATTER_PASSES
 #define SCATTER_PASSES 1  // measured: 4 node-range passes 1.05 ms vs 0.68 ms for one
@@ -276,13 +289,16 @@ __device__ __forceinline__ int reg_sort_dedupe(const uint64_t *__restrict__ keys
 // rev <= 32 reverse entries (arrival order): sort only the reverse part (one
 // key per lane), then one bitonic merge with the own part -- 26 shuffle
 // stages against 40 for sorting all 64 -- and the same duplicate drop.
-__device__ __forceinline__ int merge_own_rev(const uint64_t *__restrict__ keys, int own, int rev,
-                                             int32_t *__restrict__ out_ids,
-                                             float *__restrict__ out_d, int lane) {
-  uint64_t e0 = lane < own ? keys[lane] : KEY_MAX;
-  uint64_t r = lane < rev ? keys[own + lane] : KEY_MAX;
+// (register core: e0 = the ascending own part, r = the unsorted reverse part,
+// KEY_MAX past their lengths; len = own + rev)
+__device__ __forceinline__ int merge_own_rev_regs(uint64_t e0, uint64_t r, int len, int nr,
+                                                  int32_t *__restrict__ out_ids,
+                                                  float *__restrict__ out_d, int lane) {
+  // nr keys sit in lanes 0..nr-1 of r (KEY_MAX behind them): the network only
+  // has to sort the first power-of-two block that holds them (warp-uniform)
 #pragma unroll
   for (int k = 2; k <= 32; k <<= 1) {
+    if ((k >> 1) >= nr) break;
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
       const uint64_t o = __shfl_xor_sync(0xffffffffu, r, j);
@@ -306,7 +322,6 @@ __device__ __forceinline__ int merge_own_rev(const uint64_t *__restrict__ keys, 
     e0 = lower ? (e0 < o0 ? e0 : o0) : (e0 < o0 ? o0 : e0);
     e1 = lower ? (e1 < o1 ? e1 : o1) : (e1 < o1 ? o1 : e1);
   }
-  const int len = own + rev;
   int m = 0;
   uint64_t last = 0;
 #pragma unroll
@@ -329,6 +344,199 @@ __device__ __forceinline__ int merge_own_rev(const uint64_t *__restrict__ keys, 
   return m;
 }
 
+__device__ __forceinline__ int merge_own_rev(const uint64_t *__restrict__ keys, int own, int rev,
+                                             int32_t *__restrict__ out_ids,
+                                             float *__restrict__ out_d, int lane) {
+  const uint64_t e0 = lane < own ? keys[lane] : KEY_MAX;
+  const uint64_t r = lane < rev ? keys[own + lane] : KEY_MAX;
+  return merge_own_rev_regs(e0, r, own + rev, rev, out_ids, out_d, lane);
+}
+
+// ---------------------------------------------------------------------------
+// Fused merge + re-prune of short unions (exact-integer rows, rng / slack).
+// At config 2 68 % of the merged rows hold <= 32 candidates: too little work
+// for the tcgen05 Gram pipeline, whose per-point hand-offs (gather -> MMA ->
+// masks -> greedy) cost more than the row itself.  Here the warp that merged
+// the slice keeps it in registers and prunes it on the spot:
+//   * lane t = candidate t; lane (g, tig) = (lane / 4, lane % 4) loads 32 bytes
+//     of each of the rows g, g + 8, g + 16, g + 24 (two LDG.128 per row);
+//   * the 32 x 32 Gram matrix C C^T (exact s32) by warp-level
+//     mma.sync.m16n8k32.u8.u8 on exactly those registers -- a lane's rows are
+//     both its A fragments (rows g, g + 8 of an m-tile) and its B fragments
+//     (column g of an n-tile), and the k order is the same lane-local word
+//     order on both sides, so no data moves between lanes; lower-triangle
+//     tiles only;
+//   * the dominance masks, the greedy scan and the lazy-evaluation counters of
+//     prune_gram_kernel (prune_gram.cu: same integer compare, same popcount
+//     formulas), on one 32-bit mask per candidate.
+// No shared-memory tiles, no TMEM, no barriers; the merged row never travels
+// through HBM.  Rows with more than 32 merged candidates are written to the
+// merged CSR as before and listed (todo) for the tcgen05 kernels.
+__device__ __forceinline__ void mma_u8_16832(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                             uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+struct FusedOut {
+  const uint8_t *xu8;      // (N, 128) exact-integer rows
+  const int32_t *norms;    // |x|^2
+  int strategy;            // 0 rng, 2 slack
+  double p;                // slack: s^2
+  int M, width;
+  int32_t *out_ids;
+  float *out_dists;
+  int32_t *out_counts;
+  int64_t *dist_evals, *angle_evals;
+};
+
+// lane t holds candidate t (id < 0 past m), m <= 32, ascending (dist, id)
+__device__ __forceinline__ void warp_prune_u8(const FusedOut &o, int64_t u, int m, int32_t id,
+                                              float dv, int lane) {
+  const int g = lane >> 2, tig = lane & 3;
+  const int nv = id >= 0 ? o.norms[id] : 0;
+  // rows g + 8q, 32 bytes each: words 0..3 = bytes 16 tig.., 4..7 = bytes 64 + 16 tig..
+  uint32_t w[4][8];
+  const int nq = (m + 7) >> 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int32_t rid = __shfl_sync(0xffffffffu, id, g + 8 * q);
+    uint4 lo = make_uint4(0, 0, 0, 0), hi = lo;
+    if (q < nq && rid >= 0) {
+      const uint4 *rp = reinterpret_cast<const uint4 *>(o.xu8 + (int64_t)rid * 128);
+      lo = __ldg(rp + tig);
+      hi = __ldg(rp + 4 + tig);
+    }
+    w[q][0] = lo.x; w[q][1] = lo.y; w[q][2] = lo.z; w[q][3] = lo.w;
+    w[q][4] = hi.x; w[q][5] = hi.y; w[q][6] = hi.z; w[q][7] = hi.w;
+  }
+  // c_i dominates c_t iff |c_i|^2 - 2 G[t][i] <= thr_t (prune_gram.cu: dle - |c_t|^2)
+  int dle;
+  if (dv >= 2.0e9f) {
+    dle = 0x7fffffff;
+  } else if (o.strategy != 2) {
+    const float fl = floorf(dv);
+    const int x = (int)fl - (fl == dv ? 1 : 0);
+    dle = x > 0 ? x : 0;
+  } else {
+    const double p = o.p;
+    int64_t x = (int64_t)floor((double)dv / p);
+    while (x >= 0 && !(p * (double)x < (double)dv)) --x;
+    while (p * (double)(x + 1) < (double)dv) ++x;
+    dle = (int)(x > 0 ? x : 0);
+  }
+  const int thr = dle == 0x7fffffff ? 0x7fffffff : dle - nv;
+  // Gram tiles (m-tile mt: rows 16 mt.., n-tile j: columns 8 j..), lower
+  // triangle; one m-tile at a time (its accumulators become mask bits before
+  // the next one is computed).  This lane's columns are 8 j + 2 tig + e, its
+  // rows g + 8 q.
+  int ncol[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    ncol[j][0] = __shfl_sync(0xffffffffu, nv, 8 * j + 2 * tig);
+    ncol[j][1] = __shfl_sync(0xffffffffu, nv, 8 * j + 2 * tig + 1);
+  }
+  uint32_t mine = 0;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    if (mt == 1 && m <= 16) break;  // warp-uniform
+    int acc[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j > 2 * mt + 1) continue;  // upper triangle: never read
+        mma_u8_16832(acc[j], w[2 * mt][2 * ks], w[2 * mt + 1][2 * ks], w[2 * mt][2 * ks + 1],
+                     w[2 * mt + 1][2 * ks + 1], w[j][2 * ks], w[j][2 * ks + 1]);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = 2 * mt + h;
+      const int thq = __shfl_sync(0xffffffffu, thr, g + 8 * q);
+      uint32_t pmq = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j > 2 * mt + 1) continue;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool dom = ncol[j][e] - 2 * acc[j][2 * h + e] <= thq;
+          pmq |= dom ? (1u << (8 * j + 2 * tig + e)) : 0u;
+        }
+      }
+      pmq |= __shfl_xor_sync(0xffffffffu, pmq, 1);
+      pmq |= __shfl_xor_sync(0xffffffffu, pmq, 2);
+      // candidate t = g' + 8 q' reads row slot q' of lane 4 g'
+      const uint32_t got = __shfl_sync(0xffffffffu, pmq, 4 * (lane & 7));
+      if ((lane >> 3) == q) mine = got;
+    }
+  }
+  const uint32_t zu = __ballot_sync(0xffffffffu, dv == 0.0f);  // duw == 0: no distance computed
+  const uint32_t pm = (mine | zu) & lanemask_lt();
+  const uint32_t ex = __ballot_sync(0xffffffffu, lane < m && id != (int32_t)u);
+  // greedy scan (_kernels.py:364-427): first candidate not dominated by a kept one
+  uint32_t km = 0, mm = ex;
+  int kept = 0, stop_j = 32;
+  while (mm) {
+    const int li = __ffs(mm) - 1;
+    km |= 1u << li;
+    if (++kept == o.M) {
+      stop_j = li;
+      break;
+    }
+    const uint32_t dom = __ballot_sync(0xffffffffu, (pm >> li) & 1u);
+    mm &= ~(dom | ((2u << li) - 1u));
+  }
+  // kept candidates in scan order as one padded row
+  {
+    const int src_lane = __fns(km, 0, lane + 1);  // lane of the (lane+1)-th kept candidate
+    const int32_t kid = __shfl_sync(0xffffffffu, id, src_lane & 31);
+    const float kd = __shfl_sync(0xffffffffu, dv, src_lane & 31);
+    for (int j = lane; j < o.width; j += 32) {
+      const bool has = j < kept;  // kept <= 32: only j == lane can be kept
+      o.out_ids[u * o.width + j] = has ? kid : -1;
+      o.out_dists[u * o.width + j] = has ? kd : __int_as_float(0x7f800000);
+    }
+  }
+  // exact lazy counters of every examined candidate
+  long long ev = 0;
+  if (lane <= stop_j && ((ex >> lane) & 1u)) {
+    const uint32_t d = pm & km;  // pm holds only earlier candidates
+    const int f = d ? __ffs(d) - 1 : -1;
+    const int end = f >= 0 ? f : lane;
+    ev = __popc(km & ((1u << end) - 1u));
+    if (f >= 0 && !((zu >> f) & 1u)) ev += 1;
+  }
+#pragma unroll
+  for (int of = 16; of > 0; of >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, of);
+  if (lane == 0) {
+    o.dist_evals[u] = ev;
+    o.angle_evals[u] = 0;
+    o.out_counts[u] = kept;
+  }
+}
+
+// FUSED: slices whose merged row holds <= 32 candidates are pruned by the
+// merging warp itself (warp_prune_u8) and marked mrg_counts = -1, which the
+// tcgen05 kernels skip; rows are walked in the caller's locality order.
+// the general register sort of one slice (every length up to SORT_SMEM_KEYS)
+__device__ __forceinline__ int sort_slice(const uint64_t *__restrict__ keys, int own, int len,
+                                          int32_t *__restrict__ out_ids,
+                                          float *__restrict__ out_d, int lane) {
+  if (len > 32 && own <= 32 && len - own <= 32)
+    return merge_own_rev(keys, own, len - own, out_ids, out_d, lane);
+  if (len <= 32) return reg_sort_dedupe<1>(keys, len, out_ids, out_d, lane);
+  if (len <= 64) return reg_sort_dedupe<2>(keys, len, out_ids, out_d, lane);
+  if (len <= 128) return reg_sort_dedupe<4>(keys, len, out_ids, out_d, lane);
+  if (len <= 256) return reg_sort_dedupe<8>(keys, len, out_ids, out_d, lane);
+  return reg_sort_dedupe<16>(keys, len, out_ids, out_d, lane);
+}
+
 __global__ void __launch_bounds__(SORT_WARPS * 32)
     merge_sort_kernel(const int64_t *__restrict__ mrg_off, int64_t n,
                       const int32_t *__restrict__ own_counts,
@@ -336,26 +544,109 @@ __global__ void __launch_bounds__(SORT_WARPS * 32)
                       int32_t *__restrict__ mrg_ids, float *__restrict__ mrg_d,
                       int32_t *__restrict__ mrg_counts,
                       int32_t *__restrict__ long_list,
-                      int32_t *__restrict__ long_count) {
+                      int32_t *__restrict__ long_count, int only_flagged) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t u = (int64_t)blockIdx.x * SORT_WARPS + warp; u < n;
        u += (int64_t)gridDim.x * SORT_WARPS) {
+    // after merge_prune_kernel: only the slices it left (mrg_counts == -2)
+    if (only_flagged && mrg_counts[u] != -2) continue;
     const int64_t lo = mrg_off[u];
     const int len = (int)(mrg_off[u + 1] - lo);
     if (len > SORT_SMEM_KEYS) {
       if (lane == 0) long_list[atomicAdd(long_count, 1)] = (int32_t)u;
       continue;
     }
-    int m;
-    const int own = own_counts[u];
-    if (len > 32 && own <= 32 && len - own <= 32)
-      m = merge_own_rev(keys + lo, own, len - own, mrg_ids + lo, mrg_d + lo, lane);
-    else if (len <= 32) m = reg_sort_dedupe<1>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
-    else if (len <= 64) m = reg_sort_dedupe<2>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
-    else if (len <= 128) m = reg_sort_dedupe<4>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
-    else if (len <= 256) m = reg_sort_dedupe<8>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
-    else m = reg_sort_dedupe<16>(keys + lo, len, mrg_ids + lo, mrg_d + lo, lane);
+    const int m = sort_slice(keys + lo, own_counts[u], len, mrg_ids + lo, mrg_d + lo, lane);
     if (lane == 0) mrg_counts[u] = m;
+  }
+}
+
+// Fused form: slices whose merged row holds <= 32 candidates are pruned by the
+// merging warp itself (warp_prune_u8) and marked mrg_counts = -1, which the
+// tcgen05 kernels skip; rows are walked in the caller's locality order.  A
+// warp's rows come in batches of 32 (lane l loads row l's id, offsets and own
+// count: one exposed latency per 32 rows) and the next row's keys are loaded
+// while the current row is merged and pruned.
+constexpr int FUSED_WARPS = 8;
+#ifndef FUSED_MINB
+#define FUSED_MINB 3
+#endif
+__global__ void __launch_bounds__(FUSED_WARPS * 32, FUSED_MINB)
+    merge_prune_kernel(const int64_t *__restrict__ mrg_off, int64_t n,
+                       const int32_t *__restrict__ own_counts,
+                       const uint64_t *__restrict__ keys,
+                       int32_t *__restrict__ mrg_ids, float *__restrict__ mrg_d,
+                       int32_t *__restrict__ mrg_counts,
+                       const int32_t *__restrict__ row_order, const FusedOut fo) {
+  __shared__ int32_t sh_ids[FUSED_WARPS][64];
+  __shared__ float sh_d[FUSED_WARPS][64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t *si = sh_ids[warp];
+  float *sd = sh_d[warp];
+  const int64_t i0 = (int64_t)blockIdx.x * FUSED_WARPS + warp;
+  const int64_t stride = (int64_t)gridDim.x * FUSED_WARPS;
+  const int64_t nw = i0 < n ? (n - 1 - i0) / stride + 1 : 0;  // this warp's rows
+  for (int64_t kb = 0; kb < nw; kb += 32) {
+    int64_t bu = 0, blo = 0;
+    int blen = 0, bown = 0;
+    if (kb + lane < nw) {
+      const int64_t i = i0 + (kb + lane) * stride;
+      bu = row_order ? (int64_t)row_order[i] : i;
+      blo = mrg_off[bu];
+      blen = (int)(mrg_off[bu + 1] - blo);
+      bown = own_counts[bu];
+    }
+    const int nb = (int)min((int64_t)32, nw - kb);
+    // keys of a short slice: A = own part (or the whole slice when len <= 32),
+    // B = reverse part of a two-part slice
+    auto load_keys = [&](int64_t lo, int len, int own, uint64_t &A, uint64_t &B) {
+      const bool two = len > 32 && own <= 32 && len - own <= 32;
+      A = B = KEY_MAX;
+      if (two) {
+        if (lane < own) A = keys[lo + lane];
+        if (lane < len - own) B = keys[lo + own + lane];
+      } else if (len <= 32) {
+        if (lane < len) A = keys[lo + lane];
+      }
+    };
+    uint64_t ka, kr;
+    load_keys(__shfl_sync(0xffffffffu, blo, 0), __shfl_sync(0xffffffffu, blen, 0),
+              __shfl_sync(0xffffffffu, bown, 0), ka, kr);
+    for (int j = 0; j < nb; ++j) {
+      const int64_t u = __shfl_sync(0xffffffffu, bu, j);
+      const int64_t lo = __shfl_sync(0xffffffffu, blo, j);
+      const int len = __shfl_sync(0xffffffffu, blen, j);
+      const int own = __shfl_sync(0xffffffffu, bown, j);
+      uint64_t na = KEY_MAX, nr = KEY_MAX;
+      if (j + 1 < nb)
+        load_keys(__shfl_sync(0xffffffffu, blo, j + 1), __shfl_sync(0xffffffffu, blen, j + 1),
+                  __shfl_sync(0xffffffffu, bown, j + 1), na, nr);
+      const bool two = len > 32 && own <= 32 && len - own <= 32;
+      if (two || len <= 32) {
+        // len <= 32: the whole slice sits in the part that gets sorted
+        const int m = merge_own_rev_regs(two ? ka : KEY_MAX, two ? kr : ka, len,
+                                         two ? len - own : len, si, sd, lane);
+        __syncwarp();
+        if (m <= 32) {
+          const int32_t id = lane < m ? si[lane] : -1;
+          const float dv = lane < m ? sd[lane] : 0.0f;
+          __syncwarp();
+          warp_prune_u8(fo, u, m, id, dv, lane);
+          if (lane == 0) mrg_counts[u] = -1;  // done here
+        } else {
+          for (int t = lane; t < m; t += 32) {
+            mrg_ids[lo + t] = si[t];
+            mrg_d[lo + t] = sd[t];
+          }
+          if (lane == 0) mrg_counts[u] = m;
+          __syncwarp();
+        }
+      } else if (lane == 0) {
+        mrg_counts[u] = -2;  // longer slices: merge_sort_kernel, next launch
+      }
+      ka = na;
+      kr = nr;
+    }
   }
 }
 
@@ -485,8 +776,27 @@ int add_reverse_and_prune(const float *X, const uint8_t *xu8, const int32_t *nor
 
   const unsigned sblocks =
       (unsigned)std::min<int64_t>((n + SORT_WARPS - 1) / SORT_WARPS, (int64_t)sms * 8);
-  merge_sort_kernel<<<sblocks, SORT_WARPS * 32, 0, stream>>>(
-      L.mrg_off, n, a_counts, L.keys, L.mrg_ids, L.mrg_d, L.mrg_counts, L.long_list, L.long_count);
+  // exact-integer rows on the tensor-core selection path, rng / slack, phase-A
+  // rows of <= 32 entries: short unions are pruned by the merging warp itself
+  FusedOut fo{xu8, norms, strategy, cos_alpha, (int)M, (int)out_width, out_ids, out_dists,
+              out_counts, dist_evals, angle_evals};
+  const bool fused = rev_fused_enabled() && xu8 && norms && d <= 128 && gram_enabled() &&
+                     L.prune_bytes >= gram_workspace(n) && strategy != 1 && M >= 1 &&
+                     out_width >= 1;
+  if (fused) {
+    const unsigned fblocks =
+        (unsigned)std::min<int64_t>((n + FUSED_WARPS - 1) / FUSED_WARPS, (int64_t)sms * FUSED_MINB);
+    merge_prune_kernel<<<fblocks, FUSED_WARPS * 32, 0, stream>>>(
+        L.mrg_off, n, a_counts, L.keys, L.mrg_ids, L.mrg_d, L.mrg_counts, row_order, fo);
+    PGK_CHECK_LAUNCH("merge_prune_kernel");
+    merge_sort_kernel<<<sblocks, SORT_WARPS * 32, 0, stream>>>(
+        L.mrg_off, n, a_counts, L.keys, L.mrg_ids, L.mrg_d, L.mrg_counts, L.long_list,
+        L.long_count, 1);
+  } else {
+    merge_sort_kernel<<<sblocks, SORT_WARPS * 32, 0, stream>>>(
+        L.mrg_off, n, a_counts, L.keys, L.mrg_ids, L.mrg_d, L.mrg_counts, L.long_list,
+        L.long_count, 0);
+  }
   PGK_CHECK_LAUNCH("merge_sort_kernel");
   long_sort_kernel<<<(unsigned)sms, 512, 0, stream>>>(L.mrg_off, L.keys, L.scratch,
                                                       L.long_list, L.long_count,
