@@ -723,7 +723,7 @@ struct KnnLayout {
   size_t total;
 };
 
-size_t tc_pool_workspace(int64_t n, int64_t nq, bool self);
+size_t tc_pool_workspace(int64_t n, int64_t nq, bool self, bool k1 = false);
 bool tc_pool_supported(int64_t d, int64_t k);
 size_t tiles_workspace(int64_t n, int64_t d);
 int64_t tiles_rows(int64_t n);

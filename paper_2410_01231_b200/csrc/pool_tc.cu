@@ -53,7 +53,10 @@ constexpr int CPP = HN / 32;      // 32-column epilogue chunks per part
 constexpr int CTAS_PER_SM = TC_CTAS;  // co-resident CTAs share the tensor core
 constexpr int TILE_BYTES = BN * KB;
 constexpr int NYBUF = ACC + 2;  // the MMA runs up to ACC tiles ahead of the epilogue
-constexpr int CAP = 1024;  // per-row candidate buffer (keys, global memory)
+#ifndef TC_CAP
+#define TC_CAP 512  // measured: same pass-2 / finalize times as 1024 (config 2), half the buffers
+#endif
+constexpr int CAP = TC_CAP;  // per-row candidate buffer (keys, global memory)
 constexpr int THREADS = 192;  // warp 0 TMA, warp 1 TMEM alloc + MMA, warps 2-5 epilogue
 constexpr int TMEM_COLS = ACC * BN;
 constexpr int GUESSED = 1 << 30;  // row_cnt flag: the row ran under a guessed threshold
@@ -157,7 +160,8 @@ enum { ST_WAIT, ST_MAIN, ST_SLOW, ST_COMPACT, ST_FINAL, ST_NSLOW, ST_NCOMPACT, S
 // DENSE_TILES tiles per row in the row's CAP x 8-byte slot, for
 // tc_kth_dense_kernel.  128 x the K-th smallest stored value bounds the K-th
 // smallest distance from above (within 128 of it): half the bytes of u32.
-constexpr int DENSE_TILES = 2 * CAP / BN;
+constexpr int DENSE_TILES = 16;  // u16 values: 16 tiles x 128 x 2 B = 4 KB of the row's slot
+static_assert(DENSE_TILES * BN * 2 <= CAP * 8, "dense pass-1 values must fit the row's buffer");
 constexpr int DENSE_Q = 7;  // quantisation: dist / 2^7, rounded up
 
 __device__ __forceinline__ uint32_t dense_val(int dist, int64_t col, int64_t n, int32_t pid,
@@ -1295,12 +1299,13 @@ bool make_bf16_tile_map(CUtensorMap *tm, const void *base, int64_t rows, int64_t
 // instrumentation (PGK_TILES_STATS): pass-1 order statistics per row
 uint32_t *g_dense_ostat = nullptr;
 
-size_t tc_pool_workspace(int64_t n, int64_t nq, bool self) {
-  const int sms = num_sms();
+// k1: the K = 1 pass whose epilogue writes the answer itself (the center
+// assignment) buffers no candidates: no per-row buffers (8 KB per row)
+size_t tc_pool_workspace(int64_t n, int64_t nq, bool self, bool k1) {
   size_t b = (size_t)n * tc::KB + 1024;
   if (!self) b += (size_t)nq * tc::KB + 1024;
   const int64_t rows = (nq + tc::BM - 1) / tc::BM * tc::BM;
-  b += (size_t)rows * tc::CAP * sizeof(uint64_t) + 1024;  // per-row candidate buffers
+  if (!k1) b += (size_t)rows * tc::CAP * sizeof(uint64_t) + 1024;  // per-row candidate buffers
   b += (size_t)rows * (sizeof(int32_t) + sizeof(uint64_t)) + 2048;
   b += 256;  // dynamic block-schedule counter
   return b;
@@ -1334,7 +1339,9 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   }
   if (!tc_pool_supported(d, K)) return PGK_OK;
   const bool self = (Q == X);
-  if (tc_bytes < tc_pool_workspace(n, nq, self)) {
+  // K == 1 into keys (not the pool arrays): the epilogue writes the answer
+  const int k1_direct = (K == 1 && !(out && !kth_only)) ? 1 : 0;
+  if (tc_bytes < tc_pool_workspace(n, nq, self, k1_direct != 0)) {
     set_error("tc pool workspace too small");
     return PGK_ERR_NOMEM;
   }
@@ -1343,7 +1350,7 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   uint8_t *qu8 = self ? xu8 : c.take<uint8_t>((size_t)nq * tc::KB);
   const int sms = num_sms();
   const int64_t rows = (nq + tc::BM - 1) / tc::BM * tc::BM;
-  uint64_t *bufs = c.take<uint64_t>((size_t)rows * tc::CAP);
+  uint64_t *bufs = k1_direct ? nullptr : c.take<uint64_t>((size_t)rows * tc::CAP);
   int32_t *row_cnt = c.take<int32_t>(rows);
   uint64_t *row_tau = c.take<uint64_t>(rows);
   int32_t *sched = c.take<int32_t>(1);
@@ -1381,8 +1388,6 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
   // pass-1 bounds over tile lists: dense distances + exact K-th selection
   const bool dense = kth_only && K > 1 && tlist;
   const char *se = getenv("PGK_TC_STATS");
-  // K == 1 into keys (not the pool arrays): the epilogue writes the answer
-  const int k1_direct = (K == 1 && !(out && !kth_only)) ? 1 : 0;
   if (dense) {
     tc::tc_pool_u8_kernel<false, true><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, nullptr, tlist, tlen,
@@ -1402,7 +1407,8 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
     PGK_CUDA(cudaMemsetAsync(dstats, 0, sizeof(unsigned long long) * tc::ST_COUNT, stream));
     tc::tc_pool_u8_kernel<true, false><<<grid, tc::THREADS, smem, stream>>>(
         tmX, tmQ, n, nq, exclude_self, xnorm, qnorm, K, bufs, keys, dstats, tlist, tlen,
-        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, 0, gate, gate_min);
+        tstride, perm, init_keys, shrink, row_cnt, row_tau, sched, row_mask, k1_direct, gate,
+        gate_min);
     PGK_CHECK_LAUNCH("tc_pool_u8_kernel<stats>");
     unsigned long long h[tc::ST_COUNT];
     PGK_CUDA(cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, stream));
@@ -1414,6 +1420,10 @@ int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, in
             "cycles; slow-chunks %.3g compactions %.3g; appends/row-block %.1f\n",
             h[0] / warps, h[1] / warps, h[2] / warps, h[3] / warps, h[4] / warps, h[5] / warps,
             h[6] / warps, (double)h[7] / (double)nq);
+    if (k1_direct) {
+      *handled = true;
+      return PGK_OK;
+    }
   } else {
     if (K == 1)
       tc::tc_pool_u8_kernel<false, false, true><<<grid, tc::THREADS, smem, stream>>>(

@@ -704,7 +704,7 @@ struct Layout {
 
 }  // namespace tiles
 
-size_t tc_pool_workspace(int64_t n, int64_t nq, bool self);
+size_t tc_pool_workspace(int64_t n, int64_t nq, bool self, bool k1 = false);
 int launch_norms_u8(const float *X, int64_t n, int d, int32_t *out, cudaStream_t stream);
 int launch_pool_tc_u8_lists(const float *X, int64_t n, int d, const float *Q, int64_t nq,
                             int exclude_self, const int32_t *xnorm, const int32_t *qnorm,
@@ -755,7 +755,7 @@ static tiles::Layout tiles_layout(void *ws, size_t bytes, int64_t n, int64_t d) 
   L.rr = c.take<int32_t>(NP + 32);
   L.U = c.take<double>(T);
   L.total = c.take<unsigned long long>(4);
-  L.sub_bytes = tc_pool_workspace(C, n, false);
+  L.sub_bytes = tc_pool_workspace(C, n, false, true);  // K = 1 assignment only
   L.sub_ws = c.take<char>(L.sub_bytes);
   L.bytes = c.off;
   return L;
@@ -1237,7 +1237,7 @@ static tiles::LayoutF32 tiles_layout_f32(void *ws, size_t bytes, int64_t n, int6
   L.dcm = c.take<float>((size_t)T * T);
   L.U = c.take<double>(T);
   L.keys1 = c.take<uint64_t>((size_t)n * K);
-  L.sub_bytes = tc_pool_workspace(C, n, false);
+  L.sub_bytes = tc_pool_workspace(C, n, false, true);  // K = 1 assignment only
   L.sub_ws = c.take<char>(L.sub_bytes);
   L.tcf_bytes = tcf32_supported(d, K) ? tcf32_workspace(NP, T, d) : 0;
   L.tcf_ws = L.tcf_bytes ? c.take<char>(L.tcf_bytes) : nullptr;
