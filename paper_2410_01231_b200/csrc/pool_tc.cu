@@ -54,7 +54,8 @@ constexpr int CTAS_PER_SM = TC_CTAS;  // co-resident CTAs share the tensor core
 constexpr int TILE_BYTES = BN * KB;
 constexpr int NYBUF = ACC + 2;  // the MMA runs up to ACC tiles ahead of the epilogue
 #ifndef TC_CAP
-#define TC_CAP 512  // measured: same pass-2 / finalize times as 1024 (config 2), half the buffers
+#define TC_CAP 1024  // 512: same pass-2 / finalize times at config 2 and half the buffers, but the
+                     // finalize faults on non-integer rows pushed through this path (unresolved)
 #endif
 constexpr int CAP = TC_CAP;  // per-row candidate buffer (keys, global memory)
 constexpr int THREADS = 192;  // warp 0 TMA, warp 1 TMEM alloc + MMA, warps 2-5 epilogue
@@ -1001,6 +1002,11 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, FIN_MINB)
       continue;
     }
     const int64_t orow = perm ? (int64_t)perm[r] : r;
+#ifdef TC_DEBUG
+    if (lane == 0 && (cnt > CAP || orow < 0 || orow >= nrows))
+      printf("[tc_finalize] r=%lld raw=%d cnt=%d orow=%lld K=%d nrows=%lld\n", (long long)r, raw,
+             cnt, (long long)orow, K, (long long)nrows);
+#endif
     if (K == 1) {  // the kernel's threshold is the answer
       const uint64_t tau = row_tau[r];
       if (lane == 0) {

@@ -120,9 +120,13 @@ class RngBuilder:
         """Build a sequence of datasets of this shape from pinned host arrays
         (hosts[i]: (n, d) float32) into pinned outputs (host_outs[i]: (ids,
         counts), as build's host_out), double-buffered: dataset i+1 is copied
-        to the device on a side stream while dataset i is being built, so the
-        transfers hide under the builds instead of preceding them.  Every
-        dataset's own copy happens inside the call.  The exact-integer check
+        to the device on a side stream while dataset i is being built, and
+        dataset i's adjacency rows and degrees (written to one of two device
+        output sets) are copied out on a third stream under build i+1, so the
+        transfers of both directions hide under the builds instead of
+        preceding / following them (the zero-copy output of build() would
+        stretch the last kernels to the PCIe rate: 132 MB per build at config
+        2).  Every dataset's own copies happen inside the call.  The exact-integer check
         runs on the device per dataset; a dataset that fails it is rebuilt
         through the float path at the end.  Returns the BuildOutputs (device
         tensors of the last build are overwritten by the next; the host
@@ -141,15 +145,19 @@ class RngBuilder:
             self._stream = (torch.cuda.Stream(device=dev),
                             [torch.empty((self.n, self.d), dtype=torch.float32, device=dev)
                              for _ in range(2)],
-                            torch.ones(max(k, 1), dtype=torch.int32, device=dev))
-        cs, xb, flags = self._stream
+                            torch.ones(max(k, 1), dtype=torch.int32, device=dev),
+                            torch.cuda.Stream(device=dev),
+                            [self.b_out, tuple(torch.empty_like(t) for t in self.b_out)])
+        cs, xb, flags, osr, bouts = self._stream
         if flags.numel() < k:
             flags = torch.ones(k, dtype=torch.int32, device=xb[0].device)
-            self._stream = (cs, xb, flags)
+            self._stream = (cs, xb, flags, osr, bouts)
         main = torch.cuda.current_stream()
         flags[:k].fill_(1)
         landed = [torch.cuda.Event() for _ in range(k)]
         freed = [torch.cuda.Event() for _ in range(k)]
+        built = [torch.cuda.Event() for _ in range(k)]
+        copied = [torch.cuda.Event() for _ in range(k)]
         cs.wait_stream(main)  # earlier work on these buffers is done
         with torch.cuda.stream(cs):
             xb[0].copy_(hosts[0], non_blocking=True)
@@ -168,8 +176,19 @@ class RngBuilder:
             if self.mode == _lib.POOL_U8 and self.d <= 128:
                 _lib.check(L.pgk_detect_u8_async(_lib.ptr(X), self.n, self.d,
                                                  _lib.ptr(flags[i:i + 1]), _lib.stream_handle()))
-            outs.append(self.build(X, host_outs[i]))
+            if i >= 2:  # this output set's previous copy-out is done
+                main.wait_event(copied[i - 2])
+            self.b_out = bouts[i % 2]
+            outs.append(self.build(X, None))
             freed[i].record(main)
+            built[i].record(main)
+            with torch.cuda.stream(osr):
+                osr.wait_event(built[i])
+                host_outs[i][0].copy_(outs[i].ids, non_blocking=True)
+                host_outs[i][1].copy_(outs[i].counts, non_blocking=True)
+                copied[i].record(osr)
+        self.b_out = bouts[0]
+        main.wait_stream(osr)
         if self.mode == _lib.POOL_U8 and self.d <= 128:
             bad = torch.nonzero(flags[:k] == 0).flatten().tolist()  # one read at the end
             for i in bad:  # not exact-integer after all: the float path
