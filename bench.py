@@ -469,7 +469,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(N * R * 4 + N * 4),
                 "api": "RngBuilder.build_host_stream: the K steps' datasets from pinned host "
                        "memory, each copied in and its adjacency + degrees copied out inside "
-                       "the timed region; dataset i+1's copy overlaps build i",
+                       "the timed region; dataset i+1's copy-in and dataset i-1's copy-out (third stream, two device output sets) overlap build i",
                 "single_call": {"value": e2e_single, "unit": UNIT,
                                 "api": "RngBuilder.build_host per step (chunked copy "
                                        "overlapped with the per-row work; copy and build "

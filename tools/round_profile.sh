@@ -17,3 +17,6 @@ ncu --set full --import-source on --clock-control none -k regex:tc_pool_u8_kerne
 ncu --set full --import-source on --clock-control none -k regex:tc_finalize -c 1 \
     -o $o/${tag}_fin python tools/prof_path.py --stage pool --config 2 --n 1000000 --reps 1 \
     > $o/${tag}_ncu_fin.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:merge_prune_kernel -c 1 \
+    -o $o/${tag}_mprune python tools/prof_path.py --stage all --config 2 --n 1000000 --reps 1 \
+    > $o/${tag}_ncu_mprune.log 2>&1
