@@ -54,7 +54,11 @@ __global__ void norms_u8_kernel(const float *__restrict__ X, int64_t n, int d,
        r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     int acc = 0;
     for (int i = lane; i < d; i += 32) {
-      int v = (int)X[r * d + i];
+      // the norm of the row AS STORED (u8 bytes): for exact-integer data the
+      // value itself; for anything else (a caller's optimistic exact-integer
+      // attempt, rejected later by the device check) still consistent with the
+      // u8 rows, so the pass stays a well-formed exact k-NN of those bytes
+      const int v = (int)(uint8_t)__float2int_rn(X[r * d + i]);
       acc += v * v;
     }
 #pragma unroll

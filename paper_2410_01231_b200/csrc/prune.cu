@@ -804,7 +804,7 @@ __global__ void make_u8_kernel(const float *__restrict__ X, int64_t n, int d,
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int c = lane + 32 * k;
-      const int v = c < d ? __float2int_rn(X[r * d + c]) : 0;
+      const int v = c < d ? (int)(uint8_t)__float2int_rn(X[r * d + c]) : 0;  // norm of the stored byte
       out[r * 128 + c] = (uint8_t)v;
       acc += v * v;
     }

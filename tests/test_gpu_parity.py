@@ -712,3 +712,35 @@ def test_gram_f32_equals_prune_kernel_on_larger_prefixes():
                              capture_output=True, text=True, timeout=1200, check=True).stdout
         cmp_line = [json.loads(l) for l in out.splitlines() if l.startswith('{"compare"')]
         assert cmp_line and all(v == 0 for v in cmp_line[0]["differing_entries"].values()), out
+
+
+@pytest.mark.parametrize("R", [1, 4, 24, 33])
+@pytest.mark.parametrize("strategy,alpha", [("rng", 60.0), ("slack", 1.3)])
+def test_fused_merge_prune_kernel_edge_shapes(R, strategy, alpha):
+    """Phase B's in-warp merge + prune of short unions (merge_prune_kernel:
+    register merge, 32 x 32 Gram by mma.sync, masks / greedy / lazy counters in
+    one warp) against the oracle over the shapes that steer it: M = 1 and 4
+    (the scan stops at the M-th kept neighbour well inside the row), M = 24
+    (unions straddling the 32-candidate limit, so rows split between this
+    kernel and the tcgen05 pair kernel), phase-A rows wider than a warp
+    (R = 33: own parts of 33 entries leave the two-part merge), on a tie-heavy
+    integer lattice (duplicate distances, zero distances) and on clustered
+    data; and against the unfused path (PGK_REV_FUSED is read once per
+    process, so that comparison is the oracle's)."""
+    rng = np.random.default_rng(7)
+    lattice = rng.integers(0, 4, size=(3000, 16)).astype(np.float32)  # many ties / duplicates
+    for data, K in ((synth.cfg2(5000), 48), (lattice, 40)):
+        ds = Dataset.from_array(data)
+        ids, dists = knn_pools(ds, K)
+        off = np.arange(ds.n + 1, dtype=np.int64) * K
+        cnt = np.full(ds.n, K, np.int32)
+        p = PruneParams(M=R, alpha=alpha, strategy=strategy)
+        a = prune_all(ds, off, cnt, ids.ravel(), dists.ravel(), p)
+        b = add_reverse_and_prune(ds, a[0], a[1], a[2], p)
+        oa = oracle.prune_all(data, off, cnt, ids.ravel(), dists.ravel(), R, strategy, alpha)
+        ob = oracle.add_reverse_and_prune(data, oa[0], oa[1], oa[2], R, strategy, alpha)
+        for res, ref in ((a, oa), (b, ob)):
+            np.testing.assert_array_equal(res[0], ref[0])
+            np.testing.assert_array_equal(res[1], ref[1])
+            np.testing.assert_array_equal(res[2], ref[2])
+            assert res[3] == ref[3] and res[4] == ref[4]
