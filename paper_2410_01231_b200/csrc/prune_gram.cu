@@ -53,6 +53,9 @@ constexpr int C = 128;          // candidates per point (TMEM lanes)
 #ifndef GRAM_TMA_SINGLE
 #define GRAM_TMA_SINGLE 0  // 1: lane 0 issues all gather4 ops from shared-memory ids
 #endif
+#ifndef GRAM_TMA_UNIFORM
+#define GRAM_TMA_UNIFORM 0  // 1: warp-uniform gather4 issue loop (lane g's ids broadcast, lane 0 issues)
+#endif
 #ifndef GRAM_TMA_ROWS
 #define GRAM_TMA_ROWS 64  // with GRAM_ROWS_CPASYNC: rows per point left to TMA gather4
 #endif
@@ -327,6 +330,24 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
           }
         }
         __syncwarp();
+#elif GRAM_TMA_UNIFORM
+        // warp-uniform issue loop: pass g broadcasts lane g's four row ids and
+        // lane 0 issues; no per-lane ELECT / branch waterfall, and the passes
+        // are independent, so their register -> uniform-register moves overlap
+        {
+          uint8_t *tb = s.tile[stage] + (r0 >> 3) * 1024;
+          uint64_t *fb = &s.full[stage];
+#pragma unroll 4
+          for (int g = 0; g < ngt; ++g) {
+            const int32_t a = __shfl_sync(0xffffffffu, i0[0], g);
+            const int32_t b1 = __shfl_sync(0xffffffffu, i0[1], g);
+            const int32_t b2 = __shfl_sync(0xffffffffu, i0[2], g);
+            const int32_t b3 = __shfl_sync(0xffffffffu, i0[3], g);
+            if (lane == 0)
+              tma_gather4(tb + (g >> 1) * 1024 + (g & 1) * 512, &tmX, fb, 0, a, b1 >= 0 ? b1 : a,
+                          b2 >= 0 ? b2 : a, b3 >= 0 ? b3 : a);
+          }
+        }
 #else
         if (lane < ngt) {
           const int32_t a = i0[0];

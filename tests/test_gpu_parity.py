@@ -744,3 +744,44 @@ def test_fused_merge_prune_kernel_edge_shapes(R, strategy, alpha):
             np.testing.assert_array_equal(res[1], ref[1])
             np.testing.assert_array_equal(res[2], ref[2])
             assert res[3] == ref[3] and res[4] == ref[4]
+
+
+def test_build_host_falls_back_when_tiles_are_not_supported():
+    """RngBuilder.build_host on shapes the tile-pruned pipeline does not take
+    (pgk_tiles_supported false: K > 256 here, PGK_DISABLE_PRUNE=1 in a
+    subprocess -- the switch is read once per process) copies, then builds:
+    same rows as the device build instead of a ValueError."""
+    import os
+    import subprocess
+    import sys
+    from paper_2410_01231_b200 import _lib
+    from paper_2410_01231_b200.index import RngBuilder
+    n, K, R = 6000, 300, 24
+    assert not _lib.lib().pgk_tiles_supported(n, 128, K)
+    data = synth.cfg2(n)
+    X = torch.from_numpy(data).cuda()
+    ref = RngBuilder(n, 128, K, PruneParams(M=R), _lib.POOL_U8).build(X)
+    b = RngBuilder(n, 128, K, PruneParams(M=R), _lib.POOL_U8)
+    h_ids = torch.full((n, R), 7, dtype=torch.int32).pin_memory()
+    h_cnt = torch.zeros(n, dtype=torch.int32).pin_memory()
+    b.build_host(torch.from_numpy(data).pin_memory(), host_out=(h_ids, h_cnt))
+    torch.cuda.synchronize()
+    assert torch.equal(h_ids, ref.ids.cpu()) and torch.equal(h_cnt, ref.counts.cpu())
+    code = (
+        "import torch, numpy as np\n"
+        "from paper_2410_01231_b200 import _lib, synth, PruneParams\n"
+        "from paper_2410_01231_b200.index import RngBuilder\n"
+        "n, K, R = 6000, 64, 24\n"
+        "assert not _lib.lib().pgk_tiles_supported(n, 128, K)\n"
+        "data = synth.cfg2(n)\n"
+        "ref = RngBuilder(n, 128, K, PruneParams(M=R), _lib.POOL_U8).build(torch.from_numpy(data).cuda())\n"
+        "h = (torch.zeros((n, R), dtype=torch.int32).pin_memory(), torch.zeros(n, dtype=torch.int32).pin_memory())\n"
+        "RngBuilder(n, 128, K, PruneParams(M=R), _lib.POOL_U8).build_host(torch.from_numpy(data).pin_memory(), host_out=h)\n"
+        "torch.cuda.synchronize()\n"
+        "assert torch.equal(h[0], ref.ids.cpu()) and torch.equal(h[1], ref.counts.cpu())\n"
+        "print('ok')\n")
+    env = dict(os.environ, PGK_DISABLE_PRUNE="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
