@@ -64,7 +64,16 @@ constexpr int GUESSED = 1 << 30;  // row_cnt flag: the row ran under a guessed t
 struct __align__(1024) Smem {
   uint8_t a[BM * KB];
   uint8_t b[STAGES][TILE_BYTES];
-  int32_t sv[4][32 * 36];  // per epilogue warp: one chunk of dot products per lane
+#ifndef TC_APPEND_UNROLL
+#define TC_APPEND_UNROLL 2
+#endif
+#ifndef TC_PAIR_APPEND
+#define TC_PAIR_APPEND 1  // survivors of a 64-column part appended in one loop (K > 1 pass 2):
+                          // 3.51 -> 3.22 ms at config 2; 0 = one loop per 32-column chunk
+#endif
+  // per epilogue warp: one chunk (TC_PAIR_APPEND: one part = two chunks) of dot
+  // products per lane
+  int32_t sv[4][32 * (TC_PAIR_APPEND ? 68 : 36)];  // lane stride = 4 (mod 32) words: conflict-free STS.128
   // |x|^2 and original ids (pruned path) of the tile's columns, 3 buffers by
   // running tile count: the MMA warp prefetches tile g+1's while the
   // epilogue may still read tile g-1's
@@ -155,19 +164,33 @@ enum { ST_WAIT, ST_MAIN, ST_SLOW, ST_COMPACT, ST_FINAL, ST_NSLOW, ST_NCOMPACT, S
        ST_COUNT };
 
 // DENSE (pass-1 bound mode): no threshold, no survivor lists -- every row
-// stores every column's distance, densely, as u16 ceil(dist / 128) (exact
-// u8 distances are < 2^23, so < 0xfffe; 0xffff = invalid), at most
+// stores every column's distance, densely, as u16 ceil(dist / 2^DENSE_Q)
+// (exact u8 distances are < 2^23; the top value = invalid), at most
 // DENSE_TILES tiles per row in the row's CAP x 8-byte slot, for
-// tc_kth_dense_kernel.  128 x the K-th smallest stored value bounds the K-th
-// smallest distance from above (within 128 of it): half the bytes of u32.
+// tc_kth_dense_kernel.  2^DENSE_Q x the K-th smallest stored value bounds the
+// K-th smallest distance from above (within 2^DENSE_Q of it): half the bytes
+// of u32.
 constexpr int DENSE_TILES = 16;  // u16 values: 16 tiles x 128 x 2 B = 4 KB of the row's slot
 static_assert(DENSE_TILES * BN * 2 <= CAP * 8, "dense pass-1 values must fit the row's buffer");
+#ifndef TC_DENSE_PACKED
+#define TC_DENSE_PACKED 1  // 15-bit values (dist / 2^8), counted two per instruction in the K-th search
+#endif
+#if TC_DENSE_PACKED
+// values < 2^15 (u8 distances < 2^23; 0x7fff = invalid): two per 32-bit word,
+// and (mid + 0x8000 - v) has bit 15 set iff v <= mid with no borrow between
+// the halves, so one subtraction compares both
+constexpr int DENSE_Q = 8;  // quantisation: dist / 2^8, rounded up
+constexpr uint32_t DENSE_INVALID = 0x7fffu, DENSE_VMAX = 0x7ffeu;
+#else
 constexpr int DENSE_Q = 7;  // quantisation: dist / 2^7, rounded up
+constexpr uint32_t DENSE_INVALID = 0xffffu, DENSE_VMAX = 0xfffeu;
+#endif
 
 __device__ __forceinline__ uint32_t dense_val(int dist, int64_t col, int64_t n, int32_t pid,
                                               bool self) {
-  return (col < n && pid >= 0 && !self) ? min(((uint32_t)dist + 127u) >> DENSE_Q, 0xfffeu)
-                                        : 0xffffu;
+  return (col < n && pid >= 0 && !self)
+             ? min(((uint32_t)dist + ((1u << DENSE_Q) - 1u)) >> DENSE_Q, DENSE_VMAX)
+             : DENSE_INVALID;
 }
 
 // K1: the K = 1 (nearest neighbour) instantiation; the K > 1 one carries no
@@ -329,7 +352,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
     // ---------------- epilogue ----------------
     const int q = warp & 3;  // TMEM lane quarter this warp may access (warp % 4)
     int32_t *const svw = s.sv[warp - 2];  // this warp's staging: lane l at svw[l * 36]
-    int32_t *sv = svw + lane * 36;
+    int32_t *sv = svw + lane * (TC_PAIR_APPEND ? 68 : 36);
     uint32_t g = 0;  // tiles consumed by this CTA (accumulator g % ACC, norm buffer g % NYBUF)
     for (int it = 0;; ++it) {
       mbar_wait(&s.a_full, it & 1);
@@ -384,6 +407,127 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
         const int aslot = (int)(g % ACC);
         const uint32_t acc_phase = (g / ACC) & 1;
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + aslot * BN;
+#if TC_PAIR_APPEND
+        if (!STATS && !DENSE && !K1) {
+          // One 64-column part at a time: both chunks' survivor masks first (raw
+          // dot products of chunks with survivors staged per lane), the part
+          // handed back to the MMA, then ONE append loop over the part's
+          // survivors: its trip count is the warp's maximum per-row survivor
+          // count of the part (less than the sum of the two chunks' maxima) and
+          // the per-chunk ballots / reductions are paid once.
+          static_assert(CPP == 2, "a part is two 32-column chunks");
+          static_assert(CAP >= 256 + 64, "room for K <= 256 plus one part");
+#pragma unroll 1
+          for (int part = 0; part < HALVES; ++part) {
+            if (part == 0) mbar_wait(&s.nfull[tpar], (g / NYBUF) & 1);  // the tile's norms / ids
+            mbar_wait(&s.tfull[aslot][part], acc_phase);
+            tc_fence_after();
+            uint32_t mk[2];
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+              const int c = part * 2 + cc;
+              uint32_t r[32];
+              tmem_ld32(tbase + c * 32, r);
+              tmem_wait_ld();
+              const int64_t cb = col0 + c * 32;
+              const int4 *nyp = reinterpret_cast<const int4 *>(s.ny[tpar] + c * 32);
+              uint32_t mask = 0;
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                const int4 w = nyp[v];
+                mask |= ((w.x - 2 * (int)r[4 * v]) <= tp) ? (1u << (4 * v)) : 0u;
+                mask |= ((w.y - 2 * (int)r[4 * v + 1]) <= tp) ? (1u << (4 * v + 1)) : 0u;
+                mask |= ((w.z - 2 * (int)r[4 * v + 2]) <= tp) ? (1u << (4 * v + 2)) : 0u;
+                mask |= ((w.w - 2 * (int)r[4 * v + 3]) <= tp) ? (1u << (4 * v + 3)) : 0u;
+              }
+              if (__any_sync(0xffffffffu, mask != 0)) {
+                if (__any_sync(0xffffffffu, tp >= 0x3f000000)) {  // rows without a threshold
+                  const int64_t colj = cb + lane;
+                  const int32_t cidj = perm ? s.pid[tpar][c * 32 + lane] : (int32_t)colj;
+                  mask &= __ballot_sync(0xffffffffu, colj < n && cidj >= 0);
+                }
+                if (exclude_self && row >= cb && row < cb + 32) mask &= ~(1u << (int)(row - cb));
+                if (mask) {
+#pragma unroll
+                  for (int v = 0; v < 8; ++v)
+                    reinterpret_cast<int4 *>(sv + cc * 32)[v] = make_int4(
+                        (int)r[4 * v], (int)r[4 * v + 1], (int)r[4 * v + 2], (int)r[4 * v + 3]);
+                }
+              }
+              mk[cc] = mask;
+            }
+            // the part's columns are consumed (registers / staging): the MMA may reuse it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.tempty[aslot][part]);
+            const uint32_t m0 = mk[0], m1 = mk[1];
+            if (__any_sync(0xffffffffu, (m0 | m1) != 0)) {
+              const int32_t *tny = s.ny[tpar] + part * 64;
+              const int32_t *tpid = s.pid[tpar] + part * 64;
+              const int64_t cb = col0 + part * 64;
+              const int np = __popc(m0) + __popc(m1);
+              const bool track = tau == KEY_MAX && np;
+              if (track) {  // rare: rows still without a threshold
+                for (unsigned mm = m0; mm; mm &= mm - 1) {
+                  const int j = __ffs(mm) - 1;
+                  smax = max(smax, tny[j] - 2 * sv[j]);
+                }
+                for (unsigned mm = m1; mm; mm &= mm - 1) {
+                  const int j = __ffs(mm) - 1;
+                  smax = max(smax, tny[32 + j] - 2 * sv[32 + j]);
+                }
+              }
+              unsigned need = __ballot_sync(0xffffffffu, cnt + np > CAP);
+              while (need) {
+                const int src = __ffs(need) - 1;
+                need &= need - 1;
+                const int c_src = __shfl_sync(0xffffffffu, cnt, src);
+                const uint64_t t_src = __shfl_sync(0xffffffffu, tau, src);
+                const uint64_t nt = select_k(wbuf + (size_t)src * CAP, c_src, K,
+                                             t_src == KEY_MAX ? 0xffffffffu : khi(t_src), lane);
+                if (lane == src) {
+                  cnt = K;
+                  tau = (uint64_t)(khi(nt) + 1) << 32;
+                  tp = row_tp(tau, nx, K);
+                }
+              }
+              uint64_t *mybuf = wbuf + (size_t)lane * CAP + cnt;
+              const int trips = (int)__reduce_max_sync(0xffffffffu, (unsigned)np);
+              unsigned mm0 = m0, mm1 = m1;
+#if TC_APPEND_UNROLL == 4
+#pragma unroll 4
+#elif TC_APPEND_UNROLL == 1
+#pragma unroll 1
+#else
+#pragma unroll 2
+#endif
+              for (int it = 0; it < trips; ++it) {
+                const bool a0 = mm0 != 0;
+                const unsigned mc = a0 ? mm0 : mm1;
+                const bool act = mc != 0;
+                const int j = act ? __ffs(mc) - 1 : 0;
+                const int cj = (a0 ? 0 : 32) + j;   // column within the part = staging slot
+                const int32_t cid = perm ? tpid[cj] : (int32_t)(cb + cj);
+                const uint64_t key =
+                    ((uint64_t)(uint32_t)(tny[cj] - 2 * sv[cj] + nx) << 32) | (uint32_t)cid;
+                if (act) *mybuf = key;
+                mybuf += act ? 1 : 0;
+                const unsigned nm = mc & (mc - 1);
+                mm0 = a0 ? nm : mm0;
+                mm1 = a0 ? mm1 : nm;
+              }
+              cnt += np;
+              if (track && cnt >= K) {
+                tau = (uint64_t)((uint32_t)(smax + nx) + 1) << 32;
+                tp = row_tp(tau, nx, K);
+              }
+              __syncwarp();
+            }
+          }
+          ++g;
+          continue;
+        }
+#endif
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           if (c == 0) mbar_wait(&s.nfull[tpar], (g / NYBUF) & 1);  // the tile's norms / ids
@@ -1051,10 +1195,49 @@ template <int VPL>
 __device__ __noinline__ uint32_t kth_dense(const uint16_t *__restrict__ buf, int cnt, int K,
                                            int lane) {
   static_assert(VPL % 2 == 0, "values are loaded in u16 pairs");
+  const uint32_t *buf2 = reinterpret_cast<const uint32_t *>(buf);  // cnt is a multiple of 128
+#if TC_DENSE_PACKED
+  // words of two 15-bit values; invalid (0x7fff) never counts: mid stays
+  // below it.  Past cnt: two invalid values.
+  uint32_t w2[VPL / 2];
+  int nv = 0;
+  uint32_t vmin = 0xffffffffu, vmax = 0;
+#pragma unroll
+  for (int i = 0; i < VPL / 2; ++i) {
+    const int idx = i * 32 + lane;  // word: values 2 idx, 2 idx + 1 (order is irrelevant)
+    const uint32_t w = 2 * idx < cnt ? buf2[idx] : 0x7fff7fffu;
+    w2[i] = w;
+    const uint32_t a = w & 0xffffu, b = w >> 16;
+    if (a != DENSE_INVALID) {
+      ++nv;
+      vmin = min(vmin, a);
+      vmax = max(vmax, a);
+    }
+    if (b != DENSE_INVALID) {
+      ++nv;
+      vmin = min(vmin, b);
+      vmax = max(vmax, b);
+    }
+  }
+  if ((int)__reduce_add_sync(0xffffffffu, (unsigned)nv) < K) return 0xffffffffu;
+  uint32_t lo = __reduce_min_sync(0xffffffffu, vmin);
+  uint32_t hi = __reduce_max_sync(0xffffffffu, vmax);
+  const uint32_t tol = (hi - lo) >> 10;
+  while (hi - lo > tol) {
+    const uint32_t mid = lo + ((hi - lo) >> 1);
+    const uint32_t m2 = (mid | (mid << 16)) + 0x80008000u;
+    uint32_t c2 = 0;  // two 16-bit counters (VPL / 2 <= 32 words per lane)
+#pragma unroll
+    for (int i = 0; i < VPL / 2; ++i) c2 += ((m2 - w2[i]) >> 15) & 0x00010001u;
+    const unsigned c = (c2 & 0xffffu) + (c2 >> 16);
+    if ((int)__reduce_add_sync(0xffffffffu, c) >= K) hi = mid;
+    else lo = mid + 1;
+  }
+  return hi;
+#else
   uint32_t v[VPL];
   int nv = 0;
   uint32_t vmin = 0xffffffffu, vmax = 0;
-  const uint32_t *buf2 = reinterpret_cast<const uint32_t *>(buf);  // cnt is a multiple of 128
 #pragma unroll
   for (int i = 0; i < VPL / 2; ++i) {
     const int idx = i * 32 + lane;  // word: values 2 idx, 2 idx + 1 (order is irrelevant)
@@ -1083,6 +1266,7 @@ __device__ __noinline__ uint32_t kth_dense(const uint16_t *__restrict__ buf, int
     else lo = mid + 1;
   }
   return hi;
+#endif
 }
 
 // Pass-1 bound of every row from its dense distances (warp per row): an

@@ -371,7 +371,8 @@ __device__ __forceinline__ int merge_own_rev(const uint64_t *__restrict__ keys, 
 //     formulas), on one 32-bit mask per candidate.
 // No shared-memory tiles, no TMEM, no barriers; the merged row never travels
 // through HBM.  Rows with more than 32 merged candidates are written to the
-// merged CSR as before and listed (todo) for the tcgen05 kernels.
+// merged CSR as before for the tcgen05 kernels; slices too long for the
+// two-part merge are listed (todo) for merge_sort_kernel.
 __device__ __forceinline__ void mma_u8_16832(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                              uint32_t a3, uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -544,12 +545,14 @@ __global__ void __launch_bounds__(SORT_WARPS * 32)
                       int32_t *__restrict__ mrg_ids, float *__restrict__ mrg_d,
                       int32_t *__restrict__ mrg_counts,
                       int32_t *__restrict__ long_list,
-                      int32_t *__restrict__ long_count, int only_flagged) {
+                      int32_t *__restrict__ long_count,
+                      const int32_t *__restrict__ todo, const int32_t *__restrict__ todo_count) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t u = (int64_t)blockIdx.x * SORT_WARPS + warp; u < n;
-       u += (int64_t)gridDim.x * SORT_WARPS) {
-    // after merge_prune_kernel: only the slices it left (mrg_counts == -2)
-    if (only_flagged && mrg_counts[u] != -2) continue;
+  // after merge_prune_kernel: only the slices it listed (todo), else every row
+  const int64_t rows = todo ? (int64_t)*todo_count : n;
+  for (int64_t i = (int64_t)blockIdx.x * SORT_WARPS + warp; i < rows;
+       i += (int64_t)gridDim.x * SORT_WARPS) {
+    const int64_t u = todo ? (int64_t)todo[i] : i;
     const int64_t lo = mrg_off[u];
     const int len = (int)(mrg_off[u + 1] - lo);
     if (len > SORT_SMEM_KEYS) {
@@ -576,7 +579,8 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, FUSED_MINB)
                        const int32_t *__restrict__ own_counts,
                        const uint64_t *__restrict__ keys,
                        int32_t *__restrict__ mrg_ids, float *__restrict__ mrg_d,
-                       int32_t *__restrict__ mrg_counts,
+                       int32_t *__restrict__ mrg_counts, int32_t *__restrict__ todo,
+                       int32_t *__restrict__ todo_count,
                        const int32_t *__restrict__ row_order, const FusedOut fo) {
   __shared__ int32_t sh_ids[FUSED_WARPS][64];
   __shared__ float sh_d[FUSED_WARPS][64];
@@ -642,7 +646,7 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, FUSED_MINB)
           __syncwarp();
         }
       } else if (lane == 0) {
-        mrg_counts[u] = -2;  // longer slices: merge_sort_kernel, next launch
+        todo[atomicAdd(todo_count, 1)] = (int32_t)u;  // longer slices: merge_sort_kernel, next launch
       }
       ka = na;
       kr = nr;
@@ -693,7 +697,7 @@ __global__ void long_sort_kernel(const int64_t *__restrict__ mrg_off,
 }
 
 struct RevLayout {
-  int32_t *rev_cnt, *rev_left, *long_list, *long_count;
+  int32_t *rev_cnt, *rev_left, *long_list, *long_count, *todo_list, *todo_count;
   int64_t *mrg_off;
   uint64_t *keys, *scratch;
   int32_t *mrg_ids, *mrg_counts;
@@ -712,6 +716,8 @@ static RevLayout rev_layout(void *ws, size_t ws_bytes, int64_t n, int64_t width)
   L.rev_left = c.take<int32_t>(n);
   L.long_list = c.take<int32_t>(n);
   L.long_count = c.take<int32_t>(1);
+  L.todo_list = c.take<int32_t>(n);
+  L.todo_count = c.take<int32_t>(1);
   L.mrg_off = c.take<int64_t>(n + 1);
   L.mrg_counts = c.take<int32_t>(n);
   L.keys = c.take<uint64_t>(cap);
@@ -753,6 +759,7 @@ int add_reverse_and_prune(const float *X, const uint8_t *xu8, const int32_t *nor
 
   PGK_CUDA(cudaMemsetAsync(L.rev_cnt, 0, sizeof(int32_t) * n, stream));
   PGK_CUDA(cudaMemsetAsync(L.long_count, 0, sizeof(int32_t), stream));
+  PGK_CUDA(cudaMemsetAsync(L.todo_count, 0, sizeof(int32_t), stream));
   rev_count_kernel<<<rblocks, 256, 0, stream>>>(a_ids, a_counts, n, (int)a_width, L.rev_cnt);
   PGK_CHECK_LAUNCH("rev_count_kernel");
 
@@ -787,15 +794,16 @@ int add_reverse_and_prune(const float *X, const uint8_t *xu8, const int32_t *nor
     const unsigned fblocks =
         (unsigned)std::min<int64_t>((n + FUSED_WARPS - 1) / FUSED_WARPS, (int64_t)sms * FUSED_MINB);
     merge_prune_kernel<<<fblocks, FUSED_WARPS * 32, 0, stream>>>(
-        L.mrg_off, n, a_counts, L.keys, L.mrg_ids, L.mrg_d, L.mrg_counts, row_order, fo);
+        L.mrg_off, n, a_counts, L.keys, L.mrg_ids, L.mrg_d, L.mrg_counts, L.todo_list,
+        L.todo_count, row_order, fo);
     PGK_CHECK_LAUNCH("merge_prune_kernel");
     merge_sort_kernel<<<sblocks, SORT_WARPS * 32, 0, stream>>>(
         L.mrg_off, n, a_counts, L.keys, L.mrg_ids, L.mrg_d, L.mrg_counts, L.long_list,
-        L.long_count, 1);
+        L.long_count, L.todo_list, L.todo_count);
   } else {
     merge_sort_kernel<<<sblocks, SORT_WARPS * 32, 0, stream>>>(
         L.mrg_off, n, a_counts, L.keys, L.mrg_ids, L.mrg_d, L.mrg_counts, L.long_list,
-        L.long_count, 0);
+        L.long_count, nullptr, nullptr);
   }
   PGK_CHECK_LAUNCH("merge_sort_kernel");
   long_sort_kernel<<<(unsigned)sms, 512, 0, stream>>>(L.mrg_off, L.keys, L.scratch,
