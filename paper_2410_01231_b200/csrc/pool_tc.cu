@@ -551,9 +551,34 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
           const int4 *nyp = reinterpret_cast<const int4 *>(s.ny[tpar] + c * 32);
           if (DENSE) {
             if (row_ok && t < DENSE_TILES) {
-              const int4 *pp = reinterpret_cast<const int4 *>(s.pid[tpar] + c * 32);
               uint2 *dst = reinterpret_cast<uint2 *>(reinterpret_cast<uint16_t *>(bufs + row * CAP) +
                                                      t * BN + c * 32);
+#if TC_DENSE_PACKED
+              // Columns that are no points (padding slots of the tile sort,
+              // columns past n) carry |x|^2 = 0x3f3f3f3f: their value clamps to
+              // DENSE_VMAX, above every real distance, so counting them cannot
+              // lower a row's K-th value below its K-th real distance -- no
+              // per-value validity test.  Only the row's own column must not
+              // count, and it lies in one chunk (rows of a warp share row / 32).
+              uint32_t a[32];
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                const int4 w = nyp[v];
+                a[4 * v] = min((uint32_t)(w.x - 2 * (int)r[4 * v] + nx + 255) >> DENSE_Q, DENSE_VMAX);
+                a[4 * v + 1] = min((uint32_t)(w.y - 2 * (int)r[4 * v + 1] + nx + 255) >> DENSE_Q, DENSE_VMAX);
+                a[4 * v + 2] = min((uint32_t)(w.z - 2 * (int)r[4 * v + 2] + nx + 255) >> DENSE_Q, DENSE_VMAX);
+                a[4 * v + 3] = min((uint32_t)(w.w - 2 * (int)r[4 * v + 3] + nx + 255) >> DENSE_Q, DENSE_VMAX);
+              }
+              if (exclude_self && row >= cb && row < cb + 32) {
+                const int sj = (int)(row - cb);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) a[j] = j == sj ? DENSE_INVALID : a[j];
+              }
+#pragma unroll
+              for (int v = 0; v < 8; ++v)
+                dst[v] = make_uint2(a[4 * v] | (a[4 * v + 1] << 16), a[4 * v + 2] | (a[4 * v + 3] << 16));
+#else
+              const int4 *pp = reinterpret_cast<const int4 *>(s.pid[tpar] + c * 32);
               const bool es = exclude_self != 0;
 #pragma unroll
               for (int v = 0; v < 8; ++v) {
@@ -566,6 +591,7 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
                 const uint32_t a3 = dense_val(w.w - 2 * (int)r[4 * v + 3] + nx, cj + 3, n, pd.w, es && row == cj + 3);
                 dst[v] = make_uint2(a0 | (a1 << 16), a2 | (a3 << 16));
               }
+#endif
             }
             continue;
           }
