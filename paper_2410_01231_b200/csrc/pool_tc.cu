@@ -172,6 +172,9 @@ enum { ST_WAIT, ST_MAIN, ST_SLOW, ST_COMPACT, ST_FINAL, ST_NSLOW, ST_NCOMPACT, S
 // of u32.
 constexpr int DENSE_TILES = 16;  // u16 values: 16 tiles x 128 x 2 B = 4 KB of the row's slot
 static_assert(DENSE_TILES * BN * 2 <= CAP * 8, "dense pass-1 values must fit the row's buffer");
+#ifndef TC_DENSE_NOVALID
+#define TC_DENSE_NOVALID 0  // 1: no per-value validity tests in the dense pass-1 epilogue
+#endif
 #ifndef TC_DENSE_PACKED
 #define TC_DENSE_PACKED 1  // 15-bit values (dist / 2^8), counted two per instruction in the K-th search
 #endif
@@ -553,7 +556,11 @@ __global__ void __maxnreg__(TC_CTAS == 3 ? 112 : 168)
             if (row_ok && t < DENSE_TILES) {
               uint2 *dst = reinterpret_cast<uint2 *>(reinterpret_cast<uint16_t *>(bufs + row * CAP) +
                                                      t * BN + c * 32);
-#if TC_DENSE_PACKED
+#if TC_DENSE_NOVALID
+              // (measured and left off: the dense pass is not bound by these
+              // instructions, 0.767 vs 0.764 ms, and the padding values widen the
+              // K-th search's range, so its 1/1024 tolerance loosens the seeds:
+              // pool 9.81 -> 10.71 ms)
               // Columns that are no points (padding slots of the tile sort,
               // columns past n) carry |x|^2 = 0x3f3f3f3f: their value clamps to
               // DENSE_VMAX, above every real distance, so counting them cannot
