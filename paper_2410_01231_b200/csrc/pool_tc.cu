@@ -1126,7 +1126,7 @@ __device__ __forceinline__ void finalize_row(const uint64_t *buf, int cnt, int K
   // quarter of the per-key work for the rows just above a power of two)
   if (cnt <= 128)
     sort = select_stage<4>(buf, cnt, K, kth_only, orow, out_keys, hist, stage, 32 * NPL, lane);
-#if FIN_MID_SIZES
+#if FIN_MID_SIZES == 1
   else if (cnt <= 192)
     sort = select_stage<6>(buf, cnt, K, kth_only, orow, out_keys, hist, stage, 32 * NPL, lane);
 #endif
